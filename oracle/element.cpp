@@ -1,0 +1,175 @@
+// element.cpp — Q1 Nitsche element matrices and beta_e (TEST INFRASTRUCTURE).
+// SPEC.md:205-222 (nitsche_beta, assemble_element); PAPER.md:314-348 (forms
+// A_e, l_e, beta_e = 2 lambda_max of B_e x = lambda D_e x).
+// dense_generalized_eigs_max follows linalg.cpp:108-136 (eigendecompose D,
+// keep eigenvalues >= kernel_tol * lambda_max(D), project B, largest
+// eigenvalue of the deflated pencil) with a cyclic Jacobi eigensolver in
+// place of Eigen's SelfAdjointEigenSolver.
+//
+// Everything is computed on the reference cell [0,1]^3 and scaled:
+//   D = h Dr, B = Br, M_gamma = h^2 Mr, N = h Nr, beta = 2 lambda(Br, Dr) / h,
+//   K_e = h (Dr + 2 lambda Mr - Nr - Nr^T), f_e = h^3 int_ref phi_b  (f = 1, g = 0).
+// Pin: a cut cell whose retained volume rule is
+// empty contributes nothing (no volume and no Nitsche term).
+#include <cmath>
+#include <cstring>
+
+#include "oracle.hpp"
+
+namespace oracle {
+
+// Cyclic Jacobi: a (n x n row-major, destroyed) -> eigenvalues ev, vectors v
+// (columns, row-major storage v[i*n+k]). Sweep order p<q row-wise; stop when
+// the off-diagonal Frobenius norm is <= 1e-300 or after 100 sweeps; rotations
+// skipped when |a_pq| is exactly zero.
+void jacobi_eigs(int n, double* a, double* v, double* ev) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) v[i * n + j] = i == j ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int i = 0; i < n; ++i) {
+      diag += a[i * n + i] * a[i * n + i];
+      for (int j = i + 1; j < n; ++j) off += a[i * n + j] * a[i * n + j];
+    }
+    if (off <= 1e-32 * diag || off < 1e-300) break;
+    for (int p = 0; p < n; ++p) {
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = a[p * n + q];
+        if (apq == 0.0) continue;
+        const double app = a[p * n + p], aqq = a[q * n + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0);
+        const double s = t * c;
+        for (int k = 0; k < n; ++k) {
+          const double akp = a[k * n + p], akq = a[k * n + q];
+          a[k * n + p] = c * akp - s * akq;
+          a[k * n + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double apk = a[p * n + k], aqk = a[q * n + k];
+          a[p * n + k] = c * apk - s * aqk;
+          a[q * n + k] = s * apk + c * aqk;
+        }
+        a[p * n + q] = 0.0;
+        a[q * n + p] = 0.0;
+        for (int k = 0; k < n; ++k) {
+          const double vkp = v[k * n + p], vkq = v[k * n + q];
+          v[k * n + p] = c * vkp - s * vkq;
+          v[k * n + q] = s * vkp + c * vkq;
+        }
+      }
+    }
+  }
+  for (int i = 0; i < n; ++i) ev[i] = a[i * n + i];
+}
+
+double dense_generalized_eigs_max(const double* b, const double* d, int n, double kernel_tol) {
+  if (n <= 0 || n > 16) fail(ErrorCode::InvalidArgument, "generalized eigs: dimension mismatch");
+  double a[256], v[256], ev[16];
+  std::memcpy(a, d, sizeof(double) * n * n);
+  jacobi_eigs(n, a, v, ev);
+  double lmax = ev[0];
+  for (int i = 1; i < n; ++i) lmax = std::max(lmax, ev[i]);
+  if (!(lmax > 0.0)) fail(ErrorCode::Degenerate, "generalized eigs: D is numerically zero (degenerate element)");
+  int keep[16], m = 0;
+  for (int k = 0; k < n; ++k)
+    if (ev[k] >= kernel_tol * lmax) keep[m++] = k;
+  if (m == 0) fail(ErrorCode::Degenerate, "generalized eigs: all directions deflated (degenerate element)");
+  // C = Dk^{-1/2} Q^T B Q Dk^{-1/2}
+  double bq[256];  // B Q : n x m
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < m; ++k) {
+      double s = 0;
+      for (int j = 0; j < n; ++j) s += b[i * n + j] * v[j * n + keep[k]];
+      bq[i * m + k] = s;
+    }
+  double c[256], cv[256], cev[16];
+  for (int k = 0; k < m; ++k)
+    for (int l = 0; l < m; ++l) {
+      double s = 0;
+      for (int i = 0; i < n; ++i) s += v[i * n + keep[k]] * bq[i * m + l];
+      c[k * m + l] = s / (std::sqrt(ev[keep[k]]) * std::sqrt(ev[keep[l]]));
+    }
+  for (int k = 0; k < m; ++k)
+    for (int l = k + 1; l < m; ++l) {
+      const double s = 0.5 * (c[k * m + l] + c[l * m + k]);
+      c[k * m + l] = s;
+      c[l * m + k] = s;
+    }
+  jacobi_eigs(m, c, cv, cev);
+  double best = cev[0];
+  for (int k = 1; k < m; ++k) best = std::max(best, cev[k]);
+  return best;
+}
+
+namespace {
+
+inline void q1_eval(const double xi[3], double val[8], double grad[8][3]) {
+  for (int l = 0; l < 8; ++l) {
+    double f[3], df[3];
+    for (int d = 0; d < 3; ++d) {
+      const bool bit = (l >> d) & 1;
+      f[d] = bit ? xi[d] : 1.0 - xi[d];
+      df[d] = bit ? 1.0 : -1.0;
+    }
+    val[l] = f[0] * f[1] * f[2];
+    grad[l][0] = df[0] * f[1] * f[2];
+    grad[l][1] = f[0] * df[1] * f[2];
+    grad[l][2] = f[0] * f[1] * df[2];
+  }
+}
+
+}  // namespace
+
+Element element_matrix(const Mesh& m, std::int64_t cell) {
+  Element e{};
+  const double h = m.h[0];
+  const bool cut = m.cls[(size_t)cell] == kCut;
+  std::int64_t nodes[8];
+  m.cell_nodes(cell, nodes);
+  double phiv[8];
+  for (int l = 0; l < 8; ++l) phiv[l] = m.phi[(size_t)nodes[l]];
+  const CutRule rule = cut ? cut_quadrature_ref(phiv) : full_quadrature_ref();
+  if (rule.vol.empty()) {
+    e.empty = true;
+    return e;
+  }
+  double dr[64] = {0}, br[64] = {0}, mr[64] = {0}, nr[64] = {0}, fr[8] = {0};
+  double val[8], grad[8][3];
+  for (const auto& p : rule.vol) {
+    const double xi[3] = {p[0], p[1], p[2]};
+    q1_eval(xi, val, grad);
+    for (int a = 0; a < 8; ++a) {
+      fr[a] += p[3] * val[a];
+      for (int b = 0; b < 8; ++b)
+        dr[a * 8 + b] += p[3] * (grad[a][0] * grad[b][0] + grad[a][1] * grad[b][1] + grad[a][2] * grad[b][2]);
+    }
+  }
+  double lambda = 0.0;
+  if (!rule.surf.empty()) {
+    for (const auto& p : rule.surf) {
+      const double xi[3] = {p[0], p[1], p[2]};
+      q1_eval(xi, val, grad);
+      double gn[8];
+      for (int a = 0; a < 8; ++a) gn[a] = p[4] * grad[a][0] + p[5] * grad[a][1] + p[6] * grad[a][2];
+      for (int a = 0; a < 8; ++a)
+        for (int b = 0; b < 8; ++b) {
+          br[a * 8 + b] += p[3] * (gn[a] * gn[b]);
+          mr[a * 8 + b] += p[3] * (val[a] * val[b]);
+          nr[a * 8 + b] += p[3] * (val[b] * gn[a]);
+        }
+    }
+    lambda = dense_generalized_eigs_max(br, dr, 8, 1e-12);
+  }
+  const double betar = 2.0 * lambda;
+  for (int a = 0; a < 8; ++a)
+    for (int b = 0; b < 8; ++b)
+      e.k[a * 8 + b] = h * (dr[a * 8 + b] + betar * mr[a * 8 + b] - nr[a * 8 + b] - nr[b * 8 + a]);
+  for (int a = 0; a < 8; ++a) e.f[a] = h * h * h * fr[a];
+  e.beta = betar / h;
+  e.empty = false;
+  return e;
+}
+
+}  // namespace oracle

@@ -1,0 +1,160 @@
+"""Workload configurations of BASELINE.json restated as concrete solver inputs.
+
+Every run: unit-cube box [0,1]^3, zero translation, Poisson f=1, u=0 weakly on
+the embedded surface (Nitsche, beta_e = 2 lambda_max), no strong Dirichlet on
+the box, fp64, x0 = 0, rtol 1e-6, max_iter 2000.
+
+Pinned choices:
+  * cfg3 icosahedron: vertices (0,+-1,+-g), (+-1,+-g,0), (+-g,0,+-1), g the
+    golden ratio, in the loop order below, normalised, scaled to 0.30, shifted
+    to (0.5,0.5,0.5); the central ball comes first.
+  * cfg4/cfg5: std::mt19937_64(seed), u = (x >> 11) * 2^-53, draws per ball in
+    the order cx, cy, cz, r, each mapped to [a, b) as a + (b - a) * u.
+    Seed 1703.
+  * cfg4 4-GPU mesh is 96^3 (102 is not divisible by 16).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+OBJ_C, OBJ_CE, OBJ_CEF = 0, 1, 2
+W_TOPOLOGICAL, W_STIFFNESS = 0, 1
+V_STANDARD, V1, V2 = 0, 1, 2
+
+OBJ_NAMES = {"c": OBJ_C, "ce": OBJ_CE, "cef": OBJ_CEF}
+W_NAMES = {"topological": W_TOPOLOGICAL, "cardinality": W_TOPOLOGICAL, "stiffness": W_STIFFNESS}
+V_NAMES = {"standard": V_STANDARD, "v1": V1, "v2": V2}
+
+
+class MT19937_64:
+    """Restatement of std::mt19937_64 ([rand.predef]: 10000th output for the
+    default seed 5489 is 9981545732273789042)."""
+
+    _N, _M = 312, 156
+    _MASK = (1 << 64) - 1
+
+    def __init__(self, seed: int = 5489):
+        self.mt = [0] * self._N
+        self.mt[0] = seed & self._MASK
+        for i in range(1, self._N):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & self._MASK
+        self.idx = self._N
+
+    def _twist(self):
+        mt, n, m = self.mt, self._N, self._M
+        upper, lower = 0xFFFFFFFF80000000, 0x7FFFFFFF
+        for i in range(n):
+            x = (mt[i] & upper) | (mt[(i + 1) % n] & lower)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + m) % n] ^ xa
+        self.idx = 0
+
+    def __call__(self) -> int:
+        if self.idx >= self._N:
+            self._twist()
+        y = self.mt[self.idx]
+        self.idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEB9CC000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & self._MASK
+
+    def uniform(self) -> float:
+        return (self() >> 11) * (1.0 / 9007199254740992.0)
+
+
+def seeded_balls(n: int, lo: float, hi: float, rlo: float, rhi: float, seed: int = 1703):
+    rng = MT19937_64(seed)
+    balls = []
+    for _ in range(n):
+        cx = lo + (hi - lo) * rng.uniform()
+        cy = lo + (hi - lo) * rng.uniform()
+        cz = lo + (hi - lo) * rng.uniform()
+        r = rlo + (rhi - rlo) * rng.uniform()
+        balls.append((cx, cy, cz, r))
+    return balls
+
+
+def icosahedron_balls():
+    g = (1.0 + math.sqrt(5.0)) / 2.0
+    verts = []
+    for a in (1.0, -1.0):
+        for b in (1.0, -1.0):
+            verts.append((0.0, a, b * g))
+    for a in (1.0, -1.0):
+        for b in (1.0, -1.0):
+            verts.append((a, b * g, 0.0))
+    for a in (1.0, -1.0):
+        for b in (1.0, -1.0):
+            verts.append((b * g, 0.0, a))
+    nrm = math.sqrt(1.0 + g * g)
+    balls = [(0.5, 0.5, 0.5, 0.30)]
+    for v in verts:
+        balls.append((0.5 + 0.30 * (v[0] / nrm), 0.5 + 0.30 * (v[1] / nrm), 0.5 + 0.30 * (v[2] / nrm), 0.12))
+    return balls
+
+
+@dataclass
+class Config:
+    name: str
+    cells: int
+    block: int
+    balls: list
+    objects: int = OBJ_CE
+    weighting: int = W_TOPOLOGICAL
+    variant: int = V_STANDARD
+    rtol: float = 1e-6
+    max_iter: int = 2000
+    lo: tuple = (0.0, 0.0, 0.0)
+    hi: tuple = (1.0, 1.0, 1.0)
+    translation: tuple = (0.0, 0.0, 0.0)
+    extra: dict = field(default_factory=dict)
+
+    def with_(self, **kw) -> "Config":
+        d = dict(self.__dict__)
+        d.update(kw)
+        return Config(**d)
+
+
+CFG4_CELLS = {1: 64, 2: 80, 4: 96, 8: 128}
+
+
+def get(name: str, gpus: int = 1, objects=None, weighting=None, variant=None) -> Config:
+    """cfg1 .. cfg5 of BASELINE.json (configs[0..4]); cfg2 defaults to
+    topological/ce (its four-run matrix is chosen with the keyword overrides);
+    cfg5 defaults to the {stiffness, cef} run."""
+    if name == "cfg1":
+        c = Config("cfg1", 20, 10, [(0.5, 0.5, 0.5, 0.4)], OBJ_CE, W_TOPOLOGICAL)
+    elif name == "cfg2":
+        c = Config("cfg2", 40, 10, [(0.5, 0.5, 0.5, 0.4013)], OBJ_CE, W_TOPOLOGICAL)
+    elif name == "cfg3":
+        c = Config("cfg3", 80, 10, icosahedron_balls(), OBJ_CEF, W_STIFFNESS)
+    elif name == "cfg4":
+        c = Config("cfg4", CFG4_CELLS[gpus], 16, seeded_balls(32, 0.2, 0.8, 0.05, 0.15), OBJ_CEF, W_STIFFNESS)
+    elif name == "cfg5":
+        c = Config("cfg5", 256, 16, seeded_balls(256, 0.1, 0.9, 0.02, 0.08), OBJ_CEF, W_STIFFNESS)
+    elif name == "sphere-id1":
+        # paper Table sphere row Id 1: reference default sphere
+        # (levelset.cpp:23 r=0.7, centre 0) in its default box [-1,1]^3.
+        c = Config("sphere-id1", 16, 8, [(0.0, 0.0, 0.0, 0.7)], OBJ_CE, W_TOPOLOGICAL,
+                   lo=(-1.0, -1.0, -1.0), hi=(1.0, 1.0, 1.0))
+    else:
+        raise KeyError(name)
+    if objects is not None:
+        c.objects = OBJ_NAMES[objects] if isinstance(objects, str) else objects
+    if weighting is not None:
+        c.weighting = W_NAMES[weighting] if isinstance(weighting, str) else weighting
+    if variant is not None:
+        c.variant = V_NAMES[variant] if isinstance(variant, str) else variant
+    return c
+
+
+def sphere_id(k: int) -> Config:
+    """Paper Table sphere rows Id 1..5: 16*2^(k-1) cells per axis, H/h = 8."""
+    n = 16 * 2 ** (k - 1)
+    return Config(f"sphere-id{k}", n, 8, [(0.0, 0.0, 0.0, 0.7)], OBJ_CE, W_TOPOLOGICAL,
+                  lo=(-1.0, -1.0, -1.0), hi=(1.0, 1.0, 1.0))
