@@ -165,7 +165,7 @@ Element element_matrix(const Mesh& m, std::int64_t cell) {
   const double betar = 2.0 * lambda;
   for (int a = 0; a < 8; ++a)
     for (int b = 0; b < 8; ++b)
-      e.k[a * 8 + b] = h * (dr[a * 8 + b] + betar * mr[a * 8 + b] - nr[a * 8 + b] - nr[b * 8 + a]);
+      e.k[a * 8 + b] = h * (dr[a * 8 + b] + betar * mr[a * 8 + b] - (nr[a * 8 + b] + nr[b * 8 + a]));
   for (int a = 0; a < 8; ++a) e.f[a] = h * h * h * fr[a];
   e.beta = betar / h;
   e.empty = false;
