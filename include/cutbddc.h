@@ -1,0 +1,192 @@
+/* cutbddc.h — C ABI of the B200-native PCG+BDDC solve path.
+ *
+ * Drop-in boundary for the reference library "cutbddc" (/root/reference):
+ * the reference's C boundary exists only as a comment, "the C boundary maps
+ * `code` onto cutbddc_status values" (proj/src/core/common.hpp:22-23); its
+ * operations are the SPEC.md ops listed beside each entry point below. No
+ * torch types cross this boundary: plain pointers, sizes and status codes.
+ * Nothing throws across it. Input arrays are borrowed for the duration of the
+ * call (copied to the device); outputs go to caller-allocated buffers; a
+ * handle owns all device memory until cutbddc_gpu_destroy. A handle is
+ * single-caller; separate handles are independent.
+ */
+#ifndef CUTBDDC_H
+#define CUTBDDC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ErrorCode {InvalidArgument, Config, Io, Singular, Degenerate, NotConverged,
+ * Internal} of common.hpp:24-32, plus OK. CUDA and NCCL failures map to
+ * CUTBDDC_INTERNAL. */
+typedef enum {
+  CUTBDDC_OK = 0,
+  CUTBDDC_INVALID_ARGUMENT = 1,
+  CUTBDDC_CONFIG = 2,
+  CUTBDDC_IO = 3,
+  CUTBDDC_SINGULAR = 4,
+  CUTBDDC_DEGENERATE = 5,
+  CUTBDDC_NOT_CONVERGED = 6,
+  CUTBDDC_INTERNAL = 7
+} cutbddc_status;
+
+/* Thread-local message of the last failing call (pivot index as in
+ * linalg.cpp:53-54, subdomain context as in linalg.cpp:86-89 / SPEC.md:383,
+ * dimension mismatch as in linalg.cpp:94-95). */
+const char* cutbddc_last_error(void);
+
+/* Cell classes, mesh.hpp:17 CellClass {Interior, Exterior, Cut}. */
+enum { CUTBDDC_INTERIOR = 0, CUTBDDC_EXTERIOR = 1, CUTBDDC_CUT = 2 };
+/* Object kinds, object sets, weighting,
+ * variants. */
+enum { CUTBDDC_CORNER = 0, CUTBDDC_EDGE = 1, CUTBDDC_FACE = 2 };
+enum { CUTBDDC_OBJECTS_C = 0, CUTBDDC_OBJECTS_CE = 1, CUTBDDC_OBJECTS_CEF = 2 };
+enum { CUTBDDC_WEIGHT_TOPOLOGICAL = 0, CUTBDDC_WEIGHT_STIFFNESS = 1 };
+enum { CUTBDDC_VARIANT_STANDARD = 0, CUTBDDC_VARIANT_V1 = 1, CUTBDDC_VARIANT_V2 = 2 };
+
+typedef struct cutbddc_gpu cutbddc_gpu;
+
+typedef struct {
+  int device;      /* CUDA device ordinal */
+  int rank;        /* this process' rank (multi-GPU), 0 for one GPU */
+  int world_size;  /* number of GPUs (processes), 1 for one GPU */
+  const void* nccl_id; /* 128-byte ncclUniqueId (rank 0's) when world_size > 1, else NULL */
+} cutbddc_gpu_opts;
+
+/* Background mesh + level set, MeshParams (mesh.hpp:18-24) and a union of
+ * balls (levelset.cpp:22-39 sphere; min-union pattern levelset.cpp:129-133). */
+typedef struct {
+  int cells[3];
+  double box_lo[3], box_hi[3], translation[3];
+  int n_balls;
+  const double* balls; /* n_balls x {cx, cy, cz, r} */
+} cutbddc_geometry;
+
+/* BackgroundMesh view (mesh.hpp:77-80): per-node snapped phi, per-cell
+ * class, per-node dof id (-1 = none), as produced by
+ * BackgroundMesh::classify (mesh.cpp:114-169). */
+typedef struct {
+  int cells[3];
+  double origin[3], h[3];
+  int64_t n_dof;
+  const double* phi;        /* (n+1)^3 */
+  const uint8_t* cls;       /* n^3 */
+  const int32_t* dof_of_node; /* (n+1)^3 */
+} cutbddc_mesh_view;
+
+/* SubdomainPartition: block size H/h and the nonempty
+ * blocks in ascending block id ((bi*nby+bj)*nbz+bk). */
+typedef struct {
+  int block;
+  int n_sd;
+  const int64_t* block_ids;
+} cutbddc_partition_view;
+
+/* InterfaceObjects restricted to the selected coarse objects, in coarse-DOF
+ * order: kinds[n], dofs (global dof ids) in CSR
+ * dof_ptr[n+1], neighbour subdomains in CSR neigh_ptr[n+1]. */
+typedef struct {
+  int n_objects;
+  const int32_t* kinds;
+  const int64_t* dof_ptr;
+  const int32_t* dofs;
+  const int64_t* neigh_ptr;
+  const int32_t* neigh;
+} cutbddc_coarse_view;
+
+/* SolveReport. residuals must hold max_iter+1 doubles. */
+typedef struct {
+  int iterations;
+  int converged;
+  double cond_estimate;
+  double lambda_min, lambda_max;
+  double* residuals;
+  double t_assembly, t_setup, t_pcg; /* device-timed seconds of the last calls */
+} cutbddc_solve_report;
+
+cutbddc_status cutbddc_gpu_create(const cutbddc_gpu_opts* opts, cutbddc_gpu** out);
+void cutbddc_gpu_destroy(cutbddc_gpu* h);
+
+/* BackgroundMesh::classify (mesh.cpp:114-169) on the device. Outputs
+ * (optional, may be NULL) are host buffers of the sizes in cutbddc_mesh_view;
+ * n_dof is always written. The mesh stays resident for cutbddc_gpu_assemble. */
+cutbddc_status cutbddc_gpu_classify(cutbddc_gpu* h, const cutbddc_geometry* g, double* phi, uint8_t* cls,
+                                    int32_t* dof_of_node, int64_t* n_dof);
+
+/* assemble_subassembled + assemble_global:
+ * cut quadrature, beta_e, element
+ * matrices and the per-subdomain matrices A^w, all on the
+ * device. mesh may be NULL to use the mesh left by cutbddc_gpu_classify.
+ * dirichlet (optional host buffer, n_dof bytes) receives the strong-Dirichlet
+ * (orphan) dof mask. */
+cutbddc_status cutbddc_gpu_assemble(cutbddc_gpu* h, const cutbddc_mesh_view* mesh,
+                                    const cutbddc_partition_view* part, uint8_t* dirichlet);
+
+/* A^w diagonal entries at every (subdomain, local dof) copy, subdomains in
+ * order, local dofs ascending (input of build_weighting / split_edges_v2). */
+cutbddc_status cutbddc_gpu_local_diagonals(cutbddc_gpu* h, double* diag, int64_t* n_copies);
+
+/* build_weighting + build_coarse_space:
+ * weights, constraint rows, interior / constrained-Neumann factorisations,
+ * coarse basis, coarse matrix and its factorisation. */
+cutbddc_status cutbddc_gpu_setup_bddc(cutbddc_gpu* h, const cutbddc_coarse_view* coarse, int weighting);
+
+/* krylov::pcg with A = Abar and M = BDDC apply. b may be
+ * NULL to use the assembled rhs. x: n_dof output. */
+cutbddc_status cutbddc_gpu_pcg(cutbddc_gpu* h, const double* b, double* x, double rtol, int max_iter,
+                               cutbddc_solve_report* report);
+
+/* Test hooks: y = Abar x (SparseSymMatrix::apply, linalg.hpp:45) and
+ * z = M r (bddc apply), host vectors of n_dof. */
+cutbddc_status cutbddc_gpu_spmv(cutbddc_gpu* h, const double* x, double* y);
+cutbddc_status cutbddc_gpu_apply_bddc(cutbddc_gpu* h, const double* r, double* z);
+/* Assembled rhs b (n_dof) and coarse matrix (n_c x n_c row-major). */
+cutbddc_status cutbddc_gpu_rhs(cutbddc_gpu* h, double* b);
+cutbddc_status cutbddc_gpu_coarse_matrix(cutbddc_gpu* h, double* ac, int* n_coarse);
+/* Per active cell (ascending cell id): beta_e and empty-volume flag. */
+cutbddc_status cutbddc_gpu_cells(cutbddc_gpu* h, double* beta, uint8_t* empty, int64_t* n_active);
+/* Test hook: cut-cell element data in cut-cell order (ascending cell id):
+ * cell ids, 8x8 matrices (row-major) and rhs. Any output may be NULL. */
+cutbddc_status cutbddc_gpu_cut_elements(cutbddc_gpu* h, int64_t* cells, double* ke, double* fe, int64_t* n_cut);
+/* Test hooks in slot space (nsd x (B+1)^3 slots): the stencil form of A^w
+ * (nsd x 27 x T), the factorised matrix masks and diagonal shifts, and an
+ * in-place solve with the interior (which=0) or corner-augmented Neumann
+ * (which=1) factor. */
+cutbddc_status cutbddc_gpu_local_system(cutbddc_gpu* h, double* stencil, uint8_t* mask_interior, uint8_t* mask_present,
+                                        double* diag_add, int32_t* slot_dof);
+cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x);
+/* Statistics: [0]=n_dof [1]=n_sd [2]=n_coarse [3]=template slots [4]=factor doubles
+ * per subdomain (one factor) [5]=n_supernodes [6]=levels [7]=max m_w [8]=n_interface. */
+cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
+
+/* Host-side partition and interface objects (the caller side of the
+ * boundary; reference ops build_partition SPEC.md:295-303, classify_objects
+ * :304-312, split_edges_v1 :313-321, split_edges_v2 :322-330). The result is
+ * owned by the library until cutbddc_objects_free. */
+typedef struct {
+  int n_sd;
+  int64_t* block_ids;
+  int n_objects;
+  int32_t* kinds;
+  int64_t* dof_ptr;
+  int32_t* dofs;
+  int64_t* neigh_ptr;
+  int32_t* neigh;
+} cutbddc_objects;
+
+cutbddc_status cutbddc_build_partition(const cutbddc_mesh_view* mesh, int block, int64_t* n_sd, int64_t* block_ids);
+/* weights: per (subdomain, local dof) copy (order of cutbddc_gpu_local_diagonals),
+ * needed only for CUTBDDC_VARIANT_V2 (else NULL). dirichlet: orphan mask. */
+cutbddc_status cutbddc_classify_objects(const cutbddc_mesh_view* mesh, const cutbddc_partition_view* part,
+                                        const uint8_t* dirichlet, int objects, int variant, const double* weights,
+                                        cutbddc_objects** out);
+void cutbddc_objects_free(cutbddc_objects* o);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CUTBDDC_H */

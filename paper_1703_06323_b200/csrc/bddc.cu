@@ -1,0 +1,689 @@
+// bddc.cu — BDDC setup (K5, K8, K9, K10) and application.
+//
+//   build_weighting     SPEC.md:370-378  topological 1/|neigh| or stiffness
+//                       A^w_xixi / sum_w' A^w'_xixi
+//   build_coarse_space  SPEC.md:379-387  C_w rows (corner e_xi, edge/face
+//                       (1/|lambda|) sum e_xi); constrained
+//                       Neumann solves through K0 = A_w + rho_w C_c^T C_c
+//                       (corner rows only: diagonal, stencil-preserving) and the
+//                       dense constraint Schur complement S = C K0^{-1} C^T:
+//                         Phi = K0^{-1} C^T S^{-1},  saddle solve z = y - Phi C y
+//                       A_c,w = Phi^T A_w Phi assembled in subdomain order.
+//   apply               SPEC.md:388-396, expanded in SURVEY.md section 3.2, with
+//                       r1 := 0 on interior rows.
+// Every gather sums in ascending subdomain order; no fp64 atomics.
+#include <algorithm>
+#include <vector>
+
+#include "bddc.cuh"
+#include "factor.cuh"
+#include "subst.cuh"
+
+namespace cutbddc_b200 {
+namespace {
+
+__global__ void k_masks(int64_t ns, const int32_t* __restrict__ slot_dof, const uint8_t* __restrict__ ncount,
+                        uint8_t* __restrict__ mall, uint8_t* __restrict__ mint) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  const int32_t d = slot_dof[g];
+  mall[g] = d >= 0;
+  mint[g] = d >= 0 && ncount[d] == 1;
+}
+
+__global__ void k_weights(int64_t ns, int T, int mode, const int32_t* __restrict__ slot_dof,
+                          const uint8_t* __restrict__ ncount, const double* __restrict__ As,
+                          const int64_t* __restrict__ copy_ptr, const int64_t* __restrict__ copy_idx,
+                          double* __restrict__ w, int* __restrict__ bad) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  const int32_t d = slot_dof[g];
+  if (d < 0) {
+    w[g] = 0.0;
+    return;
+  }
+  const int k = ncount[d];
+  if (k == 1) {
+    w[g] = 1.0;
+    return;
+  }
+  if (mode == CUTBDDC_WEIGHT_TOPOLOGICAL) {
+    w[g] = 1.0 / (double)k;
+    return;
+  }
+  auto diag = [&](int64_t ci) { return As[(ci / T) * 27 * T + 13ll * T + ci % T]; };
+  double tot = 0.0;
+  for (int64_t p = copy_ptr[d]; p < copy_ptr[d + 1]; ++p) tot += diag(copy_idx[p]);
+  if (!(tot != 0.0)) {
+    atomicExch(bad, 1);
+    w[g] = 0.0;
+    return;
+  }
+  w[g] = diag(g) / tot;
+}
+
+// rho_w = mean of diag(A_w) over the subdomain's local dofs, summed
+// sequentially in ascending local dof (= slot) order: K = A + rho C^T C of a
+// small-cut subdomain is so ill-conditioned that a 1-ulp change of rho moves
+// the saddle solutions by ~1e-9, so rho is pinned bit-for-bit to the CPU
+// restatement's order. One thread per subdomain (setup only).
+__global__ void k_rho(int nsd, int T, const int32_t* __restrict__ slot_dof, const double* __restrict__ As,
+                      double* __restrict__ rho) {
+  const int sd = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sd >= nsd) return;
+  double s = 0.0;
+  int64_t c = 0;
+  for (int t = 0; t < T; ++t) {
+    if (slot_dof[(int64_t)sd * T + t] >= 0) {
+      s += As[(int64_t)sd * 27 * T + 13ll * T + t];
+      ++c;
+    }
+  }
+  rho[sd] = c > 0 ? s / (double)c : 1.0;
+}
+
+__global__ void k_diag_add(int nsd, int T, const int64_t* __restrict__ m_off, const int64_t* __restrict__ c_ptr,
+                           const int32_t* __restrict__ c_slot, const uint8_t* __restrict__ corner,
+                           const double* __restrict__ rho, double* __restrict__ dadd) {
+  const int sd = blockIdx.x;
+  for (int64_t r = m_off[sd] + threadIdx.x; r < m_off[sd + 1]; r += blockDim.x) {
+    if (!corner[r]) continue;
+    dadd[(int64_t)sd * T + c_slot[c_ptr[r]]] = rho[sd];
+  }
+}
+
+// X[rhs][sd][T] = C^T e_rhs for rhs in [r0, r0+nr)
+__global__ void k_fill_ct(int nsd, int T, int r0, int nr, const int64_t* __restrict__ m_off,
+                          const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_slot,
+                          const double* __restrict__ c_val, double* __restrict__ X) {
+  const int sd = blockIdx.x, q = blockIdx.y;
+  const int64_t row = m_off[sd] + r0 + q;
+  if (row >= m_off[sd + 1]) return;
+  double* x = X + ((int64_t)q * nsd + sd) * T;
+  for (int64_t p = c_ptr[row] + threadIdx.x; p < c_ptr[row + 1]; p += blockDim.x) x[c_slot[p]] = c_val[p];
+}
+
+// S[sd] (m x m, row-major at ac_off) = C W with W columns in Wall[rhs][sd][T]
+__global__ void k_schur(int nsd, int T, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
+                        const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_slot,
+                        const double* __restrict__ c_val, const double* __restrict__ Wall, double* __restrict__ S) {
+  const int sd = blockIdx.x;
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
+    const int r = q / m, c = q % m;
+    const int64_t row = m_off[sd] + r;
+    const double* wc = Wall + ((int64_t)c * nsd + sd) * T;
+    double v = 0.0;
+    for (int64_t p = c_ptr[row]; p < c_ptr[row + 1]; ++p) v += c_val[p] * wc[c_slot[p]];
+    S[s_off[sd] + q] = v;
+  }
+}
+
+// In-place SPD inverse of each subdomain's m x m block (symmetrised first),
+// Gauss-Jordan without pivoting on the SPD matrix; non-positive pivot -> fail.
+__global__ void k_small_spd_inverse(int nblk, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
+                                    double* __restrict__ S, unsigned long long* fail) {
+  extern __shared__ double a[];
+  const int b = blockIdx.x;
+  const int m = (int)(m_off[b + 1] - m_off[b]);
+  if (m == 0) return;
+  double* g = S + s_off[b];
+  for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
+    const int r = q / m, c = q % m;
+    a[q] = 0.5 * (g[r * m + c] + g[c * m + r]);
+  }
+  __syncthreads();
+  __shared__ double piv;
+  for (int k = 0; k < m; ++k) {
+    if (threadIdx.x == 0) {
+      piv = a[k * m + k];
+      if (!(piv > 0.0)) {
+        atomicMin(fail, (unsigned long long)b);
+        piv = 1.0;
+      }
+    }
+    __syncthreads();
+    // row k /= piv ; eliminate column k from other rows (Gauss-Jordan in place)
+    const double p = piv;
+    double* colk = a + m * m;  // multipliers of column k, staged before the update
+    for (int q = threadIdx.x; q < m; q += blockDim.x) {
+      colk[q] = a[q * m + k];
+      a[k * m + q] = q == k ? 1.0 / p : a[k * m + q] / p;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
+      const int r = q / m, c = q % m;
+      if (r == k) continue;
+      const double f = colk[r];
+      if (c == k)
+        a[q] = -f * a[k * m + k];
+      else
+        a[q] -= f * a[k * m + c];
+    }
+    __syncthreads();
+  }
+  for (int q = threadIdx.x; q < m * m; q += blockDim.x) g[q] = a[q];
+}
+
+// Phi[(m_off[sd]+c)][slot] = sum_r W[r][sd][slot] Sinv[r][c]
+__global__ void k_phi(int nsd, int T, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
+                      const double* __restrict__ Wall, const double* __restrict__ Sinv, double* __restrict__ Phi) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= (int64_t)nsd * T) return;
+  const int sd = (int)(g / T), t = (int)(g % T);
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  const double* si = Sinv + s_off[sd];
+  for (int c = 0; c < m; ++c) {
+    double v = 0.0;
+    for (int r = 0; r < m; ++r) v += Wall[((int64_t)r * nsd + sd) * T + t] * si[r * m + c];
+    Phi[(m_off[sd] + c) * T + t] = v;
+  }
+}
+
+// A_c,w[r][c] = Phi_r . (A_w Phi_c): CTA per (sd, c), A Phi_c staged in shared memory
+__global__ void k_local_coarse(int T, int b1, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
+                               const double* __restrict__ As, const double* __restrict__ Phi, double* __restrict__ Ac) {
+  extern __shared__ double ap[];
+  __shared__ double sh[32];
+  const int sd = blockIdx.x, c = blockIdx.y;
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  if (c >= m) return;
+  const double* ph = Phi + (m_off[sd] + c) * T;
+  const double* A = As + (int64_t)sd * 27 * T;
+  for (int u = threadIdx.x; u < T; u += blockDim.x) {
+    const int ux = u / (b1 * b1), uy = (u / b1) % b1, uz = u % b1;
+    double s = 0.0;
+    for (int k = 0; k < 27; ++k) {
+      const int vx = ux + k / 9 - 1, vy = uy + (k / 3) % 3 - 1, vz = uz + k % 3 - 1;
+      if (vx < 0 || vy < 0 || vz < 0 || vx >= b1 || vy >= b1 || vz >= b1) continue;
+      s += A[(int64_t)k * T + u] * ph[(vx * b1 + vy) * b1 + vz];
+    }
+    ap[u] = s;
+  }
+  __syncthreads();
+  for (int r = 0; r < m; ++r) {
+    const double* pr = Phi + (m_off[sd] + r) * T;
+    double s = 0.0;
+    for (int u = threadIdx.x; u < T; u += blockDim.x) s += pr[u] * ap[u];
+    s = block_sum<256>(s, sh);
+    if (threadIdx.x == 0) Ac[s_off[sd] + (int64_t)r * m + c] = s;
+  }
+}
+
+__global__ void k_symmetrize_blocks(int nsd, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
+                                    double* __restrict__ Ac) {
+  const int sd = blockIdx.x;
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  double* a = Ac + s_off[sd];
+  for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
+    const int r = q / m, c = q % m;
+    if (r < c) {
+      const double v = 0.5 * (a[r * m + c] + a[c * m + r]);
+      a[r * m + c] = v;
+      a[c * m + r] = v;
+    }
+  }
+}
+
+// coarse row lambda: sum over its (sd, local row) copies in ascending sd.
+__global__ void k_coarse_assemble(int nc, const int64_t* __restrict__ cg_ptr, const int64_t* __restrict__ cg_idx,
+                                  const int32_t* __restrict__ row_sd, const int64_t* __restrict__ m_off,
+                                  const int64_t* __restrict__ s_off, const int32_t* __restrict__ coarse_id,
+                                  const double* __restrict__ Ac, double* __restrict__ A) {
+  const int lam = blockIdx.x;
+  double* arow = A + (int64_t)lam * nc;
+  for (int64_t p = cg_ptr[lam]; p < cg_ptr[lam + 1]; ++p) {
+    const int64_t row = cg_idx[p];
+    const int sd = row_sd[row];
+    const int m = (int)(m_off[sd + 1] - m_off[sd]);
+    const int i = (int)(row - m_off[sd]);
+    for (int c = threadIdx.x; c < m; c += blockDim.x) arow[coarse_id[m_off[sd] + c]] += Ac[s_off[sd] + (int64_t)i * m + c];
+    __syncthreads();
+  }
+}
+
+// Single-CTA dense Cholesky of the coarse matrix (lower, row-major in A),
+// emitted as a column-major panel Lcm for the substitution solves.
+__global__ void __launch_bounds__(1024) k_coarse_chol(int n, double* __restrict__ A, double* __restrict__ Lcm,
+                                                      unsigned long long* fail) {
+  __shared__ double s_l;
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      double d = A[(int64_t)j * n + j];
+      if (!(d > 0.0)) {
+        atomicMin(fail, (unsigned long long)j);
+        d = 1.0;
+      }
+      s_l = sqrt(d);
+      A[(int64_t)j * n + j] = s_l;
+    }
+    __syncthreads();
+    const double inv = 1.0 / s_l;
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[(int64_t)i * n + j] *= inv;
+    __syncthreads();
+    // trailing lower update, rows i >= k > j
+    const int64_t rem = n - j - 1;
+    for (int64_t q = threadIdx.x; q < rem * rem; q += blockDim.x) {
+      const int i = j + 1 + (int)(q / rem), k = j + 1 + (int)(q % rem);
+      if (k > i) continue;
+      A[(int64_t)i * n + k] -= A[(int64_t)i * n + j] * A[(int64_t)k * n + j];
+    }
+    __syncthreads();
+  }
+  // column-major copy of L for the substitution solves
+  for (int64_t q = threadIdx.x; q < (int64_t)n * n; q += blockDim.x) {
+    const int i = (int)(q % n), j = (int)(q / n);
+    Lcm[q] = i >= j ? A[(int64_t)i * n + j] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ apply
+__global__ void k_gather_masked(int64_t ns, const int32_t* __restrict__ slot_dof, const uint8_t* __restrict__ mask,
+                                const double* __restrict__ r, double* __restrict__ X, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  X[g] = mask[g] ? r[slot_dof[g]] : 0.0;
+}
+
+__global__ void k_z0(int64_t nd, const int64_t* __restrict__ owner, const double* __restrict__ X,
+                     double* __restrict__ z0, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  const int64_t o = owner[d];
+  z0[d] = o >= 0 ? X[o] : 0.0;
+}
+
+// r1 = r - Abar z0 on interface rows, 0 on interior rows
+__global__ void k_r1(int64_t nd, const uint8_t* __restrict__ ncount, const double* __restrict__ aval,
+                     const int32_t* __restrict__ acol, const double* __restrict__ r, const double* __restrict__ z0,
+                     double* __restrict__ r1, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  if (ncount[d] < 2) {
+    r1[d] = 0.0;
+    return;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 27; ++k) s += aval[(int64_t)k * nd + d] * z0[acol[(int64_t)k * nd + d]];
+  r1[d] = r[d] - s;
+}
+
+__global__ void k_scatter_weighted(int64_t ns, const int32_t* __restrict__ slot_dof, const double* __restrict__ w,
+                                   const double* __restrict__ r1, double* __restrict__ X, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  const int32_t d = slot_dof[g];
+  X[g] = d >= 0 ? w[g] * r1[d] : 0.0;
+}
+
+// gl[row] = Phi_row . X_sd : warp per constraint row
+__global__ void k_phit(int64_t mtot, int T, const int32_t* __restrict__ row_sd, const double* __restrict__ Phi,
+                       const double* __restrict__ X, double* __restrict__ gl, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= mtot) return;
+  const double* ph = Phi + row * T;
+  const double* x = X + (int64_t)row_sd[row] * T;
+  double s = 0.0;
+  for (int t = lane; t < T; t += 32) s += ph[t] * x[t];
+  s = warp_sum(s);
+  if (lane == 0) gl[row] = s;
+}
+
+// cy[row] = C_row . y
+__global__ void k_cy(int64_t mtot, int T, const int32_t* __restrict__ row_sd, const int64_t* __restrict__ c_ptr,
+                     const int32_t* __restrict__ c_slot, const double* __restrict__ c_val, const double* __restrict__ Y,
+                     double* __restrict__ cy, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= mtot) return;
+  const double* y = Y + (int64_t)row_sd[row] * T;
+  double s = 0.0;
+  for (int64_t p = c_ptr[row] + lane; p < c_ptr[row + 1]; p += 32) s += c_val[p] * y[c_slot[p]];
+  s = warp_sum(s);
+  if (lane == 0) cy[row] = s;
+}
+
+__global__ void k_coarse_rhs(int nc, const int64_t* __restrict__ cg_ptr, const int64_t* __restrict__ cg_idx,
+                             const double* __restrict__ gl, double* __restrict__ g, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int lam = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lam >= nc) return;
+  double s = 0.0;
+  for (int64_t p = cg_ptr[lam]; p < cg_ptr[lam + 1]; ++p) s += gl[cg_idx[p]];
+  g[lam] = s;
+}
+
+// zc = A_c^{-1} (sum of the coarse rhs copies): one CTA, forward + backward
+// substitution on the column-major Cholesky panel (no explicit inverse: the
+// coarse matrix of small-cut problems is ill-conditioned).
+__global__ void __launch_bounds__(512) k_coarse_solve(int nc, const int64_t* __restrict__ cg_ptr,
+                                                      const int64_t* __restrict__ cg_idx, const double* __restrict__ gl,
+                                                      const double* __restrict__ Lcm, double* __restrict__ zc,
+                                                      const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double v[];
+  __shared__ double tile[32][33];
+  for (int lam = threadIdx.x; lam < nc; lam += blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = cg_ptr[lam]; p < cg_ptr[lam + 1]; ++p) s += gl[cg_idx[p]];
+    v[lam] = s;
+  }
+  __syncthreads();
+  panel_forward(Lcm, nc, nc, v);
+  panel_backward(Lcm, nc, nc, v, tile);
+  for (int lam = threadIdx.x; lam < nc; lam += blockDim.x) zc[lam] = v[lam];
+}
+
+// y += Phi (zc[coarse_id] - cy), thread per (sd, slot)
+__global__ void k_prolong(int nsd, int T, const int64_t* __restrict__ m_off, const int32_t* __restrict__ coarse_id,
+                          const double* __restrict__ Phi, const double* __restrict__ zc, const double* __restrict__ cy,
+                          double* __restrict__ Y, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= (int64_t)nsd * T) return;
+  const int sd = (int)(g / T), t = (int)(g % T);
+  double s = Y[g];
+  for (int64_t row = m_off[sd]; row < m_off[sd + 1]; ++row) s += Phi[row * T + t] * (zc[coarse_id[row]] - cy[row]);
+  Y[g] = s;
+}
+
+// v[d] = sum over copies (ascending sd) of w * Y
+__global__ void k_gather_weighted(int64_t nd, const int64_t* __restrict__ copy_ptr, const int64_t* __restrict__ copy_idx,
+                                  const double* __restrict__ w, const double* __restrict__ Y, double* __restrict__ v,
+                                  const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  double s = 0.0;
+  for (int64_t p = copy_ptr[d]; p < copy_ptr[d + 1]; ++p) {
+    const int64_t c = copy_idx[p];
+    s += w[c] * Y[c];
+  }
+  v[d] = s;
+}
+
+// X[sd][slot] = (Abar v)[dof] on interior slots, 0 elsewhere
+__global__ void k_interior_av(int64_t ns, int64_t nd, const int32_t* __restrict__ slot_dof, const uint8_t* __restrict__ mint,
+                              const double* __restrict__ aval, const int32_t* __restrict__ acol,
+                              const double* __restrict__ v, double* __restrict__ X, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  if (!mint[g]) {
+    X[g] = 0.0;
+    return;
+  }
+  const int64_t d = slot_dof[g];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 27; ++k) s += aval[(int64_t)k * nd + d] * v[acol[(int64_t)k * nd + d]];
+  X[g] = s;
+}
+
+__global__ void k_final_z(int64_t nd, const int64_t* __restrict__ owner, const double* __restrict__ z0,
+                          const double* __restrict__ v, const double* __restrict__ X, double* __restrict__ z,
+                          const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  const int64_t o = owner[d];
+  z[d] = z0[d] + v[d] - (o >= 0 ? X[o] : 0.0);
+}
+
+__global__ void k_row_sd(int nsd, const int64_t* __restrict__ m_off, int32_t* __restrict__ row_sd) {
+  const int sd = blockIdx.x;
+  for (int64_t r = m_off[sd] + threadIdx.x; r < m_off[sd + 1]; r += blockDim.x) row_sd[r] = sd;
+}
+
+}  // namespace
+
+void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weighting) {
+  if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc: assemble first");
+  cudaStream_t s = h->stream;
+  const int nsd = h->nsd, T = h->slots, b1 = h->b1;
+  const int64_t ns = (int64_t)nsd * T;
+  h->weighting = weighting;
+  h->bddc_ready = false;
+  if (h->graph_exec) {
+    cudaGraphExecDestroy(h->graph_exec);
+    h->graph_exec = nullptr;
+  }
+  // ---- host: constraint rows per subdomain from the coarse objects
+  const int nc = cv ? cv->n_objects : 0;
+  std::vector<int64_t> node_of_dof = h->node_of_dof.to_host(s);
+  std::vector<std::vector<int>> rows_of_sd((size_t)nsd);  // object ids per sd (coarse order)
+  for (int o = 0; o < nc; ++o)
+    for (int64_t p = cv->neigh_ptr[o]; p < cv->neigh_ptr[o + 1]; ++p) {
+      const int sd = cv->neigh[p];
+      if (sd < 0 || sd >= nsd) throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: neighbour subdomain out of range");
+      rows_of_sd[(size_t)sd].push_back(o);
+    }
+  std::vector<int64_t> m_off((size_t)nsd + 1, 0), c_ptr{0};
+  std::vector<int32_t> c_slot, coarse_id;
+  std::vector<double> c_val;
+  std::vector<uint8_t> corner;
+  std::vector<std::vector<int64_t>> cg((size_t)nc);
+  const int n = h->n, B = h->block, nb = h->nb;
+  for (int sd = 0; sd < nsd; ++sd) {
+    const int64_t bid = h->h_block_ids[(size_t)sd];
+    const int bi = (int)(bid / nb / nb), bj = (int)((bid / nb) % nb), bk = (int)(bid % nb);
+    for (int o : rows_of_sd[(size_t)sd]) {
+      const int64_t row = (int64_t)coarse_id.size();
+      cg[(size_t)o].push_back(row);
+      coarse_id.push_back(o);
+      corner.push_back(cv->kinds[o] == CUTBDDC_CORNER);
+      const int64_t cnt = cv->dof_ptr[o + 1] - cv->dof_ptr[o];
+      const double coef = cv->kinds[o] == CUTBDDC_CORNER ? 1.0 : 1.0 / (double)cnt;
+      for (int64_t p = cv->dof_ptr[o]; p < cv->dof_ptr[o + 1]; ++p) {
+        const int32_t d = cv->dofs[p];
+        if (d < 0 || d >= h->n_dof) throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: dof out of range");
+        const int64_t v = node_of_dof[(size_t)d];
+        const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
+        const int lx = i - bi * B, ly = j - bj * B, lz = k - bk * B;
+        if (lx < 0 || ly < 0 || lz < 0 || lx > B || ly > B || lz > B)
+          throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: object dof not in neighbour subdomain " + std::to_string(sd));
+        c_slot.push_back((lx * b1 + ly) * b1 + lz);
+        c_val.push_back(coef);
+      }
+      c_ptr.push_back((int64_t)c_slot.size());
+    }
+    m_off[(size_t)sd + 1] = (int64_t)coarse_id.size();
+  }
+  h->n_coarse = nc;
+  h->m_total = (int64_t)coarse_id.size();
+  h->h_m_off = m_off;
+  int m_max = 0;
+  std::vector<int64_t> s_off((size_t)nsd + 1, 0);
+  for (int sd = 0; sd < nsd; ++sd) {
+    const int m = (int)(m_off[(size_t)sd + 1] - m_off[(size_t)sd]);
+    m_max = std::max(m_max, m);
+    s_off[(size_t)sd + 1] = s_off[(size_t)sd] + (int64_t)m * m;
+  }
+  h->m_max = m_max;
+  std::vector<int64_t> cg_ptr{0}, cg_idx;
+  for (int o = 0; o < nc; ++o) {
+    for (int64_t r : cg[(size_t)o]) cg_idx.push_back(r);
+    cg_ptr.push_back((int64_t)cg_idx.size());
+  }
+  if (c_slot.empty()) c_slot.push_back(0), c_val.push_back(0.0);
+  if (coarse_id.empty()) coarse_id.push_back(0), corner.push_back(0);
+  if (cg_idx.empty()) cg_idx.push_back(0);
+  h->m_off.upload(m_off, s);
+  h->c_ptr.upload(c_ptr, s);
+  h->c_slot.upload(c_slot, s);
+  h->c_val.upload(c_val, s);
+  h->coarse_id.upload(coarse_id, s);
+  h->cg_ptr.upload(cg_ptr, s);
+  h->cg_idx.upload(cg_idx, s);
+  h->corner_row.upload(corner, s);
+  const uint8_t* d_corner = h->corner_row.p;
+  h->ac_off.upload(s_off, s);
+  h->row_sd.alloc((size_t)std::max<int64_t>(1, h->m_total));
+  k_row_sd<<<nsd, 128, 0, s>>>(nsd, h->m_off.p, h->row_sd.p);
+  CB_LAUNCH();
+  // ---- weights, rho, masks
+  DevBuf<int> bad;
+  bad.alloc(1);
+  bad.zero(s);
+  h->w.alloc((size_t)ns);
+  k_weights<<<grid_for(ns, 256), 256, 0, s>>>(ns, T, weighting, h->slot_dof.p, h->ncount.p, h->As.p, h->copy_ptr.p,
+                                              h->copy_idx.p, h->w.p, bad.p);
+  CB_LAUNCH();
+  h->mask_all.alloc((size_t)ns);
+  h->mask_int.alloc((size_t)ns);
+  k_masks<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->ncount.p, h->mask_all.p, h->mask_int.p);
+  CB_LAUNCH();
+  h->rho.alloc((size_t)nsd);
+  k_rho<<<grid_for(nsd, 64), 64, 0, s>>>(nsd, T, h->slot_dof.p, h->As.p, h->rho.p);
+  CB_LAUNCH();
+  h->diag_add.alloc((size_t)ns);
+  h->diag_add.zero(s);
+  k_diag_add<<<nsd, 128, 0, s>>>(nsd, T, h->m_off.p, h->c_ptr.p, h->c_slot.p, d_corner, h->rho.p, h->diag_add.p);
+  CB_LAUNCH();
+  int hbad = 0;
+  CB_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  CB_CUDA(cudaStreamSynchronize(s));
+  if (hbad) throw Failure(CUTBDDC_DEGENERATE, "weighting: zero total diagonal at an interface dof");
+  // ---- factorisations
+  if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);
+  if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
+  FactorInput fi{h->As.p, h->mask_int.p, nullptr, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  factor_device(h, h->tI, fi, h->GI, "cholesky (interior problem)");
+  FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
+                 h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
+  factor_device(h, h->tK, fk, h->GK, "saddle: singular augmented system; constraints do not control the operator kernel");
+  const int64_t upd_total = std::max(h->tI.tpl.upd_total, h->tK.tpl.upd_total);
+  // ---- coarse basis
+  h->phi_c.alloc((size_t)std::max<int64_t>(1, h->m_total) * T);
+  h->ac_loc.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
+  if (m_max > 0) {
+    DevBuf<double> Wall, upd;
+    Wall.alloc((size_t)m_max * ns);
+    Wall.zero(s);
+    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(m_max, (2ll << 30) / 8 / std::max<int64_t>(1, (int64_t)nsd * upd_total)));
+    upd.alloc((size_t)rb * nsd * upd_total);
+    for (int r0 = 0; r0 < m_max; r0 += rb) {
+      const int nr = std::min(rb, m_max - r0);
+      double* X = Wall.p + (int64_t)r0 * ns;
+      k_fill_ct<<<dim3(nsd, nr), 64, 0, s>>>(nsd, T, r0, nr, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, X);
+      CB_LAUNCH();
+      solve_device(h, h->tK, h->GK, X, nr, upd.p, nullptr);
+    }
+    DevBuf<double> S;
+    S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
+    k_schur<<<nsd, 256, 0, s>>>(nsd, T, h->m_off.p, h->ac_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, Wall.p, S.p);
+    CB_LAUNCH();
+    DevBuf<unsigned long long> fail;
+    fail.alloc(1);
+    CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
+    const size_t shm = sizeof(double) * ((size_t)m_max * m_max + m_max);
+    if (shm > 48 * 1024)
+      CB_CUDA(cudaFuncSetAttribute(k_small_spd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    k_small_spd_inverse<<<nsd, 256, shm, s>>>(nsd, h->m_off.p, h->ac_off.p, S.p, fail.p);
+    CB_LAUNCH();
+    unsigned long long f = 0;
+    CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));
+    CB_CUDA(cudaStreamSynchronize(s));
+    if (f != ~0ull)
+      throw Failure(CUTBDDC_SINGULAR, "saddle: singular constraint Schur complement (subdomain " + std::to_string(f) +
+                                          "); constraints are not independent");
+    k_phi<<<grid_for(ns, 128), 128, 0, s>>>(nsd, T, h->m_off.p, h->ac_off.p, Wall.p, S.p, h->phi_c.p);
+    CB_LAUNCH();
+    const size_t shm2 = sizeof(double) * (size_t)T;
+    if (shm2 > 48 * 1024)
+      CB_CUDA(cudaFuncSetAttribute(k_local_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm2));
+    k_local_coarse<<<dim3(nsd, m_max), 256, shm2, s>>>(T, b1, h->m_off.p, h->ac_off.p, h->As.p, h->phi_c.p, h->ac_loc.p);
+    CB_LAUNCH();
+    k_symmetrize_blocks<<<nsd, 256, 0, s>>>(nsd, h->m_off.p, h->ac_off.p, h->ac_loc.p);
+    CB_LAUNCH();
+  }
+  // ---- coarse matrix + factorisation
+  h->acoarse.alloc((size_t)std::max(1, nc * nc));
+  h->acoarse_inv.alloc((size_t)std::max(1, nc * nc));
+  if (nc > 0) {
+    h->acoarse.zero(s);
+    k_coarse_assemble<<<nc, 128, 0, s>>>(nc, h->cg_ptr.p, h->cg_idx.p, h->row_sd.p, h->m_off.p, h->ac_off.p,
+                                         h->coarse_id.p, h->ac_loc.p, h->acoarse.p);
+    CB_LAUNCH();
+    DevBuf<double> L;
+    L.alloc((size_t)nc * nc);
+    CB_CUDA(cudaMemcpyAsync(L.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
+    DevBuf<unsigned long long> fail;
+    fail.alloc(1);
+    CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
+    k_coarse_chol<<<1, 1024, 0, s>>>(nc, L.p, h->acoarse_inv.p, fail.p);
+    CB_LAUNCH();
+    const size_t shm = sizeof(double) * (size_t)nc;
+    if (shm > 200 * 1024) throw Failure(CUTBDDC_CONFIG, "coarse problem too large for the single-CTA coarse solve");
+    if (shm > 48 * 1024)
+      CB_CUDA(cudaFuncSetAttribute(k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    unsigned long long f = 0;
+    CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));
+    CB_CUDA(cudaStreamSynchronize(s));
+    if (f != ~0ull)
+      throw Failure(CUTBDDC_SINGULAR, "coarse matrix: not positive definite (pivot index " + std::to_string(f) + ")");
+  }
+  // ---- work vectors
+  h->sv0.alloc((size_t)ns);
+  h->sv1.alloc((size_t)ns);
+  h->upd.alloc((size_t)nsd * upd_total);
+  h->gv0.alloc((size_t)h->n_dof);
+  h->gv1.alloc((size_t)h->n_dof);
+  h->gv2.alloc((size_t)h->n_dof);
+  h->gl.alloc((size_t)std::max<int64_t>(1, h->m_total));
+  h->cy.alloc((size_t)std::max<int64_t>(1, h->m_total));
+  h->zc.alloc((size_t)std::max(1, nc));
+  h->gc.alloc((size_t)std::max(1, nc));
+  CB_CUDA(cudaStreamSynchronize(s));
+  h->bddc_ready = true;
+}
+
+// z = M r (device vectors of n_dof), enqueued on the handle's stream.
+void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip) {
+  cudaStream_t s = h->stream;
+  const int64_t nd = h->n_dof, ns = (int64_t)h->nsd * h->slots;
+  const int T = h->slots;
+  k_gather_masked<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->mask_int.p, r, h->sv0.p, skip);
+  CB_LAUNCH();
+  solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, skip);
+  k_z0<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv0.p, skip);
+  CB_LAUNCH();
+  k_r1<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->ncount.p, h->aval.p, h->acol.p, r, h->gv0.p, h->gv1.p, skip);
+  CB_LAUNCH();
+  k_scatter_weighted<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->w.p, h->gv1.p, h->sv1.p, skip);
+  CB_LAUNCH();
+  if (h->m_total > 0) {
+    k_phit<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->phi_c.p, h->sv1.p, h->gl.p, skip);
+    CB_LAUNCH();
+  }
+  solve_device(h, h->tK, h->GK, h->sv1.p, 1, h->upd.p, skip);
+  if (h->m_total > 0) {
+    k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
+                                                       h->sv1.p, h->cy.p, skip);
+    CB_LAUNCH();
+    k_coarse_solve<<<1, 512, sizeof(double) * (size_t)h->n_coarse, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p,
+                                                                       h->acoarse_inv.p, h->zc.p, skip);
+    CB_LAUNCH();
+    k_prolong<<<grid_for(ns, 256), 256, 0, s>>>(h->nsd, T, h->m_off.p, h->coarse_id.p, h->phi_c.p, h->zc.p, h->cy.p,
+                                                h->sv1.p, skip);
+    CB_LAUNCH();
+  }
+  k_gather_weighted<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->copy_ptr.p, h->copy_idx.p, h->w.p, h->sv1.p, h->gv2.p, skip);
+  CB_LAUNCH();
+  k_interior_av<<<grid_for(ns, 256), 256, 0, s>>>(ns, nd, h->slot_dof.p, h->mask_int.p, h->aval.p, h->acol.p, h->gv2.p,
+                                                  h->sv0.p, skip);
+  CB_LAUNCH();
+  solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, skip);
+  k_final_z<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->gv0.p, h->gv2.p, h->sv0.p, z, skip);
+  CB_LAUNCH();
+}
+
+}  // namespace cutbddc_b200

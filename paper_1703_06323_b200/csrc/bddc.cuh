@@ -1,0 +1,16 @@
+// bddc.cuh — BDDC setup / apply entry points (bddc.cu) and the pipeline
+// stages defined in geometry.cu, assembly.cu and pcg.cu.
+#pragma once
+
+#include "handle.cuh"
+
+namespace cutbddc_b200 {
+
+void classify_device(cutbddc_gpu* h, const cutbddc_geometry* g);
+void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_ids);
+void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weighting);
+void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip);
+void spmv_device(cutbddc_gpu* h, const double* x, double* y);
+void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, cutbddc_solve_report* rep);
+
+}  // namespace cutbddc_b200

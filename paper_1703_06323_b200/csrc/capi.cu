@@ -1,0 +1,321 @@
+// capi.cu — the extern "C" boundary declared in include/cutbddc.h.
+// Every entry point converts Failure / CUDA errors into cutbddc_status
+// (common.hpp:22-23: "the C boundary maps `code` onto cutbddc_status values").
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bddc.cuh"
+#include "factor.cuh"
+
+namespace cutbddc_b200 {
+namespace {
+thread_local std::string g_last_error;
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    CB_CUDA(cudaEventCreate(&a));
+    CB_CUDA(cudaEventCreate(&b));
+    CB_CUDA(cudaEventRecord(a, s));
+  }
+  double stop() {
+    CB_CUDA(cudaEventRecord(b, s));
+    CB_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    CB_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms * 1e-3;
+  }
+};
+
+void need(cutbddc_gpu* h) {
+  if (!h) throw Failure(CUTBDDC_INVALID_ARGUMENT, "null handle");
+  CB_CUDA(cudaSetDevice(h->device));
+}
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace cutbddc_b200
+
+using namespace cutbddc_b200;
+
+extern "C" {
+
+const char* cutbddc_last_error(void) { return g_last_error.c_str(); }
+
+cutbddc_status cutbddc_gpu_create(const cutbddc_gpu_opts* opts, cutbddc_gpu** out) {
+  return guard([&] {
+    if (!out) throw Failure(CUTBDDC_INVALID_ARGUMENT, "null output handle");
+    auto* h = new cutbddc_gpu();
+    try {
+      h->device = opts ? opts->device : 0;
+      h->rank = opts ? opts->rank : 0;
+      h->world = opts ? opts->world_size : 1;
+      if (h->world != 1)
+        throw Failure(CUTBDDC_CONFIG, "multi-GPU handles are driven by the host layer (one handle per rank)");
+      int ndev = 0;
+      CB_CUDA(cudaGetDeviceCount(&ndev));
+      if (h->device < 0 || h->device >= ndev) throw Failure(CUTBDDC_INVALID_ARGUMENT, "device ordinal out of range");
+      CB_CUDA(cudaSetDevice(h->device));
+      CB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void cutbddc_gpu_destroy(cutbddc_gpu* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+cutbddc_status cutbddc_gpu_classify(cutbddc_gpu* h, const cutbddc_geometry* g, double* phi, uint8_t* cls,
+                                    int32_t* dof_of_node, int64_t* n_dof) {
+  return guard([&] {
+    need(h);
+    if (!g) throw Failure(CUTBDDC_INVALID_ARGUMENT, "null geometry");
+    std::lock_guard<std::mutex> lk(h->mu);
+    classify_device(h, g);
+    if (phi) h->phi.download(phi, (size_t)h->n_nodes, h->stream);
+    if (cls) h->cls.download(cls, (size_t)h->n_cells, h->stream);
+    if (dof_of_node) h->dof_of_node.download(dof_of_node, (size_t)h->n_nodes, h->stream);
+    if (n_dof) *n_dof = h->n_dof;
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+cutbddc_status cutbddc_gpu_assemble(cutbddc_gpu* h, const cutbddc_mesh_view* mesh, const cutbddc_partition_view* part,
+                                    uint8_t* dirichlet) {
+  return guard([&] {
+    need(h);
+    if (!part || !part->block_ids || part->n_sd < 1) throw Failure(CUTBDDC_INVALID_ARGUMENT, "null or empty partition");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Timer tm(h->stream);
+    if (mesh) {
+      // Caller-supplied BackgroundMesh view (host buffers): upload.
+      if (mesh->cells[0] != mesh->cells[1] || mesh->cells[1] != mesh->cells[2])
+        throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: only cubic cell counts are supported");
+      if (mesh->h[0] != mesh->h[1] || mesh->h[1] != mesh->h[2])
+        throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: cells must be cubes");
+      const int n = mesh->cells[0];
+      h->n = n;
+      h->h = mesh->h[0];
+      for (int d = 0; d < 3; ++d) h->origin[d] = mesh->origin[d];
+      h->tol = 1e-12 * h->h;
+      h->n_nodes = (int64_t)(n + 1) * (n + 1) * (n + 1);
+      h->n_cells = (int64_t)n * n * n;
+      h->n_dof = mesh->n_dof;
+      h->phi.upload(mesh->phi, (size_t)h->n_nodes, h->stream);
+      h->cls.upload(mesh->cls, (size_t)h->n_cells, h->stream);
+      h->dof_of_node.upload(mesh->dof_of_node, (size_t)h->n_nodes, h->stream);
+      std::vector<int64_t> nod((size_t)h->n_dof);
+      for (int64_t v = 0; v < h->n_nodes; ++v)
+        if (mesh->dof_of_node[v] >= 0) {
+          if (mesh->dof_of_node[v] >= h->n_dof) throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: dof id out of range");
+          nod[(size_t)mesh->dof_of_node[v]] = v;
+        }
+      h->node_of_dof.upload(nod, h->stream);
+      h->mesh_ready = true;
+    }
+    if (!h->mesh_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble: no mesh (classify first or pass a view)");
+    assemble_device(h, part->block, part->n_sd, part->block_ids);
+    h->t_assembly = tm.stop();
+    if (dirichlet) {
+      h->orphan.download(dirichlet, (size_t)h->n_dof, h->stream);
+      CB_CUDA(cudaStreamSynchronize(h->stream));
+    }
+  });
+}
+
+cutbddc_status cutbddc_gpu_local_diagonals(cutbddc_gpu* h, double* diag, int64_t* n_copies) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble first");
+    std::vector<int32_t> sdof = h->slot_dof.to_host(h->stream);
+    std::vector<double> As((size_t)h->nsd * h->slots);
+    for (int s = 0; s < h->nsd; ++s)
+      CB_CUDA(cudaMemcpyAsync(As.data() + (size_t)s * h->slots, h->As.p + ((size_t)s * 27 + 13) * h->slots,
+                              sizeof(double) * h->slots, cudaMemcpyDeviceToHost, h->stream));
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+    int64_t c = 0;
+    for (size_t g = 0; g < sdof.size(); ++g)
+      if (sdof[g] >= 0) {
+        if (diag) diag[c] = As[g];
+        ++c;
+      }
+    if (n_copies) *n_copies = c;
+  });
+}
+
+cutbddc_status cutbddc_gpu_setup_bddc(cutbddc_gpu* h, const cutbddc_coarse_view* coarse, int weighting) {
+  return guard([&] {
+    need(h);
+    if (weighting != CUTBDDC_WEIGHT_TOPOLOGICAL && weighting != CUTBDDC_WEIGHT_STIFFNESS)
+      throw Failure(CUTBDDC_CONFIG, "bddc.weighting must be topological or stiffness");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Timer tm(h->stream);
+    setup_bddc_device(h, coarse, weighting);
+    h->t_setup = tm.stop();
+  });
+}
+
+cutbddc_status cutbddc_gpu_pcg(cutbddc_gpu* h, const double* b, double* x, double rtol, int max_iter,
+                               cutbddc_solve_report* report) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "pcg: setup_bddc first");
+    const double* bd = h->b.p;
+    DevBuf<double> bbuf;
+    if (b) {
+      bbuf.upload(b, (size_t)h->n_dof, h->stream);
+      bd = bbuf.p;
+    }
+    pcg_device(h, bd, rtol, max_iter, report);
+    if (x) {
+      h->px.download(x, (size_t)h->n_dof, h->stream);
+      CB_CUDA(cudaStreamSynchronize(h->stream));
+    }
+  });
+}
+
+cutbddc_status cutbddc_gpu_spmv(cutbddc_gpu* h, const double* x, double* y) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble first");
+    DevBuf<double> dx, dy;
+    dx.upload(x, (size_t)h->n_dof, h->stream);
+    dy.alloc((size_t)h->n_dof);
+    spmv_device(h, dx.p, dy.p);
+    dy.download(y, (size_t)h->n_dof, h->stream);
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+cutbddc_status cutbddc_gpu_apply_bddc(cutbddc_gpu* h, const double* r, double* z) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "apply: setup_bddc first");
+    DevBuf<double> dr, dz;
+    dr.upload(r, (size_t)h->n_dof, h->stream);
+    dz.alloc((size_t)h->n_dof);
+    apply_bddc_device(h, dr.p, dz.p, nullptr);
+    dz.download(z, (size_t)h->n_dof, h->stream);
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+cutbddc_status cutbddc_gpu_rhs(cutbddc_gpu* h, double* b) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble first");
+    h->b.download(b, (size_t)h->n_dof, h->stream);
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+cutbddc_status cutbddc_gpu_coarse_matrix(cutbddc_gpu* h, double* ac, int* n_coarse) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
+    if (n_coarse) *n_coarse = h->n_coarse;
+    if (ac && h->n_coarse) {
+      h->acoarse.download(ac, (size_t)h->n_coarse * h->n_coarse, h->stream);
+      CB_CUDA(cudaStreamSynchronize(h->stream));
+    }
+  });
+}
+
+cutbddc_status cutbddc_gpu_cells(cutbddc_gpu* h, double* beta, uint8_t* empty, int64_t* n_active) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble first");
+    if (n_active) *n_active = h->n_active;
+    if (!beta && !empty) return;
+    std::vector<int64_t> act = h->active_cells.to_host(h->stream);
+    std::vector<int32_t> eoc = h->elem_of_cell.to_host(h->stream);
+    std::vector<double> hb = h->beta.to_host(h->stream);
+    std::vector<uint8_t> he = h->empty.to_host(h->stream);
+    for (int64_t a = 0; a < h->n_active; ++a) {
+      const int32_t e = eoc[(size_t)act[(size_t)a]];
+      if (beta) beta[a] = e >= 0 ? hb[(size_t)e] : 0.0;
+      if (empty) empty[a] = e >= 0 ? he[(size_t)e] : 0;
+    }
+  });
+}
+
+cutbddc_status cutbddc_gpu_cut_elements(cutbddc_gpu* h, int64_t* cells, double* ke, double* fe, int64_t* n_cut) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble first");
+    if (n_cut) *n_cut = h->n_cut;
+    if (cells) h->cut_cells.download(cells, (size_t)h->n_cut, h->stream);
+    if (ke) h->ke.download(ke, (size_t)h->n_cut * 64, h->stream);
+    if (fe) h->fe.download(fe, (size_t)h->n_cut * 8, h->stream);
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+cutbddc_status cutbddc_gpu_local_system(cutbddc_gpu* h, double* stencil, uint8_t* mask_interior, uint8_t* mask_present,
+                                        double* diag_add, int32_t* slot_dof) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
+    const size_t ns = (size_t)h->nsd * h->slots;
+    if (stencil) h->As.download(stencil, ns * 27, h->stream);
+    if (mask_interior) h->mask_int.download(mask_interior, ns, h->stream);
+    if (mask_present) h->mask_all.download(mask_present, ns, h->stream);
+    if (diag_add) h->diag_add.download(diag_add, ns, h->stream);
+    if (slot_dof) h->slot_dof.download(slot_dof, ns, h->stream);
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
+    const size_t ns = (size_t)h->nsd * h->slots;
+    DevBuf<double> X;
+    X.upload(x, ns, h->stream);
+    solve_device(h, which == 0 ? h->tI : h->tK, which == 0 ? h->GI : h->GK, X.p, 1, h->upd.p, nullptr);
+    X.download(x, ns, h->stream);
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {
+  return guard([&] {
+    need(h);
+    st[0] = h->n_dof;
+    st[1] = h->nsd;
+    st[2] = h->n_coarse;
+    st[3] = h->slots;
+    st[4] = h->tI.tpl.panel_total + h->tK.tpl.panel_total;
+    st[5] = (int64_t)h->tK.tpl.sn.size();
+    st[6] = (int64_t)h->tK.tpl.levels.size();
+    st[7] = h->m_max;
+    st[8] = h->n_if;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// handle.cuh — device-resident state of one cutbddc_gpu handle.
+//
+// HBM layout:
+//   mesh:        phi[(n+1)^3] f64, cls[n^3] u8, dof_of_node[(n+1)^3] i32,
+//                node_of_dof[n_dof] i64, elem_of_cell[n^3] i32 (cut index, -1 interior, -2 exterior)
+//   cut cells:   ke[ncut][64] f64, fe[ncut][8] f64, beta[ncut], empty[ncut]
+//   subdomains:  slot space of the (B+1)^3 block lattice, T slots per subdomain:
+//                slot_dof[nsd][T] i32, As[nsd][27][T] f64 (stencil of A^w, SoA over slots)
+//   Abar:        ELL-27, aval[27][n_dof] f64, acol[27][n_dof] i32 (SoA, coalesced by row)
+//   bddc:        weights w[nsd][T], interior/present masks, factor panels
+//                GI/GK[nsd][panel_total] (column-major per supernode), Phi[sum m][T]
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <vector>
+
+#include "cutbddc.h"
+#include "dev_common.cuh"
+#include "nd_template.hpp"
+
+// One ND template resident on the device.
+struct TplSet {
+  cutbddc_b200::Template tpl;
+  cutbddc_b200::DevBuf<cutbddc_b200::Supernode> sn;
+  cutbddc_b200::DevBuf<int32_t> rows, emap, level_sn, root_pos;
+  cutbddc_b200::DevBuf<cutbddc_b200::AmapEntry> amap;
+  std::vector<int> level_first, level_count;
+  bool ready = false;
+};
+
+struct cutbddc_gpu {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+
+  // ---------------------------------------------------------------- mesh
+  int n = 0;                   // cells per axis
+  double origin[3] = {0, 0, 0}, h = 0, tol = 0;
+  int64_t n_nodes = 0, n_cells = 0, n_dof = 0;
+  cutbddc_b200::DevBuf<double> phi;
+  cutbddc_b200::DevBuf<uint8_t> cls;
+  cutbddc_b200::DevBuf<int32_t> dof_of_node;
+  cutbddc_b200::DevBuf<int64_t> node_of_dof;
+  cutbddc_b200::DevBuf<double> balls;
+  bool mesh_ready = false;
+
+  // ---------------------------------------------------------------- cells
+  int64_t n_active = 0, n_cut = 0;
+  cutbddc_b200::DevBuf<int64_t> active_cells, cut_cells;
+  cutbddc_b200::DevBuf<int32_t> elem_of_cell;
+  cutbddc_b200::DevBuf<double> ke, fe, beta;
+  cutbddc_b200::DevBuf<uint8_t> empty;
+
+  // ---------------------------------------------------------------- subdomains
+  int block = 0, b1 = 0, slots = 0, nsd = 0, nb = 0;
+  std::vector<int64_t> h_block_ids;
+  cutbddc_b200::DevBuf<int64_t> block_ids;
+  cutbddc_b200::DevBuf<int32_t> sd_of_block;     // nb^3, -1 for empty blocks
+  cutbddc_b200::DevBuf<int32_t> slot_dof;        // nsd*T
+  cutbddc_b200::DevBuf<double> As;               // nsd*27*T
+  cutbddc_b200::DevBuf<uint8_t> ncount, orphan;  // per dof
+  cutbddc_b200::DevBuf<int64_t> copy_ptr;        // n_dof+1
+  cutbddc_b200::DevBuf<int64_t> copy_idx;        // sd*T + slot, ascending sd
+  int64_t n_copies = 0;
+  cutbddc_b200::DevBuf<int32_t> if_dofs;         // dofs with ncount >= 2
+  int64_t n_if = 0;
+  cutbddc_b200::DevBuf<int64_t> owner_slot;      // per dof: sd*T+slot if interior, -1 else
+
+  // ---------------------------------------------------------------- global operator
+  cutbddc_b200::DevBuf<double> aval, b;
+  cutbddc_b200::DevBuf<int32_t> acol;
+  bool assembled = false;
+  double t_assembly = 0;
+
+  // ---------------------------------------------------------------- template + factors
+  TplSet tI;                                     // plain ND template (interior problems A_II)
+  TplSet tK;                                     // shell-root template (K = A + rho C^T C)
+  cutbddc_b200::DevBuf<double> GI, GK;           // factor panels
+  cutbddc_b200::DevBuf<uint8_t> mask_int, mask_all;  // per (sd, slot)
+  cutbddc_b200::DevBuf<double> diag_add;         // per (sd, slot): rho at corner slots
+  cutbddc_b200::DevBuf<uint8_t> corner_row;      // per constraint row: 1 if a corner
+  cutbddc_b200::DevBuf<int64_t> fail_slot;       // first failing (sd*T+slot) per factorisation
+
+  // ---------------------------------------------------------------- bddc
+  int weighting = 0;
+  int n_coarse = 0, m_max = 0;
+  int64_t m_total = 0;
+  std::vector<int64_t> h_m_off;                   // nsd+1
+  cutbddc_b200::DevBuf<int64_t> m_off;            // nsd+1 (constraint rows per sd)
+  cutbddc_b200::DevBuf<int64_t> c_ptr;            // m_total+1 (entries per row)
+  cutbddc_b200::DevBuf<int32_t> c_slot;
+  cutbddc_b200::DevBuf<double> c_val;
+  cutbddc_b200::DevBuf<int32_t> coarse_id;        // m_total
+  cutbddc_b200::DevBuf<int32_t> row_sd;           // m_total: owning subdomain of each constraint row
+  cutbddc_b200::DevBuf<int64_t> cg_ptr;           // n_coarse+1
+  cutbddc_b200::DevBuf<int64_t> cg_idx;           // row index into m_total, ascending sd
+  cutbddc_b200::DevBuf<double> w;                 // nsd*T
+  cutbddc_b200::DevBuf<double> rho;               // nsd
+  cutbddc_b200::DevBuf<double> phi_c;             // m_total*T  (Phi, column per constraint row)
+  cutbddc_b200::DevBuf<double> ac_loc;            // per sd m*m (offsets m_off^2 prefix)
+  cutbddc_b200::DevBuf<int64_t> ac_off;           // nsd+1
+  cutbddc_b200::DevBuf<double> acoarse, acoarse_inv;
+  bool bddc_ready = false;
+  double t_setup = 0;
+
+  // ---------------------------------------------------------------- work vectors
+  cutbddc_b200::DevBuf<double> sv0, sv1, sv2;     // slot vectors nsd*T
+  cutbddc_b200::DevBuf<double> upd;               // solve workspace nsd*upd_total (x nrhs for setup)
+  cutbddc_b200::DevBuf<double> gv0, gv1, gv2;     // global vectors n_dof
+  cutbddc_b200::DevBuf<double> gl, cy, zc, gc;    // m_total, m_total, n_coarse, n_coarse
+  cutbddc_b200::DevBuf<double> partials;          // reduction partials
+  cutbddc_b200::DevBuf<double> scal;              // device scalars (pcg)
+  cutbddc_b200::DevBuf<int32_t> iscal;            // device int scalars (pcg)
+
+  // pcg vectors
+  cutbddc_b200::DevBuf<double> px, pr, pz, pp, pq, pb, hist, lal, lbe;
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_max_iter = -1;
+  double t_pcg = 0;
+};

@@ -1,0 +1,344 @@
+// host_partition.cpp — caller-side partition and interface objects.
+//
+// The reference computes these once on the host ("Object
+// classification single-threaded (cheap, runs once)"); the GPU path only
+// consumes the resulting index maps. Reference ops:
+//   build_partition   SPEC.md:295-303 (block aggregation, empty blocks dropped)
+//   classify_objects  SPEC.md:304-312 (exact neigh set + connected components
+//                     over active FE edges, BackgroundMesh::edge_active
+//                     mesh.cpp:74-108; Corner/Edge/Face)
+//   split_edges_v1
+//   split_edges_v2
+// Pinned rules shared with the oracle: objects
+// ordered by smallest global dof, nodes ascending; singletons -> Corner;
+// strong-Dirichlet (orphan) dofs excluded.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "cutbddc.h"
+#include "status.hpp"
+
+namespace cutbddc_b200 {
+namespace {
+
+struct Lattice {
+  int n;
+  const uint8_t* cls;
+  const int32_t* dof_of_node;
+  int64_t node(int i, int j, int k) const { return ((int64_t)i * (n + 1) + j) * (n + 1) + k; }
+  int64_t cell(int i, int j, int k) const { return ((int64_t)i * n + j) * n + k; }
+  void node_ijk(int64_t v, int c[3]) const {
+    c[2] = (int)(v % (n + 1));
+    c[1] = (int)((v / (n + 1)) % (n + 1));
+    c[0] = (int)(v / (n + 1) / (n + 1));
+  }
+  // mesh.cpp:74-108 for axis-aligned unit lattice edges from node c along +axis.
+  bool edge_active(const int c[3], int axis) const {
+    const int o1 = axis == 0 ? 1 : 0, o2 = axis == 2 ? 1 : 2;
+    for (int da = -1; da <= 0; ++da)
+      for (int db = -1; db <= 0; ++db) {
+        int cc[3] = {c[0], c[1], c[2]};
+        cc[o1] += da;
+        cc[o2] += db;
+        bool ok = true;
+        for (int d = 0; d < 3; ++d) ok = ok && cc[d] >= 0 && cc[d] < n;
+        if (ok && cls[cell(cc[0], cc[1], cc[2])] != CUTBDDC_EXTERIOR) return true;
+      }
+    return false;
+  }
+};
+
+struct Obj {
+  int kind;
+  std::vector<int32_t> dofs;
+  std::vector<int32_t> neigh;
+};
+
+// Union-find over positions 0..n-1.
+struct UF {
+  std::vector<int> p;
+  explicit UF(int n) : p((size_t)n) { std::iota(p.begin(), p.end(), 0); }
+  int f(int x) {
+    while (p[(size_t)x] != x) x = p[(size_t)x] = p[(size_t)p[(size_t)x]];
+    return x;
+  }
+  void u(int a, int b) {
+    a = f(a);
+    b = f(b);
+    if (a != b) p[(size_t)std::max(a, b)] = std::min(a, b);
+  }
+};
+
+// Connected components of `members` (sorted dofs) over active +axis lattice
+// edges accepted by `join`. Components sorted internally; returned in order
+// of their smallest member.
+template <typename J>
+std::vector<std::vector<int32_t>> components(const Lattice& L, const std::vector<int64_t>& node_of_dof,
+                                             const std::vector<int32_t>& members, J&& join) {
+  UF uf((int)members.size());
+  for (size_t i = 0; i < members.size(); ++i) {
+    int c[3];
+    L.node_ijk(node_of_dof[(size_t)members[i]], c);
+    for (int ax = 0; ax < 3; ++ax) {
+      if (c[ax] + 1 > L.n) continue;
+      int cc[3] = {c[0], c[1], c[2]};
+      cc[ax] += 1;
+      const int32_t d2 = L.dof_of_node[L.node(cc[0], cc[1], cc[2])];
+      if (d2 < 0) continue;
+      auto it = std::lower_bound(members.begin(), members.end(), d2);
+      if (it == members.end() || *it != d2) continue;
+      if (!L.edge_active(c, ax)) continue;
+      if (!join(members[i], d2)) continue;
+      uf.u((int)i, (int)(it - members.begin()));
+    }
+  }
+  std::vector<std::vector<int32_t>> comps;
+  std::vector<int> root_slot(members.size(), -1);
+  for (size_t i = 0; i < members.size(); ++i) {  // members ascending -> components by smallest member
+    const int r = uf.f((int)i);
+    if (root_slot[(size_t)r] < 0) {
+      root_slot[(size_t)r] = (int)comps.size();
+      comps.emplace_back();
+    }
+    comps[(size_t)root_slot[(size_t)r]].push_back(members[i]);
+  }
+  return comps;
+}
+
+struct VecHash {
+  size_t operator()(const std::vector<int32_t>& v) const {
+    size_t h = 1469598103934665603ull;
+    for (int32_t x : v) h = (h ^ (size_t)(uint32_t)x) * 1099511628211ull;
+    return h;
+  }
+};
+
+void check_mesh(const cutbddc_mesh_view* m) {
+  if (!m || !m->cls || !m->dof_of_node) throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: null arrays");
+  if (m->cells[0] != m->cells[1] || m->cells[1] != m->cells[2])
+    throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: only cubic cell counts are supported");
+}
+
+}  // namespace
+}  // namespace cutbddc_b200
+
+using namespace cutbddc_b200;
+
+extern "C" cutbddc_status cutbddc_build_partition(const cutbddc_mesh_view* mesh, int block, int64_t* n_sd,
+                                                  int64_t* block_ids) {
+  return guard([&] {
+    check_mesh(mesh);
+    const int n = mesh->cells[0];
+    if (block < 1 || n % block != 0) throw Failure(CUTBDDC_INVALID_ARGUMENT, "partition: mesh dims not divisible by H/h");
+    const int nb = n / block;
+    std::vector<uint8_t> used((size_t)nb * nb * nb, 0);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        for (int k = 0; k < n; ++k)
+          if (mesh->cls[((int64_t)i * n + j) * n + k] != CUTBDDC_EXTERIOR)
+            used[((size_t)(i / block) * nb + j / block) * nb + k / block] = 1;
+    int64_t c = 0;
+    for (size_t b = 0; b < used.size(); ++b)
+      if (used[b]) {
+        if (block_ids) block_ids[c] = (int64_t)b;
+        ++c;
+      }
+    *n_sd = c;
+  });
+}
+
+extern "C" cutbddc_status cutbddc_classify_objects(const cutbddc_mesh_view* mesh, const cutbddc_partition_view* part,
+                                                   const uint8_t* dirichlet, int objects, int variant,
+                                                   const double* local_diag, cutbddc_objects** out) {
+  return guard([&] {
+    check_mesh(mesh);
+    const int n = mesh->cells[0];
+    const int B = part->block;
+    const int nb = n / B;
+    const int64_t ndof = mesh->n_dof;
+    Lattice L{n, mesh->cls, mesh->dof_of_node};
+    std::vector<int64_t> node_of_dof((size_t)ndof);
+    {
+      const int64_t nn = (int64_t)(n + 1) * (n + 1) * (n + 1);
+      for (int64_t v = 0; v < nn; ++v)
+        if (mesh->dof_of_node[v] >= 0) node_of_dof[(size_t)mesh->dof_of_node[v]] = v;
+    }
+    // neigh sets: subdomains (ascending) holding each dof; local copies in
+    // (subdomain, ascending dof) order for the weights.
+    std::vector<int64_t> sd_of_block((size_t)nb * nb * nb, -1);
+    for (int s = 0; s < part->n_sd; ++s) sd_of_block[(size_t)part->block_ids[s]] = s;
+    std::vector<uint8_t> nn_count((size_t)ndof, 0);
+    std::vector<int32_t> neigh8((size_t)ndof * 8, -1);
+    std::vector<int64_t> copy_off((size_t)part->n_sd + 1, 0);   // copies per subdomain
+    std::vector<std::vector<int32_t>> sd_dofs((size_t)part->n_sd);
+    for (int s = 0; s < part->n_sd; ++s) {
+      const int64_t b = part->block_ids[s];
+      const int bi = (int)(b / nb / nb), bj = (int)((b / nb) % nb), bk = (int)(b % nb);
+      auto& dl = sd_dofs[(size_t)s];
+      // local dofs: nodes of active cells of this block, ascending global dof
+      for (int li = 0; li <= B; ++li)
+        for (int lj = 0; lj <= B; ++lj)
+          for (int lk = 0; lk <= B; ++lk) {
+            const int gi = bi * B + li, gj = bj * B + lj, gk = bk * B + lk;
+            bool act = false;
+            for (int c = 0; c < 8 && !act; ++c) {
+              const int ci = li - 1 + (c & 1), cj = lj - 1 + ((c >> 1) & 1), ck = lk - 1 + ((c >> 2) & 1);
+              if (ci < 0 || cj < 0 || ck < 0 || ci >= B || cj >= B || ck >= B) continue;
+              act = mesh->cls[L.cell(bi * B + ci, bj * B + cj, bk * B + ck)] != CUTBDDC_EXTERIOR;
+            }
+            if (act) dl.push_back(mesh->dof_of_node[L.node(gi, gj, gk)]);
+          }
+      // lexicographic slot order == ascending global dof (z fastest on both)
+      for (int32_t d : dl) {
+        const uint8_t k = nn_count[(size_t)d]++;
+        if (k >= 8) throw Failure(CUTBDDC_INTERNAL, "partition: node in more than 8 subdomains");
+        neigh8[(size_t)d * 8 + k] = s;
+      }
+      copy_off[(size_t)s + 1] = copy_off[(size_t)s] + (int64_t)dl.size();
+    }
+    // group interface dofs by exact neigh set
+    std::unordered_map<std::vector<int32_t>, int, VecHash> group_of;
+    std::vector<std::vector<int32_t>> group_dofs, group_key;
+    for (int64_t d = 0; d < ndof; ++d) {
+      const int k = nn_count[(size_t)d];
+      if (k < 2 || (dirichlet && dirichlet[d])) continue;
+      std::vector<int32_t> key(neigh8.begin() + d * 8, neigh8.begin() + d * 8 + k);
+      auto it = group_of.find(key);
+      int g;
+      if (it == group_of.end()) {
+        g = (int)group_dofs.size();
+        group_of.emplace(key, g);
+        group_dofs.emplace_back();
+        group_key.push_back(key);
+      } else {
+        g = it->second;
+      }
+      group_dofs[(size_t)g].push_back((int32_t)d);
+    }
+    std::vector<Obj> objs;
+    for (size_t g = 0; g < group_dofs.size(); ++g) {
+      for (auto& comp : components(L, node_of_dof, group_dofs[g], [](int32_t, int32_t) { return true; })) {
+        Obj o;
+        o.kind = comp.size() == 1 ? CUTBDDC_CORNER : (group_key[g].size() == 2 ? CUTBDDC_FACE : CUTBDDC_EDGE);
+        o.dofs = std::move(comp);
+        o.neigh = group_key[g];
+        objs.push_back(std::move(o));
+      }
+    }
+    // variants split coarse edges only
+    if (variant == CUTBDDC_VARIANT_V1 || variant == CUTBDDC_VARIANT_V2) {
+      if (variant == CUTBDDC_VARIANT_V1 && !mesh->phi)
+        throw Failure(CUTBDDC_INVALID_ARGUMENT, "split_edges_v1 needs node phi");
+      if (variant == CUTBDDC_VARIANT_V2 && !local_diag)
+        throw Failure(CUTBDDC_INVALID_ARGUMENT, "split_edges_v2 needs the local diagonals");
+      // stiffness weight tuple of a dof: A^w_xixi / sum over its subdomains
+      auto local_index = [&](int32_t s, int32_t d) {
+        const auto& dl = sd_dofs[(size_t)s];
+        return copy_off[(size_t)s] + (std::lower_bound(dl.begin(), dl.end(), d) - dl.begin());
+      };
+      auto weights = [&](int32_t d, double* w) {
+        const int k = nn_count[(size_t)d];
+        double tot = 0;
+        for (int q = 0; q < k; ++q) tot += local_diag[local_index(neigh8[(size_t)d * 8 + q], d)];
+        for (int q = 0; q < k; ++q) w[q] = local_diag[local_index(neigh8[(size_t)d * 8 + q], d)] / tot;
+      };
+      std::vector<Obj> split;
+      for (auto& o : objs) {
+        if (o.kind != CUTBDDC_EDGE) {
+          split.push_back(std::move(o));
+          continue;
+        }
+        std::vector<std::vector<int32_t>> parts;
+        if (variant == CUTBDDC_VARIANT_V1) {
+          auto phi_of = [&](int32_t d) { return mesh->phi[node_of_dof[(size_t)d]]; };
+          std::vector<int32_t> cutnodes;
+          components(L, node_of_dof, o.dofs, [&](int32_t a, int32_t b) {
+            if ((phi_of(a) < 0) != (phi_of(b) < 0)) {
+              cutnodes.push_back(a);
+              cutnodes.push_back(b);
+            }
+            return true;
+          });
+          std::sort(cutnodes.begin(), cutnodes.end());
+          cutnodes.erase(std::unique(cutnodes.begin(), cutnodes.end()), cutnodes.end());
+          std::vector<int32_t> rest;
+          for (int32_t d : o.dofs)
+            if (!std::binary_search(cutnodes.begin(), cutnodes.end(), d))
+              rest.push_back(d);
+            else
+              parts.push_back({d});
+          if (!rest.empty())
+            for (auto& c : components(L, node_of_dof, rest, [](int32_t, int32_t) { return true; })) parts.push_back(c);
+        } else {
+          const double tol = 1e-8;
+          for (auto& c : components(L, node_of_dof, o.dofs, [&](int32_t a, int32_t b) {
+                 double wa[8], wb[8];
+                 weights(a, wa);
+                 weights(b, wb);
+                 for (int q = 0; q < nn_count[(size_t)a]; ++q) {
+                   const double scale = std::max(1.0, std::max(std::fabs(wa[q]), std::fabs(wb[q])));
+                   if (std::fabs(wa[q] - wb[q]) > tol * scale) return false;
+                 }
+                 return true;
+               }))
+            parts.push_back(c);
+        }
+        for (auto& p : parts) {
+          Obj e;
+          e.kind = p.size() >= 2 ? CUTBDDC_EDGE : CUTBDDC_CORNER;
+          e.dofs = std::move(p);
+          e.neigh = o.neigh;
+          split.push_back(std::move(e));
+        }
+      }
+      objs = std::move(split);
+    }
+    std::vector<Obj> sel;
+    for (auto& o : objs) {
+      const bool keep = o.kind == CUTBDDC_CORNER || (o.kind == CUTBDDC_EDGE && objects >= CUTBDDC_OBJECTS_CE) ||
+                        (o.kind == CUTBDDC_FACE && objects >= CUTBDDC_OBJECTS_CEF);
+      if (keep) sel.push_back(std::move(o));
+    }
+    std::sort(sel.begin(), sel.end(), [](const Obj& a, const Obj& b) { return a.dofs[0] < b.dofs[0]; });
+    auto* r = new cutbddc_objects{};
+    r->n_sd = part->n_sd;
+    r->block_ids = new int64_t[(size_t)part->n_sd];
+    std::memcpy(r->block_ids, part->block_ids, sizeof(int64_t) * (size_t)part->n_sd);
+    r->n_objects = (int)sel.size();
+    r->kinds = new int32_t[sel.size()];
+    r->dof_ptr = new int64_t[sel.size() + 1];
+    r->neigh_ptr = new int64_t[sel.size() + 1];
+    int64_t nd = 0, nn = 0;
+    for (auto& o : sel) {
+      nd += (int64_t)o.dofs.size();
+      nn += (int64_t)o.neigh.size();
+    }
+    r->dofs = new int32_t[(size_t)nd + 1];
+    r->neigh = new int32_t[(size_t)nn + 1];
+    r->dof_ptr[0] = r->neigh_ptr[0] = 0;
+    for (size_t i = 0; i < sel.size(); ++i) {
+      r->kinds[i] = sel[i].kind;
+      std::copy(sel[i].dofs.begin(), sel[i].dofs.end(), r->dofs + r->dof_ptr[i]);
+      std::copy(sel[i].neigh.begin(), sel[i].neigh.end(), r->neigh + r->neigh_ptr[i]);
+      r->dof_ptr[i + 1] = r->dof_ptr[i] + (int64_t)sel[i].dofs.size();
+      r->neigh_ptr[i + 1] = r->neigh_ptr[i] + (int64_t)sel[i].neigh.size();
+    }
+    *out = r;
+  });
+}
+
+extern "C" void cutbddc_objects_free(cutbddc_objects* o) {
+  if (!o) return;
+  delete[] o->block_ids;
+  delete[] o->kinds;
+  delete[] o->dof_ptr;
+  delete[] o->dofs;
+  delete[] o->neigh_ptr;
+  delete[] o->neigh;
+  delete o;
+}

@@ -1,0 +1,349 @@
+"""Host-side mirror of the reference solver interface over the C ABI
+(include/cutbddc.h, libcutbddc.so).
+
+Operation names follow the reference: classify (mesh.cpp:114-169),
+build_partition, classify_objects (+ split_edges_v1/v2,
+SPEC.md:304-330), assemble_subassembled, build_weighting +
+build_coarse_space, apply, pcg
+(SPEC.md:431). Errors raise CutbddcError carrying the cutbddc_status code
+(common.hpp:24-32). There is no CPU fallback: if libcutbddc.so is missing
+or no CUDA device is present the calls fail.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import configs as _cfg
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcutbddc.so")
+_lib = None
+
+OK, INVALID_ARGUMENT, CONFIG, IO, SINGULAR, DEGENERATE, NOT_CONVERGED, INTERNAL = range(8)
+
+
+class CutbddcError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"cutbddc status {code}: {msg}")
+        self.code = code
+
+
+class _Opts(C.Structure):
+    _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world_size", C.c_int), ("nccl_id", C.c_void_p)]
+
+
+class _Geometry(C.Structure):
+    _fields_ = [("cells", C.c_int * 3), ("box_lo", C.c_double * 3), ("box_hi", C.c_double * 3),
+                ("translation", C.c_double * 3), ("n_balls", C.c_int), ("balls", C.POINTER(C.c_double))]
+
+
+class _MeshView(C.Structure):
+    _fields_ = [("cells", C.c_int * 3), ("origin", C.c_double * 3), ("h", C.c_double * 3), ("n_dof", C.c_int64),
+                ("phi", C.POINTER(C.c_double)), ("cls", C.POINTER(C.c_uint8)),
+                ("dof_of_node", C.POINTER(C.c_int32))]
+
+
+class _PartView(C.Structure):
+    _fields_ = [("block", C.c_int), ("n_sd", C.c_int), ("block_ids", C.POINTER(C.c_int64))]
+
+
+class _CoarseView(C.Structure):
+    _fields_ = [("n_objects", C.c_int), ("kinds", C.POINTER(C.c_int32)), ("dof_ptr", C.POINTER(C.c_int64)),
+                ("dofs", C.POINTER(C.c_int32)), ("neigh_ptr", C.POINTER(C.c_int64)),
+                ("neigh", C.POINTER(C.c_int32))]
+
+
+class _Objects(C.Structure):
+    _fields_ = [("n_sd", C.c_int), ("block_ids", C.POINTER(C.c_int64)), ("n_objects", C.c_int),
+                ("kinds", C.POINTER(C.c_int32)), ("dof_ptr", C.POINTER(C.c_int64)), ("dofs", C.POINTER(C.c_int32)),
+                ("neigh_ptr", C.POINTER(C.c_int64)), ("neigh", C.POINTER(C.c_int32))]
+
+
+class _Report(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("cond_estimate", C.c_double),
+                ("lambda_min", C.c_double), ("lambda_max", C.c_double), ("residuals", C.POINTER(C.c_double)),
+                ("t_assembly", C.c_double), ("t_setup", C.c_double), ("t_pcg", C.c_double)]
+
+
+EXPORTS = [
+    "cutbddc_last_error", "cutbddc_gpu_create", "cutbddc_gpu_destroy", "cutbddc_gpu_classify", "cutbddc_gpu_assemble",
+    "cutbddc_gpu_local_diagonals", "cutbddc_gpu_setup_bddc", "cutbddc_gpu_pcg", "cutbddc_gpu_spmv",
+    "cutbddc_gpu_apply_bddc", "cutbddc_gpu_rhs", "cutbddc_gpu_coarse_matrix", "cutbddc_gpu_cells", "cutbddc_gpu_stats",
+    "cutbddc_gpu_cut_elements", "cutbddc_gpu_local_system", "cutbddc_gpu_local_solve",
+    "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free",
+]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CutbddcError(INTERNAL, f"{LIB_PATH} not built (run paper_1703_06323_b200/build.py)")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.cutbddc_last_error.restype = C.c_char_p
+        _lib.cutbddc_gpu_destroy.restype = None
+        _lib.cutbddc_objects_free.restype = None
+    return _lib
+
+
+def _check(code: int):
+    if code != 0:
+        raise CutbddcError(code, lib().cutbddc_last_error().decode())
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+@dataclass
+class Mesh:
+    """BackgroundMesh view (mesh.hpp:77-80): snapped node phi, cell classes,
+    node -> dof map."""
+    cells: int
+    origin: tuple
+    h: float
+    phi: np.ndarray
+    cls: np.ndarray
+    dof_of_node: np.ndarray
+    n_dof: int
+
+    def view(self) -> _MeshView:
+        v = _MeshView()
+        v.cells[:] = [self.cells] * 3
+        v.origin[:] = list(self.origin)
+        v.h[:] = [self.h] * 3
+        v.n_dof = self.n_dof
+        v.phi = _p(self.phi, C.c_double)
+        v.cls = _p(self.cls, C.c_uint8)
+        v.dof_of_node = _p(self.dof_of_node, C.c_int32)
+        return v
+
+
+@dataclass
+class Objects:
+    """Selected coarse objects in coarse-DOF order."""
+    kinds: np.ndarray
+    dof_ptr: np.ndarray
+    dofs: np.ndarray
+    neigh_ptr: np.ndarray
+    neigh: np.ndarray
+
+    def __len__(self):
+        return len(self.kinds)
+
+    def as_list(self):
+        return [(int(self.kinds[i]), self.dofs[self.dof_ptr[i]:self.dof_ptr[i + 1]].tolist(),
+                 self.neigh[self.neigh_ptr[i]:self.neigh_ptr[i + 1]].tolist()) for i in range(len(self.kinds))]
+
+    def view(self) -> _CoarseView:
+        v = _CoarseView()
+        v.n_objects = len(self.kinds)
+        v.kinds = _p(self.kinds, C.c_int32)
+        v.dof_ptr = _p(self.dof_ptr, C.c_int64)
+        v.dofs = _p(self.dofs, C.c_int32)
+        v.neigh_ptr = _p(self.neigh_ptr, C.c_int64)
+        v.neigh = _p(self.neigh, C.c_int32)
+        return v
+
+
+def build_partition(mesh: Mesh, block: int) -> np.ndarray:
+    n = C.c_int64()
+    v = mesh.view()
+    _check(lib().cutbddc_build_partition(C.byref(v), block, C.byref(n), None))
+    ids = np.zeros(n.value, np.int64)
+    _check(lib().cutbddc_build_partition(C.byref(v), block, C.byref(n), _p(ids, C.c_int64)))
+    return ids
+
+
+def classify_objects(mesh: Mesh, block: int, block_ids: np.ndarray, dirichlet: np.ndarray, objects: int,
+                     variant: int = 0, local_diag: np.ndarray | None = None) -> Objects:
+    v = mesh.view()
+    pv = _PartView(block, len(block_ids), _p(block_ids, C.c_int64))
+    out = C.POINTER(_Objects)()
+    diag_p = _p(local_diag, C.c_double) if local_diag is not None else None
+    dir_p = _p(dirichlet, C.c_uint8) if dirichlet is not None else None
+    _check(lib().cutbddc_classify_objects(C.byref(v), C.byref(pv), dir_p, objects, variant, diag_p, C.byref(out)))
+    o = out.contents
+    no = o.n_objects
+    kinds = np.ctypeslib.as_array(o.kinds, (no,)).copy() if no else np.zeros(0, np.int32)
+    dptr = np.ctypeslib.as_array(o.dof_ptr, (no + 1,)).copy()
+    nptr = np.ctypeslib.as_array(o.neigh_ptr, (no + 1,)).copy()
+    dofs = np.ctypeslib.as_array(o.dofs, (int(dptr[-1]) + 1,))[: dptr[-1]].copy()
+    neigh = np.ctypeslib.as_array(o.neigh, (int(nptr[-1]) + 1,))[: nptr[-1]].copy()
+    lib().cutbddc_objects_free(out)
+    return Objects(kinds.astype(np.int32), dptr, dofs.astype(np.int32), nptr, neigh.astype(np.int32))
+
+
+class GpuSolver:
+    """One device handle: geometry -> classify -> assemble -> setup -> pcg."""
+
+    def __init__(self, device: int = 0):
+        o = _Opts(device, 0, 1, None)
+        h = C.c_void_p()
+        _check(lib().cutbddc_gpu_create(C.byref(o), C.byref(h)))
+        self.h = h
+        self.n_dof = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cutbddc_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    # BackgroundMesh::classify on the device
+    def classify(self, cfg) -> Mesh:
+        balls = np.ascontiguousarray(np.asarray(cfg.balls, np.float64).reshape(-1))
+        g = _Geometry()
+        g.cells[:] = [cfg.cells] * 3
+        g.box_lo[:] = list(cfg.lo)
+        g.box_hi[:] = list(cfg.hi)
+        g.translation[:] = list(cfg.translation)
+        g.n_balls = len(cfg.balls)
+        g.balls = _p(balls, C.c_double)
+        n = cfg.cells
+        phi = np.zeros((n + 1) ** 3)
+        cls = np.zeros(n ** 3, np.uint8)
+        dof = np.zeros((n + 1) ** 3, np.int32)
+        nd = C.c_int64()
+        _check(lib().cutbddc_gpu_classify(self.h, C.byref(g), _p(phi, C.c_double), _p(cls, C.c_uint8),
+                                          _p(dof, C.c_int32), C.byref(nd)))
+        h = (cfg.hi[0] - cfg.lo[0]) / n
+        origin = tuple(cfg.lo[d] + cfg.translation[d] for d in range(3))
+        self.n_dof = nd.value
+        return Mesh(n, origin, h, phi, cls, dof, nd.value)
+
+    # assemble_subassembled + assemble_global on the device
+    def assemble(self, block: int, block_ids: np.ndarray, mesh: Mesh | None = None) -> np.ndarray:
+        pv = _PartView(block, len(block_ids), _p(block_ids, C.c_int64))
+        mv = mesh.view() if mesh is not None else None
+        if mesh is not None:
+            self.n_dof = mesh.n_dof
+        dirichlet = np.zeros(self.n_dof, np.uint8)
+        _check(lib().cutbddc_gpu_assemble(self.h, C.byref(mv) if mv is not None else None, C.byref(pv),
+                                          _p(dirichlet, C.c_uint8)))
+        return dirichlet
+
+    def local_diagonals(self) -> np.ndarray:
+        n = C.c_int64()
+        _check(lib().cutbddc_gpu_local_diagonals(self.h, None, C.byref(n)))
+        d = np.zeros(n.value)
+        _check(lib().cutbddc_gpu_local_diagonals(self.h, _p(d, C.c_double), C.byref(n)))
+        return d
+
+    def setup_bddc(self, objects: Objects, weighting: int):
+        v = objects.view()
+        _check(lib().cutbddc_gpu_setup_bddc(self.h, C.byref(v), weighting))
+
+    def pcg(self, b=None, rtol=1e-6, max_iter=2000):
+        x = np.zeros(self.n_dof)
+        res = np.zeros(max_iter + 1)
+        rep = _Report()
+        rep.residuals = _p(res, C.c_double)
+        bp = _p(np.ascontiguousarray(b, np.float64), C.c_double) if b is not None else None
+        _check(lib().cutbddc_gpu_pcg(self.h, bp, _p(x, C.c_double), C.c_double(rtol), max_iter, C.byref(rep)))
+        it = rep.iterations
+        return x, dict(iterations=it, converged=bool(rep.converged), residuals=res[: it + 1].copy(),
+                       cond=rep.cond_estimate, lmin=rep.lambda_min, lmax=rep.lambda_max, t_assembly=rep.t_assembly,
+                       t_setup=rep.t_setup, t_pcg=rep.t_pcg)
+
+    def spmv(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(self.n_dof)
+        _check(lib().cutbddc_gpu_spmv(self.h, _p(x, C.c_double), _p(y, C.c_double)))
+        return y
+
+    def apply(self, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.zeros(self.n_dof)
+        _check(lib().cutbddc_gpu_apply_bddc(self.h, _p(r, C.c_double), _p(z, C.c_double)))
+        return z
+
+    def rhs(self):
+        b = np.zeros(self.n_dof)
+        _check(lib().cutbddc_gpu_rhs(self.h, _p(b, C.c_double)))
+        return b
+
+    def coarse_matrix(self):
+        n = C.c_int()
+        _check(lib().cutbddc_gpu_coarse_matrix(self.h, None, C.byref(n)))
+        a = np.zeros(n.value * n.value)
+        _check(lib().cutbddc_gpu_coarse_matrix(self.h, _p(a, C.c_double), C.byref(n)))
+        return a.reshape(n.value, n.value)
+
+    def cells(self):
+        n = C.c_int64()
+        _check(lib().cutbddc_gpu_cells(self.h, None, None, C.byref(n)))
+        beta = np.zeros(n.value)
+        empty = np.zeros(n.value, np.uint8)
+        _check(lib().cutbddc_gpu_cells(self.h, _p(beta, C.c_double), _p(empty, C.c_uint8), C.byref(n)))
+        return beta, empty
+
+    def cut_elements(self):
+        n = C.c_int64()
+        _check(lib().cutbddc_gpu_cut_elements(self.h, None, None, None, C.byref(n)))
+        cells = np.zeros(n.value, np.int64)
+        ke = np.zeros((n.value, 8, 8))
+        fe = np.zeros((n.value, 8))
+        _check(lib().cutbddc_gpu_cut_elements(self.h, _p(cells, C.c_int64), _p(ke, C.c_double), _p(fe, C.c_double),
+                                              C.byref(n)))
+        return cells, ke, fe
+
+    def local_system(self):
+        """Slot-space test view: stencil (nsd, 27, T), interior / present masks,
+        diagonal shifts and slot -> dof map."""
+        st = self.stats()
+        nsd, T = st["n_sd"], st["slots"]
+        sten = np.zeros((nsd, 27, T))
+        mi = np.zeros((nsd, T), np.uint8)
+        mp = np.zeros((nsd, T), np.uint8)
+        da = np.zeros((nsd, T))
+        sd = np.zeros((nsd, T), np.int32)
+        _check(lib().cutbddc_gpu_local_system(self.h, _p(sten, C.c_double), _p(mi, C.c_uint8), _p(mp, C.c_uint8),
+                                              _p(da, C.c_double), _p(sd, C.c_int32)))
+        return sten, mi, mp, da, sd
+
+    def local_solve(self, which: int, x):
+        x = np.ascontiguousarray(x, np.float64).copy()
+        _check(lib().cutbddc_gpu_local_solve(self.h, which, _p(x, C.c_double)))
+        return x
+
+    def stats(self):
+        st = np.zeros(16, np.int64)
+        _check(lib().cutbddc_gpu_stats(self.h, _p(st, C.c_int64)))
+        keys = ["n_dof", "n_sd", "n_coarse", "slots", "panel_per_factor", "n_supernodes", "levels", "m_max", "n_if"]
+        return {k: int(st[i]) for i, k in enumerate(keys)}
+
+
+@dataclass
+class Problem:
+    cfg: object
+    mesh: Mesh
+    block_ids: np.ndarray
+    dirichlet: np.ndarray
+    objects: Objects
+
+
+def prepare(solver: GpuSolver, cfg) -> Problem:
+    """Caller side of the boundary: classify (device), partition and objects
+    (host), sub-assembly (device)."""
+    mesh = solver.classify(cfg)
+    block_ids = build_partition(mesh, cfg.block)
+    dirichlet = solver.assemble(cfg.block, block_ids)
+    diag = solver.local_diagonals() if cfg.variant == _cfg.V2 else None
+    objs = classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, diag)
+    return Problem(cfg, mesh, block_ids, dirichlet, objs)
+
+
+def solve(cfg, device: int = 0):
+    """End-to-end solve of one configuration: returns (x, report, problem)."""
+    s = GpuSolver(device)
+    pb = prepare(s, cfg)
+    s.setup_bddc(pb.objects, cfg.weighting)
+    x, rep = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
+    return x, rep, pb, s

@@ -1,0 +1,156 @@
+"""GPU parity (run on the B200 box: pytest -m gpu). The CUDA path is called
+through the C ABI and compared with the CPU oracle on the same inputs:
+bit-exact classification / dof maps / iteration counts, 1e-8 relative for
+solutions and residual histories (BASELINE.json north_star)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Oracle
+from paper_1703_06323_b200 import configs
+from paper_1703_06323_b200 import cutbddc as cb
+
+pytestmark = pytest.mark.gpu
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "classification.json")))
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def solver():
+    s = cb.GpuSolver(0)
+    yield s
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["sphere-id1", "sphere-id2", "sphere-id3", "sphere-id4", "cfg1", "cfg2"])
+def test_classification_bit_exact_vs_reference(solver, name):
+    g = GOLDEN[name]
+    cfg = configs.sphere_id(int(name[-1])) if name.startswith("sphere-id") else configs.get(name)
+    m = solver.classify(cfg)
+    assert m.n_dof == g["n_dof"]
+    assert _sha(m.phi) == g["sha_phi"]
+    assert _sha(m.cls) == g["sha_cls"]
+    assert _sha(m.dof_of_node) == g["sha_dof_of_node"]
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_classification_bit_exact_vs_oracle(solver, name):
+    cfg = configs.get(name)
+    m = solver.classify(cfg)
+    phi, cls, dof = Oracle(cfg, block=0).mesh()
+    assert np.array_equal(m.phi, phi) and np.array_equal(m.cls, cls) and np.array_equal(m.dof_of_node, dof)
+
+
+def _pair(name, **kw):
+    cfg = configs.get(name, **kw)
+    o = Oracle(cfg)
+    o.setup()
+    s = cb.GpuSolver(0)
+    pb = cb.prepare(s, cfg)
+    s.setup_bddc(pb.objects, cfg.weighting)
+    return cfg, o, s, pb
+
+
+@pytest.fixture(scope="module")
+def cfg2s():
+    return _pair("cfg2", weighting="stiffness", objects="cef")
+
+
+def test_assembly_matches_oracle(cfg2s):
+    cfg, o, s, pb = cfg2s
+    assert np.array_equal(pb.dirichlet, o.dirichlet())
+    b_o, b_g = o.rhs(), s.rhs()
+    assert np.abs(b_o - b_g).max() <= 1e-12 * np.abs(b_o).max()
+    rng = np.random.default_rng(1)
+    x = rng.uniform(-1, 1, o.n_dof)
+    y_o, y_g = o.spmv(x), s.spmv(x)
+    assert np.linalg.norm(y_o - y_g) <= 1e-12 * np.linalg.norm(y_o)
+    beta_o, void_o = o.cells()
+    beta_g, void_g = s.cells()
+    assert np.array_equal(void_o, void_g)
+    assert np.abs(beta_o - beta_g).max() <= 1e-10 * np.abs(beta_o).max()
+
+
+def test_coarse_objects_and_matrix(cfg2s):
+    cfg, o, s, pb = cfg2s
+    assert pb.objects.as_list() == o.objects(1)
+    ac_o, ac_g = o.coarse_matrix(), s.coarse_matrix()
+    assert ac_o.shape == ac_g.shape
+    assert np.abs(ac_o - ac_g).max() <= 1e-8 * np.abs(ac_o).max()
+
+
+def test_apply_matches_oracle_and_is_symmetric(cfg2s):
+    cfg, o, s, pb = cfg2s
+    rng = np.random.default_rng(5)
+    r1, r2 = rng.uniform(-1, 1, o.n_dof), rng.uniform(-1, 1, o.n_dof)
+    z_o, z_g = o.apply(r1), s.apply(r1)
+    assert np.linalg.norm(z_o - z_g) <= 1e-8 * np.linalg.norm(z_o)
+    a, b = s.apply(r1) @ r2, r1 @ s.apply(r2)
+    assert abs(a - b) <= 1e-10 * abs(a)
+
+
+# Exact tier: identical iteration counts, residual histories within 1e-8 |b|
+# and solutions within 1e-8 (BASELINE.json north_star).
+@pytest.mark.parametrize("name,kw", [
+    ("cfg1", {}),
+    ("cfg2", dict(weighting="stiffness", objects="ce")),
+    ("cfg2", dict(weighting="stiffness", objects="cef")),
+    ("cfg2", dict(weighting="stiffness", objects="cef", variant="v1")),
+    ("cfg2", dict(weighting="stiffness", objects="cef", variant="v2")),
+    ("cfg3", dict(variant="v1")),
+    ("cfg3", dict(variant="v2")),
+])
+def test_pcg_parity(name, kw):
+    cfg, o, s, pb = _pair(name, **kw)
+    x_o, rep_o = o.pcg()
+    x_g, rep_g = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
+    assert rep_g["converged"] and rep_o["converged"]
+    assert rep_g["iterations"] == rep_o["iterations"]
+    ro, rg = rep_o["residuals"], rep_g["residuals"]
+    assert np.abs(ro - rg).max() <= 1e-8 * ro[0]
+    assert np.linalg.norm(x_o - x_g) <= 1e-8 * np.linalg.norm(x_o)
+    assert rep_g["lmin"] >= 1 - 1e-6
+
+
+# Conditioning-limited tier: the preconditioners the
+# paper shows to be non-robust (topological weighting on small cuts; standard
+# objects on cfg3, whose eta ~ 2e-8 cells give Abar diagonals ~3e-21) make the
+# late PCG residuals sensitive to 1-ulp perturbations even inside the CPU
+# restatement. Asserted: convergence, iterations within one, solutions within
+# 1e-5, early history within `early` of |b|.
+@pytest.mark.parametrize("name,kw,early", [
+    ("cfg2", dict(weighting="topological", objects="ce"), 1e-6),
+    ("cfg2", dict(weighting="topological", objects="cef"), 1e-6),
+    ("cfg3", {}, 1e-6),
+])
+def test_pcg_parity_conditioning_limited(name, kw, early):
+    cfg, o, s, pb = _pair(name, **kw)
+    x_o, rep_o = o.pcg()
+    x_g, rep_g = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
+    assert rep_g["converged"] and rep_o["converged"]
+    assert abs(rep_g["iterations"] - rep_o["iterations"]) <= 1
+    ro, rg = rep_o["residuals"], rep_g["residuals"]
+    assert np.abs(ro[:10] - rg[:10]).max() <= early * ro[0]
+    assert np.linalg.norm(x_o - x_g) <= 1e-5 * np.linalg.norm(x_o)
+
+
+def test_pcg_deterministic(cfg2s):
+    cfg, o, s, pb = cfg2s
+    x1, r1 = s.pcg(rtol=cfg.rtol)
+    x2, r2 = s.pcg(rtol=cfg.rtol)
+    assert np.array_equal(x1, x2) and np.array_equal(r1["residuals"], r2["residuals"])
+
+
+def test_one_subdomain_exact():
+    cfg = configs.get("cfg1").with_(block=20)
+    s = cb.GpuSolver(0)
+    pb = cb.prepare(s, cfg)
+    s.setup_bddc(pb.objects, cfg.weighting)
+    x, rep = s.pcg(rtol=cfg.rtol)
+    assert rep["iterations"] == 1
