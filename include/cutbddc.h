@@ -159,8 +159,14 @@ cutbddc_status cutbddc_gpu_local_system(cutbddc_gpu* h, double* stencil, uint8_t
                                         double* diag_add, int32_t* slot_dof);
 cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x);
 /* Statistics: [0]=n_dof [1]=n_sd [2]=n_coarse [3]=template slots [4]=factor doubles
- * per subdomain (one factor) [5]=n_supernodes [6]=levels [7]=max m_w [8]=n_interface. */
+ * per subdomain (both factors) [5]=supernodes (Neumann template) [6]=levels
+ * [7]=max m_w [8]=n_interface [9]=kernel launches so far (process-wide)
+ * [10]/[11]=panel doubles per subdomain of the interior / Neumann factor. */
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
+/* Measurement hook: average device time of the triangular-solve sweeps of
+ * one BDDC apply (interior, Neumann, interior) over `reps` repetitions, and
+ * their algorithmic bytes (panel lower parts + front vectors). */
+cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds, double* bytes);
 
 /* Host-side partition and interface objects (the caller side of the
  * boundary; reference ops build_partition SPEC.md:295-303, classify_objects

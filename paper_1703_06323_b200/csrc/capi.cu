@@ -38,6 +38,7 @@ void need(cutbddc_gpu* h) {
 }  // namespace
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+std::atomic<long long> g_kernel_launches{0};
 
 }  // namespace cutbddc_b200
 
@@ -303,6 +304,38 @@ cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x) {
   });
 }
 
+// Algorithmic bytes of one forward+backward sweep over every subdomain with a
+// template: the lower part of each panel once per sweep plus the front's
+// vector rows read and written.
+static double sweep_bytes(const Template& t, int nsd) {
+  double b = 0;
+  for (const auto& s : t.sn) {
+    const double r = s.nrows, c = s.ncols;
+    b += 2.0 * 8.0 * (r * c - c * (c - 1) / 2.0) + 2.0 * 2.0 * 8.0 * r;
+  }
+  return b * nsd;
+}
+
+cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds, double* bytes) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
+    if (reps < 1) reps = 1;
+    // warm
+    solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, nullptr);
+    solve_device(h, h->tK, h->GK, h->sv1.p, 1, h->upd.p, nullptr);
+    Timer tm(h->stream);
+    for (int r = 0; r < reps; ++r) {
+      solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, nullptr);
+      solve_device(h, h->tK, h->GK, h->sv1.p, 1, h->upd.p, nullptr);
+      solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, nullptr);
+    }
+    *seconds = tm.stop() / reps;
+    *bytes = 2.0 * sweep_bytes(h->tI.tpl, h->nsd) + sweep_bytes(h->tK.tpl, h->nsd);
+  });
+}
+
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {
   return guard([&] {
     need(h);
@@ -315,6 +348,9 @@ cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {
     st[6] = (int64_t)h->tK.tpl.levels.size();
     st[7] = h->m_max;
     st[8] = h->n_if;
+    st[9] = g_kernel_launches.load();
+    st[10] = h->tI.tpl.panel_total;
+    st[11] = h->tK.tpl.panel_total;
   });
 }
 

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -19,7 +20,13 @@ namespace cutbddc_b200 {
                                                           " at " __FILE__ ":" + std::to_string(__LINE__)); \
   } while (0)
 
-#define CB_LAUNCH() CB_CUDA(cudaGetLastError())
+// Count of this library's kernel launches (reported by cutbddc_gpu_stats).
+extern std::atomic<long long> g_kernel_launches;
+#define CB_LAUNCH()                                              \
+  do {                                                           \
+    ::cutbddc_b200::g_kernel_launches.fetch_add(1);              \
+    CB_CUDA(cudaGetLastError());                                 \
+  } while (0)
 
 // Owning device buffer.
 template <typename T>

@@ -118,5 +118,6 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<double> px, pr, pz, pp, pq, pb, hist, lal, lbe;
   cudaGraphExec_t graph_exec = nullptr;
   int graph_max_iter = -1;
+  long long graph_nodes = 0;                      // kernel nodes per PCG-iteration graph
   double t_pcg = 0;
 };

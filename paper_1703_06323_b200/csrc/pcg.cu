@@ -259,11 +259,13 @@ void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, 
   CB_CUDA(cudaEventCreate(&e1));
   CB_CUDA(cudaEventRecord(e0, s));
   k_copy<<<kRedBlocks, kRedThreads, 0, s>>>(nd, b_dev, h->pb.p);
+  CB_LAUNCH();
   k_copy<<<kRedBlocks, kRedThreads, 0, s>>>(nd, b_dev, h->pr.p);
   CB_LAUNCH();
   h->px.zero(s);
   h->iscal.zero(s);
   k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pb.p, h->pb.p, h->partials.p, nullptr);
+  CB_LAUNCH();
   std::vector<double> part(kRedBlocks);
   CB_CUDA(cudaMemcpyAsync(part.data(), h->partials.p, sizeof(double) * kRedBlocks, cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
@@ -284,7 +286,9 @@ void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, 
     CB_CUDA(cudaMemcpyAsync(h->iscal.p, host_is, sizeof(host_is), cudaMemcpyHostToDevice, s));
     apply_bddc_device(h, h->pr.p, h->pz.p, nullptr);
     k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pr.p, h->pz.p, h->partials.p, nullptr);
+    CB_LAUNCH();
     k_init_rz<<<1, kRedThreads, 0, s>>>(h->partials.p, h->scal.p, h->iscal.p);
+    CB_LAUNCH();
     k_copy<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pz.p, h->pp.p);
     CB_LAUNCH();
     if (h->graph_exec && h->graph_max_iter != max_iter) {
@@ -294,20 +298,28 @@ void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, 
     if (!h->graph_exec) {
       h->graph_max_iter = max_iter;
       cudaGraph_t g;
+      const long long c0 = g_kernel_launches.load();
       CB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       enqueue_iteration(h);
       CB_CUDA(cudaStreamEndCapture(s, &g));
       CB_CUDA(cudaGraphInstantiate(&h->graph_exec, g, 0));
+      size_t nodes = 0;
+      CB_CUDA(cudaGraphGetNodes(g, nullptr, &nodes));
+      h->graph_nodes = (long long)nodes;
+      g_kernel_launches.store(c0);  // captured, not executed
       CB_CUDA(cudaGraphDestroy(g));
     }
     int is_host[I_COUNT] = {0};
     int launched = 0, batch = 4;
     while (true) {
-      for (int q = 0; q < batch && launched < max_iter; ++q, ++launched) CB_CUDA(cudaGraphLaunch(h->graph_exec, s));
+      for (int q = 0; q < batch && launched < max_iter; ++q, ++launched) {
+        CB_CUDA(cudaGraphLaunch(h->graph_exec, s));
+        g_kernel_launches.fetch_add(h->graph_nodes);
+      }
       CB_CUDA(cudaMemcpyAsync(is_host, h->iscal.p, sizeof(is_host), cudaMemcpyDeviceToHost, s));
       CB_CUDA(cudaStreamSynchronize(s));
       if (is_host[I_DONE] || launched >= max_iter) break;
-      batch = std::min(32, batch * 2);
+      batch = std::min(8, batch * 2);
     }
     conv = is_host[I_CONV];
     iters = is_host[I_ITERS];

@@ -73,7 +73,7 @@ EXPORTS = [
     "cutbddc_last_error", "cutbddc_gpu_create", "cutbddc_gpu_destroy", "cutbddc_gpu_classify", "cutbddc_gpu_assemble",
     "cutbddc_gpu_local_diagonals", "cutbddc_gpu_setup_bddc", "cutbddc_gpu_pcg", "cutbddc_gpu_spmv",
     "cutbddc_gpu_apply_bddc", "cutbddc_gpu_rhs", "cutbddc_gpu_coarse_matrix", "cutbddc_gpu_cells", "cutbddc_gpu_stats",
-    "cutbddc_gpu_cut_elements", "cutbddc_gpu_local_system", "cutbddc_gpu_local_solve",
+    "cutbddc_gpu_cut_elements", "cutbddc_gpu_local_system", "cutbddc_gpu_local_solve", "cutbddc_gpu_time_solves",
     "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free",
 ]
 
@@ -313,10 +313,18 @@ class GpuSolver:
         _check(lib().cutbddc_gpu_local_solve(self.h, which, _p(x, C.c_double)))
         return x
 
+    def roofline(self, reps: int = 5):
+        """Live timing of the dominant kernel family (triangular-solve sweeps
+        of one BDDC apply) and its algorithmic bytes."""
+        sec, byt = C.c_double(), C.c_double()
+        _check(lib().cutbddc_gpu_time_solves(self.h, reps, C.byref(sec), C.byref(byt)))
+        return dict(kernel="k_fwd_level+k_bwd_level (3 solves of one BDDC apply)", seconds=sec.value, bytes=byt.value)
+
     def stats(self):
         st = np.zeros(16, np.int64)
         _check(lib().cutbddc_gpu_stats(self.h, _p(st, C.c_int64)))
-        keys = ["n_dof", "n_sd", "n_coarse", "slots", "panel_per_factor", "n_supernodes", "levels", "m_max", "n_if"]
+        keys = ["n_dof", "n_sd", "n_coarse", "slots", "panel_per_subdomain", "n_supernodes", "levels", "m_max", "n_if",
+                "launches", "panel_interior", "panel_neumann"]
         return {k: int(st[i]) for i, k in enumerate(keys)}
 
 
