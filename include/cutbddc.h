@@ -158,10 +158,11 @@ cutbddc_status cutbddc_gpu_cut_elements(cutbddc_gpu* h, int64_t* cells, double* 
 cutbddc_status cutbddc_gpu_local_system(cutbddc_gpu* h, double* stencil, uint8_t* mask_interior, uint8_t* mask_present,
                                         double* diag_add, int32_t* slot_dof);
 cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x);
-/* Statistics: [0]=n_dof [1]=n_sd [2]=n_coarse [3]=template slots [4]=factor doubles
- * per subdomain (both factors) [5]=supernodes (Neumann template) [6]=levels
- * [7]=max m_w [8]=n_interface [9]=kernel launches so far (process-wide)
- * [10]/[11]=panel doubles per subdomain of the interior / Neumann factor. */
+/* Statistics (16 slots): [0]=n_dof [1]=n_sd [2]=n_coarse [3]=template slots
+ * [4]=factor panel doubles (both factorisations, all subdomains)
+ * [5]=supernodes (Neumann template) [6]=levels [7]=max m_w [8]=n_interface
+ * [9]=kernel launches so far (process-wide) [10]/[11]=panel doubles of the
+ * interior / Neumann factorisation [12]=partial-Cholesky flops of both. */
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
 /* Measurement hook: average device time of the triangular-solve sweeps of
  * one BDDC apply (interior, Neumann, interior) over `reps` repetitions, and

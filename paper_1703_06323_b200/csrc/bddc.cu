@@ -17,6 +17,7 @@
 
 #include "bddc.cuh"
 #include "factor.cuh"
+#include "dense_chol.cuh"
 #include "subst.cuh"
 
 namespace cutbddc_b200 {
@@ -242,39 +243,12 @@ __global__ void k_coarse_assemble(int nc, const int64_t* __restrict__ cg_ptr, co
   }
 }
 
-// Single-CTA dense Cholesky of the coarse matrix (lower, row-major in A),
-// emitted as a column-major panel Lcm for the substitution solves.
-__global__ void __launch_bounds__(1024) k_coarse_chol(int n, double* __restrict__ A, double* __restrict__ Lcm,
-                                                      unsigned long long* fail) {
-  __shared__ double s_l;
-  for (int j = 0; j < n; ++j) {
-    if (threadIdx.x == 0) {
-      double d = A[(int64_t)j * n + j];
-      if (!(d > 0.0)) {
-        atomicMin(fail, (unsigned long long)j);
-        d = 1.0;
-      }
-      s_l = sqrt(d);
-      A[(int64_t)j * n + j] = s_l;
-    }
-    __syncthreads();
-    const double inv = 1.0 / s_l;
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[(int64_t)i * n + j] *= inv;
-    __syncthreads();
-    // trailing lower update, rows i >= k > j
-    const int64_t rem = n - j - 1;
-    for (int64_t q = threadIdx.x; q < rem * rem; q += blockDim.x) {
-      const int i = j + 1 + (int)(q / rem), k = j + 1 + (int)(q % rem);
-      if (k > i) continue;
-      A[(int64_t)i * n + k] -= A[(int64_t)i * n + j] * A[(int64_t)k * n + j];
-    }
-    __syncthreads();
-  }
-  // column-major copy of L for the substitution solves
-  for (int64_t q = threadIdx.x; q < (int64_t)n * n; q += blockDim.x) {
-    const int i = (int)(q % n), j = (int)(q / n);
-    Lcm[q] = i >= j ? A[(int64_t)i * n + j] : 0.0;
-  }
+// Single-CTA blocked Cholesky of the coarse matrix. A is symmetric (both
+// triangles stored), so the row-major buffer is read as column-major; the
+// result is the column-major lower panel used by the substitution solves.
+__global__ void __launch_bounds__(256) k_coarse_chol(int n, double* __restrict__ A, unsigned long long* fail) {
+  __shared__ CholSmem sm;
+  front_partial_cholesky(A, n, n, sm, [&](int j) { atomicMin(fail, (unsigned long long)j); });
 }
 
 // ------------------------------------------------------------------ apply
@@ -556,11 +530,11 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);
   if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
   FactorInput fi{h->As.p, h->mask_int.p, nullptr, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  factor_device(h, h->tI, fi, h->GI, "cholesky (interior problem)");
+  factor_device(h, h->tI, fi, h->fI, "cholesky (interior problem)");
   FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
                  h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
-  factor_device(h, h->tK, fk, h->GK, "saddle: singular augmented system; constraints do not control the operator kernel");
-  const int64_t upd_total = std::max(h->tI.tpl.upd_total, h->tK.tpl.upd_total);
+  factor_device(h, h->tK, fk, h->fK, "saddle: singular augmented system; constraints do not control the operator kernel");
+  const int64_t upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, h->fK.upd_total));
   // ---- coarse basis
   h->phi_c.alloc((size_t)std::max<int64_t>(1, h->m_total) * T);
   h->ac_loc.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
@@ -568,14 +542,16 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     DevBuf<double> Wall, upd;
     Wall.alloc((size_t)m_max * ns);
     Wall.zero(s);
-    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(m_max, (2ll << 30) / 8 / std::max<int64_t>(1, (int64_t)nsd * upd_total)));
-    upd.alloc((size_t)rb * nsd * upd_total);
+    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(m_max, (2ll << 30) / 8 / std::max(upd_total, ns)));
+    upd.alloc((size_t)rb * upd_total);
+    DevBuf<double> ys;
+    ys.alloc((size_t)rb * ns);
     for (int r0 = 0; r0 < m_max; r0 += rb) {
       const int nr = std::min(rb, m_max - r0);
       double* X = Wall.p + (int64_t)r0 * ns;
       k_fill_ct<<<dim3(nsd, nr), 64, 0, s>>>(nsd, T, r0, nr, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, X);
       CB_LAUNCH();
-      solve_device(h, h->tK, h->GK, X, nr, upd.p, nullptr);
+      solve_device(h, h->tK, h->fK, X, nr, upd.p, ys.p, nullptr);
     }
     DevBuf<double> S;
     S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
@@ -613,13 +589,12 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     k_coarse_assemble<<<nc, 128, 0, s>>>(nc, h->cg_ptr.p, h->cg_idx.p, h->row_sd.p, h->m_off.p, h->ac_off.p,
                                          h->coarse_id.p, h->ac_loc.p, h->acoarse.p);
     CB_LAUNCH();
-    DevBuf<double> L;
-    L.alloc((size_t)nc * nc);
-    CB_CUDA(cudaMemcpyAsync(L.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
+    // acoarse_inv holds the column-major Cholesky panel of A_c
+    CB_CUDA(cudaMemcpyAsync(h->acoarse_inv.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
     DevBuf<unsigned long long> fail;
     fail.alloc(1);
     CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
-    k_coarse_chol<<<1, 1024, 0, s>>>(nc, L.p, h->acoarse_inv.p, fail.p);
+    k_coarse_chol<<<1, 256, 0, s>>>(nc, h->acoarse_inv.p, fail.p);
     CB_LAUNCH();
     const size_t shm = sizeof(double) * (size_t)nc;
     if (shm > 200 * 1024) throw Failure(CUTBDDC_CONFIG, "coarse problem too large for the single-CTA coarse solve");
@@ -634,7 +609,8 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   // ---- work vectors
   h->sv0.alloc((size_t)ns);
   h->sv1.alloc((size_t)ns);
-  h->upd.alloc((size_t)nsd * upd_total);
+  h->upd.alloc((size_t)upd_total);
+  h->ysave.alloc((size_t)ns);
   h->gv0.alloc((size_t)h->n_dof);
   h->gv1.alloc((size_t)h->n_dof);
   h->gv2.alloc((size_t)h->n_dof);
@@ -653,7 +629,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   const int T = h->slots;
   k_gather_masked<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->mask_int.p, r, h->sv0.p, skip);
   CB_LAUNCH();
-  solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, skip);
+  solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, skip);
   k_z0<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv0.p, skip);
   CB_LAUNCH();
   k_r1<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->ncount.p, h->aval.p, h->acol.p, r, h->gv0.p, h->gv1.p, skip);
@@ -664,7 +640,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     k_phit<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->phi_c.p, h->sv1.p, h->gl.p, skip);
     CB_LAUNCH();
   }
-  solve_device(h, h->tK, h->GK, h->sv1.p, 1, h->upd.p, skip);
+  solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
   if (h->m_total > 0) {
     k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
                                                        h->sv1.p, h->cy.p, skip);
@@ -681,7 +657,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   k_interior_av<<<grid_for(ns, 256), 256, 0, s>>>(ns, nd, h->slot_dof.p, h->mask_int.p, h->aval.p, h->acol.p, h->gv2.p,
                                                   h->sv0.p, skip);
   CB_LAUNCH();
-  solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, skip);
+  solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, skip);
   k_final_z<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->gv0.p, h->gv2.p, h->sv0.p, z, skip);
   CB_LAUNCH();
 }

@@ -298,22 +298,10 @@ cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x) {
     const size_t ns = (size_t)h->nsd * h->slots;
     DevBuf<double> X;
     X.upload(x, ns, h->stream);
-    solve_device(h, which == 0 ? h->tI : h->tK, which == 0 ? h->GI : h->GK, X.p, 1, h->upd.p, nullptr);
+    solve_device(h, which == 0 ? h->tI : h->tK, which == 0 ? h->fI : h->fK, X.p, 1, h->upd.p, h->ysave.p, nullptr);
     X.download(x, ns, h->stream);
     CB_CUDA(cudaStreamSynchronize(h->stream));
   });
-}
-
-// Algorithmic bytes of one forward+backward sweep over every subdomain with a
-// template: the lower part of each panel once per sweep plus the front's
-// vector rows read and written.
-static double sweep_bytes(const Template& t, int nsd) {
-  double b = 0;
-  for (const auto& s : t.sn) {
-    const double r = s.nrows, c = s.ncols;
-    b += 2.0 * 8.0 * (r * c - c * (c - 1) / 2.0) + 2.0 * 2.0 * 8.0 * r;
-  }
-  return b * nsd;
 }
 
 cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds, double* bytes) {
@@ -323,16 +311,16 @@ cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds
     if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
     if (reps < 1) reps = 1;
     // warm
-    solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, nullptr);
-    solve_device(h, h->tK, h->GK, h->sv1.p, 1, h->upd.p, nullptr);
+    solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
+    solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
     Timer tm(h->stream);
     for (int r = 0; r < reps; ++r) {
-      solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, nullptr);
-      solve_device(h, h->tK, h->GK, h->sv1.p, 1, h->upd.p, nullptr);
-      solve_device(h, h->tI, h->GI, h->sv0.p, 1, h->upd.p, nullptr);
+      solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
+      solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
+      solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
     }
     *seconds = tm.stop() / reps;
-    *bytes = 2.0 * sweep_bytes(h->tI.tpl, h->nsd) + sweep_bytes(h->tK.tpl, h->nsd);
+    *bytes = 2.0 * sweep_bytes(h->fI) + sweep_bytes(h->fK);
   });
 }
 
@@ -343,14 +331,15 @@ cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {
     st[1] = h->nsd;
     st[2] = h->n_coarse;
     st[3] = h->slots;
-    st[4] = h->tI.tpl.panel_total + h->tK.tpl.panel_total;
+    st[4] = h->fI.panel_total + h->fK.panel_total;
     st[5] = (int64_t)h->tK.tpl.sn.size();
     st[6] = (int64_t)h->tK.tpl.levels.size();
     st[7] = h->m_max;
     st[8] = h->n_if;
     st[9] = g_kernel_launches.load();
-    st[10] = h->tI.tpl.panel_total;
-    st[11] = h->tK.tpl.panel_total;
+    st[10] = h->fI.panel_total;
+    st[11] = h->fK.panel_total;
+    st[12] = (int64_t)(h->fI.flops + h->fK.flops);
   });
 }
 

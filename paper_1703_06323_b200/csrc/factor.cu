@@ -3,64 +3,114 @@
 //
 // Replaces SparseCholesky (linalg.cpp:34-62) for the interior problems A_II
 // and the augmented Neumann matrices K = A + rho C^T C used by the
-// constrained solves (linalg.cpp:64-106 / SPEC.md:379-396). One launch per
-// elimination-tree level covers (every supernode of the level) x (every
-// subdomain): all subdomains share the template, so front shapes are uniform
-// across the batch. Fronts are dense (column-major) in an HBM workspace; the
-// parent gathers its children's update matrices (extend-add, fixed child
+// constrained solves (linalg.cpp:64-106 / SPEC.md:379-396).
+//
+// All subdomains share one elimination tree (the (B+1)^3 lattice template,
+// nd_template.cpp); each front is compacted per subdomain to the slots the
+// matrix actually has (interior dofs for A_II, local dofs for K), so a cut
+// subdomain pays only for its own dofs. One launch per tree level covers
+// (every supernode of the level) x (every subdomain); a CTA owns one
+// compact front. Fronts are dense column-major in an HBM workspace; the
+// parent gathers its children's update matrices (extend-add in fixed child
 // order: deterministic, no atomics).
 //
-// Factor storage per supernode s (rows r, pivots c): the Cholesky panel
-// [L11; L21] (r x c, column-major, lower part only). Solves use blocked
-// substitution on it (32-column diagonal blocks solved by one warp from
-// registers, the rest of the panel applied as coalesced GEMV updates), which
-// keeps the backward stability of the CPU restatement's triangular solves
-// (explicit L11^{-1} panels lost ~1e-9 on ill-conditioned cut subdomains).
-// Non-positive pivots are reported with the offending (subdomain, slot), the
-// pivot rule of linalg.cpp:42-54.
+// Factor storage per (subdomain, supernode): the Cholesky panel [L11; L21]
+// (r' x c', column-major, lower part). Solves use blocked substitution
+// (subst.cuh). Non-positive pivots are reported with the offending
+// (subdomain, slot) — the pivot rule of linalg.cpp:42-54.
 #include <algorithm>
+#include <vector>
 
+#include "dense_chol.cuh"
 #include "factor.cuh"
 #include "subst.cuh"
 
 namespace cutbddc_b200 {
 namespace {
 
-constexpr int kFactorThreads = 256;
+constexpr int kThreads = 256;
 
-__device__ inline double entry_value(const FactorInput& in, int64_t sdT, int u, int k) {
-  // value of A(v, u), v = u + offset(k), in the masked/augmented matrix
-  const int b1 = in.b1;
-  const int ux = u / (b1 * b1), uy = (u / b1) % b1, uz = u % b1;
-  const int v = ((ux + k / 9 - 1) * b1 + (uy + (k / 3) % 3 - 1)) * b1 + (uz + k % 3 - 1);
-  const bool mu = in.mask[sdT + u], mv = in.mask[sdT + v];
-  if (!(mu && mv)) return k == 13 ? 1.0 : 0.0;
-  double a = in.As[(sdT / in.T) * 27 * in.T + (int64_t)k * in.T + u];
-  if (k == 13 && in.diag_add) a += in.diag_add[sdT + u];
+// Compact row index of template row q of supernode s in subdomain sd.
+__device__ inline int pfx_at(const FactorDev& f, const TplDev& t, int sd, const Supernode& s, int q) {
+  return f.pfx[(int64_t)sd * t.rows_total + s.rows_off + q];
+}
+
+// ---------------------------------------------------------------- symbolic
+// CTA per (supernode, subdomain): prefix-count the masked template rows.
+__global__ void __launch_bounds__(kThreads) k_symbolic(TplDev t, int nsd, const uint8_t* __restrict__ mask,
+                                                       int32_t* __restrict__ pfx, int2* __restrict__ rc) {
+  const int sid = blockIdx.x, sd = blockIdx.y;
+  const Supernode s = t.sn[sid];
+  const int r = s.nrows;
+  const int per = (r + kThreads - 1) / kThreads;
+  const int q0 = threadIdx.x * per, q1 = min(r, q0 + per);
+  int cnt = 0;
+  for (int q = q0; q < q1; ++q) cnt += mask[(int64_t)sd * t.T + t.rows[s.rows_off + q]] != 0;
+  __shared__ int sc[kThreads + 1];
+  sc[threadIdx.x] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < kThreads; ++i) {
+      const int v = sc[i];
+      sc[i] = acc;
+      acc += v;
+    }
+    sc[kThreads] = acc;
+  }
+  __syncthreads();
+  int run = sc[threadIdx.x];
+  int32_t* out = pfx + (int64_t)sd * t.rows_total + s.rows_off;
+  int ccount = 0;
+  for (int q = q0; q < q1; ++q) {
+    const bool p = mask[(int64_t)sd * t.T + t.rows[s.rows_off + q]] != 0;
+    out[q] = p ? run : -1;
+    run += p;
+  }
+  // compact cols = present rows among the first ncols template rows
+  __shared__ int ncols_present;
+  if (threadIdx.x == 0) ncols_present = 0;
+  __syncthreads();
+  for (int q = threadIdx.x; q < s.ncols; q += blockDim.x) ccount += mask[(int64_t)sd * t.T + t.rows[s.rows_off + q]] != 0;
+  atomicAdd(&ncols_present, ccount);
+  __syncthreads();
+  if (threadIdx.x == 0) rc[(int64_t)sd * t.nsn + sid] = make_int2(sc[kThreads], ncols_present);
+}
+
+// ---------------------------------------------------------------- numeric
+__device__ inline double stencil_value(const FactorInput& in, int sd, int u, int k) {
+  double a = in.As[(int64_t)sd * 27 * in.T + (int64_t)k * in.T + u];
+  if (k == 13 && in.diag_add) a += in.diag_add[(int64_t)sd * in.T + u];
   return a;
 }
 
-__global__ void __launch_bounds__(kFactorThreads) k_factor_level(TplDev t, const int32_t* __restrict__ level_sn,
-                                                                 FactorInput in, int sd0, double* __restrict__ front,
-                                                                 double* __restrict__ G, unsigned long long* fail) {
+__global__ void __launch_bounds__(kThreads) k_factor_level(TplDev t, FactorDev f, const int32_t* __restrict__ level_sn,
+                                                           FactorInput in, int sd0, const int64_t* __restrict__ front_off,
+                                                           int64_t front_base0, const int64_t* __restrict__ front_base,
+                                                           double* __restrict__ front, double* __restrict__ panel,
+                                                           unsigned long long* fail) {
   const int sid = level_sn[blockIdx.x];
-  const Supernode sn = t.sn[sid];
-  const int sdl = blockIdx.y;          // within chunk
-  const int sd = sd0 + sdl;
-  const int64_t sdT = (int64_t)sd * t.T;
-  const int r = sn.nrows, c = sn.ncols;
-  double* F = front + (int64_t)sdl * t.front_total + sn.front_off;
+  const Supernode s = t.sn[sid];
+  const int sd = sd0 + blockIdx.y;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  if (r == 0) return;
   const int tid = threadIdx.x;
+  double* F = front + (front_base[sd] - front_base0) + front_off[(int64_t)sd * t.nsn + sid];
   for (int64_t q = tid; q < (int64_t)r * r; q += blockDim.x) F[q] = 0.0;
   __syncthreads();
-  for (int q = tid; q < sn.amap_len; q += blockDim.x) {
-    const AmapEntry e = t.amap[sn.amap_off + q];
-    F[e.pos] = entry_value(in, sdT, e.slot, e.k);
+  // original entries: template (row, col) positions -> compact
+  for (int q = tid; q < s.amap_len; q += blockDim.x) {
+    const AmapEntry e = t.amap[s.amap_off + q];
+    const int qr = e.pos % s.nrows, qc = e.pos / s.nrows;
+    const int pr = pfx_at(f, t, sd, s, qr), pc = pfx_at(f, t, sd, s, qc);
+    if (pr < 0 || pc < 0) continue;
+    F[pr + (int64_t)pc * r] = stencil_value(in, sd, e.slot, e.k);
   }
   __syncthreads();
   if (sid == t.root && in.c_ptr) {
-    // rho c c^T of every edge/face constraint row; objects are disjoint, so
-    // every (p, q) pair of a row hits a distinct front entry.
+    // rho c c^T of every edge/face constraint row (objects are disjoint:
+    // every (p, q) pair of a row hits a distinct entry)
     const double rho = in.rho[sd];
     for (int64_t row = in.m_off[sd]; row < in.m_off[sd + 1]; ++row) {
       if (in.corner[row]) continue;
@@ -68,105 +118,367 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor_level(TplDev t, const
       const int len = (int)(in.c_ptr[row + 1] - p0);
       for (int q = tid; q < len * len; q += blockDim.x) {
         const int a = q / len, b = q % len;
-        const int pa = t.root_pos[in.c_slot[p0 + a]], pb = t.root_pos[in.c_slot[p0 + b]];
-        if (pa < pb) continue;
+        const int pa = pfx_at(f, t, sd, s, t.root_pos[in.c_slot[p0 + a]]);
+        const int pb = pfx_at(f, t, sd, s, t.root_pos[in.c_slot[p0 + b]]);
+        if (pa < pb || pa < 0 || pb < 0) continue;
         F[pa + (int64_t)pb * r] += rho * in.c_val[p0 + a] * in.c_val[p0 + b];
       }
     }
     __syncthreads();
   }
-  for (int ch = 0; ch < sn.nchild; ++ch) {
-    const Supernode cs = t.sn[sn.child[ch]];
-    const int rc = cs.nrows, cc = cs.ncols, nu = rc - cc;
-    const double* U = front + (int64_t)sdl * t.front_total + cs.front_off;
-    const int32_t* em = t.emap + cs.emap_off;
+  // extend-add of the children's update matrices (the child-row map reuses
+  // the shared memory of the Cholesky phase)
+  __shared__ __align__(16) unsigned char smraw[sizeof(CholSmem)];
+  static_assert(sizeof(CholSmem) >= 2048 * sizeof(int), "cmap does not fit");
+  int* cmap = reinterpret_cast<int*>(smraw);
+  for (int ch = 0; ch < s.nchild; ++ch) {
+    const int cid = s.child[ch];
+    const Supernode cs = t.sn[cid];
+    const int2 crc = f.rc[(int64_t)sd * t.nsn + cid];
+    const int rcc = crc.x, ccc = crc.y, nu = rcc - ccc;
+    if (nu <= 0) continue;
+    // compact child rest row -> compact parent row
+    for (int a = tid; a < cs.nrows - cs.ncols; a += blockDim.x) {
+      const int ia = pfx_at(f, t, sd, cs, cs.ncols + a);
+      if (ia >= 0) cmap[ia - ccc] = pfx_at(f, t, sd, s, t.emap[cs.emap_off + a]);
+    }
+    __syncthreads();
+    const double* U = front + (front_base[sd] - front_base0) + front_off[(int64_t)sd * t.nsn + cid];
     for (int64_t q = tid; q < (int64_t)nu * nu; q += blockDim.x) {
       const int a = (int)(q % nu), b = (int)(q / nu);
       if (a < b) continue;
-      const int pa = em[a], pb = em[b];
+      const int pa = cmap[a], pb = cmap[b];
       const int row = max(pa, pb), col = min(pa, pb);
-      F[row + (int64_t)col * r] += U[(cc + a) + (int64_t)(cc + b) * rc];
+      F[row + (int64_t)col * r] += U[(ccc + a) + (int64_t)(ccc + b) * rcc];
     }
     __syncthreads();
   }
-  // right-looking partial Cholesky of the c pivot columns
-  __shared__ double s_ljj;
-  for (int j = 0; j < c; ++j) {
-    if (tid == 0) {
-      double d = F[j + (int64_t)j * r];
-      if (!(d > 0.0)) {
-        atomicMin(fail, (unsigned long long)(sdT + t.rows[sn.rows_off + j]));
-        d = 1.0;
+  // blocked right-looking partial Cholesky of the c pivot columns
+  CholSmem& sm = *reinterpret_cast<CholSmem*>(smraw);
+  front_partial_cholesky(F, r, c, sm, [&](int j) {
+    // report the template slot of compact column j
+    for (int q = 0; q < s.ncols; ++q)
+      if (pfx_at(f, t, sd, s, q) == j) {
+        atomicMin(fail, (unsigned long long)((int64_t)sd * t.T + t.rows[s.rows_off + q]));
+        break;
       }
-      s_ljj = sqrt(d);
-      F[j + (int64_t)j * r] = s_ljj;
-    }
-    __syncthreads();
-    const double inv = 1.0 / s_ljj;
-    for (int i = j + 1 + tid; i < r; i += blockDim.x) F[i + (int64_t)j * r] *= inv;
-    __syncthreads();
-    for (int k = j + 1; k < r; ++k) {
-      const double lkj = F[k + (int64_t)j * r];
-      if (lkj == 0.0) continue;
-      for (int i = k + tid; i < r; i += blockDim.x) F[i + (int64_t)k * r] -= F[i + (int64_t)j * r] * lkj;
-    }
-    __syncthreads();
-  }
-  // panel [L11; L21] (lower part; the strict upper triangle of L11 is never read)
-  double* P = G + (int64_t)sd * t.panel_total + sn.panel_off;
+  });
+  __syncthreads();
+  if (t.is_big[sid]) return;  // big fronts: G panel written by k_trinv / k_gemm_m
+  double* P = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
   for (int j = 0; j < c; ++j)
     for (int i = j + tid; i < r; i += blockDim.x) P[i + (int64_t)j * r] = F[i + (int64_t)j * r];
 }
 
-// forward elimination step: X holds b on entry (slot vectors), y on exit at
-// cols; the update v_rest - L21 y goes to the parent through `upd`.
-__global__ void __launch_bounds__(256) k_fwd_level(TplDev t, const int32_t* __restrict__ level_sn, int nsd,
-                                                   const double* __restrict__ G, double* __restrict__ X,
-                                                   double* __restrict__ upd, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  extern __shared__ double v[];
-  const Supernode sn = t.sn[level_sn[blockIdx.x]];
-  const int sd = blockIdx.y, rhs = blockIdx.z;
-  const int r = sn.nrows, c = sn.ncols;
-  double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
-  double* ub = upd + ((int64_t)rhs * nsd + sd) * t.upd_total;
-  const int32_t* rows = t.rows + sn.rows_off;
-  for (int i = threadIdx.x; i < r; i += blockDim.x) v[i] = i < c ? x[rows[i]] : 0.0;
-  __syncthreads();
-  for (int ch = 0; ch < sn.nchild; ++ch) {
-    const Supernode cs = t.sn[sn.child[ch]];
-    const int nu = cs.nrows - cs.ncols;
-    const int32_t* em = t.emap + cs.emap_off;
-    const double* cu = ub + cs.upd_off;
-    for (int a = threadIdx.x; a < nu; a += blockDim.x) v[em[a]] += cu[a];
+// Big fronts: X = L11^{-1} into the top c x c block of the G panel, one CTA
+// per (32-column right-hand-side block, front). Left-looking over 32-row
+// blocks: acc = E - sum_k L[ib,kb] X[kb,:] (32^3 tiles in shared memory),
+// then a 32x32 triangular solve with 32 right-hand sides.
+__global__ void __launch_bounds__(256) k_trinv(TplDev t, FactorDev f, const int2* __restrict__ items, int sd0,
+                                               const int64_t* __restrict__ front_off, int64_t front_base0,
+                                               const int64_t* __restrict__ front_base, const double* __restrict__ front,
+                                               double* __restrict__ panel) {
+  const int2 it = items[blockIdx.x];
+  const int sid = it.x, jb = it.y;
+  const int sd = sd0 + blockIdx.y;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  const int j0 = jb * 32;
+  if (j0 >= c) return;
+  const int nb = min(32, c - j0);
+  const double* L = front + (front_base[sd] - front_base0) + front_off[(int64_t)sd * t.nsn + sid];
+  double* X = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
+  __shared__ double lt[32][33], xt[32][33], ab[32][33];
+  const int tid = threadIdx.x, ti = tid & 31, tj = tid >> 5;  // 8 groups of 4 rhs columns
+  // zero the strictly upper part of this column block (rows < j0)
+  for (int q = tid; q < j0 * nb; q += blockDim.x) X[(q % j0) + (int64_t)(j0 + q / j0) * r] = 0.0;
+  for (int i0 = j0; i0 < c; i0 += 32) {
+    const int mb = min(32, c - i0);
+    double acc[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int j = tj + 8 * a;
+      acc[a] = (i0 + ti == j0 + j) ? 1.0 : 0.0;
+    }
+    for (int k0 = j0; k0 < i0; k0 += 32) {
+      for (int q = tid; q < 32 * 32; q += blockDim.x) {
+        const int i = q & 31, k = q >> 5;
+        lt[i][k] = (i < mb) ? L[(i0 + i) + (int64_t)(k0 + k) * r] : 0.0;
+        xt[i][k] = (k < nb) ? X[(k0 + i) + (int64_t)(j0 + k) * r] : 0.0;  // xt[row k0+i][rhs k]
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const double l = lt[ti][k];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) acc[a] -= l * xt[k][tj + 8 * a];
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) ab[ti][tj + 8 * a] = acc[a];
+    for (int q = tid; q < 32 * 32; q += blockDim.x) {
+      const int i = q & 31, k = q >> 5;
+      lt[i][k] = (i < mb && k < mb) ? L[(i0 + i) + (int64_t)(i0 + k) * r] : 0.0;
+    }
     __syncthreads();
-  }
-  panel_forward(G + (int64_t)sd * t.panel_total + sn.panel_off, r, c, v);
-  for (int i = threadIdx.x; i < r; i += blockDim.x) {
-    if (i < c)
-      x[rows[i]] = v[i];
-    else
-      ub[sn.upd_off + (i - c)] = v[i];
+    if (tid < nb) {
+      const int j = tid;
+      for (int i = 0; i < mb; ++i) {
+        double s = ab[i][j];
+        for (int k = 0; k < i; ++k) s -= lt[i][k] * ab[k][j];
+        ab[i][j] = s / lt[i][i];
+      }
+      for (int i = 0; i < mb; ++i) X[(i0 + i) + (int64_t)(j0 + j) * r] = ab[i][j];
+    }
+    __syncthreads();
   }
 }
 
-// backward substitution step: X holds y at cols of this level, final x at
-// ancestors (rest rows). x_c = L11^{-T} (y - L21^T x_rest).
-__global__ void __launch_bounds__(256) k_bwd_level(TplDev t, const int32_t* __restrict__ level_sn, int nsd,
-                                                   const double* __restrict__ G, double* __restrict__ X,
+// Big fronts: M = L21 X into rows c..r of the G panel (64x64 output tiles,
+// k loop from the tile's first column: X is lower triangular).
+__global__ void __launch_bounds__(256) k_gemm_m(TplDev t, FactorDev f, const int2* __restrict__ items, int sd0,
+                                                const int64_t* __restrict__ front_off, int64_t front_base0,
+                                                const int64_t* __restrict__ front_base, const double* __restrict__ front,
+                                                double* __restrict__ panel) {
+  const int2 it = items[blockIdx.x];
+  const int sid = it.x;
+  const int sd = sd0 + blockIdx.y;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y, m = r - c;
+  const int ncb = (c + 63) / 64;
+  if (ncb == 0) return;
+  const int tiI = it.y / ncb, tiJ = it.y % ncb;
+  const int i0 = c + tiI * 64, j0 = tiJ * 64;
+  if (tiI * 64 >= m || j0 >= c) return;
+  const double* L = front + (front_base[sd] - front_base0) + front_off[(int64_t)sd * t.nsn + sid];
+  double* G = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
+  __shared__ double la[32][64];  // [k][row]
+  __shared__ double xb[32][64];  // [k][col]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int k0 = j0; k0 < c; k0 += 32) {
+    for (int q = tid; q < 32 * 64; q += blockDim.x) {
+      const int ii = q & 63, k = q >> 6;
+      const int i = i0 + ii, kk = k0 + k, j = j0 + ii;
+      la[k][ii] = (i < r && kk < c) ? L[i + (int64_t)kk * r] : 0.0;
+      xb[k][ii] = (j < c && kk < c && kk >= j) ? G[kk + (int64_t)j * r] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+      double pa[4], pb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) pa[a] = la[k][tx + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) pb[b] = xb[k][ty + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] += pa[a] * pb[b];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = i0 + tx + 16 * a;
+    if (i >= r) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + ty + 16 * b;
+      if (j < c) G[i + (int64_t)j * r] = acc[a][b];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- solves
+// forward elimination: X holds b on entry (slot vectors), y on exit at the
+// front's columns; v_rest - L21 y goes to the parent through `upd`.
+__global__ void __launch_bounds__(256) k_fwd_level(TplDev t, FactorDev f, const int32_t* __restrict__ level_sn, int nsd,
+                                                   const double* __restrict__ panel, double* __restrict__ X,
+                                                   double* __restrict__ upd, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double v[];
+  const int sid = level_sn[blockIdx.x];
+  const Supernode s = t.sn[sid];
+  const int sd = blockIdx.y, rhs = blockIdx.z;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  if (r == 0) return;
+  double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
+  double* ub = upd + (int64_t)rhs * f.upd_total;
+  const int32_t* rows = t.rows + s.rows_off;
+  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
+    const int p = pfx_at(f, t, sd, s, q);
+    if (p >= 0) v[p] = q < s.ncols ? x[rows[q]] : 0.0;
+  }
+  __syncthreads();
+  for (int ch = 0; ch < s.nchild; ++ch) {
+    const int cid = s.child[ch];
+    const Supernode cs = t.sn[cid];
+    const int ccc = f.rc[(int64_t)sd * t.nsn + cid].y;
+    const double* cu = ub + f.upd_off[(int64_t)sd * t.nsn + cid];
+    for (int a = threadIdx.x; a < cs.nrows - cs.ncols; a += blockDim.x) {
+      const int ia = pfx_at(f, t, sd, cs, cs.ncols + a);
+      if (ia >= 0) v[pfx_at(f, t, sd, s, t.emap[cs.emap_off + a])] += cu[ia - ccc];
+    }
+    __syncthreads();
+  }
+  panel_forward(panel + f.panel_off[(int64_t)sd * t.nsn + sid], r, c, v);
+  double* uo = ub + f.upd_off[(int64_t)sd * t.nsn + sid];
+  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
+    const int p = pfx_at(f, t, sd, s, q);
+    if (p < 0) continue;
+    if (q < s.ncols)
+      x[rows[q]] = v[p];
+    else
+      uo[p - c] = v[p];
+  }
+}
+
+// backward substitution: X holds y at this level's columns and the final x
+// at ancestors; x_c = L11^{-T} (y - L21^T x_rest).
+__global__ void __launch_bounds__(256) k_bwd_level(TplDev t, FactorDev f, const int32_t* __restrict__ level_sn, int nsd,
+                                                   const double* __restrict__ panel, double* __restrict__ X,
                                                    const int* __restrict__ skip) {
   if (skip && *skip) return;
   extern __shared__ double w[];
   __shared__ double tile[32][33];
-  const Supernode sn = t.sn[level_sn[blockIdx.x]];
+  const int sid = level_sn[blockIdx.x];
+  const Supernode s = t.sn[sid];
   const int sd = blockIdx.y, rhs = blockIdx.z;
-  const int r = sn.nrows, c = sn.ncols;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  if (c == 0) return;
   double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
-  const int32_t* rows = t.rows + sn.rows_off;
-  for (int i = threadIdx.x; i < r; i += blockDim.x) w[i] = x[rows[i]];
+  const int32_t* rows = t.rows + s.rows_off;
+  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
+    const int p = pfx_at(f, t, sd, s, q);
+    if (p >= 0) w[p] = x[rows[q]];
+  }
   __syncthreads();
-  panel_backward(G + (int64_t)sd * t.panel_total + sn.panel_off, r, c, w, tile);
-  for (int j = threadIdx.x; j < c; j += blockDim.x) x[rows[j]] = w[j];
+  panel_backward(panel + f.panel_off[(int64_t)sd * t.nsn + sid], r, c, w, tile);
+  for (int q = threadIdx.x; q < s.ncols; q += blockDim.x) {
+    const int p = pfx_at(f, t, sd, s, q);
+    if (p >= 0) x[rows[q]] = w[p];
+  }
+}
+
+// Big fronts, forward: [y; t] = G v_c as a GEMV split into 128-row chunks
+// (one CTA each). Every chunk rebuilds the full front vector (gather +
+// children's updates) in shared memory; y goes to `ysave` (x keeps b at the
+// columns until the backward sweep, so concurrent chunks never race).
+constexpr int kBigRows = 128;
+constexpr int kBigCols = 32;
+
+__global__ void __launch_bounds__(256) k_fwd_big(TplDev t, FactorDev f, const int2* __restrict__ items, int nsd,
+                                                 const double* __restrict__ panel, const double* __restrict__ X,
+                                                 double* __restrict__ ysave, double* __restrict__ upd,
+                                                 const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double v[];
+  int* slot_of = reinterpret_cast<int*>(v + 2048);
+  const int2 it = items[blockIdx.x];
+  const int sid = it.x;
+  const Supernode s = t.sn[sid];
+  const int sd = blockIdx.y, rhs = blockIdx.z;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  const int i0 = it.y * kBigRows;
+  if (i0 >= r) return;
+  const int i1 = min(r, i0 + kBigRows);
+  const double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
+  double* ys = ysave + ((int64_t)rhs * nsd + sd) * t.T;
+  double* ub = upd + (int64_t)rhs * f.upd_total;
+  const int32_t* rows = t.rows + s.rows_off;
+  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
+    const int p = pfx_at(f, t, sd, s, q);
+    if (p >= 0) {
+      v[p] = q < s.ncols ? x[rows[q]] : 0.0;
+      slot_of[p] = rows[q];
+    }
+  }
+  __syncthreads();
+  for (int ch = 0; ch < s.nchild; ++ch) {
+    const int cid = s.child[ch];
+    const Supernode cs = t.sn[cid];
+    const int ccc = f.rc[(int64_t)sd * t.nsn + cid].y;
+    const double* cu = ub + f.upd_off[(int64_t)sd * t.nsn + cid];
+    for (int a = threadIdx.x; a < cs.nrows - cs.ncols; a += blockDim.x) {
+      const int ia = pfx_at(f, t, sd, cs, cs.ncols + a);
+      if (ia >= 0) v[pfx_at(f, t, sd, s, t.emap[cs.emap_off + a])] += cu[ia - ccc];
+    }
+    __syncthreads();
+  }
+  const double* G = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
+  double* uo = ub + f.upd_off[(int64_t)sd * t.nsn + sid];
+  // two threads per row (even / odd columns), combined through a shuffle
+  const int half = threadIdx.x & 1;
+  for (int base = i0; base < i1; base += blockDim.x >> 1) {
+    const int i = base + (threadIdx.x >> 1);
+    const bool act = i < i1;
+    double s0 = 0.0, s1 = 0.0;
+    if (act) {
+      const int jmax = i < c ? i + 1 : c;
+      int j = half;
+      for (; j + 2 < jmax; j += 4) {
+        s0 += G[i + (int64_t)j * r] * v[j];
+        s1 += G[i + (int64_t)(j + 2) * r] * v[j + 2];
+      }
+      for (; j < jmax; j += 2) s0 += G[i + (int64_t)j * r] * v[j];
+    }
+    double o = s0 + s1;
+    o += __shfl_xor_sync(0xffffffffu, o, 1);
+    if (act && half == 0) {
+      if (i < c)
+        ys[slot_of[i]] = o;
+      else
+        uo[i - c] = v[i] - o;
+    }
+  }
+}
+
+// Big fronts, backward: x_c = G^T [y; -x_rest], 32 columns per CTA, one warp
+// per column reducing over the rows.
+__global__ void __launch_bounds__(256) k_bwd_big(TplDev t, FactorDev f, const int2* __restrict__ items, int nsd,
+                                                 const double* __restrict__ panel, double* __restrict__ X,
+                                                 const double* __restrict__ ysave, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double w[];
+  int* slot_of = reinterpret_cast<int*>(w + 2048);
+  const int2 it = items[blockIdx.x];
+  const int sid = it.x;
+  const Supernode s = t.sn[sid];
+  const int sd = blockIdx.y, rhs = blockIdx.z;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  const int j0 = it.y * kBigCols;
+  if (j0 >= c) return;
+  const int j1 = min(c, j0 + kBigCols);
+  double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
+  const double* ys = ysave + ((int64_t)rhs * nsd + sd) * t.T;
+  const int32_t* rows = t.rows + s.rows_off;
+  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
+    const int p = pfx_at(f, t, sd, s, q);
+    if (p >= 0) {
+      w[p] = p < c ? ys[rows[q]] : -x[rows[q]];
+      slot_of[p] = rows[q];
+    }
+  }
+  __syncthreads();
+  const double* G = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = j0 + wid; j < j1; j += nw) {
+    const double* col = G + (int64_t)j * r;
+    double s0 = 0.0;
+    for (int i = j + lane; i < r; i += 32) s0 += col[i] * w[i];
+    s0 = warp_sum(s0);
+    if (lane == 0) x[slot_of[j]] = s0;
+  }
 }
 
 }  // namespace
@@ -178,83 +490,214 @@ TplDev tpl_dev(const TplSet& ts, int slots) {
   t.amap = ts.amap.p;
   t.emap = ts.emap.p;
   t.root_pos = ts.root_pos.p;
+  t.is_big = ts.big_flag.p;
   t.T = slots;
-  t.root = (int)ts.tpl.sn.size() - 1;
-  t.panel_total = ts.tpl.panel_total;
-  t.front_total = ts.tpl.front_total;
-  t.upd_total = ts.tpl.upd_total;
+  t.nsn = (int)ts.tpl.sn.size();
+  t.root = t.nsn - 1;
+  t.rows_total = (int64_t)ts.tpl.rows.size();
   return t;
+}
+
+FactorDev factor_dev(const FactorSet& f) {
+  return FactorDev{f.pfx.p, f.rc.p, f.panel_off.p, f.upd_off.p, f.upd_total};
 }
 
 void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
   cudaStream_t s = h->stream;
   ts.tpl = build_template(h->block, 27, shell_root);
+  if (ts.tpl.max_rows > 2048) throw Failure(CUTBDDC_CONFIG, "nd template: front larger than 2048 rows");
   ts.sn.upload(ts.tpl.sn, s);
   ts.rows.upload(ts.tpl.rows, s);
   ts.amap.upload(ts.tpl.amap, s);
   ts.emap.upload(ts.tpl.emap.empty() ? std::vector<int32_t>{0} : ts.tpl.emap, s);
   ts.root_pos.upload(ts.tpl.root_pos, s);
-  std::vector<int32_t> lv;
+  std::vector<int32_t> lv, small, big;
+  std::vector<int2> fwd, bwd, inv, gem;
   ts.level_first.clear();
   ts.level_count.clear();
+  ts.small_first.clear();
+  ts.small_count.clear();
+  ts.big_first.clear();
+  ts.big_count.clear();
+  ts.fwd_first.clear();
+  ts.fwd_count.clear();
+  ts.bwd_first.clear();
+  ts.bwd_count.clear();
+  ts.inv_first.clear();
+  ts.inv_count.clear();
+  ts.gemm_first.clear();
+  ts.gemm_count.clear();
+  ts.is_big.assign(ts.tpl.sn.size(), 0);
   for (auto& L : ts.tpl.levels) {
     ts.level_first.push_back((int)lv.size());
     ts.level_count.push_back((int)L.size());
     lv.insert(lv.end(), L.begin(), L.end());
+    ts.small_first.push_back((int)small.size());
+    ts.big_first.push_back((int)big.size());
+    ts.fwd_first.push_back((int)fwd.size());
+    ts.bwd_first.push_back((int)bwd.size());
+    ts.inv_first.push_back((int)inv.size());
+    ts.gemm_first.push_back((int)gem.size());
+    for (int sid : L) {
+      const Supernode& sn = ts.tpl.sn[(size_t)sid];
+      // big: explicit-inverse panel swept by many CTAs
+      const bool is_big = sn.ncols >= 96;
+      ts.is_big[(size_t)sid] = is_big;
+      if (!is_big) {
+        small.push_back(sid);
+        continue;
+      }
+      big.push_back(sid);
+      for (int ch = 0; ch < (sn.nrows + kBigRows - 1) / kBigRows; ++ch) fwd.push_back(make_int2(sid, ch));
+      for (int ch = 0; ch < (sn.ncols + kBigCols - 1) / kBigCols; ++ch) bwd.push_back(make_int2(sid, ch));
+      for (int ch = 0; ch < (sn.ncols + 31) / 32; ++ch) inv.push_back(make_int2(sid, ch));
+      const int tiles = ((sn.nrows - sn.ncols + 63) / 64) * ((sn.ncols + 63) / 64);
+      for (int ch = 0; ch < tiles; ++ch) gem.push_back(make_int2(sid, ch));
+    }
+    ts.small_count.push_back((int)small.size() - ts.small_first.back());
+    ts.big_count.push_back((int)big.size() - ts.big_first.back());
+    ts.fwd_count.push_back((int)fwd.size() - ts.fwd_first.back());
+    ts.bwd_count.push_back((int)bwd.size() - ts.bwd_first.back());
+    ts.inv_count.push_back((int)inv.size() - ts.inv_first.back());
+    ts.gemm_count.push_back((int)gem.size() - ts.gemm_first.back());
   }
+  auto nz32 = [](std::vector<int32_t> v) { return v.empty() ? std::vector<int32_t>{0} : v; };
+  auto nz2 = [](std::vector<int2> v) { return v.empty() ? std::vector<int2>{make_int2(0, 0)} : v; };
   ts.level_sn.upload(lv, s);
+  ts.small_sn.upload(nz32(small), s);
+  ts.big_sn.upload(nz32(big), s);
+  ts.fwd_items.upload(nz2(fwd), s);
+  ts.bwd_items.upload(nz2(bwd), s);
+  ts.inv_items.upload(nz2(inv), s);
+  ts.gemm_items.upload(nz2(gem), s);
+  ts.big_flag.upload(ts.is_big, s);
   ts.ready = true;
 }
 
-// Factor every subdomain's masked/augmented matrix into G (nsd * panel_total).
-void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, DevBuf<double>& G, const char* what) {
+double sweep_bytes(const FactorSet& f) { return f.bytes_per_sweep; }
+
+// Symbolic (compact structure) + numeric factorisation of every subdomain.
+void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, FactorSet& f, const char* what) {
   cudaStream_t s = h->stream;
   const TplDev t = tpl_dev(ts, h->slots);
-  G.alloc((size_t)h->nsd * ts.tpl.panel_total);
-  // subdomain chunks bounded by a front-workspace budget (~4 GiB)
-  const int64_t per = ts.tpl.front_total;
-  int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(h->nsd, (4ll << 30) / 8 / per));
-  DevBuf<double> front;
-  front.alloc((size_t)chunk * per);
+  const int nsd = h->nsd, nsn = t.nsn;
+  // symbolic: compact rows per (sd, supernode)
+  f.pfx.alloc((size_t)nsd * t.rows_total);
+  f.rc.alloc((size_t)nsd * nsn);
+  k_symbolic<<<dim3(nsn, nsd), kThreads, 0, s>>>(t, nsd, in.mask, f.pfx.p, f.rc.p);
+  CB_LAUNCH();
+  f.h_rc = f.rc.to_host(s);
+  std::vector<int64_t> poff((size_t)nsd * nsn), uoff((size_t)nsd * nsn), foff((size_t)nsd * nsn);
+  f.h_front_base.assign((size_t)nsd + 1, 0);
+  int64_t pt = 0, ut = 0;
+  double bytes = 0, flops = 0;
+  for (int sd = 0; sd < nsd; ++sd) {
+    int64_t fo = 0;
+    for (int q = 0; q < nsn; ++q) {
+      const int2 v = f.h_rc[(size_t)sd * nsn + q];
+      const double r = v.x, c = v.y;
+      poff[(size_t)sd * nsn + q] = pt;
+      pt += (int64_t)v.x * v.y;
+      uoff[(size_t)sd * nsn + q] = ut;
+      ut += v.x - v.y;
+      foff[(size_t)sd * nsn + q] = fo;
+      fo += (int64_t)v.x * v.x;
+      bytes += 2.0 * 8.0 * (r * c - c * (c - 1) / 2.0) + 2.0 * 2.0 * 8.0 * r;
+      flops += c * c * c / 3.0 + (r - c) * c * c + (r - c) * (r - c) * c;
+    }
+    f.h_front_base[(size_t)sd + 1] = f.h_front_base[(size_t)sd] + fo;
+  }
+  f.panel_total = pt;
+  f.upd_total = ut;
+  f.bytes_per_sweep = bytes;
+  f.flops = flops;
+  f.panel_off.upload(poff, s);
+  f.upd_off.upload(uoff, s);
+  f.front_off.upload(foff, s);
+  DevBuf<int64_t> fbase;
+  fbase.upload(f.h_front_base, s);
+  f.panel.alloc((size_t)std::max<int64_t>(1, pt));
+  const FactorDev fd = factor_dev(f);
+  // numeric, in subdomain chunks bounded by a front-workspace budget
+  const int64_t budget = (3ll << 30) / 8;
   DevBuf<unsigned long long> fail;
   fail.alloc(1);
   CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
+  DevBuf<double> front;
   const int nlev = (int)ts.level_first.size();
-  for (int sd0 = 0; sd0 < h->nsd; sd0 += chunk) {
-    const int nc = std::min(chunk, h->nsd - sd0);
+  int sd0 = 0;
+  while (sd0 < nsd) {
+    int sd1 = sd0 + 1;
+    while (sd1 < nsd && f.h_front_base[(size_t)sd1 + 1] - f.h_front_base[(size_t)sd0] <= budget) ++sd1;
+    const int64_t need = f.h_front_base[(size_t)sd1] - f.h_front_base[(size_t)sd0];
+    if ((int64_t)front.n < need) front.alloc((size_t)need);
     for (int L = nlev - 1; L >= 0; --L) {
-      dim3 grid(ts.level_count[(size_t)L], nc);
-      k_factor_level<<<grid, kFactorThreads, 0, s>>>(t, ts.level_sn.p + ts.level_first[(size_t)L], in, sd0, front.p,
-                                                     G.p, fail.p);
+      dim3 grid(ts.level_count[(size_t)L], sd1 - sd0);
+      k_factor_level<<<grid, kThreads, 0, s>>>(t, fd, ts.level_sn.p + ts.level_first[(size_t)L], in, sd0,
+                                               f.front_off.p, f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p,
+                                               fail.p);
       CB_LAUNCH();
+      if (ts.inv_count[(size_t)L] > 0) {
+        dim3 gi(ts.inv_count[(size_t)L], sd1 - sd0);
+        k_trinv<<<gi, 256, 0, s>>>(t, fd, ts.inv_items.p + ts.inv_first[(size_t)L], sd0, f.front_off.p,
+                                   f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p);
+        CB_LAUNCH();
+      }
+      if (ts.gemm_count[(size_t)L] > 0) {
+        dim3 gg(ts.gemm_count[(size_t)L], sd1 - sd0);
+        k_gemm_m<<<gg, 256, 0, s>>>(t, fd, ts.gemm_items.p + ts.gemm_first[(size_t)L], sd0, f.front_off.p,
+                                    f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p);
+        CB_LAUNCH();
+      }
     }
+    sd0 = sd1;
   }
-  unsigned long long f = 0;
-  CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long fl = 0;
+  CB_CUDA(cudaMemcpyAsync(&fl, fail.p, 8, cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
-  if (f != ~0ull) {
-    const int64_t sd = (int64_t)(f / (unsigned long long)h->slots), slot = (int64_t)(f % (unsigned long long)h->slots);
+  if (fl != ~0ull) {
+    const int64_t sd = (int64_t)(fl / (unsigned long long)h->slots), slot = (int64_t)(fl % (unsigned long long)h->slots);
     throw Failure(CUTBDDC_SINGULAR, std::string(what) + ": matrix is not positive definite (subdomain " +
                                         std::to_string(sd) + ", pivot slot " + std::to_string(slot) + ")");
   }
 }
 
-// In-place solve of nrhs x nsd slot vectors X ([rhs][sd][T]) with factor G.
-void solve_device(cutbddc_gpu* h, const TplSet& ts, const DevBuf<double>& G, double* X, int nrhs, double* upd,
-                  const int* skip) {
+// In-place solve of nrhs x nsd slot vectors X ([rhs][sd][T]); masked-out
+// slots are left untouched. upd must hold nrhs * f.upd_total doubles.
+void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, int nrhs, double* upd,
+                  double* ysave, const int* skip) {
   cudaStream_t s = h->stream;
   const TplDev t = tpl_dev(ts, h->slots);
+  const FactorDev fd = factor_dev(f);
   const int nlev = (int)ts.level_first.size();
   const size_t shm = sizeof(double) * (size_t)ts.tpl.max_rows;
+  const size_t shm_big = (sizeof(double) + sizeof(int)) * 2048;
   for (int L = nlev - 1; L >= 0; --L) {
-    dim3 grid(ts.level_count[(size_t)L], h->nsd, nrhs);
-    k_fwd_level<<<grid, 256, shm, s>>>(t, ts.level_sn.p + ts.level_first[(size_t)L], h->nsd, G.p, X, upd, skip);
-    CB_LAUNCH();
+    if (ts.small_count[(size_t)L] > 0) {
+      dim3 grid(ts.small_count[(size_t)L], h->nsd, nrhs);
+      k_fwd_level<<<grid, 256, shm, s>>>(t, fd, ts.small_sn.p + ts.small_first[(size_t)L], h->nsd, f.panel.p, X, upd,
+                                         skip);
+      CB_LAUNCH();
+    }
+    if (ts.fwd_count[(size_t)L] > 0) {
+      dim3 grid(ts.fwd_count[(size_t)L], h->nsd, nrhs);
+      k_fwd_big<<<grid, 256, shm_big, s>>>(t, fd, ts.fwd_items.p + ts.fwd_first[(size_t)L], h->nsd, f.panel.p, X, ysave,
+                                           upd, skip);
+      CB_LAUNCH();
+    }
   }
   for (int L = 0; L < nlev; ++L) {
-    dim3 grid(ts.level_count[(size_t)L], h->nsd, nrhs);
-    k_bwd_level<<<grid, 256, shm, s>>>(t, ts.level_sn.p + ts.level_first[(size_t)L], h->nsd, G.p, X, skip);
-    CB_LAUNCH();
+    if (ts.bwd_count[(size_t)L] > 0) {
+      dim3 grid(ts.bwd_count[(size_t)L], h->nsd, nrhs);
+      k_bwd_big<<<grid, 256, shm_big, s>>>(t, fd, ts.bwd_items.p + ts.bwd_first[(size_t)L], h->nsd, f.panel.p, X, ysave,
+                                           skip);
+      CB_LAUNCH();
+    }
+    if (ts.small_count[(size_t)L] > 0) {
+      dim3 grid(ts.small_count[(size_t)L], h->nsd, nrhs);
+      k_bwd_level<<<grid, 256, shm, s>>>(t, fd, ts.small_sn.p + ts.small_first[(size_t)L], h->nsd, f.panel.p, X, skip);
+      CB_LAUNCH();
+    }
   }
 }
 

@@ -11,21 +11,35 @@ struct TplDev {
   const AmapEntry* amap;
   const int32_t* emap;
   const int32_t* root_pos;
+  const uint8_t* is_big;
   int T;
+  int nsn;
   int root;  // id of the root supernode (last in postorder)
-  int64_t panel_total, front_total, upd_total;
+  int64_t rows_total;
 };
 
-// Matrix fed to the factorisation: A^w stencil restricted to `mask` slots
-// (identity rows elsewhere), plus diag_add on the diagonal (may be null) and,
-// on the root front, rho_w c c^T for every non-corner constraint row c
-// (K = A + rho C^T C; the root of the shell template holds every object node).
+// Per-subdomain compact structure of one factorisation (see factor.cu):
+//   pfx[sd][rows_total]  compact row index of every template row position of
+//                        every supernode (-1 when the slot is masked out)
+//   rc[sd][nsn]          compact (rows, cols) of each front
+//   panel_off / upd_off  offsets of the compact panel / forward update vector
+struct FactorDev {
+  const int32_t* pfx;
+  const int2* rc;
+  const int64_t* panel_off;
+  const int64_t* upd_off;
+  int64_t upd_total;  // doubles of the forward-update workspace per right-hand side
+};
+
+// Matrix fed to the factorisation: the A^w stencil restricted to `mask`
+// slots, plus diag_add on the diagonal (may be null) and, on the root front,
+// rho_w c c^T for every non-corner constraint row c (K = A + rho C^T C; the
+// root of the shell template holds every object node).
 struct FactorInput {
   const double* As;
   const uint8_t* mask;
   const double* diag_add;
   int T, b1;
-  // dense penalty rows (null for the interior problem)
   const int64_t* m_off;
   const int64_t* c_ptr;
   const int32_t* c_slot;
@@ -35,9 +49,13 @@ struct FactorInput {
 };
 
 TplDev tpl_dev(const TplSet& t, int slots);
+FactorDev factor_dev(const FactorSet& f);
 void upload_template(cutbddc_gpu* h, TplSet& t, bool shell_root);
-void factor_device(cutbddc_gpu* h, const TplSet& t, const FactorInput& in, DevBuf<double>& G, const char* what);
-void solve_device(cutbddc_gpu* h, const TplSet& t, const DevBuf<double>& G, double* X, int nrhs, double* upd,
-                  const int* skip);
+void factor_device(cutbddc_gpu* h, const TplSet& t, const FactorInput& in, FactorSet& f, const char* what);
+// ysave: nrhs x nsd x T doubles of scratch (forward results of big fronts).
+void solve_device(cutbddc_gpu* h, const TplSet& t, const FactorSet& f, double* X, int nrhs, double* upd,
+                  double* ysave, const int* skip);
+// algorithmic bytes of one forward + backward sweep (panel lower parts + front vectors)
+double sweep_bytes(const FactorSet& f);
 
 }  // namespace cutbddc_b200

@@ -27,7 +27,35 @@ struct TplSet {
   cutbddc_b200::DevBuf<int32_t> rows, emap, level_sn, root_pos;
   cutbddc_b200::DevBuf<cutbddc_b200::AmapEntry> amap;
   std::vector<int> level_first, level_count;
+  // per level: small supernodes (one CTA each, substitution on [L11; L21])
+  // and big supernodes (explicit G = [L11^{-1}; L21 L11^{-1}] panels, swept
+  // by many CTAs as GEMVs). Work items are (supernode, chunk) pairs.
+  cutbddc_b200::DevBuf<int32_t> small_sn;       // per level, concatenated
+  std::vector<int> small_first, small_count;
+  cutbddc_b200::DevBuf<int2> fwd_items, bwd_items, inv_items;  // (sn, chunk)
+  std::vector<int> fwd_first, fwd_count, bwd_first, bwd_count, inv_first, inv_count;
+  cutbddc_b200::DevBuf<int32_t> big_sn;         // per level, concatenated
+  std::vector<int> big_first, big_count;
+  std::vector<uint8_t> is_big;                  // per supernode
+  cutbddc_b200::DevBuf<uint8_t> big_flag;
+  cutbddc_b200::DevBuf<int2> gemm_items;
+  std::vector<int> gemm_first, gemm_count;
+  int max_cblocks = 0;
   bool ready = false;
+};
+
+// One factorisation over a template, compacted per subdomain (masked-out
+// slots dropped from every front).
+struct FactorSet {
+  cutbddc_b200::DevBuf<double> panel;          // compact [L11; L21] panels
+  cutbddc_b200::DevBuf<int32_t> pfx;           // nsd x rows_total
+  cutbddc_b200::DevBuf<int2> rc;               // nsd x nsn
+  cutbddc_b200::DevBuf<int64_t> panel_off, upd_off, front_off;  // nsd x nsn
+  std::vector<int2> h_rc;
+  std::vector<int64_t> h_front_base;           // nsd + 1 (front workspace prefix)
+  int64_t panel_total = 0, upd_total = 0;
+  double bytes_per_sweep = 0;                  // algorithmic bytes of fwd + bwd sweeps
+  double flops = 0;                            // partial-Cholesky flops
 };
 
 struct cutbddc_gpu {
@@ -77,7 +105,7 @@ struct cutbddc_gpu {
   // ---------------------------------------------------------------- template + factors
   TplSet tI;                                     // plain ND template (interior problems A_II)
   TplSet tK;                                     // shell-root template (K = A + rho C^T C)
-  cutbddc_b200::DevBuf<double> GI, GK;           // factor panels
+  FactorSet fI, fK;                              // interior / Neumann factorisations
   cutbddc_b200::DevBuf<uint8_t> mask_int, mask_all;  // per (sd, slot)
   cutbddc_b200::DevBuf<double> diag_add;         // per (sd, slot): rho at corner slots
   cutbddc_b200::DevBuf<uint8_t> corner_row;      // per constraint row: 1 if a corner
@@ -107,6 +135,7 @@ struct cutbddc_gpu {
 
   // ---------------------------------------------------------------- work vectors
   cutbddc_b200::DevBuf<double> sv0, sv1, sv2;     // slot vectors nsd*T
+  cutbddc_b200::DevBuf<double> ysave;             // big-front forward results, nsd*T
   cutbddc_b200::DevBuf<double> upd;               // solve workspace nsd*upd_total (x nrhs for setup)
   cutbddc_b200::DevBuf<double> gv0, gv1, gv2;     // global vectors n_dof
   cutbddc_b200::DevBuf<double> gl, cy, zc, gc;    // m_total, m_total, n_coarse, n_coarse

@@ -323,8 +323,8 @@ class GpuSolver:
     def stats(self):
         st = np.zeros(16, np.int64)
         _check(lib().cutbddc_gpu_stats(self.h, _p(st, C.c_int64)))
-        keys = ["n_dof", "n_sd", "n_coarse", "slots", "panel_per_subdomain", "n_supernodes", "levels", "m_max", "n_if",
-                "launches", "panel_interior", "panel_neumann"]
+        keys = ["n_dof", "n_sd", "n_coarse", "slots", "panel_total", "n_supernodes", "levels", "m_max", "n_if",
+                "launches", "panel_interior", "panel_neumann", "factor_flops"]
         return {k: int(st[i]) for i, k in enumerate(keys)}
 
 
