@@ -335,9 +335,40 @@ __global__ void k_coarse_rhs(int nc, const int64_t* __restrict__ cg_ptr, const i
   g[lam] = s;
 }
 
-// zc = A_c^{-1} (sum of the coarse rhs copies): one CTA, forward + backward
-// substitution on the column-major Cholesky panel (no explicit inverse: the
-// coarse matrix of small-cut problems is ill-conditioned).
+// Setup: column j of A_c^{-1} by forward + backward substitution on the
+// column-major Cholesky panel (one CTA per column, all in parallel).
+__global__ void __launch_bounds__(256) k_coarse_invert(int nc, const double* __restrict__ Lcm, double* __restrict__ Ainv) {
+  extern __shared__ double v[];
+  __shared__ double tile[32][33];
+  const int j = blockIdx.x;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) v[i] = i == j ? 1.0 : 0.0;
+  __syncthreads();
+  panel_forward(Lcm, nc, nc, v);
+  panel_backward(Lcm, nc, nc, v, tile);
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) Ainv[(int64_t)j * nc + i] = v[i];
+}
+
+// zc = A_c^{-1} g: warp per row of the (symmetric) explicit inverse.
+__global__ void k_coarse_gemv(int nc, const double* __restrict__ Ainv, const double* __restrict__ g,
+                              double* __restrict__ zc, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= nc) return;
+  const double* a = Ainv + row * nc;
+  double s0 = 0.0, s1 = 0.0;
+  int c = lane;
+  for (; c + 32 < nc; c += 64) {
+    s0 += a[c] * g[c];
+    s1 += a[c + 32] * g[c + 32];
+  }
+  for (; c < nc; c += 32) s0 += a[c] * g[c];
+  const double s = warp_sum(s0 + s1);
+  if (lane == 0) zc[row] = s;
+}
+
+// (reference path, unused in the apply) zc = A_c^{-1} (sum of the coarse rhs
+// copies) by one CTA of substitution on the Cholesky panel.
 __global__ void __launch_bounds__(512) k_coarse_solve(int nc, const int64_t* __restrict__ cg_ptr,
                                                       const int64_t* __restrict__ cg_idx, const double* __restrict__ gl,
                                                       const double* __restrict__ Lcm, double* __restrict__ zc,
@@ -589,17 +620,22 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     k_coarse_assemble<<<nc, 128, 0, s>>>(nc, h->cg_ptr.p, h->cg_idx.p, h->row_sd.p, h->m_off.p, h->ac_off.p,
                                          h->coarse_id.p, h->ac_loc.p, h->acoarse.p);
     CB_LAUNCH();
-    // acoarse_inv holds the column-major Cholesky panel of A_c
-    CB_CUDA(cudaMemcpyAsync(h->acoarse_inv.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
+    // Cholesky panel of A_c (column-major), then the explicit inverse by
+    // parallel column solves; the apply multiplies by it (one GEMV).
+    DevBuf<double> Lc;
+    Lc.alloc((size_t)nc * nc);
+    CB_CUDA(cudaMemcpyAsync(Lc.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
     DevBuf<unsigned long long> fail;
     fail.alloc(1);
     CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
-    k_coarse_chol<<<1, 256, 0, s>>>(nc, h->acoarse_inv.p, fail.p);
+    k_coarse_chol<<<1, 256, 0, s>>>(nc, Lc.p, fail.p);
     CB_LAUNCH();
     const size_t shm = sizeof(double) * (size_t)nc;
-    if (shm > 200 * 1024) throw Failure(CUTBDDC_CONFIG, "coarse problem too large for the single-CTA coarse solve");
+    if (shm > 200 * 1024) throw Failure(CUTBDDC_CONFIG, "coarse problem too large for the coarse inverse");
     if (shm > 48 * 1024)
-      CB_CUDA(cudaFuncSetAttribute(k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+      CB_CUDA(cudaFuncSetAttribute(k_coarse_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    k_coarse_invert<<<nc, 256, shm, s>>>(nc, Lc.p, h->acoarse_inv.p);
+    CB_LAUNCH();
     unsigned long long f = 0;
     CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));
     CB_CUDA(cudaStreamSynchronize(s));
@@ -645,8 +681,10 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
                                                        h->sv1.p, h->cy.p, skip);
     CB_LAUNCH();
-    k_coarse_solve<<<1, 512, sizeof(double) * (size_t)h->n_coarse, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p,
-                                                                       h->acoarse_inv.p, h->zc.p, skip);
+    k_coarse_rhs<<<grid_for(h->n_coarse, 128), 128, 0, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->gc.p, skip);
+    CB_LAUNCH();
+    k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_inv.p, h->gc.p,
+                                                                         h->zc.p, skip);
     CB_LAUNCH();
     k_prolong<<<grid_for(ns, 256), 256, 0, s>>>(h->nsd, T, h->m_off.p, h->coarse_id.p, h->phi_c.p, h->zc.p, h->cy.p,
                                                 h->sv1.p, skip);

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_factor_level(TplDev t, FactorDev f
     }
     __syncthreads();
   }
+  if (t.is_split[sid]) return;  // large fronts: factorised by the multi-CTA panel steps
   // blocked right-looking partial Cholesky of the c pivot columns
   CholSmem& sm = *reinterpret_cast<CholSmem*>(smraw);
   front_partial_cholesky(F, r, c, sm, [&](int j) {
@@ -168,6 +169,156 @@ __global__ void __launch_bounds__(kThreads) k_factor_level(TplDev t, FactorDev f
   double* P = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
   for (int j = 0; j < c; ++j)
     for (int i = j + tid; i < r; i += blockDim.x) P[i + (int64_t)j * r] = F[i + (int64_t)j * r];
+}
+
+// ---------------------------------------------------------------- split fronts
+// Large fronts (template rows >= kSplitRows) are factorised by three
+// launches per 32-column panel step so that many CTAs share one front:
+// (1) the diagonal block, (2) the panel rows below it in 128-row chunks,
+// (3) the rank-32 update of the trailing lower triangle in 64x64 tiles.
+constexpr int kSplitRows = 600;
+
+struct SplitArgs {
+  const int32_t* sn;          // split supernodes of this level
+  int sd0;
+  const int64_t* front_off;
+  int64_t front_base0;
+  const int64_t* front_base;
+  double* front;
+  unsigned long long* fail;
+};
+
+__device__ inline double* split_front(const TplDev& t, const FactorDev& f, const SplitArgs& a, int sid, int sd) {
+  return a.front + (a.front_base[sd] - a.front_base0) + a.front_off[(int64_t)sd * t.nsn + sid];
+}
+
+__global__ void __launch_bounds__(32) k_split_diag(TplDev t, FactorDev f, SplitArgs a, int k) {
+  const int sid = a.sn[blockIdx.x];
+  const int sd = a.sd0 + blockIdx.y;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  if (k >= c) return;
+  const int nb = min(32, c - k);
+  double* F = split_front(t, f, a, sid, sd);
+  __shared__ double d[32][33];
+  const int lane = threadIdx.x;
+  for (int j = 0; j < nb; ++j) d[lane][j] = (lane < nb && lane >= j) ? F[(k + lane) + (int64_t)(k + j) * r] : 0.0;
+  __syncwarp();
+  for (int j = 0; j < nb; ++j) {
+    double djj = d[j][j];
+    if (lane == 0 && !(djj > 0.0)) {
+      const Supernode s = t.sn[sid];
+      for (int q = 0; q < s.ncols; ++q)
+        if (f.pfx[(int64_t)sd * t.rows_total + s.rows_off + q] == k + j) {
+          atomicMin(a.fail, (unsigned long long)((int64_t)sd * t.T + t.rows[s.rows_off + q]));
+          break;
+        }
+    }
+    if (!(djj > 0.0)) djj = 1.0;
+    const double l = sqrt(djj);
+    __syncwarp();
+    if (lane == j) d[j][j] = l;
+    if (lane > j && lane < nb) d[lane][j] /= l;
+    __syncwarp();
+    if (lane > j && lane < nb) {
+      const double lij = d[lane][j];
+      for (int q = j + 1; q <= lane; ++q) d[lane][q] -= lij * d[q][j];
+    }
+    __syncwarp();
+  }
+  for (int j = 0; j < nb; ++j)
+    if (lane < nb && lane >= j) F[(k + lane) + (int64_t)(k + j) * r] = d[lane][j];
+}
+
+__global__ void __launch_bounds__(128) k_split_trsm(TplDev t, FactorDev f, SplitArgs a, int k) {
+  const int sid = a.sn[blockIdx.y];
+  const int sd = a.sd0 + blockIdx.z;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  if (k >= c) return;
+  const int nb = min(32, c - k);
+  const int i = k + nb + blockIdx.x * 128 + threadIdx.x;
+  double* F = split_front(t, f, a, sid, sd);
+  __shared__ double d[32][33];
+  __shared__ double inv[32];
+  for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
+    const int ii = q & 31, jj = q >> 5;
+    d[ii][jj] = (ii < nb && jj < nb && ii >= jj) ? F[(k + ii) + (int64_t)(k + jj) * r] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) inv[threadIdx.x] = threadIdx.x < nb ? 1.0 / d[threadIdx.x][threadIdx.x] : 0.0;
+  __syncthreads();
+  if (i >= r) return;
+  double x[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) x[q] = q < nb ? F[i + (int64_t)(k + q) * r] : 0.0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    if (q < nb) {
+      double s = x[q];
+#pragma unroll
+      for (int u = 0; u < q; ++u) s -= x[u] * d[q][u];
+      x[q] = s * inv[q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 32; ++q)
+    if (q < nb) F[i + (int64_t)(k + q) * r] = x[q];
+}
+
+__global__ void __launch_bounds__(256) k_split_syrk(TplDev t, FactorDev f, SplitArgs a, int k) {
+  const int sid = a.sn[blockIdx.y];
+  const int sd = a.sd0 + blockIdx.z;
+  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
+  const int r = rc.x, c = rc.y;
+  if (k >= c) return;
+  const int nb = min(32, c - k);
+  const int m0 = k + nb;
+  // tile pair (ti >= tj) from the linear index
+  const int q = blockIdx.x;
+  int ti = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+  while ((ti + 1) * (ti + 2) / 2 <= q) ++ti;
+  while (ti * (ti + 1) / 2 > q) --ti;
+  const int tj = q - ti * (ti + 1) / 2;
+  const int i0 = m0 + ti * 64, j0 = m0 + tj * 64;
+  if (i0 >= r) return;
+  double* F = split_front(t, f, a, sid, sd);
+  __shared__ double pi[32][64], pj[32][64];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int e = tid; e < 32 * 64; e += blockDim.x) {
+    const int rr = e & 63, kk = e >> 6;
+    const int i = i0 + rr, j = j0 + rr;
+    pi[kk][rr] = (kk < nb && i < r) ? F[i + (int64_t)(k + kk) * r] : 0.0;
+    pj[kk][rr] = (kk < nb && j < r) ? F[j + (int64_t)(k + kk) * r] : 0.0;
+  }
+  __syncthreads();
+  double acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+  for (int kk = 0; kk < nb; ++kk) {
+    double pa[4], pb[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) pa[x] = pi[kk][tx + 16 * x];
+#pragma unroll
+    for (int y = 0; y < 4; ++y) pb[y] = pj[kk][ty + 16 * y];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y] += pa[x] * pb[y];
+  }
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    const int j = j0 + ty + 16 * y;
+    if (j >= r) continue;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int i = i0 + tx + 16 * x;
+      if (i >= r || i < j) continue;
+      F[i + (int64_t)j * r] -= acc[x][y];
+    }
+  }
 }
 
 // Big fronts: X = L11^{-1} into the top c x c block of the G panel, one CTA
@@ -372,8 +523,12 @@ __global__ void __launch_bounds__(256) k_bwd_level(TplDev t, FactorDev f, const 
 // (one CTA each). Every chunk rebuilds the full front vector (gather +
 // children's updates) in shared memory; y goes to `ysave` (x keeps b at the
 // columns until the backward sweep, so concurrent chunks never race).
-constexpr int kBigRows = 128;
-constexpr int kBigCols = 32;
+// Fronts with at least kBigMinCols template columns get explicit-inverse
+// panels and multi-CTA GEMV sweeps; all fronts do (measured: the blocked
+// substitution path was latency-bound at every level).
+constexpr int kBigMinCols = 1;
+constexpr int kBigRows = 32;   // forward: rows per CTA (one row per lane)
+constexpr int kBigCols = 16;   // backward: columns per CTA (two per warp)
 
 __global__ void __launch_bounds__(256) k_fwd_big(TplDev t, FactorDev f, const int2* __restrict__ items, int nsd,
                                                  const double* __restrict__ panel, const double* __restrict__ X,
@@ -416,29 +571,36 @@ __global__ void __launch_bounds__(256) k_fwd_big(TplDev t, FactorDev f, const in
   }
   const double* G = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
   double* uo = ub + f.upd_off[(int64_t)sd * t.nsn + sid];
-  // two threads per row (even / odd columns), combined through a shuffle
-  const int half = threadIdx.x & 1;
-  for (int base = i0; base < i1; base += blockDim.x >> 1) {
-    const int i = base + (threadIdx.x >> 1);
-    const bool act = i < i1;
-    double s0 = 0.0, s1 = 0.0;
-    if (act) {
-      const int jmax = i < c ? i + 1 : c;
-      int j = half;
-      for (; j + 2 < jmax; j += 4) {
-        s0 += G[i + (int64_t)j * r] * v[j];
-        s1 += G[i + (int64_t)(j + 2) * r] * v[j + 2];
-      }
-      for (; j < jmax; j += 2) s0 += G[i + (int64_t)j * r] * v[j];
+  // lane = row of the 32-row chunk, warp = contiguous column range; four
+  // independent accumulators keep 4 coalesced 256-B loads per warp in flight.
+  // (G's strict upper triangle is stored as zeros, so rows need no mask.)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int jend = min(c, i1);
+  const int cw = (jend + nw - 1) / nw;
+  const int ja = min(jend, wid * cw), jb = min(jend, ja + cw);
+  const int i = i0 + lane;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (i < i1) {
+    const double* gi = G + i;
+    int j = ja;
+    for (; j + 4 <= jb; j += 4) {
+      s0 += gi[(int64_t)j * r] * v[j];
+      s1 += gi[(int64_t)(j + 1) * r] * v[j + 1];
+      s2 += gi[(int64_t)(j + 2) * r] * v[j + 2];
+      s3 += gi[(int64_t)(j + 3) * r] * v[j + 3];
     }
-    double o = s0 + s1;
-    o += __shfl_xor_sync(0xffffffffu, o, 1);
-    if (act && half == 0) {
-      if (i < c)
-        ys[slot_of[i]] = o;
-      else
-        uo[i - c] = v[i] - o;
-    }
+    for (; j < jb; ++j) s0 += gi[(int64_t)j * r] * v[j];
+  }
+  __shared__ double part[8][33];
+  part[wid][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (wid == 0 && i < i1) {
+    double o = 0.0;
+    for (int q = 0; q < nw; ++q) o += part[q][lane];
+    if (i < c)
+      ys[slot_of[i]] = o;
+    else
+      uo[i - c] = v[i] - o;
   }
 }
 
@@ -474,10 +636,17 @@ __global__ void __launch_bounds__(256) k_bwd_big(TplDev t, FactorDev f, const in
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = j0 + wid; j < j1; j += nw) {
     const double* col = G + (int64_t)j * r;
-    double s0 = 0.0;
-    for (int i = j + lane; i < r; i += 32) s0 += col[i] * w[i];
-    s0 = warp_sum(s0);
-    if (lane == 0) x[slot_of[j]] = s0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = j + lane;
+    for (; i + 96 < r; i += 128) {
+      s0 += col[i] * w[i];
+      s1 += col[i + 32] * w[i + 32];
+      s2 += col[i + 64] * w[i + 64];
+      s3 += col[i + 96] * w[i + 96];
+    }
+    for (; i < r; i += 32) s0 += col[i] * w[i];
+    const double sum = warp_sum((s0 + s1) + (s2 + s3));
+    if (lane == 0) x[slot_of[j]] = sum;
   }
 }
 
@@ -491,6 +660,7 @@ TplDev tpl_dev(const TplSet& ts, int slots) {
   t.emap = ts.emap.p;
   t.root_pos = ts.root_pos.p;
   t.is_big = ts.big_flag.p;
+  t.is_split = ts.split_flag.p;
   t.T = slots;
   t.nsn = (int)ts.tpl.sn.size();
   t.root = t.nsn - 1;
@@ -528,6 +698,28 @@ void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
   ts.gemm_first.clear();
   ts.gemm_count.clear();
   ts.is_big.assign(ts.tpl.sn.size(), 0);
+  std::vector<uint8_t> is_split(ts.tpl.sn.size(), 0);
+  std::vector<int32_t> split;
+  ts.split_first.clear();
+  ts.split_count.clear();
+  ts.split_maxc.clear();
+  ts.split_maxr.clear();
+  for (auto& L : ts.tpl.levels) {
+    ts.split_first.push_back((int)split.size());
+    int maxc = 0, maxr = 0;
+    for (int sid : L) {
+      const Supernode& sn = ts.tpl.sn[(size_t)sid];
+      if (sn.nrows >= kSplitRows) {
+        is_split[(size_t)sid] = 1;
+        split.push_back(sid);
+        maxc = std::max(maxc, sn.ncols);
+        maxr = std::max(maxr, sn.nrows);
+      }
+    }
+    ts.split_count.push_back((int)split.size() - ts.split_first.back());
+    ts.split_maxc.push_back(maxc);
+    ts.split_maxr.push_back(maxr);
+  }
   for (auto& L : ts.tpl.levels) {
     ts.level_first.push_back((int)lv.size());
     ts.level_count.push_back((int)L.size());
@@ -541,7 +733,7 @@ void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
     for (int sid : L) {
       const Supernode& sn = ts.tpl.sn[(size_t)sid];
       // big: explicit-inverse panel swept by many CTAs
-      const bool is_big = sn.ncols >= 96;
+      const bool is_big = sn.ncols >= kBigMinCols;
       ts.is_big[(size_t)sid] = is_big;
       if (!is_big) {
         small.push_back(sid);
@@ -571,6 +763,8 @@ void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
   ts.inv_items.upload(nz2(inv), s);
   ts.gemm_items.upload(nz2(gem), s);
   ts.big_flag.upload(ts.is_big, s);
+  ts.split_flag.upload(is_split, s);
+  ts.split_sn.upload(nz32(split), s);
   ts.ready = true;
 }
 
@@ -637,6 +831,23 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
                                                f.front_off.p, f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p,
                                                fail.p);
       CB_LAUNCH();
+      if (ts.split_count[(size_t)L] > 0) {
+        SplitArgs sa{ts.split_sn.p + ts.split_first[(size_t)L], sd0, f.front_off.p, f.h_front_base[(size_t)sd0],
+                     fbase.p, front.p, fail.p};
+        const int ns_ = ts.split_count[(size_t)L], nc_ = sd1 - sd0;
+        const int maxc = ts.split_maxc[(size_t)L], maxr = ts.split_maxr[(size_t)L];
+        for (int k = 0; k < maxc; k += 32) {
+          k_split_diag<<<dim3(ns_, nc_), 32, 0, s>>>(t, fd, sa, k);
+          CB_LAUNCH();
+          const int rows_below = maxr - k - 1;
+          if (rows_below <= 0) continue;
+          k_split_trsm<<<dim3((rows_below + 127) / 128, ns_, nc_), 128, 0, s>>>(t, fd, sa, k);
+          CB_LAUNCH();
+          const int nt = (rows_below + 63) / 64;
+          k_split_syrk<<<dim3(nt * (nt + 1) / 2, ns_, nc_), 256, 0, s>>>(t, fd, sa, k);
+          CB_LAUNCH();
+        }
+      }
       if (ts.inv_count[(size_t)L] > 0) {
         dim3 gi(ts.inv_count[(size_t)L], sd1 - sd0);
         k_trinv<<<gi, 256, 0, s>>>(t, fd, ts.inv_items.p + ts.inv_first[(size_t)L], sd0, f.front_off.p,

@@ -12,6 +12,7 @@ struct TplDev {
   const int32_t* emap;
   const int32_t* root_pos;
   const uint8_t* is_big;
+  const uint8_t* is_split;
   int T;
   int nsn;
   int root;  // id of the root supernode (last in postorder)

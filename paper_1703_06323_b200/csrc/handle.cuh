@@ -37,7 +37,9 @@ struct TplSet {
   cutbddc_b200::DevBuf<int32_t> big_sn;         // per level, concatenated
   std::vector<int> big_first, big_count;
   std::vector<uint8_t> is_big;                  // per supernode
-  cutbddc_b200::DevBuf<uint8_t> big_flag;
+  cutbddc_b200::DevBuf<uint8_t> big_flag, split_flag;
+  cutbddc_b200::DevBuf<int32_t> split_sn;       // large fronts per level (multi-CTA factorisation)
+  std::vector<int> split_first, split_count, split_maxc, split_maxr;
   cutbddc_b200::DevBuf<int2> gemm_items;
   std::vector<int> gemm_first, gemm_count;
   int max_cblocks = 0;
