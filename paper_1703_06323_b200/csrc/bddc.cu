@@ -559,12 +559,19 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   if (hbad) throw Failure(CUTBDDC_DEGENERATE, "weighting: zero total diagonal at an interface dof");
   // ---- factorisations
   if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);
-  if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
   FactorInput fi{h->As.p, h->mask_int.p, nullptr, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   factor_device(h, h->tI, fi, h->fI, "cholesky (interior problem)");
-  FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
-                 h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
-  factor_device(h, h->tK, fk, h->fK, "saddle: singular augmented system; constraints do not control the operator kernel");
+  // Without an interface (one subdomain) every dof is interior: the weighted
+  // residual r_w is identically zero and the constrained Neumann solve drops
+  // out of the apply ("preconditioner reduces to exact interior solve").
+  h->has_K = h->n_if > 0;
+  h->fK.upd_total = 0;
+  if (h->has_K) {
+    if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
+    FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
+                   h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
+    factor_device(h, h->tK, fk, h->fK, "saddle: singular augmented system; constraints do not control the operator kernel");
+  }
   const int64_t upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, h->fK.upd_total));
   // ---- coarse basis
   h->phi_c.alloc((size_t)std::max<int64_t>(1, h->m_total) * T);
@@ -676,7 +683,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     k_phit<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->phi_c.p, h->sv1.p, h->gl.p, skip);
     CB_LAUNCH();
   }
-  solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
+  if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
   if (h->m_total > 0) {
     k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
                                                        h->sv1.p, h->cy.p, skip);

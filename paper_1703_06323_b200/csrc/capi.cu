@@ -296,6 +296,7 @@ cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x) {
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
     const size_t ns = (size_t)h->nsd * h->slots;
+    if (which != 0 && !h->has_K) throw Failure(CUTBDDC_INVALID_ARGUMENT, "no constrained Neumann factor (no interface)");
     DevBuf<double> X;
     X.upload(x, ns, h->stream);
     solve_device(h, which == 0 ? h->tI : h->tK, which == 0 ? h->fI : h->fK, X.p, 1, h->upd.p, h->ysave.p, nullptr);
@@ -312,15 +313,15 @@ cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds
     if (reps < 1) reps = 1;
     // warm
     solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
-    solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
+    if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
     Timer tm(h->stream);
     for (int r = 0; r < reps; ++r) {
       solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
-      solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
+      if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
       solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
     }
     *seconds = tm.stop() / reps;
-    *bytes = 2.0 * sweep_bytes(h->fI) + sweep_bytes(h->fK);
+    *bytes = 2.0 * sweep_bytes(h->fI) + (h->has_K ? sweep_bytes(h->fK) : 0.0);
   });
 }
 

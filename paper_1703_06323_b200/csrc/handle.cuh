@@ -108,6 +108,7 @@ struct cutbddc_gpu {
   TplSet tI;                                     // plain ND template (interior problems A_II)
   TplSet tK;                                     // shell-root template (K = A + rho C^T C)
   FactorSet fI, fK;                              // interior / Neumann factorisations
+  bool has_K = false;                            // false without an interface (one subdomain)
   cutbddc_b200::DevBuf<uint8_t> mask_int, mask_all;  // per (sd, slot)
   cutbddc_b200::DevBuf<double> diag_add;         // per (sd, slot): rho at corner slots
   cutbddc_b200::DevBuf<uint8_t> corner_row;      // per constraint row: 1 if a corner
