@@ -258,12 +258,13 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
   const int64_t nc = h->n_cells;
   const int grid = 148 * 8;
   // active / cut cell lists (ascending)
-  DevBuf<uint8_t> act, cut;
+  DevBuf<uint8_t>& act = h->ws_act;
+  DevBuf<uint8_t>& cut = h->ws_cut;
   act.alloc((size_t)nc);
   cut.alloc((size_t)nc);
   k_cell_flags<<<grid, 256, 0, s>>>(nc, h->cls.p, act.p, cut.p);
   CB_LAUNCH();
-  DevBuf<int64_t> cnt;
+  DevBuf<int64_t>& cnt = h->ws_cnt;
   cnt.alloc(2);
   h->active_cells.alloc((size_t)nc);
   h->cut_cells.alloc((size_t)nc);
@@ -271,7 +272,7 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
   cub::CountingInputIterator<int64_t> it(0);
   CB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, act.p, h->active_cells.p, cnt.p, nc, s));
   CB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, it, cut.p, h->cut_cells.p, cnt.p + 1, nc, s));
-  DevBuf<uint8_t> tmp;
+  DevBuf<uint8_t>& tmp = h->ws_tmp;
   tmp.alloc(std::max(tb, tb2));
   CB_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, act.p, h->active_cells.p, cnt.p, nc, s));
   CB_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb2, it, cut.p, h->cut_cells.p, cnt.p + 1, nc, s));
@@ -289,7 +290,7 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
   }
   // element matrices
   cut_elements_device(h);
-  DevBuf<double> kint;
+  DevBuf<double>& kint = h->ws_kint;
   kint.alloc(72);
   interior_element_device(h, kint.p, kint.p + 64);
   // subdomain maps
@@ -315,7 +316,7 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
   k_subassemble<<<grid_for(ns, 128), 128, 0, s>>>(nsd, m, h->block_ids.p, h->orphan.p, h->ncount.p, h->slot_dof.p, h->As.p);
   CB_LAUNCH();
   // copies CSR
-  DevBuf<int64_t> nc64;
+  DevBuf<int64_t>& nc64 = h->ws_nc64;
   nc64.alloc((size_t)nd);
   k_u8_to_i64<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->ncount.p, nc64.p);
   CB_LAUNCH();

@@ -67,20 +67,25 @@ __global__ void k_weights(int64_t ns, int T, int mode, const int32_t* __restrict
 // sequentially in ascending local dof (= slot) order: K = A + rho C^T C of a
 // small-cut subdomain is so ill-conditioned that a 1-ulp change of rho moves
 // the saddle solutions by ~1e-9, so rho is pinned bit-for-bit to the CPU
-// restatement's order. One thread per subdomain (setup only).
+// restatement's order. One warp per subdomain: coalesced loads of 32 slots,
+// then the 32 values are added in slot order (absent slots add +0.0, which
+// leaves the running sum unchanged).
 __global__ void k_rho(int nsd, int T, const int32_t* __restrict__ slot_dof, const double* __restrict__ As,
                       double* __restrict__ rho) {
-  const int sd = blockIdx.x * blockDim.x + threadIdx.x;
+  const int sd = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (sd >= nsd) return;
   double s = 0.0;
-  int64_t c = 0;
-  for (int t = 0; t < T; ++t) {
-    if (slot_dof[(int64_t)sd * T + t] >= 0) {
-      s += As[(int64_t)sd * 27 * T + 13ll * T + t];
-      ++c;
-    }
+  long long c = 0;
+  for (int base = 0; base < T; base += 32) {
+    const int t = base + lane;
+    const bool p = t < T && slot_dof[(int64_t)sd * T + t] >= 0;
+    const double v = p ? As[(int64_t)sd * 27 * T + 13ll * T + t] : 0.0;
+    c += __popc(__ballot_sync(0xffffffffu, p));
+#pragma unroll
+    for (int l = 0; l < 32; ++l) s += __shfl_sync(0xffffffffu, v, l);
   }
-  rho[sd] = c > 0 ? s / (double)c : 1.0;
+  if (lane == 0) rho[sd] = c > 0 ? s / (double)c : 1.0;
 }
 
 __global__ void k_diag_add(int nsd, int T, const int64_t* __restrict__ m_off, const int64_t* __restrict__ c_ptr,
@@ -535,7 +540,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   k_row_sd<<<nsd, 128, 0, s>>>(nsd, h->m_off.p, h->row_sd.p);
   CB_LAUNCH();
   // ---- weights, rho, masks
-  DevBuf<int> bad;
+  DevBuf<int>& bad = h->ws_flag;
   bad.alloc(1);
   bad.zero(s);
   h->w.alloc((size_t)ns);
@@ -547,7 +552,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   k_masks<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->ncount.p, h->mask_all.p, h->mask_int.p);
   CB_LAUNCH();
   h->rho.alloc((size_t)nsd);
-  k_rho<<<grid_for(nsd, 64), 64, 0, s>>>(nsd, T, h->slot_dof.p, h->As.p, h->rho.p);
+  k_rho<<<grid_for((int64_t)nsd * 32, 128), 128, 0, s>>>(nsd, T, h->slot_dof.p, h->As.p, h->rho.p);
   CB_LAUNCH();
   h->diag_add.alloc((size_t)ns);
   h->diag_add.zero(s);
@@ -577,25 +582,26 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->phi_c.alloc((size_t)std::max<int64_t>(1, h->m_total) * T);
   h->ac_loc.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
   if (m_max > 0) {
-    DevBuf<double> Wall, upd;
+    DevBuf<double>& Wall = h->ws_wall;
+    DevBuf<double>& upd = h->ws_upd;
     Wall.alloc((size_t)m_max * ns);
     Wall.zero(s);
     const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(m_max, (2ll << 30) / 8 / std::max(upd_total, ns)));
     upd.alloc((size_t)rb * upd_total);
-    DevBuf<double> ys;
+    DevBuf<double>& ys = h->ws_ys;
     ys.alloc((size_t)rb * ns);
     for (int r0 = 0; r0 < m_max; r0 += rb) {
       const int nr = std::min(rb, m_max - r0);
       double* X = Wall.p + (int64_t)r0 * ns;
       k_fill_ct<<<dim3(nsd, nr), 64, 0, s>>>(nsd, T, r0, nr, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, X);
       CB_LAUNCH();
-      solve_device(h, h->tK, h->fK, X, nr, upd.p, ys.p, nullptr);
+      solve_device(h, h->tK, h->fK, X, nr, upd.p, ys.p, nullptr, /*rhs_root_only=*/true);
     }
-    DevBuf<double> S;
+    DevBuf<double>& S = h->ws_s;
     S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
     k_schur<<<nsd, 256, 0, s>>>(nsd, T, h->m_off.p, h->ac_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, Wall.p, S.p);
     CB_LAUNCH();
-    DevBuf<unsigned long long> fail;
+    DevBuf<unsigned long long>& fail = h->ws_fail;
     fail.alloc(1);
     CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
     const size_t shm = sizeof(double) * ((size_t)m_max * m_max + m_max);
@@ -629,10 +635,10 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     CB_LAUNCH();
     // Cholesky panel of A_c (column-major), then the explicit inverse by
     // parallel column solves; the apply multiplies by it (one GEMV).
-    DevBuf<double> Lc;
+    DevBuf<double>& Lc = h->ws_lc;
     Lc.alloc((size_t)nc * nc);
     CB_CUDA(cudaMemcpyAsync(Lc.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
-    DevBuf<unsigned long long> fail;
+    DevBuf<unsigned long long>& fail = h->ws_fail;
     fail.alloc(1);
     CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
     k_coarse_chol<<<1, 256, 0, s>>>(nc, Lc.p, fail.p);

@@ -28,11 +28,12 @@ extern std::atomic<long long> g_kernel_launches;
     CB_CUDA(cudaGetLastError());                                 \
   } while (0)
 
-// Owning device buffer.
+// Owning device buffer; grow-only (a smaller alloc reuses the allocation, so
+// repeated solves do no cudaMalloc/cudaFree inside the timed phases).
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
-  size_t n = 0;
+  size_t n = 0, cap = 0;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -40,14 +41,17 @@ struct DevBuf {
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
-    n = 0;
+    n = cap = 0;
   }
   void alloc(size_t count) {
-    if (count == n && p) return;
+    if (p && count <= cap) {
+      n = count;
+      return;
+    }
     release();
     if (count == 0) return;
     CB_CUDA(cudaMalloc(&p, count * sizeof(T)));
-    n = count;
+    n = cap = count;
   }
   void zero(cudaStream_t s) {
     if (n) CB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));

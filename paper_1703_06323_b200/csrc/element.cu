@@ -334,7 +334,7 @@ void interior_element_device(cutbddc_gpu* h, double* kint, double* fint) {
 }
 
 void cut_elements_device(cutbddc_gpu* h) {
-  DevBuf<int> degen;
+  DevBuf<int>& degen = h->ws_flag;
   degen.alloc(1);
   degen.zero(h->stream);
   h->ke.alloc((size_t)std::max<int64_t>(1, h->n_cut) * 64);
@@ -342,7 +342,7 @@ void cut_elements_device(cutbddc_gpu* h) {
   h->beta.alloc((size_t)std::max<int64_t>(1, h->n_cut));
   h->empty.alloc((size_t)std::max<int64_t>(1, h->n_cut));
   if (h->n_cut > 0) {
-    DevBuf<double> q8all;
+    DevBuf<double>& q8all = h->ws_q8;
     q8all.alloc((size_t)h->n_cut * 8);
     k_gather_q8<<<grid_for(h->n_cut, 256), 256, 0, h->stream>>>(h->n, h->n_cut, h->cut_cells.p, h->phi.p, q8all.p);
     CB_LAUNCH();

@@ -38,7 +38,8 @@ __device__ inline int pfx_at(const FactorDev& f, const TplDev& t, int sd, const 
 // ---------------------------------------------------------------- symbolic
 // CTA per (supernode, subdomain): prefix-count the masked template rows.
 __global__ void __launch_bounds__(kThreads) k_symbolic(TplDev t, int nsd, const uint8_t* __restrict__ mask,
-                                                       int32_t* __restrict__ pfx, int2* __restrict__ rc) {
+                                                       int32_t* __restrict__ pfx, int32_t* __restrict__ tpos,
+                                                       int2* __restrict__ rc) {
   const int sid = blockIdx.x, sd = blockIdx.y;
   const Supernode s = t.sn[sid];
   const int r = s.nrows;
@@ -62,9 +63,11 @@ __global__ void __launch_bounds__(kThreads) k_symbolic(TplDev t, int nsd, const 
   int run = sc[threadIdx.x];
   int32_t* out = pfx + (int64_t)sd * t.rows_total + s.rows_off;
   int ccount = 0;
+  int32_t* inv = tpos + (int64_t)sd * t.rows_total + s.rows_off;
   for (int q = q0; q < q1; ++q) {
     const bool p = mask[(int64_t)sd * t.T + t.rows[s.rows_off + q]] != 0;
     out[q] = p ? run : -1;
+    if (p) inv[run] = q;  // compact row -> template row position
     run += p;
   }
   // compact cols = present rows among the first ncols template rows
@@ -90,6 +93,7 @@ __global__ void __launch_bounds__(kThreads) k_factor_level(TplDev t, FactorDev f
                                                            double* __restrict__ front, double* __restrict__ panel,
                                                            unsigned long long* fail) {
   const int sid = level_sn[blockIdx.x];
+  if (t.is_split[sid]) return;  // large fronts: multi-CTA assembly + panel steps
   const Supernode s = t.sn[sid];
   const int sd = sd0 + blockIdx.y;
   const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
@@ -153,7 +157,6 @@ __global__ void __launch_bounds__(kThreads) k_factor_level(TplDev t, FactorDev f
     }
     __syncthreads();
   }
-  if (t.is_split[sid]) return;  // large fronts: factorised by the multi-CTA panel steps
   // blocked right-looking partial Cholesky of the c pivot columns
   CholSmem& sm = *reinterpret_cast<CholSmem*>(smraw);
   front_partial_cholesky(F, r, c, sm, [&](int j) {
@@ -190,6 +193,77 @@ struct SplitArgs {
 
 __device__ inline double* split_front(const TplDev& t, const FactorDev& f, const SplitArgs& a, int sid, int sd) {
   return a.front + (a.front_base[sd] - a.front_base0) + a.front_off[(int64_t)sd * t.nsn + sid];
+}
+
+// Multi-CTA assembly of split fronts: zero, original entries, rho c c^T
+// (root), then each child's update matrix (one launch per child; the entries
+// of one child map to distinct parent entries).
+__global__ void __launch_bounds__(256) k_split_zero(TplDev t, FactorDev f, SplitArgs a) {
+  const int sid = a.sn[blockIdx.y];
+  const int sd = a.sd0 + blockIdx.z;
+  const int r = f.rc[(int64_t)sd * t.nsn + sid].x;
+  double* F = split_front(t, f, a, sid, sd);
+  const int64_t n = (int64_t)r * r;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) F[q] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_split_amap(TplDev t, FactorDev f, SplitArgs a, FactorInput in) {
+  const int sid = a.sn[blockIdx.y];
+  const int sd = a.sd0 + blockIdx.z;
+  const Supernode s = t.sn[sid];
+  const int r = f.rc[(int64_t)sd * t.nsn + sid].x;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= s.amap_len || r == 0) return;
+  const AmapEntry e = t.amap[s.amap_off + q];
+  const int pr = pfx_at(f, t, sd, s, e.pos % s.nrows), pc = pfx_at(f, t, sd, s, e.pos / s.nrows);
+  if (pr < 0 || pc < 0) return;
+  split_front(t, f, a, sid, sd)[pr + (int64_t)pc * r] = stencil_value(in, sd, e.slot, e.k);
+}
+
+__global__ void __launch_bounds__(256) k_split_penalty(TplDev t, FactorDev f, SplitArgs a, FactorInput in) {
+  const int sid = a.sn[blockIdx.y];
+  if (sid != t.root || !in.c_ptr) return;
+  const int sd = a.sd0 + blockIdx.z;
+  const int64_t row = in.m_off[sd] + blockIdx.x;
+  if (row >= in.m_off[sd + 1] || in.corner[row]) return;
+  const Supernode s = t.sn[sid];
+  const int r = f.rc[(int64_t)sd * t.nsn + sid].x;
+  double* F = split_front(t, f, a, sid, sd);
+  const double rho = in.rho[sd];
+  const int64_t p0 = in.c_ptr[row];
+  const int len = (int)(in.c_ptr[row + 1] - p0);
+  for (int q = threadIdx.x; q < len * len; q += blockDim.x) {
+    const int x = q / len, y = q % len;
+    const int pa = pfx_at(f, t, sd, s, t.root_pos[in.c_slot[p0 + x]]);
+    const int pb = pfx_at(f, t, sd, s, t.root_pos[in.c_slot[p0 + y]]);
+    if (pa < pb || pa < 0 || pb < 0) continue;
+    F[pa + (int64_t)pb * r] += rho * in.c_val[p0 + x] * in.c_val[p0 + y];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_split_extend(TplDev t, FactorDev f, SplitArgs a, int ch) {
+  const int sid = a.sn[blockIdx.y];
+  const int sd = a.sd0 + blockIdx.z;
+  const Supernode s = t.sn[sid];
+  if (ch >= s.nchild) return;
+  const int cid = s.child[ch];
+  const Supernode cs = t.sn[cid];
+  const int2 crc = f.rc[(int64_t)sd * t.nsn + cid];
+  const int rcc = crc.x, ccc = crc.y, nu = rcc - ccc;
+  if (nu <= 0) return;
+  const int r = f.rc[(int64_t)sd * t.nsn + sid].x;
+  double* F = split_front(t, f, a, sid, sd);
+  const double* U = split_front(t, f, a, cid, sd);
+  const int32_t* ctp = f.tpos + (int64_t)sd * t.rows_total + cs.rows_off;
+  const int64_t n = (int64_t)nu * nu;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(q % nu), y = (int)(q / nu);
+    if (x < y) continue;
+    const int px = pfx_at(f, t, sd, s, t.emap[cs.emap_off + ctp[ccc + x] - cs.ncols]);
+    const int py = pfx_at(f, t, sd, s, t.emap[cs.emap_off + ctp[ccc + y] - cs.ncols]);
+    const int row = max(px, py), col = min(px, py);
+    F[row + (int64_t)col * r] += U[(ccc + x) + (int64_t)(ccc + y) * rcc];
+  }
 }
 
 __global__ void __launch_bounds__(32) k_split_diag(TplDev t, FactorDev f, SplitArgs a, int k) {
@@ -669,7 +743,7 @@ TplDev tpl_dev(const TplSet& ts, int slots) {
 }
 
 FactorDev factor_dev(const FactorSet& f) {
-  return FactorDev{f.pfx.p, f.rc.p, f.panel_off.p, f.upd_off.p, f.upd_total};
+  return FactorDev{f.pfx.p, f.tpos.p, f.rc.p, f.panel_off.p, f.upd_off.p, f.upd_total};
 }
 
 void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
@@ -777,8 +851,9 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   const int nsd = h->nsd, nsn = t.nsn;
   // symbolic: compact rows per (sd, supernode)
   f.pfx.alloc((size_t)nsd * t.rows_total);
+  f.tpos.alloc((size_t)nsd * t.rows_total);
   f.rc.alloc((size_t)nsd * nsn);
-  k_symbolic<<<dim3(nsn, nsd), kThreads, 0, s>>>(t, nsd, in.mask, f.pfx.p, f.rc.p);
+  k_symbolic<<<dim3(nsn, nsd), kThreads, 0, s>>>(t, nsd, in.mask, f.pfx.p, f.tpos.p, f.rc.p);
   CB_LAUNCH();
   f.h_rc = f.rc.to_host(s);
   std::vector<int64_t> poff((size_t)nsd * nsn), uoff((size_t)nsd * nsn), foff((size_t)nsd * nsn);
@@ -808,16 +883,16 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   f.panel_off.upload(poff, s);
   f.upd_off.upload(uoff, s);
   f.front_off.upload(foff, s);
-  DevBuf<int64_t> fbase;
+  DevBuf<int64_t>& fbase = h->ws_fbase;
   fbase.upload(f.h_front_base, s);
   f.panel.alloc((size_t)std::max<int64_t>(1, pt));
   const FactorDev fd = factor_dev(f);
   // numeric, in subdomain chunks bounded by a front-workspace budget
   const int64_t budget = (3ll << 30) / 8;
-  DevBuf<unsigned long long> fail;
+  DevBuf<unsigned long long>& fail = h->ws_fail;
   fail.alloc(1);
   CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
-  DevBuf<double> front;
+  DevBuf<double>& front = h->ws_front;
   const int nlev = (int)ts.level_first.size();
   int sd0 = 0;
   while (sd0 < nsd) {
@@ -836,6 +911,30 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
                      fbase.p, front.p, fail.p};
         const int ns_ = ts.split_count[(size_t)L], nc_ = sd1 - sd0;
         const int maxc = ts.split_maxc[(size_t)L], maxr = ts.split_maxr[(size_t)L];
+        int max_amap = 0, max_child_nu = 0;
+        for (int sid : ts.tpl.levels[(size_t)L]) {
+          const Supernode& sn = ts.tpl.sn[(size_t)sid];
+          if (sn.nrows < kSplitRows) continue;
+          max_amap = std::max(max_amap, sn.amap_len);
+          for (int c2 = 0; c2 < sn.nchild; ++c2) {
+            const Supernode& cs = ts.tpl.sn[(size_t)sn.child[c2]];
+            max_child_nu = std::max(max_child_nu, cs.nrows - cs.ncols);
+          }
+        }
+        k_split_zero<<<dim3(64, ns_, nc_), 256, 0, s>>>(t, fd, sa);
+        CB_LAUNCH();
+        k_split_amap<<<dim3((max_amap + 255) / 256, ns_, nc_), 256, 0, s>>>(t, fd, sa, in);
+        CB_LAUNCH();
+        if (in.c_ptr && h->m_max > 0) {
+          k_split_penalty<<<dim3(h->m_max, ns_, nc_), 256, 0, s>>>(t, fd, sa, in);
+          CB_LAUNCH();
+        }
+        const int64_t pairs = (int64_t)max_child_nu * max_child_nu;
+        const int eb = (int)std::min<int64_t>(4096, (pairs + 255) / 256);
+        for (int c2 = 0; c2 < 2; ++c2) {
+          k_split_extend<<<dim3(std::max(1, eb), ns_, nc_), 256, 0, s>>>(t, fd, sa, c2);
+          CB_LAUNCH();
+        }
         for (int k = 0; k < maxc; k += 32) {
           k_split_diag<<<dim3(ns_, nc_), 32, 0, s>>>(t, fd, sa, k);
           CB_LAUNCH();
@@ -876,14 +975,21 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
 // In-place solve of nrhs x nsd slot vectors X ([rhs][sd][T]); masked-out
 // slots are left untouched. upd must hold nrhs * f.upd_total doubles.
 void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, int nrhs, double* upd,
-                  double* ysave, const int* skip) {
+                  double* ysave, const int* skip, bool rhs_root_only) {
   cudaStream_t s = h->stream;
   const TplDev t = tpl_dev(ts, h->slots);
   const FactorDev fd = factor_dev(f);
   const int nlev = (int)ts.level_first.size();
   const size_t shm = sizeof(double) * (size_t)ts.tpl.max_rows;
   const size_t shm_big = (sizeof(double) + sizeof(int)) * 2048;
+  if (rhs_root_only) {
+    // right-hand sides supported on the root columns only (C^T of the shell
+    // template): every lower forward step is zero, so only the root is swept.
+    CB_CUDA(cudaMemsetAsync(upd, 0, sizeof(double) * (size_t)nrhs * f.upd_total, s));
+    CB_CUDA(cudaMemsetAsync(ysave, 0, sizeof(double) * (size_t)nrhs * h->nsd * h->slots, s));
+  }
   for (int L = nlev - 1; L >= 0; --L) {
+    if (rhs_root_only && L > 0) continue;
     if (ts.small_count[(size_t)L] > 0) {
       dim3 grid(ts.small_count[(size_t)L], h->nsd, nrhs);
       k_fwd_level<<<grid, 256, shm, s>>>(t, fd, ts.small_sn.p + ts.small_first[(size_t)L], h->nsd, f.panel.p, X, upd,

@@ -26,6 +26,7 @@ struct TplDev {
 //   panel_off / upd_off  offsets of the compact panel / forward update vector
 struct FactorDev {
   const int32_t* pfx;
+  const int32_t* tpos;  // inverse of pfx: compact row -> template row position
   const int2* rc;
   const int64_t* panel_off;
   const int64_t* upd_off;
@@ -54,8 +55,10 @@ FactorDev factor_dev(const FactorSet& f);
 void upload_template(cutbddc_gpu* h, TplSet& t, bool shell_root);
 void factor_device(cutbddc_gpu* h, const TplSet& t, const FactorInput& in, FactorSet& f, const char* what);
 // ysave: nrhs x nsd x T doubles of scratch (forward results of big fronts).
+// rhs_root_only: the right-hand sides are nonzero only on root columns (the
+// W = K^{-1} C^T solve on the shell template); the lower forward steps are skipped.
 void solve_device(cutbddc_gpu* h, const TplSet& t, const FactorSet& f, double* X, int nrhs, double* upd,
-                  double* ysave, const int* skip);
+                  double* ysave, const int* skip, bool rhs_root_only = false);
 // algorithmic bytes of one forward + backward sweep (panel lower parts + front vectors)
 double sweep_bytes(const FactorSet& f);
 

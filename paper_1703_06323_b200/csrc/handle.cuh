@@ -51,6 +51,7 @@ struct TplSet {
 struct FactorSet {
   cutbddc_b200::DevBuf<double> panel;          // compact [L11; L21] panels
   cutbddc_b200::DevBuf<int32_t> pfx;           // nsd x rows_total
+  cutbddc_b200::DevBuf<int32_t> tpos;          // nsd x rows_total (inverse of pfx)
   cutbddc_b200::DevBuf<int2> rc;               // nsd x nsn
   cutbddc_b200::DevBuf<int64_t> panel_off, upd_off, front_off;  // nsd x nsn
   std::vector<int2> h_rc;
@@ -145,6 +146,13 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<double> partials;          // reduction partials
   cutbddc_b200::DevBuf<double> scal;              // device scalars (pcg)
   cutbddc_b200::DevBuf<int32_t> iscal;            // device int scalars (pcg)
+
+  // persistent scratch (grow-only) so repeated solves allocate nothing
+  cutbddc_b200::DevBuf<double> ws_front, ws_wall, ws_upd, ws_ys, ws_s, ws_lc, ws_q8, ws_kint;
+  cutbddc_b200::DevBuf<unsigned long long> ws_fail;
+  cutbddc_b200::DevBuf<int64_t> ws_fbase, ws_cnt, ws_nc64;
+  cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp;
+  cutbddc_b200::DevBuf<int> ws_flag;
 
   // pcg vectors
   cutbddc_b200::DevBuf<double> px, pr, pz, pp, pq, pb, hist, lal, lbe;
