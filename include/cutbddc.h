@@ -53,7 +53,9 @@ typedef struct {
   int device;      /* CUDA device ordinal */
   int rank;        /* this process' rank (multi-GPU), 0 for one GPU */
   int world_size;  /* number of GPUs (processes), 1 for one GPU */
-  const void* nccl_id; /* 128-byte ncclUniqueId (rank 0's) when world_size > 1, else NULL */
+  const void* nccl_id; /* 128-byte ncclUniqueId (rank 0's, cutbddc_nccl_unique_id); required when
+                          world_size > 1; with world_size 1 it creates a one-rank communicator
+                          (every exchange runs); NULL: no communicator */
 } cutbddc_gpu_opts;
 
 /* Background mesh + level set, MeshParams (mesh.hpp:18-24) and a union of
@@ -162,7 +164,8 @@ cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x);
  * [4]=factor panel doubles (both factorisations, all subdomains)
  * [5]=supernodes (Neumann template) [6]=levels [7]=max m_w [8]=n_interface
  * [9]=kernel launches so far (process-wide) [10]/[11]=panel doubles of the
- * interior / Neumann factorisation [12]=partial-Cholesky flops of both. */
+ * interior / Neumann factorisation [12]=partial-Cholesky flops of both
+ * [13]=world size [14]=1 if the handle owns an NCCL communicator. */
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
 /* Measurement hook: average device time of the triangular-solve sweeps of
  * one BDDC apply (interior, Neumann, interior) over `reps` repetitions, and
@@ -191,6 +194,19 @@ cutbddc_status cutbddc_classify_objects(const cutbddc_mesh_view* mesh, const cut
                                         const uint8_t* dirichlet, int objects, int variant, const double* weights,
                                         cutbddc_objects** out);
 void cutbddc_objects_free(cutbddc_objects* o);
+
+/* Multi-GPU (one process and one handle per GPU). Subdomains are assigned
+ * to ranks in contiguous Morton-curve chunks of equal estimated cost
+ * (cost may be NULL: unit cost). rank_of_sd: n_sd outputs. */
+cutbddc_status cutbddc_assign_subdomains(const cutbddc_partition_view* part, int cells, int world, const double* cost,
+                                         int32_t* rank_of_sd);
+/* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it). */
+cutbddc_status cutbddc_nccl_unique_id(void* id128);
+/* Distributed handles: global subdomain index of each local subdomain (the
+ * local partition view holds this rank's block ids, ascending). Must be
+ * called after cutbddc_gpu_assemble and before cutbddc_gpu_setup_bddc; the
+ * coarse view then refers to global subdomain indices. */
+cutbddc_status cutbddc_gpu_set_global_ids(cutbddc_gpu* h, int n_sd_global, const int32_t* global_of_local);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,18 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NO_FMA = {"geometry.cu", "element.cu"}
 CU = ["geometry.cu", "element.cu", "assembly.cu", "factor.cu", "bddc.cu", "pcg.cu", "capi.cu"]
 CPP = ["nd_template.cpp", "host_partition.cpp"]
+def _nccl_dir() -> str:
+    """NCCL of the torch wheel (the one torch itself loads: one libnccl per process)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (list(spec.submodule_search_locations) if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("NCCL headers not found (nvidia-nccl wheel)")
+
+
+NCCL = _nccl_dir()
 HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh"))] + [
     os.path.join(ROOT, "include", "cutbddc.h")]
 
@@ -41,7 +53,7 @@ def _run(cmd):
 
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
+    inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(NCCL, "include")]
     jobs = []
     objs = []
     for f in CU:
@@ -64,7 +76,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for o in outs:
             sys.stdout.write(o)
     if jobs or not os.path.exists(LIB):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"])
+        lib = os.path.join(NCCL, "lib")
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
+             ["-lcudart", "-L" + lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib])
     return LIB
 
 

@@ -68,8 +68,10 @@ __device__ inline const double* elem_k(const MeshArgs& m, int64_t cell, const do
   return m.ke + (int64_t)e * 64;
 }
 
-// per dof: |neigh| (distinct blocks among incident active cells), orphan flag
-__global__ void k_dof_info(int64_t ndof, MeshArgs m, uint8_t* __restrict__ ncount, uint8_t* __restrict__ orphan) {
+// per dof: |neigh| (distinct blocks among incident active cells), how many of
+// them are this handle's subdomains, orphan flag
+__global__ void k_dof_info(int64_t ndof, MeshArgs m, uint8_t* __restrict__ ncount, uint8_t* __restrict__ lcount,
+                           uint8_t* __restrict__ orphan) {
   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (d >= ndof) return;
   const int n = m.n;
@@ -92,7 +94,10 @@ __global__ void k_dof_info(int64_t ndof, MeshArgs m, uint8_t* __restrict__ ncoun
         for (int q = 0; q < nbk; ++q) seen |= blks[q] == bid;
         if (!seen) blks[nbk++] = bid;
       }
+  int nloc = 0;
+  for (int q = 0; q < nbk; ++q) nloc += m.sd_of_block[blks[q]] >= 0;
   ncount[d] = (uint8_t)nbk;
+  lcount[d] = (uint8_t)nloc;
   orphan[d] = !nonvoid;
 }
 
@@ -191,8 +196,8 @@ __global__ void k_subassemble(int nsd, MeshArgs m, const int64_t* __restrict__ b
   for (int q = 0; q < 27; ++q) A[(int64_t)q * T] = acc[q];
 }
 
-// per dof: its (subdomain, slot) copies in ascending subdomain order; owner
-// slot for interior dofs.
+// per dof: its (subdomain, slot) copies in this handle's subdomains, ascending
+// subdomain order; owner slot for interior dofs of this handle's subdomains.
 __global__ void k_copies(int64_t ndof, MeshArgs m, const int64_t* __restrict__ copy_ptr, int64_t* __restrict__ copy_idx,
                          int64_t* __restrict__ owner) {
   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -220,14 +225,17 @@ __global__ void k_copies(int64_t ndof, MeshArgs m, const int64_t* __restrict__ c
       blks[c] = blks[c - 1];
       blks[c - 1] = tmp;
     }
-  int64_t p = copy_ptr[d];
+  const int64_t p = copy_ptr[d];
+  int nloc = 0;
   for (int q = 0; q < nbk; ++q) {
     const int64_t bid = blks[q];
+    const int32_t sd = m.sd_of_block[bid];
+    if (sd < 0) continue;  // another rank's subdomain
     const int bi = (int)(bid / m.nb / m.nb), bj = (int)((bid / m.nb) % m.nb), bk = (int)(bid % m.nb);
     const int slot = ((i - bi * B) * b1 + (j - bj * B)) * b1 + (k - bk * B);
-    copy_idx[p + q] = (int64_t)m.sd_of_block[bid] * m.T + slot;
+    copy_idx[p + nloc++] = (int64_t)sd * m.T + slot;
   }
-  owner[d] = nbk == 1 ? copy_idx[p] : -1;
+  owner[d] = nbk == 1 && nloc == 1 ? copy_idx[p] : -1;
 }
 
 __global__ void k_u8_to_i64(int64_t n, const uint8_t* __restrict__ a, int64_t* __restrict__ b) {
@@ -251,6 +259,8 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
   h->slots = h->b1 * h->b1 * h->b1;
   h->nb = n / block;
   h->nsd = nsd;
+  h->nsd_global = 0;  // local numbering until cutbddc_gpu_set_global_ids
+  h->global_of_local.clear();
   h->h_block_ids.assign(block_ids, block_ids + nsd);
   for (int i = 1; i < nsd; ++i)
     if (block_ids[i] <= block_ids[i - 1]) throw Failure(CUTBDDC_INVALID_ARGUMENT, "partition: block ids must ascend");
@@ -302,8 +312,9 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
              h->ke.p, h->fe.p, h->empty.p, kint.p, kint.p + 64, h->sd_of_block.p};
   const int64_t nd = h->n_dof;
   h->ncount.alloc((size_t)nd);
+  h->lcount.alloc((size_t)nd);
   h->orphan.alloc((size_t)nd);
-  k_dof_info<<<grid_for(nd, 256), 256, 0, s>>>(nd, m, h->ncount.p, h->orphan.p);
+  k_dof_info<<<grid_for(nd, 256), 256, 0, s>>>(nd, m, h->ncount.p, h->lcount.p, h->orphan.p);
   CB_LAUNCH();
   h->aval.alloc((size_t)nd * 27);
   h->acol.alloc((size_t)nd * 27);
@@ -318,7 +329,7 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
   // copies CSR
   DevBuf<int64_t>& nc64 = h->ws_nc64;
   nc64.alloc((size_t)nd);
-  k_u8_to_i64<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->ncount.p, nc64.p);
+  k_u8_to_i64<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->lcount.p, nc64.p);
   CB_LAUNCH();
   h->copy_ptr.alloc((size_t)nd + 1);
   CB_CUDA(cudaMemsetAsync(h->copy_ptr.p, 0, sizeof(int64_t), s));

@@ -17,6 +17,7 @@
 
 #include "bddc.cuh"
 #include "factor.cuh"
+#include "comm.cuh"
 #include "dense_chol.cuh"
 #include "subst.cuh"
 
@@ -32,10 +33,23 @@ __global__ void k_masks(int64_t ns, const int32_t* __restrict__ slot_dof, const 
   mint[g] = d >= 0 && ncount[d] == 1;
 }
 
+// per dof: sum of the A^w diagonals over this handle's copies, ascending sd
+// (the stiffness-weight denominator; all-reduced over ranks when distributed)
+__global__ void k_dtot(int64_t nd, int T, const double* __restrict__ As, const int64_t* __restrict__ copy_ptr,
+                       const int64_t* __restrict__ copy_idx, double* __restrict__ tot) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  double s = 0.0;
+  for (int64_t p = copy_ptr[d]; p < copy_ptr[d + 1]; ++p) {
+    const int64_t ci = copy_idx[p];
+    s += As[(ci / T) * 27 * T + 13ll * T + ci % T];
+  }
+  tot[d] = s;
+}
+
 __global__ void k_weights(int64_t ns, int T, int mode, const int32_t* __restrict__ slot_dof,
                           const uint8_t* __restrict__ ncount, const double* __restrict__ As,
-                          const int64_t* __restrict__ copy_ptr, const int64_t* __restrict__ copy_idx,
-                          double* __restrict__ w, int* __restrict__ bad) {
+                          const double* __restrict__ dtot, double* __restrict__ w, int* __restrict__ bad) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ns) return;
   const int32_t d = slot_dof[g];
@@ -52,15 +66,13 @@ __global__ void k_weights(int64_t ns, int T, int mode, const int32_t* __restrict
     w[g] = 1.0 / (double)k;
     return;
   }
-  auto diag = [&](int64_t ci) { return As[(ci / T) * 27 * T + 13ll * T + ci % T]; };
-  double tot = 0.0;
-  for (int64_t p = copy_ptr[d]; p < copy_ptr[d + 1]; ++p) tot += diag(copy_idx[p]);
+  const double tot = dtot[d];
   if (!(tot != 0.0)) {
     atomicExch(bad, 1);
     w[g] = 0.0;
     return;
   }
-  w[g] = diag(g) / tot;
+  w[g] = As[(g / T) * 27 * T + 13ll * T + g % T] / tot;
 }
 
 // rho_w = mean of diag(A_w) over the subdomain's local dofs, summed
@@ -448,6 +460,26 @@ __global__ void k_final_z(int64_t nd, const int64_t* __restrict__ owner, const d
   z[d] = z0[d] + v[d] - (o >= 0 ? X[o] : 0.0);
 }
 
+// distributed form of k_final_z: c[d] = -X[owner] on this rank's interior
+// dofs (all-reduced: each interior dof has exactly one owner), then
+// z = (z0 + v) + c, which equals z0 + v - X[owner] bit for bit.
+__global__ void k_owned_neg(int64_t nd, const int64_t* __restrict__ owner, const double* __restrict__ X,
+                            double* __restrict__ c, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  const int64_t o = owner[d];
+  c[d] = o >= 0 ? -X[o] : 0.0;
+}
+
+__global__ void k_final_sum(int64_t nd, const double* __restrict__ z0, const double* __restrict__ v,
+                            const double* __restrict__ c, double* __restrict__ z, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  z[d] = z0[d] + v[d] + c[d];
+}
+
 __global__ void k_row_sd(int nsd, const int64_t* __restrict__ m_off, int32_t* __restrict__ row_sd) {
   const int sd = blockIdx.x;
   for (int64_t r = m_off[sd] + threadIdx.x; r < m_off[sd + 1]; r += blockDim.x) row_sd[r] = sd;
@@ -470,11 +502,17 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   const int nc = cv ? cv->n_objects : 0;
   std::vector<int64_t> node_of_dof = h->node_of_dof.to_host(s);
   std::vector<std::vector<int>> rows_of_sd((size_t)nsd);  // object ids per sd (coarse order)
+  // the coarse view names global subdomains; keep the rows of this rank's
+  const int nsd_g = h->nsd_global > 0 ? h->nsd_global : nsd;
+  std::vector<int32_t> local_of_global((size_t)nsd_g, -1);
+  for (int sd = 0; sd < nsd; ++sd)
+    local_of_global[(size_t)(h->nsd_global > 0 ? h->global_of_local[(size_t)sd] : sd)] = sd;
   for (int o = 0; o < nc; ++o)
     for (int64_t p = cv->neigh_ptr[o]; p < cv->neigh_ptr[o + 1]; ++p) {
-      const int sd = cv->neigh[p];
-      if (sd < 0 || sd >= nsd) throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: neighbour subdomain out of range");
-      rows_of_sd[(size_t)sd].push_back(o);
+      const int sg = cv->neigh[p];
+      if (sg < 0 || sg >= nsd_g) throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: neighbour subdomain out of range");
+      const int sd = local_of_global[(size_t)sg];
+      if (sd >= 0) rows_of_sd[(size_t)sd].push_back(o);
     }
   std::vector<int64_t> m_off((size_t)nsd + 1, 0), c_ptr{0};
   std::vector<int32_t> c_slot, coarse_id;
@@ -544,8 +582,14 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   bad.alloc(1);
   bad.zero(s);
   h->w.alloc((size_t)ns);
-  k_weights<<<grid_for(ns, 256), 256, 0, s>>>(ns, T, weighting, h->slot_dof.p, h->ncount.p, h->As.p, h->copy_ptr.p,
-                                              h->copy_idx.p, h->w.p, bad.p);
+  h->dtot.alloc((size_t)h->n_dof);
+  if (weighting == CUTBDDC_WEIGHT_STIFFNESS) {
+    k_dtot<<<grid_for(h->n_dof, 256), 256, 0, s>>>(h->n_dof, T, h->As.p, h->copy_ptr.p, h->copy_idx.p, h->dtot.p);
+    CB_LAUNCH();
+    allreduce_sum(h, h->dtot.p, (size_t)h->n_dof);
+  }
+  k_weights<<<grid_for(ns, 256), 256, 0, s>>>(ns, T, weighting, h->slot_dof.p, h->ncount.p, h->As.p, h->dtot.p, h->w.p,
+                                              bad.p);
   CB_LAUNCH();
   h->mask_all.alloc((size_t)ns);
   h->mask_int.alloc((size_t)ns);
@@ -633,6 +677,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     k_coarse_assemble<<<nc, 128, 0, s>>>(nc, h->cg_ptr.p, h->cg_idx.p, h->row_sd.p, h->m_off.p, h->ac_off.p,
                                          h->coarse_id.p, h->ac_loc.p, h->acoarse.p);
     CB_LAUNCH();
+    allreduce_sum(h, h->acoarse.p, (size_t)nc * nc);  // SPEC.md:386 sum over all subdomains
     // Cholesky panel of A_c (column-major), then the explicit inverse by
     // parallel column solves; the apply multiplies by it (one GEMV).
     DevBuf<double>& Lc = h->ws_lc;
@@ -663,6 +708,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->gv0.alloc((size_t)h->n_dof);
   h->gv1.alloc((size_t)h->n_dof);
   h->gv2.alloc((size_t)h->n_dof);
+  if (distributed(h)) h->gv3.alloc((size_t)h->n_dof);
   h->gl.alloc((size_t)std::max<int64_t>(1, h->m_total));
   h->cy.alloc((size_t)std::max<int64_t>(1, h->m_total));
   h->zc.alloc((size_t)std::max(1, nc));
@@ -681,6 +727,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, skip);
   k_z0<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv0.p, skip);
   CB_LAUNCH();
+  allreduce_sum(h, h->gv0.p, (size_t)nd);  // one owner per interior dof: exact
   k_r1<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->ncount.p, h->aval.p, h->acol.p, r, h->gv0.p, h->gv1.p, skip);
   CB_LAUNCH();
   k_scatter_weighted<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->w.p, h->gv1.p, h->sv1.p, skip);
@@ -696,6 +743,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     CB_LAUNCH();
     k_coarse_rhs<<<grid_for(h->n_coarse, 128), 128, 0, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->gc.p, skip);
     CB_LAUNCH();
+    allreduce_sum(h, h->gc.p, (size_t)h->n_coarse);
     k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_inv.p, h->gc.p,
                                                                          h->zc.p, skip);
     CB_LAUNCH();
@@ -705,12 +753,21 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   }
   k_gather_weighted<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->copy_ptr.p, h->copy_idx.p, h->w.p, h->sv1.p, h->gv2.p, skip);
   CB_LAUNCH();
+  allreduce_sum(h, h->gv2.p, (size_t)nd);
   k_interior_av<<<grid_for(ns, 256), 256, 0, s>>>(ns, nd, h->slot_dof.p, h->mask_int.p, h->aval.p, h->acol.p, h->gv2.p,
                                                   h->sv0.p, skip);
   CB_LAUNCH();
   solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, skip);
-  k_final_z<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->gv0.p, h->gv2.p, h->sv0.p, z, skip);
-  CB_LAUNCH();
+  if (distributed(h)) {
+    k_owned_neg<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv3.p, skip);
+    CB_LAUNCH();
+    allreduce_sum(h, h->gv3.p, (size_t)nd);
+    k_final_sum<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->gv0.p, h->gv2.p, h->gv3.p, z, skip);
+    CB_LAUNCH();
+  } else {
+    k_final_z<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->gv0.p, h->gv2.p, h->sv0.p, z, skip);
+    CB_LAUNCH();
+  }
 }
 
 }  // namespace cutbddc_b200

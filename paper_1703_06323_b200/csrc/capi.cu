@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "bddc.cuh"
+#include "comm.cuh"
 #include "factor.cuh"
 
 namespace cutbddc_b200 {
@@ -56,14 +57,29 @@ cutbddc_status cutbddc_gpu_create(const cutbddc_gpu_opts* opts, cutbddc_gpu** ou
       h->device = opts ? opts->device : 0;
       h->rank = opts ? opts->rank : 0;
       h->world = opts ? opts->world_size : 1;
-      if (h->world != 1)
-        throw Failure(CUTBDDC_CONFIG, "multi-GPU handles are driven by the host layer (one handle per rank)");
+      if (h->world < 1 || h->rank < 0 || h->rank >= h->world)
+        throw Failure(CUTBDDC_INVALID_ARGUMENT, "rank / world_size out of range");
+      const void* id = opts ? opts->nccl_id : nullptr;
+      if (h->world > 1 && !id) throw Failure(CUTBDDC_CONFIG, "world_size > 1 needs the rank-0 NCCL unique id");
       int ndev = 0;
       CB_CUDA(cudaGetDeviceCount(&ndev));
       if (h->device < 0 || h->device >= ndev) throw Failure(CUTBDDC_INVALID_ARGUMENT, "device ordinal out of range");
       CB_CUDA(cudaSetDevice(h->device));
       CB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      if (id) {
+        // one communicator per handle; a world of 1 exercises every exchange
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        nccl_check(ncclCommInitRank(&h->comm, h->world, uid, h->rank), "init");
+        // first collective outside any stream capture (connection setup)
+        DevBuf<double> one;
+        one.alloc(1);
+        one.zero(h->stream);
+        allreduce_sum(h, one.p, 1);
+        CB_CUDA(cudaStreamSynchronize(h->stream));
+      }
     } catch (...) {
+      if (h->stream) cudaStreamDestroy(h->stream);
       delete h;
       throw;
     }
@@ -76,8 +92,35 @@ void cutbddc_gpu_destroy(cutbddc_gpu* h) {
   cudaSetDevice(h->device);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm) ncclCommDestroy(h->comm);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
+}
+
+cutbddc_status cutbddc_nccl_unique_id(void* id128) {
+  return guard([&] {
+    if (!id128) throw Failure(CUTBDDC_INVALID_ARGUMENT, "null id buffer");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId uid;
+    nccl_check(ncclGetUniqueId(&uid), "unique id");
+    std::memcpy(id128, &uid, sizeof(uid));
+  });
+}
+
+cutbddc_status cutbddc_gpu_set_global_ids(cutbddc_gpu* h, int n_sd_global, const int32_t* global_of_local) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "set_global_ids: assemble first");
+    if (!global_of_local || n_sd_global < h->nsd) throw Failure(CUTBDDC_INVALID_ARGUMENT, "set_global_ids: bad ids");
+    std::vector<int32_t> g(global_of_local, global_of_local + h->nsd);
+    for (int i = 0; i < h->nsd; ++i)
+      if (g[(size_t)i] < 0 || g[(size_t)i] >= n_sd_global || (i && g[(size_t)i] <= g[(size_t)i - 1]))
+        throw Failure(CUTBDDC_INVALID_ARGUMENT, "set_global_ids: ids must ascend within [0, n_sd_global)");
+    h->nsd_global = n_sd_global;
+    h->global_of_local = std::move(g);
+    h->bddc_ready = false;
+  });
 }
 
 cutbddc_status cutbddc_gpu_classify(cutbddc_gpu* h, const cutbddc_geometry* g, double* phi, uint8_t* cls,
@@ -341,6 +384,8 @@ cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {
     st[10] = h->fI.panel_total;
     st[11] = h->fK.panel_total;
     st[12] = (int64_t)(h->fI.flops + h->fK.flops);
+    st[13] = h->world;
+    st[14] = h->comm != nullptr;
   });
 }
 

@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <mutex>
 #include <vector>
@@ -66,6 +67,13 @@ struct cutbddc_gpu {
   cudaStream_t stream = nullptr;
   std::mutex mu;
 
+  // ---------------------------------------------------------------- multi-GPU
+  // Subdomains are distributed over ranks; global dof vectors are replicated.
+  // comm == nullptr: one process owns every subdomain (no collectives).
+  ncclComm_t comm = nullptr;
+  int nsd_global = 0;                            // 0: local == global numbering
+  std::vector<int32_t> global_of_local;          // nsd
+
   // ---------------------------------------------------------------- mesh
   int n = 0;                   // cells per axis
   double origin[3] = {0, 0, 0}, h = 0, tol = 0;
@@ -91,7 +99,9 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int32_t> sd_of_block;     // nb^3, -1 for empty blocks
   cutbddc_b200::DevBuf<int32_t> slot_dof;        // nsd*T
   cutbddc_b200::DevBuf<double> As;               // nsd*27*T
-  cutbddc_b200::DevBuf<uint8_t> ncount, orphan;  // per dof
+  cutbddc_b200::DevBuf<uint8_t> ncount, orphan;  // per dof (ncount over all ranks' subdomains)
+  cutbddc_b200::DevBuf<uint8_t> lcount;          // per dof: copies in this rank's subdomains
+  cutbddc_b200::DevBuf<double> dtot;             // per dof: sum of A^w diagonals over all copies
   cutbddc_b200::DevBuf<int64_t> copy_ptr;        // n_dof+1
   cutbddc_b200::DevBuf<int64_t> copy_idx;        // sd*T + slot, ascending sd
   int64_t n_copies = 0;
@@ -141,7 +151,7 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<double> sv0, sv1, sv2;     // slot vectors nsd*T
   cutbddc_b200::DevBuf<double> ysave;             // big-front forward results, nsd*T
   cutbddc_b200::DevBuf<double> upd;               // solve workspace nsd*upd_total (x nrhs for setup)
-  cutbddc_b200::DevBuf<double> gv0, gv1, gv2;     // global vectors n_dof
+  cutbddc_b200::DevBuf<double> gv0, gv1, gv2, gv3;  // global vectors n_dof
   cutbddc_b200::DevBuf<double> gl, cy, zc, gc;    // m_total, m_total, n_coarse, n_coarse
   cutbddc_b200::DevBuf<double> partials;          // reduction partials
   cutbddc_b200::DevBuf<double> scal;              // device scalars (pcg)

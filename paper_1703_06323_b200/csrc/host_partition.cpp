@@ -342,3 +342,40 @@ extern "C" void cutbddc_objects_free(cutbddc_objects* o) {
   delete[] o->neigh;
   delete o;
 }
+
+// Multi-GPU assignment: nonempty subdomains ordered
+// along a Morton curve over their block coordinates, cut into `world`
+// contiguous chunks of (nearly) equal estimated cost. cost[s] may be NULL
+// (unit cost). rank_of_sd[s] receives the rank of global subdomain s.
+extern "C" cutbddc_status cutbddc_assign_subdomains(const cutbddc_partition_view* part, int cells, int world,
+                                                    const double* cost, int32_t* rank_of_sd) {
+  return guard([&] {
+    if (!part || part->n_sd < 1 || world < 1) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assign: empty partition");
+    const int nb = cells / part->block;
+    auto morton = [](uint32_t x, uint32_t y, uint32_t z) {
+      uint64_t key = 0;
+      for (int b = 0; b < 21; ++b) {
+        key |= (uint64_t)((x >> b) & 1) << (3 * b + 2);
+        key |= (uint64_t)((y >> b) & 1) << (3 * b + 1);
+        key |= (uint64_t)((z >> b) & 1) << (3 * b);
+      }
+      return key;
+    };
+    std::vector<std::pair<uint64_t, int>> order;
+    for (int s = 0; s < part->n_sd; ++s) {
+      const int64_t b = part->block_ids[s];
+      order.emplace_back(morton((uint32_t)(b / nb / nb), (uint32_t)((b / nb) % nb), (uint32_t)(b % nb)), s);
+    }
+    std::sort(order.begin(), order.end());
+    double total = 0;
+    for (int s = 0; s < part->n_sd; ++s) total += cost ? cost[s] : 1.0;
+    double acc = 0;
+    for (auto& [key, s] : order) {
+      const double c = cost ? cost[s] : 1.0;
+      // rank by the midpoint of this subdomain's cost interval
+      int r = (int)((acc + 0.5 * c) / total * world);
+      rank_of_sd[s] = std::min(world - 1, std::max(0, r));
+      acc += c;
+    }
+  });
+}

@@ -75,6 +75,7 @@ EXPORTS = [
     "cutbddc_gpu_apply_bddc", "cutbddc_gpu_rhs", "cutbddc_gpu_coarse_matrix", "cutbddc_gpu_cells", "cutbddc_gpu_stats",
     "cutbddc_gpu_cut_elements", "cutbddc_gpu_local_system", "cutbddc_gpu_local_solve", "cutbddc_gpu_time_solves",
     "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free",
+    "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_global_ids",
 ]
 
 
@@ -178,15 +179,44 @@ def classify_objects(mesh: Mesh, block: int, block_ids: np.ndarray, dirichlet: n
     return Objects(kinds.astype(np.int32), dptr, dofs.astype(np.int32), nptr, neigh.astype(np.int32))
 
 
-class GpuSolver:
-    """One device handle: geometry -> classify -> assemble -> setup -> pcg."""
+def assign_subdomains(block: int, block_ids: np.ndarray, cells: int, world: int,
+                      cost: np.ndarray | None = None) -> np.ndarray:
+    """Rank of every (global) subdomain: contiguous Morton-curve chunks of
+    equal estimated cost."""
+    block_ids = np.ascontiguousarray(block_ids, np.int64)
+    pv = _PartView(block, len(block_ids), _p(block_ids, C.c_int64))
+    out = np.zeros(len(block_ids), np.int32)
+    cp = _p(np.ascontiguousarray(cost, np.float64), C.c_double) if cost is not None else None
+    _check(lib().cutbddc_assign_subdomains(C.byref(pv), cells, world, cp, _p(out, C.c_int32)))
+    return out
 
-    def __init__(self, device: int = 0):
-        o = _Opts(device, 0, 1, None)
+
+def nccl_unique_id() -> bytes:
+    """Rank 0 creates the 128-byte NCCL id; the caller broadcasts it."""
+    buf = C.create_string_buffer(128)
+    _check(lib().cutbddc_nccl_unique_id(buf))
+    return buf.raw
+
+
+class GpuSolver:
+    """One device handle: geometry -> classify -> assemble -> setup -> pcg.
+
+    Multi-GPU: one handle per rank, created with the rank-0 NCCL id; each
+    rank assembles its own subdomains (assemble with the local block ids, then
+    set_global_ids) and every call is collective over the ranks."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        o = _Opts(device, rank, world, C.addressof(self._id) if self._id is not None else None)
         h = C.c_void_p()
         _check(lib().cutbddc_gpu_create(C.byref(o), C.byref(h)))
         self.h = h
         self.n_dof = 0
+        self.rank, self.world = rank, world
+
+    def set_global_ids(self, n_sd_global: int, global_of_local: np.ndarray):
+        g = np.ascontiguousarray(global_of_local, np.int32)
+        _check(lib().cutbddc_gpu_set_global_ids(self.h, n_sd_global, _p(g, C.c_int32)))
 
     def close(self):
         if getattr(self, "h", None):
@@ -318,13 +348,14 @@ class GpuSolver:
         of one BDDC apply) and its algorithmic bytes."""
         sec, byt = C.c_double(), C.c_double()
         _check(lib().cutbddc_gpu_time_solves(self.h, reps, C.byref(sec), C.byref(byt)))
-        return dict(kernel="k_fwd_level+k_bwd_level (3 solves of one BDDC apply)", seconds=sec.value, bytes=byt.value)
+        return dict(kernel="k_fwd_big+k_bwd_big+k_fwd_level+k_bwd_level (3 front solves of one BDDC apply)",
+                    seconds=sec.value, bytes=byt.value)
 
     def stats(self):
         st = np.zeros(16, np.int64)
         _check(lib().cutbddc_gpu_stats(self.h, _p(st, C.c_int64)))
         keys = ["n_dof", "n_sd", "n_coarse", "slots", "panel_total", "n_supernodes", "levels", "m_max", "n_if",
-                "launches", "panel_interior", "panel_neumann", "factor_flops"]
+                "launches", "panel_interior", "panel_neumann", "factor_flops", "world", "has_comm"]
         return {k: int(st[i]) for i, k in enumerate(keys)}
 
 
@@ -346,6 +377,37 @@ def prepare(solver: GpuSolver, cfg) -> Problem:
     diag = solver.local_diagonals() if cfg.variant == _cfg.V2 else None
     objs = classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, diag)
     return Problem(cfg, mesh, block_ids, dirichlet, objs)
+
+
+@dataclass
+class LocalPart:
+    """This rank's share of the global partition."""
+    rank_of_sd: np.ndarray     # per global subdomain
+    local_sd: np.ndarray       # global indices of this rank's subdomains, ascending
+    local_block_ids: np.ndarray
+
+
+def local_part(block: int, block_ids: np.ndarray, cells: int, rank: int, world: int) -> LocalPart:
+    rank_of_sd = assign_subdomains(block, block_ids, cells, world)
+    local_sd = np.flatnonzero(rank_of_sd == rank).astype(np.int32)
+    if len(local_sd) == 0:
+        raise CutbddcError(CONFIG, f"rank {rank} received no subdomain ({len(block_ids)} subdomains, {world} ranks)")
+    return LocalPart(rank_of_sd, local_sd, np.ascontiguousarray(block_ids[local_sd], np.int64))
+
+
+def prepare_distributed(solver: GpuSolver, cfg) -> tuple[Problem, LocalPart]:
+    """prepare() for one rank of a multi-GPU solve: the mesh, partition and
+    objects are built identically on every rank (host work, replicated);
+    the device work is split by subdomain."""
+    if cfg.variant == _cfg.V2:
+        raise CutbddcError(CONFIG, "variant v2 needs every subdomain's diagonals; not supported distributed")
+    mesh = solver.classify(cfg)
+    block_ids = build_partition(mesh, cfg.block)
+    lp = local_part(cfg.block, block_ids, cfg.cells, solver.rank, solver.world)
+    dirichlet = solver.assemble(cfg.block, lp.local_block_ids)
+    solver.set_global_ids(len(block_ids), lp.local_sd)
+    objs = classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, None)
+    return Problem(cfg, mesh, block_ids, dirichlet, objs), lp
 
 
 def solve(cfg, device: int = 0):

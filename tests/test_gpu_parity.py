@@ -154,3 +154,23 @@ def test_one_subdomain_exact():
     s.setup_bddc(pb.objects, cfg.weighting)
     x, rep = s.pcg(rtol=cfg.rtol)
     assert rep["iterations"] == 1
+
+
+def test_nccl_world1_bit_identical(cfg2s):
+    """The distributed code path (NCCL communicator, global subdomain ids,
+    split weighting / coarse / apply reductions) on a one-rank world must
+    reproduce the single-process path bit for bit."""
+    cfg, o, s, pb = cfg2s
+    d = cb.GpuSolver(0, rank=0, world=1, nccl_id=cb.nccl_unique_id())
+    pbd, lp = cb.prepare_distributed(d, cfg)
+    assert np.array_equal(lp.local_sd, np.arange(len(pb.block_ids)))
+    d.setup_bddc(pbd.objects, cfg.weighting)
+    assert d.stats()["has_comm"] == 1 and s.stats()["has_comm"] == 0
+    assert np.array_equal(d.coarse_matrix(), s.coarse_matrix())
+    r = np.random.default_rng(11).uniform(-1, 1, o.n_dof)
+    assert np.array_equal(d.apply(r), s.apply(r))
+    x1, r1 = s.pcg(rtol=cfg.rtol)
+    x2, r2 = d.pcg(rtol=cfg.rtol)
+    assert r1["iterations"] == r2["iterations"]
+    assert np.array_equal(r1["residuals"], r2["residuals"]) and np.array_equal(x1, x2)
+    d.close()
