@@ -267,6 +267,7 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
   h->block_ids.upload(h->h_block_ids, s);
   const int64_t nc = h->n_cells;
   const int grid = 148 * 8;
+  ProfScope ps(h->prof, s, "assembly 1 cell lists");
   // active / cut cell lists (ascending)
   DevBuf<uint8_t>& act = h->ws_act;
   DevBuf<uint8_t>& cut = h->ws_cut;
@@ -299,11 +300,13 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
     CB_LAUNCH();
   }
   // element matrices
+  ps.next("assembly 2 cut elements");
   cut_elements_device(h);
   DevBuf<double>& kint = h->ws_kint;
   kint.alloc(72);
   interior_element_device(h, kint.p, kint.p + 64);
   // subdomain maps
+  ps.next("assembly 3 abar+subassembly+copies");
   h->sd_of_block.alloc((size_t)h->nb * h->nb * h->nb);
   CB_CUDA(cudaMemsetAsync(h->sd_of_block.p, 0xff, h->sd_of_block.n * 4, s));
   k_sd_of_block<<<grid_for(nsd, 256), 256, 0, s>>>(nsd, h->block_ids.p, h->sd_of_block.p);

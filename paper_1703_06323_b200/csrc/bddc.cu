@@ -499,6 +499,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     h->graph_exec = nullptr;
   }
   // ---- host: constraint rows per subdomain from the coarse objects
+  ProfScope ps_host(h->prof, s, "setup 0 host rows+uploads+weights");
   const int nc = cv ? cv->n_objects : 0;
   std::vector<int64_t> node_of_dof = h->node_of_dof.to_host(s);
   std::vector<std::vector<int>> rows_of_sd((size_t)nsd);  // object ids per sd (coarse order)
@@ -606,6 +607,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   CB_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
   if (hbad) throw Failure(CUTBDDC_DEGENERATE, "weighting: zero total diagonal at an interface dof");
+  ps_host.next("setup 1 factorisations");
   // ---- factorisations
   if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);
   FactorInput fi{h->As.p, h->mask_int.p, nullptr, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -625,6 +627,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   // ---- coarse basis
   h->phi_c.alloc((size_t)std::max<int64_t>(1, h->m_total) * T);
   h->ac_loc.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
+  ps_host.next("setup 2 W = K^-1 C^T");
   if (m_max > 0) {
     DevBuf<double>& Wall = h->ws_wall;
     DevBuf<double>& upd = h->ws_upd;
@@ -641,6 +644,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
       CB_LAUNCH();
       solve_device(h, h->tK, h->fK, X, nr, upd.p, ys.p, nullptr, /*rhs_root_only=*/true);
     }
+    ps_host.next("setup 3 schur+phi+local coarse");
     DevBuf<double>& S = h->ws_s;
     S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
     k_schur<<<nsd, 256, 0, s>>>(nsd, T, h->m_off.p, h->ac_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, Wall.p, S.p);
@@ -670,6 +674,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     CB_LAUNCH();
   }
   // ---- coarse matrix + factorisation
+  ps_host.next("setup 4 coarse assemble+chol+inverse");
   h->acoarse.alloc((size_t)std::max(1, nc * nc));
   h->acoarse_inv.alloc((size_t)std::max(1, nc * nc));
   if (nc > 0) {
@@ -701,6 +706,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
       throw Failure(CUTBDDC_SINGULAR, "coarse matrix: not positive definite (pivot index " + std::to_string(f) + ")");
   }
   // ---- work vectors
+  ps_host.next("setup 5 work vectors");
   h->sv0.alloc((size_t)ns);
   h->sv1.alloc((size_t)ns);
   h->upd.alloc((size_t)upd_total);
@@ -722,9 +728,12 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   cudaStream_t s = h->stream;
   const int64_t nd = h->n_dof, ns = (int64_t)h->nsd * h->slots;
   const int T = h->slots;
+  ProfScope ps(h->prof, s, "apply vec 1 gather");
   k_gather_masked<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->mask_int.p, r, h->sv0.p, skip);
   CB_LAUNCH();
+  ps.close();
   solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, skip);
+  ps.next("apply vec 2 z0 r1 scatter phit");
   k_z0<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv0.p, skip);
   CB_LAUNCH();
   allreduce_sum(h, h->gv0.p, (size_t)nd);  // one owner per interior dof: exact
@@ -736,7 +745,9 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     k_phit<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->phi_c.p, h->sv1.p, h->gl.p, skip);
     CB_LAUNCH();
   }
+  ps.close();
   if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
+  ps.next("apply vec 3 cy coarse prolong gather Av");
   if (h->m_total > 0) {
     k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
                                                        h->sv1.p, h->cy.p, skip);
@@ -757,7 +768,9 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   k_interior_av<<<grid_for(ns, 256), 256, 0, s>>>(ns, nd, h->slot_dof.p, h->mask_int.p, h->aval.p, h->acol.p, h->gv2.p,
                                                   h->sv0.p, skip);
   CB_LAUNCH();
+  ps.close();
   solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, skip);
+  ps.next("apply vec 4 final");
   if (distributed(h)) {
     k_owned_neg<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv3.p, skip);
     CB_LAUNCH();

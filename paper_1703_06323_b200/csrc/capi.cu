@@ -92,6 +92,7 @@ void cutbddc_gpu_destroy(cutbddc_gpu* h) {
   cudaSetDevice(h->device);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  h->prof.dump();
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;

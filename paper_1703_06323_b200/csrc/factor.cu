@@ -19,6 +19,7 @@
 // (subst.cuh). Non-positive pivots are reported with the offending
 // (subdomain, slot) — the pivot rule of linalg.cpp:42-54.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "dense_chol.cuh"
@@ -601,6 +602,9 @@ __global__ void __launch_bounds__(256) k_bwd_level(TplDev t, FactorDev f, const 
 // panels and multi-CTA GEMV sweeps; all fronts do (measured: the blocked
 // substitution path was latency-bound at every level).
 constexpr int kBigMinCols = 1;
+// ND leaf size: boxes of at most this many lattice nodes are leaf fronts
+// (CUTBDDC_LEAF overrides, for measurements).
+constexpr int kLeafMax = 125;  // cfg4: 27 -> 125 cut the apply's solve time 744 -> 668 us
 constexpr int kBigRows = 32;   // forward: rows per CTA (one row per lane)
 constexpr int kBigCols = 16;   // backward: columns per CTA (two per warp)
 
@@ -748,7 +752,11 @@ FactorDev factor_dev(const FactorSet& f) {
 
 void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
   cudaStream_t s = h->stream;
-  ts.tpl = build_template(h->block, 27, shell_root);
+  static const int leaf = [] {
+    const char* e = std::getenv("CUTBDDC_LEAF");
+    return e ? std::max(8, std::atoi(e)) : kLeafMax;
+  }();
+  ts.tpl = build_template(h->block, leaf, shell_root);
   if (ts.tpl.max_rows > 2048) throw Failure(CUTBDDC_CONFIG, "nd template: front larger than 2048 rows");
   ts.sn.upload(ts.tpl.sn, s);
   ts.rows.upload(ts.tpl.rows, s);
@@ -853,6 +861,7 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   f.pfx.alloc((size_t)nsd * t.rows_total);
   f.tpos.alloc((size_t)nsd * t.rows_total);
   f.rc.alloc((size_t)nsd * nsn);
+  ProfScope psym(h->prof, s, std::string("factor") + (&ts == &h->tI ? "I" : "K") + " total");
   k_symbolic<<<dim3(nsn, nsd), kThreads, 0, s>>>(t, nsd, in.mask, f.pfx.p, f.tpos.p, f.rc.p);
   CB_LAUNCH();
   f.h_rc = f.rc.to_host(s);
@@ -886,6 +895,7 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   DevBuf<int64_t>& fbase = h->ws_fbase;
   fbase.upload(f.h_front_base, s);
   f.panel.alloc((size_t)std::max<int64_t>(1, pt));
+  build_sweep_plan(h, ts, f, poff, uoff);
   const FactorDev fd = factor_dev(f);
   // numeric, in subdomain chunks bounded by a front-workspace budget
   const int64_t budget = (3ll << 30) / 8;
@@ -900,13 +910,16 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
     while (sd1 < nsd && f.h_front_base[(size_t)sd1 + 1] - f.h_front_base[(size_t)sd0] <= budget) ++sd1;
     const int64_t need = f.h_front_base[(size_t)sd1] - f.h_front_base[(size_t)sd0];
     if ((int64_t)front.n < need) front.alloc((size_t)need);
+    const std::string tag = std::string("factor") + (&ts == &h->tI ? "I" : "K") + " L";
     for (int L = nlev - 1; L >= 0; --L) {
       dim3 grid(ts.level_count[(size_t)L], sd1 - sd0);
+      ProfScope ps0(h->prof, s, tag + std::to_string(L) + " all");
       k_factor_level<<<grid, kThreads, 0, s>>>(t, fd, ts.level_sn.p + ts.level_first[(size_t)L], in, sd0,
                                                f.front_off.p, f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p,
                                                fail.p);
       CB_LAUNCH();
       if (ts.split_count[(size_t)L] > 0) {
+        ProfScope ps1(h->prof, s, tag + std::to_string(L) + " split");
         SplitArgs sa{ts.split_sn.p + ts.split_first[(size_t)L], sd0, f.front_off.p, f.h_front_base[(size_t)sd0],
                      fbase.p, front.p, fail.p};
         const int ns_ = ts.split_count[(size_t)L], nc_ = sd1 - sd0;
@@ -948,12 +961,14 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
         }
       }
       if (ts.inv_count[(size_t)L] > 0) {
+        ProfScope ps2(h->prof, s, tag + std::to_string(L) + " trinv");
         dim3 gi(ts.inv_count[(size_t)L], sd1 - sd0);
         k_trinv<<<gi, 256, 0, s>>>(t, fd, ts.inv_items.p + ts.inv_first[(size_t)L], sd0, f.front_off.p,
                                    f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p);
         CB_LAUNCH();
       }
       if (ts.gemm_count[(size_t)L] > 0) {
+        ProfScope ps3(h->prof, s, tag + std::to_string(L) + " gemm");
         dim3 gg(ts.gemm_count[(size_t)L], sd1 - sd0);
         k_gemm_m<<<gg, 256, 0, s>>>(t, fd, ts.gemm_items.p + ts.gemm_first[(size_t)L], sd0, f.front_off.p,
                                     f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p);
@@ -972,10 +987,24 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   }
 }
 
+// CUTBDDC_LEVEL_SWEEPS=1 selects the level-synchronous sweeps for single
+// right-hand sides too (A/B measurement of the dataflow sweeps).
+static bool level_sweeps() {
+  static const bool v = [] {
+    const char* e = std::getenv("CUTBDDC_LEVEL_SWEEPS");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 // In-place solve of nrhs x nsd slot vectors X ([rhs][sd][T]); masked-out
 // slots are left untouched. upd must hold nrhs * f.upd_total doubles.
 void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, int nrhs, double* upd,
                   double* ysave, const int* skip, bool rhs_root_only) {
+  if (nrhs == 1 && !rhs_root_only && !level_sweeps()) {
+    sweep_solve(h, ts, f, X, ysave, upd, skip);
+    return;
+  }
   cudaStream_t s = h->stream;
   const TplDev t = tpl_dev(ts, h->slots);
   const FactorDev fd = factor_dev(f);
@@ -988,8 +1017,10 @@ void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* 
     CB_CUDA(cudaMemsetAsync(upd, 0, sizeof(double) * (size_t)nrhs * f.upd_total, s));
     CB_CUDA(cudaMemsetAsync(ysave, 0, sizeof(double) * (size_t)nrhs * h->nsd * h->slots, s));
   }
+  const std::string tag = std::string("solve") + (&ts == &h->tI ? "I" : "K") + (nrhs > 1 ? "m " : " ");
   for (int L = nlev - 1; L >= 0; --L) {
     if (rhs_root_only && L > 0) continue;
+    ProfScope ps(h->prof, s, tag + "fwd L" + std::to_string(L));
     if (ts.small_count[(size_t)L] > 0) {
       dim3 grid(ts.small_count[(size_t)L], h->nsd, nrhs);
       k_fwd_level<<<grid, 256, shm, s>>>(t, fd, ts.small_sn.p + ts.small_first[(size_t)L], h->nsd, f.panel.p, X, upd,
@@ -1004,6 +1035,7 @@ void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* 
     }
   }
   for (int L = 0; L < nlev; ++L) {
+    ProfScope ps(h->prof, s, tag + "bwd L" + std::to_string(L));
     if (ts.bwd_count[(size_t)L] > 0) {
       dim3 grid(ts.bwd_count[(size_t)L], h->nsd, nrhs);
       k_bwd_big<<<grid, 256, shm_big, s>>>(t, fd, ts.bwd_items.p + ts.bwd_first[(size_t)L], h->nsd, f.panel.p, X, ysave,

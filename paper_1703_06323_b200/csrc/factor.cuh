@@ -61,5 +61,10 @@ void solve_device(cutbddc_gpu* h, const TplSet& t, const FactorSet& f, double* X
                   double* ysave, const int* skip, bool rhs_root_only = false);
 // algorithmic bytes of one forward + backward sweep (panel lower parts + front vectors)
 double sweep_bytes(const FactorSet& f);
+// sweep.cu: dataflow sweeps for one right-hand side (plan built per factorisation)
+void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std::vector<int64_t>& poff,
+                      const std::vector<int64_t>& uoff);
+void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
+                 const int* skip);
 
 }  // namespace cutbddc_b200

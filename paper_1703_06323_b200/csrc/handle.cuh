@@ -20,6 +20,7 @@
 #include "cutbddc.h"
 #include "dev_common.cuh"
 #include "nd_template.hpp"
+#include "prof.cuh"
 
 // One ND template resident on the device.
 struct TplSet {
@@ -60,12 +61,25 @@ struct FactorSet {
   int64_t panel_total = 0, upd_total = 0;
   double bytes_per_sweep = 0;                  // algorithmic bytes of fwd + bwd sweeps
   double flops = 0;                            // partial-Cholesky flops
+  // dataflow sweeps (sweep.cu): one persistent launch per sweep direction
+  cutbddc_b200::DevBuf<int4> desc;             // nsd x nsn front descriptors (6 x int4 each, sweep.cu)
+  cutbddc_b200::DevBuf<int32_t> cslot;         // vec_total: slot of each compact front row
+  cutbddc_b200::DevBuf<int32_t> umap;          // upd_total: parent compact row of each update entry
+  cutbddc_b200::DevBuf<int4> items_f, items_b; // (kind, supernode, subdomain, chunk) in dependency order
+  cutbddc_b200::DevBuf<int32_t> counters;      // done_f | ready_f | done_b | ready_b | tickets
+  cutbddc_b200::DevBuf<double> vbuf;           // vec_total: assembled vectors of chunked fronts
+  cutbddc_b200::DevBuf<int32_t> sub_sids;      // template subtrees: supernodes grouped by level, deepest first
+  cutbddc_b200::DevBuf<int32_t> sub_meta;      // per subtree: [n_groups, group starts..., end] into sub_sids
+  cutbddc_b200::DevBuf<unsigned long long> trace;  // CUTBDDC_SWEEP_TRACE only: per-item timestamps
+  int64_t vec_total = 0;
+  int n_items_f = 0, n_items_b = 0;
 };
 
 struct cutbddc_gpu {
   int device = 0, rank = 0, world = 1;
   cudaStream_t stream = nullptr;
   std::mutex mu;
+  cutbddc_b200::Prof prof;                       // CUTBDDC_PROFILE=1 phase timing
 
   // ---------------------------------------------------------------- multi-GPU
   // Subdomains are distributed over ranks; global dof vectors are replicated.

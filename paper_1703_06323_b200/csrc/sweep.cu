@@ -1,0 +1,761 @@
+// sweep.cu — dataflow triangular-solve sweeps of the batched multifrontal
+// factors (the solves inside SparseCholesky::solve, linalg.cpp:56-61, and
+// SaddleFactorization::solve, linalg.cpp:97-106, for every subdomain at once).
+//
+// One persistent launch per sweep direction replaces one launch per
+// elimination level. Work items are listed in dependency order and handed
+// out by an atomic ticket; an item waits (spinning on a per-front counter)
+// only for items with smaller tickets, all of which are held by running
+// CTAs, so the schedule cannot deadlock and parents start as soon as their
+// own children finish (no level barriers).
+//
+// Item kinds per (subdomain, front) with r compact rows and c columns:
+//   T  the bottom kSubLevels levels below one front (all fronts small): one
+//      CTA runs them one after another (no cross-CTA synchronisation).
+//   S  r <= kSmallRows above the subtrees: one CTA per front.
+//   A  larger fronts: one CTA gathers the front vector once into `vbuf`.
+//   C  larger fronts: GEMV chunks (128 rows forward, 16 columns backward)
+//      reading the gathered vector from vbuf.
+// Every front applies its explicit panel G = [L11^{-1}; L21 L11^{-1}]
+// (r x c, column-major, strict upper part of L11^{-1} stored as zeros):
+// forward [y; L21 y] = G v_c, y -> ysave at the front's column slots and
+// v_rest - L21 y -> the update vector the parent gathers (umap);
+// backward x_c = G^T [y; -x_rest] -> X at the column slots.
+// Everything an item needs that does not depend on other items (its
+// descriptor, b or y at its columns, the first panel columns) is loaded
+// before it waits, so the wait hides that latency. Every sum has a fixed
+// order: the sweeps are deterministic.
+#include <cstdio>
+#include <cstdlib>
+
+#include "factor.cuh"
+#include "prof.cuh"
+
+namespace cutbddc_b200 {
+namespace {
+
+constexpr int kSmallRows = 256;  // S items and subtree fronts
+constexpr int kFwdRows = 128;    // C items forward: 128 x 128 tiles (four rows per lane)
+constexpr int kFwdCols = 128;
+constexpr int kBwdCols = 16;     // C items backward: columns per CTA (two per warp)
+constexpr int kSubLevels = 3;    // T items: the bottom levels of the elimination tree
+constexpr int kThreadsSweep = 256;
+constexpr int kWarps = kThreadsSweep / 32;
+constexpr int kMinBlocks = 4;  // resident CTAs per SM (items in flight): <= 64 registers
+constexpr int kVecDoubles = 2048;                   // front vector: >= every template front
+constexpr int kPartDoubles = kWarps * kSmallRows;   // per-warp row partials of the forward GEMV
+constexpr int kShmDoubles = kVecDoubles + kPartDoubles;
+enum { kItemS = 0, kItemA = 1, kItemC = 2, kItemT = 3 };
+
+// Everything one (subdomain, front) needs, in one 96-byte record.
+struct __align__(16) FrontDesc {
+  int r, c, nch, pfs;      // rows, columns, children, parent front (backward dependency) or -1
+  long long vo, po;        // compact front vector / panel offsets
+  long long uo, cuo0;      // own update offset, child 0 update offset
+  long long cuo1;          // child 1 update offset
+  long long tpo;           // forward tile partials of a chunked front (in vbuf)
+  int cfs0, cfs1;          // child fronts (sd * nsn + sid)
+  int cnu0, cnu1;          // child update lengths
+  int cnf0, cnf1;          // child forward completion counts
+  int pnb, rbo;            // parent backward completion count; row-block counters of a chunked front
+};
+static_assert(sizeof(FrontDesc) == 96, "FrontDesc is six int4");
+
+struct SweepDev {
+  const FrontDesc* desc;
+  const int32_t* cslot;  // sd * T + slot of every compact front row
+  const int32_t* umap;   // parent compact row of every update entry
+  const int32_t* sub_sids;
+  const int32_t* sub_meta;
+  int nsn;
+  int32_t* done_f;
+  int32_t* ready_f;
+  int32_t* done_b;
+  int32_t* ready_b;
+  int32_t* ticket;  // [0] forward, [1] backward
+  int32_t* rbcnt;   // forward tile arrivals per (chunked front, row block)
+  double* vbuf;
+  unsigned long long* trace;  // CUTBDDC_SWEEP_TRACE: per item {grab, deps met, done, sm}, else null
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+struct TraceState {
+  int it;
+  unsigned long long t0, t1;
+};
+__shared__ TraceState s_trace;
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// thread 0 waits until *p >= target; the whole CTA then proceeds
+__device__ __forceinline__ void cta_wait(const SweepDev& sp, const int32_t* p, int target) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire(p) < target) __nanosleep(32);
+    __threadfence();
+    if (sp.trace) s_trace.t1 = gtimer();
+  }
+  __syncthreads();
+}
+
+// all of the CTA's global writes are published before *p is incremented
+__device__ __forceinline__ void cta_signal(int32_t* p) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(p, 1);
+  }
+}
+
+__device__ __forceinline__ int next_item(const SweepDev& sp, int32_t* ticket, bool first) {
+  __shared__ int s_item;
+  __syncthreads();  // previous item finished with shared memory
+  if (threadIdx.x == 0) {
+    if (sp.trace) {
+      const unsigned long long now = gtimer();
+      if (!first) {
+        unsigned long long* tr = sp.trace + 4ll * s_trace.it;
+        tr[0] = s_trace.t0;
+        tr[1] = s_trace.t1;
+        tr[2] = now;
+        tr[3] = smid();
+      }
+      s_trace.t0 = s_trace.t1 = now;
+    }
+    s_item = atomicAdd(ticket, 1);
+    if (sp.trace) s_trace.it = s_item;
+  }
+  __syncthreads();
+  return s_item;
+}
+
+__device__ __forceinline__ FrontDesc load_desc(const FrontDesc* p) {
+  FrontDesc d;
+  const int4* s = reinterpret_cast<const int4*>(p);
+  int4* o = reinterpret_cast<int4*>(&d);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) o[k] = s[k];
+  return d;
+}
+
+// acc[k] (k < 16) summed over the warp; lane L returns the total of
+// acc[L & 15]. A butterfly over lane bit 4, then recursive halving: 31
+// shuffles in a fixed order (deterministic).
+__device__ __forceinline__ double reduce_scatter16(double (&acc)[16], int lane) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 16);
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int k = 0; k < off; ++k) {
+      const double send = up ? acc[k] : acc[k + off];
+      const double keep = up ? acc[k + off] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return acc[0];
+}
+
+// v[umap] += child updates (children in order; `cross`: produced by other CTAs)
+__device__ __forceinline__ void add_child_updates(const SweepDev& p, const FrontDesc& d, const double* upd, double* v,
+                                                  bool cross) {
+  const int tid = threadIdx.x;
+  if (d.nch > 0) {
+    for (int a = tid; a < d.cnu0; a += kThreadsSweep)
+      v[p.umap[d.cuo0 + a]] += cross ? __ldcg(upd + d.cuo0 + a) : upd[d.cuo0 + a];
+    __syncthreads();
+  }
+  if (d.nch > 1) {
+    for (int a = tid; a < d.cnu1; a += kThreadsSweep)
+      v[p.umap[d.cuo1 + a]] += cross ? __ldcg(upd + d.cuo1 + a) : upd[d.cuo1 + a];
+    __syncthreads();
+  }
+}
+
+// Forward GEMV o[i] = sum_j G[i + j r] v[j] for rows [i0, i1) (at most 32 R)
+// and columns [jlo, jhi): warps split the columns, each lane accumulates its
+// R rows in registers (coalesced 256-B column segments, R loads in flight per
+// column), the warp partials are summed in warp order (deterministic).
+// Row blocks entirely above column j are skipped (zero part of L11^{-1}).
+// The first column of every warp is loaded before `between()` (which
+// completes v: dependency wait + children's updates).
+template <int R, typename Between, typename Out>
+__device__ __forceinline__ void cta_gemv_fwd(const double* __restrict__ G, int r, int jlo, int jhi, int i0, int i1,
+                                             double* v, double* part, Between between, Out out) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int cw = (jhi - jlo + kWarps - 1) / kWarps;
+  const int ja = min(jhi, jlo + wid * cw), jb = min(jhi, ja + cw);
+  const double* gl = G + i0 + lane;
+  double acc[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const bool row = i0 + 32 * k + lane < i1;
+    acc[k] = (ja < jb && row && i0 + 32 * k + 31 >= ja) ? gl[(int64_t)ja * r + 32 * k] : 0.0;
+  }
+  between();
+  const double v0 = ja < jb ? v[ja] : 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[k] *= v0;
+#pragma unroll 2
+  for (int j = ja + 1; j < jb; ++j) {
+    const double vj = v[j];
+    const double* gj = gl + (int64_t)j * r;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (i0 + 32 * k + 31 >= j && i0 + 32 * k + lane < i1) acc[k] += gj[32 * k] * vj;
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) part[wid * 32 * R + 32 * k + lane] = acc[k];
+  __syncthreads();
+  for (int q = tid; q < i1 - i0; q += kThreadsSweep) {
+    double o = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) o += part[w * 32 * R + q];
+    out(i0 + q, o);
+  }
+  __syncthreads();
+}
+
+// Forward of one front (r <= kSmallRows) by the whole CTA. `wait` = the
+// children belong to other items (wait for them, read their updates from L2).
+__device__ void cta_front_fwd(const SweepDev& p, const FrontDesc& d, const double* __restrict__ panel,
+                              const double* __restrict__ X, double* ysave, double* upd, double* v, bool wait) {
+  const int r = d.r, c = d.c;
+  if (r == 0) return;
+  const int tid = threadIdx.x;
+  const int32_t* cs = p.cslot + d.vo;
+  for (int q = tid; q < r; q += kThreadsSweep) v[q] = q < c ? X[cs[q]] : 0.0;
+  double* uo = upd + d.uo;
+  cta_gemv_fwd<kSmallRows / 32>(
+      panel + d.po, r, 0, c, 0, r, v, v + kVecDoubles,
+      [&] {
+        if (wait) {
+          if (d.nch > 0) cta_wait(p, p.done_f + d.cfs0, d.cnf0);
+          if (d.nch > 1) cta_wait(p, p.done_f + d.cfs1, d.cnf1);
+        }
+        __syncthreads();
+        add_child_updates(p, d, upd, v, wait);
+      },
+      [&](int i, double o) {
+        if (i < c)
+          ysave[cs[i]] = o;
+        else
+          uo[i - c] = v[i] - o;
+      });
+}
+
+// Backward of one front (r <= kSmallRows) by the whole CTA: rows split over
+// the warps, 16 columns at a time accumulated in registers, reduce-scattered
+// in each warp and the warp partials summed in order. The first row of each
+// lane (first column block) and y at the columns are loaded before the wait.
+__device__ void cta_front_bwd(const SweepDev& p, const FrontDesc& d, const double* __restrict__ panel, double* X,
+                              const double* __restrict__ ysave, double* w, double (*part)[33], bool wait) {
+  const int r = d.r, c = d.c;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (c == 0) {
+    if (wait && d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
+    return;
+  }
+  const int32_t* cs = p.cslot + d.vo;
+  for (int q = tid; q < c; q += kThreadsSweep) w[q] = ysave[cs[q]];
+  const double* G = panel + d.po;
+  const int rw = (r + kWarps - 1) / kWarps;
+  const int ra = wid * rw, rb = min(r, ra + rw);
+  const int i_first = ra + lane;
+  double acc[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = (i_first < rb && k < c) ? G[i_first + (int64_t)k * r] : 0.0;
+  if (wait && d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
+  for (int q = c + tid; q < r; q += kThreadsSweep) w[q] = -__ldcg(X + cs[q]);
+  __syncthreads();
+  for (int jb = 0; jb < c; jb += 16) {
+    int i = max(ra, jb) + lane;
+    if (jb == 0) {
+      const double wi = i_first < rb ? w[i_first] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[k] *= wi;
+      i = i_first + 32;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+    }
+    for (; i < rb; i += 32) {
+      const double wi = w[i];
+      const double* gi = G + i + (int64_t)jb * r;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (jb + k < c) acc[k] += gi[(int64_t)k * r] * wi;
+    }
+    part[wid][lane] = reduce_scatter16(acc, lane);
+    __syncthreads();
+    if (wid == 0 && lane < 16 && jb + lane < c) {
+      double x = 0.0;
+      for (int q = 0; q < kWarps; ++q) x += part[q][lane];
+      X[cs[jb + lane]] = x;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDev p, const int4* __restrict__ items, int n_items,
+                                                             const double* __restrict__ panel,
+                                                             const double* __restrict__ X, double* __restrict__ ysave,
+                                                             double* upd, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double v[];
+  const int tid = threadIdx.x;
+  for (bool first = true;; first = false) {
+    const int it = next_item(p, p.ticket, first);
+    if (it >= n_items) return;
+    const int4 w = items[it];
+    const int kind = w.x, sid = w.y, sd = w.z, chunk = w.w;
+    const int64_t fs = (int64_t)sd * p.nsn + sid;
+    if (kind == kItemT) {
+      // bottom subtree of sid: its fronts deepest level first, one after another
+      const int32_t* meta = p.sub_meta + chunk;
+      const int ng = meta[0];
+      for (int k = meta[1]; k < meta[1 + ng]; ++k) {
+        const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
+        cta_front_fwd(p, d, panel, X, ysave, upd, v, false);
+      }
+      cta_signal(p.done_f + fs);
+      continue;
+    }
+    const FrontDesc d = load_desc(p.desc + fs);
+    if (kind == kItemS) {
+      cta_front_fwd(p, d, panel, X, ysave, upd, v, true);
+      cta_signal(p.done_f + fs);
+      continue;
+    }
+    const int r = d.r, c = d.c;
+    const int32_t* cs = p.cslot + d.vo;
+    if (kind == kItemA) {
+      for (int q = tid; q < r; q += kThreadsSweep) v[q] = q < c ? X[cs[q]] : 0.0;
+      if (d.nch > 0) cta_wait(p, p.done_f + d.cfs0, d.cnf0);
+      if (d.nch > 1) cta_wait(p, p.done_f + d.cfs1, d.cnf1);
+      __syncthreads();
+      add_child_updates(p, d, upd, v, true);
+      for (int q = tid; q < r; q += kThreadsSweep) p.vbuf[d.vo + q] = v[q];
+      cta_signal(p.ready_f + fs);
+      continue;
+    }
+    // C: tile (row block rb, column block cb) of a chunked front. Partial row
+    // sums go to vbuf; the last tile of a row block to arrive sums them in
+    // column-block order (deterministic) and writes the rows.
+    const int mcb = max(1, (c + kFwdCols - 1) / kFwdCols);
+    const int rb = chunk / mcb, cb = chunk % mcb;
+    const int i0 = rb * kFwdRows, i1 = min(r, i0 + kFwdRows);
+    const int jrow = min(c, i1);
+    const int jlo = cb * kFwdCols, jhi = min(jrow, jlo + kFwdCols);
+    double* tp = p.vbuf + d.tpo + (int64_t)rb * mcb * kFwdRows;
+    cta_gemv_fwd<kFwdRows / 32>(
+        panel + d.po, r, jlo, jhi, i0, i1, v, v + kVecDoubles,
+        [&] {
+          cta_wait(p, p.ready_f + fs, 1);
+          for (int q = jlo + tid; q < jhi; q += kThreadsSweep) v[q] = __ldcg(p.vbuf + d.vo + q);
+          __syncthreads();
+        },
+        [&](int i, double o) { tp[(int64_t)cb * kFwdRows + i - i0] = o; });
+    __shared__ int s_last;
+    if (tid == 0) {
+      __threadfence();
+      const int ncb = max(1, (jrow + kFwdCols - 1) / kFwdCols);
+      s_last = atomicAdd(p.rbcnt + d.rbo + rb, 1) == ncb - 1;
+      if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (!s_last) continue;
+    const int ncb = max(1, (jrow + kFwdCols - 1) / kFwdCols);
+    double* uo = upd + d.uo;
+    for (int q = tid; q < i1 - i0; q += kThreadsSweep) {
+      const int i = i0 + q;
+      double o = 0.0;
+      for (int k = 0; k < ncb; ++k) o += __ldcg(tp + (int64_t)k * kFwdRows + q);
+      if (i < c)
+        ysave[cs[i]] = o;
+      else
+        uo[i - c] = __ldcg(p.vbuf + d.vo + i) - o;
+    }
+    cta_signal(p.done_f + fs);
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDev p, const int4* __restrict__ items, int n_items,
+                                                             const double* __restrict__ panel, double* X,
+                                                             const double* __restrict__ ysave,
+                                                             const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double w[];
+  __shared__ double part[kWarps][33];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (bool first = true;; first = false) {
+    const int it = next_item(p, p.ticket + 1, first);
+    if (it >= n_items) return;
+    const int4 iw = items[it];
+    const int kind = iw.x, sid = iw.y, sd = iw.z, chunk = iw.w;
+    const int64_t fs = (int64_t)sd * p.nsn + sid;
+    if (kind == kItemT) {
+      // bottom subtree of sid: shallowest level first, one front after another;
+      // only its root depends on other items (its parent)
+      const int32_t* meta = p.sub_meta + chunk;
+      const int ng = meta[0];
+      for (int k = meta[1 + ng] - 1; k >= meta[1]; --k) {
+        const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
+        cta_front_bwd(p, d, panel, X, ysave, w, part, k == meta[1 + ng] - 1);
+      }
+      continue;  // nothing outside the subtree waits on it
+    }
+    const FrontDesc d = load_desc(p.desc + fs);
+    if (kind == kItemS) {
+      cta_front_bwd(p, d, panel, X, ysave, w, part, true);
+      cta_signal(p.done_b + fs);
+      continue;
+    }
+    const int r = d.r, c = d.c;
+    const int32_t* cs = p.cslot + d.vo;
+    if (kind == kItemA) {
+      for (int q = tid; q < c; q += kThreadsSweep) p.vbuf[d.vo + q] = ysave[cs[q]];
+      if (d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
+      for (int q = c + tid; q < r; q += kThreadsSweep) p.vbuf[d.vo + q] = -__ldcg(X + cs[q]);
+      cta_signal(p.ready_b + fs);
+      continue;
+    }
+    // C: columns [j0, j1) of a chunked front, one warp per column
+    const double* G = panel + d.po;
+    cta_wait(p, p.ready_b + fs, 1);
+    for (int q = tid; q < r; q += kThreadsSweep) w[q] = __ldcg(p.vbuf + d.vo + q);
+    __syncthreads();
+    const int j0 = chunk * kBwdCols, j1 = min(c, j0 + kBwdCols);
+    for (int j = j0 + wid; j < j1; j += kWarps) {
+      const double* col = G + (int64_t)j * r;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int i = j + lane;
+      for (; i + 96 < r; i += 128) {
+        s0 += col[i] * w[i];
+        s1 += col[i + 32] * w[i + 32];
+        s2 += col[i + 64] * w[i + 64];
+        s3 += col[i + 96] * w[i + 96];
+      }
+      for (; i < r; i += 32) s0 += col[i] * w[i];
+      const double sum = warp_sum((s0 + s1) + (s2 + s3));
+      if (lane == 0) X[cs[j]] = sum;
+    }
+    cta_signal(p.done_b + fs);
+  }
+}
+
+// compact slot of every front row, and the parent position of every update entry
+__global__ void k_sweep_maps(TplDev t, FactorDev f, const FrontDesc* __restrict__ desc, int32_t* __restrict__ cslot,
+                             int32_t* __restrict__ umap) {
+  const int sid = blockIdx.x, sd = blockIdx.y;
+  const Supernode s = t.sn[sid];
+  const int64_t fs = (int64_t)sd * t.nsn + sid;
+  const int32_t* pf = f.pfx + (int64_t)sd * t.rows_total + s.rows_off;
+  const int64_t vo = desc[fs].vo;
+  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
+    const int pq = pf[q];
+    if (pq >= 0) cslot[vo + pq] = sd * t.T + t.rows[s.rows_off + q];  // index into the nsd x T slot vector
+  }
+  if (s.parent < 0) return;
+  const Supernode ps = t.sn[s.parent];
+  const int32_t* ppf = f.pfx + (int64_t)sd * t.rows_total + ps.rows_off;
+  const int c = desc[fs].c;
+  const int64_t uo = desc[fs].uo;
+  for (int a = threadIdx.x; a < s.nrows - s.ncols; a += blockDim.x) {
+    const int ia = pf[s.ncols + a];
+    if (ia >= 0) umap[uo + ia - c] = ppf[t.emap[s.emap_off + a]];
+  }
+}
+
+SweepDev sweep_dev(const FactorSet& f, int nsd, int nsn, unsigned long long* trace) {
+  const int64_t n = (int64_t)nsd * nsn;
+  int32_t* cnt = const_cast<int32_t*>(f.counters.p);
+  return SweepDev{reinterpret_cast<const FrontDesc*>(f.desc.p),
+                  f.cslot.p,
+                  f.umap.p,
+                  f.sub_sids.p,
+                  f.sub_meta.p,
+                  nsn,
+                  cnt,
+                  cnt + n,
+                  cnt + 2 * n,
+                  cnt + 3 * n,
+                  cnt + 4 * n,
+                  cnt + 4 * n + 2,
+                  const_cast<double*>(f.vbuf.p),
+                  trace};
+}
+
+const char* trace_prefix() {
+  static const char* e = std::getenv("CUTBDDC_SWEEP_TRACE");
+  return e && e[0] ? e : nullptr;
+}
+
+// host dump of one sweep's trace: items (int4) then timestamps (4 x u64 per item)
+void dump_trace(const std::string& path, const FactorSet& f, bool fwd, cudaStream_t s) {
+  const int n = fwd ? f.n_items_f : f.n_items_b;
+  std::vector<int4> items = (fwd ? f.items_f : f.items_b).to_host(s);
+  std::vector<unsigned long long> tr((size_t)4 * n);
+  f.trace.download(tr.data(), tr.size(), s);
+  CB_CUDA(cudaStreamSynchronize(s));
+  FILE* fp = std::fopen(path.c_str(), "wb");
+  if (!fp) return;
+  std::fwrite(&n, sizeof(int), 1, fp);
+  std::fwrite(items.data(), sizeof(int4), (size_t)n, fp);
+  std::fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fp);
+  std::fclose(fp);
+}
+
+int sweep_grid(const void* fn) {
+  static int cached[2] = {0, 0};
+  const int k = fn == (const void*)k_sweep_fwd ? 0 : 1;
+  if (!cached[k]) {
+    int per_sm = 0;
+    CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsSweep, sizeof(double) * kShmDoubles));
+    int dev = 0, sms = 0;
+    CB_CUDA(cudaGetDevice(&dev));
+    CB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cached[k] = std::max(1, per_sm) * sms;
+  }
+  return cached[k];
+}
+
+}  // namespace
+
+// Host: descriptors, maps, completion counts and the ordered work lists of
+// one factorisation (after its symbolic phase; poff / uoff are the panel and
+// update offsets per (sd, supernode) the numeric phase uses).
+void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std::vector<int64_t>& poff,
+                      const std::vector<int64_t>& uoff) {
+  cudaStream_t s = h->stream;
+  const Template& tp = ts.tpl;
+  const int nsd = h->nsd, nsn = (int)tp.sn.size();
+  const auto& lv = tp.levels;
+  const int nlev = (int)lv.size();
+  if (tp.max_rows > kVecDoubles) throw Failure(CUTBDDC_CONFIG, "sweep: front larger than the shared vector");
+  // subtree level: the shallowest level from which every front is small,
+  // and no more than kSubLevels above the deepest level
+  int lsub = nlev;
+  while (lsub > 0) {
+    bool small = true;
+    for (int sid : lv[(size_t)lsub - 1]) small &= tp.sn[(size_t)sid].nrows <= kSmallRows;
+    if (!small) break;
+    --lsub;
+  }
+  lsub = std::max(lsub, nlev - kSubLevels);
+  if (lsub == 0 && nlev > 1) lsub = 1;  // keep the root as its own item
+  // template subtrees: descendants of each level-lsub root grouped by level
+  std::vector<int32_t> sids, meta;
+  std::vector<int> meta_of((size_t)nsn, -1);
+  std::vector<uint8_t> in_sub((size_t)nsn, 0);
+  if (lsub < nlev) {
+    for (int root : lv[(size_t)lsub]) {
+      std::vector<std::vector<int>> by((size_t)(nlev - lsub));
+      std::vector<int> stack{root};
+      while (!stack.empty()) {
+        const int x = stack.back();
+        stack.pop_back();
+        in_sub[(size_t)x] = 1;
+        by[(size_t)(tp.sn[(size_t)x].level - lsub)].push_back(x);
+        for (int ch = 0; ch < tp.sn[(size_t)x].nchild; ++ch) stack.push_back(tp.sn[(size_t)x].child[ch]);
+      }
+      meta_of[(size_t)root] = (int)meta.size();
+      int ng = 0;
+      for (auto& g : by) ng += !g.empty();
+      meta.push_back(ng);
+      for (int g = (int)by.size() - 1; g >= 0; --g) {  // deepest first
+        if (by[(size_t)g].empty()) continue;
+        meta.push_back((int)sids.size());
+        sids.insert(sids.end(), by[(size_t)g].begin(), by[(size_t)g].end());
+      }
+      meta.push_back((int)sids.size());
+    }
+  }
+  // completion counts: forward items per front (T items signal their root),
+  // backward items per front (every front with rows above the subtrees has
+  // at least one, so waiting on the parent covers every ancestor)
+  std::vector<int32_t> nf((size_t)nsd * nsn, 0), nb((size_t)nsd * nsn, 0);
+  std::vector<int64_t> voff((size_t)nsd * nsn);
+  int64_t tot = 0;
+  for (int sd = 0; sd < nsd; ++sd)
+    for (int q = 0; q < nsn; ++q) {
+      const int2 v = f.h_rc[(size_t)sd * nsn + q];
+      const size_t i = (size_t)sd * nsn + q;
+      voff[i] = tot;
+      tot += v.x;
+      if (in_sub[(size_t)q]) {
+        nf[i] = meta_of[(size_t)q] >= 0 ? 1 : 0;
+        continue;
+      }
+      const bool small = v.x <= kSmallRows;
+      nf[i] = v.x == 0 ? 0 : small ? 1 : (v.x + kFwdRows - 1) / kFwdRows;
+      nb[i] = v.x == 0 ? 0 : (small || v.y == 0) ? 1 : (v.y + kBwdCols - 1) / kBwdCols;
+    }
+  f.vec_total = tot;
+  // forward tiles of chunked fronts: partial storage (after the front
+  // vectors in vbuf) and one arrival counter per row block
+  auto mcb_of = [](int c) { return std::max(1, (c + kFwdCols - 1) / kFwdCols); };
+  auto ncb_of = [](int r, int c, int rb) {
+    return std::max(1, (std::min(c, std::min(r, (rb + 1) * kFwdRows)) + kFwdCols - 1) / kFwdCols);
+  };
+  std::vector<int64_t> tpo((size_t)nsd * nsn, 0);
+  std::vector<int32_t> rbo((size_t)nsd * nsn, 0);
+  int64_t ptot = tot;
+  int32_t nrb_tot = 0;
+  for (size_t i = 0; i < (size_t)nsd * nsn; ++i) {
+    const int2 v = f.h_rc[i];
+    if (in_sub[i % (size_t)nsn] || v.x <= kSmallRows) continue;
+    const int nrb = (v.x + kFwdRows - 1) / kFwdRows;
+    tpo[i] = ptot;
+    ptot += (int64_t)nrb * mcb_of(v.y) * kFwdRows;
+    rbo[i] = nrb_tot;
+    nrb_tot += nrb;
+  }
+  std::vector<FrontDesc> desc((size_t)nsd * nsn);
+  for (int sd = 0; sd < nsd; ++sd)
+    for (int q = 0; q < nsn; ++q) {
+      const size_t i = (size_t)sd * nsn + q;
+      const Supernode& sn = tp.sn[(size_t)q];
+      const int2 v = f.h_rc[i];
+      FrontDesc& d = desc[i];
+      d = FrontDesc{};
+      d.r = v.x;
+      d.c = v.y;
+      d.vo = voff[i];
+      d.po = poff[i];
+      d.uo = uoff[i];
+      d.tpo = tpo[i];
+      d.rbo = rbo[i];
+      d.nch = sn.nchild;
+      d.cfs0 = d.cfs1 = -1;
+      for (int ch = 0; ch < sn.nchild; ++ch) {
+        const size_t ci = (size_t)sd * nsn + sn.child[ch];
+        const int2 cv = f.h_rc[ci];
+        if (ch == 0) {
+          d.cfs0 = (int)ci;
+          d.cnu0 = cv.x - cv.y;
+          d.cuo0 = uoff[ci];
+          d.cnf0 = nf[ci];
+        } else {
+          d.cfs1 = (int)ci;
+          d.cnu1 = cv.x - cv.y;
+          d.cuo1 = uoff[ci];
+          d.cnf1 = nf[ci];
+        }
+      }
+      // backward: the parent's columns hold every row of this front once the
+      // parent's items are done (they waited for their own parent)
+      d.pfs = -1;
+      if (sn.parent >= 0 && v.x > v.y) {
+        d.pfs = (int)((size_t)sd * nsn + sn.parent);
+        d.pnb = nb[(size_t)d.pfs];
+      }
+    }
+  std::vector<int4> fw, bw;
+  auto front_items = [&](int L, bool fwd, std::vector<int4>& out) {
+    for (int sid : lv[(size_t)L])
+      for (int sd = 0; sd < nsd; ++sd) {
+        const int2 v = f.h_rc[(size_t)sd * nsn + sid];
+        if (v.x > 0)
+          out.push_back(make_int4(v.x <= kSmallRows || (!fwd && v.y == 0) ? kItemS : kItemA, sid, sd, 0));
+      }
+    for (int sid : lv[(size_t)L])
+      for (int sd = 0; sd < nsd; ++sd) {
+        const size_t i = (size_t)sd * nsn + sid;
+        const int2 v = f.h_rc[i];
+        if (v.x <= kSmallRows) continue;
+        if (fwd) {
+          const int mcb = mcb_of(v.y);
+          for (int rb = 0; rb < nf[i]; ++rb)
+            for (int cb = 0; cb < ncb_of(v.x, v.y, rb); ++cb) out.push_back(make_int4(kItemC, sid, sd, rb * mcb + cb));
+        } else if (v.y > 0) {
+          for (int k = 0; k < nb[i]; ++k) out.push_back(make_int4(kItemC, sid, sd, k));
+        }
+      }
+  };
+  auto subtree_items = [&](std::vector<int4>& out) {
+    if (lsub >= nlev) return;
+    for (int root : lv[(size_t)lsub])
+      for (int sd = 0; sd < nsd; ++sd) out.push_back(make_int4(kItemT, root, sd, meta_of[(size_t)root]));
+  };
+  subtree_items(fw);
+  for (int L = lsub - 1; L >= 0; --L) front_items(L, true, fw);  // leaves first
+  for (int L = 0; L < lsub; ++L) front_items(L, false, bw);     // root first
+  subtree_items(bw);
+  f.n_items_f = (int)fw.size();
+  f.n_items_b = (int)bw.size();
+  if (fw.empty()) fw.push_back(make_int4(0, 0, 0, 0));
+  if (bw.empty()) bw.push_back(make_int4(0, 0, 0, 0));
+  if (sids.empty()) sids.push_back(0);
+  if (meta.empty()) meta.push_back(0);
+  f.desc.upload(reinterpret_cast<const int4*>(desc.data()), desc.size() * 6, s);
+  f.items_f.upload(fw, s);
+  f.items_b.upload(bw, s);
+  f.sub_sids.upload(sids, s);
+  f.sub_meta.upload(meta, s);
+  f.cslot.alloc((size_t)std::max<int64_t>(1, tot));
+  f.umap.alloc((size_t)std::max<int64_t>(1, f.upd_total));
+  f.vbuf.alloc((size_t)std::max<int64_t>(1, ptot));
+  f.counters.alloc((size_t)4 * nsd * nsn + 2 + nrb_tot);
+  const TplDev t = tpl_dev(ts, h->slots);
+  k_sweep_maps<<<dim3(nsn, nsd), 256, 0, s>>>(t, factor_dev(f), reinterpret_cast<const FrontDesc*>(f.desc.p),
+                                              f.cslot.p, f.umap.p);
+  CB_LAUNCH();
+  CB_CUDA(cudaStreamSynchronize(s));  // the host vectors above are pageable and go out of scope
+}
+
+// In-place solve of one right-hand side X (nsd x T slot vector): two launches
+// (plus the counter reset) for the whole elimination tree of every subdomain.
+void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
+                 const int* skip) {
+  cudaStream_t s = h->stream;
+  const int nsd = h->nsd, nsn = (int)ts.tpl.sn.size();
+  const char* tp = trace_prefix();
+  FactorSet& fm = const_cast<FactorSet&>(f);
+  if (tp) fm.trace.alloc((size_t)4 * std::max(f.n_items_f, f.n_items_b) + 4);
+  const SweepDev p = sweep_dev(f, nsd, nsn, tp ? fm.trace.p : nullptr);
+  const size_t shm = sizeof(double) * kShmDoubles;
+  static bool attr = false;
+  if (!attr) {
+    CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    CB_CUDA(cudaFuncSetAttribute(k_sweep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    attr = true;
+  }
+  const std::string tag = std::string("sweep") + (&ts == &h->tI ? "I" : "K");
+  CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
+  {
+    ProfScope ps(h->prof, s, tag + " fwd");
+    if (f.n_items_f > 0) {
+      const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd));
+      k_sweep_fwd<<<g, kThreadsSweep, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, skip);
+      CB_LAUNCH();
+    }
+  }
+  if (tp) dump_trace(std::string(tp) + "_" + tag + "_fwd.bin", f, true, s);
+  {
+    ProfScope ps(h->prof, s, tag + " bwd");
+    if (f.n_items_b > 0) {
+      const int g = std::min(f.n_items_b, sweep_grid((const void*)k_sweep_bwd));
+      k_sweep_bwd<<<g, kThreadsSweep, shm, s>>>(p, f.items_b.p, f.n_items_b, f.panel.p, X, ysave, skip);
+      CB_LAUNCH();
+    }
+  }
+  if (tp) dump_trace(std::string(tp) + "_" + tag + "_bwd.bin", f, false, s);
+}
+
+}  // namespace cutbddc_b200
