@@ -204,8 +204,9 @@ __global__ void __launch_bounds__(256) k_split_zero(TplDev t, FactorDev f, Split
   const int sd = a.sd0 + blockIdx.z;
   const int r = f.rc[(int64_t)sd * t.nsn + sid].x;
   double* F = split_front(t, f, a, sid, sd);
-  const int64_t n = (int64_t)r * r;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) F[q] = 0.0;
+  // lower triangle only (nothing reads the strict upper part of a split front)
+  for (int j = blockIdx.x; j < r; j += gridDim.x)
+    for (int i = j + threadIdx.x; i < r; i += blockDim.x) F[i + (int64_t)j * r] = 0.0;
 }
 
 __global__ void __launch_bounds__(256) k_split_amap(TplDev t, FactorDev f, SplitArgs a, FactorInput in) {
@@ -242,28 +243,31 @@ __global__ void __launch_bounds__(256) k_split_penalty(TplDev t, FactorDev f, Sp
   }
 }
 
-__global__ void __launch_bounds__(256) k_split_extend(TplDev t, FactorDev f, SplitArgs a, int ch) {
+// umap (sweep.cu: parent compact row of every update entry) places the
+// child's update matrix; one CTA per update column, threads down the column.
+__global__ void __launch_bounds__(256) k_split_extend(TplDev t, FactorDev f, SplitArgs a, int ch,
+                                                      const int32_t* __restrict__ umap) {
   const int sid = a.sn[blockIdx.y];
   const int sd = a.sd0 + blockIdx.z;
   const Supernode s = t.sn[sid];
   if (ch >= s.nchild) return;
   const int cid = s.child[ch];
-  const Supernode cs = t.sn[cid];
-  const int2 crc = f.rc[(int64_t)sd * t.nsn + cid];
+  const int64_t cf = (int64_t)sd * t.nsn + cid;
+  const int2 crc = f.rc[cf];
   const int rcc = crc.x, ccc = crc.y, nu = rcc - ccc;
   if (nu <= 0) return;
   const int r = f.rc[(int64_t)sd * t.nsn + sid].x;
   double* F = split_front(t, f, a, sid, sd);
   const double* U = split_front(t, f, a, cid, sd);
-  const int32_t* ctp = f.tpos + (int64_t)sd * t.rows_total + cs.rows_off;
-  const int64_t n = (int64_t)nu * nu;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(q % nu), y = (int)(q / nu);
-    if (x < y) continue;
-    const int px = pfx_at(f, t, sd, s, t.emap[cs.emap_off + ctp[ccc + x] - cs.ncols]);
-    const int py = pfx_at(f, t, sd, s, t.emap[cs.emap_off + ctp[ccc + y] - cs.ncols]);
-    const int row = max(px, py), col = min(px, py);
-    F[row + (int64_t)col * r] += U[(ccc + x) + (int64_t)(ccc + y) * rcc];
+  const int32_t* um = umap + f.upd_off[cf];
+  for (int y = blockIdx.x; y < nu; y += gridDim.x) {
+    const int py = um[y];
+    const double* uc = U + ccc + (int64_t)(ccc + y) * rcc;
+    for (int x = y + threadIdx.x; x < nu; x += blockDim.x) {
+      const int px = um[x];
+      const int row = max(px, py), col = min(px, py);
+      F[row + (int64_t)col * r] += uc[x];
+    }
   }
 }
 
@@ -403,9 +407,10 @@ __global__ void __launch_bounds__(256) k_split_syrk(TplDev t, FactorDev f, Split
 __global__ void __launch_bounds__(256) k_trinv(TplDev t, FactorDev f, const int2* __restrict__ items, int sd0,
                                                const int64_t* __restrict__ front_off, int64_t front_base0,
                                                const int64_t* __restrict__ front_base, const double* __restrict__ front,
-                                               double* __restrict__ panel) {
+                                               double* __restrict__ panel, int skip_split) {
   const int2 it = items[blockIdx.x];
   const int sid = it.x, jb = it.y;
+  if (skip_split && t.is_split[sid]) return;  // G written by the dense DAG (dense_dag.cu)
   const int sd = sd0 + blockIdx.y;
   const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
   const int r = rc.x, c = rc.y;
@@ -466,9 +471,10 @@ __global__ void __launch_bounds__(256) k_trinv(TplDev t, FactorDev f, const int2
 __global__ void __launch_bounds__(256) k_gemm_m(TplDev t, FactorDev f, const int2* __restrict__ items, int sd0,
                                                 const int64_t* __restrict__ front_off, int64_t front_base0,
                                                 const int64_t* __restrict__ front_base, const double* __restrict__ front,
-                                                double* __restrict__ panel) {
+                                                double* __restrict__ panel, int skip_split) {
   const int2 it = items[blockIdx.x];
   const int sid = it.x;
+  if (skip_split && t.is_split[sid]) return;  // G written by the dense DAG (dense_dag.cu)
   const int sd = sd0 + blockIdx.y;
   const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
   const int r = rc.x, c = rc.y, m = r - c;
@@ -904,6 +910,10 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
   DevBuf<double>& front = h->ws_front;
   const int nlev = (int)ts.level_first.size();
+  static const int use_dag = [] {  // CUTBDDC_SPLIT_STEPS=1: the 32-column panel steps (A/B measurement)
+    const char* e = std::getenv("CUTBDDC_SPLIT_STEPS");
+    return e && e[0] == '1' ? 0 : 1;
+  }();
   int sd0 = 0;
   while (sd0 < nsd) {
     int sd1 = sd0 + 1;
@@ -934,7 +944,7 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
             max_child_nu = std::max(max_child_nu, cs.nrows - cs.ncols);
           }
         }
-        k_split_zero<<<dim3(64, ns_, nc_), 256, 0, s>>>(t, fd, sa);
+        k_split_zero<<<dim3(std::min(maxr, 512), ns_, nc_), 256, 0, s>>>(t, fd, sa);
         CB_LAUNCH();
         k_split_amap<<<dim3((max_amap + 255) / 256, ns_, nc_), 256, 0, s>>>(t, fd, sa, in);
         CB_LAUNCH();
@@ -942,36 +952,43 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
           k_split_penalty<<<dim3(h->m_max, ns_, nc_), 256, 0, s>>>(t, fd, sa, in);
           CB_LAUNCH();
         }
-        const int64_t pairs = (int64_t)max_child_nu * max_child_nu;
-        const int eb = (int)std::min<int64_t>(4096, (pairs + 255) / 256);
         for (int c2 = 0; c2 < 2; ++c2) {
-          k_split_extend<<<dim3(std::max(1, eb), ns_, nc_), 256, 0, s>>>(t, fd, sa, c2);
+          k_split_extend<<<dim3(std::max(1, std::min(max_child_nu, 1024)), ns_, nc_), 256, 0, s>>>(t, fd, sa, c2,
+                                                                                                   f.umap.p);
           CB_LAUNCH();
         }
-        for (int k = 0; k < maxc; k += 32) {
-          k_split_diag<<<dim3(ns_, nc_), 32, 0, s>>>(t, fd, sa, k);
-          CB_LAUNCH();
-          const int rows_below = maxr - k - 1;
-          if (rows_below <= 0) continue;
-          k_split_trsm<<<dim3((rows_below + 127) / 128, ns_, nc_), 128, 0, s>>>(t, fd, sa, k);
-          CB_LAUNCH();
-          const int nt = (rows_below + 63) / 64;
-          k_split_syrk<<<dim3(nt * (nt + 1) / 2, ns_, nc_), 256, 0, s>>>(t, fd, sa, k);
-          CB_LAUNCH();
+        if (use_dag) {
+          // tiled Cholesky + inverse panel of every split front (dense_dag.cu)
+          std::vector<int> sids;
+          for (int sid : ts.tpl.levels[(size_t)L])
+            if (ts.tpl.sn[(size_t)sid].nrows >= kSplitRows) sids.push_back(sid);
+          dense_dag_level(h, ts, f, sids, sd0, sd1, foff, poff, front.p, fail.p);
+        } else {
+          for (int k = 0; k < maxc; k += 32) {
+            k_split_diag<<<dim3(ns_, nc_), 32, 0, s>>>(t, fd, sa, k);
+            CB_LAUNCH();
+            const int rows_below = maxr - k - 1;
+            if (rows_below <= 0) continue;
+            k_split_trsm<<<dim3((rows_below + 127) / 128, ns_, nc_), 128, 0, s>>>(t, fd, sa, k);
+            CB_LAUNCH();
+            const int nt = (rows_below + 63) / 64;
+            k_split_syrk<<<dim3(nt * (nt + 1) / 2, ns_, nc_), 256, 0, s>>>(t, fd, sa, k);
+            CB_LAUNCH();
+          }
         }
       }
       if (ts.inv_count[(size_t)L] > 0) {
         ProfScope ps2(h->prof, s, tag + std::to_string(L) + " trinv");
         dim3 gi(ts.inv_count[(size_t)L], sd1 - sd0);
         k_trinv<<<gi, 256, 0, s>>>(t, fd, ts.inv_items.p + ts.inv_first[(size_t)L], sd0, f.front_off.p,
-                                   f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p);
+                                   f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p, use_dag);
         CB_LAUNCH();
       }
       if (ts.gemm_count[(size_t)L] > 0) {
         ProfScope ps3(h->prof, s, tag + std::to_string(L) + " gemm");
         dim3 gg(ts.gemm_count[(size_t)L], sd1 - sd0);
         k_gemm_m<<<gg, 256, 0, s>>>(t, fd, ts.gemm_items.p + ts.gemm_first[(size_t)L], sd0, f.front_off.p,
-                                    f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p);
+                                    f.h_front_base[(size_t)sd0], fbase.p, front.p, f.panel.p, use_dag);
         CB_LAUNCH();
       }
     }

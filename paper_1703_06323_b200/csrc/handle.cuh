@@ -177,6 +177,9 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int64_t> ws_fbase, ws_cnt, ws_nc64;
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp;
   cutbddc_b200::DevBuf<int> ws_flag;
+  cutbddc_b200::DevBuf<long long> ws_dag_fronts;  // dense_dag.cu: per-level front records
+  cutbddc_b200::DevBuf<int4> ws_dag_tasks;
+  cutbddc_b200::DevBuf<int> ws_dag_counters;
 
   // pcg vectors
   cutbddc_b200::DevBuf<double> px, pr, pz, pp, pq, pb, hist, lal, lbe;
