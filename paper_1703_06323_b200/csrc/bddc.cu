@@ -4,11 +4,12 @@
 //                       A^w_xixi / sum_w' A^w'_xixi
 //   build_coarse_space  SPEC.md:379-387  C_w rows (corner e_xi, edge/face
 //                       (1/|lambda|) sum e_xi); constrained
-//                       Neumann solves through K0 = A_w + rho_w C_c^T C_c
-//                       (corner rows only: diagonal, stencil-preserving) and the
-//                       dense constraint Schur complement S = C K0^{-1} C^T:
-//                         Phi = K0^{-1} C^T S^{-1},  saddle solve z = y - Phi C y
-//                       A_c,w = Phi^T A_w Phi assembled in subdomain order.
+//                       Neumann solves through the augmented K = A_w + rho_w C^T C
+//                       (shell-root factorisation, factor.cu) and the constraint
+//                       Schur complement S = C K^{-1} C^T, all in the root space
+//                       of K (k_root_h): Phi = K^{-1} C^T S^{-1} is never formed,
+//                       A_c,w = Phi^T A_w Phi = S^{-1} - rho_w I, assembled in
+//                       subdomain order.
 //   apply               SPEC.md:388-396, expanded in SURVEY.md section 3.2, with
 //                       r1 := 0 on interior rows.
 // Every gather sums in ascending subdomain order; no fp64 atomics.
@@ -110,33 +111,6 @@ __global__ void k_diag_add(int nsd, int T, const int64_t* __restrict__ m_off, co
   }
 }
 
-// X[rhs][sd][T] = C^T e_rhs for rhs in [r0, r0+nr)
-__global__ void k_fill_ct(int nsd, int T, int r0, int nr, const int64_t* __restrict__ m_off,
-                          const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_slot,
-                          const double* __restrict__ c_val, double* __restrict__ X) {
-  const int sd = blockIdx.x, q = blockIdx.y;
-  const int64_t row = m_off[sd] + r0 + q;
-  if (row >= m_off[sd + 1]) return;
-  double* x = X + ((int64_t)q * nsd + sd) * T;
-  for (int64_t p = c_ptr[row] + threadIdx.x; p < c_ptr[row + 1]; p += blockDim.x) x[c_slot[p]] = c_val[p];
-}
-
-// S[sd] (m x m, row-major at ac_off) = C W with W columns in Wall[rhs][sd][T]
-__global__ void k_schur(int nsd, int T, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
-                        const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_slot,
-                        const double* __restrict__ c_val, const double* __restrict__ Wall, double* __restrict__ S) {
-  const int sd = blockIdx.x;
-  const int m = (int)(m_off[sd + 1] - m_off[sd]);
-  for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
-    const int r = q / m, c = q % m;
-    const int64_t row = m_off[sd] + r;
-    const double* wc = Wall + ((int64_t)c * nsd + sd) * T;
-    double v = 0.0;
-    for (int64_t p = c_ptr[row]; p < c_ptr[row + 1]; ++p) v += c_val[p] * wc[c_slot[p]];
-    S[s_off[sd] + q] = v;
-  }
-}
-
 // In-place SPD inverse of each subdomain's m x m block (symmetrised first),
 // Gauss-Jordan without pivoting on the SPD matrix; non-positive pivot -> fail.
 __global__ void k_small_spd_inverse(int nblk, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
@@ -181,66 +155,6 @@ __global__ void k_small_spd_inverse(int nblk, const int64_t* __restrict__ m_off,
     __syncthreads();
   }
   for (int q = threadIdx.x; q < m * m; q += blockDim.x) g[q] = a[q];
-}
-
-// Phi[(m_off[sd]+c)][slot] = sum_r W[r][sd][slot] Sinv[r][c]
-__global__ void k_phi(int nsd, int T, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
-                      const double* __restrict__ Wall, const double* __restrict__ Sinv, double* __restrict__ Phi) {
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= (int64_t)nsd * T) return;
-  const int sd = (int)(g / T), t = (int)(g % T);
-  const int m = (int)(m_off[sd + 1] - m_off[sd]);
-  const double* si = Sinv + s_off[sd];
-  for (int c = 0; c < m; ++c) {
-    double v = 0.0;
-    for (int r = 0; r < m; ++r) v += Wall[((int64_t)r * nsd + sd) * T + t] * si[r * m + c];
-    Phi[(m_off[sd] + c) * T + t] = v;
-  }
-}
-
-// A_c,w[r][c] = Phi_r . (A_w Phi_c): CTA per (sd, c), A Phi_c staged in shared memory
-__global__ void k_local_coarse(int T, int b1, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
-                               const double* __restrict__ As, const double* __restrict__ Phi, double* __restrict__ Ac) {
-  extern __shared__ double ap[];
-  __shared__ double sh[32];
-  const int sd = blockIdx.x, c = blockIdx.y;
-  const int m = (int)(m_off[sd + 1] - m_off[sd]);
-  if (c >= m) return;
-  const double* ph = Phi + (m_off[sd] + c) * T;
-  const double* A = As + (int64_t)sd * 27 * T;
-  for (int u = threadIdx.x; u < T; u += blockDim.x) {
-    const int ux = u / (b1 * b1), uy = (u / b1) % b1, uz = u % b1;
-    double s = 0.0;
-    for (int k = 0; k < 27; ++k) {
-      const int vx = ux + k / 9 - 1, vy = uy + (k / 3) % 3 - 1, vz = uz + k % 3 - 1;
-      if (vx < 0 || vy < 0 || vz < 0 || vx >= b1 || vy >= b1 || vz >= b1) continue;
-      s += A[(int64_t)k * T + u] * ph[(vx * b1 + vy) * b1 + vz];
-    }
-    ap[u] = s;
-  }
-  __syncthreads();
-  for (int r = 0; r < m; ++r) {
-    const double* pr = Phi + (m_off[sd] + r) * T;
-    double s = 0.0;
-    for (int u = threadIdx.x; u < T; u += blockDim.x) s += pr[u] * ap[u];
-    s = block_sum<256>(s, sh);
-    if (threadIdx.x == 0) Ac[s_off[sd] + (int64_t)r * m + c] = s;
-  }
-}
-
-__global__ void k_symmetrize_blocks(int nsd, const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
-                                    double* __restrict__ Ac) {
-  const int sd = blockIdx.x;
-  const int m = (int)(m_off[sd + 1] - m_off[sd]);
-  double* a = Ac + s_off[sd];
-  for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
-    const int r = q / m, c = q % m;
-    if (r < c) {
-      const double v = 0.5 * (a[r * m + c] + a[c * m + r]);
-      a[r * m + c] = v;
-      a[c * m + r] = v;
-    }
-  }
 }
 
 // coarse row lambda: sum over its (sd, local row) copies in ascending sd.
@@ -312,21 +226,6 @@ __global__ void k_scatter_weighted(int64_t ns, const int32_t* __restrict__ slot_
   X[g] = d >= 0 ? w[g] * r1[d] : 0.0;
 }
 
-// gl[row] = Phi_row . X_sd : warp per constraint row
-__global__ void k_phit(int64_t mtot, int T, const int32_t* __restrict__ row_sd, const double* __restrict__ Phi,
-                       const double* __restrict__ X, double* __restrict__ gl, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= mtot) return;
-  const double* ph = Phi + row * T;
-  const double* x = X + (int64_t)row_sd[row] * T;
-  double s = 0.0;
-  for (int t = lane; t < T; t += 32) s += ph[t] * x[t];
-  s = warp_sum(s);
-  if (lane == 0) gl[row] = s;
-}
-
 // cy[row] = C_row . y
 __global__ void k_cy(int64_t mtot, int T, const int32_t* __restrict__ row_sd, const int64_t* __restrict__ c_ptr,
                      const int32_t* __restrict__ c_slot, const double* __restrict__ c_val, const double* __restrict__ Y,
@@ -382,39 +281,6 @@ __global__ void k_coarse_gemv(int nc, const double* __restrict__ Ainv, const dou
   for (; c < nc; c += 32) s0 += a[c] * g[c];
   const double s = warp_sum(s0 + s1);
   if (lane == 0) zc[row] = s;
-}
-
-// (reference path, unused in the apply) zc = A_c^{-1} (sum of the coarse rhs
-// copies) by one CTA of substitution on the Cholesky panel.
-__global__ void __launch_bounds__(512) k_coarse_solve(int nc, const int64_t* __restrict__ cg_ptr,
-                                                      const int64_t* __restrict__ cg_idx, const double* __restrict__ gl,
-                                                      const double* __restrict__ Lcm, double* __restrict__ zc,
-                                                      const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  extern __shared__ double v[];
-  __shared__ double tile[32][33];
-  for (int lam = threadIdx.x; lam < nc; lam += blockDim.x) {
-    double s = 0.0;
-    for (int64_t p = cg_ptr[lam]; p < cg_ptr[lam + 1]; ++p) s += gl[cg_idx[p]];
-    v[lam] = s;
-  }
-  __syncthreads();
-  panel_forward(Lcm, nc, nc, v);
-  panel_backward(Lcm, nc, nc, v, tile);
-  for (int lam = threadIdx.x; lam < nc; lam += blockDim.x) zc[lam] = v[lam];
-}
-
-// y += Phi (zc[coarse_id] - cy), thread per (sd, slot)
-__global__ void k_prolong(int nsd, int T, const int64_t* __restrict__ m_off, const int32_t* __restrict__ coarse_id,
-                          const double* __restrict__ Phi, const double* __restrict__ zc, const double* __restrict__ cy,
-                          double* __restrict__ Y, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= (int64_t)nsd * T) return;
-  const int sd = (int)(g / T), t = (int)(g % T);
-  double s = Y[g];
-  for (int64_t row = m_off[sd]; row < m_off[sd + 1]; ++row) s += Phi[row * T + t] * (zc[coarse_id[row]] - cy[row]);
-  Y[g] = s;
 }
 
 // v[d] = sum over copies (ascending sd) of w * Y
@@ -478,6 +344,170 @@ __global__ void k_final_sum(int64_t nd, const double* __restrict__ z0, const dou
   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (d >= nd) return;
   z[d] = z0[d] + v[d] + c[d];
+}
+
+// ---------------------------------------------------------------- root-space coarse basis
+// The constraint rows live on the shell, i.e. on the root columns of the
+// shell-root factorisation K = L L^T (K = A + rho C^T C), so with G_r the
+// explicit root panel (L_r^{-1}) and C_r the rows on root positions:
+//   H = G_r C_r^T,  S = C K^{-1} C^T = H^T H,  W_r = (K^{-1} C^T)_root = G_r^T H,
+//   A_c,w = Phi^T A Phi = S^{-1} - rho I   (Phi = K^{-1} C^T S^{-1}, K - A = rho C^T C),
+//   Phi^T r = S^{-1} C (K^{-1} r),  Phi v = K^{-1} C^T S^{-1} v.
+// rinfo[4 sd + {0,1,2,3}] = {c_r, root panel offset, root vector offset, H/W offset}.
+__global__ void __launch_bounds__(256) k_root_h(const int64_t* __restrict__ rinfo, const int64_t* __restrict__ m_off,
+                                                const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_slot,
+                                                const double* __restrict__ c_val, const int32_t* __restrict__ root_pos,
+                                                const int32_t* __restrict__ pfx_root, int64_t rows_total,
+                                                const double* __restrict__ panel, double* __restrict__ H) {
+  const int sd = blockIdx.x, a = blockIdx.y;
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  if (a >= m) return;
+  const int cr = (int)rinfo[4 * sd];
+  const double* G = panel + rinfo[4 * sd + 1];
+  double* h = H + rinfo[4 * sd + 3] + (int64_t)a * cr;
+  const int64_t row = m_off[sd] + a;
+  const int32_t* pf = pfx_root + (int64_t)sd * rows_total;
+  // the row's (root column, coefficient) pairs, staged in shared memory
+  __shared__ int cj[512];
+  __shared__ double cv[512];
+  const int64_t p0 = c_ptr[row], len = c_ptr[row + 1] - p0;
+  for (int64_t q0 = 0; q0 < len; q0 += 512) {
+    const int nq = len - q0 < 512 ? (int)(len - q0) : 512;
+    __syncthreads();
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+      cj[q] = pf[root_pos[c_slot[p0 + q0 + q]]];
+      cv[q] = c_val[p0 + q0 + q];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cr; i += blockDim.x) {
+      double s = q0 == 0 ? 0.0 : h[i];
+      for (int q = 0; q < nq; ++q) {
+        const int j = cj[q];
+        if (j >= 0 && i >= j) s += cv[q] * G[i + (int64_t)j * cr];
+      }
+      h[i] = s;
+    }
+  }
+}
+
+// S = H^T H per subdomain (both triangles), warp per (a, b) pair
+__global__ void __launch_bounds__(256) k_root_s(const int64_t* __restrict__ rinfo, const int64_t* __restrict__ m_off,
+                                                const int64_t* __restrict__ s_off, const double* __restrict__ H,
+                                                double* __restrict__ S) {
+  const int sd = blockIdx.x;
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  const int cr = (int)rinfo[4 * sd];
+  const double* h = H + rinfo[4 * sd + 3];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int q = wid; q < m * m; q += blockDim.x / 32) {
+    const int a = q / m, b = q % m;
+    if (b > a) continue;
+    double s = 0.0;
+    for (int i = lane; i < cr; i += 32) s += h[i + (int64_t)a * cr] * h[i + (int64_t)b * cr];
+    s = warp_sum(s);
+    if (lane == 0) {
+      S[s_off[sd] + (int64_t)a * m + b] = s;
+      S[s_off[sd] + (int64_t)b * m + a] = s;
+    }
+  }
+}
+
+// sinv = sym(S^{-1}); A_c,w = sinv - rho I
+__global__ void k_root_coarse(const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
+                              const double* __restrict__ Sinv, const double* __restrict__ rho, double* __restrict__ sinv,
+                              double* __restrict__ ac) {
+  const int sd = blockIdx.x;
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  const int64_t o = s_off[sd];
+  for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
+    const int a = q / m, b = q % m;
+    const double v = 0.5 * (Sinv[o + (int64_t)a * m + b] + Sinv[o + (int64_t)b * m + a]);
+    sinv[o + q] = v;
+    ac[o + q] = v - (a == b ? rho[sd] : 0.0);
+  }
+}
+
+// W_r = G_r^T H: 64 root rows j per CTA, all m columns (<= 64 per pass),
+// G's lower part only (the panel above the diagonal tiles is not stored).
+__global__ void __launch_bounds__(256) k_root_w(const int64_t* __restrict__ rinfo, const int64_t* __restrict__ m_off,
+                                                const double* __restrict__ panel, const double* __restrict__ H,
+                                                double* __restrict__ W) {
+  const int sd = blockIdx.x, j0 = blockIdx.y * 64;
+  const int cr = (int)rinfo[4 * sd];
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  if (j0 >= cr || m == 0) return;
+  const double* G = panel + rinfo[4 * sd + 1];
+  const double* h = H + rinfo[4 * sd + 3];
+  double* w = W + rinfo[4 * sd + 3];
+  __shared__ double gs[32][65], hs[32][65];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int l0 = 0; l0 < m; l0 += 64) {
+    double acc[4][4] = {};
+    for (int i0 = j0; i0 < cr; i0 += 32) {
+      __syncthreads();
+      for (int e = tid; e < 32 * 64; e += 256) {
+        const int ii = e & 31, jj = e >> 5, i = i0 + ii, j = j0 + jj, l = l0 + jj;
+        gs[ii][jj] = (i < cr && j < cr && i >= j) ? G[i + (int64_t)j * cr] : 0.0;
+        hs[ii][jj] = (i < cr && l < m) ? h[i + (int64_t)l * cr] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int ii = 0; ii < 32; ++ii) {
+        double ga[4], hb[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) ga[x] = gs[ii][tx + 16 * x];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) hb[y] = hs[ii][ty + 16 * y];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] += ga[x] * hb[y];
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int j = j0 + tx + 16 * x, l = l0 + ty + 16 * y;
+        if (j < cr && l < m) w[j + (int64_t)l * cr] = acc[x][y];
+      }
+  }
+}
+
+// out[row] = sum_b S^{-1}[a][b] (zc[coarse_id] - cy)[b]   (with_zc)
+//          = sum_b S^{-1}[a][b] cy[b]                       (otherwise)
+__global__ void k_sinv_apply(int64_t mtot, const int32_t* __restrict__ row_sd, const int64_t* __restrict__ m_off,
+                             const int64_t* __restrict__ s_off, const double* __restrict__ sinv,
+                             const int32_t* __restrict__ coarse_id, const double* __restrict__ zc,
+                             const double* __restrict__ cy, double* __restrict__ out, int with_zc,
+                             const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= mtot) return;
+  const int sd = row_sd[row];
+  const int64_t b0 = m_off[sd];
+  const int m = (int)(m_off[sd + 1] - b0), a = (int)(row - b0);
+  const double* si = sinv + s_off[sd] + (int64_t)a * m;
+  double s = 0.0;
+  for (int b = 0; b < m; ++b) s += si[b] * (with_zc ? zc[coarse_id[b0 + b]] - cy[b0 + b] : cy[b0 + b]);
+  out[row] = s;
+}
+
+// X[root columns] += W_r u (the K^{-1} C^T S^{-1}(zc - cy) correction at the root)
+__global__ void k_root_correct(const int64_t* __restrict__ rinfo, const int64_t* __restrict__ m_off,
+                               const int32_t* __restrict__ cslot, const double* __restrict__ W,
+                               const double* __restrict__ u, double* __restrict__ X, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int sd = blockIdx.x;
+  const int cr = (int)rinfo[4 * sd];
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= cr) return;
+  const int64_t b0 = m_off[sd];
+  const int m = (int)(m_off[sd + 1] - b0);
+  const double* w = W + rinfo[4 * sd + 3] + j;
+  double s = 0.0;
+  for (int a = 0; a < m; ++a) s += w[(int64_t)a * cr] * u[b0 + a];
+  X[cslot[rinfo[4 * sd + 2] + j]] += s;
 }
 
 __global__ void k_row_sd(int nsd, const int64_t* __restrict__ m_off, int32_t* __restrict__ row_sd) {
@@ -624,30 +654,43 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     factor_device(h, h->tK, fk, h->fK, "saddle: singular augmented system; constraints do not control the operator kernel");
   }
   const int64_t upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, h->fK.upd_total));
-  // ---- coarse basis
-  h->phi_c.alloc((size_t)std::max<int64_t>(1, h->m_total) * T);
+  // ---- coarse basis in the root space of K (see k_root_h): H, S, S^{-1},
+  // W_r and A_c,w = S^{-1} - rho I; the apply never forms Phi
   h->ac_loc.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
-  ps_host.next("setup 2 W = K^-1 C^T");
+  h->sinv.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
+  ps_host.next("setup 2 root-space coarse basis");
   if (m_max > 0) {
-    DevBuf<double>& Wall = h->ws_wall;
-    DevBuf<double>& upd = h->ws_upd;
-    Wall.alloc((size_t)m_max * ns);
-    Wall.zero(s);
-    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(m_max, (2ll << 30) / 8 / std::max(upd_total, ns)));
-    upd.alloc((size_t)rb * upd_total);
-    DevBuf<double>& ys = h->ws_ys;
-    ys.alloc((size_t)rb * ns);
-    for (int r0 = 0; r0 < m_max; r0 += rb) {
-      const int nr = std::min(rb, m_max - r0);
-      double* X = Wall.p + (int64_t)r0 * ns;
-      k_fill_ct<<<dim3(nsd, nr), 64, 0, s>>>(nsd, T, r0, nr, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, X);
-      CB_LAUNCH();
-      solve_device(h, h->tK, h->fK, X, nr, upd.p, ys.p, nullptr, /*rhs_root_only=*/true);
+    if (!h->has_K) throw Failure(CUTBDDC_INTERNAL, "coarse space without an interface");
+    const int nsn = (int)h->tK.tpl.sn.size(), root = nsn - 1;
+    std::vector<int64_t> rinfo((size_t)4 * nsd);
+    int64_t wtot = 0;
+    int cr_max = 0;
+    for (int sd = 0; sd < nsd; ++sd) {
+      const size_t fs = (size_t)sd * nsn + root;
+      const int cr = h->fK.h_rc[fs].y;
+      if (h->fK.h_rc[fs].x != cr) throw Failure(CUTBDDC_INTERNAL, "shell root with update rows");
+      const int m = (int)(m_off[(size_t)sd + 1] - m_off[(size_t)sd]);
+      rinfo[4 * (size_t)sd] = cr;
+      rinfo[4 * (size_t)sd + 1] = h->fK.h_panel_off[fs];
+      rinfo[4 * (size_t)sd + 2] = h->fK.h_vec_off[fs];
+      rinfo[4 * (size_t)sd + 3] = wtot;
+      wtot += (int64_t)cr * m;
+      cr_max = std::max(cr_max, cr);
     }
-    ps_host.next("setup 3 schur+phi+local coarse");
+    h->root_info.upload(rinfo, s);
+    h->hroot.alloc((size_t)std::max<int64_t>(1, wtot));
+    h->wroot.alloc((size_t)std::max<int64_t>(1, wtot));
+    const int32_t* pfx_root = h->fK.pfx.p + h->tK.tpl.sn[(size_t)root].rows_off;
+    const int64_t rows_total = (int64_t)h->tK.tpl.rows.size();
+    k_root_h<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
+                                              h->tK.root_pos.p, pfx_root, rows_total, h->fK.panel.p, h->hroot.p);
+    CB_LAUNCH();
     DevBuf<double>& S = h->ws_s;
     S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
-    k_schur<<<nsd, 256, 0, s>>>(nsd, T, h->m_off.p, h->ac_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, Wall.p, S.p);
+    k_root_s<<<nsd, 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
+    CB_LAUNCH();
+    k_root_w<<<dim3(nsd, (cr_max + 63) / 64), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.panel.p, h->hroot.p,
+                                                          h->wroot.p);
     CB_LAUNCH();
     DevBuf<unsigned long long>& fail = h->ws_fail;
     fail.alloc(1);
@@ -663,14 +706,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     if (f != ~0ull)
       throw Failure(CUTBDDC_SINGULAR, "saddle: singular constraint Schur complement (subdomain " + std::to_string(f) +
                                           "); constraints are not independent");
-    k_phi<<<grid_for(ns, 128), 128, 0, s>>>(nsd, T, h->m_off.p, h->ac_off.p, Wall.p, S.p, h->phi_c.p);
-    CB_LAUNCH();
-    const size_t shm2 = sizeof(double) * (size_t)T;
-    if (shm2 > 48 * 1024)
-      CB_CUDA(cudaFuncSetAttribute(k_local_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm2));
-    k_local_coarse<<<dim3(nsd, m_max), 256, shm2, s>>>(T, b1, h->m_off.p, h->ac_off.p, h->As.p, h->phi_c.p, h->ac_loc.p);
-    CB_LAUNCH();
-    k_symmetrize_blocks<<<nsd, 256, 0, s>>>(nsd, h->m_off.p, h->ac_off.p, h->ac_loc.p);
+    k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, h->sinv.p, h->ac_loc.p);
     CB_LAUNCH();
   }
   // ---- coarse matrix + factorisation
@@ -717,6 +753,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   if (distributed(h)) h->gv3.alloc((size_t)h->n_dof);
   h->gl.alloc((size_t)std::max<int64_t>(1, h->m_total));
   h->cy.alloc((size_t)std::max<int64_t>(1, h->m_total));
+  h->uvec.alloc((size_t)std::max<int64_t>(1, h->m_total));
   h->zc.alloc((size_t)std::max(1, nc));
   h->gc.alloc((size_t)std::max(1, nc));
   CB_CUDA(cudaStreamSynchronize(s));
@@ -741,16 +778,19 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   CB_LAUNCH();
   k_scatter_weighted<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->w.p, h->gv1.p, h->sv1.p, skip);
   CB_LAUNCH();
-  if (h->m_total > 0) {
-    k_phit<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->phi_c.p, h->sv1.p, h->gl.p, skip);
-    CB_LAUNCH();
-  }
   ps.close();
-  if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
-  ps.next("apply vec 3 cy coarse prolong gather Av");
-  if (h->m_total > 0) {
+  if (h->has_K && h->m_total > 0) {
+    // z~ = K^{-1}(r_w + C^T u), u = S^{-1}(zc - C K^{-1} r_w): forward sweep,
+    // the root's backward step, the coarse problem, the root correction
+    // W_r u, then the backward sweep below the root (see k_root_h)
+    sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepFwd);
+    sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRoot);
+    ps.next("apply vec 3 cy coarse root-correction");
     k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
                                                        h->sv1.p, h->cy.p, skip);
+    CB_LAUNCH();
+    k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
+                                                           h->coarse_id.p, h->zc.p, h->cy.p, h->gl.p, 0, skip);
     CB_LAUNCH();
     k_coarse_rhs<<<grid_for(h->n_coarse, 128), 128, 0, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->gc.p, skip);
     CB_LAUNCH();
@@ -758,9 +798,19 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_inv.p, h->gc.p,
                                                                          h->zc.p, skip);
     CB_LAUNCH();
-    k_prolong<<<grid_for(ns, 256), 256, 0, s>>>(h->nsd, T, h->m_off.p, h->coarse_id.p, h->phi_c.p, h->zc.p, h->cy.p,
-                                                h->sv1.p, skip);
+    k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
+                                                           h->coarse_id.p, h->zc.p, h->cy.p, h->uvec.p, 1, skip);
     CB_LAUNCH();
+    const int cr_blocks = (int)((h->tK.tpl.sn.back().ncols + 255) / 256);
+    k_root_correct<<<dim3(h->nsd, cr_blocks), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.cslot.p, h->wroot.p,
+                                                           h->uvec.p, h->sv1.p, skip);
+    CB_LAUNCH();
+    ps.close();
+    sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRest);
+    ps.next("apply vec 3b gather Av");
+  } else {
+    if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
+    ps.next("apply vec 3b gather Av");
   }
   k_gather_weighted<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->copy_ptr.p, h->copy_idx.p, h->w.p, h->sv1.p, h->gv2.p, skip);
   CB_LAUNCH();

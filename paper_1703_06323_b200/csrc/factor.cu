@@ -896,6 +896,7 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   f.bytes_per_sweep = bytes;
   f.flops = flops;
   f.panel_off.upload(poff, s);
+  f.h_panel_off = poff;
   f.upd_off.upload(uoff, s);
   f.front_off.upload(foff, s);
   DevBuf<int64_t>& fbase = h->ws_fbase;

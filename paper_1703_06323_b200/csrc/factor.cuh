@@ -66,6 +66,9 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
                       const std::vector<int64_t>& uoff);
 void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip);
+enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3 };
+void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
+                 const int* skip, int phase);
 // dense_dag.cu: tiled Cholesky + explicit inverse panel of one level's split
 // fronts (subdomains [sd0, sd1), front workspace based at sd0)
 void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const std::vector<int>& sids, int sd0,

@@ -73,6 +73,9 @@ struct FactorSet {
   cutbddc_b200::DevBuf<unsigned long long> trace;  // CUTBDDC_SWEEP_TRACE only: per-item timestamps
   int64_t vec_total = 0;
   int n_items_f = 0, n_items_b = 0;
+  int n_items_b_root = 0;                      // leading backward items of the root level
+  std::vector<int64_t> h_vec_off;              // nsd x nsn compact front vector offsets (host copy)
+  std::vector<int64_t> h_panel_off;            // nsd x nsn panel offsets (host copy)
 };
 
 struct cutbddc_gpu {
@@ -154,10 +157,16 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int64_t> cg_idx;           // row index into m_total, ascending sd
   cutbddc_b200::DevBuf<double> w;                 // nsd*T
   cutbddc_b200::DevBuf<double> rho;               // nsd
-  cutbddc_b200::DevBuf<double> phi_c;             // m_total*T  (Phi, column per constraint row)
   cutbddc_b200::DevBuf<double> ac_loc;            // per sd m*m (offsets m_off^2 prefix)
   cutbddc_b200::DevBuf<int64_t> ac_off;           // nsd+1
   cutbddc_b200::DevBuf<double> acoarse, acoarse_inv;
+  // root-space coarse basis (bddc.cu): per sd, with c_r root columns of K
+  // and m constraint rows: S^{-1} (m x m, offsets ac_off) and
+  // W_r = (K^{-1})_rr C_r^T (c_r x m, column-major); root_info[sd] =
+  // {c_r, root panel offset, root vector offset (sweep), W_r offset}
+  cutbddc_b200::DevBuf<double> sinv, wroot, hroot;
+  cutbddc_b200::DevBuf<int64_t> root_info;
+  cutbddc_b200::DevBuf<double> uvec;              // m_total: S^{-1}(zc - cy) per constraint row
   bool bddc_ready = false;
   double t_setup = 0;
 

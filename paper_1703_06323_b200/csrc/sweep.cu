@@ -72,7 +72,7 @@ struct SweepDev {
   int32_t* ready_f;
   int32_t* done_b;
   int32_t* ready_b;
-  int32_t* ticket;  // [0] forward, [1] backward
+  int32_t* ticket;  // [0] forward, [1] backward (all, or the root phase), [2] backward below the root
   int32_t* rbcnt;   // forward tile arrivals per (chunked front, row block)
   double* vbuf;
   unsigned long long* trace;  // CUTBDDC_SWEEP_TRACE: per item {grab, deps met, done, sm}, else null
@@ -398,13 +398,13 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
 __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDev p, const int4* __restrict__ items, int n_items,
                                                              const double* __restrict__ panel, double* X,
                                                              const double* __restrict__ ysave,
-                                                             const int* __restrict__ skip) {
+                                                             const int* __restrict__ skip, int ticket_slot) {
   if (skip && *skip) return;
   extern __shared__ double w[];
   __shared__ double part[kWarps][33];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (bool first = true;; first = false) {
-    const int it = next_item(p, p.ticket + 1, first);
+    const int it = next_item(p, p.ticket + ticket_slot, first);
     if (it >= n_items) return;
     const int4 iw = items[it];
     const int kind = iw.x, sid = iw.y, sd = iw.z, chunk = iw.w;
@@ -496,7 +496,7 @@ SweepDev sweep_dev(const FactorSet& f, int nsd, int nsn, unsigned long long* tra
                   cnt + 2 * n,
                   cnt + 3 * n,
                   cnt + 4 * n,
-                  cnt + 4 * n + 2,
+                  cnt + 4 * n + 3,
                   const_cast<double*>(f.vbuf.p),
                   trace};
 }
@@ -607,6 +607,7 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
       nb[i] = v.x == 0 ? 0 : (small || v.y == 0) ? 1 : (v.y + kBwdCols - 1) / kBwdCols;
     }
   f.vec_total = tot;
+  f.h_vec_off = voff;
   // forward tiles of chunked fronts: partial storage (after the front
   // vectors in vbuf) and one arrival counter per row block
   auto mcb_of = [](int c) { return std::max(1, (c + kFwdCols - 1) / kFwdCols); };
@@ -695,7 +696,10 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   };
   subtree_items(fw);
   for (int L = lsub - 1; L >= 0; --L) front_items(L, true, fw);  // leaves first
-  for (int L = 0; L < lsub; ++L) front_items(L, false, bw);     // root first
+  for (int L = 0; L < lsub; ++L) {  // root first
+    front_items(L, false, bw);
+    if (L == 0) f.n_items_b_root = (int)bw.size();
+  }
   subtree_items(bw);
   f.n_items_f = (int)fw.size();
   f.n_items_b = (int)bw.size();
@@ -711,7 +715,7 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   f.cslot.alloc((size_t)std::max<int64_t>(1, tot));
   f.umap.alloc((size_t)std::max<int64_t>(1, f.upd_total));
   f.vbuf.alloc((size_t)std::max<int64_t>(1, ptot));
-  f.counters.alloc((size_t)4 * nsd * nsn + 2 + nrb_tot);
+  f.counters.alloc((size_t)4 * nsd * nsn + 3 + nrb_tot);
   const TplDev t = tpl_dev(ts, h->slots);
   k_sweep_maps<<<dim3(nsn, nsd), 256, 0, s>>>(t, factor_dev(f), reinterpret_cast<const FrontDesc*>(f.desc.p),
                                               f.cslot.p, f.umap.p);
@@ -719,10 +723,12 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   CB_CUDA(cudaStreamSynchronize(s));  // the host vectors above are pageable and go out of scope
 }
 
-// In-place solve of one right-hand side X (nsd x T slot vector): two launches
-// (plus the counter reset) for the whole elimination tree of every subdomain.
-void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
-                 const int* skip) {
+// In-place solve of one right-hand side X (nsd x T slot vector) in phases:
+// kSweepFwd resets the counters and runs the forward sweep; kSweepBwd the
+// whole backward sweep; kSweepBwdRoot / kSweepBwdRest split it after the
+// root level (the BDDC apply corrects the root solution in between).
+void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
+                 const int* skip, int phase) {
   cudaStream_t s = h->stream;
   const int nsd = h->nsd, nsn = (int)ts.tpl.sn.size();
   const char* tp = trace_prefix();
@@ -737,25 +743,33 @@ void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
     attr = true;
   }
   const std::string tag = std::string("sweep") + (&ts == &h->tI ? "I" : "K");
-  CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
-  {
+  if (phase == kSweepFwd) {
+    CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
     ProfScope ps(h->prof, s, tag + " fwd");
     if (f.n_items_f > 0) {
       const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd));
       k_sweep_fwd<<<g, kThreadsSweep, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, skip);
       CB_LAUNCH();
     }
+    if (tp) dump_trace(std::string(tp) + "_" + tag + "_fwd.bin", f, true, s);
+    return;
   }
-  if (tp) dump_trace(std::string(tp) + "_" + tag + "_fwd.bin", f, true, s);
-  {
-    ProfScope ps(h->prof, s, tag + " bwd");
-    if (f.n_items_b > 0) {
-      const int g = std::min(f.n_items_b, sweep_grid((const void*)k_sweep_bwd));
-      k_sweep_bwd<<<g, kThreadsSweep, shm, s>>>(p, f.items_b.p, f.n_items_b, f.panel.p, X, ysave, skip);
-      CB_LAUNCH();
-    }
+  int b0 = 0, b1 = f.n_items_b, slot = 1;
+  if (phase == kSweepBwdRoot) b1 = f.n_items_b_root;
+  if (phase == kSweepBwdRest) b0 = f.n_items_b_root, slot = 2;
+  ProfScope ps(h->prof, s, tag + " bwd");
+  if (b1 > b0) {
+    const int g = std::min(b1 - b0, sweep_grid((const void*)k_sweep_bwd));
+    k_sweep_bwd<<<g, kThreadsSweep, shm, s>>>(p, f.items_b.p + b0, b1 - b0, f.panel.p, X, ysave, skip, slot);
+    CB_LAUNCH();
   }
-  if (tp) dump_trace(std::string(tp) + "_" + tag + "_bwd.bin", f, false, s);
+  if (tp && phase == kSweepBwd) dump_trace(std::string(tp) + "_" + tag + "_bwd.bin", f, false, s);
+}
+
+void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
+                 const int* skip) {
+  sweep_phase(h, ts, f, X, ysave, upd, skip, kSweepFwd);
+  sweep_phase(h, ts, f, X, ysave, upd, skip, kSweepBwd);
 }
 
 }  // namespace cutbddc_b200
