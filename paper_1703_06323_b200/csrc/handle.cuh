@@ -65,6 +65,7 @@ struct FactorSet {
   cutbddc_b200::DevBuf<int4> desc;             // nsd x nsn front descriptors (6 x int4 each, sweep.cu)
   cutbddc_b200::DevBuf<int32_t> cslot;         // vec_total: slot of each compact front row
   cutbddc_b200::DevBuf<int32_t> umap;          // upd_total: parent compact row of each update entry
+  cutbddc_b200::DevBuf<int32_t> gmap;          // 2 x vec_total: child 0 / 1 update entry of each front row (-1: none)
   cutbddc_b200::DevBuf<int4> items_f, items_b; // (kind, supernode, subdomain, chunk) in dependency order
   cutbddc_b200::DevBuf<int32_t> counters;      // done_f | ready_f | done_b | ready_b | tickets
   cutbddc_b200::DevBuf<double> vbuf;           // vec_total: assembled vectors of chunked fronts

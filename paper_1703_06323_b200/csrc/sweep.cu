@@ -35,8 +35,9 @@ namespace cutbddc_b200 {
 namespace {
 
 constexpr int kSmallRows = 256;  // S items and subtree fronts
+constexpr int kSmallWork = 8192; // S items: at most this many panel entries (r x c), else A + C tiles
 constexpr int kFwdRows = 128;    // C items forward: 128 x 128 tiles (four rows per lane)
-constexpr int kFwdCols = 128;
+constexpr int kFwdCols = 64;
 constexpr int kBwdCols = 16;     // C items backward: columns per CTA (two per warp)
 constexpr int kSubLevels = 3;    // T items: the bottom levels of the elimination tree
 constexpr int kThreadsSweep = 256;
@@ -46,6 +47,10 @@ constexpr int kVecDoubles = 2048;                   // front vector: >= every te
 constexpr int kPartDoubles = kWarps * kSmallRows;   // per-warp row partials of the forward GEMV
 constexpr int kShmDoubles = kVecDoubles + kPartDoubles;
 enum { kItemS = 0, kItemA = 1, kItemC = 2, kItemT = 3 };
+
+// one CTA per front (S) or gather + tiles (A/C): wide fronts need the tiles'
+// parallelism (one CTA would issue r c / 256 dependent loads per thread)
+inline bool is_small(int2 rc) { return rc.x <= kSmallRows && (int64_t)rc.x * rc.y <= kSmallWork; }
 
 // Everything one (subdomain, front) needs, in one 96-byte record.
 struct __align__(16) FrontDesc {
@@ -65,6 +70,7 @@ struct SweepDev {
   const FrontDesc* desc;
   const int32_t* cslot;  // sd * T + slot of every compact front row
   const int32_t* umap;   // parent compact row of every update entry
+  const int32_t* gmap;   // per compact front row: upd index of child 0 / child 1 entry landing there, or -1
   const int32_t* sub_sids;
   const int32_t* sub_meta;
   int nsn;
@@ -171,20 +177,20 @@ __device__ __forceinline__ double reduce_scatter16(double (&acc)[16], int lane) 
   return acc[0];
 }
 
-// v[umap] += child updates (children in order; `cross`: produced by other CTAs)
-__device__ __forceinline__ void add_child_updates(const SweepDev& p, const FrontDesc& d, const double* upd, double* v,
-                                                  bool cross) {
-  const int tid = threadIdx.x;
-  if (d.nch > 0) {
-    for (int a = tid; a < d.cnu0; a += kThreadsSweep)
-      v[p.umap[d.cuo0 + a]] += cross ? __ldcg(upd + d.cuo0 + a) : upd[d.cuo0 + a];
-    __syncthreads();
-  }
-  if (d.nch > 1) {
-    for (int a = tid; a < d.cnu1; a += kThreadsSweep)
-      v[p.umap[d.cuo1 + a]] += cross ? __ldcg(upd + d.cuo1 + a) : upd[d.cuo1 + a];
-    __syncthreads();
-  }
+// The children's update entries landing on compact row q of a front
+// (gmap: child 0, child 1 indices into upd, -1 if none), added in child
+// order to b (or 0 at the update rows). `cross`: produced by other CTAs.
+__device__ __forceinline__ double child_sum(const SweepDev& p, const FrontDesc& d, const double* upd, int q, double v,
+                                            bool cross) {
+  const int2 g = reinterpret_cast<const int2*>(p.gmap)[d.vo + q];
+  if (g.x >= 0) v += cross ? __ldcg(upd + g.x) : upd[g.x];
+  if (g.y >= 0) v += cross ? __ldcg(upd + g.y) : upd[g.y];
+  return v;
+}
+
+__device__ __forceinline__ void wait_children(const SweepDev& p, const FrontDesc& d) {
+  if (d.nch > 0) cta_wait(p, p.done_f + d.cfs0, d.cnf0);
+  if (d.nch > 1) cta_wait(p, p.done_f + d.cfs1, d.cnf1);
 }
 
 // Forward GEMV o[i] = sum_j G[i + j r] v[j] for rows [i0, i1) (at most 32 R)
@@ -194,7 +200,7 @@ __device__ __forceinline__ void add_child_updates(const SweepDev& p, const Front
 // Row blocks entirely above column j are skipped (zero part of L11^{-1}).
 // The first column of every warp is loaded before `between()` (which
 // completes v: dependency wait + children's updates).
-template <int R, typename Between, typename Out>
+template <int R, int U, typename Between, typename Out>
 __device__ __forceinline__ void cta_gemv_fwd(const double* __restrict__ G, int r, int jlo, int jhi, int i0, int i1,
                                              double* v, double* part, Between between, Out out) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -211,7 +217,7 @@ __device__ __forceinline__ void cta_gemv_fwd(const double* __restrict__ G, int r
   const double v0 = ja < jb ? v[ja] : 0.0;
 #pragma unroll
   for (int k = 0; k < R; ++k) acc[k] *= v0;
-#pragma unroll 2
+#pragma unroll U
   for (int j = ja + 1; j < jb; ++j) {
     const double vj = v[j];
     const double* gj = gl + (int64_t)j * r;
@@ -241,15 +247,13 @@ __device__ void cta_front_fwd(const SweepDev& p, const FrontDesc& d, const doubl
   const int32_t* cs = p.cslot + d.vo;
   for (int q = tid; q < r; q += kThreadsSweep) v[q] = q < c ? X[cs[q]] : 0.0;
   double* uo = upd + d.uo;
-  cta_gemv_fwd<kSmallRows / 32>(
+  cta_gemv_fwd<kSmallRows / 32, 2>(
       panel + d.po, r, 0, c, 0, r, v, v + kVecDoubles,
       [&] {
-        if (wait) {
-          if (d.nch > 0) cta_wait(p, p.done_f + d.cfs0, d.cnf0);
-          if (d.nch > 1) cta_wait(p, p.done_f + d.cfs1, d.cnf1);
-        }
+        if (wait) wait_children(p, d);
         __syncthreads();
-        add_child_updates(p, d, upd, v, wait);
+        for (int q = tid; q < r; q += kThreadsSweep) v[q] = child_sum(p, d, upd, q, v[q], wait);
+        __syncthreads();
       },
       [&](int i, double o) {
         if (i < c)
@@ -344,30 +348,23 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
     }
     const int r = d.r, c = d.c;
     const int32_t* cs = p.cslot + d.vo;
-    if (kind == kItemA) {
-      for (int q = tid; q < r; q += kThreadsSweep) v[q] = q < c ? X[cs[q]] : 0.0;
-      if (d.nch > 0) cta_wait(p, p.done_f + d.cfs0, d.cnf0);
-      if (d.nch > 1) cta_wait(p, p.done_f + d.cfs1, d.cnf1);
-      __syncthreads();
-      add_child_updates(p, d, upd, v, true);
-      for (int q = tid; q < r; q += kThreadsSweep) p.vbuf[d.vo + q] = v[q];
-      cta_signal(p.ready_f + fs);
-      continue;
-    }
-    // C: tile (row block rb, column block cb) of a chunked front. Partial row
-    // sums go to vbuf; the last tile of a row block to arrive sums them in
-    // column-block order (deterministic) and writes the rows.
+    // C: tile (row block rb, column block cb) of a chunked front: its own
+    // gather of v at the tile's columns, partial row sums to vbuf; the last
+    // tile of a row block to arrive sums them in column-block order
+    // (deterministic) and writes the rows.
     const int mcb = max(1, (c + kFwdCols - 1) / kFwdCols);
     const int rb = chunk / mcb, cb = chunk % mcb;
     const int i0 = rb * kFwdRows, i1 = min(r, i0 + kFwdRows);
     const int jrow = min(c, i1);
     const int jlo = cb * kFwdCols, jhi = min(jrow, jlo + kFwdCols);
     double* tp = p.vbuf + d.tpo + (int64_t)rb * mcb * kFwdRows;
-    cta_gemv_fwd<kFwdRows / 32>(
+    for (int q = jlo + tid; q < jhi; q += kThreadsSweep) v[q] = X[cs[q]];
+    cta_gemv_fwd<kFwdRows / 32, 4>(
         panel + d.po, r, jlo, jhi, i0, i1, v, v + kVecDoubles,
         [&] {
-          cta_wait(p, p.ready_f + fs, 1);
-          for (int q = jlo + tid; q < jhi; q += kThreadsSweep) v[q] = __ldcg(p.vbuf + d.vo + q);
+          wait_children(p, d);
+          __syncthreads();
+          for (int q = jlo + tid; q < jhi; q += kThreadsSweep) v[q] = child_sum(p, d, upd, q, v[q], true);
           __syncthreads();
         },
         [&](int i, double o) { tp[(int64_t)cb * kFwdRows + i - i0] = o; });
@@ -389,7 +386,7 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
       if (i < c)
         ysave[cs[i]] = o;
       else
-        uo[i - c] = __ldcg(p.vbuf + d.vo + i) - o;
+        uo[i - c] = child_sum(p, d, upd, i, 0.0, true) - o;
     }
     cta_signal(p.done_f + fs);
   }
@@ -428,19 +425,14 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDe
     }
     const int r = d.r, c = d.c;
     const int32_t* cs = p.cslot + d.vo;
-    if (kind == kItemA) {
-      for (int q = tid; q < c; q += kThreadsSweep) p.vbuf[d.vo + q] = ysave[cs[q]];
-      if (d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
-      for (int q = c + tid; q < r; q += kThreadsSweep) p.vbuf[d.vo + q] = -__ldcg(X + cs[q]);
-      cta_signal(p.ready_b + fs);
-      continue;
-    }
-    // C: columns [j0, j1) of a chunked front, one warp per column
+    // C: columns [j0, j1) of a chunked front, one warp per column; each item
+    // gathers [y; -x_rest] itself (rows from j0 on: the columns' G is zero above)
     const double* G = panel + d.po;
-    cta_wait(p, p.ready_b + fs, 1);
-    for (int q = tid; q < r; q += kThreadsSweep) w[q] = __ldcg(p.vbuf + d.vo + q);
-    __syncthreads();
     const int j0 = chunk * kBwdCols, j1 = min(c, j0 + kBwdCols);
+    for (int q = j0 + tid; q < c; q += kThreadsSweep) w[q] = ysave[cs[q]];
+    if (d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
+    for (int q = max(c, j0) + tid; q < r; q += kThreadsSweep) w[q] = -__ldcg(X + cs[q]);
+    __syncthreads();
     for (int j = j0 + wid; j < j1; j += kWarps) {
       const double* col = G + (int64_t)j * r;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -459,9 +451,10 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDe
   }
 }
 
-// compact slot of every front row, and the parent position of every update entry
+// compact slot of every front row, the parent position of every update entry
+// (umap) and its inverse (gmap: per parent row, the entry of child 0 / 1)
 __global__ void k_sweep_maps(TplDev t, FactorDev f, const FrontDesc* __restrict__ desc, int32_t* __restrict__ cslot,
-                             int32_t* __restrict__ umap) {
+                             int32_t* __restrict__ umap, int32_t* __restrict__ gmap) {
   const int sid = blockIdx.x, sd = blockIdx.y;
   const Supernode s = t.sn[sid];
   const int64_t fs = (int64_t)sd * t.nsn + sid;
@@ -476,9 +469,14 @@ __global__ void k_sweep_maps(TplDev t, FactorDev f, const FrontDesc* __restrict_
   const int32_t* ppf = f.pfx + (int64_t)sd * t.rows_total + ps.rows_off;
   const int c = desc[fs].c;
   const int64_t uo = desc[fs].uo;
+  const int64_t pvo = desc[(int64_t)sd * t.nsn + s.parent].vo;
+  const int chx = ps.child[0] == sid ? 0 : 1;
   for (int a = threadIdx.x; a < s.nrows - s.ncols; a += blockDim.x) {
     const int ia = pf[s.ncols + a];
-    if (ia >= 0) umap[uo + ia - c] = ppf[t.emap[s.emap_off + a]];
+    if (ia < 0) continue;
+    const int pp = ppf[t.emap[s.emap_off + a]];
+    umap[uo + ia - c] = pp;
+    gmap[2 * (pvo + pp) + chx] = (int32_t)(uo + ia - c);
   }
 }
 
@@ -488,6 +486,7 @@ SweepDev sweep_dev(const FactorSet& f, int nsd, int nsn, unsigned long long* tra
   return SweepDev{reinterpret_cast<const FrontDesc*>(f.desc.p),
                   f.cslot.p,
                   f.umap.p,
+                  f.gmap.p,
                   f.sub_sids.p,
                   f.sub_meta.p,
                   nsn,
@@ -602,7 +601,7 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
         nf[i] = meta_of[(size_t)q] >= 0 ? 1 : 0;
         continue;
       }
-      const bool small = v.x <= kSmallRows;
+      const bool small = is_small(v);
       nf[i] = v.x == 0 ? 0 : small ? 1 : (v.x + kFwdRows - 1) / kFwdRows;
       nb[i] = v.x == 0 ? 0 : (small || v.y == 0) ? 1 : (v.y + kBwdCols - 1) / kBwdCols;
     }
@@ -620,7 +619,7 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   int32_t nrb_tot = 0;
   for (size_t i = 0; i < (size_t)nsd * nsn; ++i) {
     const int2 v = f.h_rc[i];
-    if (in_sub[i % (size_t)nsn] || v.x <= kSmallRows) continue;
+    if (in_sub[i % (size_t)nsn] || is_small(v)) continue;
     const int nrb = (v.x + kFwdRows - 1) / kFwdRows;
     tpo[i] = ptot;
     ptot += (int64_t)nrb * mcb_of(v.y) * kFwdRows;
@@ -672,14 +671,13 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
     for (int sid : lv[(size_t)L])
       for (int sd = 0; sd < nsd; ++sd) {
         const int2 v = f.h_rc[(size_t)sd * nsn + sid];
-        if (v.x > 0)
-          out.push_back(make_int4(v.x <= kSmallRows || (!fwd && v.y == 0) ? kItemS : kItemA, sid, sd, 0));
+        if (v.x > 0 && (is_small(v) || (!fwd && v.y == 0))) out.push_back(make_int4(kItemS, sid, sd, 0));
       }
     for (int sid : lv[(size_t)L])
       for (int sd = 0; sd < nsd; ++sd) {
         const size_t i = (size_t)sd * nsn + sid;
         const int2 v = f.h_rc[i];
-        if (v.x <= kSmallRows) continue;
+        if (is_small(v)) continue;
         if (fwd) {
           const int mcb = mcb_of(v.y);
           for (int rb = 0; rb < nf[i]; ++rb)
@@ -714,11 +712,14 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   f.sub_meta.upload(meta, s);
   f.cslot.alloc((size_t)std::max<int64_t>(1, tot));
   f.umap.alloc((size_t)std::max<int64_t>(1, f.upd_total));
+  if (f.upd_total >= (1ll << 31)) throw Failure(CUTBDDC_CONFIG, "sweep: update workspace exceeds 32-bit indexing");
+  f.gmap.alloc((size_t)2 * std::max<int64_t>(1, tot));
+  CB_CUDA(cudaMemsetAsync(f.gmap.p, 0xff, sizeof(int32_t) * f.gmap.n, s));
   f.vbuf.alloc((size_t)std::max<int64_t>(1, ptot));
   f.counters.alloc((size_t)4 * nsd * nsn + 3 + nrb_tot);
   const TplDev t = tpl_dev(ts, h->slots);
   k_sweep_maps<<<dim3(nsn, nsd), 256, 0, s>>>(t, factor_dev(f), reinterpret_cast<const FrontDesc*>(f.desc.p),
-                                              f.cslot.p, f.umap.p);
+                                              f.cslot.p, f.umap.p, f.gmap.p);
   CB_LAUNCH();
   CB_CUDA(cudaStreamSynchronize(s));  // the host vectors above are pageable and go out of scope
 }
