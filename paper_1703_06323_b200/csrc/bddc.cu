@@ -80,25 +80,29 @@ __global__ void k_weights(int64_t ns, int T, int mode, const int32_t* __restrict
 // sequentially in ascending local dof (= slot) order: K = A + rho C^T C of a
 // small-cut subdomain is so ill-conditioned that a 1-ulp change of rho moves
 // the saddle solutions by ~1e-9, so rho is pinned bit-for-bit to the CPU
-// restatement's order. One warp per subdomain: coalesced loads of 32 slots,
-// then the 32 values are added in slot order (absent slots add +0.0, which
-// leaves the running sum unchanged).
-__global__ void k_rho(int nsd, int T, const int32_t* __restrict__ slot_dof, const double* __restrict__ As,
-                      double* __restrict__ rho) {
-  const int sd = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (sd >= nsd) return;
-  double s = 0.0;
-  long long c = 0;
-  for (int base = 0; base < T; base += 32) {
-    const int t = base + lane;
-    const bool p = t < T && slot_dof[(int64_t)sd * T + t] >= 0;
-    const double v = p ? As[(int64_t)sd * 27 * T + 13ll * T + t] : 0.0;
-    c += __popc(__ballot_sync(0xffffffffu, p));
-#pragma unroll
-    for (int l = 0; l < 32; ++l) s += __shfl_sync(0xffffffffu, v, l);
+// restatement's order. One CTA per subdomain stages the diagonal in shared
+// memory (coalesced, absent slots as +0.0, which leaves the running sum
+// unchanged), then thread 0 adds it in slot order.
+__global__ void __launch_bounds__(256) k_rho(int nsd, int T, const int32_t* __restrict__ slot_dof,
+                                             const double* __restrict__ As, double* __restrict__ rho) {
+  extern __shared__ double dg[];
+  __shared__ int cnt;
+  const int sd = blockIdx.x;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int c = 0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const bool p = slot_dof[(int64_t)sd * T + t] >= 0;
+    dg[t] = p ? As[(int64_t)sd * 27 * T + 13ll * T + t] : 0.0;
+    c += p;
   }
-  if (lane == 0) rho[sd] = c > 0 ? s / (double)c : 1.0;
+  atomicAdd(&cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int t = 0; t < T; ++t) s += dg[t];
+    rho[sd] = cnt > 0 ? s / (double)cnt : 1.0;
+  }
 }
 
 __global__ void k_diag_add(int nsd, int T, const int64_t* __restrict__ m_off, const int64_t* __restrict__ c_ptr,
@@ -390,18 +394,17 @@ __global__ void __launch_bounds__(256) k_root_h(const int64_t* __restrict__ rinf
   }
 }
 
-// S = H^T H per subdomain (both triangles), warp per (a, b) pair
+// S = H^T H per subdomain (both triangles): CTA per (sd, row a), warp per b <= a
 __global__ void __launch_bounds__(256) k_root_s(const int64_t* __restrict__ rinfo, const int64_t* __restrict__ m_off,
                                                 const int64_t* __restrict__ s_off, const double* __restrict__ H,
                                                 double* __restrict__ S) {
-  const int sd = blockIdx.x;
+  const int sd = blockIdx.x, a = blockIdx.y;
   const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  if (a >= m) return;
   const int cr = (int)rinfo[4 * sd];
   const double* h = H + rinfo[4 * sd + 3];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int q = wid; q < m * m; q += blockDim.x / 32) {
-    const int a = q / m, b = q % m;
-    if (b > a) continue;
+  for (int b = wid; b <= a; b += blockDim.x / 32) {
     double s = 0.0;
     for (int i = lane; i < cr; i += 32) s += h[i + (int64_t)a * cr] * h[i + (int64_t)b * cr];
     s = warp_sum(s);
@@ -627,7 +630,9 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   k_masks<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->ncount.p, h->mask_all.p, h->mask_int.p);
   CB_LAUNCH();
   h->rho.alloc((size_t)nsd);
-  k_rho<<<grid_for((int64_t)nsd * 32, 128), 128, 0, s>>>(nsd, T, h->slot_dof.p, h->As.p, h->rho.p);
+  const size_t rho_shm = sizeof(double) * (size_t)T;
+  if (rho_shm > 48 * 1024) CB_CUDA(cudaFuncSetAttribute(k_rho, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rho_shm));
+  k_rho<<<nsd, 256, rho_shm, s>>>(nsd, T, h->slot_dof.p, h->As.p, h->rho.p);
   CB_LAUNCH();
   h->diag_add.alloc((size_t)ns);
   h->diag_add.zero(s);
@@ -687,7 +692,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     CB_LAUNCH();
     DevBuf<double>& S = h->ws_s;
     S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
-    k_root_s<<<nsd, 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
+    k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
     CB_LAUNCH();
     k_root_w<<<dim3(nsd, (cr_max + 63) / 64), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.panel.p, h->hroot.p,
                                                           h->wroot.p);

@@ -409,6 +409,7 @@ void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const
                      unsigned long long* fail) {
   cudaStream_t s = h->stream;
   const int nsn = (int)ts.tpl.sn.size();
+  ProfScope ps(h->prof, s, "dense dag host+upload");
   std::vector<DagFront> fr;
   int64_t cnt = 0;
   for (int sd = sd0; sd < sd1; ++sd)
@@ -489,6 +490,7 @@ void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const
     CB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     grid = std::max(1, per_sm) * sms;
   }
+  ps.next("dense dag kernel");
   k_dense_dag<<<std::min<int>(grid, (int)tasks.size()), kDagThreads, shm, s>>>(a);
   CB_LAUNCH();
   CB_CUDA(cudaStreamSynchronize(s));  // host task vectors go out of scope

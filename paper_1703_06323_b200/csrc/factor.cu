@@ -180,7 +180,11 @@ __global__ void __launch_bounds__(kThreads) k_factor_level(TplDev t, FactorDev f
 // launches per 32-column panel step so that many CTAs share one front:
 // (1) the diagonal block, (2) the panel rows below it in 128-row chunks,
 // (3) the rank-32 update of the trailing lower triangle in 64x64 tiles.
-constexpr int kSplitRows = 600;
+// (CUTBDDC_SPLIT_ROWS overrides, for measurements)
+static const int kSplitRows = [] {
+  const char* e = std::getenv("CUTBDDC_SPLIT_ROWS");
+  return e ? std::max(64, std::atoi(e)) : 600;
+}();
 
 struct SplitArgs {
   const int32_t* sn;          // split supernodes of this level
@@ -868,6 +872,7 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   f.tpos.alloc((size_t)nsd * t.rows_total);
   f.rc.alloc((size_t)nsd * nsn);
   ProfScope psym(h->prof, s, std::string("factor") + (&ts == &h->tI ? "I" : "K") + " total");
+  ProfScope pplan(h->prof, s, std::string("factor") + (&ts == &h->tI ? "I" : "K") + " symbolic+plan");
   k_symbolic<<<dim3(nsn, nsd), kThreads, 0, s>>>(t, nsd, in.mask, f.pfx.p, f.tpos.p, f.rc.p);
   CB_LAUNCH();
   f.h_rc = f.rc.to_host(s);
@@ -903,6 +908,7 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   fbase.upload(f.h_front_base, s);
   f.panel.alloc((size_t)std::max<int64_t>(1, pt));
   build_sweep_plan(h, ts, f, poff, uoff);
+  pplan.close();
   const FactorDev fd = factor_dev(f);
   // numeric, in subdomain chunks bounded by a front-workspace budget
   const int64_t budget = (3ll << 30) / 8;

@@ -348,7 +348,7 @@ class GpuSolver:
         of one BDDC apply) and its algorithmic bytes."""
         sec, byt = C.c_double(), C.c_double()
         _check(lib().cutbddc_gpu_time_solves(self.h, reps, C.byref(sec), C.byref(byt)))
-        return dict(kernel="k_fwd_big+k_bwd_big+k_fwd_level+k_bwd_level (3 front solves of one BDDC apply)",
+        return dict(kernel="k_sweep_fwd+k_sweep_bwd (3 triangular solves of one BDDC apply)",
                     seconds=sec.value, bytes=byt.value)
 
     def stats(self):
