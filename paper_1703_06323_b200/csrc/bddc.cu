@@ -268,6 +268,50 @@ __global__ void __launch_bounds__(256) k_coarse_invert(int nc, const double* __r
   for (int i = threadIdx.x; i < nc; i += blockDim.x) Ainv[(int64_t)j * nc + i] = v[i];
 }
 
+// A_c^{-1} = X^T X with X = L^{-1} (lower, column-major, from the dense DAG;
+// entries above X's diagonal tiles are not stored and are masked here).
+// 64 x 64 output tiles of the lower triangle, mirrored.
+__global__ void __launch_bounds__(256) k_xtx(int n, const double* __restrict__ X, double* __restrict__ C) {
+  const int ib = blockIdx.x, jb = blockIdx.y;
+  if (jb > ib) return;
+  const int i0 = ib * 64, j0 = jb * 64;
+  __shared__ double xa[32][65], xb[32][65];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double acc[4][4] = {};
+  for (int k0 = i0; k0 < n; k0 += 32) {  // X[k, i] = 0 for k < i, and i >= j
+    __syncthreads();
+    for (int e = tid; e < 32 * 64; e += 256) {
+      const int kk = e & 31, c = e >> 5, k = k0 + kk;
+      const int i = i0 + c, j = j0 + c;
+      xa[kk][c] = (k < n && i < n && k >= i) ? X[k + (int64_t)i * n] : 0.0;
+      xb[kk][c] = (k < n && j < n && k >= j) ? X[k + (int64_t)j * n] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = xa[kk][tx + 16 * x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) b[y] = xb[kk][ty + 16 * y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] += a[x] * b[y];
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int i = i0 + tx + 16 * x, j = j0 + ty + 16 * y;
+      if (i < n && j < n && j <= i) {
+        C[(int64_t)i * n + j] = acc[x][y];
+        C[(int64_t)j * n + i] = acc[x][y];
+      }
+    }
+}
+
 // zc = A_c^{-1} g: warp per row of the (symmetric) explicit inverse.
 __global__ void k_coarse_gemv(int nc, const double* __restrict__ Ainv, const double* __restrict__ g,
                               double* __restrict__ zc, const int* __restrict__ skip) {
@@ -724,21 +768,21 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
                                          h->coarse_id.p, h->ac_loc.p, h->acoarse.p);
     CB_LAUNCH();
     allreduce_sum(h, h->acoarse.p, (size_t)nc * nc);  // SPEC.md:386 sum over all subdomains
-    // Cholesky panel of A_c (column-major), then the explicit inverse by
-    // parallel column solves; the apply multiplies by it (one GEMV).
+    // Cholesky of A_c and X = L^{-1} by the tiled dense DAG (A_c is
+    // symmetric, so its row-major buffer is its column-major lower part),
+    // then the explicit inverse A_c^{-1} = X^T X; the apply multiplies by it
+    // (one GEMV).
     DevBuf<double>& Lc = h->ws_lc;
     Lc.alloc((size_t)nc * nc);
     CB_CUDA(cudaMemcpyAsync(Lc.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
+    DevBuf<double>& Xc = h->ws_xc;
+    Xc.alloc((size_t)nc * nc);
     DevBuf<unsigned long long>& fail = h->ws_fail;
     fail.alloc(1);
     CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
-    k_coarse_chol<<<1, 256, 0, s>>>(nc, Lc.p, fail.p);
-    CB_LAUNCH();
-    const size_t shm = sizeof(double) * (size_t)nc;
-    if (shm > 200 * 1024) throw Failure(CUTBDDC_CONFIG, "coarse problem too large for the coarse inverse");
-    if (shm > 48 * 1024)
-      CB_CUDA(cudaFuncSetAttribute(k_coarse_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_coarse_invert<<<nc, 256, shm, s>>>(nc, Lc.p, h->acoarse_inv.p);
+    dense_dag_matrix(h, Lc.p, Xc.p, nc, fail.p);
+    const int nb64 = (nc + 63) / 64;
+    k_xtx<<<dim3(nb64, nb64), 256, 0, s>>>(nc, Xc.p, h->acoarse_inv.p);
     CB_LAUNCH();
     unsigned long long f = 0;
     CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));

@@ -327,6 +327,10 @@ __global__ void __launch_bounds__(kDagThreads, 3) k_dense_dag(DagArgs a) {
       const int n = ext(k);
       const int col0 = bnd(d, k);
       tile_potrf_inv(tile(F, k, k), r, tile(P, k, k), r, n, sm, [&](int jj) {
+        if (d.sid < 0) {  // plain dense matrix: the pivot index
+          atomicMin(a.fail, (unsigned long long)(col0 + jj));
+          return;
+        }
         // report the template slot of compact column col0 + jj (pivot rule, linalg.cpp:42-54)
         const Supernode s = a.t.sn[d.sid];
         const int q = a.f.tpos[(int64_t)d.sd * a.t.rows_total + s.rows_off + col0 + jj];
@@ -399,6 +403,10 @@ __global__ void __launch_bounds__(kDagThreads, 3) k_dense_dag(DagArgs a) {
   }
 }
 
+// task list (step by step) + one persistent launch over `fr`
+void run_dag(cutbddc_gpu* h, std::vector<DagFront>& fr, int64_t cnt, double* front, double* panel,
+             unsigned long long* fail, const TplDev& t, const FactorDev& fdv);
+
 }  // namespace
 
 // Host: factorise the split fronts of one level for subdomains [sd0, sd1).
@@ -430,6 +438,29 @@ void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const
       fr.push_back(d);
     }
   if (fr.empty()) return;
+  ps.close();
+  run_dag(h, fr, cnt, front, f.panel.p, fail, tpl_dev(ts, h->slots), factor_dev(f));
+}
+
+// Cholesky + explicit inverse factor of one dense SPD n x n matrix (A:
+// column-major lower part, overwritten by L; X receives L^{-1}, lower part).
+// A non-positive pivot is reported as its index in *fail.
+void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long long* fail) {
+  if (n <= 0) return;
+  DagFront d{};
+  d.r = d.c = n;
+  d.np = d.nt = (n + kTile - 1) / kTile;
+  d.sd = d.sid = -1;
+  std::vector<DagFront> fr{d};
+  run_dag(h, fr, (int64_t)d.nt * (d.nt + 1), A, X, fail, TplDev{}, FactorDev{});
+}
+
+namespace {
+
+void run_dag(cutbddc_gpu* h, std::vector<DagFront>& fr, int64_t cnt, double* front, double* panel,
+             unsigned long long* fail, const TplDev& t, const FactorDev& fdv) {
+  cudaStream_t s = h->stream;
+  ProfScope ps(h->prof, s, "dense dag host+upload");
   // tasks, step by step over all fronts (largest first); within a step the
   // next pivot's chain (TRSM(k+1,k), GEMM(k+1,k+1,k)) comes right after the
   // POTRF, the inverse-panel tasks last (they are off the critical path)
@@ -478,8 +509,8 @@ void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const
   }();
   static DevBuf<unsigned long long> trace;
   if (trace_prefix) trace.alloc(4 * tasks.size());
-  DagArgs a{reinterpret_cast<const DagFront*>(dfr.p), dtk.p, (int)tasks.size(), front, f.panel.p, dcn.p, dcn.p + cnt,
-            fail, tpl_dev(ts, h->slots), factor_dev(f), trace_prefix ? trace.p : nullptr};
+  DagArgs a{reinterpret_cast<const DagFront*>(dfr.p), dtk.p, (int)tasks.size(), front, panel, dcn.p, dcn.p + cnt,
+            fail, t, fdv, trace_prefix ? trace.p : nullptr};
   const size_t shm = sizeof(double) * 2 * kTile * (kTile + 1);
   static int grid = 0;
   if (!grid) {
@@ -509,5 +540,7 @@ void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const
     }
   }
 }
+
+}  // namespace
 
 }  // namespace cutbddc_b200

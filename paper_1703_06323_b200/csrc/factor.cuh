@@ -74,5 +74,8 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
 void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const std::vector<int>& sids, int sd0,
                      int sd1, const std::vector<int64_t>& foff, const std::vector<int64_t>& poff, double* front,
                      unsigned long long* fail);
+// dense_dag.cu: Cholesky (A, column-major lower, overwritten) and X = L^{-1}
+// of one dense SPD matrix; a failing pivot index goes to *fail
+void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long long* fail);
 
 }  // namespace cutbddc_b200

@@ -182,7 +182,7 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int32_t> iscal;            // device int scalars (pcg)
 
   // persistent scratch (grow-only) so repeated solves allocate nothing
-  cutbddc_b200::DevBuf<double> ws_front, ws_wall, ws_upd, ws_ys, ws_s, ws_lc, ws_q8, ws_kint;
+  cutbddc_b200::DevBuf<double> ws_front, ws_wall, ws_upd, ws_ys, ws_s, ws_lc, ws_xc, ws_q8, ws_kint;
   cutbddc_b200::DevBuf<unsigned long long> ws_fail;
   cutbddc_b200::DevBuf<int64_t> ws_fbase, ws_cnt, ws_nc64;
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp;

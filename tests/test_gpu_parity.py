@@ -174,3 +174,25 @@ def test_nccl_world1_bit_identical(cfg2s):
     assert r1["iterations"] == r2["iterations"]
     assert np.array_equal(r1["residuals"], r2["residuals"]) and np.array_equal(x1, x2)
     d.close()
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_properties():
+    """BASELINE.json configs[4] (256^3, ~2.9M dofs, ~2000 subdomains) on one
+    GPU: no oracle at this size, so size-independent properties of the
+    solve: convergence to rtol, monotone-ish PCG residuals at the end, the
+    BDDC spectrum bound lambda_min >= 1 (SPEC.md invariants), a bounded
+    condition estimate, and the true residual of the returned solution."""
+    cfg = configs.get("cfg5")
+    s = cb.GpuSolver(0)
+    pb = cb.prepare(s, cfg)
+    s.setup_bddc(pb.objects, cfg.weighting)
+    x, rep = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
+    assert rep["converged"] and rep["iterations"] < 60
+    res = rep["residuals"]
+    assert res[-1] < cfg.rtol * res[0]
+    assert rep["lmin"] >= 1 - 1e-6 and rep["cond"] < 100
+    b = s.rhs()
+    r = b - s.spmv(x)
+    assert np.linalg.norm(r) <= 2 * cfg.rtol * np.linalg.norm(b)
+    s.close()
