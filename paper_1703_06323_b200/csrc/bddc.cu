@@ -178,14 +178,6 @@ __global__ void k_coarse_assemble(int nc, const int64_t* __restrict__ cg_ptr, co
   }
 }
 
-// Single-CTA blocked Cholesky of the coarse matrix. A is symmetric (both
-// triangles stored), so the row-major buffer is read as column-major; the
-// result is the column-major lower panel used by the substitution solves.
-__global__ void __launch_bounds__(256) k_coarse_chol(int n, double* __restrict__ A, unsigned long long* fail) {
-  __shared__ CholSmem sm;
-  front_partial_cholesky(A, n, n, sm, [&](int j) { atomicMin(fail, (unsigned long long)j); });
-}
-
 // ------------------------------------------------------------------ apply
 __global__ void k_gather_masked(int64_t ns, const int32_t* __restrict__ slot_dof, const uint8_t* __restrict__ mask,
                                 const double* __restrict__ r, double* __restrict__ X, const int* __restrict__ skip) {
@@ -255,22 +247,11 @@ __global__ void k_coarse_rhs(int nc, const int64_t* __restrict__ cg_ptr, const i
   g[lam] = s;
 }
 
-// Setup: column j of A_c^{-1} by forward + backward substitution on the
-// column-major Cholesky panel (one CTA per column, all in parallel).
-__global__ void __launch_bounds__(256) k_coarse_invert(int nc, const double* __restrict__ Lcm, double* __restrict__ Ainv) {
-  extern __shared__ double v[];
-  __shared__ double tile[32][33];
-  const int j = blockIdx.x;
-  for (int i = threadIdx.x; i < nc; i += blockDim.x) v[i] = i == j ? 1.0 : 0.0;
-  __syncthreads();
-  panel_forward(Lcm, nc, nc, v);
-  panel_backward(Lcm, nc, nc, v, tile);
-  for (int i = threadIdx.x; i < nc; i += blockDim.x) Ainv[(int64_t)j * nc + i] = v[i];
-}
-
-// A_c^{-1} = X^T X with X = L^{-1} (lower, column-major, from the dense DAG;
-// entries above X's diagonal tiles are not stored and are masked here).
-// 64 x 64 output tiles of the lower triangle, mirrored.
+// Small coarse problems (n_c <= kCoarseInverseMax): A_c^{-1} = X^T X once in
+// setup, then one GEMV per apply. 64 x 64 output tiles of the lower
+// triangle, mirrored; X's entries above its diagonal tiles are not stored
+// and are masked.
+constexpr int kCoarseInverseMax = 4096;
 __global__ void __launch_bounds__(256) k_xtx(int n, const double* __restrict__ X, double* __restrict__ C) {
   const int ib = blockIdx.x, jb = blockIdx.y;
   if (jb > ib) return;
@@ -329,6 +310,56 @@ __global__ void k_coarse_gemv(int nc, const double* __restrict__ Ainv, const dou
   for (; c < nc; c += 32) s0 += a[c] * g[c];
   const double s = warp_sum(s0 + s1);
   if (lane == 0) zc[row] = s;
+}
+
+// Large coarse problems: zc = A_c^{-1} g = X^T (X g), X = L^{-1} (lower, column-major n x n):
+//  k_xg_part: part[cb][i] = sum_{j in column block cb, j <= i} X[i, j] g[j]
+//             (thread per row, coalesced down each column);
+//  k_xg_sum:  y[i] = sum over cb <= i / 64 of part[cb][i] (in order);
+//  k_xty:     zc[j] = sum_{i >= j} X[i, j] y[i] (warp per column).
+__global__ void __launch_bounds__(256) k_xg_part(int n, const double* __restrict__ X, const double* __restrict__ g,
+                                                 double* __restrict__ part, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int i = blockIdx.x * 256 + threadIdx.x, j0 = blockIdx.y * 64;
+  if (i >= n || j0 > i) return;
+  const int j1 = min(j0 + 64, i + 1);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int j = j0;
+  for (; j + 4 <= j1; j += 4) {
+    s0 += X[i + (int64_t)j * n] * g[j];
+    s1 += X[i + (int64_t)(j + 1) * n] * g[j + 1];
+    s2 += X[i + (int64_t)(j + 2) * n] * g[j + 2];
+    s3 += X[i + (int64_t)(j + 3) * n] * g[j + 3];
+  }
+  for (; j < j1; ++j) s0 += X[i + (int64_t)j * n] * g[j];
+  part[(int64_t)blockIdx.y * n + i] = (s0 + s1) + (s2 + s3);
+}
+
+__global__ void k_xg_sum(int n, const double* __restrict__ part, double* __restrict__ y, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int cb = 0; cb <= i / 64; ++cb) s += part[(int64_t)cb * n + i];
+  y[i] = s;
+}
+
+__global__ void k_xty(int n, const double* __restrict__ X, const double* __restrict__ y, double* __restrict__ z,
+                      const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const double* col = X + j * n;
+  double s0 = 0.0, s1 = 0.0;
+  int i = (int)j + lane;
+  for (; i + 32 < n; i += 64) {
+    s0 += col[i] * y[i];
+    s1 += col[i + 32] * y[i + 32];
+  }
+  for (; i < n; i += 32) s0 += col[i] * y[i];
+  const double s = warp_sum(s0 + s1);
+  if (lane == 0) z[j] = s;
 }
 
 // v[d] = sum over copies (ascending sd) of w * Y
@@ -769,21 +800,23 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     CB_LAUNCH();
     allreduce_sum(h, h->acoarse.p, (size_t)nc * nc);  // SPEC.md:386 sum over all subdomains
     // Cholesky of A_c and X = L^{-1} by the tiled dense DAG (A_c is
-    // symmetric, so its row-major buffer is its column-major lower part),
-    // then the explicit inverse A_c^{-1} = X^T X; the apply multiplies by it
-    // (one GEMV).
+    // symmetric, so its row-major buffer is its column-major lower part);
+    // the apply solves with X^T (X g): two triangular GEMVs.
     DevBuf<double>& Lc = h->ws_lc;
     Lc.alloc((size_t)nc * nc);
     CB_CUDA(cudaMemcpyAsync(Lc.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
-    DevBuf<double>& Xc = h->ws_xc;
-    Xc.alloc((size_t)nc * nc);
     DevBuf<unsigned long long>& fail = h->ws_fail;
     fail.alloc(1);
     CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
-    dense_dag_matrix(h, Lc.p, Xc.p, nc, fail.p);
-    const int nb64 = (nc + 63) / 64;
-    k_xtx<<<dim3(nb64, nb64), 256, 0, s>>>(nc, Xc.p, h->acoarse_inv.p);
-    CB_LAUNCH();
+    dense_dag_matrix(h, Lc.p, h->acoarse_inv.p, nc, fail.p);
+    if (nc <= kCoarseInverseMax) {
+      h->acoarse_full.alloc((size_t)nc * nc);
+      const int nb64 = (nc + 63) / 64;
+      k_xtx<<<dim3(nb64, nb64), 256, 0, s>>>(nc, h->acoarse_inv.p, h->acoarse_full.p);
+      CB_LAUNCH();
+    } else {
+      h->ws_cpart.alloc((size_t)((nc + 63) / 64) * nc);
+    }
     unsigned long long f = 0;
     CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));
     CB_CUDA(cudaStreamSynchronize(s));
@@ -804,6 +837,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->cy.alloc((size_t)std::max<int64_t>(1, h->m_total));
   h->uvec.alloc((size_t)std::max<int64_t>(1, h->m_total));
   h->zc.alloc((size_t)std::max(1, nc));
+  h->uvec_c.alloc((size_t)std::max(1, nc));
   h->gc.alloc((size_t)std::max(1, nc));
   CB_CUDA(cudaStreamSynchronize(s));
   h->bddc_ready = true;
@@ -844,9 +878,20 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     k_coarse_rhs<<<grid_for(h->n_coarse, 128), 128, 0, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->gc.p, skip);
     CB_LAUNCH();
     allreduce_sum(h, h->gc.p, (size_t)h->n_coarse);
-    k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_inv.p, h->gc.p,
-                                                                         h->zc.p, skip);
-    CB_LAUNCH();
+    if (h->n_coarse <= kCoarseInverseMax) {
+      k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_full.p, h->gc.p,
+                                                                           h->zc.p, skip);
+      CB_LAUNCH();
+    } else {  // zc = X^T (X gc), X = L_c^{-1}
+      const int nc = h->n_coarse;
+      k_xg_part<<<dim3((nc + 255) / 256, (nc + 63) / 64), 256, 0, s>>>(nc, h->acoarse_inv.p, h->gc.p, h->ws_cpart.p,
+                                                                       skip);
+      CB_LAUNCH();
+      k_xg_sum<<<grid_for(nc, 256), 256, 0, s>>>(nc, h->ws_cpart.p, h->uvec_c.p, skip);
+      CB_LAUNCH();
+      k_xty<<<grid_for((int64_t)nc * 32, 256), 256, 0, s>>>(nc, h->acoarse_inv.p, h->uvec_c.p, h->zc.p, skip);
+      CB_LAUNCH();
+    }
     k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
                                                            h->coarse_id.p, h->zc.p, h->cy.p, h->uvec.p, 1, skip);
     CB_LAUNCH();

@@ -81,16 +81,30 @@ __device__ __forceinline__ void wait_eq(const int* p, int v) {
 // op(B) = B^T with B n x kk (bt) or B kk x n. 256 threads, 4x4 register
 // blocks, k staged in shared memory 32 at a time. A or B may alias C (they are
 // read completely before C is written). lower: store only rows >= columns.
+// D = A B + C on the FP64 tensor cores (DMMA), m8n8k4: lane l holds
+// A[l/4][l%4], B[l%4][l/4] and D[l/4][2(l%4) .. 2(l%4)+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// The dense trailing updates on the DMMA tensor cores: 8 warps, each owns a
+// 16 x 32 block of the 64 x 64 output (2 x 4 mma tiles); k staged through
+// shared memory 32 at a time (rows padded to 65 doubles: conflict-free
+// fragment loads).
 __device__ void tile_mm(double* C, int ldc, const double* A, int lda, const double* B, int ldb, int m, int n, int kk,
                         double alpha, bool acc, bool bt, bool lower, double* sm) {
-  double(*as)[kTile] = reinterpret_cast<double(*)[kTile]>(sm);
-  double(*bs)[kTile] = reinterpret_cast<double(*)[kTile]>(sm + 32 * kTile);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  double c4[4][4];
+  double(*as)[kTile + 1] = reinterpret_cast<double(*)[kTile + 1]>(sm);
+  double(*bs)[kTile + 1] = reinterpret_cast<double(*)[kTile + 1]>(sm + 32 * (kTile + 1));
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int wr = (wid & 3) * 16, wc = (wid >> 2) * 32;  // warp's output block origin
+  const int fr = lane >> 2, fk = lane & 3;               // fragment row/col and k index
+  double d[2][4][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) c4[a][b] = 0.0;
+    for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
   for (int k0 = 0; k0 < kk; k0 += 32) {
     __syncthreads();
     for (int e = tid; e < 32 * kTile; e += kDagThreads) {
@@ -109,32 +123,31 @@ __device__ void tile_mm(double* C, int ldc, const double* A, int lda, const doub
       }
     }
     __syncthreads();
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      double pa[4], pb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) pa[a] = as[k][tx + 16 * a];
+    for (int k = 0; k < 32; k += 4) {
+      double fa[2], fb[4];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) pb[b] = bs[k][ty + 16 * b];
+      for (int a = 0; a < 2; ++a) fa[a] = as[k + fk][wr + 8 * a + fr];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) fb[b] = bs[k + fk][wc + 8 * b + fr];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) c4[a][b] += pa[a] * pb[b];
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(d[a][b][0], d[a][b][1], fa[a], fb[b]);
     }
   }
   __syncthreads();  // A / B (possibly C itself) fully consumed
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const int j = ty + 16 * b;
-    if (j >= n) continue;
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int i = tx + 16 * a;
-      if (i >= m || (lower && i < j)) continue;
-      double* cp = C + i + (int64_t)j * ldc;
-      *cp = (acc ? *cp : 0.0) + alpha * c4[a][b];
-    }
-  }
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int i = wr + 8 * a + fr, j = wc + 8 * b + 2 * fk + h2;
+        if (i >= m || j >= n || (lower && i < j)) continue;
+        double* cp = C + i + (int64_t)j * ldc;
+        *cp = (acc ? *cp : 0.0) + alpha * d[a][b][h2];
+      }
 }
 
 // Cholesky of the n x n diagonal tile and the inverse of its factor; the

@@ -862,6 +862,9 @@ void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
 
 double sweep_bytes(const FactorSet& f) { return f.bytes_per_sweep; }
 
+// device bytes of the (grow-only, reusable) front workspace already held
+static int64_t front_bytes_held(const cutbddc_gpu* h) { return (int64_t)h->ws_front.cap * (int64_t)sizeof(double); }
+
 // Symbolic (compact structure) + numeric factorisation of every subdomain.
 void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, FactorSet& f, const char* what) {
   cudaStream_t s = h->stream;
@@ -910,8 +913,11 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   build_sweep_plan(h, ts, f, poff, uoff);
   pplan.close();
   const FactorDev fd = factor_dev(f);
-  // numeric, in subdomain chunks bounded by a front-workspace budget
-  const int64_t budget = (3ll << 30) / 8;
+  // numeric, in subdomain chunks bounded by a front-workspace budget: half
+  // of the free device memory (every chunk repeats the levels' critical paths)
+  size_t free_b = 0, total_b = 0;
+  CB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const int64_t budget = std::max<int64_t>((1ll << 30) / 8, (int64_t)(free_b / 2 + front_bytes_held(h)) / 8);
   DevBuf<unsigned long long>& fail = h->ws_fail;
   fail.alloc(1);
   CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));

@@ -160,7 +160,10 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<double> rho;               // nsd
   cutbddc_b200::DevBuf<double> ac_loc;            // per sd m*m (offsets m_off^2 prefix)
   cutbddc_b200::DevBuf<int64_t> ac_off;           // nsd+1
-  cutbddc_b200::DevBuf<double> acoarse, acoarse_inv;
+  cutbddc_b200::DevBuf<double> acoarse;
+  cutbddc_b200::DevBuf<double> acoarse_inv;       // X = L_c^{-1} (lower, column-major n_c x n_c)
+  cutbddc_b200::DevBuf<double> uvec_c;            // n_c: X g of the coarse solve
+  cutbddc_b200::DevBuf<double> acoarse_full;      // A_c^{-1} = X^T X (n_c <= 4096: one GEMV per apply)
   // root-space coarse basis (bddc.cu): per sd, with c_r root columns of K
   // and m constraint rows: S^{-1} (m x m, offsets ac_off) and
   // W_r = (K^{-1})_rr C_r^T (c_r x m, column-major); root_info[sd] =
@@ -182,7 +185,7 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int32_t> iscal;            // device int scalars (pcg)
 
   // persistent scratch (grow-only) so repeated solves allocate nothing
-  cutbddc_b200::DevBuf<double> ws_front, ws_wall, ws_upd, ws_ys, ws_s, ws_lc, ws_xc, ws_q8, ws_kint;
+  cutbddc_b200::DevBuf<double> ws_front, ws_upd, ws_s, ws_lc, ws_cpart, ws_q8, ws_kint;
   cutbddc_b200::DevBuf<unsigned long long> ws_fail;
   cutbddc_b200::DevBuf<int64_t> ws_fbase, ws_cnt, ws_nc64;
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp;
