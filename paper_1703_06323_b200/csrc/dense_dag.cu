@@ -474,39 +474,78 @@ void run_dag(cutbddc_gpu* h, std::vector<DagFront>& fr, int64_t cnt, double* fro
              unsigned long long* fail, const TplDev& t, const FactorDev& fdv) {
   cudaStream_t s = h->stream;
   ProfScope ps(h->prof, s, "dense dag host+upload");
-  // tasks, step by step over all fronts (largest first); within a step the
-  // next pivot's chain (TRSM(k+1,k), GEMM(k+1,k+1,k)) comes right after the
-  // POTRF, the inverse-panel tasks last (they are off the critical path)
-  std::vector<int4> tasks;
-  int kmax = 0;
-  for (auto& d : fr) kmax = std::max(kmax, d.np);
+  // Tasks in decreasing "bottom level" (weighted length of the longest path
+  // from the task to the end of its front's DAG): the POTRF chain and the
+  // tasks feeding it come first, wide trailing updates later. A predecessor
+  // always has a strictly larger bottom level, so this order is topological
+  // (every wait is on a smaller ticket: no deadlock).
   std::vector<int> order(fr.size());
   for (size_t q = 0; q < fr.size(); ++q) order[q] = (int)q;
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return fr[x].np > fr[y].np; });
-  for (int k = 0; k < kmax; ++k) {
-    for (int id : order) {
-      const DagFront& d = fr[(size_t)id];
-      if (k >= d.np) continue;
-      auto push = [&](int kind, int i, int j, int kk) { tasks.push_back(make_int4((kind << 24) | id, i, j, kk)); };
+  std::vector<std::vector<int4>> bucket;
+  std::vector<int4> ft;
+  std::vector<int> bl_p, bl_t, bl_g, bl_a, bl_f;
+  for (int id : order) {
+    const DagFront& d = fr[(size_t)id];
+    const int np = d.np, nt = d.nt;
+    ft.clear();
+    auto push = [&](int kind, int i, int j, int kk) { ft.push_back(make_int4((kind << 24) | id, i, j, kk)); };
+    for (int k = 0; k < np; ++k) {  // per front, step by step (successors later)
       push(kPotrf, k, k, k);
-      if (k + 1 < d.nt) {
-        push(kTrsm, k + 1, k, k);
-        push(kGemm, k + 1, k + 1, k);
-      }
-      for (int i = k + 2; i < d.nt; ++i) push(kTrsm, i, k, k);
-      for (int jj = k + 1; jj < d.nt; ++jj)
-        for (int i = jj; i < d.nt; ++i)
-          if (!(jj == k + 1 && i == k + 1)) push(kGemm, i, jj, k);
-    }
-    for (int id : order) {
-      const DagFront& d = fr[(size_t)id];
-      if (k >= d.np) continue;
-      auto push = [&](int kind, int i, int j, int kk) { tasks.push_back(make_int4((kind << 24) | id, i, j, kk)); };
+      for (int i = k + 1; i < nt; ++i) push(kTrsm, i, k, k);
+      for (int jj = k + 1; jj < nt; ++jj)
+        for (int i = jj; i < nt; ++i) push(kGemm, i, jj, k);
       for (int jj = 0; jj < k; ++jj) push(kFin, k, jj, k);
       for (int jj = 0; jj <= k; ++jj)
-        for (int i = k + 1; i < d.nt; ++i) push(kAcc, i, jj, k);
+        for (int i = k + 1; i < nt; ++i) push(kAcc, i, jj, k);
+    }
+    const size_t n2 = (size_t)nt * nt, n3 = n2 * nt;
+    bl_p.assign((size_t)nt, 0);
+    bl_t.assign(n2, 0);
+    bl_f.assign(n2, 0);
+    bl_g.assign(n3, 0);
+    bl_a.assign(n3, 0);
+    auto T = [&](int i, int k) -> int& { return bl_t[(size_t)i * nt + k]; };
+    auto Fn = [&](int i, int j) -> int& { return bl_f[(size_t)i * nt + j]; };
+    auto G = [&](int i, int j, int k) -> int& { return bl_g[((size_t)i * nt + j) * nt + k]; };
+    auto Ac = [&](int i, int j, int k) -> int& { return bl_a[((size_t)i * nt + j) * nt + k]; };
+    std::vector<int> bl(ft.size());
+    for (size_t q = ft.size(); q-- > 0;) {
+      const int kind = ft[q].x >> 24, i = ft[q].y, j = ft[q].z, k = ft[q].w;
+      int s = 0;
+      if (kind == kPotrf) {
+        for (int x = k + 1; x < nt; ++x) s = std::max({s, T(x, k), Ac(x, k, k)});
+        for (int y = 0; y < k; ++y) s = std::max(s, Fn(k, y));
+        bl[q] = bl_p[(size_t)k] = 3 + s;  // the diagonal tile weighs ~3 tile updates
+      } else if (kind == kTrsm) {
+        for (int y = k + 1; y <= i; ++y) s = std::max(s, G(i, y, k));
+        for (int x = i; x < nt; ++x) s = std::max(s, G(x, i, k));
+        for (int y = 0; y <= k; ++y) s = std::max(s, Ac(i, y, k));
+        bl[q] = T(i, k) = 1 + s;
+      } else if (kind == kGemm) {
+        if (k + 1 < j && k + 1 < np)
+          s = G(i, j, k + 1);
+        else if (j < np)
+          s = i == j ? bl_p[(size_t)j] : T(i, j);
+        bl[q] = G(i, j, k) = 1 + s;
+      } else if (kind == kAcc) {
+        if (k + 1 < std::min(i, np))
+          s = Ac(i, j, k + 1);
+        else if (i < np)
+          s = Fn(i, j);
+        bl[q] = Ac(i, j, k) = 1 + s;
+      } else {  // kFin
+        for (int x = i + 1; x < nt; ++x) s = std::max(s, Ac(x, j, i));
+        bl[q] = Fn(i, j) = 1 + s;
+      }
+    }
+    for (size_t q = 0; q < ft.size(); ++q) {
+      if ((size_t)bl[q] >= bucket.size()) bucket.resize((size_t)bl[q] + 1);
+      bucket[(size_t)bl[q]].push_back(ft[q]);
     }
   }
+  std::vector<int4> tasks;
+  for (size_t b = bucket.size(); b-- > 0;) tasks.insert(tasks.end(), bucket[b].begin(), bucket[b].end());
   if (fr.size() >= (1u << 24)) throw Failure(CUTBDDC_CONFIG, "dense dag: too many fronts in one level");
   static_assert(sizeof(DagFront) == 6 * sizeof(long long), "DagFront layout");
   DevBuf<long long>& dfr = h->ws_dag_fronts;
