@@ -19,7 +19,6 @@
 #include "bddc.cuh"
 #include "factor.cuh"
 #include "comm.cuh"
-#include "dense_chol.cuh"
 #include "subst.cuh"
 
 namespace cutbddc_b200 {

@@ -1,31 +1,39 @@
-// dense_dag.cu — tiled partial Cholesky + explicit inverse panel of the large
-// fronts (the dense top of the ND elimination tree), one persistent launch per
-// level, dataflow-scheduled.
+// dense_dag.cu — the numeric multifrontal factorisation of every subdomain
+// as ONE persistent, dataflow-scheduled launch (every front of every level:
+// no level barriers, no per-level launches), plus the dense coarse matrix.
 //
-// Replaces, for fronts of >= kSplitRows template rows, the right-looking
-// 32-column panel steps (three launches per step, the trailing matrix
-// streamed through HBM at every step) and the left-looking k_trinv /
-// k_gemm_m. The front F (r x r, column-major, lower part) is cut into tiles
-// of at most 64 x 64 whose boundaries are 0, 64, ..., c (the pivot columns)
-// and c, c + 64, ..., r (the update rows/columns). Tasks:
+// Replaces the numeric part of SparseCholesky::compute (linalg.cpp:34-62) for
+// A_II and K = A + rho C^T C, batched over subdomains. A front F (r x r,
+// column-major, lower part) is cut into tiles of at most 64 x 64 whose
+// boundaries are 0, 64, ..., c (the pivot columns) and c, c + 64, ..., r (the
+// update rows/columns). Tasks:
+//   ASM(i,j)      F_ij assembled in gather form (front_asm.cuh): children's
+//                 update blocks + the original stencil entries
+//   PEN(row)      F += rho c c^T of one constraint row (root of K)
 //   POTRF(k)      F_kk = L_kk L_kk^T and P_kk = L_kk^{-1}          (k < np)
 //   TRSM(i,k)     F_ik = F_ik P_kk^T = L_ik                          (i > k)
 //   GEMM(i,j,k)   F_ij -= L_ik L_jk^T                     (i >= j > k)
 //   ACC(i,j,k)    P_ij (+)= L_ik P_kj                 (j <= k < min(i, np))
 //   FIN(i,j)      P_ij = -P_ii P_ij                         (j < i < np)
-// P is the explicit panel G = [L11^{-1}; L21 L11^{-1}] the solve sweeps use:
-// the first c columns of M^{-1}, M = [L11 0; L21 I], with the lower block
-// negated (G21 = +sum L21 X). The trailing tiles (j >= np) end as the update
-// matrix the parent gathers (k_split_extend).
-// Every tile is updated in a fixed order (per-tile counters), so the result
-// is deterministic. Tasks are listed step by step (k), every task after the
-// tasks it waits for, and handed out by an atomic ticket: no deadlock.
+//   W             a small front whole, by one CTA: assembly, then the tile
+//                 tasks above in list order
+// "Split" fronts (factor.cu: is_split_front) get the tile tasks, spread over
+// many CTAs; the others one W task. P is the explicit panel
+// G = [L11^{-1}; L21 L11^{-1}] the solve sweeps use: the first c columns of
+// M^{-1}, M = [L11 0; L21 I], with the lower block negated (G21 = +sum L21 X).
+// The trailing tiles (j >= np) end as the update matrix the parent gathers.
+// A front's ASM / W tasks wait for its children's done counters. The GEMM
+// tiles run on the FP64 tensor cores (DMMA). Every tile is updated in a fixed
+// order (per-tile counters), so the result is deterministic. The ticket order
+// is topological (build_tasks): no deadlock.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "factor.cuh"
+#include "front_asm.cuh"
 
 namespace cutbddc_b200 {
 namespace {
@@ -33,12 +41,15 @@ namespace {
 constexpr int kTile = 64;
 constexpr int kDagThreads = 256;
 constexpr int kFinal = 1 << 20;  // X tile completed
-enum { kPotrf = 0, kTrsm = 1, kGemm = 2, kAcc = 3, kFin = 4 };
+enum { kPotrf = 0, kTrsm = 1, kGemm = 2, kAcc = 3, kFin = 4, kAsm = 5, kPen = 6, kWhole = 7 };
 
 struct DagFront {
-  long long fo, po, cnt;  // front (in the level's workspace), panel, counter offsets
+  long long fo, po, cnt;  // front (in the chunk's workspace), panel, counter offsets
   int r, c, np, nt;       // rows, pivot columns, pivot / all tile blocks
-  int sd, sid;
+  int sd, sid;            // subdomain, supernode (-1: a plain dense matrix)
+  int ch0, ch1;           // child fronts (list indices, -1: none)
+  int ntask, nasm;        // tasks of the front (its done counter's final value); assembly tasks
+  int ntile, whole;       // ASM tile tasks (PEN rows wait for them); 1: one W task runs the whole front
 };
 
 struct DagArgs {
@@ -52,6 +63,7 @@ struct DagArgs {
   unsigned long long* fail;
   TplDev t;
   FactorDev f;
+  FactorInput in;
   unsigned long long* trace;  // CUTBDDC_DAG_TRACE: per task {grab, deps met, done, sm}
 };
 
@@ -308,6 +320,146 @@ __device__ void tile_potrf_inv(double* F, int ldf, double* P, int ldp, int n, do
   }
 }
 
+// One tile task of front d (POTRF / TRSM / GEMM / ACC / FIN), no waits.
+__device__ void tile_task(const DagArgs& a, const DagFront& d, int kind, int i, int j, int k, double* sm) {
+  double* F = a.front + d.fo;
+  double* P = a.panel + d.po;
+  const int r = d.r;
+  auto tile = [&](double* base, int ti, int tj) { return base + bnd(d, ti) + (int64_t)bnd(d, tj) * r; };
+  auto ext = [&](int b) { return bnd(d, b + 1) - bnd(d, b); };
+  if (kind == kPotrf) {
+    const int col0 = bnd(d, k);
+    tile_potrf_inv(tile(F, k, k), r, tile(P, k, k), r, ext(k), sm, [&](int jj) {
+      if (d.sid < 0) {  // plain dense matrix: the pivot index
+        atomicMin(a.fail, (unsigned long long)(col0 + jj));
+        return;
+      }
+      // report the template slot of compact column col0 + jj (pivot rule, linalg.cpp:42-54)
+      const Supernode s = a.t.sn[d.sid];
+      const int q = a.f.tpos[(int64_t)d.sd * a.t.rows_total + s.rows_off + col0 + jj];
+      atomicMin(a.fail, (unsigned long long)((int64_t)d.sd * a.t.T + a.t.rows[s.rows_off + q]));
+    });
+    // (the panel above this diagonal tile is never read: the sweeps start
+    // every column at the 32-row block holding its diagonal)
+  } else if (kind == kTrsm) {
+    tile_mm(tile(F, i, k), r, tile(F, i, k), r, tile(P, k, k), r, ext(i), ext(k), ext(k), 1.0, false, true, false, sm);
+  } else if (kind == kGemm) {
+    tile_mm(tile(F, i, j), r, tile(F, i, k), r, tile(F, j, k), r, ext(i), ext(j), ext(k), -1.0, true, true, i == j, sm);
+  } else if (kind == kAcc) {
+    tile_mm(tile(P, i, j), r, tile(F, i, k), r, tile(P, k, j), r, ext(i), ext(j), ext(k), 1.0, k != j, false, false, sm);
+  } else {  // kFin
+    tile_mm(tile(P, i, j), r, tile(P, i, i), r, tile(P, i, j), r, ext(i), ext(j), ext(i), -1.0, false, false, false, sm);
+  }
+}
+
+__device__ ChildBlocks child_blocks(const DagArgs& a, const DagFront& d) {
+  ChildBlocks cb{nullptr, nullptr, 1, 1};
+  if (d.ch0 >= 0) {
+    const DagFront& c = a.fronts[d.ch0];
+    cb.u0 = a.front + c.fo + c.c + (int64_t)c.c * c.r;
+    cb.ld0 = c.r;
+  }
+  if (d.ch1 >= 0) {
+    const DagFront& c = a.fronts[d.ch1];
+    cb.u1 = a.front + c.fo + c.c + (int64_t)c.c * c.r;
+    cb.ld1 = c.r;
+  }
+  return cb;
+}
+
+__device__ __forceinline__ void wait_children(const DagArgs& a, const DagFront& d) {
+  if (d.ch0 >= 0) wait_eq(a.counters + a.fronts[d.ch0].cnt, a.fronts[d.ch0].ntask);
+  if (d.ch1 >= 0) wait_eq(a.counters + a.fronts[d.ch1].cnt, a.fronts[d.ch1].ntask);
+}
+
+// rho c c^T of constraint row `row` on the root front (a corner row is a
+// diagonal shift, already in diag_add): entries staged as (compact row,
+// value); objects are disjoint, so rows touch distinct entries.
+__device__ void penalty_row(const DagArgs& a, const DagFront& d, int64_t row, double* sm) {
+  const FactorInput& in = a.in;
+  if (in.corner[row]) return;
+  const int sd = d.sd, r = d.r;
+  const Supernode s = a.t.sn[d.sid];
+  double* F = a.front + d.fo;
+  const double rho = in.rho[sd];
+  const int64_t p0 = in.c_ptr[row];
+  const int len = (int)(in.c_ptr[row + 1] - p0);
+  auto pos = [&](int x) { return a.f.pfx[(int64_t)sd * a.t.rows_total + s.rows_off + a.t.root_pos[in.c_slot[p0 + x]]]; };
+  constexpr int kStage = 1024;
+  __syncthreads();
+  if (len > kStage) {  // very large object: unstaged
+    for (int q = threadIdx.x; q < len * len; q += blockDim.x) {
+      const int x = q / len, y = q % len;
+      const int pa = pos(x), pb = pos(y);
+      if (pa < pb || pb < 0) continue;
+      F[pa + (int64_t)pb * r] += rho * in.c_val[p0 + x] * in.c_val[p0 + y];
+    }
+    __syncthreads();
+    return;
+  }
+  double* sv = sm;
+  double* sc = sm + kStage;
+  int* sp = reinterpret_cast<int*>(sm + 2 * kStage);
+  for (int x = threadIdx.x; x < len; x += blockDim.x) {
+    sp[x] = pos(x);
+    sc[x] = in.c_val[p0 + x];
+    sv[x] = rho * sc[x];
+  }
+  __syncthreads();
+  const int n = len * len;
+  constexpr int kB = 4;  // entries per thread per pass: loads before stores
+  for (int q0 = threadIdx.x; q0 < n; q0 += kB * blockDim.x) {
+    double v[kB];
+    int64_t at[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int q = q0 + u * blockDim.x, x = q / len, y = q - x * len;
+      const int pa = q < n ? sp[x] : -1, pb = q < n ? sp[y] : -1;
+      at[u] = (pa >= pb && pb >= 0) ? pa + (int64_t)pb * r : -1;
+      v[u] = at[u] >= 0 ? F[at[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int q = q0 + u * blockDim.x, x = q / len, y = q - x * len;
+      if (at[u] >= 0) F[at[u]] = v[u] + sv[x] * sc[y];
+    }
+  }
+  __syncthreads();
+}
+
+// Assembly of rows [i0, i1) x cols [j0, j1) of front d (gather form).
+__device__ void assemble(const DagArgs& a, const DagFront& d, int i0, int i1, int j0, int j1, double* sm) {
+  const FrontDesc& fd = a.f.desc[(int64_t)d.sd * a.t.nsn + d.sid];
+  RowInfo* ri = reinterpret_cast<RowInfo*>(sm);
+  RowInfo* rj = ri + (i1 - i0);
+  const bool same = i0 == j0 && i1 == j1;
+  __syncthreads();
+  for (int q = threadIdx.x; q < i1 - i0; q += blockDim.x) ri[q] = row_info(a.f, fd, d.sd, a.in.T, a.in.b1, i0 + q);
+  if (!same)
+    for (int q = threadIdx.x; q < j1 - j0; q += blockDim.x) rj[q] = row_info(a.f, fd, d.sd, a.in.T, a.in.b1, j0 + q);
+  __syncthreads();
+  assemble_block(a.front + d.fo, d.r, d.c, i0, i1, j0, j1, ri, same ? ri : rj, child_blocks(a, d), a.in, d.sd);
+  __syncthreads();
+}
+
+// W task: the whole front by one CTA (assembly, root penalty, then every tile
+// task in list order).
+__device__ void whole_front(const DagArgs& a, const DagFront& d, double* sm) {
+  assemble(a, d, 0, d.r, 0, d.r, sm);
+  if (d.sid == a.t.root && a.in.c_ptr)
+    for (int64_t row = a.in.m_off[d.sd]; row < a.in.m_off[d.sd + 1]; ++row) penalty_row(a, d, row, sm);
+  const int np = d.np, nt = d.nt;
+  for (int k = 0; k < np; ++k) {
+    tile_task(a, d, kPotrf, k, k, k, sm);
+    for (int i = k + 1; i < nt; ++i) tile_task(a, d, kTrsm, i, k, k, sm);
+    for (int jj = k + 1; jj < nt; ++jj)
+      for (int i = jj; i < nt; ++i) tile_task(a, d, kGemm, i, jj, k, sm);
+    for (int jj = 0; jj < k; ++jj) tile_task(a, d, kFin, k, jj, k, sm);
+    for (int jj = 0; jj <= k; ++jj)
+      for (int i = k + 1; i < nt; ++i) tile_task(a, d, kAcc, i, jj, k, sm);
+  }
+}
+
 __global__ void __launch_bounds__(kDagThreads, 3) k_dense_dag(DagArgs a) {
   extern __shared__ double sm[];
   __shared__ int s_task;
@@ -323,86 +475,66 @@ __global__ void __launch_bounds__(kDagThreads, 3) k_dense_dag(DagArgs a) {
     const int4 tk = a.tasks[it];
     const int kind = tk.x >> 24, fi = tk.x & 0xffffff, i = tk.y, j = tk.z, k = tk.w;
     const DagFront d = a.fronts[fi];
-    double* F = a.front + d.fo;
-    double* P = a.panel + d.po;
-    int* A = a.counters + d.cnt;            // factor tiles: updates applied, col + 1 when final
+    int* fdone = a.counters + d.cnt;        // tasks of this front completed
+    int* fasm = fdone + 1;                  // assembly tasks completed
+    int* A = fdone + 2;                     // factor tiles: updates applied, col + 1 when final
     int* X = A + d.nt * (d.nt + 1) / 2;     // panel tiles: accumulations applied, kFinal when final
-    const int r = d.r;
-    auto tile = [&](double* base, int ti, int tj) { return base + bnd(d, ti) + (int64_t)bnd(d, tj) * r; };
-    auto ext = [&](int b) { return bnd(d, b + 1) - bnd(d, b); };
     int* done = nullptr;
     int inc = 1;
-    if (kind == kPotrf) {
-      if (tid == 0) wait_eq(A + tri(k, k), k);
-      if (a.trace && tid == 0) s_t1 = dag_timer();
-      __syncthreads();
-      __threadfence();
-      const int n = ext(k);
-      const int col0 = bnd(d, k);
-      tile_potrf_inv(tile(F, k, k), r, tile(P, k, k), r, n, sm, [&](int jj) {
-        if (d.sid < 0) {  // plain dense matrix: the pivot index
-          atomicMin(a.fail, (unsigned long long)(col0 + jj));
-          return;
+    if (tid == 0) {  // dependencies
+      if (kind == kWhole || kind == kAsm) {
+        wait_children(a, d);
+      } else if (kind == kPen) {
+        wait_eq(fasm, d.ntile);
+      } else {
+        if (k == 0) wait_eq(fasm, d.nasm);
+        if (kind == kPotrf) {
+          wait_eq(A + tri(k, k), k);
+        } else if (kind == kTrsm) {
+          wait_eq(A + tri(k, k), k + 1);
+          wait_eq(A + tri(i, k), k);
+        } else if (kind == kGemm) {
+          wait_eq(A + tri(i, k), k + 1);
+          wait_eq(A + tri(j, k), k + 1);
+          wait_eq(A + tri(i, j), k);
+        } else if (kind == kAcc) {
+          wait_eq(A + tri(i, k), k + 1);
+          if (k == j)
+            wait_eq(A + tri(j, j), j + 1);
+          else
+            wait_eq(X + tri(k, j), kFinal);
+          wait_eq(X + tri(i, j), k - j);
+        } else {  // kFin
+          wait_eq(X + tri(i, j), i - j);
+          wait_eq(A + tri(i, i), i + 1);
         }
-        // report the template slot of compact column col0 + jj (pivot rule, linalg.cpp:42-54)
-        const Supernode s = a.t.sn[d.sid];
-        const int q = a.f.tpos[(int64_t)d.sd * a.t.rows_total + s.rows_off + col0 + jj];
-        atomicMin(a.fail, (unsigned long long)((int64_t)d.sd * a.t.T + a.t.rows[s.rows_off + q]));
-      });
-      // (the panel above this diagonal tile is never read: the sweeps start
-      // every column at the 32-row block holding its diagonal)
-      done = A + tri(k, k);
-    } else if (kind == kTrsm) {
-      if (tid == 0) {
-        wait_eq(A + tri(k, k), k + 1);
-        wait_eq(A + tri(i, k), k);
       }
-      if (a.trace && tid == 0) s_t1 = dag_timer();
-      __syncthreads();
-      __threadfence();
-      tile_mm(tile(F, i, k), r, tile(F, i, k), r, tile(P, k, k), r, ext(i), ext(k), ext(k), 1.0, false, true, false, sm);
-      done = A + tri(i, k);
-    } else if (kind == kGemm) {
-      if (tid == 0) {
-        wait_eq(A + tri(i, k), k + 1);
-        wait_eq(A + tri(j, k), k + 1);
-        wait_eq(A + tri(i, j), k);
+      if (a.trace) s_t1 = dag_timer();
+    }
+    __syncthreads();
+    __threadfence();
+    if (kind == kWhole) {
+      whole_front(a, d, sm);
+    } else if (kind == kAsm) {
+      assemble(a, d, bnd(d, i), bnd(d, i + 1), bnd(d, j), bnd(d, j + 1), sm);
+      done = fasm;
+    } else if (kind == kPen) {
+      penalty_row(a, d, (int64_t)i, sm);
+      done = fasm;
+    } else {
+      tile_task(a, d, kind, i, j, k, sm);
+      if (kind == kPotrf || kind == kTrsm || kind == kGemm) {
+        done = A + tri(i, j);
+      } else {
+        done = X + tri(i, j);
+        if (kind == kFin) inc = kFinal - (i - j);  // P_ij final
       }
-      if (a.trace && tid == 0) s_t1 = dag_timer();
-      __syncthreads();
-      __threadfence();
-      tile_mm(tile(F, i, j), r, tile(F, i, k), r, tile(F, j, k), r, ext(i), ext(j), ext(k), -1.0, true, true, i == j, sm);
-      done = A + tri(i, j);
-    } else if (kind == kAcc) {
-      if (tid == 0) {
-        wait_eq(A + tri(i, k), k + 1);
-        if (k == j)
-          wait_eq(A + tri(j, j), j + 1);
-        else
-          wait_eq(X + tri(k, j), kFinal);
-        wait_eq(X + tri(i, j), k - j);
-      }
-      if (a.trace && tid == 0) s_t1 = dag_timer();
-      __syncthreads();
-      __threadfence();
-      tile_mm(tile(P, i, j), r, tile(F, i, k), r, tile(P, k, j), r, ext(i), ext(j), ext(k), 1.0, k != j, false, false, sm);
-      done = X + tri(i, j);
-    } else {  // kFin
-      if (tid == 0) {
-        wait_eq(X + tri(i, j), i - j);
-        wait_eq(A + tri(i, i), i + 1);
-      }
-      if (a.trace && tid == 0) s_t1 = dag_timer();
-      __syncthreads();
-      __threadfence();
-      tile_mm(tile(P, i, j), r, tile(P, i, i), r, tile(P, i, j), r, ext(i), ext(j), ext(i), -1.0, false, false, false, sm);
-      done = X + tri(i, j);
-      inc = kFinal - (i - j);
     }
     __syncthreads();
     if (tid == 0) {
       __threadfence();
-      atomicAdd(done, inc);
+      if (done) atomicAdd(done, inc);
+      atomicAdd(fdone, 1);
       if (a.trace) {
         unsigned long long* tr = a.trace + 4ll * it;
         unsigned sm_id;
@@ -416,153 +548,127 @@ __global__ void __launch_bounds__(kDagThreads, 3) k_dense_dag(DagArgs a) {
   }
 }
 
-// task list (step by step) + one persistent launch over `fr`
-void run_dag(cutbddc_gpu* h, std::vector<DagFront>& fr, int64_t cnt, double* front, double* panel,
-             unsigned long long* fail, const TplDev& t, const FactorDev& fdv);
+// Host list entry of one front: the device record plus what the task list needs.
+struct HostFront {
+  DagFront d;
+  int parent;          // list index of the parent front, -1: none
+  int64_t pen0, pen1;  // constraint rows added by PEN tasks (split root of K)
+};
 
-}  // namespace
-
-// Host: factorise the split fronts of one level for subdomains [sd0, sd1).
-// foff / poff: front-workspace and panel offsets per (sd, supernode); the
-// level's front workspace starts at `front` (= subdomain sd0's base).
-void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const std::vector<int>& sids, int sd0,
-                     int sd1, const std::vector<int64_t>& foff, const std::vector<int64_t>& poff, double* front,
-                     unsigned long long* fail) {
-  cudaStream_t s = h->stream;
-  const int nsn = (int)ts.tpl.sn.size();
-  ProfScope ps(h->prof, s, "dense dag host+upload");
-  std::vector<DagFront> fr;
-  int64_t cnt = 0;
-  for (int sd = sd0; sd < sd1; ++sd)
-    for (int sid : sids) {
-      const int2 v = f.h_rc[(size_t)sd * nsn + sid];
-      if (v.x == 0 || v.y == 0) continue;
-      DagFront d{};
-      d.r = v.x;
-      d.c = v.y;
-      d.np = (v.y + kTile - 1) / kTile;
-      d.nt = d.np + (v.x - v.y + kTile - 1) / kTile;
-      d.fo = (f.h_front_base[(size_t)sd] - f.h_front_base[(size_t)sd0]) + foff[(size_t)sd * nsn + sid];
-      d.po = poff[(size_t)sd * nsn + sid];
-      d.cnt = cnt;
-      d.sd = sd;
-      d.sid = sid;
-      cnt += (int64_t)d.nt * (d.nt + 1);  // A and X triangles
-      fr.push_back(d);
-    }
-  if (fr.empty()) return;
-  ps.close();
-  run_dag(h, fr, cnt, front, f.panel.p, fail, tpl_dev(ts, h->slots), factor_dev(f));
-}
-
-// Cholesky + explicit inverse factor of one dense SPD n x n matrix (A:
-// column-major lower part, overwritten by L; X receives L^{-1}, lower part).
-// A non-positive pivot is reported as its index in *fail.
-void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long long* fail) {
-  if (n <= 0) return;
-  DagFront d{};
-  d.r = d.c = n;
-  d.np = d.nt = (n + kTile - 1) / kTile;
-  d.sd = d.sid = -1;
-  std::vector<DagFront> fr{d};
-  run_dag(h, fr, (int64_t)d.nt * (d.nt + 1), A, X, fail, TplDev{}, FactorDev{});
-}
-
-namespace {
-
-void run_dag(cutbddc_gpu* h, std::vector<DagFront>& fr, int64_t cnt, double* front, double* panel,
-             unsigned long long* fail, const TplDev& t, const FactorDev& fdv) {
-  cudaStream_t s = h->stream;
-  ProfScope ps(h->prof, s, "dense dag host+upload");
-  // Tasks in decreasing "bottom level" (weighted length of the longest path
-  // from the task to the end of its front's DAG): the POTRF chain and the
-  // tasks feeding it come first, wide trailing updates later. A predecessor
-  // always has a strictly larger bottom level, so this order is topological
-  // (every wait is on a smaller ticket: no deadlock).
-  std::vector<int> order(fr.size());
-  for (size_t q = 0; q < fr.size(); ++q) order[q] = (int)q;
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return fr[x].np > fr[y].np; });
+// Task list in decreasing "bottom level" (weighted length of the longest path
+// from the task to the end of the whole tree's DAG): the POTRF chains and the
+// tasks feeding them first, wide trailing updates later. Every predecessor of
+// a task has a strictly larger bottom level (inside a front by construction;
+// across fronts every task of a child lies above its parent's first tasks),
+// so the order is topological: every wait is on a smaller ticket, held by a
+// running CTA, and the persistent launch cannot deadlock.
+std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
   std::vector<std::vector<int4>> bucket;
+  std::vector<int> entry(fr.size(), 0);  // bottom level of a front's first (children-waiting) tasks
   std::vector<int4> ft;
-  std::vector<int> bl_p, bl_t, bl_g, bl_a, bl_f;
-  for (int id : order) {
-    const DagFront& d = fr[(size_t)id];
-    const int np = d.np, nt = d.nt;
+  std::vector<int> bl, bl_p, bl_t, bl_g, bl_a, bl_f;
+  for (size_t q = fr.size(); q-- > 0;) {  // parents before children
+    HostFront& hf = fr[q];
+    DagFront& d = hf.d;
+    const int id = (int)q, np = d.np, nt = d.nt;
+    const int off = hf.parent >= 0 ? entry[(size_t)hf.parent] : 0;
     ft.clear();
-    auto push = [&](int kind, int i, int j, int kk) { ft.push_back(make_int4((kind << 24) | id, i, j, kk)); };
-    for (int k = 0; k < np; ++k) {  // per front, step by step (successors later)
-      push(kPotrf, k, k, k);
-      for (int i = k + 1; i < nt; ++i) push(kTrsm, i, k, k);
-      for (int jj = k + 1; jj < nt; ++jj)
-        for (int i = jj; i < nt; ++i) push(kGemm, i, jj, k);
-      for (int jj = 0; jj < k; ++jj) push(kFin, k, jj, k);
-      for (int jj = 0; jj <= k; ++jj)
-        for (int i = k + 1; i < nt; ++i) push(kAcc, i, jj, k);
-    }
-    const size_t n2 = (size_t)nt * nt, n3 = n2 * nt;
-    bl_p.assign((size_t)nt, 0);
-    bl_t.assign(n2, 0);
-    bl_f.assign(n2, 0);
-    bl_g.assign(n3, 0);
-    bl_a.assign(n3, 0);
-    auto T = [&](int i, int k) -> int& { return bl_t[(size_t)i * nt + k]; };
-    auto Fn = [&](int i, int j) -> int& { return bl_f[(size_t)i * nt + j]; };
-    auto G = [&](int i, int j, int k) -> int& { return bl_g[((size_t)i * nt + j) * nt + k]; };
-    auto Ac = [&](int i, int j, int k) -> int& { return bl_a[((size_t)i * nt + j) * nt + k]; };
-    std::vector<int> bl(ft.size());
-    for (size_t q = ft.size(); q-- > 0;) {
-      const int kind = ft[q].x >> 24, i = ft[q].y, j = ft[q].z, k = ft[q].w;
-      int s = 0;
-      if (kind == kPotrf) {
-        for (int x = k + 1; x < nt; ++x) s = std::max({s, T(x, k), Ac(x, k, k)});
-        for (int y = 0; y < k; ++y) s = std::max(s, Fn(k, y));
-        bl[q] = bl_p[(size_t)k] = 3 + s;  // the diagonal tile weighs ~3 tile updates
-      } else if (kind == kTrsm) {
-        for (int y = k + 1; y <= i; ++y) s = std::max(s, G(i, y, k));
-        for (int x = i; x < nt; ++x) s = std::max(s, G(x, i, k));
-        for (int y = 0; y <= k; ++y) s = std::max(s, Ac(i, y, k));
-        bl[q] = T(i, k) = 1 + s;
-      } else if (kind == kGemm) {
-        if (k + 1 < j && k + 1 < np)
-          s = G(i, j, k + 1);
-        else if (j < np)
-          s = i == j ? bl_p[(size_t)j] : T(i, j);
-        bl[q] = G(i, j, k) = 1 + s;
-      } else if (kind == kAcc) {
-        if (k + 1 < std::min(i, np))
-          s = Ac(i, j, k + 1);
-        else if (i < np)
-          s = Fn(i, j);
-        bl[q] = Ac(i, j, k) = 1 + s;
-      } else {  // kFin
-        for (int x = i + 1; x < nt; ++x) s = std::max(s, Ac(x, j, i));
-        bl[q] = Fn(i, j) = 1 + s;
+    bl.clear();
+    auto push = [&](int kind, int i, int j, int kk, int b) {
+      ft.push_back(make_int4((kind << 24) | id, i, j, kk));
+      bl.push_back(b);
+    };
+    if (d.whole) {
+      int w = 1;  // assembly, then the tile tasks in list order (POTRF ~3 tile updates)
+      for (int k = 0; k < np; ++k) w += 3 + (nt - k - 1) * (1 + (nt - k) / 2) + k + (k + 1) * (nt - k - 1);
+      push(kWhole, 0, 0, 0, off + w);
+      entry[q] = off + w;
+      d.ntask = 1;
+    } else {
+      for (int k = 0; k < np; ++k) {  // per front, step by step (successors later)
+        push(kPotrf, k, k, k, 0);
+        for (int i = k + 1; i < nt; ++i) push(kTrsm, i, k, k, 0);
+        for (int jj = k + 1; jj < nt; ++jj)
+          for (int i = jj; i < nt; ++i) push(kGemm, i, jj, k, 0);
+        for (int jj = 0; jj < k; ++jj) push(kFin, k, jj, k, 0);
+        for (int jj = 0; jj <= k; ++jj)
+          for (int i = k + 1; i < nt; ++i) push(kAcc, i, jj, k, 0);
       }
+      const size_t n2 = (size_t)nt * nt, n3 = n2 * nt;
+      bl_p.assign((size_t)nt, 0);
+      bl_t.assign(n2, 0);
+      bl_f.assign(n2, 0);
+      bl_g.assign(n3, 0);
+      bl_a.assign(n3, 0);
+      auto T = [&](int i, int k) -> int& { return bl_t[(size_t)i * nt + k]; };
+      auto Fn = [&](int i, int j) -> int& { return bl_f[(size_t)i * nt + j]; };
+      auto G = [&](int i, int j, int k) -> int& { return bl_g[((size_t)i * nt + j) * nt + k]; };
+      auto Ac = [&](int i, int j, int k) -> int& { return bl_a[((size_t)i * nt + j) * nt + k]; };
+      for (size_t x = ft.size(); x-- > 0;) {
+        const int kind = ft[x].x >> 24, i = ft[x].y, j = ft[x].z, k = ft[x].w;
+        int s = 0;
+        if (kind == kPotrf) {
+          for (int y = k + 1; y < nt; ++y) s = std::max({s, T(y, k), Ac(y, k, k)});
+          for (int y = 0; y < k; ++y) s = std::max(s, Fn(k, y));
+          bl[x] = bl_p[(size_t)k] = 3 + s;  // the diagonal tile weighs ~3 tile updates
+        } else if (kind == kTrsm) {
+          for (int y = k + 1; y <= i; ++y) s = std::max(s, G(i, y, k));
+          for (int y = i; y < nt; ++y) s = std::max(s, G(y, i, k));
+          for (int y = 0; y <= k; ++y) s = std::max(s, Ac(i, y, k));
+          bl[x] = T(i, k) = 1 + s;
+        } else if (kind == kGemm) {
+          if (k + 1 < j && k + 1 < np)
+            s = G(i, j, k + 1);
+          else if (j < np)
+            s = i == j ? bl_p[(size_t)j] : T(i, j);
+          bl[x] = G(i, j, k) = 1 + s;
+        } else if (kind == kAcc) {
+          if (k + 1 < std::min(i, np))
+            s = Ac(i, j, k + 1);
+          else if (i < np)
+            s = Fn(i, j);
+          bl[x] = Ac(i, j, k) = 1 + s;
+        } else {  // kFin
+          for (int y = i + 1; y < nt; ++y) s = std::max(s, Ac(y, j, i));
+          bl[x] = Fn(i, j) = 1 + s;
+        }
+      }
+      for (int& b : bl) b += off;
+      // assembly: ASM tiles, then the PEN rows, before every k = 0 task
+      const int top = (np > 0 ? bl_p[0] : 0) + off;
+      const int npen = (int)(hf.pen1 - hf.pen0);
+      const int asm_bl = 1 + top + (npen > 0 ? 1 : 0);
+      for (int i = 0; i < nt; ++i)
+        for (int j = 0; j <= i; ++j) push(kAsm, i, j, 0, asm_bl);
+      for (int64_t row = hf.pen0; row < hf.pen1; ++row) push(kPen, (int)row, 0, 0, top + 1);
+      d.ntile = nt * (nt + 1) / 2;
+      d.nasm = d.ntile + npen;
+      d.ntask = (int)ft.size();
+      entry[q] = asm_bl;
     }
-    for (size_t q = 0; q < ft.size(); ++q) {
-      if ((size_t)bl[q] >= bucket.size()) bucket.resize((size_t)bl[q] + 1);
-      bucket[(size_t)bl[q]].push_back(ft[q]);
+    for (size_t x = 0; x < ft.size(); ++x) {
+      if ((size_t)bl[x] >= bucket.size()) bucket.resize((size_t)bl[x] + 1);
+      bucket[(size_t)bl[x]].push_back(ft[x]);
     }
   }
   std::vector<int4> tasks;
   for (size_t b = bucket.size(); b-- > 0;) tasks.insert(tasks.end(), bucket[b].begin(), bucket[b].end());
-  if (fr.size() >= (1u << 24)) throw Failure(CUTBDDC_CONFIG, "dense dag: too many fronts in one level");
-  static_assert(sizeof(DagFront) == 6 * sizeof(long long), "DagFront layout");
-  DevBuf<long long>& dfr = h->ws_dag_fronts;
-  DevBuf<int4>& dtk = h->ws_dag_tasks;
-  DevBuf<int>& dcn = h->ws_dag_counters;
-  dfr.upload(reinterpret_cast<const long long*>(fr.data()), fr.size() * 6, s);
-  dtk.upload(tasks, s);
-  dcn.alloc((size_t)cnt + 1);
-  CB_CUDA(cudaMemsetAsync(dcn.p, 0, sizeof(int) * ((size_t)cnt + 1), s));
+  return tasks;
+}
+
+// One persistent launch over the plan's task list.
+void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, double* panel, unsigned long long* fail,
+                const TplDev& t, const FactorDev& fdv, const FactorInput& in, const std::vector<int4>* host_tasks) {
+  cudaStream_t s = h->stream;
+  CB_CUDA(cudaMemsetAsync(plan.counters.p, 0, sizeof(int) * ((size_t)plan.n_counters + 1), s));
   static const char* trace_prefix = [] {
     const char* e = std::getenv("CUTBDDC_DAG_TRACE");
     return e && e[0] ? e : (const char*)nullptr;
   }();
   static DevBuf<unsigned long long> trace;
-  if (trace_prefix) trace.alloc(4 * tasks.size());
-  DagArgs a{reinterpret_cast<const DagFront*>(dfr.p), dtk.p, (int)tasks.size(), front, panel, dcn.p, dcn.p + cnt,
-            fail, t, fdv, trace_prefix ? trace.p : nullptr};
+  if (trace_prefix) trace.alloc(4 * (size_t)plan.n_tasks);
+  DagArgs a{reinterpret_cast<const DagFront*>(plan.fronts.p), plan.tasks.p, plan.n_tasks, front, panel,
+            plan.counters.p, plan.counters.p + plan.n_counters, fail, t, fdv, in, trace_prefix ? trace.p : nullptr};
   const size_t shm = sizeof(double) * 2 * kTile * (kTile + 1);
   static int grid = 0;
   if (!grid) {
@@ -571,28 +677,141 @@ void run_dag(cutbddc_gpu* h, std::vector<DagFront>& fr, int64_t cnt, double* fro
     CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_dag, kDagThreads, shm));
     CB_CUDA(cudaGetDevice(&dev));
     CB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (const char* e = std::getenv("CUTBDDC_DAG_CTAS_PER_SM")) per_sm = std::min(per_sm, std::atoi(e));  // A/B runs
     grid = std::max(1, per_sm) * sms;
   }
-  ps.next("dense dag kernel");
-  k_dense_dag<<<std::min<int>(grid, (int)tasks.size()), kDagThreads, shm, s>>>(a);
+  ProfScope ps(h->prof, s, "dense dag kernel");
+  k_dense_dag<<<std::min<int>(grid, plan.n_tasks), kDagThreads, shm, s>>>(a);
   CB_LAUNCH();
-  CB_CUDA(cudaStreamSynchronize(s));  // host task vectors go out of scope
-  if (trace_prefix) {  // same layout as the sweep traces (tools/trace_analyze.py)
+  ps.close();
+  if (trace_prefix && host_tasks) {  // same layout as the sweep traces (tools/trace_analyze.py)
     static int seq = 0;
-    std::vector<unsigned long long> tr(4 * tasks.size());
+    std::vector<unsigned long long> tr(4 * (size_t)plan.n_tasks);
     trace.download(tr.data(), tr.size(), s);
     CB_CUDA(cudaStreamSynchronize(s));
     const std::string path = std::string(trace_prefix) + "_" + std::to_string(seq++) + ".bin";
     if (FILE* fp = std::fopen(path.c_str(), "wb")) {
-      const int n = (int)tasks.size();
+      const int n = plan.n_tasks;
       std::fwrite(&n, sizeof(int), 1, fp);
-      std::fwrite(tasks.data(), sizeof(int4), tasks.size(), fp);
+      std::fwrite(host_tasks->data(), sizeof(int4), host_tasks->size(), fp);
       std::fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fp);
+      std::vector<long long> fr(plan.fronts.n);  // front records (DagFront, 9 x int64 each)
+      plan.fronts.download(fr.data(), fr.size(), s);
+      CB_CUDA(cudaStreamSynchronize(s));
+      const int nf = (int)(fr.size() / 9);
+      std::fwrite(&nf, sizeof(int), 1, fp);
+      std::fwrite(fr.data(), sizeof(long long), fr.size(), fp);
       std::fclose(fp);
     }
   }
 }
 
+// Device copy of a host front list + task list (counters: per front done,
+// assembled, then the A and X tile triangles of a split front).
+void upload_plan(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, const std::vector<int4>& tasks) {
+  cudaStream_t s = h->stream;
+  if (fr.size() >= (1u << 24)) throw Failure(CUTBDDC_CONFIG, "dense dag: too many fronts");
+  std::vector<DagFront> dv(fr.size());
+  int64_t cnt = 0;
+  for (size_t q = 0; q < fr.size(); ++q) {
+    DagFront& d = fr[q].d;
+    d.cnt = cnt;
+    cnt += 2 + (d.whole ? 0 : (int64_t)d.nt * (d.nt + 1));
+    dv[q] = d;
+  }
+  static_assert(sizeof(DagFront) == 9 * sizeof(long long), "DagFront layout");
+  plan.fronts.upload(reinterpret_cast<const long long*>(dv.data()), dv.size() * 9, s);
+  plan.tasks.upload(tasks, s);
+  plan.n_tasks = (int)tasks.size();
+  plan.n_counters = cnt;
+  plan.counters.alloc((size_t)cnt + 1);
+}
+
 }  // namespace
+
+// Host: the whole factorisation of subdomains [sd0, sd1) as one dataflow
+// launch (every front of every level; foff / poff: front-workspace and panel
+// offsets per (sd, supernode); the chunk's workspace starts at `front`). The
+// task list is rebuilt only when the compact front sizes change.
+void dense_dag_tree(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const FactorInput& in, int sd0, int sd1,
+                    const std::vector<int64_t>& foff, const std::vector<int64_t>& poff, double* front,
+                    unsigned long long* fail) {
+  cudaStream_t s = h->stream;
+  const int nsn = (int)ts.tpl.sn.size();
+  DagPlan& plan = f.dag;
+  const bool same_rc = plan.key.size() == f.h_rc.size() &&
+                       std::memcmp(plan.key.data(), f.h_rc.data(), sizeof(int2) * f.h_rc.size()) == 0;
+  const bool hit = plan.sd0 == sd0 && plan.sd1 == sd1 && same_rc && !std::getenv("CUTBDDC_DAG_TRACE");
+  std::vector<int4> tasks;
+  if (!hit) {
+    ProfScope ps(h->prof, s, "dense dag host+upload");
+    std::vector<HostFront> fr;
+    std::vector<int> idx((size_t)(sd1 - sd0) * nsn, -1);
+    for (int sd = sd0; sd < sd1; ++sd)
+      for (int sid = 0; sid < nsn; ++sid) {  // postorder: children first
+        const int2 v = f.h_rc[(size_t)sd * nsn + sid];
+        if (v.x == 0) continue;
+        const Supernode& sn = ts.tpl.sn[(size_t)sid];
+        HostFront hf{};
+        DagFront& d = hf.d;
+        d.r = v.x;
+        d.c = v.y;
+        d.np = (v.y + kTile - 1) / kTile;
+        d.nt = d.np + (v.x - v.y + kTile - 1) / kTile;
+        d.fo = (f.h_front_base[(size_t)sd] - f.h_front_base[(size_t)sd0]) + foff[(size_t)sd * nsn + sid];
+        d.po = poff[(size_t)sd * nsn + sid];
+        d.sd = sd;
+        d.sid = sid;
+        d.whole = ts.is_split[(size_t)sid] ? 0 : 1;
+        d.ch0 = sn.nchild > 0 ? idx[(size_t)(sd - sd0) * nsn + sn.child[0]] : -1;
+        d.ch1 = sn.nchild > 1 ? idx[(size_t)(sd - sd0) * nsn + sn.child[1]] : -1;
+        hf.parent = -1;
+        hf.pen0 = hf.pen1 = 0;
+        if (!d.whole && sid == nsn - 1 && in.c_ptr) {
+          hf.pen0 = h->h_m_off[(size_t)sd];
+          hf.pen1 = h->h_m_off[(size_t)sd + 1];
+        }
+        idx[(size_t)(sd - sd0) * nsn + sid] = (int)fr.size();
+        fr.push_back(hf);
+      }
+    for (size_t q = 0; q < fr.size(); ++q) {
+      const DagFront& d = fr[q].d;
+      if (d.ch0 >= 0) fr[(size_t)d.ch0].parent = (int)q;
+      if (d.ch1 >= 0) fr[(size_t)d.ch1].parent = (int)q;
+    }
+    if (fr.empty()) return;
+    tasks = build_tasks(fr);
+    upload_plan(h, plan, fr, tasks);
+    plan.key = f.h_rc;
+    plan.sd0 = sd0;
+    plan.sd1 = sd1;
+  }
+  launch_dag(h, plan, front, f.panel.p, fail, tpl_dev(ts, h->slots), factor_dev(f), in, hit ? nullptr : &tasks);
+}
+
+// Cholesky + explicit inverse factor of one dense SPD n x n matrix (A:
+// column-major lower part, overwritten by L; X receives L^{-1}, lower part).
+// A non-positive pivot is reported as its index in *fail.
+void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long long* fail) {
+  if (n <= 0) return;
+  ProfScope ps(h->prof, h->stream, "dense dag host+upload");
+  HostFront hf{};
+  DagFront& d = hf.d;
+  d.r = d.c = n;
+  d.np = d.nt = (n + kTile - 1) / kTile;
+  d.sd = d.sid = -1;
+  d.ch0 = d.ch1 = -1;
+  hf.parent = -1;
+  std::vector<HostFront> fr{hf};
+  std::vector<int4> tasks = build_tasks(fr);
+  fr[0].d.nasm = 0;  // the matrix is assembled: no ASM tasks
+  std::vector<int4> kept;
+  for (const int4& tk : tasks)
+    if ((tk.x >> 24) != kAsm) kept.push_back(tk);
+  fr[0].d.ntask = (int)kept.size();
+  upload_plan(h, h->dag_dense, fr, kept);
+  ps.close();
+  launch_dag(h, h->dag_dense, A, X, fail, TplDev{}, FactorDev{}, FactorInput{}, &kept);
+}
 
 }  // namespace cutbddc_b200

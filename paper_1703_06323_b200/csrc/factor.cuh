@@ -1,6 +1,7 @@
 // factor.cuh — interfaces of the batched multifrontal factorisation/solves.
 #pragma once
 
+#include "front_desc.cuh"
 #include "handle.cuh"
 
 namespace cutbddc_b200 {
@@ -12,7 +13,6 @@ struct TplDev {
   const int32_t* emap;
   const int32_t* root_pos;
   const uint8_t* is_big;
-  const uint8_t* is_split;
   int T;
   int nsn;
   int root;  // id of the root supernode (last in postorder)
@@ -31,6 +31,9 @@ struct FactorDev {
   const int64_t* panel_off;
   const int64_t* upd_off;
   int64_t upd_total;  // doubles of the forward-update workspace per right-hand side
+  const FrontDesc* desc;  // per (sd, front) descriptors (sweep plan)
+  const int2* gmap;       // per compact front row: update entry of child 0 / 1 landing there, or -1
+  const int32_t* cslot;   // per compact front row: sd * T + slot
 };
 
 // Matrix fed to the factorisation: the A^w stencil restricted to `mask`
@@ -69,11 +72,11 @@ void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
 enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3 };
 void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip, int phase);
-// dense_dag.cu: tiled Cholesky + explicit inverse panel of one level's split
-// fronts (subdomains [sd0, sd1), front workspace based at sd0)
-void dense_dag_level(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const std::vector<int>& sids, int sd0,
-                     int sd1, const std::vector<int64_t>& foff, const std::vector<int64_t>& poff, double* front,
-                     unsigned long long* fail);
+// dense_dag.cu: the numeric factorisation of subdomains [sd0, sd1) as one
+// dataflow launch over every front (front workspace based at sd0)
+void dense_dag_tree(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const FactorInput& in, int sd0, int sd1,
+                    const std::vector<int64_t>& foff, const std::vector<int64_t>& poff, double* front,
+                    unsigned long long* fail);
 // dense_dag.cu: Cholesky (A, column-major lower, overwritten) and X = L^{-1}
 // of one dense SPD matrix; a failing pivot index goes to *fail
 void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long long* fail);

@@ -34,18 +34,25 @@ struct TplSet {
   // by many CTAs as GEMVs). Work items are (supernode, chunk) pairs.
   cutbddc_b200::DevBuf<int32_t> small_sn;       // per level, concatenated
   std::vector<int> small_first, small_count;
-  cutbddc_b200::DevBuf<int2> fwd_items, bwd_items, inv_items;  // (sn, chunk)
-  std::vector<int> fwd_first, fwd_count, bwd_first, bwd_count, inv_first, inv_count;
+  cutbddc_b200::DevBuf<int2> fwd_items, bwd_items;  // (sn, chunk)
+  std::vector<int> fwd_first, fwd_count, bwd_first, bwd_count;
   cutbddc_b200::DevBuf<int32_t> big_sn;         // per level, concatenated
   std::vector<int> big_first, big_count;
   std::vector<uint8_t> is_big;                  // per supernode
-  cutbddc_b200::DevBuf<uint8_t> big_flag, split_flag;
-  cutbddc_b200::DevBuf<int32_t> split_sn;       // large fronts per level (multi-CTA factorisation)
-  std::vector<int> split_first, split_count, split_maxc, split_maxr;
-  cutbddc_b200::DevBuf<int2> gemm_items;
-  std::vector<int> gemm_first, gemm_count;
+  std::vector<uint8_t> is_split;                // per supernode: tiled DAG front (else one CTA, dense_dag.cu)
+  cutbddc_b200::DevBuf<uint8_t> big_flag;
   int max_cblocks = 0;
   bool ready = false;
+};
+
+// Task list of one dataflow factorisation launch (dense_dag.cu).
+struct DagPlan {
+  cutbddc_b200::DevBuf<long long> fronts;      // per front record (9 x int64)
+  cutbddc_b200::DevBuf<int4> tasks;            // (kind << 24 | front, i, j, k) in ticket order
+  cutbddc_b200::DevBuf<int> counters;          // per front: done, assembled, tile counters; then the ticket
+  std::vector<int2> key;                       // compact front sizes the list was built for
+  int sd0 = -1, sd1 = -1, n_tasks = 0;
+  int64_t n_counters = 0;
 };
 
 // One factorisation over a template, compacted per subdomain (masked-out
@@ -77,6 +84,7 @@ struct FactorSet {
   int n_items_b_root = 0;                      // leading backward items of the root level
   std::vector<int64_t> h_vec_off;              // nsd x nsn compact front vector offsets (host copy)
   std::vector<int64_t> h_panel_off;            // nsd x nsn panel offsets (host copy)
+  DagPlan dag;                                 // dataflow factorisation (dense_dag.cu)
 };
 
 struct cutbddc_gpu {
@@ -190,9 +198,7 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int64_t> ws_fbase, ws_cnt, ws_nc64;
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp;
   cutbddc_b200::DevBuf<int> ws_flag;
-  cutbddc_b200::DevBuf<long long> ws_dag_fronts;  // dense_dag.cu: per-level front records
-  cutbddc_b200::DevBuf<int4> ws_dag_tasks;
-  cutbddc_b200::DevBuf<int> ws_dag_counters;
+  DagPlan dag_dense;                               // dense_dag.cu: the coarse matrix factorisation
 
   // pcg vectors
   cutbddc_b200::DevBuf<double> px, pr, pz, pp, pq, pb, hist, lal, lbe;

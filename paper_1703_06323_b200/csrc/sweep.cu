@@ -29,6 +29,7 @@
 #include <cstdlib>
 
 #include "factor.cuh"
+#include "front_desc.cuh"
 #include "prof.cuh"
 
 namespace cutbddc_b200 {
@@ -52,19 +53,6 @@ enum { kItemS = 0, kItemA = 1, kItemC = 2, kItemT = 3 };
 // parallelism (one CTA would issue r c / 256 dependent loads per thread)
 inline bool is_small(int2 rc) { return rc.x <= kSmallRows && (int64_t)rc.x * rc.y <= kSmallWork; }
 
-// Everything one (subdomain, front) needs, in one 96-byte record.
-struct __align__(16) FrontDesc {
-  int r, c, nch, pfs;      // rows, columns, children, parent front (backward dependency) or -1
-  long long vo, po;        // compact front vector / panel offsets
-  long long uo, cuo0;      // own update offset, child 0 update offset
-  long long cuo1;          // child 1 update offset
-  long long tpo;           // forward tile partials of a chunked front (in vbuf)
-  int cfs0, cfs1;          // child fronts (sd * nsn + sid)
-  int cnu0, cnu1;          // child update lengths
-  int cnf0, cnf1;          // child forward completion counts
-  int pnb, rbo;            // parent backward completion count; row-block counters of a chunked front
-};
-static_assert(sizeof(FrontDesc) == 96, "FrontDesc is six int4");
 
 struct SweepDev {
   const FrontDesc* desc;

@@ -1,4 +1,6 @@
-"""Summarise CUTBDDC_DAG_TRACE dumps of the dense-front DAG (dense_dag.cu)."""
+"""Summarise CUTBDDC_DAG_TRACE dumps of the dataflow factorisation (dense_dag.cu):
+per task kind wait / work times, and per template supernode (level of the
+elimination tree) when its fronts' tasks ran."""
 import glob
 import os
 import sys
@@ -8,12 +10,29 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from trace_analyze import load  # noqa: E402
 
-NAMES = ["POTRF", "TRSM", "GEMM", "ACC", "FIN"]
+NAMES = ["POTRF", "TRSM", "GEMM", "ACC", "FIN", "ASM", "PEN", "W"]
+
+
+def load_fronts(path, n_tasks):
+    with open(path, "rb") as f:
+        f.seek(4 + 16 * n_tasks + 32 * n_tasks)
+        raw = f.read(4)
+        if len(raw) < 4:
+            return None
+        nf = int(np.frombuffer(raw, np.int32)[0])
+        rec = np.frombuffer(f.read(72 * nf), np.int64).reshape(nf, 9)
+    ints = rec[:, 3:].copy().view(np.int32).reshape(nf, 12)
+    # r, c, np, nt, sd, sid, ch0, ch1, ntask, nasm, ntile, whole
+    return ints
+
+
 for p in sorted(glob.glob(sys.argv[1] + "_*.bin")):
     items, tr = load(p)
     kind = items[:, 0] >> 24
+    fid = items[:, 0] & 0xFFFFFF
     t0 = tr[:, 0].min()
-    print(f"{p}: {len(items)} tasks, {len(np.unique(items[:, 0] & 0xffffff))} fronts, span {(tr[:, 2].max() - t0) / 1e3:.1f} us")
+    print(f"{p}: {len(items)} tasks, {len(np.unique(fid))} fronts, span {(tr[:, 2].max() - t0) / 1e3:.1f} us, "
+          f"SMs {len(np.unique(tr[:, 3]))}")
     for k, name in enumerate(NAMES):
         m = kind == k
         if not m.any():
@@ -22,3 +41,13 @@ for p in sorted(glob.glob(sys.argv[1] + "_*.bin")):
         work = (tr[m, 2] - tr[m, 1]) / 1e3
         print(f"  {name:5s} n={m.sum():6d} wait mean {wait.mean():7.2f} | work mean {work.mean():6.2f} p50 {np.median(work):6.2f} "
               f"max {work.max():7.2f} us | sum {work.sum() / 1e3:7.2f} ms")
+    fr = load_fronts(p, len(items))
+    if fr is None:
+        continue
+    sid = fr[fid, 5]
+    print("  per supernode: sid  fronts  whole  rows(max) cols(max)  first start  last end (us from launch)")
+    for s in np.unique(sid)[::-1]:
+        m = sid == s
+        fm = fr[:, 5] == s
+        print(f"    {s:4d} {fm.sum():6d} {fr[fm, 11].max():5d} {fr[fm, 0].max():8d} {fr[fm, 1].max():8d}"
+              f"  {(tr[m, 0].min() - t0) / 1e3:10.1f} {(tr[m, 2].max() - t0) / 1e3:10.1f}")
