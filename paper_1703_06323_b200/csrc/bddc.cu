@@ -720,18 +720,22 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   // ---- factorisations
   if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);
   FactorInput fi{h->As.p, h->mask_int.p, nullptr, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  factor_device(h, h->tI, fi, h->fI, "cholesky (interior problem)");
+  factor_symbolic(h, h->tI, fi, h->fI);
+  std::vector<FactorJob> jobs{FactorJob{&h->tI, &fi, &h->fI, "cholesky (interior problem)"}};
   // Without an interface (one subdomain) every dof is interior: the weighted
   // residual r_w is identically zero and the constrained Neumann solve drops
   // out of the apply ("preconditioner reduces to exact interior solve").
   h->has_K = h->n_if > 0;
   h->fK.upd_total = 0;
+  FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
+                 h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
   if (h->has_K) {
     if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
-    FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
-                   h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
-    factor_device(h, h->tK, fk, h->fK, "saddle: singular augmented system; constraints do not control the operator kernel");
+    factor_symbolic(h, h->tK, fk, h->fK);
+    jobs.push_back(FactorJob{&h->tK, &fk, &h->fK,
+                             "saddle: singular augmented system; constraints do not control the operator kernel"});
   }
+  factor_numeric(h, jobs);
   const int64_t upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, h->fK.upd_total));
   // ---- coarse basis in the root space of K (see k_root_h): H, S, S^{-1},
   // W_r and A_c,w = S^{-1} - rho I; the apply never forms Phi

@@ -41,7 +41,7 @@ namespace {
 constexpr int kTile = 64;
 constexpr int kDagThreads = 256;
 constexpr int kFinal = 1 << 20;  // X tile completed
-enum { kPotrf = 0, kTrsm = 1, kGemm = 2, kAcc = 3, kFin = 4, kAsm = 5, kPen = 6, kWhole = 7 };
+enum { kPotrf = 0, kTrsm = 1, kGemm = 2, kAcc = 3, kFin = 4, kAsm = 5, kPen = 6, kWhole = 7, kDiag = 8 };
 
 struct DagFront {
   long long fo, po, cnt;  // front (in the chunk's workspace), panel, counter offsets
@@ -50,20 +50,28 @@ struct DagFront {
   int ch0, ch1;           // child fronts (list indices, -1: none)
   int ntask, nasm;        // tasks of the front (its done counter's final value); assembly tasks
   int ntile, whole;       // ASM tile tasks (PEN rows wait for them); 1: one W task runs the whole front
+  int grp, pad_;          // factorisation (DagArgs::g) the front belongs to
 };
+
+// One factorisation of a launch (the interior problems and K share one).
+struct DagGroup {
+  TplDev t;
+  FactorDev f;
+  FactorInput in;
+  double* panel;
+  unsigned long long* fail;
+};
+
+constexpr int kMaxGroups = 2;
 
 struct DagArgs {
   const DagFront* fronts;
   const int4* tasks;
   int n_tasks;
-  double* front;
-  double* panel;
+  double* front;  // every group's fronts (DagFront::fo)
   int* counters;
   int* ticket;
-  unsigned long long* fail;
-  TplDev t;
-  FactorDev f;
-  FactorInput in;
+  DagGroup g[kMaxGroups];
   unsigned long long* trace;  // CUTBDDC_DAG_TRACE: per task {grab, deps met, done, sm}
 };
 
@@ -165,165 +173,91 @@ __device__ void tile_mm(double* C, int ldc, const double* A, int lda, const doub
 // Cholesky of the n x n diagonal tile and the inverse of its factor; the
 // strict upper parts of both stored tiles become zero.
 typedef double SmTile[kTile + 1];
+#ifndef POTRF_PHASE  // microbenchmark hook (tools/debug/potrf_real_bench.cu)
+#define POTRF_PHASE(k)
+#endif
 
-// Warp: Cholesky of the m x m block at (o, o) of `ls` (m <= 16); lane i holds
-// row o + i in registers, column j values are broadcast by shuffles.
-// Non-positive pivots are reported (fail) and replaced by 1.
-template <typename Fail>
-__device__ void warp_chol16(SmTile* ls, int o, int m, int lane, Fail fail) {
-  double a[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) a[q] = (lane < m && q <= lane) ? ls[o + lane][o + q] : 0.0;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j < m) {
-      double djj = __shfl_sync(0xffffffffu, a[j], j);
-      if (!(djj > 0.0)) {
-        if (lane == 0) fail(o + j);
-        djj = 1.0;
-      }
-      const double rl = rsqrt(djj), l = djj * rl;
-      if (lane == j) {
-        a[j] = l;
-        ls[o + j][kTile] = rl;  // 1 / L_jj in the padding column (used by warp_inv16)
-      } else if (lane > j) {
-        a[j] *= rl;
-      }
-#pragma unroll
-      for (int q = j + 1; q < 16; ++q) {
-        const double lqj = __shfl_sync(0xffffffffu, a[j], q);
-        if (lane >= q) a[q] -= a[j] * lqj;
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 16; ++q)
-    if (lane < m && q <= lane) ls[o + lane][o + q] = a[q];
-}
-
-// Warp: X = L^{-1} of the m x m lower block at (o, o) (m <= 16); lane j
-// computes column j in registers (L rows broadcast from shared memory).
-__device__ void warp_inv16(SmTile* ls, SmTile* xs, int o, int m, int lane) {
-  double x[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    double v = 0.0;
-    if (i < m) {
-      const double rd = ls[o + i][kTile];  // 1 / L_ii from warp_chol16
-      double s = i == lane ? 1.0 : 0.0;
-#pragma unroll
-      for (int k = 0; k < i; ++k) s -= ls[o + i][o + k] * x[k];
-      v = lane <= i ? s * rd : 0.0;
-    }
-    x[i] = v;
-  }
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if (lane < m && i < m) xs[o + i][o + lane] = x[i];
-}
-
-// Cholesky of the n x n diagonal tile and the inverse of its factor, blocked
-// by 16: per diagonal block a register-resident warp Cholesky + inverse, then
-// the panel below (L_ib = A_ib X_bb^T) and the trailing update by the whole
-// CTA; the off-diagonal blocks of X = L^{-1} follow by block diagonals,
-// X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj. Strict upper parts stored as zero.
+// Cholesky of the n x n diagonal tile and the inverse of its factor by the
+// whole CTA, one pivot per step in the unscaled (LDL^T-like) form:
+//   U_iq -= U_ij U_qj / U_jj      (j < q <= i, the trailing lower triangle)
+//   Y_ic -= U_ij Y_jc / U_jj      (c <= j < i, Y = unscaled rows of L^{-1})
+// then L_ij = U_ij / sqrt(U_jj) and X_jc = Y_jc / sqrt(U_jj). Thread (i, g)
+// owns the entries of row i in the columns = g mod 4: one barrier per pivot,
+// short rolled loops (the unrolled warp-level variants were bound by
+// instruction fetch: this code runs once per task). Non-positive pivots are
+// reported (fail) and replaced by 1. Strict upper parts stored as zero.
 template <typename Fail>
 __device__ void tile_potrf_inv(double* F, int ldf, double* P, int ldp, int n, double* sm, Fail fail) {
   SmTile* ls = reinterpret_cast<SmTile*>(sm);
   SmTile* xs = reinterpret_cast<SmTile*>(sm + kTile * (kTile + 1));
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nb = (n + 15) / 16;
+  __shared__ double rs[kTile];
+  const int tid = threadIdx.x;
   __syncthreads();
-  for (int e = tid; e < kTile * kTile; e += kDagThreads) {
-    const int i = e & 63, j = e >> 6;
-    ls[i][j] = (i < n && j < n && i >= j) ? F[i + (int64_t)j * ldf] : 0.0;
-    xs[i][j] = 0.0;
+  {
+    constexpr int kPer = kTile * kTile / kDagThreads;  // loads in flight per thread
+    double v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kDagThreads, i = e & 63, j = e >> 6;
+      v[u] = (i < n && j < n && i >= j) ? F[i + (int64_t)j * ldf] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kDagThreads, i = e & 63, j = e >> 6;
+      ls[i][j] = v[u];
+      xs[i][j] = i == j ? 1.0 : 0.0;
+    }
+  }
+  POTRF_PHASE(0);
+  const int i = tid & 63, g = tid >> 6;
+  for (int j = 0; j < n; ++j) {
+    __syncthreads();
+    double ajj = ls[j][j];
+    if (!(ajj > 0.0)) {
+      if (tid == 0) fail(j);
+      ajj = 1.0;
+    }
+    const double r = rsqrt(ajj);
+    if (tid == 0) rs[j] = r;
+    if (i <= j || i >= n) continue;
+    const double f = ls[i][j] * (r * r);
+    // row i of the trailing block (columns q > j) and of Y (rows i > j) never
+    // overlap column j / row j read here: loads are batched ahead of stores
+    int q = j + 1 + ((g - j - 1) & 3);
+    for (; q + 12 <= i; q += 16) {
+      const double a0 = ls[i][q], a1 = ls[i][q + 4], a2 = ls[i][q + 8], a3 = ls[i][q + 12];
+      const double b0 = ls[q][j], b1 = ls[q + 4][j], b2 = ls[q + 8][j], b3 = ls[q + 12][j];
+      ls[i][q] = a0 - f * b0;
+      ls[i][q + 4] = a1 - f * b1;
+      ls[i][q + 8] = a2 - f * b2;
+      ls[i][q + 12] = a3 - f * b3;
+    }
+    for (; q <= i; q += 4) ls[i][q] -= f * ls[q][j];
+    int c = g;
+    for (; c + 12 <= j; c += 16) {
+      const double a0 = xs[i][c], a1 = xs[i][c + 4], a2 = xs[i][c + 8], a3 = xs[i][c + 12];
+      const double b0 = xs[j][c], b1 = xs[j][c + 4], b2 = xs[j][c + 8], b3 = xs[j][c + 12];
+      xs[i][c] = a0 - f * b0;
+      xs[i][c + 4] = a1 - f * b1;
+      xs[i][c + 8] = a2 - f * b2;
+      xs[i][c + 12] = a3 - f * b3;
+    }
+    for (; c <= j; c += 4) xs[i][c] -= f * xs[j][c];
   }
   __syncthreads();
-  for (int b = 0; b < nb; ++b) {
-    const int o = 16 * b, m = min(16, n - o), below = n - o - m;
-    if (wid == 0) {
-      warp_chol16(ls, o, m, lane, fail);
-      __syncwarp();
-      warp_inv16(ls, xs, o, m, lane);
-    }
-    __syncthreads();
-    if (below <= 0) break;
-    // L_ib = A_ib X_bb^T (rows o+16.., columns o..o+m)
-    double l[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kDagThreads, i = o + 16 + (e >> 4), q = e & 15;
-      double s = 0.0;
-      if (i < n && q < m)
-        for (int k = 0; k <= q; ++k) s += ls[i][o + k] * xs[o + q][o + k];
-      l[u] = s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kDagThreads, i = o + 16 + (e >> 4), q = e & 15;
-      if (i < n && q < m) ls[i][o + q] = l[u];
-    }
-    __syncthreads();
-    // trailing update A_ij -= L_ib L_jb^T (o+16 <= j <= i < n)
-    for (int e = tid; e < below * below; e += kDagThreads) {
-      const int i = o + 16 + e / below, j = o + 16 + e % below;
-      if (j > i) continue;
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) s += ls[i][o + k] * ls[j][o + k];
-      ls[i][j] -= s;
-    }
-    __syncthreads();
-  }
-  // off-diagonal blocks of X, one block diagonal at a time
-  for (int d = 1; d < nb; ++d) {
-    const int nblk = nb - d;
-    // T_ij = sum_{k=j}^{i-1} L_ik X_kj into xs block (i, j)
-    for (int e = tid; e < nblk * 256; e += kDagThreads) {
-      const int jb = e >> 8, ib = jb + d, p = (e >> 4) & 15, q = e & 15;
-      const int i = 16 * ib + p, j = 16 * jb + q;
-      double s = 0.0;
-      if (i < n)
-        for (int k = 16 * jb; k < 16 * ib; ++k) s += ls[i][k] * xs[k][j];
-      xs[i][j] = s;
-    }
-    __syncthreads();
-    double x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kDagThreads;
-      double s = 0.0;
-      if (e < nblk * 256) {
-        const int jb = e >> 8, ib = jb + d, p = (e >> 4) & 15, q = e & 15;
-        const int i = 16 * ib + p, j = 16 * jb + q;
-        for (int t = 16 * ib; t <= i; ++t) s += xs[i][t] * xs[t][j];
-      }
-      x[u] = -s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kDagThreads;
-      if (e < nblk * 256) {
-        const int jb = e >> 8, ib = jb + d, p = (e >> 4) & 15, q = e & 15;
-        xs[16 * ib + p][16 * jb + q] = x[u];
-      }
-    }
-    __syncthreads();
-  }
+  POTRF_PHASE(1);
   for (int e = tid; e < n * n; e += kDagThreads) {
-    const int i = e % n, j = e / n;
-    F[i + (int64_t)j * ldf] = i >= j ? ls[i][j] : 0.0;
-    P[i + (int64_t)j * ldp] = i >= j ? xs[i][j] : 0.0;
+    const int r = e % n, c = e / n;
+    F[r + (int64_t)c * ldf] = r >= c ? ls[r][c] * rs[c] : 0.0;
+    P[r + (int64_t)c * ldp] = r >= c ? xs[r][c] * rs[r] : 0.0;
   }
 }
 
 // One tile task of front d (POTRF / TRSM / GEMM / ACC / FIN), no waits.
 __device__ void tile_task(const DagArgs& a, const DagFront& d, int kind, int i, int j, int k, double* sm) {
   double* F = a.front + d.fo;
-  double* P = a.panel + d.po;
+  const DagGroup& G = a.g[d.grp];
+  double* P = G.panel + d.po;
   const int r = d.r;
   auto tile = [&](double* base, int ti, int tj) { return base + bnd(d, ti) + (int64_t)bnd(d, tj) * r; };
   auto ext = [&](int b) { return bnd(d, b + 1) - bnd(d, b); };
@@ -331,13 +265,13 @@ __device__ void tile_task(const DagArgs& a, const DagFront& d, int kind, int i, 
     const int col0 = bnd(d, k);
     tile_potrf_inv(tile(F, k, k), r, tile(P, k, k), r, ext(k), sm, [&](int jj) {
       if (d.sid < 0) {  // plain dense matrix: the pivot index
-        atomicMin(a.fail, (unsigned long long)(col0 + jj));
+        atomicMin(G.fail, (unsigned long long)(col0 + jj));
         return;
       }
       // report the template slot of compact column col0 + jj (pivot rule, linalg.cpp:42-54)
-      const Supernode s = a.t.sn[d.sid];
-      const int q = a.f.tpos[(int64_t)d.sd * a.t.rows_total + s.rows_off + col0 + jj];
-      atomicMin(a.fail, (unsigned long long)((int64_t)d.sd * a.t.T + a.t.rows[s.rows_off + q]));
+      const Supernode s = G.t.sn[d.sid];
+      const int q = G.f.tpos[(int64_t)d.sd * G.t.rows_total + s.rows_off + col0 + jj];
+      atomicMin(G.fail, (unsigned long long)((int64_t)d.sd * G.t.T + G.t.rows[s.rows_off + q]));
     });
     // (the panel above this diagonal tile is never read: the sweeps start
     // every column at the 32-row block holding its diagonal)
@@ -376,15 +310,16 @@ __device__ __forceinline__ void wait_children(const DagArgs& a, const DagFront& 
 // diagonal shift, already in diag_add): entries staged as (compact row,
 // value); objects are disjoint, so rows touch distinct entries.
 __device__ void penalty_row(const DagArgs& a, const DagFront& d, int64_t row, double* sm) {
-  const FactorInput& in = a.in;
+  const DagGroup& G = a.g[d.grp];
+  const FactorInput& in = G.in;
   if (in.corner[row]) return;
   const int sd = d.sd, r = d.r;
-  const Supernode s = a.t.sn[d.sid];
+  const Supernode s = G.t.sn[d.sid];
   double* F = a.front + d.fo;
   const double rho = in.rho[sd];
   const int64_t p0 = in.c_ptr[row];
   const int len = (int)(in.c_ptr[row + 1] - p0);
-  auto pos = [&](int x) { return a.f.pfx[(int64_t)sd * a.t.rows_total + s.rows_off + a.t.root_pos[in.c_slot[p0 + x]]]; };
+  auto pos = [&](int x) { return G.f.pfx[(int64_t)sd * G.t.rows_total + s.rows_off + G.t.root_pos[in.c_slot[p0 + x]]]; };
   constexpr int kStage = 1024;
   __syncthreads();
   if (len > kStage) {  // very large object: unstaged
@@ -429,16 +364,17 @@ __device__ void penalty_row(const DagArgs& a, const DagFront& d, int64_t row, do
 
 // Assembly of rows [i0, i1) x cols [j0, j1) of front d (gather form).
 __device__ void assemble(const DagArgs& a, const DagFront& d, int i0, int i1, int j0, int j1, double* sm) {
-  const FrontDesc& fd = a.f.desc[(int64_t)d.sd * a.t.nsn + d.sid];
+  const DagGroup& G = a.g[d.grp];
+  const FrontDesc& fd = G.f.desc[(int64_t)d.sd * G.t.nsn + d.sid];
   RowInfo* ri = reinterpret_cast<RowInfo*>(sm);
   RowInfo* rj = ri + (i1 - i0);
   const bool same = i0 == j0 && i1 == j1;
   __syncthreads();
-  for (int q = threadIdx.x; q < i1 - i0; q += blockDim.x) ri[q] = row_info(a.f, fd, d.sd, a.in.T, a.in.b1, i0 + q);
+  for (int q = threadIdx.x; q < i1 - i0; q += blockDim.x) ri[q] = row_info(G.f, fd, d.sd, G.in.T, G.in.b1, i0 + q);
   if (!same)
-    for (int q = threadIdx.x; q < j1 - j0; q += blockDim.x) rj[q] = row_info(a.f, fd, d.sd, a.in.T, a.in.b1, j0 + q);
+    for (int q = threadIdx.x; q < j1 - j0; q += blockDim.x) rj[q] = row_info(G.f, fd, d.sd, G.in.T, G.in.b1, j0 + q);
   __syncthreads();
-  assemble_block(a.front + d.fo, d.r, d.c, i0, i1, j0, j1, ri, same ? ri : rj, child_blocks(a, d), a.in, d.sd);
+  assemble_block(a.front + d.fo, d.r, d.c, i0, i1, j0, j1, ri, same ? ri : rj, child_blocks(a, d), G.in, d.sd);
   __syncthreads();
 }
 
@@ -446,8 +382,9 @@ __device__ void assemble(const DagArgs& a, const DagFront& d, int i0, int i1, in
 // task in list order).
 __device__ void whole_front(const DagArgs& a, const DagFront& d, double* sm) {
   assemble(a, d, 0, d.r, 0, d.r, sm);
-  if (d.sid == a.t.root && a.in.c_ptr)
-    for (int64_t row = a.in.m_off[d.sd]; row < a.in.m_off[d.sd + 1]; ++row) penalty_row(a, d, row, sm);
+  const DagGroup& G = a.g[d.grp];
+  if (d.sid == G.t.root && G.in.c_ptr)
+    for (int64_t row = G.in.m_off[d.sd]; row < G.in.m_off[d.sd + 1]; ++row) penalty_row(a, d, row, sm);
   const int np = d.np, nt = d.nt;
   for (int k = 0; k < np; ++k) {
     tile_task(a, d, kPotrf, k, k, k, sm);
@@ -493,6 +430,10 @@ __global__ void __launch_bounds__(kDagThreads, 3) k_dense_dag(DagArgs a) {
         } else if (kind == kTrsm) {
           wait_eq(A + tri(k, k), k + 1);
           wait_eq(A + tri(i, k), k);
+        } else if (kind == kDiag) {  // i = k + 1
+          wait_eq(A + tri(k, k), k + 1);
+          wait_eq(A + tri(i, k), k);
+          wait_eq(A + tri(i, i), k);
         } else if (kind == kGemm) {
           wait_eq(A + tri(i, k), k + 1);
           wait_eq(A + tri(j, k), k + 1);
@@ -521,6 +462,20 @@ __global__ void __launch_bounds__(kDagThreads, 3) k_dense_dag(DagArgs a) {
     } else if (kind == kPen) {
       penalty_row(a, d, (int64_t)i, sm);
       done = fasm;
+    } else if (kind == kDiag) {
+      // the critical path of step k in one CTA: L_ik (TRSM, published at
+      // once for the other tasks of step k), the diagonal tile's last update
+      // F_ii -= L_ik L_ik^T, then POTRF(i)
+      tile_task(a, d, kTrsm, i, k, k, sm);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(A + tri(i, k), 1);
+      }
+      tile_task(a, d, kGemm, i, i, k, sm);
+      tile_task(a, d, kPotrf, i, i, i, sm);
+      done = A + tri(i, i);
+      inc = 2;
     } else {
       tile_task(a, d, kind, i, j, k, sm);
       if (kind == kPotrf || kind == kTrsm || kind == kGemm) {
@@ -616,6 +571,9 @@ std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
           for (int y = i; y < nt; ++y) s = std::max(s, G(y, i, k));
           for (int y = 0; y <= k; ++y) s = std::max(s, Ac(i, y, k));
           bl[x] = T(i, k) = 1 + s;
+          // DIAG(i) = TRSM(i,k) + GEMM(i,i,k) + POTRF(i) (i = k + 1 < np): the
+          // earlier updates of tile (i,i) precede the whole merged task
+          if (i == k + 1 && i < np) G(i, i, k) = T(i, k);
         } else if (kind == kGemm) {
           if (k + 1 < j && k + 1 < np)
             s = G(i, j, k + 1);
@@ -632,6 +590,24 @@ std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
           for (int y = i + 1; y < nt; ++y) s = std::max(s, Ac(y, j, i));
           bl[x] = Fn(i, j) = 1 + s;
         }
+      }
+      // merge the DIAG tasks: TRSM(k+1,k) becomes DIAG(k+1) (its bottom level
+      // covers the merged GEMM and POTRF), which are dropped
+      {
+        size_t w = 0;
+        for (size_t x = 0; x < ft.size(); ++x) {
+          const int kind = ft[x].x >> 24, i = ft[x].y, j = ft[x].z, k = ft[x].w;
+          if (kind == kTrsm && i == k + 1 && i < np) {
+            ft[x].x = (kDiag << 24) | id;
+          } else if ((kind == kGemm && i == j && i == k + 1 && i < np) || (kind == kPotrf && k > 0)) {
+            continue;
+          }
+          ft[w] = ft[x];
+          bl[w] = bl[x];
+          ++w;
+        }
+        ft.resize(w);
+        bl.resize(w);
       }
       for (int& b : bl) b += off;
       // assembly: ASM tiles, then the PEN rows, before every k = 0 task
@@ -657,8 +633,8 @@ std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
 }
 
 // One persistent launch over the plan's task list.
-void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, double* panel, unsigned long long* fail,
-                const TplDev& t, const FactorDev& fdv, const FactorInput& in, const std::vector<int4>* host_tasks) {
+void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, const std::vector<DagGroup>& groups,
+                const std::vector<int4>* host_tasks) {
   cudaStream_t s = h->stream;
   CB_CUDA(cudaMemsetAsync(plan.counters.p, 0, sizeof(int) * ((size_t)plan.n_counters + 1), s));
   static const char* trace_prefix = [] {
@@ -667,8 +643,16 @@ void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, double* panel, uns
   }();
   static DevBuf<unsigned long long> trace;
   if (trace_prefix) trace.alloc(4 * (size_t)plan.n_tasks);
-  DagArgs a{reinterpret_cast<const DagFront*>(plan.fronts.p), plan.tasks.p, plan.n_tasks, front, panel,
-            plan.counters.p, plan.counters.p + plan.n_counters, fail, t, fdv, in, trace_prefix ? trace.p : nullptr};
+  DagArgs a{};
+  a.fronts = reinterpret_cast<const DagFront*>(plan.fronts.p);
+  a.tasks = plan.tasks.p;
+  a.n_tasks = plan.n_tasks;
+  a.front = front;
+  a.counters = plan.counters.p;
+  a.ticket = plan.counters.p + plan.n_counters;
+  if (groups.size() > (size_t)kMaxGroups) throw Failure(CUTBDDC_CONFIG, "dense dag: too many factorisations in one launch");
+  for (size_t g = 0; g < groups.size(); ++g) a.g[g] = groups[g];
+  a.trace = trace_prefix ? trace.p : nullptr;
   const size_t shm = sizeof(double) * 2 * kTile * (kTile + 1);
   static int grid = 0;
   if (!grid) {
@@ -688,6 +672,8 @@ void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, double* panel, uns
     static int seq = 0;
     std::vector<unsigned long long> tr(4 * (size_t)plan.n_tasks);
     trace.download(tr.data(), tr.size(), s);
+    std::vector<long long> fr(plan.fronts.n);  // front records (DagFront, 10 x int64 each)
+    plan.fronts.download(fr.data(), fr.size(), s);
     CB_CUDA(cudaStreamSynchronize(s));
     const std::string path = std::string(trace_prefix) + "_" + std::to_string(seq++) + ".bin";
     if (FILE* fp = std::fopen(path.c_str(), "wb")) {
@@ -695,10 +681,7 @@ void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, double* panel, uns
       std::fwrite(&n, sizeof(int), 1, fp);
       std::fwrite(host_tasks->data(), sizeof(int4), host_tasks->size(), fp);
       std::fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fp);
-      std::vector<long long> fr(plan.fronts.n);  // front records (DagFront, 9 x int64 each)
-      plan.fronts.download(fr.data(), fr.size(), s);
-      CB_CUDA(cudaStreamSynchronize(s));
-      const int nf = (int)(fr.size() / 9);
+      const int nf = (int)(fr.size() / 10);
       std::fwrite(&nf, sizeof(int), 1, fp);
       std::fwrite(fr.data(), sizeof(long long), fr.size(), fp);
       std::fclose(fp);
@@ -719,8 +702,8 @@ void upload_plan(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, cons
     cnt += 2 + (d.whole ? 0 : (int64_t)d.nt * (d.nt + 1));
     dv[q] = d;
   }
-  static_assert(sizeof(DagFront) == 9 * sizeof(long long), "DagFront layout");
-  plan.fronts.upload(reinterpret_cast<const long long*>(dv.data()), dv.size() * 9, s);
+  static_assert(sizeof(DagFront) == 10 * sizeof(long long), "DagFront layout");
+  plan.fronts.upload(reinterpret_cast<const long long*>(dv.data()), dv.size() * 10, s);
   plan.tasks.upload(tasks, s);
   plan.n_tasks = (int)tasks.size();
   plan.n_counters = cnt;
@@ -729,51 +712,63 @@ void upload_plan(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, cons
 
 }  // namespace
 
-// Host: the whole factorisation of subdomains [sd0, sd1) as one dataflow
-// launch (every front of every level; foff / poff: front-workspace and panel
-// offsets per (sd, supernode); the chunk's workspace starts at `front`). The
-// task list is rebuilt only when the compact front sizes change.
-void dense_dag_tree(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const FactorInput& in, int sd0, int sd1,
-                    const std::vector<int64_t>& foff, const std::vector<int64_t>& poff, double* front,
-                    unsigned long long* fail) {
+// Host: the numeric factorisation of every span (subdomains [sd0, sd1) of
+// one factorisation each; fronts at span.front_off + the subdomain's front
+// base + the per-front offset in `front`) as ONE dataflow launch: every
+// front of every level of every span. The task list is rebuilt only when the
+// compact front sizes change.
+void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, double* front) {
   cudaStream_t s = h->stream;
-  const int nsn = (int)ts.tpl.sn.size();
-  DagPlan& plan = f.dag;
-  const bool same_rc = plan.key.size() == f.h_rc.size() &&
-                       std::memcmp(plan.key.data(), f.h_rc.data(), sizeof(int2) * f.h_rc.size()) == 0;
-  const bool hit = plan.sd0 == sd0 && plan.sd1 == sd1 && same_rc && !std::getenv("CUTBDDC_DAG_TRACE");
+  DagPlan& plan = h->dag_factor;
+  std::vector<int2> key;
+  for (const FactorSpan& sp : spans) {
+    key.push_back(make_int2(sp.sd0, sp.sd1));
+    key.push_back(make_int2((int)(sp.front_off >> 31), (int)(sp.front_off & 0x7fffffff)));
+    key.insert(key.end(), sp.f->h_rc.begin(), sp.f->h_rc.end());
+  }
+  const bool hit = plan.key.size() == key.size() &&
+                   std::memcmp(plan.key.data(), key.data(), sizeof(int2) * key.size()) == 0 &&
+                   !std::getenv("CUTBDDC_DAG_TRACE");
   std::vector<int4> tasks;
   if (!hit) {
     ProfScope ps(h->prof, s, "dense dag host+upload");
     std::vector<HostFront> fr;
-    std::vector<int> idx((size_t)(sd1 - sd0) * nsn, -1);
-    for (int sd = sd0; sd < sd1; ++sd)
-      for (int sid = 0; sid < nsn; ++sid) {  // postorder: children first
-        const int2 v = f.h_rc[(size_t)sd * nsn + sid];
-        if (v.x == 0) continue;
-        const Supernode& sn = ts.tpl.sn[(size_t)sid];
-        HostFront hf{};
-        DagFront& d = hf.d;
-        d.r = v.x;
-        d.c = v.y;
-        d.np = (v.y + kTile - 1) / kTile;
-        d.nt = d.np + (v.x - v.y + kTile - 1) / kTile;
-        d.fo = (f.h_front_base[(size_t)sd] - f.h_front_base[(size_t)sd0]) + foff[(size_t)sd * nsn + sid];
-        d.po = poff[(size_t)sd * nsn + sid];
-        d.sd = sd;
-        d.sid = sid;
-        d.whole = ts.is_split[(size_t)sid] ? 0 : 1;
-        d.ch0 = sn.nchild > 0 ? idx[(size_t)(sd - sd0) * nsn + sn.child[0]] : -1;
-        d.ch1 = sn.nchild > 1 ? idx[(size_t)(sd - sd0) * nsn + sn.child[1]] : -1;
-        hf.parent = -1;
-        hf.pen0 = hf.pen1 = 0;
-        if (!d.whole && sid == nsn - 1 && in.c_ptr) {
-          hf.pen0 = h->h_m_off[(size_t)sd];
-          hf.pen1 = h->h_m_off[(size_t)sd + 1];
+    for (size_t g = 0; g < spans.size(); ++g) {
+      const FactorSpan& sp = spans[g];
+      const TplSet& ts = *sp.ts;
+      const FactorSet& f = *sp.f;
+      const int nsn = (int)ts.tpl.sn.size();
+      std::vector<int> idx((size_t)(sp.sd1 - sp.sd0) * nsn, -1);
+      for (int sd = sp.sd0; sd < sp.sd1; ++sd)
+        for (int sid = 0; sid < nsn; ++sid) {  // postorder: children first
+          const size_t fs = (size_t)sd * nsn + sid;
+          const int2 v = f.h_rc[fs];
+          if (v.x == 0) continue;
+          const Supernode& sn = ts.tpl.sn[(size_t)sid];
+          HostFront hf{};
+          DagFront& d = hf.d;
+          d.r = v.x;
+          d.c = v.y;
+          d.np = (v.y + kTile - 1) / kTile;
+          d.nt = d.np + (v.x - v.y + kTile - 1) / kTile;
+          d.fo = sp.front_off + (f.h_front_base[(size_t)sd] - f.h_front_base[(size_t)sp.sd0]) + f.h_front_off[fs];
+          d.po = f.h_panel_off[fs];
+          d.sd = sd;
+          d.sid = sid;
+          d.grp = (int)g;
+          d.whole = ts.is_split[(size_t)sid] ? 0 : 1;
+          d.ch0 = sn.nchild > 0 ? idx[(size_t)(sd - sp.sd0) * nsn + sn.child[0]] : -1;
+          d.ch1 = sn.nchild > 1 ? idx[(size_t)(sd - sp.sd0) * nsn + sn.child[1]] : -1;
+          hf.parent = -1;
+          hf.pen0 = hf.pen1 = 0;
+          if (!d.whole && sid == nsn - 1 && sp.in->c_ptr) {
+            hf.pen0 = h->h_m_off[(size_t)sd];
+            hf.pen1 = h->h_m_off[(size_t)sd + 1];
+          }
+          idx[(size_t)(sd - sp.sd0) * nsn + sid] = (int)fr.size();
+          fr.push_back(hf);
         }
-        idx[(size_t)(sd - sd0) * nsn + sid] = (int)fr.size();
-        fr.push_back(hf);
-      }
+    }
     for (size_t q = 0; q < fr.size(); ++q) {
       const DagFront& d = fr[q].d;
       if (d.ch0 >= 0) fr[(size_t)d.ch0].parent = (int)q;
@@ -782,11 +777,12 @@ void dense_dag_tree(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const Factor
     if (fr.empty()) return;
     tasks = build_tasks(fr);
     upload_plan(h, plan, fr, tasks);
-    plan.key = f.h_rc;
-    plan.sd0 = sd0;
-    plan.sd1 = sd1;
+    plan.key = key;
   }
-  launch_dag(h, plan, front, f.panel.p, fail, tpl_dev(ts, h->slots), factor_dev(f), in, hit ? nullptr : &tasks);
+  std::vector<DagGroup> groups;
+  for (const FactorSpan& sp : spans)
+    groups.push_back(DagGroup{tpl_dev(*sp.ts, h->slots), factor_dev(*sp.f), *sp.in, sp.f->panel.p, sp.fail});
+  launch_dag(h, plan, front, groups, hit ? nullptr : &tasks);
 }
 
 // Cholesky + explicit inverse factor of one dense SPD n x n matrix (A:
@@ -811,7 +807,7 @@ void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long
   fr[0].d.ntask = (int)kept.size();
   upload_plan(h, h->dag_dense, fr, kept);
   ps.close();
-  launch_dag(h, h->dag_dense, A, X, fail, TplDev{}, FactorDev{}, FactorInput{}, &kept);
+  launch_dag(h, h->dag_dense, A, {DagGroup{TplDev{}, FactorDev{}, FactorInput{}, X, fail}}, &kept);
 }
 
 }  // namespace cutbddc_b200

@@ -404,17 +404,17 @@ double sweep_bytes(const FactorSet& f) { return f.bytes_per_sweep; }
 // device bytes of the (grow-only, reusable) front workspace already held
 static int64_t front_bytes_held(const cutbddc_gpu* h) { return (int64_t)h->ws_front.cap * (int64_t)sizeof(double); }
 
-// Symbolic (compact structure) + numeric factorisation of every subdomain.
-void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, FactorSet& f, const char* what) {
+static const char* tag_of(const cutbddc_gpu* h, const TplSet& ts) { return &ts == &h->tI ? "I" : "K"; }
+
+// Symbolic phase: compact rows per (sd, supernode), offsets, sweep plan.
+void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, FactorSet& f) {
   cudaStream_t s = h->stream;
   const TplDev t = tpl_dev(ts, h->slots);
   const int nsd = h->nsd, nsn = t.nsn;
-  // symbolic: compact rows per (sd, supernode)
   f.pfx.alloc((size_t)nsd * t.rows_total);
   f.tpos.alloc((size_t)nsd * t.rows_total);
   f.rc.alloc((size_t)nsd * nsn);
-  ProfScope psym(h->prof, s, std::string("factor") + (&ts == &h->tI ? "I" : "K") + " total");
-  ProfScope pplan(h->prof, s, std::string("factor") + (&ts == &h->tI ? "I" : "K") + " symbolic+plan");
+  ProfScope pplan(h->prof, s, std::string("factor") + tag_of(h, ts) + " symbolic+plan");
   k_symbolic<<<dim3(nsn, nsd), kThreads, 0, s>>>(t, nsd, in.mask, f.pfx.p, f.tpos.p, f.rc.p);
   CB_LAUNCH();
   f.h_rc = f.rc.to_host(s);
@@ -444,41 +444,64 @@ void factor_device(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fact
   f.flops = flops;
   f.panel_off.upload(poff, s);
   f.h_panel_off = poff;
+  f.h_front_off = foff;
   f.upd_off.upload(uoff, s);
-  f.front_off.upload(foff, s);
-  DevBuf<int64_t>& fbase = h->ws_fbase;
-  fbase.upload(f.h_front_base, s);
   f.panel.alloc((size_t)std::max<int64_t>(1, pt));
   build_sweep_plan(h, ts, f, poff, uoff);
-  pplan.close();
-  // numeric, in subdomain chunks bounded by a front-workspace budget: half
-  // of the free device memory (every chunk repeats the tree's critical path)
+}
+
+// Numeric phase. The factorisations share one dataflow launch (the interior
+// problems' fronts fill the SMs the K root's POTRF chain leaves idle) when
+// all their fronts fit a workspace budget of half the free device memory;
+// otherwise each runs alone in subdomain chunks bounded by the budget (every
+// chunk repeats the tree's critical path).
+void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs) {
+  cudaStream_t s = h->stream;
+  const int nsd = h->nsd;
   size_t free_b = 0, total_b = 0;
   CB_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const int64_t budget = std::max<int64_t>((1ll << 30) / 8, (int64_t)(free_b / 2 + front_bytes_held(h)) / 8);
   DevBuf<unsigned long long>& fail = h->ws_fail;
-  fail.alloc(1);
-  CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
+  fail.alloc(jobs.size());
+  CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8 * jobs.size(), s));
   DevBuf<double>& front = h->ws_front;
-  ProfScope pnum(h->prof, s, std::string("factor") + (&ts == &h->tI ? "I" : "K") + " numeric");
-  int sd0 = 0;
-  while (sd0 < nsd) {
-    int sd1 = sd0 + 1;
-    while (sd1 < nsd && f.h_front_base[(size_t)sd1 + 1] - f.h_front_base[(size_t)sd0] <= budget) ++sd1;
-    const int64_t need = f.h_front_base[(size_t)sd1] - f.h_front_base[(size_t)sd0];
-    if ((int64_t)front.n < need) front.alloc((size_t)need);
-    dense_dag_tree(h, ts, f, in, sd0, sd1, foff, poff, front.p, fail.p);
-    sd0 = sd1;
+  ProfScope pnum(h->prof, s, "factor numeric");
+  int64_t all = 0;
+  for (const FactorJob& j : jobs) all += j.f->h_front_base[(size_t)nsd];
+  if (all <= budget) {
+    std::vector<FactorSpan> spans;
+    int64_t off = 0;
+    for (size_t g = 0; g < jobs.size(); ++g) {
+      spans.push_back(FactorSpan{jobs[g].ts, jobs[g].in, jobs[g].f, 0, nsd, off, fail.p + g});
+      off += jobs[g].f->h_front_base[(size_t)nsd];
+    }
+    if ((int64_t)front.n < all) front.alloc((size_t)std::max<int64_t>(1, all));
+    dense_dag_factor(h, spans, front.p);
+  } else {
+    for (size_t g = 0; g < jobs.size(); ++g) {
+      const FactorSet& f = *jobs[g].f;
+      int sd0 = 0;
+      while (sd0 < nsd) {
+        int sd1 = sd0 + 1;
+        while (sd1 < nsd && f.h_front_base[(size_t)sd1 + 1] - f.h_front_base[(size_t)sd0] <= budget) ++sd1;
+        const int64_t need = f.h_front_base[(size_t)sd1] - f.h_front_base[(size_t)sd0];
+        if ((int64_t)front.n < need) front.alloc((size_t)need);
+        dense_dag_factor(h, {FactorSpan{jobs[g].ts, jobs[g].in, jobs[g].f, sd0, sd1, 0, fail.p + g}}, front.p);
+        sd0 = sd1;
+      }
+    }
   }
   pnum.close();
-  unsigned long long fl = 0;
-  CB_CUDA(cudaMemcpyAsync(&fl, fail.p, 8, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> fl(jobs.size());
+  CB_CUDA(cudaMemcpyAsync(fl.data(), fail.p, 8 * jobs.size(), cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
-  if (fl != ~0ull) {
-    const int64_t sd = (int64_t)(fl / (unsigned long long)h->slots), slot = (int64_t)(fl % (unsigned long long)h->slots);
-    throw Failure(CUTBDDC_SINGULAR, std::string(what) + ": matrix is not positive definite (subdomain " +
-                                        std::to_string(sd) + ", pivot slot " + std::to_string(slot) + ")");
-  }
+  for (size_t g = 0; g < jobs.size(); ++g)
+    if (fl[g] != ~0ull) {
+      const int64_t sd = (int64_t)(fl[g] / (unsigned long long)h->slots);
+      const int64_t slot = (int64_t)(fl[g] % (unsigned long long)h->slots);
+      throw Failure(CUTBDDC_SINGULAR, std::string(jobs[g].what) + ": matrix is not positive definite (subdomain " +
+                                          std::to_string(sd) + ", pivot slot " + std::to_string(slot) + ")");
+    }
 }
 
 // CUTBDDC_LEVEL_SWEEPS=1 selects the level-synchronous sweeps for single

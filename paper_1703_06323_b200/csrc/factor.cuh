@@ -56,7 +56,18 @@ struct FactorInput {
 TplDev tpl_dev(const TplSet& t, int slots);
 FactorDev factor_dev(const FactorSet& f);
 void upload_template(cutbddc_gpu* h, TplSet& t, bool shell_root);
-void factor_device(cutbddc_gpu* h, const TplSet& t, const FactorInput& in, FactorSet& f, const char* what);
+// Symbolic phase of one factorisation: compact front sizes, panel / update /
+// front-workspace offsets, the sweep plan.
+void factor_symbolic(cutbddc_gpu* h, const TplSet& t, const FactorInput& in, FactorSet& f);
+// Numeric phase of one or two factorisations (after factor_symbolic), as one
+// dataflow launch when their fronts fit the workspace budget together.
+struct FactorJob {
+  const TplSet* ts;
+  const FactorInput* in;
+  FactorSet* f;
+  const char* what;  // error message prefix (non-positive pivot)
+};
+void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs);
 // ysave: nrhs x nsd x T doubles of scratch (forward results of big fronts).
 // rhs_root_only: the right-hand sides are nonzero only on root columns (the
 // W = K^{-1} C^T solve on the shell template); the lower forward steps are skipped.
@@ -72,11 +83,16 @@ void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
 enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3 };
 void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip, int phase);
-// dense_dag.cu: the numeric factorisation of subdomains [sd0, sd1) as one
-// dataflow launch over every front (front workspace based at sd0)
-void dense_dag_tree(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const FactorInput& in, int sd0, int sd1,
-                    const std::vector<int64_t>& foff, const std::vector<int64_t>& poff, double* front,
-                    unsigned long long* fail);
+// dense_dag.cu: numeric factorisation of every span as one dataflow launch
+struct FactorSpan {
+  const TplSet* ts;
+  const FactorInput* in;
+  FactorSet* f;
+  int sd0, sd1;                // subdomains of this factorisation in the launch
+  int64_t front_off;           // their front workspace offset in the launch's workspace
+  unsigned long long* fail;    // pivot failure report
+};
+void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, double* front);
 // dense_dag.cu: Cholesky (A, column-major lower, overwritten) and X = L^{-1}
 // of one dense SPD matrix; a failing pivot index goes to *fail
 void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long long* fail);

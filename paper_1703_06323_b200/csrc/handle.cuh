@@ -47,11 +47,11 @@ struct TplSet {
 
 // Task list of one dataflow factorisation launch (dense_dag.cu).
 struct DagPlan {
-  cutbddc_b200::DevBuf<long long> fronts;      // per front record (9 x int64)
+  cutbddc_b200::DevBuf<long long> fronts;      // per front record (10 x int64)
   cutbddc_b200::DevBuf<int4> tasks;            // (kind << 24 | front, i, j, k) in ticket order
   cutbddc_b200::DevBuf<int> counters;          // per front: done, assembled, tile counters; then the ticket
-  std::vector<int2> key;                       // compact front sizes the list was built for
-  int sd0 = -1, sd1 = -1, n_tasks = 0;
+  std::vector<int2> key;                       // spans + compact front sizes the list was built for
+  int n_tasks = 0;
   int64_t n_counters = 0;
 };
 
@@ -62,7 +62,7 @@ struct FactorSet {
   cutbddc_b200::DevBuf<int32_t> pfx;           // nsd x rows_total
   cutbddc_b200::DevBuf<int32_t> tpos;          // nsd x rows_total (inverse of pfx)
   cutbddc_b200::DevBuf<int2> rc;               // nsd x nsn
-  cutbddc_b200::DevBuf<int64_t> panel_off, upd_off, front_off;  // nsd x nsn
+  cutbddc_b200::DevBuf<int64_t> panel_off, upd_off;  // nsd x nsn
   std::vector<int2> h_rc;
   std::vector<int64_t> h_front_base;           // nsd + 1 (front workspace prefix)
   int64_t panel_total = 0, upd_total = 0;
@@ -84,7 +84,7 @@ struct FactorSet {
   int n_items_b_root = 0;                      // leading backward items of the root level
   std::vector<int64_t> h_vec_off;              // nsd x nsn compact front vector offsets (host copy)
   std::vector<int64_t> h_panel_off;            // nsd x nsn panel offsets (host copy)
-  DagPlan dag;                                 // dataflow factorisation (dense_dag.cu)
+  std::vector<int64_t> h_front_off;            // nsd x nsn front offsets inside the subdomain's workspace
 };
 
 struct cutbddc_gpu {
@@ -195,9 +195,10 @@ struct cutbddc_gpu {
   // persistent scratch (grow-only) so repeated solves allocate nothing
   cutbddc_b200::DevBuf<double> ws_front, ws_upd, ws_s, ws_lc, ws_cpart, ws_q8, ws_kint;
   cutbddc_b200::DevBuf<unsigned long long> ws_fail;
-  cutbddc_b200::DevBuf<int64_t> ws_fbase, ws_cnt, ws_nc64;
+  cutbddc_b200::DevBuf<int64_t> ws_cnt, ws_nc64;
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp;
   cutbddc_b200::DevBuf<int> ws_flag;
+  DagPlan dag_factor;                              // dense_dag.cu: the subdomain factorisations (one launch)
   DagPlan dag_dense;                               // dense_dag.cu: the coarse matrix factorisation
 
   // pcg vectors

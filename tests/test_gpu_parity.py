@@ -196,3 +196,18 @@ def test_cfg5_full_size_properties():
     r = b - s.spmv(x)
     assert np.linalg.norm(r) <= 2 * cfg.rtol * np.linalg.norm(b)
     s.close()
+
+
+def test_cut_element_matrices_match_oracle(cfg2s):
+    """Cut-cell element matrices, load vectors and beta against the oracle's
+    per-cell restatement (same rule, same operation order: 1e-13 relative)."""
+    cfg, o, s, pb = cfg2s
+    cells, ke, fe = s.cut_elements()
+    assert len(cells) > 0
+    rng = np.random.default_rng(3)
+    pick = rng.choice(len(cells), size=min(300, len(cells)), replace=False)
+    for q in pick:
+        k_o, f_o, beta_o, empty_o = o.element(int(cells[q]))
+        scale = max(np.abs(k_o).max(), 1e-300)
+        assert np.abs(ke[q] - k_o).max() <= 1e-13 * scale, int(cells[q])
+        assert np.abs(fe[q] - f_o).max() <= 1e-13 * max(np.abs(f_o).max(), 1e-300), int(cells[q])

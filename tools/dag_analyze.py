@@ -10,7 +10,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from trace_analyze import load  # noqa: E402
 
-NAMES = ["POTRF", "TRSM", "GEMM", "ACC", "FIN", "ASM", "PEN", "W"]
+NAMES = ["POTRF", "TRSM", "GEMM", "ACC", "FIN", "ASM", "PEN", "W", "DIAG"]
 
 
 def load_fronts(path, n_tasks):
@@ -20,9 +20,9 @@ def load_fronts(path, n_tasks):
         if len(raw) < 4:
             return None
         nf = int(np.frombuffer(raw, np.int32)[0])
-        rec = np.frombuffer(f.read(72 * nf), np.int64).reshape(nf, 9)
-    ints = rec[:, 3:].copy().view(np.int32).reshape(nf, 12)
-    # r, c, np, nt, sd, sid, ch0, ch1, ntask, nasm, ntile, whole
+        rec = np.frombuffer(f.read(80 * nf), np.int64).reshape(nf, 10)
+    ints = rec[:, 3:].copy().view(np.int32).reshape(nf, 14)
+    # r, c, np, nt, sd, sid, ch0, ch1, ntask, nasm, ntile, whole, grp, pad
     return ints
 
 
@@ -44,10 +44,10 @@ for p in sorted(glob.glob(sys.argv[1] + "_*.bin")):
     fr = load_fronts(p, len(items))
     if fr is None:
         continue
-    sid = fr[fid, 5]
-    print("  per supernode: sid  fronts  whole  rows(max) cols(max)  first start  last end (us from launch)")
-    for s in np.unique(sid)[::-1]:
-        m = sid == s
-        fm = fr[:, 5] == s
-        print(f"    {s:4d} {fm.sum():6d} {fr[fm, 11].max():5d} {fr[fm, 0].max():8d} {fr[fm, 1].max():8d}"
+    key = fr[fid, 12] * 100000 + fr[fid, 5]
+    print("  per supernode: grp  sid  fronts  whole  rows(max) cols(max)  first start  last end (us from launch)")
+    for s in np.unique(key)[::-1]:
+        m = key == s
+        fm = fr[:, 12] * 100000 + fr[:, 5] == s
+        print(f"    {s // 100000:3d} {s % 100000:4d} {fm.sum():6d} {fr[fm, 11].max():5d} {fr[fm, 0].max():8d} {fr[fm, 1].max():8d}"
               f"  {(tr[m, 0].min() - t0) / 1e3:10.1f} {(tr[m, 2].max() - t0) / 1e3:10.1f}")

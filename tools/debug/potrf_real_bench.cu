@@ -3,115 +3,29 @@
 // tile; per-CTA time via %globaltimer.
 // nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Ipaper_1703_06323_b200/csrc -Iinclude \
 //   -I<nccl include> tools/debug/potrf_real_bench.cu -Lpaper_1703_06323_b200 -lcutbddc
+__device__ unsigned long long g_phase[8];
+#define POTRF_PHASE(k)                                                         \
+  do {                                                                         \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                                 \
+      unsigned long long t_;                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+      g_phase[k] = t_;                                                         \
+    }                                                                          \
+  } while (0)
 #include "../../paper_1703_06323_b200/csrc/dense_dag.cu"
 
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
 namespace cutbddc_b200 {
 namespace {
-template <typename Fail>
-__device__ void potrf_phased(double* F, int ldf, double* P, int ldp, int n, double* sm, Fail fail, unsigned long long* ph) {
-  int np_ = 0;
-#define STAMP() do { __syncthreads(); if (threadIdx.x == 0) ph[np_] = dag_timer(); ++np_; } while (0)
-  SmTile* ls = reinterpret_cast<SmTile*>(sm);
-  SmTile* xs = reinterpret_cast<SmTile*>(sm + kTile * (kTile + 1));
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nb = (n + 15) / 16;
-  __syncthreads();
-  for (int e = tid; e < kTile * kTile; e += kDagThreads) {
-    const int i = e & 63, j = e >> 6;
-    ls[i][j] = (i < n && j < n && i >= j) ? F[i + (int64_t)j * ldf] : 0.0;
-    xs[i][j] = 0.0;
-  }
-  STAMP();
-  for (int b = 0; b < nb; ++b) {
-    const int o = 16 * b, m = min(16, n - o), below = n - o - m;
-    if (wid == 0) {
-      warp_chol16(ls, o, m, lane, fail);
-      __syncwarp();
-      warp_inv16(ls, xs, o, m, lane);
-    }
-    STAMP();
-    if (below <= 0) break;
-    // L_ib = A_ib X_bb^T (rows o+16.., columns o..o+m)
-    double l[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kDagThreads, i = o + 16 + (e >> 4), q = e & 15;
-      double s = 0.0;
-      if (i < n && q < m)
-        for (int k = 0; k <= q; ++k) s += ls[i][o + k] * xs[o + q][o + k];
-      l[u] = s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kDagThreads, i = o + 16 + (e >> 4), q = e & 15;
-      if (i < n && q < m) ls[i][o + q] = l[u];
-    }
-    __syncthreads();
-    // trailing update A_ij -= L_ib L_jb^T (o+16 <= j <= i < n)
-    for (int e = tid; e < below * below; e += kDagThreads) {
-      const int i = o + 16 + e / below, j = o + 16 + e % below;
-      if (j > i) continue;
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) s += ls[i][o + k] * ls[j][o + k];
-      ls[i][j] -= s;
-    }
-    STAMP();
-  }
-  // off-diagonal blocks of X, one block diagonal at a time
-  for (int d = 1; d < nb; ++d) {
-    const int nblk = nb - d;
-    // T_ij = sum_{k=j}^{i-1} L_ik X_kj into xs block (i, j)
-    for (int e = tid; e < nblk * 256; e += kDagThreads) {
-      const int jb = e >> 8, ib = jb + d, p = (e >> 4) & 15, q = e & 15;
-      const int i = 16 * ib + p, j = 16 * jb + q;
-      double s = 0.0;
-      if (i < n)
-        for (int k = 16 * jb; k < 16 * ib; ++k) s += ls[i][k] * xs[k][j];
-      xs[i][j] = s;
-    }
-    __syncthreads();
-    double x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kDagThreads;
-      double s = 0.0;
-      if (e < nblk * 256) {
-        const int jb = e >> 8, ib = jb + d, p = (e >> 4) & 15, q = e & 15;
-        const int i = 16 * ib + p, j = 16 * jb + q;
-        for (int t = 16 * ib; t <= i; ++t) s += xs[i][t] * xs[t][j];
-      }
-      x[u] = -s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kDagThreads;
-      if (e < nblk * 256) {
-        const int jb = e >> 8, ib = jb + d, p = (e >> 4) & 15, q = e & 15;
-        xs[16 * ib + p][16 * jb + q] = x[u];
-      }
-    }
-    __syncthreads();
-  }
-  STAMP();
-  for (int e = tid; e < n * n; e += kDagThreads) {
-    const int i = e % n, j = e / n;
-    F[i + (int64_t)j * ldf] = i >= j ? ls[i][j] : 0.0;
-    P[i + (int64_t)j * ldp] = i >= j ? xs[i][j] : 0.0;
-  }
-  STAMP();
-#undef STAMP
-}
-
-__global__ void k_potrf_phases(double* F, double* P, int n, unsigned long long* ph) {
+__global__ void __launch_bounds__(256, 2) k_potrf_phases(double* F, double* P, int n, unsigned long long* ph) {
   extern __shared__ double sm[];
   if (threadIdx.x == 0) ph[31] = dag_timer();
-  potrf_phased(F, n, P, n, n, sm, [](int) {}, ph);
+  tile_potrf_inv(F, n, P, n, n, sm, [](int) {});
+  __syncthreads();
+  if (threadIdx.x == 0) ph[0] = dag_timer();
 }
 
 __global__ void __launch_bounds__(kDagThreads, 3) k_potrf_bench(double* F, double* P, int n, unsigned long long* t) {
@@ -152,9 +66,24 @@ int main() {
     }
     unsigned long long h[32];
     cudaMemcpy(h, ph, sizeof(h), cudaMemcpyDeviceToHost);
-    printf("phases (us from start): load %.2f", (h[0] - h[31]) / 1e3);
-    for (int q = 1; q < 14; ++q) printf(" | %.2f", (h[q] - h[31]) / 1e3);
-    printf("\n");
+    printf("single CTA: %.2f us\n", (h[0] - h[31]) / 1e3);
+    unsigned long long gp[8];
+    cudaMemcpyFromSymbol(gp, g_phase, sizeof(gp));
+    printf("phases: load %.2f eliminate %.2f store %.2f us\n", (gp[0] - h[31]) / 1e3, (gp[1] - gp[0]) / 1e3,
+           (h[0] - gp[1]) / 1e3);
+    std::vector<double> L(n * n), X(n * n);
+    cudaMemcpy(L.data(), F, n * n * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(X.data(), P, n * n * 8, cudaMemcpyDeviceToHost);
+    double e1 = 0, e2 = 0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double s = 0, t = 0;
+        for (int k = 0; k <= j; ++k) s += L[i + k * n] * L[j + k * n];
+        for (int k = j; k <= i; ++k) t += X[i + k * n] * L[k + j * n];
+        e1 = std::max(e1, std::fabs(s - A[i + j * n]));
+        e2 = std::max(e2, std::fabs(t - (i == j ? 1.0 : 0.0)));
+      }
+    printf("max |LL^T - A| %.3e  max |XL - I| %.3e\n", e1, e2);
   }
   for (int ncta : {1, 148, 296, 444}) {
     std::vector<unsigned long long> ht(ncta);
