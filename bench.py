@@ -184,8 +184,11 @@ def main():
     def step_e2e():
         t0 = time.perf_counter()
         dirichlet = assemble(mesh)                                     # H2D of the mesh view
-        diag = solver.local_diagonals() if cfg.variant == configs.V2 else None
-        o2 = cb.classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, diag)
+        if cfg.variant == configs.V_STANDARD:                         # objects on the device
+            o2 = solver.classify_objects(cfg.objects, cfg.variant)
+        else:                                                          # v1/v2 edge splits: host
+            diag = solver.local_diagonals() if cfg.variant == configs.V2 else None
+            o2 = cb.classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, diag)
         solver.setup_bddc(o2, cfg.weighting)
         x, rep = solver.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)     # D2H of x
         return time.perf_counter() - t0, rep

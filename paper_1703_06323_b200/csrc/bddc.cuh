@@ -8,6 +8,7 @@ namespace cutbddc_b200 {
 
 void classify_device(cutbddc_gpu* h, const cutbddc_geometry* g);
 void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_ids);
+cutbddc_objects* classify_objects_device(cutbddc_gpu* h, int objects);
 void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weighting);
 void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip);
 void spmv_device(cutbddc_gpu* h, const double* x, double* y);

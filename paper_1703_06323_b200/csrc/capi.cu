@@ -203,6 +203,20 @@ cutbddc_status cutbddc_gpu_local_diagonals(cutbddc_gpu* h, double* diag, int64_t
   });
 }
 
+cutbddc_status cutbddc_gpu_classify_objects(cutbddc_gpu* h, int objects, int variant, cutbddc_objects** out) {
+  return guard([&] {
+    need(h);
+    if (!out) throw Failure(CUTBDDC_INVALID_ARGUMENT, "objects: null output");
+    if (objects < CUTBDDC_OBJECTS_C || objects > CUTBDDC_OBJECTS_CEF)
+      throw Failure(CUTBDDC_CONFIG, "bddc.objects must be c, ce or cef");
+    if (variant != CUTBDDC_VARIANT_STANDARD)
+      throw Failure(CUTBDDC_CONFIG, "device objects: standard variant only (v1/v2: cutbddc_classify_objects)");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "objects: assemble first");
+    *out = classify_objects_device(h, objects);
+  });
+}
+
 cutbddc_status cutbddc_gpu_setup_bddc(cutbddc_gpu* h, const cutbddc_coarse_view* coarse, int weighting) {
   return guard([&] {
     need(h);

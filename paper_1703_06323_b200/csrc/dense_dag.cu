@@ -728,7 +728,7 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
   }
   const bool hit = plan.key.size() == key.size() &&
                    std::memcmp(plan.key.data(), key.data(), sizeof(int2) * key.size()) == 0 &&
-                   !std::getenv("CUTBDDC_DAG_TRACE");
+                   !std::getenv("CUTBDDC_DAG_TRACE") && !std::getenv("CUTBDDC_NO_PLAN_CACHE");
   std::vector<int4> tasks;
   if (!hit) {
     ProfScope ps(h->prof, s, "dense dag host+upload");

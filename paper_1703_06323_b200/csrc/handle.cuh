@@ -196,7 +196,7 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<double> ws_front, ws_upd, ws_s, ws_lc, ws_cpart, ws_q8, ws_kint;
   cutbddc_b200::DevBuf<unsigned long long> ws_fail;
   cutbddc_b200::DevBuf<int64_t> ws_cnt, ws_nc64;
-  cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp;
+  cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp, ws_obj;
   cutbddc_b200::DevBuf<int> ws_flag;
   DagPlan dag_factor;                              // dense_dag.cu: the subdomain factorisations (one launch)
   DagPlan dag_dense;                               // dense_dag.cu: the coarse matrix factorisation

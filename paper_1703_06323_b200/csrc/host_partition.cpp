@@ -14,10 +14,13 @@
 // strong-Dirichlet (orphan) dofs excluded.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <mutex>
 #include <numeric>
+#include <thread>
 #include <string>
-#include <unordered_map>
 #include <vector>
 
 #include "cutbddc.h"
@@ -52,6 +55,36 @@ struct Lattice {
     return false;
   }
 };
+
+// Static partition of [0, n) over up to 16 host threads (results do not
+// depend on the thread count: every index writes only its own outputs).
+template <typename F>
+void parallel_for(int64_t n, F&& f) {
+  static const int hw = [] {
+    const char* e = std::getenv("CUTBDDC_HOST_THREADS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+  }();
+  const int nt = (int)std::min<int64_t>(hw, std::max<int64_t>(1, n / 4));
+  if (nt <= 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::exception_ptr err;
+  std::mutex mu;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      try {
+        for (int64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) f(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
+}
 
 struct Obj {
   int kind;
@@ -110,14 +143,6 @@ std::vector<std::vector<int32_t>> components(const Lattice& L, const std::vector
   return comps;
 }
 
-struct VecHash {
-  size_t operator()(const std::vector<int32_t>& v) const {
-    size_t h = 1469598103934665603ull;
-    for (int32_t x : v) h = (h ^ (size_t)(uint32_t)x) * 1099511628211ull;
-    return h;
-  }
-};
-
 void check_mesh(const cutbddc_mesh_view* m) {
   if (!m || !m->cls || !m->dof_of_node) throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: null arrays");
   if (m->cells[0] != m->cells[1] || m->cells[1] != m->cells[2])
@@ -162,67 +187,99 @@ extern "C" cutbddc_status cutbddc_classify_objects(const cutbddc_mesh_view* mesh
     const int nb = n / B;
     const int64_t ndof = mesh->n_dof;
     Lattice L{n, mesh->cls, mesh->dof_of_node};
-    std::vector<int64_t> node_of_dof((size_t)ndof);
-    {
-      const int64_t nn = (int64_t)(n + 1) * (n + 1) * (n + 1);
-      for (int64_t v = 0; v < nn; ++v)
-        if (mesh->dof_of_node[v] >= 0) node_of_dof[(size_t)mesh->dof_of_node[v]] = v;
-    }
-    // neigh sets: subdomains (ascending) holding each dof; local copies in
-    // (subdomain, ascending dof) order for the weights.
-    std::vector<int64_t> sd_of_block((size_t)nb * nb * nb, -1);
-    for (int s = 0; s < part->n_sd; ++s) sd_of_block[(size_t)part->block_ids[s]] = s;
-    std::vector<uint8_t> nn_count((size_t)ndof, 0);
-    std::vector<int32_t> neigh8((size_t)ndof * 8, -1);
-    std::vector<int64_t> copy_off((size_t)part->n_sd + 1, 0);   // copies per subdomain
+    // local dofs of every subdomain (in parallel): nodes of its active
+    // cells, ascending global dof (mark the 8 nodes of every active cell,
+    // then scan the lattice; lexicographic slot order == ascending dof)
+    std::vector<int64_t> node_of_dof((size_t)ndof, -1);
     std::vector<std::vector<int32_t>> sd_dofs((size_t)part->n_sd);
-    for (int s = 0; s < part->n_sd; ++s) {
+    std::vector<std::vector<int64_t>> sd_nodes((size_t)part->n_sd);
+    const int b1 = B + 1;
+    parallel_for(part->n_sd, [&](int64_t s) {
+      std::vector<uint8_t> act((size_t)b1 * b1 * b1, 0);
       const int64_t b = part->block_ids[s];
       const int bi = (int)(b / nb / nb), bj = (int)((b / nb) % nb), bk = (int)(b % nb);
       auto& dl = sd_dofs[(size_t)s];
-      // local dofs: nodes of active cells of this block, ascending global dof
-      for (int li = 0; li <= B; ++li)
-        for (int lj = 0; lj <= B; ++lj)
-          for (int lk = 0; lk <= B; ++lk) {
-            const int gi = bi * B + li, gj = bj * B + lj, gk = bk * B + lk;
-            bool act = false;
-            for (int c = 0; c < 8 && !act; ++c) {
-              const int ci = li - 1 + (c & 1), cj = lj - 1 + ((c >> 1) & 1), ck = lk - 1 + ((c >> 2) & 1);
-              if (ci < 0 || cj < 0 || ck < 0 || ci >= B || cj >= B || ck >= B) continue;
-              act = mesh->cls[L.cell(bi * B + ci, bj * B + cj, bk * B + ck)] != CUTBDDC_EXTERIOR;
-            }
-            if (act) dl.push_back(mesh->dof_of_node[L.node(gi, gj, gk)]);
+      auto& nl = sd_nodes[(size_t)s];
+      for (int ci = 0; ci < B; ++ci)
+        for (int cj = 0; cj < B; ++cj) {
+          const uint8_t* row = mesh->cls + L.cell(bi * B + ci, bj * B + cj, bk * B);
+          for (int ck = 0; ck < B; ++ck) {
+            if (row[ck] == CUTBDDC_EXTERIOR) continue;
+            uint8_t* a = act.data() + ((size_t)ci * b1 + cj) * b1 + ck;
+            a[0] = a[1] = a[b1] = a[b1 + 1] = 1;
+            a[b1 * b1] = a[b1 * b1 + 1] = a[b1 * b1 + b1] = a[b1 * b1 + b1 + 1] = 1;
           }
-      // lexicographic slot order == ascending global dof (z fastest on both)
-      for (int32_t d : dl) {
+        }
+      for (int li = 0; li <= B; ++li)
+        for (int lj = 0; lj <= B; ++lj) {
+          const uint8_t* a = act.data() + ((size_t)li * b1 + lj) * b1;
+          const int64_t v0 = L.node(bi * B + li, bj * B + lj, bk * B);
+          for (int lk = 0; lk <= B; ++lk)
+            if (a[lk]) {
+              const int32_t d = mesh->dof_of_node[v0 + lk];
+              if (d < 0 || d >= ndof) throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: active node without a dof");
+              dl.push_back(d);
+              nl.push_back(v0 + lk);
+            }
+        }
+    });
+    // neigh sets: subdomains (ascending) holding each dof; local copies in
+    // (subdomain, ascending dof) order for the weights.
+    std::vector<uint8_t> nn_count((size_t)ndof, 0);
+    std::vector<int32_t> neigh8((size_t)ndof * 8, -1);
+    std::vector<int64_t> copy_off((size_t)part->n_sd + 1, 0);   // copies per subdomain
+    for (int s = 0; s < part->n_sd; ++s) {
+      const auto& dl = sd_dofs[(size_t)s];
+      for (size_t q = 0; q < dl.size(); ++q) {
+        const int32_t d = dl[q];
+        node_of_dof[(size_t)d] = sd_nodes[(size_t)s][q];
         const uint8_t k = nn_count[(size_t)d]++;
         if (k >= 8) throw Failure(CUTBDDC_INTERNAL, "partition: node in more than 8 subdomains");
         neigh8[(size_t)d * 8 + k] = s;
       }
-      copy_off[(size_t)s + 1] = copy_off[(size_t)s] + (int64_t)dl.size();
+      copy_off[(size_t)s + 1] = copy_off[(size_t)s] + (int64_t)sd_dofs[(size_t)s].size();
     }
-    // group interface dofs by exact neigh set
-    std::unordered_map<std::vector<int32_t>, int, VecHash> group_of;
-    std::vector<std::vector<int32_t>> group_dofs, group_key;
+    // group interface dofs by exact neigh set (hash-sorted; objects are
+    // ordered by their smallest dof below, so group order does not matter)
+    auto same_key = [&](int32_t a, int32_t b) {
+      const int k = nn_count[(size_t)a];
+      return nn_count[(size_t)b] == k &&
+             std::memcmp(&neigh8[(size_t)a * 8], &neigh8[(size_t)b * 8], sizeof(int32_t) * (size_t)k) == 0;
+    };
+    std::vector<std::pair<uint64_t, int32_t>> hk;  // (hash of the neigh set, dof)
     for (int64_t d = 0; d < ndof; ++d) {
       const int k = nn_count[(size_t)d];
       if (k < 2 || (dirichlet && dirichlet[d])) continue;
-      std::vector<int32_t> key(neigh8.begin() + d * 8, neigh8.begin() + d * 8 + k);
-      auto it = group_of.find(key);
-      int g;
-      if (it == group_of.end()) {
-        g = (int)group_dofs.size();
-        group_of.emplace(key, g);
-        group_dofs.emplace_back();
-        group_key.push_back(key);
-      } else {
-        g = it->second;
-      }
-      group_dofs[(size_t)g].push_back((int32_t)d);
+      uint64_t h = 1469598103934665603ull ^ (uint64_t)k;
+      for (int q = 0; q < k; ++q) h = (h ^ (uint64_t)(uint32_t)neigh8[(size_t)d * 8 + q]) * 1099511628211ull;
+      hk.emplace_back(h, (int32_t)d);
     }
+    std::sort(hk.begin(), hk.end());
+    std::vector<std::vector<int32_t>> group_dofs, group_key;
+    for (size_t q0 = 0; q0 < hk.size();) {
+      size_t q1 = q0 + 1;
+      while (q1 < hk.size() && hk[q1].first == hk[q0].first) ++q1;
+      // one hash run: split by exact key (a collision yields several groups)
+      const size_t g0 = group_dofs.size();
+      for (size_t q = q0; q < q1; ++q) {
+        const int32_t d = hk[q].second;
+        size_t g = g0;
+        while (g < group_dofs.size() && !same_key(group_dofs[g][0], d)) ++g;
+        if (g == group_dofs.size()) {
+          group_dofs.emplace_back();
+          group_key.emplace_back(neigh8.begin() + (int64_t)d * 8, neigh8.begin() + (int64_t)d * 8 + nn_count[(size_t)d]);
+        }
+        group_dofs[g].push_back(d);  // ascending dof within a group
+      }
+      q0 = q1;
+    }
+    std::vector<std::vector<std::vector<int32_t>>> gcomp(group_dofs.size());
+    parallel_for((int64_t)group_dofs.size(), [&](int64_t g) {
+      gcomp[(size_t)g] = components(L, node_of_dof, group_dofs[(size_t)g], [](int32_t, int32_t) { return true; });
+    });
     std::vector<Obj> objs;
     for (size_t g = 0; g < group_dofs.size(); ++g) {
-      for (auto& comp : components(L, node_of_dof, group_dofs[g], [](int32_t, int32_t) { return true; })) {
+      for (auto& comp : gcomp[g]) {
         Obj o;
         o.kind = comp.size() == 1 ? CUTBDDC_CORNER : (group_key[g].size() == 2 ? CUTBDDC_FACE : CUTBDDC_EDGE);
         o.dofs = std::move(comp);

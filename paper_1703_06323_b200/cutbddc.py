@@ -74,7 +74,7 @@ EXPORTS = [
     "cutbddc_gpu_local_diagonals", "cutbddc_gpu_setup_bddc", "cutbddc_gpu_pcg", "cutbddc_gpu_spmv",
     "cutbddc_gpu_apply_bddc", "cutbddc_gpu_rhs", "cutbddc_gpu_coarse_matrix", "cutbddc_gpu_cells", "cutbddc_gpu_stats",
     "cutbddc_gpu_cut_elements", "cutbddc_gpu_local_system", "cutbddc_gpu_local_solve", "cutbddc_gpu_time_solves",
-    "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free",
+    "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free", "cutbddc_gpu_classify_objects",
     "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_global_ids",
 ]
 
@@ -168,6 +168,11 @@ def classify_objects(mesh: Mesh, block: int, block_ids: np.ndarray, dirichlet: n
     diag_p = _p(local_diag, C.c_double) if local_diag is not None else None
     dir_p = _p(dirichlet, C.c_uint8) if dirichlet is not None else None
     _check(lib().cutbddc_classify_objects(C.byref(v), C.byref(pv), dir_p, objects, variant, diag_p, C.byref(out)))
+    return _take_objects(out)
+
+
+def _take_objects(out) -> Objects:
+    """Copy a library-owned cutbddc_objects into numpy arrays and free it."""
     o = out.contents
     no = o.n_objects
     kinds = np.ctypeslib.as_array(o.kinds, (no,)).copy() if no else np.zeros(0, np.int32)
@@ -258,6 +263,13 @@ class GpuSolver:
         _check(lib().cutbddc_gpu_assemble(self.h, C.byref(mv) if mv is not None else None, C.byref(pv),
                                           _p(dirichlet, C.c_uint8)))
         return dirichlet
+
+    def classify_objects(self, objects: int, variant: int = 0) -> Objects:
+        """classify_objects on the device from the assembled mesh (standard
+        variant; bit-identical to the host classify_objects)."""
+        out = C.POINTER(_Objects)()
+        _check(lib().cutbddc_gpu_classify_objects(self.h, objects, variant, C.byref(out)))
+        return _take_objects(out)
 
     def local_diagonals(self) -> np.ndarray:
         n = C.c_int64()

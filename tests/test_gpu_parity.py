@@ -211,3 +211,24 @@ def test_cut_element_matrices_match_oracle(cfg2s):
         scale = max(np.abs(k_o).max(), 1e-300)
         assert np.abs(ke[q] - k_o).max() <= 1e-13 * scale, int(cells[q])
         assert np.abs(fe[q] - f_o).max() <= 1e-13 * max(np.abs(f_o).max(), 1e-300), int(cells[q])
+
+
+def _objects_equal(a, b):
+    return (np.array_equal(a.kinds, b.kinds) and np.array_equal(a.dof_ptr, b.dof_ptr) and
+            np.array_equal(a.dofs, b.dofs) and np.array_equal(a.neigh_ptr, b.neigh_ptr) and
+            np.array_equal(a.neigh, b.neigh))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_device_objects_bit_exact_vs_host(name):
+    """classify_objects on the device (objects.cu) against the host
+    restatement (host_partition.cpp), every object level: identical kinds,
+    dofs, neighbour lists and order."""
+    cfg = configs.get(name)
+    s = cb.GpuSolver(0)
+    pb = cb.prepare(s, cfg)
+    for level in (configs.OBJ_C, configs.OBJ_CE, configs.OBJ_CEF):
+        host = cb.classify_objects(pb.mesh, cfg.block, pb.block_ids, pb.dirichlet, level, 0, None)
+        dev = s.classify_objects(level, 0)
+        assert len(dev) == len(host) and _objects_equal(dev, host), (name, level)
+    s.close()
