@@ -232,3 +232,26 @@ def test_device_objects_bit_exact_vs_host(name):
         dev = s.classify_objects(level, 0)
         assert len(dev) == len(host) and _objects_equal(dev, host), (name, level)
     s.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_cut_elements_warp_form_bit_exact(name):
+    """The warp-per-cell cut-element kernel reproduces the thread-per-cell
+    form (the sequential arithmetic of the oracle) bit for bit: element
+    matrices, load vectors, beta_e and the empty flags of every cut cell."""
+    cfg = configs.get(name)
+    s = cb.GpuSolver(0)
+    pb = cb.prepare(s, cfg)
+    cells, ke, fe = s.cut_elements()
+    beta, empty = s.cells()
+    os.environ["CUTBDDC_CUT_THREAD"] = "1"
+    try:
+        s.assemble(cfg.block, pb.block_ids)
+        cells2, ke2, fe2 = s.cut_elements()
+        beta2, empty2 = s.cells()
+    finally:
+        del os.environ["CUTBDDC_CUT_THREAD"]
+    assert np.array_equal(cells, cells2)
+    assert np.array_equal(ke, ke2) and np.array_equal(fe, fe2)
+    assert np.array_equal(beta, beta2) and np.array_equal(empty, empty2)
+    s.close()
