@@ -241,6 +241,12 @@ def main():
             "frac": achieved / hbm, "traffic": None, "bytes_per_launch": rf["bytes"],
             "launch_ms": 1e3 * rf["seconds"], "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"
             if peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+    # roofline.traffic: DRAM bytes of the same 7 sweep launches of one apply
+    # from the committed ncu --set full capture (tools/ncu_traffic.py)
+    tj = os.path.join(ROOT, "profiles", "r01_sweep_traffic_cfg4.json")
+    if os.path.exists(tj) and world == 1 and cfg.name == "cfg4" and cfg.cells == 64:
+        roof["traffic"] = json.load(open(tj))["traffic_bytes_per_apply"]
+        roof["traffic_source"] = "profiles/r01_sweep_traffic_cfg4.json (ncu --set full, dram read+write)"
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
