@@ -109,52 +109,62 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// 8-byte cp.async (LDGSTS) global -> shared; src-size 0 zero-fills
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // The dense trailing updates on the DMMA tensor cores: 8 warps, each owns a
-// 16 x 32 block of the 64 x 64 output (2 x 4 mma tiles); k staged through
-// shared memory 32 at a time (rows padded to 65 doubles: conflict-free
-// fragment loads).
+// 16 x 32 block of the 64 x 64 output (2 x 4 mma tiles). The whole 64-deep A
+// and B tiles go to shared memory by cp.async (every load in flight at once,
+// no register staging; rows padded to 65 doubles: conflict-free fragment
+// loads) while the accumulators are loaded from C (acc: C never aliases A or
+// B then); alpha = -1 negates the A fragments, so D = C + alpha A op(B).
 __device__ void tile_mm(double* C, int ldc, const double* A, int lda, const double* B, int ldb, int m, int n, int kk,
                         double alpha, bool acc, bool bt, bool lower, double* sm) {
   double(*as)[kTile + 1] = reinterpret_cast<double(*)[kTile + 1]>(sm);
-  double(*bs)[kTile + 1] = reinterpret_cast<double(*)[kTile + 1]>(sm + 32 * (kTile + 1));
+  double(*bs)[kTile + 1] = reinterpret_cast<double(*)[kTile + 1]>(sm + kTile * (kTile + 1));
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int wr = (wid & 3) * 16, wc = (wid >> 2) * 32;  // warp's output block origin
   const int fr = lane >> 2, fk = lane & 3;               // fragment row/col and k index
-  double d[2][4][2];
+  const double sa = alpha < 0.0 ? -1.0 : 1.0;           // alpha is +-1 at every call site
+  // kk <= kTile: every tile of a front is at most 64 x 64
+  __syncthreads();  // previous users of the staging buffers are done
+  for (int e = tid; e < kTile * kTile; e += kDagThreads) {
+    const int row = e & 63, k = e >> 6;
+    const bool v = row < m && k < kk;
+    cp_async8(&as[k][row], A + (v ? row + (int64_t)k * lda : 0), v);
+  }
+  for (int e = tid; e < kTile * kTile; e += kDagThreads) {
+    const int lo = e & 63, hi = e >> 6;  // bt: (col, k); else (k, col): coalesced either way
+    const int col = bt ? lo : hi, k = bt ? hi : lo;
+    const bool v = col < n && k < kk;
+    cp_async8(&bs[k][col], B + (v ? (bt ? col + (int64_t)k * ldb : k + (int64_t)col * ldb) : 0), v);
+  }
+  double d[2][4][2];  // accumulators from C while the tiles are in flight
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
-  for (int k0 = 0; k0 < kk; k0 += 32) {
-    __syncthreads();
-    for (int e = tid; e < 32 * kTile; e += kDagThreads) {
-      const int row = e & 63, k = e >> 6;
-      as[k][row] = (row < m && k0 + k < kk) ? A[row + (int64_t)(k0 + k) * lda] : 0.0;
-    }
-    if (bt) {
-      for (int e = tid; e < 32 * kTile; e += kDagThreads) {
-        const int col = e & 63, k = e >> 6;
-        bs[k][col] = (col < n && k0 + k < kk) ? B[col + (int64_t)(k0 + k) * ldb] : 0.0;
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int i = wr + 8 * a + fr, j = wc + 8 * b + 2 * fk + h2;
+        d[a][b][h2] = (acc && i < m && j < n) ? C[i + (int64_t)j * ldc] : 0.0;
       }
-    } else {
-      for (int e = tid; e < 32 * kTile; e += kDagThreads) {
-        const int k = e & 31, col = e >> 5;
-        bs[k][col] = (col < n && k0 + k < kk) ? B[(k0 + k) + (int64_t)col * ldb] : 0.0;
-      }
-    }
-    __syncthreads();
+  cp_async_wait_all();
+  __syncthreads();
+  for (int k = 0; k < kk; k += 4) {
+    double fa[2], fb[4];
 #pragma unroll
-    for (int k = 0; k < 32; k += 4) {
-      double fa[2], fb[4];
+    for (int a = 0; a < 2; ++a) fa[a] = sa * as[k + fk][wr + 8 * a + fr];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) fa[a] = as[k + fk][wr + 8 * a + fr];
+    for (int b = 0; b < 4; ++b) fb[b] = bs[k + fk][wc + 8 * b + fr];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) fb[b] = bs[k + fk][wc + 8 * b + fr];
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma_8x8x4(d[a][b][0], d[a][b][1], fa[a], fb[b]);
-    }
+      for (int b = 0; b < 4; ++b) dmma_8x8x4(d[a][b][0], d[a][b][1], fa[a], fb[b]);
   }
   __syncthreads();  // A / B (possibly C itself) fully consumed
 #pragma unroll
@@ -165,8 +175,7 @@ __device__ void tile_mm(double* C, int ldc, const double* A, int lda, const doub
       for (int h2 = 0; h2 < 2; ++h2) {
         const int i = wr + 8 * a + fr, j = wc + 8 * b + 2 * fk + h2;
         if (i >= m || j >= n || (lower && i < j)) continue;
-        double* cp = C + i + (int64_t)j * ldc;
-        *cp = (acc ? *cp : 0.0) + alpha * d[a][b][h2];
+        C[i + (int64_t)j * ldc] = d[a][b][h2];
       }
 }
 

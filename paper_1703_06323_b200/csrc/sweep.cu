@@ -25,6 +25,7 @@
 // descriptor, b or y at its columns, the first panel columns) is loaded
 // before it waits, so the wait hides that latency. Every sum has a fixed
 // order: the sweeps are deterministic.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -181,19 +182,37 @@ __device__ __forceinline__ void wait_children(const SweepDev& p, const FrontDesc
   if (d.nch > 1) cta_wait(p, p.done_f + d.cfs1, d.cnf1);
 }
 
+// nw consecutive warps w0 .. w0 + nw - 1 of the CTA working on one front;
+// named barrier `bar` (the whole CTA: __syncthreads). T items run the
+// independent fronts of one subtree level side by side, one group each.
+struct Grp {
+  int w0, nw, bar;
+  __device__ __forceinline__ int lt() const { return (int)threadIdx.x - 32 * w0; }
+  __device__ __forceinline__ int nt() const { return 32 * nw; }
+  __device__ __forceinline__ void sync() const {
+    if (nw == kWarps)
+      __syncthreads();
+    else if (nw == 1)
+      __syncwarp();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * nw) : "memory");
+  }
+};
+__device__ __forceinline__ Grp whole_cta() { return Grp{0, kWarps, 0}; }
+
 // Forward GEMV o[i] = sum_j G[i + j r] v[j] for rows [i0, i1) (at most 32 R)
-// and columns [jlo, jhi): warps split the columns, each lane accumulates its
-// R rows in registers (coalesced 256-B column segments, R loads in flight per
-// column), the warp partials are summed in warp order (deterministic).
-// Row blocks entirely above column j are skipped (zero part of L11^{-1}).
-// The first column of every warp is loaded before `between()` (which
-// completes v: dependency wait + children's updates).
+// and columns [jlo, jhi): the group's warps split the columns, each lane
+// accumulates its R rows in registers (coalesced 256-B column segments, R
+// loads in flight per column), the warp partials are summed in warp order
+// (deterministic). Row blocks entirely above column j are skipped (zero part
+// of L11^{-1}). The first column of every warp is loaded before `between()`
+// (which completes v: dependency wait + children's updates).
 template <int R, int U, typename Between, typename Out>
-__device__ __forceinline__ void cta_gemv_fwd(const double* __restrict__ G, int r, int jlo, int jhi, int i0, int i1,
-                                             double* v, double* part, Between between, Out out) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int cw = (jhi - jlo + kWarps - 1) / kWarps;
-  const int ja = min(jhi, jlo + wid * cw), jb = min(jhi, ja + cw);
+__device__ __forceinline__ void grp_gemv_fwd(const Grp& g, const double* __restrict__ G, int r, int jlo, int jhi, int i0,
+                                             int i1, double* v, double* part, Between between, Out out) {
+  const int lt = g.lt(), lane = threadIdx.x & 31, lw = lt >> 5;
+  const int cw = (jhi - jlo + g.nw - 1) / g.nw;
+  const int ja = min(jhi, jlo + lw * cw), jb = min(jhi, ja + cw);
   const double* gl = G + i0 + lane;
   double acc[R];
 #pragma unroll
@@ -213,35 +232,37 @@ __device__ __forceinline__ void cta_gemv_fwd(const double* __restrict__ G, int r
     for (int k = 0; k < R; ++k)
       if (i0 + 32 * k + 31 >= j && i0 + 32 * k + lane < i1) acc[k] += gj[32 * k] * vj;
   }
+  double* pw = part + (int64_t)g.w0 * 32 * R;
 #pragma unroll
-  for (int k = 0; k < R; ++k) part[wid * 32 * R + 32 * k + lane] = acc[k];
-  __syncthreads();
-  for (int q = tid; q < i1 - i0; q += kThreadsSweep) {
+  for (int k = 0; k < R; ++k) pw[lw * 32 * R + 32 * k + lane] = acc[k];
+  g.sync();
+  for (int q = lt; q < i1 - i0; q += g.nt()) {
     double o = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) o += part[w * 32 * R + q];
+    for (int w = 0; w < g.nw; ++w) o += pw[w * 32 * R + q];
     out(i0 + q, o);
   }
-  __syncthreads();
+  g.sync();
 }
 
-// Forward of one front (r <= kSmallRows) by the whole CTA. `wait` = the
-// children belong to other items (wait for them, read their updates from L2).
-__device__ void cta_front_fwd(const SweepDev& p, const FrontDesc& d, const double* __restrict__ panel,
-                              const double* __restrict__ X, double* ysave, double* upd, double* v, bool wait) {
+// Forward of one front (r <= kSmallRows) by a warp group. `wait` (whole CTA
+// only) = the children belong to other items (wait for them, read their
+// updates from L2); otherwise they were produced earlier in this CTA.
+__device__ void grp_front_fwd(const Grp& g, const SweepDev& p, const FrontDesc& d, const double* __restrict__ panel,
+                              const double* __restrict__ X, double* ysave, double* upd, double* v, double* part,
+                              bool wait) {
   const int r = d.r, c = d.c;
   if (r == 0) return;
-  const int tid = threadIdx.x;
+  const int lt = g.lt(), nt = g.nt();
   const int32_t* cs = p.cslot + d.vo;
-  for (int q = tid; q < r; q += kThreadsSweep) v[q] = q < c ? X[cs[q]] : 0.0;
+  for (int q = lt; q < r; q += nt) v[q] = q < c ? X[cs[q]] : 0.0;
   double* uo = upd + d.uo;
-  cta_gemv_fwd<kSmallRows / 32, 2>(
-      panel + d.po, r, 0, c, 0, r, v, v + kVecDoubles,
+  grp_gemv_fwd<kSmallRows / 32, 2>(
+      g, panel + d.po, r, 0, c, 0, r, v, part,
       [&] {
         if (wait) wait_children(p, d);
-        __syncthreads();
-        for (int q = tid; q < r; q += kThreadsSweep) v[q] = child_sum(p, d, upd, q, v[q], wait);
-        __syncthreads();
+        g.sync();
+        for (int q = lt; q < r; q += nt) v[q] = child_sum(p, d, upd, q, v[q], wait);
+        g.sync();
       },
       [&](int i, double o) {
         if (i < c)
@@ -251,30 +272,31 @@ __device__ void cta_front_fwd(const SweepDev& p, const FrontDesc& d, const doubl
       });
 }
 
-// Backward of one front (r <= kSmallRows) by the whole CTA: rows split over
+// Backward of one front (r <= kSmallRows) by a warp group: rows split over
 // the warps, 16 columns at a time accumulated in registers, reduce-scattered
 // in each warp and the warp partials summed in order. The first row of each
-// lane (first column block) and y at the columns are loaded before the wait.
-__device__ void cta_front_bwd(const SweepDev& p, const FrontDesc& d, const double* __restrict__ panel, double* X,
-                              const double* __restrict__ ysave, double* w, double (*part)[33], bool wait) {
+// lane (first column block) and y at the columns are loaded before the wait
+// (whole CTA only).
+__device__ void grp_front_bwd(const Grp& g, const SweepDev& p, const FrontDesc& d, const double* __restrict__ panel,
+                              double* X, const double* __restrict__ ysave, double* w, double (*part)[33], bool wait) {
   const int r = d.r, c = d.c;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int lt = g.lt(), nt = g.nt(), lane = threadIdx.x & 31, lw = lt >> 5;
   if (c == 0) {
     if (wait && d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
     return;
   }
   const int32_t* cs = p.cslot + d.vo;
-  for (int q = tid; q < c; q += kThreadsSweep) w[q] = ysave[cs[q]];
+  for (int q = lt; q < c; q += nt) w[q] = ysave[cs[q]];
   const double* G = panel + d.po;
-  const int rw = (r + kWarps - 1) / kWarps;
-  const int ra = wid * rw, rb = min(r, ra + rw);
+  const int rw = (r + g.nw - 1) / g.nw;
+  const int ra = lw * rw, rb = min(r, ra + rw);
   const int i_first = ra + lane;
   double acc[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = (i_first < rb && k < c) ? G[i_first + (int64_t)k * r] : 0.0;
   if (wait && d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
-  for (int q = c + tid; q < r; q += kThreadsSweep) w[q] = -__ldcg(X + cs[q]);
-  __syncthreads();
+  for (int q = c + lt; q < r; q += nt) w[q] = -__ldcg(X + cs[q]);
+  g.sync();
   for (int jb = 0; jb < c; jb += 16) {
     int i = max(ra, jb) + lane;
     if (jb == 0) {
@@ -293,13 +315,29 @@ __device__ void cta_front_bwd(const SweepDev& p, const FrontDesc& d, const doubl
       for (int k = 0; k < 16; ++k)
         if (jb + k < c) acc[k] += gi[(int64_t)k * r] * wi;
     }
-    part[wid][lane] = reduce_scatter16(acc, lane);
-    __syncthreads();
-    if (wid == 0 && lane < 16 && jb + lane < c) {
+    part[g.w0 + lw][lane] = reduce_scatter16(acc, lane);
+    g.sync();
+    if (lw == 0 && lane < 16 && jb + lane < c) {
       double x = 0.0;
-      for (int q = 0; q < kWarps; ++q) x += part[q][lane];
+      for (int q = 0; q < g.nw; ++q) x += part[g.w0 + q][lane];
       X[cs[jb + lane]] = x;
     }
+    g.sync();
+  }
+}
+
+// One level of a T item: its nf independent fronts (sids[k0 .. k0 + nf))
+// side by side, kWarps / 2^ceil(log2 nf) warps each (rounds of kWarps
+// fronts), each with its own kSmallRows slice of the vector buffer.
+template <typename Fn>
+__device__ __forceinline__ void subtree_level(int k0, int k1, Fn fn) {
+  const int wid = threadIdx.x >> 5;
+  for (int base = k0; base < k1; base += kWarps) {
+    const int n = min(kWarps, k1 - base);
+    int wpf = kWarps;
+    while (wpf > 1 && wpf * n > kWarps) wpf >>= 1;
+    const int f = wid / wpf;
+    if (f < n) fn(Grp{f * wpf, wpf, 1 + f}, base + f, f);
     __syncthreads();
   }
 }
@@ -321,16 +359,17 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
       // bottom subtree of sid: its fronts deepest level first, one after another
       const int32_t* meta = p.sub_meta + chunk;
       const int ng = meta[0];
-      for (int k = meta[1]; k < meta[1 + ng]; ++k) {
-        const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
-        cta_front_fwd(p, d, panel, X, ysave, upd, v, false);
-      }
+      for (int gi = 0; gi < ng; ++gi)  // deepest level first
+        subtree_level(meta[1 + gi], meta[2 + gi], [&](const Grp& g, int k, int f) {
+          const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
+          grp_front_fwd(g, p, d, panel, X, ysave, upd, v + f * kSmallRows, v + kVecDoubles, false);
+        });
       cta_signal(p.done_f + fs);
       continue;
     }
     const FrontDesc d = load_desc(p.desc + fs);
     if (kind == kItemS) {
-      cta_front_fwd(p, d, panel, X, ysave, upd, v, true);
+      grp_front_fwd(whole_cta(), p, d, panel, X, ysave, upd, v, v + kVecDoubles, true);
       cta_signal(p.done_f + fs);
       continue;
     }
@@ -347,8 +386,8 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
     const int jlo = cb * kFwdCols, jhi = min(jrow, jlo + kFwdCols);
     double* tp = p.vbuf + d.tpo + (int64_t)rb * mcb * kFwdRows;
     for (int q = jlo + tid; q < jhi; q += kThreadsSweep) v[q] = X[cs[q]];
-    cta_gemv_fwd<kFwdRows / 32, 4>(
-        panel + d.po, r, jlo, jhi, i0, i1, v, v + kVecDoubles,
+    grp_gemv_fwd<kFwdRows / 32, 4>(
+        whole_cta(), panel + d.po, r, jlo, jhi, i0, i1, v, v + kVecDoubles,
         [&] {
           wait_children(p, d);
           __syncthreads();
@@ -399,15 +438,16 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDe
       // only its root depends on other items (its parent)
       const int32_t* meta = p.sub_meta + chunk;
       const int ng = meta[0];
-      for (int k = meta[1 + ng] - 1; k >= meta[1]; --k) {
-        const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
-        cta_front_bwd(p, d, panel, X, ysave, w, part, k == meta[1 + ng] - 1);
-      }
+      for (int gi = ng - 1; gi >= 0; --gi)  // shallowest level (the subtree root, one front) first
+        subtree_level(meta[1 + gi], meta[2 + gi], [&](const Grp& g, int k, int f) {
+          const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
+          grp_front_bwd(g, p, d, panel, X, ysave, w + f * kSmallRows, part, k == meta[1 + ng] - 1);
+        });
       continue;  // nothing outside the subtree waits on it
     }
     const FrontDesc d = load_desc(p.desc + fs);
     if (kind == kItemS) {
-      cta_front_bwd(p, d, panel, X, ysave, w, part, true);
+      grp_front_bwd(whole_cta(), p, d, panel, X, ysave, w, part, true);
       cta_signal(p.done_b + fs);
       continue;
     }
@@ -687,6 +727,71 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
     if (L == 0) f.n_items_b_root = (int)bw.size();
   }
   subtree_items(bw);
+  // Critical path first: every item's ticket follows the longest remaining
+  // path (estimated work) to the end of its sweep, as in the factorisation's
+  // DAG. Weights are positive, so a front's items always rank after those of
+  // its children (forward) / its parent (backward): still a topological
+  // order. Ties keep the level order (stable sort).
+  {
+    constexpr double kItemCost = 4096.0;  // per-item latency in panel entries
+    const size_t nf_all = (size_t)nsd * nsn;
+    auto rc = [&](int sd, int sid) { return f.h_rc[(size_t)sd * nsn + sid]; };
+    auto entries = [](int2 v) { return (double)v.x * v.y; };
+    auto t_work = [&](int sd, int root) {  // a T item: every front of the subtree, one CTA
+      double w = 0.0;
+      const int32_t* m = meta.data() + meta_of[(size_t)root];
+      for (int k = m[1]; k < m[1 + m[0]]; ++k) w += kItemCost + entries(rc(sd, sids[(size_t)k]));
+      return w;
+    };
+    auto fwd_item = [&](int sd, int sid) {  // work of one item of a non-subtree front
+      const int2 v = rc(sd, sid);
+      return kItemCost + (is_small(v) ? entries(v) : (double)std::min(v.x, kFwdRows) * std::min(v.y, kFwdCols));
+    };
+    auto bwd_item = [&](int sd, int sid) {
+      const int2 v = rc(sd, sid);
+      return kItemCost + (is_small(v) || v.y == 0 ? entries(v) : (double)v.x * std::min(v.y, kBwdCols));
+    };
+    // forward: remaining path from a front to the root (top-down over levels)
+    std::vector<double> remf(nf_all, 0.0), remb(nf_all, 0.0);
+    for (int L = 0; L < nlev; ++L)
+      for (int sid : lv[(size_t)L])
+        for (int sd = 0; sd < nsd; ++sd) {
+          const int par = tp.sn[(size_t)sid].parent;
+          const double up = par >= 0 ? remf[(size_t)sd * nsn + par] : 0.0;
+          remf[(size_t)sd * nsn + sid] = up + (in_sub[(size_t)sid] ? 0.0 : fwd_item(sd, sid));
+        }
+    // backward: remaining path from a front down to its deepest descendant
+    for (int L = nlev - 1; L >= 0; --L)
+      for (int sid : lv[(size_t)L])
+        for (int sd = 0; sd < nsd; ++sd) {
+          const Supernode& sn = tp.sn[(size_t)sid];
+          double down = 0.0;
+          for (int ch = 0; ch < sn.nchild; ++ch) down = std::max(down, remb[(size_t)sd * nsn + sn.child[ch]]);
+          remb[(size_t)sd * nsn + sid] =
+              down + (in_sub[(size_t)sid] ? (meta_of[(size_t)sid] >= 0 ? t_work(sd, sid) : 0.0) : bwd_item(sd, sid));
+        }
+    auto key = [&](const int4& it, bool fwd) {
+      const size_t i = (size_t)it.z * nsn + it.y;
+      if (fwd) {
+        if (it.x == kItemT) {
+          const int par = tp.sn[(size_t)it.y].parent;
+          return t_work(it.z, it.y) + (par >= 0 ? remf[(size_t)it.z * nsn + par] : 0.0);
+        }
+        return remf[i];
+      }
+      return remb[i];
+    };
+    auto order = [&](std::vector<int4>& v, size_t b, size_t e, bool fwd) {
+      std::vector<std::pair<double, int4>> kv;
+      for (size_t q = b; q < e; ++q) kv.emplace_back(key(v[q], fwd), v[q]);
+      std::stable_sort(kv.begin(), kv.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      for (size_t q = b; q < e; ++q) v[q] = kv[q - b].second;
+    };
+    order(fw, 0, fw.size(), true);
+    const size_t nroot = std::min(bw.size(), (size_t)std::max(0, f.n_items_b_root));
+    order(bw, 0, nroot, false);  // the root phase stays a launch of its own
+    order(bw, nroot, bw.size(), false);
+  }
   f.n_items_f = (int)fw.size();
   f.n_items_b = (int)bw.size();
   if (fw.empty()) fw.push_back(make_int4(0, 0, 0, 0));
