@@ -587,6 +587,93 @@ __global__ void k_root_correct(const int64_t* __restrict__ rinfo, const int64_t*
   X[cslot[rinfo[4 * sd + 2] + j]] += s;
 }
 
+// The apply's coarse problem on one GPU, two launches instead of six (same
+// summation orders as k_cy / k_sinv_apply / k_coarse_rhs / k_coarse_gemv /
+// k_root_correct). k_coarse_in, one block per subdomain: cy = C y (warp per
+// constraint row), gl = S^{-1} cy.
+constexpr int kFusedCoarseM = 256;  // constraint rows per subdomain of the fused path
+__global__ void __launch_bounds__(256) k_coarse_in(int T, const int64_t* __restrict__ m_off,
+                                                   const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_slot,
+                                                   const double* __restrict__ c_val, const double* __restrict__ Y,
+                                                   const int64_t* __restrict__ s_off, const double* __restrict__ sinv,
+                                                   double* __restrict__ cy, double* __restrict__ gl,
+                                                   const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double scy[kFusedCoarseM];
+  const int sd = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t b0 = m_off[sd];
+  const int m = (int)(m_off[sd + 1] - b0);
+  const double* y = Y + (int64_t)sd * T;
+  for (int a = wid; a < m; a += blockDim.x >> 5) {
+    const int64_t row = b0 + a;
+    double v = 0.0;
+    for (int64_t p = c_ptr[row] + lane; p < c_ptr[row + 1]; p += 32) v += c_val[p] * y[c_slot[p]];
+    v = warp_sum(v);
+    if (lane == 0) scy[a] = cy[row] = v;
+  }
+  __syncthreads();
+  for (int a = tid; a < m; a += blockDim.x) {
+    const double* si = sinv + s_off[sd] + (int64_t)a * m;
+    double v = 0.0;
+    for (int b = 0; b < m; ++b) v += si[b] * scy[b];
+    gl[b0 + a] = v;
+  }
+}
+
+// k_coarse_out, blocks (subdomain, root column chunk): gc = sum of the gl
+// copies (every block, in k_coarse_rhs order), zc at the subdomain's coarse
+// dofs (warp per row of A_c^{-1}), u = S^{-1}(zc - cy), then the root
+// correction X[root columns] += W_r u of the block's columns.
+__global__ void __launch_bounds__(256) k_coarse_out(int nc, const int64_t* __restrict__ cg_ptr,
+                                                    const int64_t* __restrict__ cg_idx, const double* __restrict__ gl,
+                                                    const double* __restrict__ Ainv, const int32_t* __restrict__ coarse_id,
+                                                    const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
+                                                    const double* __restrict__ sinv, const double* __restrict__ cy,
+                                                    const int64_t* __restrict__ rinfo, const int32_t* __restrict__ cslot,
+                                                    const double* __restrict__ W, double* __restrict__ X,
+                                                    const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double gc[];  // nc, then zc and u (kFusedCoarseM each)
+  double* zl = gc + nc;
+  double* u = zl + kFusedCoarseM;
+  const int sd = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int lam = tid; lam < nc; lam += blockDim.x) {
+    double v = 0.0;
+    for (int64_t p = cg_ptr[lam]; p < cg_ptr[lam + 1]; ++p) v += gl[cg_idx[p]];
+    gc[lam] = v;
+  }
+  __syncthreads();
+  const int64_t b0 = m_off[sd];
+  const int m = (int)(m_off[sd + 1] - b0);
+  for (int a = wid; a < m; a += blockDim.x >> 5) {
+    const double* ar = Ainv + (int64_t)coarse_id[b0 + a] * nc;
+    double s0 = 0.0, s1 = 0.0;
+    int c = lane;
+    for (; c + 32 < nc; c += 64) {
+      s0 += ar[c] * gc[c];
+      s1 += ar[c + 32] * gc[c + 32];
+    }
+    for (; c < nc; c += 32) s0 += ar[c] * gc[c];
+    const double v = warp_sum(s0 + s1);
+    if (lane == 0) zl[a] = v;
+  }
+  __syncthreads();
+  for (int a = tid; a < m; a += blockDim.x) {
+    const double* si = sinv + s_off[sd] + (int64_t)a * m;
+    double v = 0.0;
+    for (int b = 0; b < m; ++b) v += si[b] * (zl[b] - cy[b0 + b]);
+    u[a] = v;
+  }
+  __syncthreads();
+  const int cr = (int)rinfo[4 * sd];
+  const int j = blockIdx.y * blockDim.x + tid;
+  if (j >= cr) return;
+  const double* w = W + rinfo[4 * sd + 3] + j;
+  double v = 0.0;
+  for (int a = 0; a < m; ++a) v += w[(int64_t)a * cr] * u[a];
+  X[cslot[rinfo[4 * sd + 2] + j]] += v;
+}
+
 __global__ void k_row_sd(int nsd, const int64_t* __restrict__ m_off, int32_t* __restrict__ row_sd) {
   const int sd = blockIdx.x;
   for (int64_t r = m_off[sd] + threadIdx.x; r < m_off[sd + 1]; r += blockDim.x) row_sd[r] = sd;
@@ -872,36 +959,52 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepFwd);
     sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRoot);
     ps.next("apply vec 3 cy coarse root-correction");
-    k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
-                                                       h->sv1.p, h->cy.p, skip);
-    CB_LAUNCH();
-    k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
-                                                           h->coarse_id.p, h->zc.p, h->cy.p, h->gl.p, 0, skip);
-    CB_LAUNCH();
-    k_coarse_rhs<<<grid_for(h->n_coarse, 128), 128, 0, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->gc.p, skip);
-    CB_LAUNCH();
-    allreduce_sum(h, h->gc.p, (size_t)h->n_coarse);
-    if (h->n_coarse <= kCoarseInverseMax) {
-      k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_full.p, h->gc.p,
-                                                                           h->zc.p, skip);
+    const int cr_blocks = (int)((h->tK.tpl.sn.back().ncols + 255) / 256);
+    if (!distributed(h) && h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
+      k_coarse_in<<<h->nsd, 256, 0, s>>>(T, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, h->sv1.p, h->ac_off.p,
+                                         h->sinv.p, h->cy.p, h->gl.p, skip);
       CB_LAUNCH();
-    } else {  // zc = X^T (X gc), X = L_c^{-1}
-      const int nc = h->n_coarse;
-      k_xg_part<<<dim3((nc + 255) / 256, (nc + 63) / 64), 256, 0, s>>>(nc, h->acoarse_inv.p, h->gc.p, h->ws_cpart.p,
-                                                                       skip);
+      const size_t shm = sizeof(double) * ((size_t)h->n_coarse + 2 * kFusedCoarseM);
+      static size_t shm_set = 0;
+      if (shm > 48 * 1024 && shm > shm_set) {
+        CB_CUDA(cudaFuncSetAttribute(k_coarse_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        shm_set = shm;
+      }
+      k_coarse_out<<<dim3(h->nsd, cr_blocks), 256, shm, s>>>(
+          h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->acoarse_full.p, h->coarse_id.p, h->m_off.p, h->ac_off.p,
+          h->sinv.p, h->cy.p, h->root_info.p, h->fK.cslot.p, h->wroot.p, h->sv1.p, skip);
       CB_LAUNCH();
-      k_xg_sum<<<grid_for(nc, 256), 256, 0, s>>>(nc, h->ws_cpart.p, h->uvec_c.p, skip);
+    } else {
+      k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
+                                                         h->sv1.p, h->cy.p, skip);
       CB_LAUNCH();
-      k_xty<<<grid_for((int64_t)nc * 32, 256), 256, 0, s>>>(nc, h->acoarse_inv.p, h->uvec_c.p, h->zc.p, skip);
+      k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
+                                                             h->coarse_id.p, h->zc.p, h->cy.p, h->gl.p, 0, skip);
+      CB_LAUNCH();
+      k_coarse_rhs<<<grid_for(h->n_coarse, 128), 128, 0, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->gc.p, skip);
+      CB_LAUNCH();
+      allreduce_sum(h, h->gc.p, (size_t)h->n_coarse);
+      if (h->n_coarse <= kCoarseInverseMax) {
+        k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_full.p, h->gc.p,
+                                                                             h->zc.p, skip);
+        CB_LAUNCH();
+      } else {  // zc = X^T (X gc), X = L_c^{-1}
+        const int nc = h->n_coarse;
+        k_xg_part<<<dim3((nc + 255) / 256, (nc + 63) / 64), 256, 0, s>>>(nc, h->acoarse_inv.p, h->gc.p, h->ws_cpart.p,
+                                                                         skip);
+        CB_LAUNCH();
+        k_xg_sum<<<grid_for(nc, 256), 256, 0, s>>>(nc, h->ws_cpart.p, h->uvec_c.p, skip);
+        CB_LAUNCH();
+        k_xty<<<grid_for((int64_t)nc * 32, 256), 256, 0, s>>>(nc, h->acoarse_inv.p, h->uvec_c.p, h->zc.p, skip);
+        CB_LAUNCH();
+      }
+      k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
+                                                             h->coarse_id.p, h->zc.p, h->cy.p, h->uvec.p, 1, skip);
+      CB_LAUNCH();
+      k_root_correct<<<dim3(h->nsd, cr_blocks), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.cslot.p, h->wroot.p,
+                                                             h->uvec.p, h->sv1.p, skip);
       CB_LAUNCH();
     }
-    k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
-                                                           h->coarse_id.p, h->zc.p, h->cy.p, h->uvec.p, 1, skip);
-    CB_LAUNCH();
-    const int cr_blocks = (int)((h->tK.tpl.sn.back().ncols + 255) / 256);
-    k_root_correct<<<dim3(h->nsd, cr_blocks), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.cslot.p, h->wroot.p,
-                                                           h->uvec.p, h->sv1.p, skip);
-    CB_LAUNCH();
     ps.close();
     sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRest);
     ps.next("apply vec 3b gather Av");

@@ -24,7 +24,11 @@ namespace {
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs, fixed for deterministic reductions
 constexpr int kRedThreads = 256;
 
-enum { S_RZ = 0, S_PQ, S_ALPHA, S_BETA, S_STOP, S_RN, S_COUNT };
+// rz ping-pongs between S_RZ (even iterations) and S_RZ1 (odd): the fused
+// beta/p-update kernel reads the old value in every block while block 0
+// stores the new one.
+enum { S_RZ = 0, S_PQ, S_ALPHA, S_BETA, S_STOP, S_RN, S_RZ1, S_COUNT };
+__device__ __forceinline__ int rz_slot(int k) { return (k & 1) ? S_RZ1 : S_RZ; }
 enum { I_DONE = 0, I_ITER, I_ERR, I_ITERS, I_CONV, I_MAXIT, I_COUNT };
 
 __global__ void __launch_bounds__(kRedThreads) k_spmv_dot(int64_t nd, const double* __restrict__ aval,
@@ -62,47 +66,73 @@ __device__ inline double finish_sum(const double* partial, double* sh) {
   return block_sum<kRedThreads>(v, sh);
 }
 
-// alpha = rz / pq
-__global__ void k_alpha(const double* __restrict__ partial, double* __restrict__ sc, int* __restrict__ is) {
+// finish_sum, the total broadcast to every thread of the block
+__device__ inline double finish_sum_all(const double* partial, double* sh) {
+  __shared__ double tot;
+  const double v = finish_sum(partial, sh);
+  if (threadIdx.x == 0) tot = v;
+  __syncthreads();
+  return tot;
+}
+
+// alpha = rz / pq (every block from the same fixed-order sum of `partial`),
+// x += alpha p, r -= alpha q, and the partials of r.r for k_check in `rpart`
+// (k_dot's mapping; at a refresh iteration k_refresh writes them instead)
+__global__ void __launch_bounds__(kRedThreads) k_update_xr(int64_t nd, double* __restrict__ sc,
+                                                           const double* __restrict__ p, const double* __restrict__ q,
+                                                           double* __restrict__ x, double* __restrict__ r,
+                                                           double* __restrict__ lal, const double* __restrict__ partial,
+                                                           double* __restrict__ rpart, int* __restrict__ is) {
   if (is[I_DONE]) return;
   __shared__ double sh[32];
-  const double pq = finish_sum(partial, sh);
-  if (threadIdx.x == 0) {
-    sc[S_PQ] = pq;
-    if (!(pq > 0.0)) {
+  const int k = is[I_ITER];
+  const double pq = finish_sum_all(partial, sh);
+  if (!(pq > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc[S_PQ] = pq;
       is[I_ERR] = 1;
       is[I_DONE] = 1;
-      is[I_ITERS] = is[I_ITER];
-      return;
+      is[I_ITERS] = k;
     }
-    sc[S_ALPHA] = sc[S_RZ] / pq;
+    return;
   }
-}
-
-__global__ void k_update_xr(int64_t nd, const double* __restrict__ sc, const double* __restrict__ p,
-                            const double* __restrict__ q, double* __restrict__ x, double* __restrict__ r,
-                            double* __restrict__ lal, const int* __restrict__ is) {
-  if (is[I_DONE]) return;
-  const double a = sc[S_ALPHA];
+  const double a = sc[rz_slot(k)] / pq;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i0 == 0) lal[is[I_ITER] - 1] = a;
+  if (i0 == 0) {
+    sc[S_PQ] = pq;
+    sc[S_ALPHA] = a;
+    lal[k - 1] = a;
+  }
+  double acc = 0.0;
   for (int64_t i = i0; i < nd; i += (int64_t)gridDim.x * blockDim.x) {
     x[i] += a * p[i];
-    r[i] -= a * q[i];
+    const double ri = r[i] - a * q[i];
+    r[i] = ri;
+    acc += ri * ri;
   }
+  if (k % 50 == 0) return;  // k_refresh replaces r and its partials
+  acc = block_sum<kRedThreads>(acc, sh);
+  if (threadIdx.x == 0) rpart[blockIdx.x] = acc;
 }
 
-// true residual refresh at k % 50 == 0: r = b - Abar x
-__global__ void k_refresh(int64_t nd, const double* __restrict__ aval, const int32_t* __restrict__ acol,
-                          const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
-                          const int* __restrict__ is) {
+// true residual refresh at k % 50 == 0: r = b - Abar x, and the r.r partials
+__global__ void __launch_bounds__(kRedThreads) k_refresh(int64_t nd, const double* __restrict__ aval,
+                                                         const int32_t* __restrict__ acol, const double* __restrict__ x,
+                                                         const double* __restrict__ b, double* __restrict__ r,
+                                                         double* __restrict__ rpart, const int* __restrict__ is) {
   if (is[I_DONE] || is[I_ITER] % 50 != 0) return;
+  __shared__ double sh[32];
+  double acc = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < 27; ++k) s += aval[(int64_t)k * nd + i] * x[acol[(int64_t)k * nd + i]];
-    r[i] = b[i] - s;
+    const double ri = b[i] - s;
+    r[i] = ri;
+    acc += ri * ri;
   }
+  acc = block_sum<kRedThreads>(acc, sh);
+  if (threadIdx.x == 0) rpart[blockIdx.x] = acc;
 }
 
 // |r| -> history, convergence / max_iter test
@@ -128,32 +158,32 @@ __global__ void k_check(const double* __restrict__ partial, double* __restrict__
   }
 }
 
-// beta = rz_new / rz
-__global__ void k_beta(const double* __restrict__ partial, double* __restrict__ sc, int* __restrict__ is,
-                       double* __restrict__ lbe) {
+// beta = rz_new / rz (every block from the same fixed-order sum; rz_new to
+// the other ping-pong slot), p = z + beta p
+__global__ void __launch_bounds__(kRedThreads) k_update_p(int64_t nd, const double* __restrict__ partial,
+                                                          double* __restrict__ sc, const double* __restrict__ z,
+                                                          double* __restrict__ p, double* __restrict__ lbe,
+                                                          int* __restrict__ is) {
   if (is[I_DONE]) return;
   __shared__ double sh[32];
-  const double rz = finish_sum(partial, sh);
-  if (threadIdx.x == 0) {
-    if (!(rz > 0.0)) {
+  const int k = is[I_ITER];
+  const double rz = finish_sum_all(partial, sh);
+  if (!(rz > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       is[I_ERR] = 2;
       is[I_DONE] = 1;
-      is[I_ITERS] = is[I_ITER];
-      return;
+      is[I_ITERS] = k;
     }
-    const double beta = rz / sc[S_RZ];
-    sc[S_BETA] = beta;
-    sc[S_RZ] = rz;
-    lbe[is[I_ITER] - 1] = beta;
+    return;
   }
-}
-
-__global__ void k_update_p(int64_t nd, const double* __restrict__ sc, const double* __restrict__ z, double* __restrict__ p,
-                           int* __restrict__ is) {
-  if (is[I_DONE]) return;
-  const double b = sc[S_BETA];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = z[i] + b * p[i];
+  const double beta = rz / sc[rz_slot(k)];
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i0 == 0) {
+    sc[S_BETA] = beta;
+    sc[rz_slot(k + 1)] = rz;
+    lbe[k - 1] = beta;
+  }
+  for (int64_t i = i0; i < nd; i += (int64_t)gridDim.x * blockDim.x) p[i] = z[i] + beta * p[i];
 }
 
 __global__ void k_next(int* __restrict__ is) {
@@ -166,7 +196,7 @@ __global__ void k_init_rz(const double* __restrict__ partial, double* __restrict
   __shared__ double sh[32];
   const double rz = finish_sum(partial, sh);
   if (threadIdx.x == 0) {
-    sc[S_RZ] = rz;
+    sc[rz_slot(1)] = rz;
     if (!(rz > 0.0)) {
       is[I_ERR] = 2;
       is[I_DONE] = 1;
@@ -185,15 +215,14 @@ void enqueue_iteration(cutbddc_gpu* h) {
   int* is = h->iscal.p;
   double* sc = h->scal.p;
   k_spmv_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->aval.p, h->acol.p, h->pp.p, h->pq.p, h->partials.p, is);
-  k_alpha<<<1, kRedThreads, 0, s>>>(h->partials.p, sc, is);
-  k_update_xr<<<kRedBlocks, kRedThreads, 0, s>>>(nd, sc, h->pp.p, h->pq.p, h->px.p, h->pr.p, h->lal.p, is);
-  k_refresh<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->aval.p, h->acol.p, h->px.p, h->pb.p, h->pr.p, is);
-  k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pr.p, h->pr.p, h->partials.p, is);
-  k_check<<<1, kRedThreads, 0, s>>>(h->partials.p, sc, is, h->hist.p);
+  k_update_xr<<<kRedBlocks, kRedThreads, 0, s>>>(nd, sc, h->pp.p, h->pq.p, h->px.p, h->pr.p, h->lal.p, h->partials.p,
+                                                 h->partials.p + kRedBlocks, is);
+  k_refresh<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->aval.p, h->acol.p, h->px.p, h->pb.p, h->pr.p,
+                                               h->partials.p + kRedBlocks, is);
+  k_check<<<1, kRedThreads, 0, s>>>(h->partials.p + kRedBlocks, sc, is, h->hist.p);
   apply_bddc_device(h, h->pr.p, h->pz.p, is);
   k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pr.p, h->pz.p, h->partials.p, is);
-  k_beta<<<1, kRedThreads, 0, s>>>(h->partials.p, sc, is, h->lbe.p);
-  k_update_p<<<kRedBlocks, kRedThreads, 0, s>>>(nd, sc, h->pz.p, h->pp.p, is);
+  k_update_p<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->partials.p, sc, h->pz.p, h->pp.p, h->lbe.p, is);
   k_next<<<1, 1, 0, s>>>(is);
   CB_LAUNCH();
 }
@@ -251,7 +280,7 @@ void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, 
   h->hist.alloc((size_t)max_iter + 1);
   h->lal.alloc((size_t)max_iter + 1);
   h->lbe.alloc((size_t)max_iter + 1);
-  h->partials.alloc(kRedBlocks);
+  h->partials.alloc(2 * kRedBlocks);  // p.q / r.z partials, then r.r
   h->scal.alloc(S_COUNT);
   h->iscal.alloc(I_COUNT);
   cudaEvent_t e0, e1;
@@ -280,7 +309,7 @@ void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, 
     h->px.zero(s);
     conv = 1;
   } else {
-    const double host_sc[S_COUNT] = {0, 0, 0, 0, rtol * bnorm, 0};
+    const double host_sc[S_COUNT] = {0, 0, 0, 0, rtol * bnorm, 0, 0};
     CB_CUDA(cudaMemcpyAsync(h->scal.p, host_sc, sizeof(host_sc), cudaMemcpyHostToDevice, s));
     const int host_is[I_COUNT] = {0, 1, 0, 0, 0, max_iter};
     CB_CUDA(cudaMemcpyAsync(h->iscal.p, host_is, sizeof(host_is), cudaMemcpyHostToDevice, s));
