@@ -182,6 +182,28 @@ __device__ __forceinline__ void wait_children(const SweepDev& p, const FrontDesc
   if (d.nch > 1) cta_wait(p, p.done_f + d.cfs1, d.cnf1);
 }
 
+// HBM -> L2 prefetch of panel data an item is about to stream, issued before
+// its dependency wait (no registers or shared memory held): the GEMV after
+// the wait then reads L2. Rows [i0, i1) of columns [j0, j1) of a column-major
+// panel with leading dimension r, one 128-B line per request, never past a
+// column's end.
+__device__ __forceinline__ void prefetch_l2(const double* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
+__device__ __forceinline__ void prefetch_panel(const double* G, int r, int i0, int i1, int j0, int j1, int tid, int nt) {
+  const int seg = i1 - i0;
+  if (seg <= 0 || j1 <= j0) return;
+  if (seg == r) {  // whole columns: one contiguous range
+    const int64_t n = (int64_t)(j1 - j0) * r;
+    const double* b = G + (int64_t)j0 * r;
+    for (int64_t e = (int64_t)tid * 16; e < n + 15; e += (int64_t)nt * 16) prefetch_l2(b + min(e, n - 1));
+    return;
+  }
+  const int lpc = (seg + 15) / 16 + 1;  // lines per column segment (unaligned start)
+  for (int t = tid; t < (j1 - j0) * lpc; t += nt) {
+    const int j = j0 + t / lpc, l = t % lpc;
+    prefetch_l2(G + (int64_t)j * r + i0 + min(16 * l, seg - 1));
+  }
+}
+
 // nw consecutive warps w0 .. w0 + nw - 1 of the CTA working on one front;
 // named barrier `bar` (the whole CTA: __syncthreads). T items run the
 // independent fronts of one subtree level side by side, one group each.
@@ -359,6 +381,10 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
       // bottom subtree of sid: its fronts deepest level first, one after another
       const int32_t* meta = p.sub_meta + chunk;
       const int ng = meta[0];
+      for (int k = meta[1]; k < meta[1 + ng]; ++k) {
+        const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
+        prefetch_panel(panel + d.po, d.r, 0, d.r, 0, d.c, tid, kThreadsSweep);
+      }
       for (int gi = 0; gi < ng; ++gi)  // deepest level first
         subtree_level(meta[1 + gi], meta[2 + gi], [&](const Grp& g, int k, int f) {
           const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
@@ -369,6 +395,7 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
     }
     const FrontDesc d = load_desc(p.desc + fs);
     if (kind == kItemS) {
+      prefetch_panel(panel + d.po, d.r, 0, d.r, 0, d.c, tid, kThreadsSweep);
       grp_front_fwd(whole_cta(), p, d, panel, X, ysave, upd, v, v + kVecDoubles, true);
       cta_signal(p.done_f + fs);
       continue;
@@ -385,6 +412,7 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
     const int jrow = min(c, i1);
     const int jlo = cb * kFwdCols, jhi = min(jrow, jlo + kFwdCols);
     double* tp = p.vbuf + d.tpo + (int64_t)rb * mcb * kFwdRows;
+    prefetch_panel(panel + d.po, r, i0, i1, jlo, jhi, tid, kThreadsSweep);
     for (int q = jlo + tid; q < jhi; q += kThreadsSweep) v[q] = X[cs[q]];
     grp_gemv_fwd<kFwdRows / 32, 4>(
         whole_cta(), panel + d.po, r, jlo, jhi, i0, i1, v, v + kVecDoubles,
@@ -438,6 +466,10 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDe
       // only its root depends on other items (its parent)
       const int32_t* meta = p.sub_meta + chunk;
       const int ng = meta[0];
+      for (int k = meta[1]; k < meta[1 + ng]; ++k) {
+        const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
+        prefetch_panel(panel + d.po, d.r, 0, d.r, 0, d.c, tid, kThreadsSweep);
+      }
       for (int gi = ng - 1; gi >= 0; --gi)  // shallowest level (the subtree root, one front) first
         subtree_level(meta[1 + gi], meta[2 + gi], [&](const Grp& g, int k, int f) {
           const FrontDesc d = load_desc(p.desc + (int64_t)sd * p.nsn + p.sub_sids[k]);
@@ -447,6 +479,7 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDe
     }
     const FrontDesc d = load_desc(p.desc + fs);
     if (kind == kItemS) {
+      prefetch_panel(panel + d.po, d.r, 0, d.r, 0, d.c, tid, kThreadsSweep);
       grp_front_bwd(whole_cta(), p, d, panel, X, ysave, w, part, true);
       cta_signal(p.done_b + fs);
       continue;
@@ -457,6 +490,7 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDe
     // gathers [y; -x_rest] itself (rows from j0 on: the columns' G is zero above)
     const double* G = panel + d.po;
     const int j0 = chunk * kBwdCols, j1 = min(c, j0 + kBwdCols);
+    prefetch_panel(G, r, j0, r, j0, j1, tid, kThreadsSweep);
     for (int q = j0 + tid; q < c; q += kThreadsSweep) w[q] = ysave[cs[q]];
     if (d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
     for (int q = max(c, j0) + tid; q < r; q += kThreadsSweep) w[q] = -__ldcg(X + cs[q]);
@@ -782,15 +816,25 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
       return remb[i];
     };
     auto order = [&](std::vector<int4>& v, size_t b, size_t e, bool fwd) {
-      std::vector<std::pair<double, int4>> kv;
-      for (size_t q = b; q < e; ++q) kv.emplace_back(key(v[q], fwd), v[q]);
-      std::stable_sort(kv.begin(), kv.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-      for (size_t q = b; q < e; ++q) v[q] = kv[q - b].second;
+      const size_t n = e - b;
+      std::vector<double> k(n);
+      std::vector<int32_t> ix(n);
+      for (size_t q = 0; q < n; ++q) {
+        k[q] = key(v[b + q], fwd);
+        ix[q] = (int32_t)q;
+      }
+      std::sort(ix.begin(), ix.end(), [&](int32_t x, int32_t y) { return k[x] > k[y] || (k[x] == k[y] && x < y); });
+      std::vector<int4> out(n);
+      for (size_t q = 0; q < n; ++q) out[q] = v[b + ix[q]];
+      std::copy(out.begin(), out.end(), v.begin() + (std::ptrdiff_t)b);
     };
-    order(fw, 0, fw.size(), true);
-    const size_t nroot = std::min(bw.size(), (size_t)std::max(0, f.n_items_b_root));
-    order(bw, 0, nroot, false);  // the root phase stays a launch of its own
-    order(bw, nroot, bw.size(), false);
+    static const bool level_order = std::getenv("CUTBDDC_SWEEP_LEVEL_ORDER") != nullptr;  // A/B: plain level order
+    if (!level_order) {
+      const size_t nroot = std::min(bw.size(), (size_t)std::max(0, f.n_items_b_root));
+      order(fw, 0, fw.size(), true);
+      order(bw, 0, nroot, false);  // the root phase stays a launch of its own
+      order(bw, nroot, bw.size(), false);
+    }
   }
   f.n_items_f = (int)fw.size();
   f.n_items_b = (int)bw.size();
