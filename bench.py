@@ -113,7 +113,7 @@ def run_reference(args, cfg, rank, world):
         "impl": "reference", "metric": "PCG+BDDC solved DOFs/sec to rtol 1e-6 (fp64)", "value": value,
         "unit": "DOF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded ball-union geometry, BASELINE.json configs[3])",
+        "dtype": "f64", "data": f"synthetic (seeded ball-union geometry, BASELINE.json configs[{int(cfg.name[3:]) - 1}])",
         "config": _config(cfg, args),
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": "port",
                          "sample": f"{len(times)} full solves (assembly+setup+PCG, {iters} PCG iterations) of "
@@ -126,8 +126,9 @@ def run_reference(args, cfg, rank, world):
 
 
 def _config(cfg, args):
-    return {"workload": f"{cfg.name}-{cfg.cells}^3 (BASELINE.json configs[3], weak-scaling family at "
-                        f"{args.gpus} GPU)", "cells": cfg.cells, "block": cfg.block, "balls": len(cfg.balls),
+    idx = int(cfg.name[3:]) - 1
+    what = "weak-scaling family at " + f"{args.gpus} GPU" if cfg.name == "cfg4" else "single-GPU run"
+    return {"workload": f"{cfg.name}-{cfg.cells}^3 (BASELINE.json configs[{idx}], {what})", "cells": cfg.cells, "block": cfg.block, "balls": len(cfg.balls),
             "objects": ["c", "ce", "cef"][cfg.objects], "weighting": ["topological", "stiffness"][cfg.weighting],
             "variant": ["standard", "v1", "v2"][cfg.variant], "rtol": cfg.rtol, "parallelism": f"subdomains x{args.gpus}",
             "l2": "inputs larger than L2 (factor panels > 126 MB)"}
@@ -263,7 +264,7 @@ def main():
             "metric": "PCG+BDDC solved DOFs/sec to rtol 1e-6 (fp64)", "value": value, "unit": "DOF/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded ball-union geometry, BASELINE.json configs[3])",
+            "data": f"synthetic (seeded ball-union geometry, BASELINE.json configs[{int(cfg.name[3:]) - 1}])",
             "config": _config(cfg, args),
             "n_dof": n_dof, "iterations": r0["iterations"], "cond_estimate": r0["cond"],
             "phases_ms": {"assembly": 1e3 * np.mean([r["t_assembly"] for r in reps]),
