@@ -44,28 +44,66 @@ def _env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in-process
+    through NVML every 20 ms (spawning nvidia-smi takes driver locks and
+    stalls the solver's own host-side steps); nvidia-smi only as a fallback."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, {reason names})
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_sampler(self):
+        import pynvml
+        pynvml.nvmlInit()
+        idx = self.gpu
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                idx = int(vis.split(",")[self.gpu])
+            except (ValueError, IndexError):
+                pass
+        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        bits = [(n, getattr(pynvml, a)) for n, a in self.REASONS]
+
+        def sample():
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            ev = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            return float(sm), float(mx), {n for n, b in bits if ev & b}
+        return sample
+
+    def _smi_sampler(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+        def sample():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                 capture_output=True, text=True, timeout=5).stdout.strip()
+            v = [x.strip() for x in out.split(",")]
+            return float(v[0]), float(v[1]), {n for (n, _), x in zip(self.REASONS, v[2:]) if x == "Active"}
+        return sample
+
     def start(self):
+        try:
+            sample, period = self._nvml_sampler(), 0.02
+        except Exception:
+            sample, period = self._smi_sampler(), 0.2
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
-            while not self._stop.is_set():
+            while True:
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                         capture_output=True, text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([v.strip() for v in out.split(",")])
+                    self.rows.append(sample())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                if self._stop.wait(period):
+                    break
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -76,12 +114,8 @@ class ClockSampler:
             self._t.join(timeout=10)
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*(r[2] for r in self.rows))), "samples": len(self.rows)}
 
 
 def cpu_reference(cfg, steps: int, warmup: int, threads: int):
@@ -137,7 +171,7 @@ def _config(cfg, args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4")

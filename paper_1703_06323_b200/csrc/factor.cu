@@ -458,9 +458,6 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
 void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs) {
   cudaStream_t s = h->stream;
   const int nsd = h->nsd;
-  size_t free_b = 0, total_b = 0;
-  CB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const int64_t budget = std::max<int64_t>((1ll << 30) / 8, (int64_t)(free_b / 2 + front_bytes_held(h)) / 8);
   DevBuf<unsigned long long>& fail = h->ws_fail;
   fail.alloc(jobs.size());
   CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8 * jobs.size(), s));
@@ -468,6 +465,15 @@ void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs) {
   ProfScope pnum(h->prof, s, "factor numeric");
   int64_t all = 0;
   for (const FactorJob& j : jobs) all += j.f->h_front_base[(size_t)nsd];
+  // front workspace budget: what is held, plus half the free memory. The
+  // memory query (slow, and it can stall behind other driver work: up to
+  // ~90 ms seen) only when the held workspace is too small.
+  int64_t budget = (int64_t)front.cap;
+  if (all > budget) {
+    size_t free_b = 0, total_b = 0;
+    CB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    budget = std::max<int64_t>((1ll << 30) / 8, (int64_t)(free_b / 2 + front_bytes_held(h)) / 8);
+  }
   if (all <= budget) {
     std::vector<FactorSpan> spans;
     int64_t off = 0;

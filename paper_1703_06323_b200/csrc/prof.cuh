@@ -9,6 +9,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -25,6 +26,7 @@ struct Prof {
   };
   std::vector<Rec> pending;
   std::map<std::string, std::pair<long long, double>> tot;  // name -> (count, ms)
+  std::map<std::string, double> mx;                         // name -> max ms of one scope
 
   Prof() {
     const char* e = std::getenv("CUTBDDC_PROFILE");
@@ -38,6 +40,7 @@ struct Prof {
       auto& t = tot[r.name];
       t.first += 1;
       t.second += ms;
+      mx[r.name] = std::max(mx[r.name], (double)ms);
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
     }
@@ -48,10 +51,11 @@ struct Prof {
     flush();
     double all = 0;
     for (auto& kv : tot) all += kv.second.second;
-    std::fprintf(stderr, "[cutbddc profile] %-40s %8s %10s %10s\n", "scope", "count", "total ms", "mean us");
+    std::fprintf(stderr, "[cutbddc profile] %-40s %8s %10s %10s %10s\n", "scope", "count", "total ms", "mean us",
+                 "max us");
     for (auto& kv : tot)
-      std::fprintf(stderr, "[cutbddc profile] %-40s %8lld %10.3f %10.2f\n", kv.first.c_str(), kv.second.first,
-                   kv.second.second, 1e3 * kv.second.second / (double)kv.second.first);
+      std::fprintf(stderr, "[cutbddc profile] %-40s %8lld %10.3f %10.2f %10.2f\n", kv.first.c_str(), kv.second.first,
+                   kv.second.second, 1e3 * kv.second.second / (double)kv.second.first, 1e3 * mx[kv.first]);
     std::fprintf(stderr, "[cutbddc profile] (scopes may nest; sum of all = %.3f ms)\n", all);
   }
   ~Prof() {

@@ -177,6 +177,17 @@ __device__ __forceinline__ double child_sum(const SweepDev& p, const FrontDesc& 
   return v;
 }
 
+// child_sum with the gmap entry already loaded (static: loaded before the
+// dependency wait, so only the update loads remain after it)
+__device__ __forceinline__ double child_sum_g(int2 g, const double* upd, double v, bool cross) {
+  if (g.x >= 0) v += cross ? __ldcg(upd + g.x) : upd[g.x];
+  if (g.y >= 0) v += cross ? __ldcg(upd + g.y) : upd[g.y];
+  return v;
+}
+__device__ __forceinline__ int2 gmap_at(const SweepDev& p, const FrontDesc& d, int q) {
+  return reinterpret_cast<const int2*>(p.gmap)[d.vo + q];
+}
+
 __device__ __forceinline__ void wait_children(const SweepDev& p, const FrontDesc& d) {
   if (d.nch > 0) cta_wait(p, p.done_f + d.cfs0, d.cnf0);
   if (d.nch > 1) cta_wait(p, p.done_f + d.cfs1, d.cnf1);
@@ -277,13 +288,15 @@ __device__ void grp_front_fwd(const Grp& g, const SweepDev& p, const FrontDesc& 
   const int lt = g.lt(), nt = g.nt();
   const int32_t* cs = p.cslot + d.vo;
   for (int q = lt; q < r; q += nt) v[q] = q < c ? X[cs[q]] : 0.0;
+  const int2 g0 = lt < r ? gmap_at(p, d, lt) : make_int2(-1, -1);
   double* uo = upd + d.uo;
   grp_gemv_fwd<kSmallRows / 32, 2>(
       g, panel + d.po, r, 0, c, 0, r, v, part,
       [&] {
         if (wait) wait_children(p, d);
         g.sync();
-        for (int q = lt; q < r; q += nt) v[q] = child_sum(p, d, upd, q, v[q], wait);
+        if (lt < r) v[lt] = child_sum_g(g0, upd, v[lt], wait);
+        for (int q = lt + nt; q < r; q += nt) v[q] = child_sum(p, d, upd, q, v[q], wait);
         g.sync();
       },
       [&](int i, double o) {
@@ -316,8 +329,10 @@ __device__ void grp_front_bwd(const Grp& g, const SweepDev& p, const FrontDesc& 
   double acc[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = (i_first < rb && k < c) ? G[i_first + (int64_t)k * r] : 0.0;
+  const int s0 = c + lt < r ? cs[c + lt] : 0;  // slot of the first update row (static: before the wait)
   if (wait && d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
-  for (int q = c + lt; q < r; q += nt) w[q] = -__ldcg(X + cs[q]);
+  if (c + lt < r) w[c + lt] = -__ldcg(X + s0);
+  for (int q = c + lt + nt; q < r; q += nt) w[q] = -__ldcg(X + cs[q]);
   g.sync();
   for (int jb = 0; jb < c; jb += 16) {
     int i = max(ra, jb) + lane;
@@ -413,13 +428,19 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
     const int jlo = cb * kFwdCols, jhi = min(jrow, jlo + kFwdCols);
     double* tp = p.vbuf + d.tpo + (int64_t)rb * mcb * kFwdRows;
     prefetch_panel(panel + d.po, r, i0, i1, jlo, jhi, tid, kThreadsSweep);
-    for (int q = jlo + tid; q < jhi; q += kThreadsSweep) v[q] = X[cs[q]];
+    static_assert(kFwdCols <= kThreadsSweep && kFwdRows <= kThreadsSweep, "one column / row per thread");
+    const int qc = jlo + tid, qr = i0 + tid;  // this thread's column of the tile, row of the row block
+    if (qc < jhi) v[qc] = X[cs[qc]];
+    const int2 gc = qc < jhi ? gmap_at(p, d, qc) : make_int2(-1, -1);
+    const int2 gr = (qr < i1 && qr >= c) ? gmap_at(p, d, qr) : make_int2(-1, -1);
+    double cu = 0.0;  // children's updates at update row qr (used by the row block's last tile)
     grp_gemv_fwd<kFwdRows / 32, 4>(
         whole_cta(), panel + d.po, r, jlo, jhi, i0, i1, v, v + kVecDoubles,
         [&] {
           wait_children(p, d);
           __syncthreads();
-          for (int q = jlo + tid; q < jhi; q += kThreadsSweep) v[q] = child_sum(p, d, upd, q, v[q], true);
+          if (qc < jhi) v[qc] = child_sum_g(gc, upd, v[qc], true);
+          cu = child_sum_g(gr, upd, 0.0, true);
           __syncthreads();
         },
         [&](int i, double o) { tp[(int64_t)cb * kFwdRows + i - i0] = o; });
@@ -434,14 +455,14 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_fwd(SweepDe
     if (!s_last) continue;
     const int ncb = max(1, (jrow + kFwdCols - 1) / kFwdCols);
     double* uo = upd + d.uo;
-    for (int q = tid; q < i1 - i0; q += kThreadsSweep) {
-      const int i = i0 + q;
+    if (tid < i1 - i0) {
+      const int i = i0 + tid;
       double o = 0.0;
-      for (int k = 0; k < ncb; ++k) o += __ldcg(tp + (int64_t)k * kFwdRows + q);
+      for (int k = 0; k < ncb; ++k) o += __ldcg(tp + (int64_t)k * kFwdRows + tid);
       if (i < c)
         ysave[cs[i]] = o;
       else
-        uo[i - c] = child_sum(p, d, upd, i, 0.0, true) - o;
+        uo[i - c] = cu - o;
     }
     cta_signal(p.done_f + fs);
   }
@@ -492,8 +513,11 @@ __global__ void __launch_bounds__(kThreadsSweep, kMinBlocks) k_sweep_bwd(SweepDe
     const int j0 = chunk * kBwdCols, j1 = min(c, j0 + kBwdCols);
     prefetch_panel(G, r, j0, r, j0, j1, tid, kThreadsSweep);
     for (int q = j0 + tid; q < c; q += kThreadsSweep) w[q] = ysave[cs[q]];
-    if (d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);
-    for (int q = max(c, j0) + tid; q < r; q += kThreadsSweep) w[q] = -__ldcg(X + cs[q]);
+    int32_t* ci = reinterpret_cast<int32_t*>(w + kVecDoubles);  // update-row slots, staged before the wait
+    for (int q = max(c, j0) + tid; q < r; q += kThreadsSweep) ci[q] = cs[q];
+    if (d.pfs >= 0) cta_wait(p, p.done_b + d.pfs, d.pnb);  // (its __syncthreads publishes ci)
+    if (d.pfs < 0) __syncthreads();
+    for (int q = max(c, j0) + tid; q < r; q += kThreadsSweep) w[q] = -__ldcg(X + ci[q]);
     __syncthreads();
     for (int j = j0 + wid; j < j1; j += kWarps) {
       const double* col = G + (int64_t)j * r;
