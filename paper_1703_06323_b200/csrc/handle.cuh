@@ -206,5 +206,6 @@ struct cutbddc_gpu {
   cudaGraphExec_t graph_exec = nullptr;
   int graph_max_iter = -1;
   long long graph_nodes = 0;                      // kernel nodes per PCG-iteration graph
+  bool graph_while = false;                       // graph_exec runs the whole loop (conditional WHILE node)
   double t_pcg = 0;
 };

@@ -14,9 +14,11 @@
 // two-stage fixed-order reductions: bit-reproducible run to run.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "bddc.cuh"
+#include "comm.cuh"
 
 namespace cutbddc_b200 {
 namespace {
@@ -209,6 +211,57 @@ __global__ void k_copy(int64_t nd, const double* __restrict__ a, double* __restr
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
+// Loop condition of the whole-solve graph: another iteration unless done.
+__global__ void k_loop_cond(cudaGraphConditionalHandle hc, const int* __restrict__ is) {
+  cudaGraphSetConditional(hc, is[I_DONE] ? 0u : 1u);
+}
+
+void enqueue_iteration(cutbddc_gpu* h);
+
+// One graph for the whole PCG loop on one GPU: a conditional WHILE node whose
+// body is the captured iteration plus k_loop_cond. No host polling and no
+// no-op iterations after convergence. false (and nothing kept) if the driver
+// refuses any step; the caller then uses per-iteration graph launches.
+bool build_while_graph(cutbddc_gpu* h) {
+  cudaStream_t s = h->stream;
+  cudaGraph_t g = nullptr;
+  auto fail = [&] {
+    cudaGetLastError();
+    if (g) cudaGraphDestroy(g);
+    return false;
+  };
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return fail();
+  cudaGraphConditionalHandle hc;
+  if (cudaGraphConditionalHandleCreate(&hc, g, 1u, cudaGraphCondAssignDefault) != cudaSuccess) return fail();
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) return fail();
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  const long long c0 = g_kernel_launches.load();
+  if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return fail();
+  enqueue_iteration(h);
+  k_loop_cond<<<1, 1, 0, s>>>(hc, h->iscal.p);
+  const cudaError_t launch_err = cudaGetLastError();
+  const cudaError_t cap_err = cudaStreamEndCapture(s, &body);
+  g_kernel_launches.store(c0);  // captured, not executed
+  if (launch_err != cudaSuccess || cap_err != cudaSuccess) return fail();
+  size_t nodes = 0;
+  if (cudaGraphGetNodes(body, nullptr, &nodes) != cudaSuccess) return fail();
+  if (cudaGraphInstantiate(&h->graph_exec, g, 0) != cudaSuccess) {
+    h->graph_exec = nullptr;
+    return fail();
+  }
+  cudaGraphDestroy(g);
+  h->graph_nodes = (long long)nodes;
+  h->graph_while = true;
+  return true;
+}
+
 void enqueue_iteration(cutbddc_gpu* h) {
   cudaStream_t s = h->stream;
   const int64_t nd = h->n_dof;
@@ -324,8 +377,13 @@ void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, 
       cudaGraphExecDestroy(h->graph_exec);
       h->graph_exec = nullptr;
     }
+    if (!h->graph_exec && !distributed(h) && !std::getenv("CUTBDDC_NO_WHILE_GRAPH")) {
+      h->graph_max_iter = max_iter;
+      build_while_graph(h);
+    }
     if (!h->graph_exec) {
       h->graph_max_iter = max_iter;
+      h->graph_while = false;
       cudaGraph_t g;
       const long long c0 = g_kernel_launches.load();
       CB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -340,7 +398,13 @@ void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, 
     }
     int is_host[I_COUNT] = {0};
     int launched = 0, batch = 4;
-    while (true) {
+    if (h->graph_while) {
+      CB_CUDA(cudaGraphLaunch(h->graph_exec, s));
+      CB_CUDA(cudaMemcpyAsync(is_host, h->iscal.p, sizeof(is_host), cudaMemcpyDeviceToHost, s));
+      CB_CUDA(cudaStreamSynchronize(s));
+      g_kernel_launches.fetch_add(h->graph_nodes * (long long)std::max(1, is_host[I_ITER]));  // loop bodies run
+    }
+    while (!h->graph_while) {
       for (int q = 0; q < batch && launched < max_iter; ++q, ++launched) {
         CB_CUDA(cudaGraphLaunch(h->graph_exec, s));
         g_kernel_launches.fetch_add(h->graph_nodes);
