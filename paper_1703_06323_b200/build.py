@@ -63,6 +63,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
                      "--expt-relaxed-constexpr"] + ARCH + inc
             flags.append("-fmad=false" if f in NO_FMA else "-fmad=true")
+            flags += os.environ.get("CUTBDDC_NVCC_EXTRA", "").split()  # tuning macros (tools/tune_sweep.sh)
             jobs.append([NVCC] + flags + ["-c", src, "-o", obj])
     for f in CPP:
         src, obj = os.path.join(CSRC, f), os.path.join(BUILD, f + ".o")

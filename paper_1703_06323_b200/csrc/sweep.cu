@@ -37,14 +37,33 @@ namespace cutbddc_b200 {
 namespace {
 
 constexpr int kSmallRows = 256;  // S items and subtree fronts
-constexpr int kSmallWork = 8192; // S items: at most this many panel entries (r x c), else A + C tiles
-constexpr int kFwdRows = 128;    // C items forward: 128 x 128 tiles (four rows per lane)
-constexpr int kFwdCols = 64;
-constexpr int kBwdCols = 16;     // C items backward: columns per CTA (two per warp)
-constexpr int kSubLevels = 3;    // T items: the bottom levels of the elimination tree
+#ifndef CUTBDDC_SWEEP_SMALL_WORK
+#define CUTBDDC_SWEEP_SMALL_WORK 4096
+#endif
+#ifndef CUTBDDC_SWEEP_FWD_ROWS
+#define CUTBDDC_SWEEP_FWD_ROWS 128
+#endif
+#ifndef CUTBDDC_SWEEP_FWD_COLS
+#define CUTBDDC_SWEEP_FWD_COLS 64
+#endif
+#ifndef CUTBDDC_SWEEP_BWD_COLS
+#define CUTBDDC_SWEEP_BWD_COLS 16
+#endif
+#ifndef CUTBDDC_SWEEP_SUB_LEVELS
+#define CUTBDDC_SWEEP_SUB_LEVELS 3
+#endif
+#ifndef CUTBDDC_SWEEP_MIN_BLOCKS
+#define CUTBDDC_SWEEP_MIN_BLOCKS 4
+#endif
+// (the CUTBDDC_SWEEP_* macros exist for tools/tune_sweep.sh; the defaults are the measured best)
+constexpr int kSmallWork = CUTBDDC_SWEEP_SMALL_WORK; // S items: at most this many panel entries (r x c), else A + C tiles
+constexpr int kFwdRows = CUTBDDC_SWEEP_FWD_ROWS;    // C items forward: 128 x 128 tiles (four rows per lane)
+constexpr int kFwdCols = CUTBDDC_SWEEP_FWD_COLS;
+constexpr int kBwdCols = CUTBDDC_SWEEP_BWD_COLS;     // C items backward: columns per CTA (two per warp)
+constexpr int kSubLevels = CUTBDDC_SWEEP_SUB_LEVELS;    // T items: the bottom levels of the elimination tree
 constexpr int kThreadsSweep = 256;
 constexpr int kWarps = kThreadsSweep / 32;
-constexpr int kMinBlocks = 4;  // resident CTAs per SM (items in flight): <= 64 registers
+constexpr int kMinBlocks = CUTBDDC_SWEEP_MIN_BLOCKS;  // resident CTAs per SM (items in flight): <= 64 registers
 constexpr int kVecDoubles = 2048;                   // front vector: >= every template front
 constexpr int kPartDoubles = kWarps * kSmallRows;   // per-warp row partials of the forward GEMV
 constexpr int kShmDoubles = kVecDoubles + kPartDoubles;
