@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) k_bwd_level(TplDev t, FactorDev f, const 
 constexpr int kBigMinCols = 1;
 // ND leaf size: boxes of at most this many lattice nodes are leaf fronts
 // (CUTBDDC_LEAF overrides, for measurements).
-constexpr int kLeafMax = 125;  // cfg4: 27 -> 125 cut the apply's solve time 744 -> 668 us
+constexpr int kLeafMax = 216;  // cfg4: 27 -> 125 cut the apply's solve time 744 -> 668 us; 125 -> 216: 3.49 -> 3.72 M DOF/s (profiles/r01_tune_leaf.txt)
 constexpr int kBigRows = 32;   // forward: rows per CTA (one row per lane)
 constexpr int kBigCols = 16;   // backward: columns per CTA (two per warp)
 
