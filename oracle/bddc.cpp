@@ -12,6 +12,7 @@
 //   * r1 = r - Abar z0 with r1 := 0 exactly on interior dofs (App. B.12).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "oracle.hpp"
 
@@ -104,6 +105,11 @@ void build_bddc(const Problem& pb, Bddc& bd, int objects, int weighting, int var
     double dsum = 0;
     for (int i = 0; i < n; ++i) dsum += S.a.at(i, i);
     L.rho = dsum / (double)n;
+    // ORACLE_RHO_ULPS=k moves rho by k ulps (perturbation experiments only;
+    // any rho > 0 gives the same saddle solution in exact arithmetic)
+    if (const char* e = std::getenv("ORACLE_RHO_ULPS"))
+      for (int k = std::atoi(e); k != 0; k += k > 0 ? -1 : 1)
+        L.rho = std::nextafter(L.rho, k > 0 ? HUGE_VAL : 0.0);
     std::vector<std::vector<std::pair<int, double>>> rows((size_t)n);
     for (int i = 0; i < n; ++i)
       for (int p = S.a.ptr[(size_t)i]; p < S.a.ptr[(size_t)i + 1]; ++p)

@@ -308,6 +308,28 @@ int orc_pcg(void* hv, const double* b, double rtol, int max_iter, int precond, d
   });
 }
 
+// Local solve of subdomain s in its local dof order (ascending global dof):
+// which = 0: A_II^{-1} on the interior dofs (x has n_local entries; only the
+// interior ones are read and written, the rest are zeroed); which = 1: K^{-1}
+// with K = A + rho C^T C (SparseCholesky::solve, linalg.cpp:58).
+int orc_local_solve(void* hv, int s, int which, double* x) {
+  return guard([&] {
+    auto* h = static_cast<Handle*>(hv);
+    if (!h->has_bddc) fail(ErrorCode::InvalidArgument, "setup first");
+    const auto& L = h->bd.loc.at((size_t)s);
+    const size_t n = h->pb.sd.at((size_t)s).l2g.size();
+    if (which == 1) {
+      L.k.solve(x);
+      return;
+    }
+    std::vector<double> t(L.interior_local.size());
+    for (size_t k = 0; k < t.size(); ++k) t[k] = x[L.interior_local[k]];
+    if (L.has_interior) L.a_ii.solve(t.data());
+    std::fill(x, x + n, 0.0);
+    for (size_t k = 0; k < t.size(); ++k) x[L.interior_local[k]] = t[k];
+  });
+}
+
 // standalone sparse Cholesky on a CSR matrix (for linalg known-answer tests)
 int orc_cholesky_solve(int n, const int* ptr, const int* col, const double* val, double* x) {
   return guard([&] {

@@ -4,6 +4,7 @@
 // the lattice coordinates. Pivot rule of linalg.cpp:42-54: a non-positive
 // pivot raises Singular carrying the ORIGINAL index of the offending row.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 
@@ -15,8 +16,16 @@ namespace {
 
 // Recursive coordinate bisection: split the longest axis at the midpoint
 // plane; order = ND(left) ND(right) separator.
+// ND leaf size: 16 by default. ORACLE_ND_LEAF overrides it (perturbation
+// experiments of tests/test_oracle_sensitivity.py: the elimination order is
+// not part of SparseCholesky's contract, linalg.hpp:55-67).
+size_t nd_leaf() {
+  const char* e = std::getenv("ORACLE_ND_LEAF");
+  return e && e[0] ? (size_t)std::max(1, std::atoi(e)) : 16;
+}
+
 void nd_order(std::vector<int>& ids, const std::vector<std::array<int, 3>>& xyz, std::vector<int>& out) {
-  if (ids.size() <= 16) {
+  if (ids.size() <= nd_leaf()) {
     out.insert(out.end(), ids.begin(), ids.end());
     return;
   }

@@ -166,6 +166,13 @@ class Oracle:
         return dict(l2g=l2g, ptr=ptr, col=col, val=val, f=f, block=tuple(int(v) for v in info[2:5]),
                     block_id=int(info[5]))
 
+    def local_solve(self, s: int, which: int, x):
+        """Subdomain s, local dof order: which=0 -> A_II^{-1} on the interior
+        dofs (others zeroed), which=1 -> K^{-1}, K = A + rho C^T C."""
+        x = np.ascontiguousarray(x, np.float64).copy()
+        _check(lib().orc_local_solve(self.h, s, which, _p(x, D)))
+        return x
+
     def objects(self, which: int = 0):
         n = I()
         _check(lib().orc_objects(self.h, which, C.byref(n), None, None, None, None, None))

@@ -729,11 +729,25 @@ void upload_plan(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, cons
 void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, double* front) {
   cudaStream_t s = h->stream;
   DagPlan& plan = h->dag_factor;
+  // The key holds everything the task list is built from: per span the
+  // subdomain range, the workspace offset, the template (block lattice and
+  // which supernodes are split), the compact front sizes, and -- for the
+  // constrained K factorisation -- each subdomain's constraint-row range
+  // (PEN tasks store absolute row indices, so new coarse objects on the same
+  // geometry must rebuild the list).
   std::vector<int2> key;
   for (const FactorSpan& sp : spans) {
     key.push_back(make_int2(sp.sd0, sp.sd1));
     key.push_back(make_int2((int)(sp.front_off >> 31), (int)(sp.front_off & 0x7fffffff)));
+    key.push_back(make_int2(sp.ts->tpl.b1, (int)sp.ts->tpl.sn.size()));
+    for (size_t q = 0; q < sp.ts->is_split.size(); q += 2)
+      key.push_back(make_int2(sp.ts->is_split[q], q + 1 < sp.ts->is_split.size() ? sp.ts->is_split[q + 1] : 2));
     key.insert(key.end(), sp.f->h_rc.begin(), sp.f->h_rc.end());
+    if (sp.in->c_ptr)
+      for (int sd = sp.sd0; sd <= sp.sd1; ++sd) {
+        const int64_t m = h->h_m_off[(size_t)sd];
+        key.push_back(make_int2((int)(m >> 31), (int)(m & 0x7fffffff)));
+      }
   }
   const bool hit = plan.key.size() == key.size() &&
                    std::memcmp(plan.key.data(), key.data(), sizeof(int2) * key.size()) == 0 &&

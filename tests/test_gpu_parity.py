@@ -105,6 +105,8 @@ def test_apply_matches_oracle_and_is_symmetric(cfg2s):
     ("cfg2", dict(weighting="stiffness", objects="cef", variant="v2")),
     ("cfg3", dict(variant="v1")),
     ("cfg3", dict(variant="v2")),
+    ("cfg4", {}),
+    ("cfg4", dict(variant="v2")),
 ])
 def test_pcg_parity(name, kw):
     cfg, o, s, pb = _pair(name, **kw)
@@ -116,28 +118,80 @@ def test_pcg_parity(name, kw):
     assert np.abs(ro - rg).max() <= 1e-8 * ro[0]
     assert np.linalg.norm(x_o - x_g) <= 1e-8 * np.linalg.norm(x_o)
     assert rep_g["lmin"] >= 1 - 1e-6
+    s.close()
 
 
-# Conditioning-limited tier: the preconditioners the
-# paper shows to be non-robust (topological weighting on small cuts; standard
-# objects on cfg3, whose eta ~ 2e-8 cells give Abar diagonals ~3e-21) make the
-# late PCG residuals sensitive to 1-ulp perturbations even inside the CPU
-# restatement. Asserted: convergence, iteration counts within 2% (at least
-# one), solutions within `xtol`, early history within `early` of |b|.
-@pytest.mark.parametrize("name,kw,early,xtol", [
-    ("cfg2", dict(weighting="topological", objects="ce"), 1e-6, 1e-4),   # cond 3e5, ~116 iterations
-    ("cfg2", dict(weighting="topological", objects="cef"), 1e-6, 1e-6),
-    ("cfg3", {}, 1e-6, 1e-5),
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _hist(a, b, b0):
+    n = min(len(a), len(b))
+    return float(np.abs(a[:n] - b[:n]).max() / b0)
+
+
+# Sensitivity tier. For these preconditioners (topological weighting on small
+# cuts; standard objects on cfg3, whose eta ~ 2e-8 cells give Abar diagonals
+# ~3e-21) the PCG trajectory amplifies round-off by ~1e12: a 1-ulp change of
+# rho inside the CPU restatement changes one BDDC apply by < 1e-16 relative
+# but moves the residual history by 1e-5..1e-4 |b|, the solution by 2e-8 and
+# (cfg2 topological ce) the iteration count (tests/test_oracle_sensitivity.py
+# proves this on the CPU). No two implementations whose operations round
+# differently can meet the 1e-8 trajectory bar there, so:
+#   * every operator the PCG uses is compared directly at machine precision
+#     (one BDDC apply on seeded r and on b: 1e-13; coarse matrix: 1e-11);
+#   * the GPU trajectory must lie inside the oracle's own rounding envelope:
+#     the spread of the oracle under 1-ulp rho changes and other ND orders
+#     (iterations within the envelope +-1, history / solution deviation at
+#     most 10x the envelope's).
+PERTURB = [{"ORACLE_RHO_ULPS": "1"}, {"ORACLE_RHO_ULPS": "-1"}, {"ORACLE_ND_LEAF": "8"}, {"ORACLE_ND_LEAF": "64"}]
+
+
+def _oracle_with(cfg, env):
+    for k in ("ORACLE_RHO_ULPS", "ORACLE_ND_LEAF"):
+        os.environ.pop(k, None)
+    os.environ.update(env)
+    try:
+        o = Oracle(cfg)
+        o.setup()
+        return o, o.pcg()
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("cfg2", dict(weighting="topological", objects="ce")),   # cond 3e5, ~116 iterations
+    ("cfg2", dict(weighting="topological", objects="cef")),
+    ("cfg3", {}),                                            # BASELINE.json configs[2] as written
 ])
-def test_pcg_parity_conditioning_limited(name, kw, early, xtol):
+def test_pcg_parity_sensitivity(name, kw):
     cfg, o, s, pb = _pair(name, **kw)
+    r = np.random.default_rng(5).uniform(-1, 1, o.n_dof)
+    assert _rel(s.apply(r), o.apply(r)) <= 1e-13
+    assert _rel(s.coarse_matrix(), o.coarse_matrix()) <= 1e-11
+    b = o.rhs()
+    zb = o.apply(b)
     x_o, rep_o = o.pcg()
+    b0 = rep_o["residuals"][0]
+    its, hist_env, x_env, zb_env = [rep_o["iterations"]], 0.0, 0.0, 0.0
+    for env in PERTURB:
+        op, (x_p, rep_p) = _oracle_with(cfg, env)
+        assert rep_p["converged"]
+        its.append(rep_p["iterations"])
+        hist_env = max(hist_env, _hist(rep_p["residuals"], rep_o["residuals"], b0))
+        x_env = max(x_env, _rel(x_p, x_o))
+        zb_env = max(zb_env, _rel(op.apply(b), zb))
+    # M b (b has entries ~1e-17 at the small-cut dofs) is itself round-off
+    # sensitive on cfg3: bounded by the oracle's own spread
+    assert _rel(s.apply(b), zb) <= max(1e-13, 10 * zb_env)
     x_g, rep_g = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
-    assert rep_g["converged"] and rep_o["converged"]
-    assert abs(rep_g["iterations"] - rep_o["iterations"]) <= max(1, round(0.02 * rep_o["iterations"]))
-    ro, rg = rep_o["residuals"], rep_g["residuals"]
-    assert np.abs(ro[:10] - rg[:10]).max() <= early * ro[0]
-    assert np.linalg.norm(x_o - x_g) <= xtol * np.linalg.norm(x_o)
+    assert rep_g["converged"]
+    assert min(its) - 1 <= rep_g["iterations"] <= max(its) + 1, (rep_g["iterations"], its)
+    assert _hist(rep_g["residuals"], rep_o["residuals"], b0) <= 10 * hist_env
+    assert _rel(x_g, x_o) <= 10 * x_env
+    assert rep_g["lmin"] >= 1 - 1e-6
+    s.close()
 
 
 def test_pcg_deterministic(cfg2s):
