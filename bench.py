@@ -9,12 +9,27 @@ Neumann factorisations, coarse basis, coarse matrix) and PCG to rtol 1e-6.
 
   value  = n_dof / (T_assembly + T_setup + T_pcg), device-timed (CUDA events on
            the handle's stream), mesh + partition + objects already resident.
+           Every timed step rebuilds the factorisation task list
+           (CUTBDDC_NO_PLAN_CACHE=1): nothing computed for one step's
+           geometry is reused by the next except allocations and the ND
+           templates (functions of the block size only). "warm" repeats the
+           measurement with the task-list cache on (the repeated-solve case).
   e2e    = the same metric through the C ABI with HOST buffers: the mesh view
-           (phi, classes, dof map) and coarse objects are uploaded inside the
-           timed region, the solution is read back, host object classification
-           included.
+           (phi, classes, dof map) uploaded, objects classified, setup, PCG,
+           the solution read back; wall clock, median of 5, plan cache off.
+           "e2e_fresh_handle" adds creating the handle (stream, every device
+           allocation) to each solve.
+  roofline       = the dominant PCG kernel family (triangular-solve sweeps),
+                   HBM-bound; roofline_fp64 = the numeric factorisation
+                   (k_dense_dag) against the FP64 tensor (DMMA) peak measured
+                   in the same run by a committed microbenchmark (peak.cu).
+  cfg5   = BASELINE.json configs[4] (256^3, ~2.9M dofs) on the same GPU: the
+           only L2-busting config, where the sweep HBM fraction is the
+           kernels' own streaming efficiency.
   --impl reference: the CPU restatement of the reference (oracle/, the
            reference itself cannot be built: no Eigen) on the host cores.
+  --gpus N without an external launcher re-launches itself under
+           torch.distributed.run with N ranks (one per GPU).
 
 The factor panels (~2-3 GB for cfg4) exceed the 126 MB L2, so no explicit L2
 flush is needed between steps (config.l2 = "inputs larger than L2").
@@ -168,6 +183,82 @@ def _config(cfg, args):
             "l2": "inputs larger than L2 (factor panels > 126 MB)"}
 
 
+def _relaunch(args) -> int:
+    """--gpus N > 1 without torchrun: run this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def _max_over_ranks(v: float, world: int) -> float:
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _time_steps(step, steps):
+    reps = []
+    for _ in range(steps):
+        reps.append(step())
+    tot = sum(r["t_assembly"] + r["t_setup"] + r["t_pcg"] for r in reps)
+    return max(tot, 1e-12), reps
+
+
+def _phases(reps):
+    return {"assembly": 1e3 * float(np.mean([r["t_assembly"] for r in reps])),
+            "setup": 1e3 * float(np.mean([r["t_setup"] for r in reps])),
+            "pcg": 1e3 * float(np.mean([r["t_pcg"] for r in reps]))}
+
+
+def _sweep_roofline(solver, hbm, peak_source):
+    rf = solver.roofline()
+    achieved = rf["bytes"] / rf["seconds"] / 1e9 if rf["seconds"] > 0 else 0.0
+    return {"bound": "hbm", "kernel": rf["kernel"], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "bytes_per_launch": rf["bytes"],
+            "launch_ms": 1e3 * rf["seconds"], "peak_source": peak_source}
+
+
+def _fp64_roofline(solver, peak):
+    ft = solver.factor_timing()
+    flops = ft["flops_cholesky"] + ft["flops_inverse"]
+    achieved = flops / ft["seconds"] / 1e12 if ft["seconds"] > 0 else 0.0
+    return {"bound": "tensor", "kernel": ft["kernel"], "achieved": achieved, "peak": peak["dmma_tflops"],
+            "unit": "TFLOP/s", "frac": achieved / peak["dmma_tflops"], "traffic": None,
+            "flops_per_launch": flops, "flops_cholesky": ft["flops_cholesky"], "flops_inverse_panels": ft["flops_inverse"],
+            "launch_ms": 1e3 * ft["seconds"],
+            "peak_source": "measured in this run: mma.sync.m8n8k4.f64 (DMMA.8x8x4) chains, peak.cu",
+            "dfma_tflops": peak["dfma_tflops"]}
+
+
+def _cfg5_leg(cb, args, hbm, peak_source, local):
+    """BASELINE.json configs[4] on this GPU: one warm-up + 2 timed solves."""
+    cfg = configs.get("cfg5")
+    solver = cb.GpuSolver(local)
+    pb = cb.prepare(solver, cfg)
+
+    def step():
+        solver.assemble(cfg.block, pb.block_ids)
+        solver.setup_bddc(pb.objects, cfg.weighting)
+        return solver.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)[1]
+    step()
+    tot, reps = _time_steps(step, 2)
+    out = {"workload": f"cfg5-{cfg.cells}^3 (BASELINE.json configs[4], stiffness, cef)", "n_dof": pb.mesh.n_dof,
+           "n_sd": len(pb.block_ids), "n_coarse": len(pb.objects), "iterations": reps[-1]["iterations"],
+           "value": pb.mesh.n_dof * len(reps) / tot, "unit": "DOF/s", "steps": len(reps), "warmup": 1,
+           "phases_ms": _phases(reps), "roofline": _sweep_roofline(solver, hbm, peak_source)}
+    solver.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -177,8 +268,13 @@ def main():
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--variant", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 sub-measurement")
     args = ap.parse_args()
     rank, world, local = _env_rank()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _relaunch(args)
+    if world != max(1, args.gpus):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     cfg = configs.get(args.workload, gpus=max(1, args.gpus) if args.workload == "cfg4" else 1,
                       variant=args.variant)
     if args.impl == "reference":
@@ -204,30 +300,42 @@ def main():
     mesh, block_ids, objs = pb.mesh, pb.block_ids, pb.objects
     n_dof = mesh.n_dof
 
-    def assemble(mesh_view=None):
-        d = solver.assemble(cfg.block, asm_ids, mesh=mesh_view)
+    def assemble(s, mesh_view=None):
+        d = s.assemble(cfg.block, asm_ids, mesh=mesh_view)
         if lp is not None:
-            solver.set_global_ids(len(block_ids), lp.local_sd)
+            s.set_global_ids(len(block_ids), lp.local_sd)
         return d
 
     def step_device():
-        assemble()                                      # mesh resident on the device
+        assemble(solver)                                # mesh resident on the device
         solver.setup_bddc(objs, cfg.weighting)
         x, rep = solver.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
         return rep
 
+    def solve_e2e(s):
+        dirichlet = assemble(s, mesh)                                  # H2D of the mesh view
+        if cfg.variant == configs.V_STANDARD:                         # objects on the device
+            o2 = s.classify_objects(cfg.objects, cfg.variant)
+        else:                                                          # v1/v2 edge splits: host
+            diag = s.local_diagonals() if cfg.variant == configs.V2 else None
+            o2 = cb.classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, diag)
+        s.setup_bddc(o2, cfg.weighting)
+        return s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)             # D2H of x
+
     def step_e2e():
         t0 = time.perf_counter()
-        dirichlet = assemble(mesh)                                     # H2D of the mesh view
-        if cfg.variant == configs.V_STANDARD:                         # objects on the device
-            o2 = solver.classify_objects(cfg.objects, cfg.variant)
-        else:                                                          # v1/v2 edge splits: host
-            diag = solver.local_diagonals() if cfg.variant == configs.V2 else None
-            o2 = cb.classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, diag)
-        solver.setup_bddc(o2, cfg.weighting)
-        x, rep = solver.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)     # D2H of x
-        return time.perf_counter() - t0, rep
+        solve_e2e(solver)
+        return time.perf_counter() - t0
 
+    def step_e2e_fresh():  # one GPU only (a fresh NCCL communicator per solve is not measured)
+        t0 = time.perf_counter()
+        s = cb.GpuSolver(local)
+        s.n_dof = n_dof
+        solve_e2e(s)
+        s.close()
+        return time.perf_counter() - t0
+
+    os.environ["CUTBDDC_NO_PLAN_CACHE"] = "1"          # cold task list in every timed step
     for _ in range(args.warmup):
         rep = step_device()
     if world > 1:
@@ -235,55 +343,58 @@ def main():
     launches0 = solver.stats()["launches"]
     sampler = ClockSampler(local)
     sampler.start()
-    dev_times, reps = [], []
-    for _ in range(args.steps):
-        rep = step_device()
-        dev_times.append(rep["t_assembly"] + rep["t_setup"] + rep["t_pcg"])
-        reps.append(rep)
+    tot, reps = _time_steps(step_device, args.steps)
     clocks = sampler.stop()
     launches = (solver.stats()["launches"] - launches0) / args.steps
-    tot = max(sum(dev_times), 1e-12)
-    if world > 1:
-        import torch
-        t = torch.tensor([tot], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot = float(t.item())
-    # one global problem per step, solved cooperatively by all ranks
-    value = n_dof * args.steps / tot
+    tot = _max_over_ranks(tot, world)
+    value = n_dof * args.steps / tot                     # one global problem per step, solved by all ranks
 
-    # e2e through the C ABI with host buffers
-    for _ in range(1):
-        step_e2e()
-    # median of 5 wall-clock solves: one host hiccup (GC, page faults) in a
-    # ~20 ms solve must not decide the number
-    e2e_t = sorted(step_e2e()[0] for _ in range(5))
-    e2e_mean = e2e_t[len(e2e_t) // 2]
-    if world > 1:
-        import torch
-        t = torch.tensor([e2e_mean], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_mean = float(t.item())
-    e2e = n_dof / e2e_mean
+    # numeric factorisation vs the FP64 tensor peak (last timed step's setup)
+    peaks_fp64 = cb.fp64_peak(local)
+    roof64 = _fp64_roofline(solver, peaks_fp64)
+
+    # the same steps with the task-list cache on (repeated solves of one geometry)
+    os.environ.pop("CUTBDDC_NO_PLAN_CACHE", None)
+    step_device()
+    wtot, wreps = _time_steps(step_device, args.steps)
+    wtot = _max_over_ranks(wtot, world)
+    os.environ["CUTBDDC_NO_PLAN_CACHE"] = "1"
+
+    # e2e through the C ABI with host buffers: median of 5 wall-clock solves
+    # (one host hiccup in a ~15 ms solve must not decide the number)
+    step_e2e()
+    e2e_t = sorted(step_e2e() for _ in range(5))
+    e2e_med = _max_over_ranks(e2e_t[len(e2e_t) // 2], world)
+    e2e = n_dof / e2e_med
+    fresh = None
+    if world == 1:
+        step_e2e_fresh()
+        ft = sorted(step_e2e_fresh() for _ in range(3))
+        fresh = {"value": n_dof / ft[1], "unit": "DOF/s", "stat": "median of 3 solves, each on a new handle",
+                 "samples_ms": [round(1e3 * t, 3) for t in ft]}
     n = cfg.cells
-    h2d = (n + 1) ** 3 * (8 + 4) + n ** 3 + 8 * len(block_ids) + objs.dofs.nbytes + objs.neigh.nbytes + \
-        objs.kinds.nbytes + objs.dof_ptr.nbytes + objs.neigh_ptr.nbytes
-    d2h = 8 * n_dof + n_dof  # solution + dirichlet mask
+    obj_bytes = objs.dofs.nbytes + objs.neigh.nbytes + objs.kinds.nbytes + objs.dof_ptr.nbytes + objs.neigh_ptr.nbytes
+    h2d = (n + 1) ** 3 * (8 + 4) + n ** 3 + 8 * len(block_ids) + obj_bytes  # mesh view, partition, coarse view
+    d2h = 8 * n_dof + n_dof + obj_bytes  # solution, dirichlet mask, device-classified objects
 
-    # roofline of the dominant kernel family (triangular solves), timed live
-    rf = solver.roofline()
+    # roofline of the dominant PCG kernel family (triangular solves), timed live
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
-    achieved = rf["bytes"] / rf["seconds"] / 1e9 if rf["seconds"] > 0 else 0.0
-    roof = {"bound": "hbm", "kernel": rf["kernel"], "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "bytes_per_launch": rf["bytes"],
-            "launch_ms": 1e3 * rf["seconds"], "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"
-            if peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+    peak_source = ("MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6.65 TB/s (B200_PROFILING.md)")
+    roof = _sweep_roofline(solver, hbm, peak_source)
     # roofline.traffic: DRAM bytes of the same 7 sweep launches of one apply
     # from the committed ncu --set full capture (tools/ncu_traffic.py)
-    tj = os.path.join(ROOT, "profiles", "r01_sweep_traffic_cfg4.json")
-    if os.path.exists(tj) and world == 1 and cfg.name == "cfg4" and cfg.cells == 64:
-        roof["traffic"] = json.load(open(tj))["traffic_bytes_per_apply"]
-        roof["traffic_source"] = "profiles/r01_sweep_traffic_cfg4.json (ncu --set full, dram read+write)"
+    for tname in ("r02_sweep_traffic_cfg4.json", "r01_sweep_traffic_cfg4.json"):
+        tj = os.path.join(ROOT, "profiles", tname)
+        if os.path.exists(tj) and world == 1 and cfg.name == "cfg4" and cfg.cells == 64:
+            roof["traffic"] = json.load(open(tj))["traffic_bytes_per_apply"]
+            roof["traffic_source"] = f"profiles/{tname} (ncu --set full, dram read+write)"
+            break
+    solver.close()
+
+    cfg5 = None
+    if world == 1 and not args.no_cfg5 and cfg.name == "cfg4":
+        cfg5 = _cfg5_leg(cb, args, hbm, peak_source, local)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -301,17 +412,18 @@ def main():
             "data": f"synthetic (seeded ball-union geometry, BASELINE.json configs[{int(cfg.name[3:]) - 1}])",
             "config": _config(cfg, args),
             "n_dof": n_dof, "iterations": r0["iterations"], "cond_estimate": r0["cond"],
-            "phases_ms": {"assembly": 1e3 * np.mean([r["t_assembly"] for r in reps]),
-                          "setup": 1e3 * np.mean([r["t_setup"] for r in reps]),
-                          "pcg": 1e3 * np.mean([r["t_pcg"] for r in reps])},
+            "phases_ms": _phases(reps),
             "pcg_dofs_per_s": n_dof / np.mean([r["t_pcg"] for r in reps]),
-            "roofline": roof, "cpu_baseline": cpu,
+            "timing": "every step rebuilds the factorisation task list (CUTBDDC_NO_PLAN_CACHE=1)",
+            "warm": {"value": n_dof * args.steps / wtot, "unit": "DOF/s", "phases_ms": _phases(wreps),
+                     "timing": "task-list cache on (repeated solves of one geometry)"},
+            "roofline": roof, "roofline_fp64": roof64, "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "DOF/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "stat": "median of 5 solves", "samples_ms": [round(1e3 * t, 3) for t in e2e_t]},
+            "e2e_fresh_handle": fresh, "cfg5": cfg5,
             "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    solver.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -172,6 +172,16 @@ cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
  * their algorithmic bytes (panel lower parts + front vectors). */
 cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds, double* bytes);
 
+/* Measurement hook: device time of the numeric factorisation launch(es)
+ * (k_dense_dag) of the last setup, its partial-Cholesky flops
+ * (sum over fronts of c^3/3 + (r-c)c^2 + (r-c)^2 c; the reference op is
+ * SparseCholesky's factorisation, linalg.cpp:38-56) and the flops of the
+ * explicit inverse panels the sweeps use (c^3/3 + (r-c)c^2). */
+cutbddc_status cutbddc_gpu_time_factor(cutbddc_gpu* h, double* seconds, double* flops_cholesky, double* flops_inverse);
+/* FP64 roofline denominators measured on `device`: mma.sync m8n8k4 f64
+ * (DMMA) and DFMA throughput, TFLOP/s. */
+cutbddc_status cutbddc_fp64_peak(int device, double* dmma_tflops, double* dfma_tflops);
+
 /* Host-side partition and interface objects (the caller side of the
  * boundary; reference ops build_partition SPEC.md:295-303, classify_objects
  * :304-312, split_edges_v1 :313-321, split_edges_v2 :322-330). The result is

@@ -93,6 +93,7 @@ void cutbddc_gpu_destroy(cutbddc_gpu* h) {
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->prof.dump();
+  for (cudaEvent_t e : h->dag_ev) cudaEventDestroy(e);
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -381,6 +382,28 @@ cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds
     *seconds = tm.stop() / reps;
     *bytes = 2.0 * sweep_bytes(h->fI) + (h->has_K ? sweep_bytes(h->fK) : 0.0);
   });
+}
+
+cutbddc_status cutbddc_gpu_time_factor(cutbddc_gpu* h, double* seconds, double* flops_cholesky, double* flops_inverse) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
+    double t = 0.0;
+    for (size_t k = 0; k + 1 < h->dag_ev.size(); k += 2) {
+      CB_CUDA(cudaEventSynchronize(h->dag_ev[k + 1]));
+      float ms = 0.f;
+      CB_CUDA(cudaEventElapsedTime(&ms, h->dag_ev[k], h->dag_ev[k + 1]));
+      t += ms * 1e-3;
+    }
+    *seconds = t;
+    *flops_cholesky = h->fI.flops + (h->has_K ? h->fK.flops : 0.0);
+    *flops_inverse = h->fI.flops_inv + (h->has_K ? h->fK.flops_inv : 0.0);
+  });
+}
+
+cutbddc_status cutbddc_fp64_peak(int device, double* dmma_tflops, double* dfma_tflops) {
+  return guard([&] { fp64_peaks(device, dmma_tflops, dfma_tflops); });
 }
 
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {

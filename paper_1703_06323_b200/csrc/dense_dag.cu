@@ -674,8 +674,18 @@ void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, const std::vector<
     grid = std::max(1, per_sm) * sms;
   }
   ProfScope ps(h->prof, s, "dense dag kernel");
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (&plan == &h->dag_factor) {  // device time of the factorisation launches (cutbddc_gpu_time_factor)
+    for (cudaEvent_t& e : ev) CB_CUDA(cudaEventCreate(&e));
+    CB_CUDA(cudaEventRecord(ev[0], s));
+  }
   k_dense_dag<<<std::min<int>(grid, plan.n_tasks), kDagThreads, shm, s>>>(a);
   CB_LAUNCH();
+  if (ev[0]) {
+    CB_CUDA(cudaEventRecord(ev[1], s));
+    h->dag_ev.push_back(ev[0]);
+    h->dag_ev.push_back(ev[1]);
+  }
   ps.close();
   if (trace_prefix && host_tasks) {  // same layout as the sweep traces (tools/trace_analyze.py)
     static int seq = 0;

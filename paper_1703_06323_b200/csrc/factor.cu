@@ -421,7 +421,7 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
   std::vector<int64_t> poff((size_t)nsd * nsn), uoff((size_t)nsd * nsn), foff((size_t)nsd * nsn);
   f.h_front_base.assign((size_t)nsd + 1, 0);
   int64_t pt = 0, ut = 0;
-  double bytes = 0, flops = 0;
+  double bytes = 0, flops = 0, flops_inv = 0;
   for (int sd = 0; sd < nsd; ++sd) {
     int64_t fo = 0;
     for (int q = 0; q < nsn; ++q) {
@@ -435,6 +435,7 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
       fo += (int64_t)v.x * v.x;
       bytes += 2.0 * 8.0 * (r * c - c * (c - 1) / 2.0) + 2.0 * 2.0 * 8.0 * r;
       flops += c * c * c / 3.0 + (r - c) * c * c + (r - c) * (r - c) * c;
+      flops_inv += c * c * c / 3.0 + (r - c) * c * c;
     }
     f.h_front_base[(size_t)sd + 1] = f.h_front_base[(size_t)sd] + fo;
   }
@@ -442,6 +443,7 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
   f.upd_total = ut;
   f.bytes_per_sweep = bytes;
   f.flops = flops;
+  f.flops_inv = flops_inv;
   f.panel_off.upload(poff, s);
   f.h_panel_off = poff;
   f.h_front_off = foff;
@@ -462,6 +464,8 @@ void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs) {
   fail.alloc(jobs.size());
   CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8 * jobs.size(), s));
   DevBuf<double>& front = h->ws_front;
+  for (cudaEvent_t e : h->dag_ev) cudaEventDestroy(e);
+  h->dag_ev.clear();
   ProfScope pnum(h->prof, s, "factor numeric");
   int64_t all = 0;
   for (const FactorJob& j : jobs) all += j.f->h_front_base[(size_t)nsd];

@@ -96,5 +96,7 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
 // dense_dag.cu: Cholesky (A, column-major lower, overwritten) and X = L^{-1}
 // of one dense SPD matrix; a failing pivot index goes to *fail
 void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long long* fail);
+// peak.cu: FP64 tensor (DMMA) and FP64 FMA throughput microbenchmarks, TFLOP/s
+void fp64_peaks(int device, double* dmma_tflops, double* dfma_tflops);
 
 }  // namespace cutbddc_b200

@@ -68,6 +68,7 @@ struct FactorSet {
   int64_t panel_total = 0, upd_total = 0;
   double bytes_per_sweep = 0;                  // algorithmic bytes of fwd + bwd sweeps
   double flops = 0;                            // partial-Cholesky flops
+  double flops_inv = 0;                        // explicit inverse panel G = [L11^{-1}; L21 L11^{-1}] flops
   // dataflow sweeps (sweep.cu): one persistent launch per sweep direction
   cutbddc_b200::DevBuf<int4> desc;             // nsd x nsn front descriptors (6 x int4 each, sweep.cu)
   cutbddc_b200::DevBuf<int32_t> cslot;         // vec_total: slot of each compact front row
@@ -199,6 +200,7 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp, ws_obj;
   cutbddc_b200::DevBuf<int> ws_flag;
   DagPlan dag_factor;                              // dense_dag.cu: the subdomain factorisations (one launch)
+  std::vector<cudaEvent_t> dag_ev;                 // start/stop event pairs of the last numeric factorisation's launches
   DagPlan dag_dense;                               // dense_dag.cu: the coarse matrix factorisation
 
   // pcg vectors

@@ -75,7 +75,8 @@ EXPORTS = [
     "cutbddc_gpu_apply_bddc", "cutbddc_gpu_rhs", "cutbddc_gpu_coarse_matrix", "cutbddc_gpu_cells", "cutbddc_gpu_stats",
     "cutbddc_gpu_cut_elements", "cutbddc_gpu_local_system", "cutbddc_gpu_local_solve", "cutbddc_gpu_time_solves",
     "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free", "cutbddc_gpu_classify_objects",
-    "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_global_ids",
+    "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_global_ids", "cutbddc_gpu_time_factor",
+    "cutbddc_fp64_peak",
 ]
 
 
@@ -194,6 +195,13 @@ def assign_subdomains(block: int, block_ids: np.ndarray, cells: int, world: int,
     cp = _p(np.ascontiguousarray(cost, np.float64), C.c_double) if cost is not None else None
     _check(lib().cutbddc_assign_subdomains(C.byref(pv), cells, world, cp, _p(out, C.c_int32)))
     return out
+
+
+def fp64_peak(device: int = 0) -> dict:
+    """Measured FP64 throughput (TFLOP/s): DMMA (mma.sync m8n8k4 f64) and DFMA."""
+    a, b = C.c_double(), C.c_double()
+    _check(lib().cutbddc_fp64_peak(device, C.byref(a), C.byref(b)))
+    return dict(dmma_tflops=a.value, dfma_tflops=b.value)
 
 
 def nccl_unique_id() -> bytes:
@@ -362,6 +370,14 @@ class GpuSolver:
         _check(lib().cutbddc_gpu_time_solves(self.h, reps, C.byref(sec), C.byref(byt)))
         return dict(kernel="k_sweep_fwd+k_sweep_bwd (3 triangular solves of one BDDC apply)",
                     seconds=sec.value, bytes=byt.value)
+
+    def factor_timing(self):
+        """Device time of the last setup's numeric factorisation launch(es)
+        and its flops (partial Cholesky; explicit inverse panels)."""
+        sec, fc, fi = C.c_double(), C.c_double(), C.c_double()
+        _check(lib().cutbddc_gpu_time_factor(self.h, C.byref(sec), C.byref(fc), C.byref(fi)))
+        return dict(kernel="k_dense_dag (numeric factorisation of every front, one launch)", seconds=sec.value,
+                    flops_cholesky=fc.value, flops_inverse=fi.value)
 
     def stats(self):
         st = np.zeros(16, np.int64)
