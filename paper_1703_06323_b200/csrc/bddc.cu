@@ -965,11 +965,12 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
                                          h->sinv.p, h->cy.p, h->gl.p, skip);
       CB_LAUNCH();
       const size_t shm = sizeof(double) * ((size_t)h->n_coarse + 2 * kFusedCoarseM);
-      static size_t shm_set = 0;
-      if (shm > 48 * 1024 && shm > shm_set) {
-        CB_CUDA(cudaFuncSetAttribute(k_coarse_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        shm_set = shm;
-      }
+      if (shm > 48 * 1024)  // opt in once per device, to the largest size this kernel can ever need
+        device_memo(kMemoCoarseOutShm, [] {
+          CB_CUDA(cudaFuncSetAttribute(k_coarse_out, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * (kCoarseInverseMax + 2 * kFusedCoarseM))));
+          return 1ll;
+        });
       k_coarse_out<<<dim3(h->nsd, cr_blocks), 256, shm, s>>>(
           h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->acoarse_full.p, h->coarse_id.p, h->m_off.p, h->ac_off.p,
           h->sinv.p, h->cy.p, h->root_info.p, h->fK.cslot.p, h->wroot.p, h->sv1.p, skip);

@@ -663,16 +663,15 @@ void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, const std::vector<
   for (size_t g = 0; g < groups.size(); ++g) a.g[g] = groups[g];
   a.trace = trace_prefix ? trace.p : nullptr;
   const size_t shm = sizeof(double) * 2 * kTile * (kTile + 1);
-  static int grid = 0;
-  if (!grid) {
+  const int grid = (int)device_memo(kMemoDagGrid, [&] {
     CB_CUDA(cudaFuncSetAttribute(k_dense_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     int per_sm = 0, dev = 0, sms = 0;
     CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_dag, kDagThreads, shm));
     CB_CUDA(cudaGetDevice(&dev));
     CB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (const char* e = std::getenv("CUTBDDC_DAG_CTAS_PER_SM")) per_sm = std::min(per_sm, std::atoi(e));  // A/B runs
-    grid = std::max(1, per_sm) * sms;
-  }
+    return (long long)std::max(1, per_sm) * sms;
+  });
   ProfScope ps(h->prof, s, "dense dag kernel");
   cudaEvent_t ev[2] = {nullptr, nullptr};
   if (&plan == &h->dag_factor) {  // device time of the factorisation launches (cutbddc_gpu_time_factor)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -71,6 +72,29 @@ struct DevBuf {
     return v;
   }
 };
+
+// Per-device, thread-safe memo of launch configuration (occupancy-derived
+// grid sizes, shared-memory opt-ins): kernel attributes are per device, so a
+// value computed (or an attribute set) on one device must not be reused on
+// another. `fn` runs once per (slot, device) under a mutex; later calls on the
+// same device read the stored value. Slots name the call sites.
+enum DeviceMemoSlot { kMemoSweepFwd = 0, kMemoSweepBwd, kMemoSweepAttr, kMemoDagGrid, kMemoCoarseOutShm, kMemoSlots };
+template <typename Fn>
+long long device_memo(int slot, Fn fn) {
+  constexpr int kMaxDev = 64;
+  static std::mutex mu;
+  static long long val[kMemoSlots][kMaxDev];
+  static bool set[kMemoSlots][kMaxDev];
+  int dev = 0;
+  CB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDev) dev = kMaxDev - 1;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!set[slot][dev]) {
+    val[slot][dev] = fn();
+    set[slot][dev] = true;
+  }
+  return val[slot][dev];
+}
 
 inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
 

@@ -448,7 +448,7 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
   f.h_panel_off = poff;
   f.h_front_off = foff;
   f.upd_off.upload(uoff, s);
-  f.panel.alloc((size_t)std::max<int64_t>(1, pt));
+  f.panel.alloc((size_t)pt + 2);  // +2: the sweeps' 16-byte aligned bulk copies may read one double past the end
   build_sweep_plan(h, ts, f, poff, uoff);
 }
 

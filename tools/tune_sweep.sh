@@ -8,7 +8,7 @@ mkdir -p gpurun_out
 run() {
   touch paper_1703_06323_b200/csrc/sweep.cu
   CUTBDDC_NVCC_EXTRA="$1" python -m paper_1703_06323_b200.build > /dev/null || { echo "$1 BUILD FAILED" >> $out; return; }
-  timeout 300 python bench.py --no-cpu-baseline --steps 10 --warmup 3 2> /dev/null | python -c "
+  timeout 300 python bench.py --no-cpu-baseline --no-cfg5 --workload ${TUNE_WORKLOAD:-cfg4} --steps ${TUNE_STEPS:-10} --warmup 3 2> /dev/null | python -c "
 import json, sys
 l = [x for x in sys.stdin if x.startswith('{')]
 if not l: print('$1', 'NO OUTPUT'); sys.exit()
