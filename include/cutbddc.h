@@ -165,7 +165,9 @@ cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x);
  * [5]=supernodes (Neumann template) [6]=levels [7]=max m_w [8]=n_interface
  * [9]=kernel launches so far (process-wide) [10]/[11]=panel doubles of the
  * interior / Neumann factorisation [12]=partial-Cholesky flops of both
- * [13]=world size [14]=1 if the handle owns an NCCL communicator. */
+ * [13]=world size [14]=1 if the handle owns an NCCL communicator
+ * [15]=1 if the constrained Neumann factor is the corner-augmented
+ * K_c = A + rho C_corner^T C_corner (else K = A + rho C^T C). */
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
 /* Measurement hook: average device time of the triangular-solve sweeps of
  * one BDDC apply (interior, Neumann, interior) over `reps` repetitions, and

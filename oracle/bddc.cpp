@@ -114,7 +114,12 @@ void build_bddc(const Problem& pb, Bddc& bd, int objects, int weighting, int var
     for (int i = 0; i < n; ++i)
       for (int p = S.a.ptr[(size_t)i]; p < S.a.ptr[(size_t)i + 1]; ++p)
         rows[(size_t)i].emplace_back(S.a.col[(size_t)p], S.a.val[(size_t)p]);
+    // ORACLE_K_CORNERS=1: augment with the corner rows only (K_c = A + rho
+    // C_c^T C_c, the GPU's corner formulation; same saddle solutions in exact
+    // arithmetic -- used to compare the GPU's K_c solves factor for factor)
+    const bool corners_only = std::getenv("ORACLE_K_CORNERS") != nullptr;
     for (int r = 0; r < m; ++r)
+      if (!corners_only || bd.coarse_objects[(size_t)L.coarse_ids[(size_t)r]].kind == kCorner)
       for (int p = L.c_ptr[(size_t)r]; p < L.c_ptr[(size_t)r + 1]; ++p)
         for (int q = L.c_ptr[(size_t)r]; q < L.c_ptr[(size_t)r + 1]; ++q) {
           const int i = L.c_col[(size_t)p], j = L.c_col[(size_t)q];

@@ -14,6 +14,8 @@
 //                       r1 := 0 on interior rows.
 // Every gather sums in ascending subdomain order; no fp64 atomics.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "bddc.cuh"
@@ -489,9 +491,11 @@ __global__ void __launch_bounds__(256) k_root_s(const int64_t* __restrict__ rinf
   }
 }
 
-// sinv = sym(S^{-1}); A_c,w = sinv - rho I
+// sinv = sym(S^{-1}); A_c,w = sinv - rho I (K = A + rho C^T C), or
+// sinv - rho I_corner (K_c = A + rho C_corner^T C_corner: corner_row != null)
 __global__ void k_root_coarse(const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
-                              const double* __restrict__ Sinv, const double* __restrict__ rho, double* __restrict__ sinv,
+                              const double* __restrict__ Sinv, const double* __restrict__ rho,
+                              const uint8_t* __restrict__ corner_row, double* __restrict__ sinv,
                               double* __restrict__ ac) {
   const int sd = blockIdx.x;
   const int m = (int)(m_off[sd + 1] - m_off[sd]);
@@ -500,8 +504,112 @@ __global__ void k_root_coarse(const int64_t* __restrict__ m_off, const int64_t* 
     const int a = q / m, b = q % m;
     const double v = 0.5 * (Sinv[o + (int64_t)a * m + b] + Sinv[o + (int64_t)b * m + a]);
     sinv[o + q] = v;
-    ac[o + q] = v - (a == b ? rho[sd] : 0.0);
+    const bool shift = a == b && (!corner_row || corner_row[m_off[sd] + a]);
+    ac[o + q] = v - (shift ? rho[sd] : 0.0);
   }
+}
+
+// ---------------------------------------------------------------- corner formulation
+// K_c = A + rho sum_corners e e^T = L L^T on the plain ND template. The
+// constrained Neumann solve z = K_c^{-1}(r - C^T mu), C z = 0 gives
+//   S = C K_c^{-1} C^T = H^T H,  H = L^{-1} C^T (one multi-RHS forward sweep),
+//   A_c,w = Phi^T A Phi = S^{-1} - rho I_corner,
+//   apply: y' = L^{-1} r_w (forward sweep), cy = C K_c^{-1} r_w = H^T y',
+//   u = S^{-1}(z_c - cy), z~ = L^{-T}(y' + H u) (backward sweep).
+// H is kept over each subdomain's present slots in front-column order.
+
+// right-hand sides C^T e_a, a = pass * 8 + rr, in slot space (X8 zeroed)
+__global__ void k_ct_rhs(int pass, int64_t ns, int T, const int64_t* __restrict__ m_off, const int64_t* __restrict__ c_ptr,
+                         const int32_t* __restrict__ c_slot, const double* __restrict__ c_val, double* __restrict__ X8) {
+  const int sd = blockIdx.x, rr = blockIdx.y;
+  const int64_t a = (int64_t)pass * kSweepMultiRhs + rr;
+  if (a >= m_off[sd + 1] - m_off[sd]) return;
+  const int64_t row = m_off[sd] + a;
+  for (int64_t p = c_ptr[row] + threadIdx.x; p < c_ptr[row + 1]; p += blockDim.x)
+    X8[rr * ns + (int64_t)sd * T + c_slot[p]] = c_val[p];
+}
+
+// H columns a = pass * 8 + rr from the forward sweep's column values, and
+// (pass 0) the slot of every compact position
+__global__ void k_h_compact(int pass, int nsn, int64_t ns, const FrontDesc* __restrict__ desc,
+                            const int32_t* __restrict__ cslot, const int32_t* __restrict__ coff,
+                            const int64_t* __restrict__ m_off, const int64_t* __restrict__ rinfo,
+                            const double* __restrict__ Y8, double* __restrict__ H, int32_t* __restrict__ hslot) {
+  const int sid = blockIdx.x, sd = blockIdx.y;
+  const FrontDesc& d = desc[(int64_t)sd * nsn + sid];
+  const int m = (int)(m_off[sd + 1] - m_off[sd]);
+  const int np = (int)rinfo[4 * sd];
+  const int k0 = coff[(int64_t)sd * nsn + sid];
+  double* hs = H + rinfo[4 * sd + 3];
+  for (int j = threadIdx.x; j < d.c; j += blockDim.x) {
+    const int sl = cslot[d.vo + j];
+    if (pass == 0) hslot[rinfo[4 * sd + 1] + k0 + j] = sl;
+#pragma unroll
+    for (int rr = 0; rr < kSweepMultiRhs; ++rr) {
+      const int a = pass * kSweepMultiRhs + rr;
+      if (a < m) hs[(int64_t)a * np + k0 + j] = Y8[rr * ns + sl];
+    }
+  }
+}
+
+// K_c pivots: every column's pivot L_jj^2 = 1 / G_jj^2 against the original
+// diagonal of K_c at its slot; a pivot below 1e-12 of it (a fragment whose
+// constant mode no corner and no Nitsche boundary controls) sets *bad
+__global__ void k_pivot_check(int nsn, int T, const FrontDesc* __restrict__ desc, const double* __restrict__ panel,
+                              const int32_t* __restrict__ cslot, const double* __restrict__ As,
+                              const double* __restrict__ dadd, int* __restrict__ bad) {
+  const int sid = blockIdx.x, sd = blockIdx.y;
+  const FrontDesc& d = desc[(int64_t)sd * nsn + sid];
+  for (int j = threadIdx.x; j < d.c; j += blockDim.x) {
+    const double g = panel[d.po + (int64_t)j * d.r + j];
+    const double piv = 1.0 / (g * g);
+    const int sl = cslot[d.vo + j];
+    const double orig = As[(int64_t)(sl / T) * 27 * T + 13ll * T + sl % T] + dadd[sl];
+    if (!(piv > 1e-12 * orig)) atomicExch(bad, 1);
+  }
+}
+
+// cy[row] = (H^T y')[row]: warp per constraint row, y' the forward sweep's
+// column values in slot space
+__global__ void k_h_cy(int64_t mtot, const int32_t* __restrict__ row_sd, const int64_t* __restrict__ m_off,
+                       const int64_t* __restrict__ rinfo, const double* __restrict__ H, const int32_t* __restrict__ hslot,
+                       const double* __restrict__ Y, double* __restrict__ cy, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= mtot) return;
+  const int sd = row_sd[row];
+  const int a = (int)(row - m_off[sd]), np = (int)rinfo[4 * sd];
+  const double* hc = H + rinfo[4 * sd + 3] + (int64_t)a * np;
+  const int32_t* hs = hslot + rinfo[4 * sd + 1];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four independent load chains per lane
+  int k = lane;
+  for (; k + 96 < np; k += 128) {
+    s0 += hc[k] * Y[hs[k]];
+    s1 += hc[k + 32] * Y[hs[k + 32]];
+    s2 += hc[k + 64] * Y[hs[k + 64]];
+    s3 += hc[k + 96] * Y[hs[k + 96]];
+  }
+  for (; k < np; k += 32) s0 += hc[k] * Y[hs[k]];
+  const double s = warp_sum((s0 + s1) + (s2 + s3));
+  if (lane == 0) cy[row] = s;
+}
+
+// y'[slot_k] += (H u)[k]: blocks (subdomain, 256 compact positions)
+__global__ void k_h_correct(const int64_t* __restrict__ m_off, const int64_t* __restrict__ rinfo,
+                            const double* __restrict__ H, const int32_t* __restrict__ hslot,
+                            const double* __restrict__ u, double* __restrict__ Y, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int sd = blockIdx.x;
+  const int np = (int)rinfo[4 * sd];
+  const int k = blockIdx.y * blockDim.x + threadIdx.x;
+  if (k >= np) return;
+  const int64_t b0 = m_off[sd];
+  const int m = (int)(m_off[sd + 1] - b0);
+  const double* hc = H + rinfo[4 * sd + 3] + k;
+  double v = 0.0;
+  for (int a = 0; a < m; ++a) v += hc[(int64_t)a * np] * u[b0 + a];
+  Y[hslot[rinfo[4 * sd + 1] + k]] += v;
 }
 
 // W_r = G_r^T H: 64 root rows j per CTA, all m columns (<= 64 per pass),
@@ -597,7 +705,8 @@ __global__ void __launch_bounds__(256) k_coarse_in(int T, const int64_t* __restr
                                                    const double* __restrict__ c_val, const double* __restrict__ Y,
                                                    const int64_t* __restrict__ s_off, const double* __restrict__ sinv,
                                                    double* __restrict__ cy, double* __restrict__ gl,
-                                                   const int* __restrict__ skip) {
+                                                   const int* __restrict__ skip, const int64_t* __restrict__ rinfo,
+                                                   const double* __restrict__ Hc, const int32_t* __restrict__ hslot) {
   if (skip && *skip) return;
   __shared__ double scy[kFusedCoarseM];
   const int sd = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -607,7 +716,14 @@ __global__ void __launch_bounds__(256) k_coarse_in(int T, const int64_t* __restr
   for (int a = wid; a < m; a += blockDim.x >> 5) {
     const int64_t row = b0 + a;
     double v = 0.0;
-    for (int64_t p = c_ptr[row] + lane; p < c_ptr[row + 1]; p += 32) v += c_val[p] * y[c_slot[p]];
+    if (Hc) {  // corner formulation: cy = H^T y' (Y: the forward sweep's column values)
+      const int np = (int)rinfo[4 * sd];
+      const double* hc = Hc + rinfo[4 * sd + 3] + (int64_t)a * np;
+      const int32_t* hs = hslot + rinfo[4 * sd + 1];
+      for (int k = lane; k < np; k += 32) v += hc[k] * Y[hs[k]];
+    } else {
+      for (int64_t p = c_ptr[row] + lane; p < c_ptr[row + 1]; p += 32) v += c_val[p] * y[c_slot[p]];
+    }
     v = warp_sum(v);
     if (lane == 0) scy[a] = cy[row] = v;
   }
@@ -631,7 +747,8 @@ __global__ void __launch_bounds__(256) k_coarse_out(int nc, const int64_t* __res
                                                     const double* __restrict__ sinv, const double* __restrict__ cy,
                                                     const int64_t* __restrict__ rinfo, const int32_t* __restrict__ cslot,
                                                     const double* __restrict__ W, double* __restrict__ X,
-                                                    const int* __restrict__ skip) {
+                                                    const int* __restrict__ skip, const double* __restrict__ Hc,
+                                                    const int32_t* __restrict__ hslot) {
   if (skip && *skip) return;
   extern __shared__ double gc[];  // nc, then zc and u (kFusedCoarseM each)
   double* zl = gc + nc;
@@ -668,6 +785,13 @@ __global__ void __launch_bounds__(256) k_coarse_out(int nc, const int64_t* __res
   const int cr = (int)rinfo[4 * sd];
   const int j = blockIdx.y * blockDim.x + tid;
   if (j >= cr) return;
+  if (Hc) {  // corner formulation: y'[slot_j] += (H u)_j (X: the forward sweep's column values)
+    const double* hc = Hc + rinfo[4 * sd + 3] + j;
+    double v = 0.0;
+    for (int a = 0; a < m; ++a) v += hc[(int64_t)a * cr] * u[a];
+    X[hslot[rinfo[4 * sd + 1] + j]] += v;
+    return;
+  }
   const double* w = W + rinfo[4 * sd + 3] + j;
   double v = 0.0;
   for (int a = 0; a < m; ++a) v += w[(int64_t)a * cr] * u[a];
@@ -677,6 +801,101 @@ __global__ void __launch_bounds__(256) k_coarse_out(int nc, const int64_t* __res
 __global__ void k_row_sd(int nsd, const int64_t* __restrict__ m_off, int32_t* __restrict__ row_sd) {
   const int sd = blockIdx.x;
   for (int64_t r = m_off[sd] + threadIdx.x; r < m_off[sd + 1]; r += blockDim.x) row_sd[r] = sd;
+}
+
+// K_c pivots against the original diagonal (k_pivot_check): false if any is tiny
+bool corner_pivots_ok(cutbddc_gpu* h) {
+  cudaStream_t s = h->stream;
+  const int nsn = (int)h->tI.tpl.sn.size();
+  DevBuf<int>& bad = h->ws_flag;
+  bad.alloc(1);
+  bad.zero(s);
+  k_pivot_check<<<dim3(nsn, h->nsd), 128, 0, s>>>(nsn, h->slots, reinterpret_cast<const FrontDesc*>(h->fK.desc.p),
+                                                   h->fK.panel.p, h->fK.cslot.p, h->As.p, h->diag_add.p, bad.p);
+  CB_LAUNCH();
+  int hb = 0;
+  CB_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  CB_CUDA(cudaStreamSynchronize(s));
+  if (hb && std::getenv("CUTBDDC_K_STATS")) std::fprintf(stderr, "[cutbddc] tiny K_c pivot: shell-root K fallback\n");
+  return hb == 0;
+}
+
+// S^{-1} (symmetrised) of every subdomain's m x m block in place; a
+// non-positive pivot means dependent constraints
+void invert_schur(cutbddc_gpu* h, double* S) {
+  cudaStream_t s = h->stream;
+  DevBuf<unsigned long long>& fail = h->ws_fail;
+  fail.alloc(1);
+  CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
+  const size_t shm = sizeof(double) * ((size_t)h->m_max * h->m_max + h->m_max);
+  if (shm > 48 * 1024)
+    CB_CUDA(cudaFuncSetAttribute(k_small_spd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  k_small_spd_inverse<<<h->nsd, 256, shm, s>>>(h->nsd, h->m_off.p, h->ac_off.p, S, fail.p);
+  CB_LAUNCH();
+  unsigned long long f = 0;
+  CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));
+  CB_CUDA(cudaStreamSynchronize(s));
+  if (f != ~0ull)
+    throw Failure(CUTBDDC_SINGULAR, "saddle: singular constraint Schur complement (subdomain " + std::to_string(f) +
+                                        "); constraints are not independent");
+}
+
+// Coarse basis of the corner formulation: H = L^{-1} C^T by multi-RHS
+// forward sweeps (kSweepMultiRhs constraint rows of every subdomain per
+// pass), S = H^T H, S^{-1}, A_c,w = S^{-1} - rho I_corner.
+void coarse_basis_corner(cutbddc_gpu* h, const std::vector<int64_t>& m_off, const std::vector<int64_t>& s_off) {
+  cudaStream_t s = h->stream;
+  const int nsd = h->nsd, T = h->slots, m_max = h->m_max;
+  const TplSet& ts = h->tI;
+  const FactorSet& f = h->fK;
+  const int nsn = (int)ts.tpl.sn.size();
+  std::vector<int32_t> coff((size_t)nsd * nsn);
+  std::vector<int64_t> rinfo((size_t)4 * nsd);
+  int64_t hs = 0, ht = 0;
+  int np_max = 0;
+  for (int sd = 0; sd < nsd; ++sd) {
+    int k = 0;
+    for (int sid = 0; sid < nsn; ++sid) {
+      coff[(size_t)sd * nsn + sid] = k;
+      k += f.h_rc[(size_t)sd * nsn + sid].y;
+    }
+    const int64_t m = m_off[(size_t)sd + 1] - m_off[(size_t)sd];
+    rinfo[4 * (size_t)sd] = k;
+    rinfo[4 * (size_t)sd + 1] = hs;
+    rinfo[4 * (size_t)sd + 2] = 0;
+    rinfo[4 * (size_t)sd + 3] = ht;
+    hs += k;
+    ht += (int64_t)k * m;
+    np_max = std::max(np_max, k);
+  }
+  h->np_max = np_max;
+  h->root_info.upload(rinfo, s);
+  DevBuf<int32_t>& dcoff = h->ws_coff;
+  dcoff.upload(coff, s);
+  h->hroot.alloc((size_t)std::max<int64_t>(1, ht));
+  h->hslot.alloc((size_t)std::max<int64_t>(1, hs));
+  const int64_t ns = (int64_t)nsd * T;
+  h->ws_x8.alloc((size_t)kSweepMultiRhs * ns);
+  h->ws_y8.alloc((size_t)kSweepMultiRhs * ns);
+  h->ws_u8.alloc((size_t)kSweepMultiRhs * std::max<int64_t>(1, f.upd_total));
+  h->ws_v8.alloc((size_t)kSweepMultiRhs * std::max<size_t>(1, f.vbuf.n));
+  for (int pass = 0; pass * kSweepMultiRhs < m_max; ++pass) {
+    h->ws_x8.zero(s);
+    k_ct_rhs<<<dim3(nsd, kSweepMultiRhs), 128, 0, s>>>(pass, ns, T, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
+                                                        h->ws_x8.p);
+    CB_LAUNCH();
+    sweep_forward_multi(h, ts, f, h->ws_x8.p, h->ws_y8.p, h->ws_u8.p, h->ws_v8.p);
+    k_h_compact<<<dim3(nsn, nsd), 128, 0, s>>>(pass, nsn, ns, reinterpret_cast<const FrontDesc*>(f.desc.p), f.cslot.p,
+                                              dcoff.p, h->m_off.p, h->root_info.p, h->ws_y8.p, h->hroot.p, h->hslot.p);
+    CB_LAUNCH();
+  }
+  DevBuf<double>& S = h->ws_s;
+  S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
+  k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
+  CB_LAUNCH();
+  invert_schur(h, S.p);
+  k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, h->corner_row.p, h->sinv.p, h->ac_loc.p);
+  CB_LAUNCH();
 }
 
 }  // namespace
@@ -814,22 +1033,47 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   // out of the apply ("preconditioner reduces to exact interior solve").
   h->has_K = h->n_if > 0;
   h->fK.upd_total = 0;
+  // K: corner-augmented K_c = A + rho sum_corners e e^T on the plain ND
+  // template (no rho C^T C rows: fk_c has no constraint rows), else the full
+  // K = A + rho C^T C on the shell-root template (PEN rows of the root).
+  static const bool force_shell = [] {
+    const char* e = std::getenv("CUTBDDC_K_SHELL");
+    return e && e[0] == '1';
+  }();
+  h->k_corner = !force_shell && m_max > 0;
   FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
                  h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
+  FactorInput fk_c{h->As.p, h->mask_all.p, h->diag_add.p, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  static const char* kSaddleMsg = "saddle: singular augmented system; constraints do not control the operator kernel";
+  bool k_failed = false;
   if (h->has_K) {
-    if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
-    factor_symbolic(h, h->tK, fk, h->fK);
-    jobs.push_back(FactorJob{&h->tK, &fk, &h->fK,
-                             "saddle: singular augmented system; constraints do not control the operator kernel"});
+    if (h->k_corner) {
+      factor_symbolic(h, h->tI, fk_c, h->fK);
+      jobs.push_back(FactorJob{&h->tI, &fk_c, &h->fK, kSaddleMsg, &k_failed});
+    } else {
+      if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
+      factor_symbolic(h, h->tK, fk, h->fK);
+      jobs.push_back(FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg});
+    }
   }
   factor_numeric(h, jobs);
+  if (h->has_K && h->k_corner && (k_failed || !corner_pivots_ok(h))) {
+    // a floating fragment (no corner, no Nitsche boundary) leaves K_c
+    // singular: the full augmented K on the shell-root template instead
+    h->k_corner = false;
+    if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
+    factor_symbolic(h, h->tK, fk, h->fK);
+    factor_numeric(h, {FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg}});
+  }
   const int64_t upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, h->fK.upd_total));
   // ---- coarse basis in the root space of K (see k_root_h): H, S, S^{-1},
   // W_r and A_c,w = S^{-1} - rho I; the apply never forms Phi
   h->ac_loc.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
   h->sinv.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
   ps_host.next("setup 2 root-space coarse basis");
-  if (m_max > 0) {
+  if (m_max > 0 && h->k_corner) {
+    coarse_basis_corner(h, m_off, s_off);
+  } else if (m_max > 0) {
     if (!h->has_K) throw Failure(CUTBDDC_INTERNAL, "coarse space without an interface");
     const int nsn = (int)h->tK.tpl.sn.size(), root = nsn - 1;
     std::vector<int64_t> rinfo((size_t)4 * nsd);
@@ -862,21 +1106,8 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     k_root_w<<<dim3(nsd, (cr_max + 63) / 64), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.panel.p, h->hroot.p,
                                                           h->wroot.p);
     CB_LAUNCH();
-    DevBuf<unsigned long long>& fail = h->ws_fail;
-    fail.alloc(1);
-    CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
-    const size_t shm = sizeof(double) * ((size_t)m_max * m_max + m_max);
-    if (shm > 48 * 1024)
-      CB_CUDA(cudaFuncSetAttribute(k_small_spd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_small_spd_inverse<<<nsd, 256, shm, s>>>(nsd, h->m_off.p, h->ac_off.p, S.p, fail.p);
-    CB_LAUNCH();
-    unsigned long long f = 0;
-    CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));
-    CB_CUDA(cudaStreamSynchronize(s));
-    if (f != ~0ull)
-      throw Failure(CUTBDDC_SINGULAR, "saddle: singular constraint Schur complement (subdomain " + std::to_string(f) +
-                                          "); constraints are not independent");
-    k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, h->sinv.p, h->ac_loc.p);
+    invert_schur(h, S.p);
+    k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, nullptr, h->sinv.p, h->ac_loc.p);
     CB_LAUNCH();
   }
   // ---- coarse matrix + factorisation
@@ -953,16 +1184,31 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   CB_LAUNCH();
   ps.close();
   if (h->has_K && h->m_total > 0) {
-    // z~ = K^{-1}(r_w + C^T u), u = S^{-1}(zc - C K^{-1} r_w): forward sweep,
-    // the root's backward step, the coarse problem, the root correction
-    // W_r u, then the backward sweep below the root (see k_root_h)
-    sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepFwd);
-    sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRoot);
+    // z~ = K^{-1}(r_w + C^T u), u = S^{-1}(zc - C K^{-1} r_w). Corner
+    // formulation: the forward sweep (y' = L^{-1} r_w in ysave), cy = H^T y',
+    // the coarse problem, y' += H u, the backward sweep. Shell formulation:
+    // the forward sweep, the root's backward step, the coarse problem, the
+    // root correction W_r u, then the backward sweep below the root (k_root_h).
+    const bool corner = h->k_corner;
+    const TplSet& tk = h->tplK();
+    double* Yc = corner ? h->ysave.p : h->sv1.p;  // where cy is read and the correction lands
+    const double* Hc = corner ? h->hroot.p : nullptr;
+    sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepFwd);
+    if (!corner) sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRoot);
     ps.next("apply vec 3 cy coarse root-correction");
-    const int cr_blocks = (int)((h->tK.tpl.sn.back().ncols + 255) / 256);
+    const int cr_blocks = corner ? (h->np_max + 255) / 256 : (int)((h->tK.tpl.sn.back().ncols + 255) / 256);
     if (!distributed(h) && h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
-      k_coarse_in<<<h->nsd, 256, 0, s>>>(T, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, h->sv1.p, h->ac_off.p,
-                                         h->sinv.p, h->cy.p, h->gl.p, skip);
+      if (corner) {  // cy = H^T y' (a warp per constraint row), gl = S^{-1} cy
+        k_h_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->root_info.p,
+                                                               h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
+        CB_LAUNCH();
+        k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p,
+                                                               h->sinv.p, h->coarse_id.p, h->zc.p, h->cy.p, h->gl.p, 0,
+                                                               skip);
+      } else {
+        k_coarse_in<<<h->nsd, 256, 0, s>>>(T, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, Yc, h->ac_off.p,
+                                           h->sinv.p, h->cy.p, h->gl.p, skip, h->root_info.p, nullptr, nullptr);
+      }
       CB_LAUNCH();
       const size_t shm = sizeof(double) * ((size_t)h->n_coarse + 2 * kFusedCoarseM);
       if (shm > 48 * 1024)  // opt in once per device, to the largest size this kernel can ever need
@@ -973,11 +1219,16 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
         });
       k_coarse_out<<<dim3(h->nsd, cr_blocks), 256, shm, s>>>(
           h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->acoarse_full.p, h->coarse_id.p, h->m_off.p, h->ac_off.p,
-          h->sinv.p, h->cy.p, h->root_info.p, h->fK.cslot.p, h->wroot.p, h->sv1.p, skip);
+          h->sinv.p, h->cy.p, h->root_info.p, h->fK.cslot.p, h->wroot.p, Yc, skip, Hc, h->hslot.p);
       CB_LAUNCH();
     } else {
-      k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
-                                                         h->sv1.p, h->cy.p, skip);
+      if (corner) {
+        k_h_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->root_info.p,
+                                                               h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
+      } else {
+        k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p,
+                                                           h->c_val.p, h->sv1.p, h->cy.p, skip);
+      }
       CB_LAUNCH();
       k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
                                                              h->coarse_id.p, h->zc.p, h->cy.p, h->gl.p, 0, skip);
@@ -1002,15 +1253,19 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
       k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
                                                              h->coarse_id.p, h->zc.p, h->cy.p, h->uvec.p, 1, skip);
       CB_LAUNCH();
-      k_root_correct<<<dim3(h->nsd, cr_blocks), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.cslot.p, h->wroot.p,
-                                                             h->uvec.p, h->sv1.p, skip);
+      if (corner)
+        k_h_correct<<<dim3(h->nsd, cr_blocks), 256, 0, s>>>(h->m_off.p, h->root_info.p, h->hroot.p, h->hslot.p,
+                                                            h->uvec.p, Yc, skip);
+      else
+        k_root_correct<<<dim3(h->nsd, cr_blocks), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.cslot.p, h->wroot.p,
+                                                               h->uvec.p, h->sv1.p, skip);
       CB_LAUNCH();
     }
     ps.close();
-    sweep_phase(h, h->tK, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRest);
+    sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, corner ? kSweepBwd : kSweepBwdRest);
     ps.next("apply vec 3b gather Av");
   } else {
-    if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
+    if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
     ps.next("apply vec 3b gather Av");
   }
   k_gather_weighted<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->copy_ptr.p, h->copy_idx.p, h->w.p, h->sv1.p, h->gv2.p, skip);

@@ -358,7 +358,7 @@ cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x) {
     if (which != 0 && !h->has_K) throw Failure(CUTBDDC_INVALID_ARGUMENT, "no constrained Neumann factor (no interface)");
     DevBuf<double> X;
     X.upload(x, ns, h->stream);
-    solve_device(h, which == 0 ? h->tI : h->tK, which == 0 ? h->fI : h->fK, X.p, 1, h->upd.p, h->ysave.p, nullptr);
+    solve_device(h, which == 0 ? h->tI : h->tplK(), which == 0 ? h->fI : h->fK, X.p, 1, h->upd.p, h->ysave.p, nullptr);
     X.download(x, ns, h->stream);
     CB_CUDA(cudaStreamSynchronize(h->stream));
   });
@@ -372,11 +372,11 @@ cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds
     if (reps < 1) reps = 1;
     // warm
     solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
-    if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
+    if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
     Timer tm(h->stream);
     for (int r = 0; r < reps; ++r) {
       solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
-      if (h->has_K) solve_device(h, h->tK, h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
+      if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
       solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
     }
     *seconds = tm.stop() / reps;
@@ -414,8 +414,8 @@ cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {
     st[2] = h->n_coarse;
     st[3] = h->slots;
     st[4] = h->fI.panel_total + h->fK.panel_total;
-    st[5] = (int64_t)h->tK.tpl.sn.size();
-    st[6] = (int64_t)h->tK.tpl.levels.size();
+    st[5] = (int64_t)h->tplK().tpl.sn.size();
+    st[6] = (int64_t)h->tplK().tpl.levels.size();
     st[7] = h->m_max;
     st[8] = h->n_if;
     st[9] = g_kernel_launches.load();
@@ -424,6 +424,7 @@ cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {
     st[12] = (int64_t)(h->fI.flops + h->fK.flops);
     st[13] = h->world;
     st[14] = h->comm != nullptr;
+    st[15] = h->has_K && h->k_corner;
   });
 }
 

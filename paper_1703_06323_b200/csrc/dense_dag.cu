@@ -27,6 +27,8 @@
 // order (per-tile counters), so the result is deterministic. The ticket order
 // is topological (build_tasks): no deadlock.
 #include <algorithm>
+#include <chrono>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -526,11 +528,22 @@ struct HostFront {
 // across fronts every task of a child lies above its parent's first tasks),
 // so the order is topological: every wait is on a smaller ticket, held by a
 // running CTA, and the persistent launch cannot deadlock.
+// A split front's tile tasks and their bottom levels (relative to the front's
+// parent entry) depend only on its tile counts (np, nt): computed once per
+// shape and reused by every front of that shape.
+struct SplitShape {
+  std::vector<int4> ft;  // (kind << 24, i, j, k); the front id is or-ed in per front
+  std::vector<int> bl;
+  int top = 0;           // bottom level of the first POTRF (bl_p[0])
+};
+
 std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
-  std::vector<std::vector<int4>> bucket;
+  std::vector<int4> all;  // every task, front by front
+  std::vector<int> all_bl;
   std::vector<int> entry(fr.size(), 0);  // bottom level of a front's first (children-waiting) tasks
   std::vector<int4> ft;
   std::vector<int> bl, bl_p, bl_t, bl_g, bl_a, bl_f;
+  std::map<std::pair<int, int>, SplitShape> shapes;
   for (size_t q = fr.size(); q-- > 0;) {  // parents before children
     HostFront& hf = fr[q];
     DagFront& d = hf.d;
@@ -549,6 +562,8 @@ std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
       entry[q] = off + w;
       d.ntask = 1;
     } else {
+      SplitShape& sh = shapes[std::make_pair(np, nt)];
+      if (sh.ft.empty() && np > 0) {
       for (int k = 0; k < np; ++k) {  // per front, step by step (successors later)
         push(kPotrf, k, k, k, 0);
         for (int i = k + 1; i < nt; ++i) push(kTrsm, i, k, k, 0);
@@ -618,9 +633,20 @@ std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
         ft.resize(w);
         bl.resize(w);
       }
-      for (int& b : bl) b += off;
+      sh.ft = ft;
+      for (int4& t : sh.ft) t.x &= ~0xffffff;  // kind only: the front id is or-ed in per front
+      sh.bl = bl;
+      sh.top = np > 0 ? bl_p[0] : 0;
+      }
+      ft.clear();
+      bl.clear();
+      for (size_t x = 0; x < sh.ft.size(); ++x) {
+        const int4 t = sh.ft[x];
+        ft.push_back(make_int4(t.x | (int)q, t.y, t.z, t.w));
+        bl.push_back(sh.bl[x] + off);
+      }
       // assembly: ASM tiles, then the PEN rows, before every k = 0 task
-      const int top = (np > 0 ? bl_p[0] : 0) + off;
+      const int top = sh.top + off;
       const int npen = (int)(hf.pen1 - hf.pen0);
       const int asm_bl = 1 + top + (npen > 0 ? 1 : 0);
       for (int i = 0; i < nt; ++i)
@@ -631,13 +657,17 @@ std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
       d.ntask = (int)ft.size();
       entry[q] = asm_bl;
     }
-    for (size_t x = 0; x < ft.size(); ++x) {
-      if ((size_t)bl[x] >= bucket.size()) bucket.resize((size_t)bl[x] + 1);
-      bucket[(size_t)bl[x]].push_back(ft[x]);
-    }
+    all.insert(all.end(), ft.begin(), ft.end());
+    all_bl.insert(all_bl.end(), bl.begin(), bl.end());
   }
-  std::vector<int4> tasks;
-  for (size_t b = bucket.size(); b-- > 0;) tasks.insert(tasks.end(), bucket[b].begin(), bucket[b].end());
+  // decreasing bottom level, stable (counting sort)
+  int maxbl = 0;
+  for (int b : all_bl) maxbl = std::max(maxbl, b);
+  std::vector<int64_t> start((size_t)maxbl + 2, 0);
+  for (int b : all_bl) ++start[(size_t)(maxbl - b) + 1];
+  for (size_t b = 1; b < start.size(); ++b) start[b] += start[b - 1];
+  std::vector<int4> tasks(all.size());
+  for (size_t x = 0; x < all.size(); ++x) tasks[(size_t)start[(size_t)(maxbl - all_bl[x])]++] = all[x];
   return tasks;
 }
 
@@ -807,9 +837,17 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
       if (d.ch1 >= 0) fr[(size_t)d.ch1].parent = (int)q;
     }
     if (fr.empty()) return;
+    const auto t0 = std::chrono::steady_clock::now();
     tasks = build_tasks(fr);
+    const auto t1 = std::chrono::steady_clock::now();
     upload_plan(h, plan, fr, tasks);
     plan.key = key;
+    if (std::getenv("CUTBDDC_DAG_STATS")) {
+      const auto t2 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[dag stats] fronts %zu tasks %zu build %.2f ms upload %.2f ms\n", fr.size(), tasks.size(),
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
   }
   std::vector<DagGroup> groups;
   for (const FactorSpan& sp : spans)

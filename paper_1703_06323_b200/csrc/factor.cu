@@ -19,6 +19,7 @@
 // (subst.cuh). Non-positive pivots are reported with the offending
 // (subdomain, slot) — the pivot rule of linalg.cpp:42-54.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -404,7 +405,7 @@ double sweep_bytes(const FactorSet& f) { return f.bytes_per_sweep; }
 // device bytes of the (grow-only, reusable) front workspace already held
 static int64_t front_bytes_held(const cutbddc_gpu* h) { return (int64_t)h->ws_front.cap * (int64_t)sizeof(double); }
 
-static const char* tag_of(const cutbddc_gpu* h, const TplSet& ts) { return &ts == &h->tI ? "I" : "K"; }
+static const char* tag_of(const cutbddc_gpu* h, const FactorSet& f) { return &f == &h->fI ? "I" : "K"; }
 
 // Symbolic phase: compact rows per (sd, supernode), offsets, sweep plan.
 void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, FactorSet& f) {
@@ -414,7 +415,7 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
   f.pfx.alloc((size_t)nsd * t.rows_total);
   f.tpos.alloc((size_t)nsd * t.rows_total);
   f.rc.alloc((size_t)nsd * nsn);
-  ProfScope pplan(h->prof, s, std::string("factor") + tag_of(h, ts) + " symbolic+plan");
+  ProfScope pplan(h->prof, s, std::string("factor") + tag_of(h, f) + " symbolic+plan");
   k_symbolic<<<dim3(nsn, nsd), kThreads, 0, s>>>(t, nsd, in.mask, f.pfx.p, f.tpos.p, f.rc.p);
   CB_LAUNCH();
   f.h_rc = f.rc.to_host(s);
@@ -506,7 +507,14 @@ void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs) {
   CB_CUDA(cudaMemcpyAsync(fl.data(), fail.p, 8 * jobs.size(), cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
   for (size_t g = 0; g < jobs.size(); ++g)
-    if (fl[g] != ~0ull) {
+    if (jobs[g].failed) {
+      *jobs[g].failed = fl[g] != ~0ull;
+      if (fl[g] != ~0ull && std::getenv("CUTBDDC_K_STATS"))
+        std::fprintf(stderr, "[cutbddc] %s: non-positive pivot at subdomain %lld slot %lld\n", jobs[g].what,
+                     (long long)(fl[g] / (unsigned long long)h->slots), (long long)(fl[g] % (unsigned long long)h->slots));
+    }
+  for (size_t g = 0; g < jobs.size(); ++g)
+    if (fl[g] != ~0ull && !jobs[g].failed) {
       const int64_t sd = (int64_t)(fl[g] / (unsigned long long)h->slots);
       const int64_t slot = (int64_t)(fl[g] % (unsigned long long)h->slots);
       throw Failure(CUTBDDC_SINGULAR, std::string(jobs[g].what) + ": matrix is not positive definite (subdomain " +
@@ -544,7 +552,7 @@ void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* 
     CB_CUDA(cudaMemsetAsync(upd, 0, sizeof(double) * (size_t)nrhs * f.upd_total, s));
     CB_CUDA(cudaMemsetAsync(ysave, 0, sizeof(double) * (size_t)nrhs * h->nsd * h->slots, s));
   }
-  const std::string tag = std::string("solve") + (&ts == &h->tI ? "I" : "K") + (nrhs > 1 ? "m " : " ");
+  const std::string tag = std::string("solve") + (&f == &h->fI ? "I" : "K") + (nrhs > 1 ? "m " : " ");
   for (int L = nlev - 1; L >= 0; --L) {
     if (rhs_root_only && L > 0) continue;
     ProfScope ps(h->prof, s, tag + "fwd L" + std::to_string(L));

@@ -65,7 +65,8 @@ struct FactorJob {
   const TplSet* ts;
   const FactorInput* in;
   FactorSet* f;
-  const char* what;  // error message prefix (non-positive pivot)
+  const char* what;       // error message prefix (non-positive pivot)
+  bool* failed = nullptr;  // set: a non-positive pivot is reported here instead of thrown
 };
 void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs);
 // ysave: nrhs x nsd x T doubles of scratch (forward results of big fronts).
@@ -80,7 +81,11 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
                       const std::vector<int64_t>& uoff);
 void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip);
-enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3 };
+enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3, kSweepAttrOnly = 4 };
+// sweep.cu: forward sweep of kSweepMultiRhs right-hand sides at once
+constexpr int kSweepMultiRhs = 8;
+void sweep_forward_multi(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const double* X, double* ysave,
+                         double* upd, double* vbuf8);
 void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip, int phase);
 // dense_dag.cu: numeric factorisation of every span as one dataflow launch

@@ -147,6 +147,13 @@ struct cutbddc_gpu {
   TplSet tK;                                     // shell-root template (K = A + rho C^T C)
   FactorSet fI, fK;                              // interior / Neumann factorisations
   bool has_K = false;                            // false without an interface (one subdomain)
+  // K formulation: corner-augmented K_c = A + rho
+  // sum_corners e e^T on the plain ND template (tI), coarse basis through
+  // H = L^{-1} C^T (k_corner); or the full K = A + rho C^T C on the
+  // shell-root template (tK), coarse basis in the root space (fallback when a
+  // K_c pivot is tiny or non-positive, or CUTBDDC_K_SHELL=1)
+  bool k_corner = true;
+  const TplSet& tplK() const { return k_corner ? tI : tK; }
   cutbddc_b200::DevBuf<uint8_t> mask_int, mask_all;  // per (sd, slot)
   cutbddc_b200::DevBuf<double> diag_add;         // per (sd, slot): rho at corner slots
   cutbddc_b200::DevBuf<uint8_t> corner_row;      // per constraint row: 1 if a corner
@@ -179,6 +186,11 @@ struct cutbddc_gpu {
   // {c_r, root panel offset, root vector offset (sweep), W_r offset}
   cutbddc_b200::DevBuf<double> sinv, wroot, hroot;
   cutbddc_b200::DevBuf<int64_t> root_info;
+  // corner formulation: H = L^{-1} C^T over each subdomain's present slots in
+  // front-column order (column-major, np_sd x m_sd at root_info[4 sd + 3]),
+  // hslot[root_info[4 sd + 1] + k] = sd * T + slot of compact position k
+  cutbddc_b200::DevBuf<int32_t> hslot;
+  int np_max = 0;
   cutbddc_b200::DevBuf<double> uvec;              // m_total: S^{-1}(zc - cy) per constraint row
   bool bddc_ready = false;
   double t_setup = 0;
@@ -199,6 +211,8 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int64_t> ws_cnt, ws_nc64;
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp, ws_obj;
   cutbddc_b200::DevBuf<int> ws_flag;
+  cutbddc_b200::DevBuf<int32_t> ws_coff;                       // corner coarse basis: front column offsets
+  cutbddc_b200::DevBuf<double> ws_x8, ws_y8, ws_u8, ws_v8;      // multi-RHS forward sweep vectors
   DagPlan dag_factor;                              // dense_dag.cu: the subdomain factorisations (one launch)
   std::vector<cudaEvent_t> dag_ev;                 // start/stop event pairs of the last numeric factorisation's launches
   DagPlan dag_dense;                               // dense_dag.cu: the coarse matrix factorisation

@@ -301,16 +301,24 @@ __device__ void producer(const SweepDev& p, const int4* __restrict__ items, int 
   }
 }
 
+// Right-hand-side strides of a multi-RHS forward sweep (doubles): slot
+// vectors (X, ysave), update workspace, tile partials.
+struct RhsStride {
+  int64_t x, u, v;
+};
+
 // Forward of one item: o[i] = sum_j G[i, j] v[j] over the item's rows and
-// column range (rows split over thread groups, columns interleaved over the
-// groups: every row's sum has a fixed order). One column range: the item
-// writes y (column rows) and the parent's update v_rest - o (update rows);
-// several: partial sums to vbuf, the last range of a row block to arrive
-// sums them in range order. Everything static (b at the columns, gmap rows)
-// is loaded before the dependency wait.
+// column range for NR right-hand sides at once (rows split over thread
+// groups, columns interleaved over the groups: every row's sum has a fixed
+// order). One column range: the item writes y (column rows) and the
+// parent's update v_rest - o (update rows); several: partial sums to vbuf,
+// the last range of a row block to arrive sums them in range order.
+// Everything static (b at the columns, gmap rows) is loaded before the
+// dependency wait.
+template <int NR>
 __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, const int* segoff, SlotRec* sr,
                          int& chunk_seq, const double* __restrict__ X, double* ysave, double* upd, double* v,
-                         double* part, unsigned long long& t_dep) {
+                         double* part, unsigned long long& t_dep, RhsStride rs) {
   const int tid = threadIdx.x;
   const FrontDesc d = R.d;
   const int kind = R.item.x;
@@ -320,10 +328,13 @@ __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
   const ItemGeom g = item_geom(p, d, kind, R.item.w, true);
   const int nrow = g.i1 - g.i0;
   // static loads: b at the item's columns (v), the gmap of its columns and rows
-  for (int q = tid; q < g.jhi - g.jlo; q += kThreadsSweep) v[q] = X[cs[g.jlo + q]];
+  for (int q = tid; q < g.jhi - g.jlo; q += kThreadsSweep) {
+    const int sl = cs[g.jlo + q];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) v[q * NR + rr] = X[rr * rs.x + sl];
+  }
   const int qr = g.i0 + tid;  // this thread's row (rows <= 256)
-  const int2 gr = (tid < nrow && (qr >= c || g.mcb == 1)) ? reinterpret_cast<const int2*>(p.gmap)[d.vo + qr]
-                                                         : make_int2(-1, -1);
+  const int2 gr = (tid < nrow && qr >= c) ? reinterpret_cast<const int2*>(p.gmap)[d.vo + qr] : make_int2(-1, -1);
   if (d.nch > 0) cta_wait(p.done_f + d.cfs0, d.cnf0);
   if (d.nch > 1) cta_wait(p.done_f + d.cfs1, d.cnf1);
   csync();  // every consumer has its copy of the record: the producer may take the next ticket
@@ -333,18 +344,27 @@ __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
   }
   for (int q = tid; q < g.jhi - g.jlo; q += kThreadsSweep) {  // the children's updates at the columns
     const int2 gc = reinterpret_cast<const int2*>(p.gmap)[d.vo + g.jlo + q];
-    double x = v[q];
-    if (gc.x >= 0) x += __ldcg(upd + gc.x);
-    if (gc.y >= 0) x += __ldcg(upd + gc.y);
-    v[q] = x;
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {
+      double x = v[q * NR + rr];
+      if (gc.x >= 0) x += __ldcg(upd + rr * rs.u + gc.x);
+      if (gc.y >= 0) x += __ldcg(upd + rr * rs.u + gc.y);
+      v[q * NR + rr] = x;
+    }
   }
-  double cu = 0.0;  // the children's updates at row qr (update rows)
-  if (gr.x >= 0) cu += __ldcg(upd + gr.x);
-  if (gr.y >= 0) cu += __ldcg(upd + gr.y);
+  double cu[NR];  // the children's updates at row qr (update rows)
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) {
+    cu[rr] = 0.0;
+    if (gr.x >= 0) cu[rr] += __ldcg(upd + rr * rs.u + gr.x);
+    if (gr.y >= 0) cu[rr] += __ldcg(upd + rr * rs.u + gr.y);
+  }
   csync();
   const int Rw = (nrow + 31) & ~31, ng = kThreadsSweep / Rw;  // Rw <= 256 rows per group, ng groups
   const int row = tid % Rw, grp = tid / Rw, i = g.i0 + row;
-  double acc = 0.0;
+  double acc[NR];
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
   for (int q = 0; q < g.nchunk; ++q, ++chunk_seq) {
     const int slot = chunk_seq % kSlots;
     const Chunk ch = chunk_of(g, q, true);
@@ -353,19 +373,30 @@ __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
     const int* so = segoff + slot * kMaxSegs;
     if (grp < ng && row < nrow) {
       const int jend = min(ch.jb, i + 1);
-      for (int j = ch.ja + grp; j < jend; j += ng) acc += S[so[j - ch.ja] + i] * v[j - g.jlo];
+      for (int j = ch.ja + grp; j < jend; j += ng) {
+        const double gij = S[so[j - ch.ja] + i];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) acc[rr] += gij * v[(j - g.jlo) * NR + rr];
+      }
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&sr[slot].empty);
   }
-  if (grp < ng && row < nrow) part[grp * Rw + row] = acc;
-  csync();
-  double o = 0.0;
-  if (tid < nrow)
-    for (int q = 0; q < ng; ++q) o += part[q * Rw + tid];
+  double o[NR];
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) {  // group partials summed in group order, one right-hand side at a time
+    if (grp < ng && row < nrow) part[grp * Rw + row] = acc[rr];
+    csync();
+    o[rr] = 0.0;
+    if (tid < nrow)
+      for (int q = 0; q < ng; ++q) o[rr] += part[q * Rw + tid];
+    csync();
+  }
   if (g.mcb > 1) {
     double* tp = p.vbuf + d.tpo + (int64_t)g.rb * g.mcb * kFwdRows;
-    if (tid < nrow) tp[(int64_t)g.cb * kFwdRows + tid] = o;
+    if (tid < nrow)
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) tp[rr * rs.v + (int64_t)g.cb * kFwdRows + tid] = o[rr];
     __shared__ int s_last;
     csync();
     const int ncb = max(1, (min(c, g.i1) + p.fwd_cols - 1) / p.fwd_cols);
@@ -376,16 +407,22 @@ __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
     }
     csync();
     if (!s_last) return;  // another range of the row block finishes it
-    if (tid < nrow) {
-      o = 0.0;
-      for (int k = 0; k < ncb; ++k) o += __ldcg(tp + (int64_t)k * kFwdRows + tid);
-    }
+    if (tid < nrow)
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        o[rr] = 0.0;
+        for (int k = 0; k < ncb; ++k) o[rr] += __ldcg(tp + rr * rs.v + (int64_t)k * kFwdRows + tid);
+      }
   }
   if (tid < nrow) {
-    if (qr < c)
-      ysave[cs[qr]] = o;
-    else
-      upd[d.uo + qr - c] = cu - o;
+    if (qr < c) {
+      const int sl = cs[qr];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) ysave[rr * rs.x + sl] = o[rr];
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) upd[rr * rs.u + d.uo + qr - c] = cu[rr] - o[rr];
+    }
   }
   cta_signal(p.done_f + fs);
 }
@@ -452,10 +489,11 @@ __device__ void bwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
 // unfinished ticket is always some CTA's current item, whose dependencies
 // (smaller tickets) are done, and whose chunks come first in its ring: no
 // deadlock.
-template <bool kFwd>
+template <bool kFwd, int NR = 1>
 __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __restrict__ items, int n_items,
                                            int32_t* ticket, const double* __restrict__ panel, const double* X,
-                                           double* Xw, const double* ysave_in, double* ysave, double* upd) {
+                                           double* Xw, const double* ysave_in, double* ysave, double* upd,
+                                           RhsStride rs = RhsStride{0, 0, 0}) {
   extern __shared__ __align__(128) double shm[];
   double* ring = shm;
   double* vec = shm + kSlots * kSlot;
@@ -488,7 +526,7 @@ __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __rest
     const unsigned long long t_grab = R.t_grab;
     unsigned long long t_dep = 0;
     if (kFwd)
-      fwd_item(p, R, ring, segoff, sr, chunk_seq, X, ysave, upd, vec, part, t_dep);
+      fwd_item<NR>(p, R, ring, segoff, sr, chunk_seq, X, ysave, upd, vec, part, t_dep, rs);
     else
       bwd_item(p, R, ring, segoff, sr, chunk_seq, Xw, ysave_in, vec, t_dep);
     csync();  // vec / part are free (the item record was released after the dependency wait)
@@ -508,6 +546,17 @@ __global__ void __launch_bounds__(kThreadsSweep + 32, kMinBlocks) k_sweep_fwd(Sw
                                                              double* upd, const int* __restrict__ skip) {
   if (skip && *skip) return;
   sweep_loop<true>(p, items, n_items, p.ticket, panel, X, nullptr, nullptr, ysave, upd);
+}
+
+// Forward sweep of kMultiRhs right-hand sides at once (the coarse-basis
+// setup: H = L^{-1} C^T), same items and schedule as k_sweep_fwd.
+constexpr int kMultiRhs = 8;
+static_assert(kMultiRhs * kSmallRows <= kVecDoubles, "multi-RHS front vector");
+__global__ void __launch_bounds__(kThreadsSweep + 32, 1) k_sweep_fwd_multi(SweepDev p, const int4* __restrict__ items, int n_items,
+                                                             const double* __restrict__ panel,
+                                                             const double* __restrict__ X, double* __restrict__ ysave,
+                                                             double* upd, RhsStride rs) {
+  sweep_loop<true, kMultiRhs>(p, items, n_items, p.ticket, panel, X, nullptr, nullptr, ysave, upd, rs);
 }
 
 __global__ void __launch_bounds__(kThreadsSweep + 32, kMinBlocks) k_sweep_bwd(SweepDev p, const int4* __restrict__ items, int n_items,
@@ -588,7 +637,8 @@ void dump_trace(const std::string& path, const FactorSet& f, bool fwd, cudaStrea
 }
 
 int sweep_grid(const void* fn) {
-  const int slot = fn == (const void*)k_sweep_fwd ? kMemoSweepFwd : kMemoSweepBwd;
+  const int slot = fn == (const void*)k_sweep_fwd ? kMemoSweepFwd
+                   : fn == (const void*)k_sweep_bwd ? kMemoSweepBwd : kMemoSweepMulti;
   return (int)device_memo(slot, [&] {
     int per_sm = 0;
     CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsSweep + 32, kShmBytes));
@@ -614,7 +664,7 @@ void choose_item_sizes(cutbddc_gpu* h, FactorSet& f) {
   int fc = wide ? 256 : 128, bc = wide ? 32 : 16, sw = wide ? 32768 : 8192;
   if (const char* e = std::getenv("CUTBDDC_SWEEP_ITEMS")) std::sscanf(e, "%d,%d,%d", &fc, &bc, &sw);
   bc = std::max(kWarps, std::min(kMaxBwdCols, bc / kWarps * kWarps));
-  f.fwd_cols = std::max(16, fc);
+  f.fwd_cols = std::max(16, std::min(kSmallRows, fc));  // <= kSmallRows: the multi-RHS front vector fits
   f.bwd_cols = bc;
   f.small_work = std::max(1, sw);
 }
@@ -856,9 +906,11 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
   device_memo(kMemoSweepAttr, [&] {
     CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     CB_CUDA(cudaFuncSetAttribute(k_sweep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     return 1ll;
   });
-  const std::string tag = std::string("sweep") + (&ts == &h->tI ? "I" : "K");
+  if (phase == kSweepAttrOnly) return;
+  const std::string tag = std::string("sweep") + (&f == &h->fI ? "I" : "K");
   if (phase == kSweepFwd) {
     CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
     ProfScope ps(h->prof, s, tag + " fwd");
@@ -880,6 +932,26 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
     CB_LAUNCH();
   }
   if (tp && phase == kSweepBwd) dump_trace(std::string(tp) + "_" + tag + "_bwd.bin", f, false, s);
+}
+
+// Forward sweep of kSweepMultiRhs right-hand sides X[rhs][nsd*T] (the
+// columns' y to ysave[rhs][nsd*T], updates in upd[rhs][upd_total], tile
+// partials in vbuf8[rhs][f.vbuf.n]).
+void sweep_forward_multi(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const double* X, double* ysave,
+                         double* upd, double* vbuf8) {
+  static_assert(kMultiRhs == kSweepMultiRhs, "multi-RHS width");
+  cudaStream_t s = h->stream;
+  const int nsd = h->nsd, nsn = (int)ts.tpl.sn.size();
+  SweepDev p = sweep_dev(f, nsd, nsn, nullptr);
+  p.vbuf = vbuf8;
+  const size_t shm = kShmBytes;
+  sweep_phase(h, ts, f, nullptr, nullptr, nullptr, nullptr, kSweepAttrOnly);
+  CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
+  if (f.n_items_f == 0) return;
+  const RhsStride rs{(int64_t)nsd * h->slots, f.upd_total, (int64_t)f.vbuf.n};
+  const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd_multi));
+  k_sweep_fwd_multi<<<g, kThreadsSweep + 32, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, rs);
+  CB_LAUNCH();
 }
 
 void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,

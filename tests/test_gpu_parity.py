@@ -144,11 +144,15 @@ def _hist(a, b, b0):
 #     the spread of the oracle under 1-ulp rho changes and other ND orders
 #     (iterations within the envelope +-1, history / solution deviation at
 #     most 10x the envelope's).
-PERTURB = [{"ORACLE_RHO_ULPS": "1"}, {"ORACLE_RHO_ULPS": "-1"}, {"ORACLE_ND_LEAF": "8"}, {"ORACLE_ND_LEAF": "64"}]
+# the oracle's own rounding variants: rho moved by one ulp, other ND orders,
+# and the corner-augmented saddle formulation (K_c = A + rho C_corner^T C_corner,
+# the GPU's default; mathematically the same preconditioner)
+PERTURB = [{"ORACLE_RHO_ULPS": "1"}, {"ORACLE_RHO_ULPS": "-1"}, {"ORACLE_ND_LEAF": "8"}, {"ORACLE_ND_LEAF": "64"},
+           {"ORACLE_K_CORNERS": "1"}]
 
 
 def _oracle_with(cfg, env):
-    for k in ("ORACLE_RHO_ULPS", "ORACLE_ND_LEAF"):
+    for k in ("ORACLE_RHO_ULPS", "ORACLE_ND_LEAF", "ORACLE_K_CORNERS"):
         os.environ.pop(k, None)
     os.environ.update(env)
     try:

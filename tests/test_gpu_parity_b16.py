@@ -70,6 +70,15 @@ def test_cfg4_local_solves_match_oracle(cfg4, which):
     factorisation + dataflow sweeps against the oracle's simplicial
     SparseCholesky (different elimination orders, same matrices)."""
     cfg, o, s, pb = cfg4
+    if which == 1 and s.stats()["k_corner"]:
+        # the GPU factors K_c = A + rho C_corner^T C_corner (DESIGN.md): compare
+        # with the oracle's SparseCholesky of the same matrix
+        os.environ["ORACLE_K_CORNERS"] = "1"
+        try:
+            o = Oracle(cfg)
+            o.setup()
+        finally:
+            del os.environ["ORACLE_K_CORNERS"]
     nsd = len(pb.block_ids)
     maps, T = _slot_maps(s, o, nsd)
     rng = np.random.default_rng(17 + which)
@@ -89,8 +98,8 @@ def test_cfg4_local_solves_match_oracle(cfg4, which):
         y_g = Y[k * T + slots][sel]
         ref = y_o[pos][sel]
         worst = max(worst, _rel(y_g, ref))
-    # interior problems: 1e-10; K = A + rho C^T C of subdomains with small cut
-    # cells is far worse conditioned: the north_star fp64 bar, 1e-8
+    # interior problems: 1e-10; the constrained Neumann matrix of subdomains
+    # with small cut cells is far worse conditioned: the north_star fp64 bar, 1e-8
     assert worst <= (1e-10 if which == 0 else 1e-8), worst
 
 
