@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_exports_match_header():
     hdr = open(os.path.join(ROOT, "include", "cutbddc.h")).read()
-    declared = set(re.findall(r"\b(cutbddc_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(cutbddc_[a-z0-9_]+)\s*\(", hdr))
     lib = cb.lib()
     for name in declared:
         assert hasattr(lib, name), name
