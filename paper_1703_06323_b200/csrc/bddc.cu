@@ -1173,7 +1173,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   k_gather_masked<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->mask_int.p, r, h->sv0.p, skip);
   CB_LAUNCH();
   ps.close();
-  solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, skip);
+  solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, skip);
   ps.next("apply vec 2 z0 r1 scatter phit");
   k_z0<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv0.p, skip);
   CB_LAUNCH();
@@ -1265,7 +1265,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, corner ? kSweepBwd : kSweepBwdRest);
     ps.next("apply vec 3b gather Av");
   } else {
-    if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, skip);
+    if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, skip);
     ps.next("apply vec 3b gather Av");
   }
   k_gather_weighted<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->copy_ptr.p, h->copy_idx.p, h->w.p, h->sv1.p, h->gv2.p, skip);
@@ -1275,7 +1275,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
                                                   h->sv0.p, skip);
   CB_LAUNCH();
   ps.close();
-  solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, skip);
+  solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, skip);
   ps.next("apply vec 4 final");
   if (distributed(h)) {
     k_owned_neg<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv3.p, skip);

@@ -358,7 +358,7 @@ cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x) {
     if (which != 0 && !h->has_K) throw Failure(CUTBDDC_INVALID_ARGUMENT, "no constrained Neumann factor (no interface)");
     DevBuf<double> X;
     X.upload(x, ns, h->stream);
-    solve_device(h, which == 0 ? h->tI : h->tplK(), which == 0 ? h->fI : h->fK, X.p, 1, h->upd.p, h->ysave.p, nullptr);
+    solve_device(h, which == 0 ? h->tI : h->tplK(), which == 0 ? h->fI : h->fK, X.p, h->upd.p, h->ysave.p, nullptr);
     X.download(x, ns, h->stream);
     CB_CUDA(cudaStreamSynchronize(h->stream));
   });
@@ -371,13 +371,13 @@ cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds
     if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
     if (reps < 1) reps = 1;
     // warm
-    solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
-    if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
+    solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
+    if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, nullptr);
     Timer tm(h->stream);
     for (int r = 0; r < reps; ++r) {
-      solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
-      if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, 1, h->upd.p, h->ysave.p, nullptr);
-      solve_device(h, h->tI, h->fI, h->sv0.p, 1, h->upd.p, h->ysave.p, nullptr);
+      solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
+      if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, nullptr);
+      solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
     }
     *seconds = tm.stop() / reps;
     *bytes = 2.0 * sweep_bytes(h->fI) + (h->has_K ? sweep_bytes(h->fK) : 0.0);

@@ -1,5 +1,5 @@
 // factor.cu — batched multifrontal Cholesky over the ND template (K6) and
-// the level-scheduled triangular solves (K7).
+// the symbolic phase of the dataflow triangular solves (sweep.cu).
 //
 // Replaces SparseCholesky (linalg.cpp:34-62) for the interior problems A_II
 // and the augmented Neumann matrices K = A + rho C^T C used by the
@@ -103,213 +103,6 @@ static bool is_split_front(const Supernode& sn) {
   return sn.nrows >= kSplitRows || mflop >= kSplitMflop;
 }
 
-// ---------------------------------------------------------------- solves
-// forward elimination: X holds b on entry (slot vectors), y on exit at the
-// front's columns; v_rest - L21 y goes to the parent through `upd`.
-__global__ void __launch_bounds__(256) k_fwd_level(TplDev t, FactorDev f, const int32_t* __restrict__ level_sn, int nsd,
-                                                   const double* __restrict__ panel, double* __restrict__ X,
-                                                   double* __restrict__ upd, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  extern __shared__ double v[];
-  const int sid = level_sn[blockIdx.x];
-  const Supernode s = t.sn[sid];
-  const int sd = blockIdx.y, rhs = blockIdx.z;
-  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
-  const int r = rc.x, c = rc.y;
-  if (r == 0) return;
-  double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
-  double* ub = upd + (int64_t)rhs * f.upd_total;
-  const int32_t* rows = t.rows + s.rows_off;
-  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
-    const int p = pfx_at(f, t, sd, s, q);
-    if (p >= 0) v[p] = q < s.ncols ? x[rows[q]] : 0.0;
-  }
-  __syncthreads();
-  for (int ch = 0; ch < s.nchild; ++ch) {
-    const int cid = s.child[ch];
-    const Supernode cs = t.sn[cid];
-    const int ccc = f.rc[(int64_t)sd * t.nsn + cid].y;
-    const double* cu = ub + f.upd_off[(int64_t)sd * t.nsn + cid];
-    for (int a = threadIdx.x; a < cs.nrows - cs.ncols; a += blockDim.x) {
-      const int ia = pfx_at(f, t, sd, cs, cs.ncols + a);
-      if (ia >= 0) v[pfx_at(f, t, sd, s, t.emap[cs.emap_off + a])] += cu[ia - ccc];
-    }
-    __syncthreads();
-  }
-  panel_forward(panel + f.panel_off[(int64_t)sd * t.nsn + sid], r, c, v);
-  double* uo = ub + f.upd_off[(int64_t)sd * t.nsn + sid];
-  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
-    const int p = pfx_at(f, t, sd, s, q);
-    if (p < 0) continue;
-    if (q < s.ncols)
-      x[rows[q]] = v[p];
-    else
-      uo[p - c] = v[p];
-  }
-}
-
-// backward substitution: X holds y at this level's columns and the final x
-// at ancestors; x_c = L11^{-T} (y - L21^T x_rest).
-__global__ void __launch_bounds__(256) k_bwd_level(TplDev t, FactorDev f, const int32_t* __restrict__ level_sn, int nsd,
-                                                   const double* __restrict__ panel, double* __restrict__ X,
-                                                   const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  extern __shared__ double w[];
-  __shared__ double tile[32][33];
-  const int sid = level_sn[blockIdx.x];
-  const Supernode s = t.sn[sid];
-  const int sd = blockIdx.y, rhs = blockIdx.z;
-  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
-  const int r = rc.x, c = rc.y;
-  if (c == 0) return;
-  double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
-  const int32_t* rows = t.rows + s.rows_off;
-  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
-    const int p = pfx_at(f, t, sd, s, q);
-    if (p >= 0) w[p] = x[rows[q]];
-  }
-  __syncthreads();
-  panel_backward(panel + f.panel_off[(int64_t)sd * t.nsn + sid], r, c, w, tile);
-  for (int q = threadIdx.x; q < s.ncols; q += blockDim.x) {
-    const int p = pfx_at(f, t, sd, s, q);
-    if (p >= 0) x[rows[q]] = w[p];
-  }
-}
-
-// Big fronts, forward: [y; t] = G v_c as a GEMV split into 128-row chunks
-// (one CTA each). Every chunk rebuilds the full front vector (gather +
-// children's updates) in shared memory; y goes to `ysave` (x keeps b at the
-// columns until the backward sweep, so concurrent chunks never race).
-// Fronts with at least kBigMinCols template columns get explicit-inverse
-// panels and multi-CTA GEMV sweeps; all fronts do (measured: the blocked
-// substitution path was latency-bound at every level).
-constexpr int kBigMinCols = 1;
-// ND leaf size: boxes of at most this many lattice nodes are leaf fronts
-// (CUTBDDC_LEAF overrides, for measurements).
-constexpr int kLeafMax = 216;  // cfg4: 27 -> 125 cut the apply's solve time 744 -> 668 us; 125 -> 216: 3.49 -> 3.72 M DOF/s (profiles/r01_tune_leaf.txt)
-constexpr int kBigRows = 32;   // forward: rows per CTA (one row per lane)
-constexpr int kBigCols = 16;   // backward: columns per CTA (two per warp)
-
-__global__ void __launch_bounds__(256) k_fwd_big(TplDev t, FactorDev f, const int2* __restrict__ items, int nsd,
-                                                 const double* __restrict__ panel, const double* __restrict__ X,
-                                                 double* __restrict__ ysave, double* __restrict__ upd,
-                                                 const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  extern __shared__ double v[];
-  int* slot_of = reinterpret_cast<int*>(v + 2048);
-  const int2 it = items[blockIdx.x];
-  const int sid = it.x;
-  const Supernode s = t.sn[sid];
-  const int sd = blockIdx.y, rhs = blockIdx.z;
-  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
-  const int r = rc.x, c = rc.y;
-  const int i0 = it.y * kBigRows;
-  if (i0 >= r) return;
-  const int i1 = min(r, i0 + kBigRows);
-  const double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
-  double* ys = ysave + ((int64_t)rhs * nsd + sd) * t.T;
-  double* ub = upd + (int64_t)rhs * f.upd_total;
-  const int32_t* rows = t.rows + s.rows_off;
-  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
-    const int p = pfx_at(f, t, sd, s, q);
-    if (p >= 0) {
-      v[p] = q < s.ncols ? x[rows[q]] : 0.0;
-      slot_of[p] = rows[q];
-    }
-  }
-  __syncthreads();
-  for (int ch = 0; ch < s.nchild; ++ch) {
-    const int cid = s.child[ch];
-    const Supernode cs = t.sn[cid];
-    const int ccc = f.rc[(int64_t)sd * t.nsn + cid].y;
-    const double* cu = ub + f.upd_off[(int64_t)sd * t.nsn + cid];
-    for (int a = threadIdx.x; a < cs.nrows - cs.ncols; a += blockDim.x) {
-      const int ia = pfx_at(f, t, sd, cs, cs.ncols + a);
-      if (ia >= 0) v[pfx_at(f, t, sd, s, t.emap[cs.emap_off + a])] += cu[ia - ccc];
-    }
-    __syncthreads();
-  }
-  const double* G = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
-  double* uo = ub + f.upd_off[(int64_t)sd * t.nsn + sid];
-  // lane = row of the 32-row chunk, warp = contiguous column range; four
-  // independent accumulators keep 4 coalesced 256-B loads per warp in flight.
-  // (G's strict upper triangle is stored as zeros, so rows need no mask.)
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int jend = min(c, i1);
-  const int cw = (jend + nw - 1) / nw;
-  const int ja = min(jend, wid * cw), jb = min(jend, ja + cw);
-  const int i = i0 + lane;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  if (i < i1) {
-    const double* gi = G + i;
-    int j = ja;
-    for (; j + 4 <= jb; j += 4) {
-      s0 += gi[(int64_t)j * r] * v[j];
-      s1 += gi[(int64_t)(j + 1) * r] * v[j + 1];
-      s2 += gi[(int64_t)(j + 2) * r] * v[j + 2];
-      s3 += gi[(int64_t)(j + 3) * r] * v[j + 3];
-    }
-    for (; j < jb; ++j) s0 += gi[(int64_t)j * r] * v[j];
-  }
-  __shared__ double part[8][33];
-  part[wid][lane] = (s0 + s1) + (s2 + s3);
-  __syncthreads();
-  if (wid == 0 && i < i1) {
-    double o = 0.0;
-    for (int q = 0; q < nw; ++q) o += part[q][lane];
-    if (i < c)
-      ys[slot_of[i]] = o;
-    else
-      uo[i - c] = v[i] - o;
-  }
-}
-
-// Big fronts, backward: x_c = G^T [y; -x_rest], 32 columns per CTA, one warp
-// per column reducing over the rows.
-__global__ void __launch_bounds__(256) k_bwd_big(TplDev t, FactorDev f, const int2* __restrict__ items, int nsd,
-                                                 const double* __restrict__ panel, double* __restrict__ X,
-                                                 const double* __restrict__ ysave, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  extern __shared__ double w[];
-  int* slot_of = reinterpret_cast<int*>(w + 2048);
-  const int2 it = items[blockIdx.x];
-  const int sid = it.x;
-  const Supernode s = t.sn[sid];
-  const int sd = blockIdx.y, rhs = blockIdx.z;
-  const int2 rc = f.rc[(int64_t)sd * t.nsn + sid];
-  const int r = rc.x, c = rc.y;
-  const int j0 = it.y * kBigCols;
-  if (j0 >= c) return;
-  const int j1 = min(c, j0 + kBigCols);
-  double* x = X + ((int64_t)rhs * nsd + sd) * t.T;
-  const double* ys = ysave + ((int64_t)rhs * nsd + sd) * t.T;
-  const int32_t* rows = t.rows + s.rows_off;
-  for (int q = threadIdx.x; q < s.nrows; q += blockDim.x) {
-    const int p = pfx_at(f, t, sd, s, q);
-    if (p >= 0) {
-      w[p] = p < c ? ys[rows[q]] : -x[rows[q]];
-      slot_of[p] = rows[q];
-    }
-  }
-  __syncthreads();
-  const double* G = panel + f.panel_off[(int64_t)sd * t.nsn + sid];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = j0 + wid; j < j1; j += nw) {
-    const double* col = G + (int64_t)j * r;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int i = j + lane;
-    for (; i + 96 < r; i += 128) {
-      s0 += col[i] * w[i];
-      s1 += col[i + 32] * w[i + 32];
-      s2 += col[i + 64] * w[i + 64];
-      s3 += col[i + 96] * w[i + 96];
-    }
-    for (; i < r; i += 32) s0 += col[i] * w[i];
-    const double sum = warp_sum((s0 + s1) + (s2 + s3));
-    if (lane == 0) x[slot_of[j]] = sum;
-  }
-}
-
 }  // namespace
 
 TplDev tpl_dev(const TplSet& ts, int slots) {
@@ -319,7 +112,6 @@ TplDev tpl_dev(const TplSet& ts, int slots) {
   t.amap = ts.amap.p;
   t.emap = ts.emap.p;
   t.root_pos = ts.root_pos.p;
-  t.is_big = ts.big_flag.p;
   t.T = slots;
   t.nsn = (int)ts.tpl.sn.size();
   t.root = t.nsn - 1;
@@ -335,6 +127,8 @@ FactorDev factor_dev(const FactorSet& f) {
                    f.cslot.p};
 }
 
+constexpr int kLeafMax = 216;  // cfg4: 27 -> 125 cut the apply's solve time 744 -> 668 us; 125 -> 216: 3.49 -> 3.72 M DOF/s (profiles/r01_tune_leaf.txt)
+
 void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
   cudaStream_t s = h->stream;
   static const int leaf = [] {
@@ -348,55 +142,8 @@ void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
   ts.amap.upload(ts.tpl.amap, s);
   ts.emap.upload(ts.tpl.emap.empty() ? std::vector<int32_t>{0} : ts.tpl.emap, s);
   ts.root_pos.upload(ts.tpl.root_pos, s);
-  std::vector<int32_t> lv, small, big;
-  std::vector<int2> fwd, bwd;
-  ts.level_first.clear();
-  ts.level_count.clear();
-  ts.small_first.clear();
-  ts.small_count.clear();
-  ts.big_first.clear();
-  ts.big_count.clear();
-  ts.fwd_first.clear();
-  ts.fwd_count.clear();
-  ts.bwd_first.clear();
-  ts.bwd_count.clear();
-  ts.is_big.assign(ts.tpl.sn.size(), 0);
   ts.is_split.assign(ts.tpl.sn.size(), 0);
   for (size_t sid = 0; sid < ts.tpl.sn.size(); ++sid) ts.is_split[sid] = is_split_front(ts.tpl.sn[sid]);
-  for (auto& L : ts.tpl.levels) {
-    ts.level_first.push_back((int)lv.size());
-    ts.level_count.push_back((int)L.size());
-    lv.insert(lv.end(), L.begin(), L.end());
-    ts.small_first.push_back((int)small.size());
-    ts.big_first.push_back((int)big.size());
-    ts.fwd_first.push_back((int)fwd.size());
-    ts.bwd_first.push_back((int)bwd.size());
-    for (int sid : L) {
-      const Supernode& sn = ts.tpl.sn[(size_t)sid];
-      // big: explicit-inverse panel swept by many CTAs
-      const bool is_big = sn.ncols >= kBigMinCols;
-      ts.is_big[(size_t)sid] = is_big;
-      if (!is_big) {
-        small.push_back(sid);
-        continue;
-      }
-      big.push_back(sid);
-      for (int ch = 0; ch < (sn.nrows + kBigRows - 1) / kBigRows; ++ch) fwd.push_back(make_int2(sid, ch));
-      for (int ch = 0; ch < (sn.ncols + kBigCols - 1) / kBigCols; ++ch) bwd.push_back(make_int2(sid, ch));
-    }
-    ts.small_count.push_back((int)small.size() - ts.small_first.back());
-    ts.big_count.push_back((int)big.size() - ts.big_first.back());
-    ts.fwd_count.push_back((int)fwd.size() - ts.fwd_first.back());
-    ts.bwd_count.push_back((int)bwd.size() - ts.bwd_first.back());
-  }
-  auto nz32 = [](std::vector<int32_t> v) { return v.empty() ? std::vector<int32_t>{0} : v; };
-  auto nz2 = [](std::vector<int2> v) { return v.empty() ? std::vector<int2>{make_int2(0, 0)} : v; };
-  ts.level_sn.upload(lv, s);
-  ts.small_sn.upload(nz32(small), s);
-  ts.big_sn.upload(nz32(big), s);
-  ts.fwd_items.upload(nz2(fwd), s);
-  ts.bwd_items.upload(nz2(bwd), s);
-  ts.big_flag.upload(ts.is_big, s);
   ts.ready = true;
 }
 
@@ -522,67 +269,11 @@ void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs) {
     }
 }
 
-// CUTBDDC_LEVEL_SWEEPS=1 selects the level-synchronous sweeps for single
-// right-hand sides too (A/B measurement of the dataflow sweeps).
-static bool level_sweeps() {
-  static const bool v = [] {
-    const char* e = std::getenv("CUTBDDC_LEVEL_SWEEPS");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
-// In-place solve of nrhs x nsd slot vectors X ([rhs][sd][T]); masked-out
-// slots are left untouched. upd must hold nrhs * f.upd_total doubles.
-void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, int nrhs, double* upd,
-                  double* ysave, const int* skip, bool rhs_root_only) {
-  if (nrhs == 1 && !rhs_root_only && !level_sweeps()) {
-    sweep_solve(h, ts, f, X, ysave, upd, skip);
-    return;
-  }
-  cudaStream_t s = h->stream;
-  const TplDev t = tpl_dev(ts, h->slots);
-  const FactorDev fd = factor_dev(f);
-  const int nlev = (int)ts.level_first.size();
-  const size_t shm = sizeof(double) * (size_t)ts.tpl.max_rows;
-  const size_t shm_big = (sizeof(double) + sizeof(int)) * 2048;
-  if (rhs_root_only) {
-    // right-hand sides supported on the root columns only (C^T of the shell
-    // template): every lower forward step is zero, so only the root is swept.
-    CB_CUDA(cudaMemsetAsync(upd, 0, sizeof(double) * (size_t)nrhs * f.upd_total, s));
-    CB_CUDA(cudaMemsetAsync(ysave, 0, sizeof(double) * (size_t)nrhs * h->nsd * h->slots, s));
-  }
-  const std::string tag = std::string("solve") + (&f == &h->fI ? "I" : "K") + (nrhs > 1 ? "m " : " ");
-  for (int L = nlev - 1; L >= 0; --L) {
-    if (rhs_root_only && L > 0) continue;
-    ProfScope ps(h->prof, s, tag + "fwd L" + std::to_string(L));
-    if (ts.small_count[(size_t)L] > 0) {
-      dim3 grid(ts.small_count[(size_t)L], h->nsd, nrhs);
-      k_fwd_level<<<grid, 256, shm, s>>>(t, fd, ts.small_sn.p + ts.small_first[(size_t)L], h->nsd, f.panel.p, X, upd,
-                                         skip);
-      CB_LAUNCH();
-    }
-    if (ts.fwd_count[(size_t)L] > 0) {
-      dim3 grid(ts.fwd_count[(size_t)L], h->nsd, nrhs);
-      k_fwd_big<<<grid, 256, shm_big, s>>>(t, fd, ts.fwd_items.p + ts.fwd_first[(size_t)L], h->nsd, f.panel.p, X, ysave,
-                                           upd, skip);
-      CB_LAUNCH();
-    }
-  }
-  for (int L = 0; L < nlev; ++L) {
-    ProfScope ps(h->prof, s, tag + "bwd L" + std::to_string(L));
-    if (ts.bwd_count[(size_t)L] > 0) {
-      dim3 grid(ts.bwd_count[(size_t)L], h->nsd, nrhs);
-      k_bwd_big<<<grid, 256, shm_big, s>>>(t, fd, ts.bwd_items.p + ts.bwd_first[(size_t)L], h->nsd, f.panel.p, X, ysave,
-                                           skip);
-      CB_LAUNCH();
-    }
-    if (ts.small_count[(size_t)L] > 0) {
-      dim3 grid(ts.small_count[(size_t)L], h->nsd, nrhs);
-      k_bwd_level<<<grid, 256, shm, s>>>(t, fd, ts.small_sn.p + ts.small_first[(size_t)L], h->nsd, f.panel.p, X, skip);
-      CB_LAUNCH();
-    }
-  }
+// In-place solve of the nsd slot vectors X ([sd][T]) by the dataflow sweeps
+// (sweep.cu); masked-out slots are left untouched.
+void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* upd, double* ysave,
+                  const int* skip) {
+  sweep_solve(h, ts, f, X, ysave, upd, skip);
 }
 
 }  // namespace cutbddc_b200

@@ -12,7 +12,6 @@ struct TplDev {
   const AmapEntry* amap;
   const int32_t* emap;
   const int32_t* root_pos;
-  const uint8_t* is_big;
   int T;
   int nsn;
   int root;  // id of the root supernode (last in postorder)
@@ -69,11 +68,9 @@ struct FactorJob {
   bool* failed = nullptr;  // set: a non-positive pivot is reported here instead of thrown
 };
 void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs);
-// ysave: nrhs x nsd x T doubles of scratch (forward results of big fronts).
-// rhs_root_only: the right-hand sides are nonzero only on root columns (the
-// W = K^{-1} C^T solve on the shell template); the lower forward steps are skipped.
-void solve_device(cutbddc_gpu* h, const TplSet& t, const FactorSet& f, double* X, int nrhs, double* upd,
-                  double* ysave, const int* skip, bool rhs_root_only = false);
+// ysave: nsd x T doubles of scratch (forward results of big fronts).
+void solve_device(cutbddc_gpu* h, const TplSet& t, const FactorSet& f, double* X, double* upd, double* ysave,
+                  const int* skip);
 // algorithmic bytes of one forward + backward sweep (panel lower parts + front vectors)
 double sweep_bytes(const FactorSet& f);
 // sweep.cu: dataflow sweeps for one right-hand side (plan built per factorisation)

@@ -26,22 +26,9 @@
 struct TplSet {
   cutbddc_b200::Template tpl;
   cutbddc_b200::DevBuf<cutbddc_b200::Supernode> sn;
-  cutbddc_b200::DevBuf<int32_t> rows, emap, level_sn, root_pos;
+  cutbddc_b200::DevBuf<int32_t> rows, emap, root_pos;
   cutbddc_b200::DevBuf<cutbddc_b200::AmapEntry> amap;
-  std::vector<int> level_first, level_count;
-  // per level: small supernodes (one CTA each, substitution on [L11; L21])
-  // and big supernodes (explicit G = [L11^{-1}; L21 L11^{-1}] panels, swept
-  // by many CTAs as GEMVs). Work items are (supernode, chunk) pairs.
-  cutbddc_b200::DevBuf<int32_t> small_sn;       // per level, concatenated
-  std::vector<int> small_first, small_count;
-  cutbddc_b200::DevBuf<int2> fwd_items, bwd_items;  // (sn, chunk)
-  std::vector<int> fwd_first, fwd_count, bwd_first, bwd_count;
-  cutbddc_b200::DevBuf<int32_t> big_sn;         // per level, concatenated
-  std::vector<int> big_first, big_count;
-  std::vector<uint8_t> is_big;                  // per supernode
   std::vector<uint8_t> is_split;                // per supernode: tiled DAG front (else one CTA, dense_dag.cu)
-  cutbddc_b200::DevBuf<uint8_t> big_flag;
-  int max_cblocks = 0;
   bool ready = false;
 };
 
