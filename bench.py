@@ -292,19 +292,15 @@ def main():
         # caller side (untimed): classify on device, partition + objects on
         # host (replicated), this rank's subdomains assembled on its GPU
         pb, lp = cb.prepare_distributed(solver, cfg)
-        asm_ids = lp.local_block_ids
     else:
         solver = cb.GpuSolver(local)
         pb = cb.prepare(solver, cfg)
-        lp, asm_ids = None, pb.block_ids
+        lp = None
     mesh, block_ids, objs = pb.mesh, pb.block_ids, pb.objects
     n_dof = mesh.n_dof
 
-    def assemble(s, mesh_view=None):
-        d = s.assemble(cfg.block, asm_ids, mesh=mesh_view)
-        if lp is not None:
-            s.set_global_ids(len(block_ids), lp.local_sd)
-        return d
+    def assemble(s, mesh_view=None):  # the global partition; a distributed handle takes its own subdomains
+        return s.assemble(cfg.block, block_ids, mesh=mesh_view)
 
     def step_device():
         assemble(solver)                                # mesh resident on the device

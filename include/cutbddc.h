@@ -137,12 +137,14 @@ cutbddc_status cutbddc_gpu_local_diagonals(cutbddc_gpu* h, double* diag, int64_t
 cutbddc_status cutbddc_gpu_setup_bddc(cutbddc_gpu* h, const cutbddc_coarse_view* coarse, int weighting);
 
 /* krylov::pcg with A = Abar and M = BDDC apply. b may be
- * NULL to use the assembled rhs. x: n_dof output. */
+ * NULL to use the assembled rhs. x: n_dof output (a distributed handle
+ * writes the dofs it owns, see cutbddc_gpu_set_distribution). */
 cutbddc_status cutbddc_gpu_pcg(cutbddc_gpu* h, const double* b, double* x, double rtol, int max_iter,
                                cutbddc_solve_report* report);
 
-/* Test hooks: y = Abar x (SparseSymMatrix::apply, linalg.hpp:45) and
- * z = M r (bddc apply), host vectors of n_dof. */
+/* Test hooks: y = Abar x (SparseSymMatrix::apply, linalg.hpp:45; applied
+ * matrix-free as Σ_w R_w^T A_w R_w) and z = M r (bddc apply,
+ * SPEC.md:388-396), host vectors of n_dof (owned entries written). */
 cutbddc_status cutbddc_gpu_spmv(cutbddc_gpu* h, const double* x, double* y);
 cutbddc_status cutbddc_gpu_apply_bddc(cutbddc_gpu* h, const double* r, double* z);
 /* Assembled rhs b (n_dof) and coarse matrix (n_c x n_c row-major). */
@@ -219,11 +221,55 @@ cutbddc_status cutbddc_assign_subdomains(const cutbddc_partition_view* part, int
                                          int32_t* rank_of_sd);
 /* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it). */
 cutbddc_status cutbddc_nccl_unique_id(void* id128);
-/* Distributed handles: global subdomain index of each local subdomain (the
- * local partition view holds this rank's block ids, ascending). Must be
- * called after cutbddc_gpu_assemble and before cutbddc_gpu_setup_bddc; the
- * coarse view then refers to global subdomain indices. */
-cutbddc_status cutbddc_gpu_set_global_ids(cutbddc_gpu* h, int n_sd_global, const int32_t* global_of_local);
+/* Distribution of the subdomains over ranks (one process and one handle per
+ * GPU). Every rank passes the same GLOBAL partition and rank_of_sd (e.g.
+ * from cutbddc_assign_subdomains); the handle then assembles, factorises and
+ * solves the subdomains with rank_of_sd == rank, and cutbddc_gpu_assemble
+ * takes that same global partition. Call before cutbddc_gpu_assemble. With a
+ * communicator, rank / world must be the handle's own; a handle without one
+ * may take any rank's view to inspect its exchange plan
+ * (cutbddc_gpu_exchange_plan): assembly then builds the plan only, and the
+ * numerical entry points return CUTBDDC_CONFIG.
+ *
+ * Vectors at the boundary are always in global dof numbering (n_dof
+ * doubles). A distributed handle reads its local dofs from inputs and writes
+ * the dofs it OWNS into outputs (a dof is owned by the rank of its
+ * lowest-numbered subdomain: exactly one rank), leaving other entries
+ * untouched. Every scalar (dots, iteration counts, residual histories) and
+ * every owned entry is the same, bit for bit, for any world size. */
+cutbddc_status cutbddc_gpu_set_distribution(cutbddc_gpu* h, const cutbddc_partition_view* part,
+                                            const int32_t* rank_of_sd, int rank, int world);
+
+/* Interface exchange plan of one rank (dist.cu builds it on the device;
+ * cutbddc_build_exchange_plan builds the same plan on the host):
+ *   local dofs: loc_glob[n_loc] global dof ids, segment by segment — the
+ *     dofs whose lowest subdomain is local subdomain s are
+ *     [seg_ptr[s], seg_ptr[s+1]) (ascending global), the ghost dofs (owned
+ *     by another rank) follow from seg_ptr[n_sd_local];
+ *   copies of local dof i, ascending global subdomain: copy_src[copy_ptr[i]
+ *     .. copy_ptr[i+1]), >= 0: local slot index (local sd * slots + slot of
+ *     its (H/h+1)^3 lattice), < 0: receive-buffer index -1 - src;
+ *   neighbour ranks nbr[n_nbr] (ascending); message to / from nbr[k]:
+ *     send_src[send_ptr[k] .. send_ptr[k+1]) local slot indices, received
+ *     into [recv_ptr[k], recv_ptr[k+1]). Messages list the shared dofs in
+ *     ascending global dof, each dof's copies in ascending subdomain. */
+typedef struct {
+  int64_t n_loc, n_own;
+  int n_sd_local, n_nbr;
+  int32_t* loc_glob;
+  int32_t* seg_ptr;
+  int32_t* copy_ptr;
+  int32_t* copy_src;
+  int32_t* nbr;
+  int64_t* send_ptr;
+  int32_t* send_src;
+  int64_t* recv_ptr;
+} cutbddc_exchange_plan;
+cutbddc_status cutbddc_build_exchange_plan(const cutbddc_mesh_view* mesh, const cutbddc_partition_view* part,
+                                           const int32_t* rank_of_sd, int rank, int world,
+                                           cutbddc_exchange_plan** out);
+cutbddc_status cutbddc_gpu_exchange_plan(cutbddc_gpu* h, cutbddc_exchange_plan** out);
+void cutbddc_exchange_plan_free(cutbddc_exchange_plan* p);
 
 #ifdef __cplusplus
 }

@@ -1,14 +1,21 @@
-// assembly.cu — sub-assembled subdomain matrices and the global operator (K3).
+// assembly.cu — sub-assembled subdomain matrices (K3).
 //
-// assemble_subassembled and assemble_global
-// as deterministic gathers: every (row, 27-stencil column) entry sums the
-// element contributions of the <= 8 active cells around the row node in
-// ascending cell id, the same order the CPU restatement's triplet merge
-// uses (linalg.cpp:12-32 semantics), so no fp64 atomics are involved.
-// Strong-Dirichlet (orphan) dofs: all incident active cells empty ->
-// identity row in Abar, 1/|neigh| diagonal in every A^w.
+// assemble_subassembled as a deterministic gather: every
+// (slot, 27-stencil column) entry sums the element contributions of the <= 8
+// cells of the subdomain around the slot node in ascending cell id, the same
+// order the CPU restatement's triplet merge uses (linalg.cpp:12-32
+// semantics), so no fp64 atomics are involved. assemble_global
+// is not formed: Abar = Σ_w R_w^T A_w R_w is applied
+// matrix-free (dist.cu), and the load vector is the interface sum of the
+// sub-assembled ones. Only this rank's subdomains are assembled; cut cells
+// of other ranks are never integrated here (their void flags arrive by one
+// all-reduce of a byte per cell). Strong-Dirichlet (orphan) dofs: all
+// incident active cells empty -> 1/|neigh| diagonal in every A^w, so the sum
+// over copies is the identity row of Abar.
 #include <cub/cub.cuh>
 
+#include "comm.cuh"
+#include "dist.cuh"
 #include "handle.cuh"
 
 namespace cutbddc_b200 {
@@ -18,22 +25,33 @@ void interior_element_device(cutbddc_gpu* h, double* kint, double* fint);
 
 namespace {
 
-__global__ void k_cell_flags(int64_t nc, const uint8_t* __restrict__ cls, uint8_t* __restrict__ act,
+// active cells; cut cells of this rank's subdomains
+__global__ void k_cell_flags(int64_t nc, int n, int B, int nb, const uint8_t* __restrict__ cls,
+                             const int32_t* __restrict__ sd_of_block, uint8_t* __restrict__ act,
                              uint8_t* __restrict__ cut) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
     act[c] = cls[c] != CUTBDDC_EXTERIOR;
-    cut[c] = cls[c] == CUTBDDC_CUT;
+    const int64_t k = c % n, j = (c / n) % n, i = c / n / n;
+    cut[c] = cls[c] == CUTBDDC_CUT && sd_of_block[((i / B) * nb + j / B) * nb + k / B] >= 0;
   }
 }
 
+// -2 exterior, -1 interior, -3 cut (another rank's, or until k_scatter_cut)
 __global__ void k_elem_of_cell(int64_t nc, const uint8_t* __restrict__ cls, int32_t* __restrict__ eoc) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x)
-    eoc[c] = cls[c] == CUTBDDC_EXTERIOR ? -2 : -1;
+    eoc[c] = cls[c] == CUTBDDC_EXTERIOR ? -2 : (cls[c] == CUTBDDC_CUT ? -3 : -1);
 }
 
 __global__ void k_scatter_cut(int64_t ncut, const int64_t* __restrict__ cut_cells, int32_t* __restrict__ eoc) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e < ncut) eoc[cut_cells[e]] = (int32_t)e;
+}
+
+// void flag of this rank's cut cells (all-reduced by max over ranks)
+__global__ void k_vcell(int64_t ncut, const int64_t* __restrict__ cut_cells, const uint8_t* __restrict__ empty,
+                        uint8_t* __restrict__ vcell) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < ncut) vcell[cut_cells[e]] = empty[e];
 }
 
 __global__ void k_sd_of_block(int nsd, const int64_t* __restrict__ bids, int32_t* __restrict__ sob) {
@@ -68,9 +86,9 @@ __device__ inline const double* elem_k(const MeshArgs& m, int64_t cell, const do
   return m.ke + (int64_t)e * 64;
 }
 
-// per dof: |neigh| (distinct blocks among incident active cells), how many of
-// them are this handle's subdomains, orphan flag
-__global__ void k_dof_info(int64_t ndof, MeshArgs m, uint8_t* __restrict__ ncount, uint8_t* __restrict__ lcount,
+// per dof: |neigh| (distinct blocks among incident active cells, every
+// rank's) and the orphan flag (every incident active cell void)
+__global__ void k_dof_info(int64_t ndof, MeshArgs m, const uint8_t* __restrict__ vcell, uint8_t* __restrict__ ncount,
                            uint8_t* __restrict__ orphan) {
   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (d >= ndof) return;
@@ -88,68 +106,21 @@ __global__ void k_dof_info(int64_t ndof, MeshArgs m, uint8_t* __restrict__ ncoun
         const int64_t cell = ((int64_t)ci * n + cj) * n + ck;
         const int32_t e = m.eoc[cell];
         if (e == -2) continue;
-        if (e == -1 || !m.empty[e]) nonvoid = true;
+        if (e == -1 || !vcell[cell]) nonvoid = true;
         const int64_t bid = ((int64_t)(ci / m.B) * m.nb + cj / m.B) * m.nb + ck / m.B;
         bool seen = false;
         for (int q = 0; q < nbk; ++q) seen |= blks[q] == bid;
         if (!seen) blks[nbk++] = bid;
       }
-  int nloc = 0;
-  for (int q = 0; q < nbk; ++q) nloc += m.sd_of_block[blks[q]] >= 0;
   ncount[d] = (uint8_t)nbk;
-  lcount[d] = (uint8_t)nloc;
   orphan[d] = !nonvoid;
 }
 
-// Abar as ELL-27 (SoA): row = dof; column k = node + stencil offset.
-__global__ void k_abar(int64_t ndof, MeshArgs m, const uint8_t* __restrict__ orphan, double* __restrict__ aval,
-                       int32_t* __restrict__ acol, double* __restrict__ b) {
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= ndof) return;
-  const int n = m.n;
-  const int64_t v = m.node_of_dof[d];
-  const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
-  double acc[27];
-#pragma unroll
-  for (int q = 0; q < 27; ++q) acc[q] = 0.0;
-  double bb = 0.0;
-  for (int dx = 0; dx < 2; ++dx)
-    for (int dy = 0; dy < 2; ++dy)
-      for (int dz = 0; dz < 2; ++dz) {
-        const int ci = i - 1 + dx, cj = j - 1 + dy, ck = k - 1 + dz;
-        if (ci < 0 || cj < 0 || ck < 0 || ci >= n || cj >= n || ck >= n) continue;
-        const double* f = nullptr;
-        const double* K = elem_k(m, ((int64_t)ci * n + cj) * n + ck, &f);
-        if (!K) continue;
-        const int lv = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
-        bb += f[lv];
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const int q = stencil_k((w & 1) - (lv & 1), ((w >> 1) & 1) - ((lv >> 1) & 1), ((w >> 2) & 1) - ((lv >> 2) & 1));
-          acc[q] += K[lv * 8 + w];
-        }
-      }
-  if (orphan[d]) {
-#pragma unroll
-    for (int q = 0; q < 27; ++q) acc[q] = 0.0;
-    acc[13] = 1.0;
-    bb = 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < 27; ++q) {
-    const int ii = i + q / 9 - 1, jj = j + (q / 3) % 3 - 1, kk = k + q % 3 - 1;
-    int32_t col = -1;
-    if (ii >= 0 && jj >= 0 && kk >= 0 && ii <= n && jj <= n && kk <= n)
-      col = m.dof_of_node[((int64_t)ii * (n + 1) + jj) * (n + 1) + kk];
-    acol[(int64_t)q * ndof + d] = col < 0 ? (int32_t)d : col;
-    aval[(int64_t)q * ndof + d] = col < 0 ? 0.0 : acc[q];
-  }
-  b[d] = bb;
-}
-
-// A^w in slot space: thread per (subdomain, slot).
+// A^w in slot space, its load vector and the strong-Dirichlet diagonal:
+// thread per (subdomain, slot).
 __global__ void k_subassemble(int nsd, MeshArgs m, const int64_t* __restrict__ bids, const uint8_t* __restrict__ orphan,
-                              const uint8_t* __restrict__ ncount, int32_t* __restrict__ slot_dof, double* __restrict__ As) {
+                              const uint8_t* __restrict__ ncount, int32_t* __restrict__ slot_dof, double* __restrict__ As,
+                              double* __restrict__ fs, double* __restrict__ odiag) {
   const int T = m.T;
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid >= (int64_t)nsd * T) return;
@@ -162,6 +133,7 @@ __global__ void k_subassemble(int nsd, MeshArgs m, const int64_t* __restrict__ b
   double acc[27];
 #pragma unroll
   for (int q = 0; q < 27; ++q) acc[q] = 0.0;
+  double bb = 0.0, od = 0.0;
   bool local = false;
   for (int dx = 0; dx < 2; ++dx)
     for (int dy = 0; dy < 2; ++dy)
@@ -175,6 +147,7 @@ __global__ void k_subassemble(int nsd, MeshArgs m, const int64_t* __restrict__ b
         const double* K = elem_k(m, cell, &f);
         if (!K) continue;
         const int lv = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+        bb += f[lv];
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
           const int q = stencil_k((w & 1) - (lv & 1), ((w >> 1) & 1) - ((lv >> 1) & 1), ((w >> 2) & 1) - ((lv >> 2) & 1));
@@ -187,60 +160,25 @@ __global__ void k_subassemble(int nsd, MeshArgs m, const int64_t* __restrict__ b
     if (orphan[dof]) {
 #pragma unroll
       for (int q = 0; q < 27; ++q) acc[q] = 0.0;
-      acc[13] = 1.0 / (double)ncount[dof];
+      acc[13] = od = 1.0 / (double)ncount[dof];
+      bb = 0.0;
     }
   }
   slot_dof[gid] = dof;
+  fs[gid] = bb;
+  odiag[gid] = od;
   double* A = As + (int64_t)s * 27 * T + t;
 #pragma unroll
   for (int q = 0; q < 27; ++q) A[(int64_t)q * T] = acc[q];
 }
 
-// per dof: its (subdomain, slot) copies in this handle's subdomains, ascending
-// subdomain order; owner slot for interior dofs of this handle's subdomains.
-__global__ void k_copies(int64_t ndof, MeshArgs m, const int64_t* __restrict__ copy_ptr, int64_t* __restrict__ copy_idx,
-                         int64_t* __restrict__ owner) {
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= ndof) return;
-  const int n = m.n, B = m.B, b1 = B + 1;
-  const int64_t v = m.node_of_dof[d];
-  const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
-  int64_t blks[8];
-  int nbk = 0;
-  for (int dx = 0; dx < 2; ++dx)
-    for (int dy = 0; dy < 2; ++dy)
-      for (int dz = 0; dz < 2; ++dz) {
-        const int ci = i - 1 + dx, cj = j - 1 + dy, ck = k - 1 + dz;
-        if (ci < 0 || cj < 0 || ck < 0 || ci >= n || cj >= n || ck >= n) continue;
-        if (m.eoc[((int64_t)ci * n + cj) * n + ck] == -2) continue;
-        const int64_t bid = ((int64_t)(ci / B) * m.nb + cj / B) * m.nb + ck / B;
-        bool seen = false;
-        for (int q = 0; q < nbk; ++q) seen |= blks[q] == bid;
-        if (!seen) blks[nbk++] = bid;
-      }
-  // ascending block id == ascending subdomain id
-  for (int a = 1; a < nbk; ++a)
-    for (int c = a; c > 0 && blks[c - 1] > blks[c]; --c) {
-      const int64_t tmp = blks[c];
-      blks[c] = blks[c - 1];
-      blks[c - 1] = tmp;
-    }
-  const int64_t p = copy_ptr[d];
-  int nloc = 0;
-  for (int q = 0; q < nbk; ++q) {
-    const int64_t bid = blks[q];
-    const int32_t sd = m.sd_of_block[bid];
-    if (sd < 0) continue;  // another rank's subdomain
-    const int bi = (int)(bid / m.nb / m.nb), bj = (int)((bid / m.nb) % m.nb), bk = (int)(bid % m.nb);
-    const int slot = ((i - bi * B) * b1 + (j - bj * B)) * b1 + (k - bk * B);
-    copy_idx[p + nloc++] = (int64_t)sd * m.T + slot;
-  }
-  owner[d] = nbk == 1 && nloc == 1 ? copy_idx[p] : -1;
-}
-
-__global__ void k_u8_to_i64(int64_t n, const uint8_t* __restrict__ a, int64_t* __restrict__ b) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) b[i] = a[i];
+__global__ void k_masks(int64_t ns, const int32_t* __restrict__ slot_dof, const uint8_t* __restrict__ ncount,
+                        uint8_t* __restrict__ mall, uint8_t* __restrict__ mint) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  const int32_t d = slot_dof[g];
+  mall[g] = d >= 0;
+  mint[g] = d >= 0 && ncount[d] == 1;
 }
 
 struct IsInterface {
@@ -250,30 +188,40 @@ struct IsInterface {
 
 }  // namespace
 
-void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_ids) {
+void assemble_device(cutbddc_gpu* h, const cutbddc_partition_view* part) {
   cudaStream_t s = h->stream;
-  const int n = h->n;
+  const int n = h->n, block = part->block;
   if (block < 1 || n % block != 0) throw Failure(CUTBDDC_INVALID_ARGUMENT, "partition: mesh dims not divisible by H/h");
+  // the distribution: set by the caller (every rank passes the global
+  // partition) or every subdomain on this handle
+  if (!h->dist_explicit) {
+    dist_default(h, part);
+  } else if (h->dist_block != block || h->nsd_g != part->n_sd ||
+             !std::equal(h->g_block_ids.begin(), h->g_block_ids.end(), part->block_ids)) {
+    throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble: partition differs from the distribution's");
+  }
   h->block = block;
   h->b1 = block + 1;
   h->slots = h->b1 * h->b1 * h->b1;
   h->nb = n / block;
+  const int nsd = (int)h->global_of_local.size();
   h->nsd = nsd;
-  h->nsd_global = 0;  // local numbering until cutbddc_gpu_set_global_ids
-  h->global_of_local.clear();
-  h->h_block_ids.assign(block_ids, block_ids + nsd);
-  for (int i = 1; i < nsd; ++i)
-    if (block_ids[i] <= block_ids[i - 1]) throw Failure(CUTBDDC_INVALID_ARGUMENT, "partition: block ids must ascend");
+  h->h_block_ids.resize((size_t)nsd);
+  for (int i = 0; i < nsd; ++i) h->h_block_ids[(size_t)i] = h->g_block_ids[(size_t)h->global_of_local[(size_t)i]];
   h->block_ids.upload(h->h_block_ids, s);
   const int64_t nc = h->n_cells;
   const int grid = 148 * 8;
   ProfScope ps(h->prof, s, "assembly 1 cell lists");
-  // active / cut cell lists (ascending)
+  h->sd_of_block.alloc((size_t)h->nb * h->nb * h->nb);
+  CB_CUDA(cudaMemsetAsync(h->sd_of_block.p, 0xff, h->sd_of_block.n * 4, s));
+  k_sd_of_block<<<grid_for(nsd, 256), 256, 0, s>>>(nsd, h->block_ids.p, h->sd_of_block.p);
+  CB_LAUNCH();
+  // active cells (all) / cut cells of this rank's subdomains (ascending)
   DevBuf<uint8_t>& act = h->ws_act;
   DevBuf<uint8_t>& cut = h->ws_cut;
   act.alloc((size_t)nc);
   cut.alloc((size_t)nc);
-  k_cell_flags<<<grid, 256, 0, s>>>(nc, h->cls.p, act.p, cut.p);
+  k_cell_flags<<<grid, 256, 0, s>>>(nc, n, block, h->nb, h->cls.p, h->sd_of_block.p, act.p, cut.p);
   CB_LAUNCH();
   DevBuf<int64_t>& cnt = h->ws_cnt;
   cnt.alloc(2);
@@ -299,61 +247,62 @@ void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_id
     k_scatter_cut<<<grid_for(h->n_cut, 256), 256, 0, s>>>(h->n_cut, h->cut_cells.p, h->elem_of_cell.p);
     CB_LAUNCH();
   }
-  // element matrices
+  // element matrices of this rank's cut cells
   ps.next("assembly 2 cut elements");
   cut_elements_device(h);
   DevBuf<double>& kint = h->ws_kint;
   kint.alloc(72);
   interior_element_device(h, kint.p, kint.p + 64);
-  // subdomain maps
-  ps.next("assembly 3 abar+subassembly+copies");
-  h->sd_of_block.alloc((size_t)h->nb * h->nb * h->nb);
-  CB_CUDA(cudaMemsetAsync(h->sd_of_block.p, 0xff, h->sd_of_block.n * 4, s));
-  k_sd_of_block<<<grid_for(nsd, 256), 256, 0, s>>>(nsd, h->block_ids.p, h->sd_of_block.p);
-  CB_LAUNCH();
+  ps.next("assembly 3 subassembly+plan+rhs");
+  // void cut cells of every rank: one byte per cell, all-reduced (max)
+  h->vcell.alloc((size_t)nc);
+  h->vcell.zero(s);
+  if (h->n_cut) {
+    k_vcell<<<grid_for(h->n_cut, 256), 256, 0, s>>>(h->n_cut, h->cut_cells.p, h->empty.p, h->vcell.p);
+    CB_LAUNCH();
+  }
+  // plan-only distribution (a rank's view without a communicator, for plan
+  // inspection): other ranks' void cells and the load vector are unknown
+  const bool plan_only = h->dist_world > 1 && !h->comm;
+  if (h->dist_world > 1 && !plan_only)
+    nccl_check(ncclAllReduce(h->vcell.p, h->vcell.p, (size_t)nc, ncclUint8, ncclMax, h->comm, s), "void cells");
   MeshArgs m{n, block, h->nb, h->slots, h->elem_of_cell.p, h->dof_of_node.p, h->node_of_dof.p,
              h->ke.p, h->fe.p, h->empty.p, kint.p, kint.p + 64, h->sd_of_block.p};
   const int64_t nd = h->n_dof;
   h->ncount.alloc((size_t)nd);
-  h->lcount.alloc((size_t)nd);
   h->orphan.alloc((size_t)nd);
-  k_dof_info<<<grid_for(nd, 256), 256, 0, s>>>(nd, m, h->ncount.p, h->lcount.p, h->orphan.p);
-  CB_LAUNCH();
-  h->aval.alloc((size_t)nd * 27);
-  h->acol.alloc((size_t)nd * 27);
-  h->b.alloc((size_t)nd);
-  k_abar<<<grid_for(nd, 128), 128, 0, s>>>(nd, m, h->orphan.p, h->aval.p, h->acol.p, h->b.p);
+  k_dof_info<<<grid_for(nd, 256), 256, 0, s>>>(nd, m, h->vcell.p, h->ncount.p, h->orphan.p);
   CB_LAUNCH();
   const int64_t ns = (int64_t)nsd * h->slots;
   h->slot_dof.alloc((size_t)ns);
   h->As.alloc((size_t)ns * 27);
-  k_subassemble<<<grid_for(ns, 128), 128, 0, s>>>(nsd, m, h->block_ids.p, h->orphan.p, h->ncount.p, h->slot_dof.p, h->As.p);
+  h->fs.alloc((size_t)ns);
+  h->odiag.alloc((size_t)ns);
+  k_subassemble<<<grid_for(ns, 128), 128, 0, s>>>(nsd, m, h->block_ids.p, h->orphan.p, h->ncount.p, h->slot_dof.p, h->As.p,
+                                                  h->fs.p, h->odiag.p);
   CB_LAUNCH();
-  // copies CSR
-  DevBuf<int64_t>& nc64 = h->ws_nc64;
-  nc64.alloc((size_t)nd);
-  k_u8_to_i64<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->lcount.p, nc64.p);
+  h->mask_all.alloc((size_t)ns);
+  h->mask_int.alloc((size_t)ns);
+  k_masks<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->ncount.p, h->mask_all.p, h->mask_int.p);
   CB_LAUNCH();
-  h->copy_ptr.alloc((size_t)nd + 1);
-  CB_CUDA(cudaMemsetAsync(h->copy_ptr.p, 0, sizeof(int64_t), s));
-  tb = 0;
-  CB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, nc64.p, h->copy_ptr.p + 1, nd, s));
-  tmp.alloc(std::max(tmp.n, tb));
-  CB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, nc64.p, h->copy_ptr.p + 1, nd, s));
-  CB_CUDA(cudaMemcpyAsync(&h->n_copies, h->copy_ptr.p + nd, 8, cudaMemcpyDeviceToHost, s));
-  CB_CUDA(cudaStreamSynchronize(s));
-  h->copy_idx.alloc((size_t)h->n_copies);
-  h->owner_slot.alloc((size_t)nd);
-  k_copies<<<grid_for(nd, 256), 256, 0, s>>>(nd, m, h->copy_ptr.p, h->copy_idx.p, h->owner_slot.p);
-  CB_LAUNCH();
-  // interface dof list
-  h->if_dofs.alloc((size_t)nd);
+  // local dof space, copy and exchange lists
+  build_plan_device(h);
+  // load vector: interface sum of the sub-assembled ones
+  h->b.alloc((size_t)std::max<int64_t>(1, h->n_loc));
+  h->plan_only = plan_only;
+  if (!plan_only) {
+    iface_exchange(h, h->fs.p, nullptr, nullptr);
+    iface_sum(h, h->fs.p, nullptr, h->b.p, nullptr);
+  }
+  // interface dofs of the global problem
+  DevBuf<int32_t>& ifd = h->ws_glist;
+  ifd.alloc((size_t)nd);
   cub::CountingInputIterator<int32_t> it32(0);
   IsInterface pred{h->ncount.p};
   tb = 0;
-  CB_CUDA(cub::DeviceSelect::If(nullptr, tb, it32, h->if_dofs.p, cnt.p, (int32_t)nd, pred, s));
+  CB_CUDA(cub::DeviceSelect::If(nullptr, tb, it32, ifd.p, cnt.p, (int32_t)nd, pred, s));
   tmp.alloc(std::max(tmp.n, tb));
-  CB_CUDA(cub::DeviceSelect::If(tmp.p, tb, it32, h->if_dofs.p, cnt.p, (int32_t)nd, pred, s));
+  CB_CUDA(cub::DeviceSelect::If(tmp.p, tb, it32, ifd.p, cnt.p, (int32_t)nd, pred, s));
   CB_CUDA(cudaMemcpyAsync(&h->n_if, cnt.p, 8, cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
   h->assembled = true;

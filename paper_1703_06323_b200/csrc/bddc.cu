@@ -21,37 +21,24 @@
 #include "bddc.cuh"
 #include "factor.cuh"
 #include "comm.cuh"
+#include "dist.cuh"
 #include "subst.cuh"
 
 namespace cutbddc_b200 {
 namespace {
 
-__global__ void k_masks(int64_t ns, const int32_t* __restrict__ slot_dof, const uint8_t* __restrict__ ncount,
-                        uint8_t* __restrict__ mall, uint8_t* __restrict__ mint) {
+// slot vector of the A^w diagonals (input of the stiffness-weight denominators)
+__global__ void k_diag_slots(int64_t ns, int T, const double* __restrict__ As, double* __restrict__ dg) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ns) return;
-  const int32_t d = slot_dof[g];
-  mall[g] = d >= 0;
-  mint[g] = d >= 0 && ncount[d] == 1;
+  dg[g] = As[(g / T) * 27 * T + 13ll * T + g % T];
 }
 
-// per dof: sum of the A^w diagonals over this handle's copies, ascending sd
-// (the stiffness-weight denominator; all-reduced over ranks when distributed)
-__global__ void k_dtot(int64_t nd, int T, const double* __restrict__ As, const int64_t* __restrict__ copy_ptr,
-                       const int64_t* __restrict__ copy_idx, double* __restrict__ tot) {
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= nd) return;
-  double s = 0.0;
-  for (int64_t p = copy_ptr[d]; p < copy_ptr[d + 1]; ++p) {
-    const int64_t ci = copy_idx[p];
-    s += As[(ci / T) * 27 * T + 13ll * T + ci % T];
-  }
-  tot[d] = s;
-}
-
+// dtot: per local dof, the sum of the A^w diagonals over every copy (all ranks)
 __global__ void k_weights(int64_t ns, int T, int mode, const int32_t* __restrict__ slot_dof,
-                          const uint8_t* __restrict__ ncount, const double* __restrict__ As,
-                          const double* __restrict__ dtot, double* __restrict__ w, int* __restrict__ bad) {
+                          const int32_t* __restrict__ slot_loc, const uint8_t* __restrict__ ncount,
+                          const double* __restrict__ As, const double* __restrict__ dtot, double* __restrict__ w,
+                          int* __restrict__ bad) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ns) return;
   const int32_t d = slot_dof[g];
@@ -68,7 +55,7 @@ __global__ void k_weights(int64_t ns, int T, int mode, const int32_t* __restrict
     w[g] = 1.0 / (double)k;
     return;
   }
-  const double tot = dtot[d];
+  const double tot = dtot[slot_loc[g]];
   if (!(tot != 0.0)) {
     atomicExch(bad, 1);
     w[g] = 0.0;
@@ -162,65 +149,70 @@ __global__ void k_small_spd_inverse(int nblk, const int64_t* __restrict__ m_off,
   for (int q = threadIdx.x; q < m * m; q += blockDim.x) g[q] = a[q];
 }
 
-// coarse row lambda: sum over its (sd, local row) copies in ascending sd.
+// coarse row lambda: sum over its (sd, local row) copies in ascending global
+// sd. Rows and the m x m blocks A_c,w are addressed in the gathered staging
+// layout (rank-major, dist.cuh): p = staging position of a constraint row,
+// srow = {staging position of its subdomain's first row, m, staging offset
+// of the subdomain's block}, scoarse = coarse id of every staged row.
 __global__ void k_coarse_assemble(int nc, const int64_t* __restrict__ cg_ptr, const int64_t* __restrict__ cg_idx,
-                                  const int32_t* __restrict__ row_sd, const int64_t* __restrict__ m_off,
-                                  const int64_t* __restrict__ s_off, const int32_t* __restrict__ coarse_id,
+                                  const int64_t* __restrict__ srow, const int32_t* __restrict__ scoarse,
                                   const double* __restrict__ Ac, double* __restrict__ A) {
   const int lam = blockIdx.x;
   double* arow = A + (int64_t)lam * nc;
   for (int64_t p = cg_ptr[lam]; p < cg_ptr[lam + 1]; ++p) {
     const int64_t row = cg_idx[p];
-    const int sd = row_sd[row];
-    const int m = (int)(m_off[sd + 1] - m_off[sd]);
-    const int i = (int)(row - m_off[sd]);
-    for (int c = threadIdx.x; c < m; c += blockDim.x) arow[coarse_id[m_off[sd] + c]] += Ac[s_off[sd] + (int64_t)i * m + c];
+    const int64_t first = srow[3 * row];
+    const int m = (int)srow[3 * row + 1];
+    const int i = (int)(row - first);
+    const double* blk = Ac + srow[3 * row + 2] + (int64_t)i * m;
+    for (int c = threadIdx.x; c < m; c += blockDim.x) arow[scoarse[first + c]] += blk[c];
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ apply
-__global__ void k_gather_masked(int64_t ns, const int32_t* __restrict__ slot_dof, const uint8_t* __restrict__ mask,
+// Vectors are in the rank's local dof space (dist.cuh); slot vectors per
+// local subdomain.
+__global__ void k_gather_masked(int64_t ns, const int32_t* __restrict__ slot_loc, const uint8_t* __restrict__ mask,
                                 const double* __restrict__ r, double* __restrict__ X, const int* __restrict__ skip) {
   if (skip && *skip) return;
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ns) return;
-  X[g] = mask[g] ? r[slot_dof[g]] : 0.0;
+  X[g] = mask[g] ? r[slot_loc[g]] : 0.0;
 }
 
-__global__ void k_z0(int64_t nd, const int64_t* __restrict__ owner, const double* __restrict__ X,
+// z0 = the interior solution at interior dofs (one copy), 0 elsewhere
+__global__ void k_z0(int64_t nloc, const int32_t* __restrict__ owner, const double* __restrict__ X,
                      double* __restrict__ z0, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= nd) return;
-  const int64_t o = owner[d];
-  z0[d] = o >= 0 ? X[o] : 0.0;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  const int32_t o = owner[i];
+  z0[i] = o >= 0 ? X[o] : 0.0;
 }
 
-// r1 = r - Abar z0 on interface rows, 0 on interior rows
-__global__ void k_r1(int64_t nd, const uint8_t* __restrict__ ncount, const double* __restrict__ aval,
-                     const int32_t* __restrict__ acol, const double* __restrict__ r, const double* __restrict__ z0,
-                     double* __restrict__ r1, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= nd) return;
-  if (ncount[d] < 2) {
-    r1[d] = 0.0;
-    return;
-  }
-  double s = 0.0;
-#pragma unroll
-  for (int k = 0; k < 27; ++k) s += aval[(int64_t)k * nd + d] * z0[acol[(int64_t)k * nd + d]];
-  r1[d] = r[d] - s;
-}
-
-__global__ void k_scatter_weighted(int64_t ns, const int32_t* __restrict__ slot_dof, const double* __restrict__ w,
-                                   const double* __restrict__ r1, double* __restrict__ X, const int* __restrict__ skip) {
+// X[slot] = w * r1[dof] with r1 = r - Abar z0 on interface rows and 0 on
+// interior rows; (Abar z0)[dof] = Σ over the copies,
+// ascending global sd, of (A_w z0_w)[slot] (Y, remote copies from recv)
+__global__ void k_scatter_r1(int64_t ns, const int32_t* __restrict__ slot_loc, const uint8_t* __restrict__ mint,
+                             const double* __restrict__ w, const double* __restrict__ r,
+                             const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
+                             const double* __restrict__ Y, const double* __restrict__ recv, double* __restrict__ X,
+                             const int* __restrict__ skip) {
   if (skip && *skip) return;
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ns) return;
-  const int32_t d = slot_dof[g];
-  X[g] = d >= 0 ? w[g] * r1[d] : 0.0;
+  const int32_t l = slot_loc[g];
+  if (l < 0 || mint[g]) {
+    X[g] = 0.0;
+    return;
+  }
+  double az = 0.0;
+  for (int32_t p = cptr[l]; p < cptr[l + 1]; ++p) {
+    const int32_t c = csrc[p];
+    az += c >= 0 ? Y[c] : recv[-1 - c];
+  }
+  X[g] = w[g] * (r[l] - az);
 }
 
 // cy[row] = C_row . y
@@ -363,67 +355,27 @@ __global__ void k_xty(int n, const double* __restrict__ X, const double* __restr
   if (lane == 0) z[j] = s;
 }
 
-// v[d] = sum over copies (ascending sd) of w * Y
-__global__ void k_gather_weighted(int64_t nd, const int64_t* __restrict__ copy_ptr, const int64_t* __restrict__ copy_idx,
-                                  const double* __restrict__ w, const double* __restrict__ Y, double* __restrict__ v,
-                                  const int* __restrict__ skip) {
+// z = z0 + v - X[owner] over the local dofs (interior dofs: minus the
+// harmonic correction), a block per segment (dist.cuh); with r, every local
+// subdomain's partial of r.z for the PCG (bit-reproducible for any world size)
+__global__ void __launch_bounds__(kSegThreads) k_final_z(SegArgs a, const int32_t* __restrict__ owner,
+                                                         const double* __restrict__ z0, const double* __restrict__ v,
+                                                         const double* __restrict__ X, double* __restrict__ z,
+                                                         const double* __restrict__ r, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= nd) return;
-  double s = 0.0;
-  for (int64_t p = copy_ptr[d]; p < copy_ptr[d + 1]; ++p) {
-    const int64_t c = copy_idx[p];
-    s += w[c] * Y[c];
+  __shared__ double sh[32];
+  int lo, hi;
+  const bool part = seg_range(a, lo, hi);
+  double acc = 0.0;
+  for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
+    const int32_t o = owner[i];
+    const double zi = z0[i] + v[i] - (o >= 0 ? X[o] : 0.0);
+    z[i] = zi;
+    if (r) acc += r[i] * zi;
   }
-  v[d] = s;
-}
-
-// X[sd][slot] = (Abar v)[dof] on interior slots, 0 elsewhere
-__global__ void k_interior_av(int64_t ns, int64_t nd, const int32_t* __restrict__ slot_dof, const uint8_t* __restrict__ mint,
-                              const double* __restrict__ aval, const int32_t* __restrict__ acol,
-                              const double* __restrict__ v, double* __restrict__ X, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= ns) return;
-  if (!mint[g]) {
-    X[g] = 0.0;
-    return;
-  }
-  const int64_t d = slot_dof[g];
-  double s = 0.0;
-#pragma unroll
-  for (int k = 0; k < 27; ++k) s += aval[(int64_t)k * nd + d] * v[acol[(int64_t)k * nd + d]];
-  X[g] = s;
-}
-
-__global__ void k_final_z(int64_t nd, const int64_t* __restrict__ owner, const double* __restrict__ z0,
-                          const double* __restrict__ v, const double* __restrict__ X, double* __restrict__ z,
-                          const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= nd) return;
-  const int64_t o = owner[d];
-  z[d] = z0[d] + v[d] - (o >= 0 ? X[o] : 0.0);
-}
-
-// distributed form of k_final_z: c[d] = -X[owner] on this rank's interior
-// dofs (all-reduced: each interior dof has exactly one owner), then
-// z = (z0 + v) + c, which equals z0 + v - X[owner] bit for bit.
-__global__ void k_owned_neg(int64_t nd, const int64_t* __restrict__ owner, const double* __restrict__ X,
-                            double* __restrict__ c, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= nd) return;
-  const int64_t o = owner[d];
-  c[d] = o >= 0 ? -X[o] : 0.0;
-}
-
-__global__ void k_final_sum(int64_t nd, const double* __restrict__ z0, const double* __restrict__ v,
-                            const double* __restrict__ c, double* __restrict__ z, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (d >= nd) return;
-  z[d] = z0[d] + v[d] + c[d];
+  if (!r || !part) return;
+  acc = block_sum<kSegThreads>(acc, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
 }
 
 // ---------------------------------------------------------------- root-space coarse basis
@@ -894,7 +846,8 @@ void coarse_basis_corner(cutbddc_gpu* h, const std::vector<int64_t>& m_off, cons
   k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
   CB_LAUNCH();
   invert_schur(h, S.p);
-  k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, h->corner_row.p, h->sinv.p, h->ac_loc.p);
+  k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, h->corner_row.p, h->sinv.p,
+                                    h->ac_loc.p + (int64_t)h->dist_rank * h->maxac);
   CB_LAUNCH();
 }
 
@@ -911,35 +864,73 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     cudaGraphExecDestroy(h->graph_exec);
     h->graph_exec = nullptr;
   }
-  // ---- host: constraint rows per subdomain from the coarse objects
+  if (h->graph_exec_ref) {
+    cudaGraphExecDestroy(h->graph_exec_ref);
+    h->graph_exec_ref = nullptr;
+  }
+  if (h->plan_only) throw Failure(CUTBDDC_CONFIG, "setup_bddc: plan-only distribution (no communicator)");
+  // ---- host: constraint rows per subdomain from the coarse objects. The
+  // coarse view names global subdomains (every rank passes the same view).
+  // Local rows: this rank's subdomains in order, objects ascending. Staged
+  // rows (the rank-major layout the coarse all-gathers fill, dist.cuh): every
+  // subdomain's rows at rank(sd) * maxrows + (rows of that rank's earlier
+  // subdomains); one rank: staged == local.
   ProfScope ps_host(h->prof, s, "setup 0 host rows+uploads+weights");
   const int nc = cv ? cv->n_objects : 0;
+  const int nsd_g = h->nsd_g, world = h->dist_world, rank = h->dist_rank;
   std::vector<int64_t> node_of_dof = h->node_of_dof.to_host(s);
-  std::vector<std::vector<int>> rows_of_sd((size_t)nsd);  // object ids per sd (coarse order)
-  // the coarse view names global subdomains; keep the rows of this rank's
-  const int nsd_g = h->nsd_global > 0 ? h->nsd_global : nsd;
-  std::vector<int32_t> local_of_global((size_t)nsd_g, -1);
-  for (int sd = 0; sd < nsd; ++sd)
-    local_of_global[(size_t)(h->nsd_global > 0 ? h->global_of_local[(size_t)sd] : sd)] = sd;
+  std::vector<std::vector<int>> obj_of_gsd((size_t)nsd_g);  // object ids per global sd (ascending)
   for (int o = 0; o < nc; ++o)
     for (int64_t p = cv->neigh_ptr[o]; p < cv->neigh_ptr[o + 1]; ++p) {
       const int sg = cv->neigh[p];
       if (sg < 0 || sg >= nsd_g) throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: neighbour subdomain out of range");
-      const int sd = local_of_global[(size_t)sg];
-      if (sd >= 0) rows_of_sd[(size_t)sd].push_back(o);
+      if (!obj_of_gsd[(size_t)sg].empty() && obj_of_gsd[(size_t)sg].back() >= o)
+        throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: repeated neighbour subdomain");
+      obj_of_gsd[(size_t)sg].push_back(o);
     }
+  std::vector<int64_t> rows_of_rank((size_t)world, 0), ac_of_rank((size_t)world, 0), roff_g((size_t)nsd_g),
+      aoff_g((size_t)nsd_g);
+  int64_t m_total_g = 0;
+  for (int g = 0; g < nsd_g; ++g) {
+    const int q = h->rank_of_gsd[(size_t)g];
+    const int64_t m = (int64_t)obj_of_gsd[(size_t)g].size();
+    roff_g[(size_t)g] = rows_of_rank[(size_t)q];
+    aoff_g[(size_t)g] = ac_of_rank[(size_t)q];
+    rows_of_rank[(size_t)q] += m;
+    ac_of_rank[(size_t)q] += m * m;
+    m_total_g += m;
+  }
+  h->maxrows = std::max<int64_t>(1, *std::max_element(rows_of_rank.begin(), rows_of_rank.end()));
+  h->maxac = std::max<int64_t>(1, *std::max_element(ac_of_rank.begin(), ac_of_rank.end()));
+  h->m_total_g = m_total_g;
+  const int64_t nstage = (int64_t)world * h->maxrows;
+  std::vector<int64_t> srow((size_t)3 * nstage, 0);
+  std::vector<int32_t> scoarse((size_t)nstage, 0);
+  std::vector<std::vector<int64_t>> cg((size_t)nc);
+  for (int g = 0; g < nsd_g; ++g) {
+    const int q = h->rank_of_gsd[(size_t)g];
+    const int64_t first = (int64_t)q * h->maxrows + roff_g[(size_t)g];
+    const int64_t m = (int64_t)obj_of_gsd[(size_t)g].size();
+    for (int64_t a2 = 0; a2 < m; ++a2) {
+      const int64_t p = first + a2;
+      srow[(size_t)(3 * p)] = first;
+      srow[(size_t)(3 * p + 1)] = m;
+      srow[(size_t)(3 * p + 2)] = (int64_t)q * h->maxac + aoff_g[(size_t)g];
+      const int o = obj_of_gsd[(size_t)g][(size_t)a2];
+      scoarse[(size_t)p] = o;
+      cg[(size_t)o].push_back(p);  // ascending global sd
+    }
+  }
   std::vector<int64_t> m_off((size_t)nsd + 1, 0), c_ptr{0};
   std::vector<int32_t> c_slot, coarse_id;
   std::vector<double> c_val;
   std::vector<uint8_t> corner;
-  std::vector<std::vector<int64_t>> cg((size_t)nc);
   const int n = h->n, B = h->block, nb = h->nb;
   for (int sd = 0; sd < nsd; ++sd) {
+    const int g = h->global_of_local[(size_t)sd];
     const int64_t bid = h->h_block_ids[(size_t)sd];
     const int bi = (int)(bid / nb / nb), bj = (int)((bid / nb) % nb), bk = (int)(bid % nb);
-    for (int o : rows_of_sd[(size_t)sd]) {
-      const int64_t row = (int64_t)coarse_id.size();
-      cg[(size_t)o].push_back(row);
+    for (int o : obj_of_gsd[(size_t)g]) {
       coarse_id.push_back(o);
       corner.push_back(cv->kinds[o] == CUTBDDC_CORNER);
       const int64_t cnt = cv->dof_ptr[o + 1] - cv->dof_ptr[o];
@@ -951,7 +942,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
         const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
         const int lx = i - bi * B, ly = j - bj * B, lz = k - bk * B;
         if (lx < 0 || ly < 0 || lz < 0 || lx > B || ly > B || lz > B)
-          throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: object dof not in neighbour subdomain " + std::to_string(sd));
+          throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: object dof not in neighbour subdomain " + std::to_string(g));
         c_slot.push_back((lx * b1 + ly) * b1 + lz);
         c_val.push_back(coef);
       }
@@ -966,9 +957,9 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   std::vector<int64_t> s_off((size_t)nsd + 1, 0);
   for (int sd = 0; sd < nsd; ++sd) {
     const int m = (int)(m_off[(size_t)sd + 1] - m_off[(size_t)sd]);
-    m_max = std::max(m_max, m);
     s_off[(size_t)sd + 1] = s_off[(size_t)sd] + (int64_t)m * m;
   }
+  for (int g = 0; g < nsd_g; ++g) m_max = std::max(m_max, (int)obj_of_gsd[(size_t)g].size());  // uniform over ranks
   h->m_max = m_max;
   std::vector<int64_t> cg_ptr{0}, cg_idx;
   for (int o = 0; o < nc; ++o) {
@@ -985,49 +976,58 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->coarse_id.upload(coarse_id, s);
   h->cg_ptr.upload(cg_ptr, s);
   h->cg_idx.upload(cg_idx, s);
+  h->srow.upload(srow, s);
+  h->scoarse.upload(scoarse, s);
   h->corner_row.upload(corner, s);
   const uint8_t* d_corner = h->corner_row.p;
   h->ac_off.upload(s_off, s);
   h->row_sd.alloc((size_t)std::max<int64_t>(1, h->m_total));
   k_row_sd<<<nsd, 128, 0, s>>>(nsd, h->m_off.p, h->row_sd.p);
   CB_LAUNCH();
-  // ---- weights, rho, masks
+  // ---- weights, rho
   DevBuf<int>& bad = h->ws_flag;
   bad.alloc(1);
   bad.zero(s);
   h->w.alloc((size_t)ns);
-  h->dtot.alloc((size_t)h->n_dof);
-  if (weighting == CUTBDDC_WEIGHT_STIFFNESS) {
-    k_dtot<<<grid_for(h->n_dof, 256), 256, 0, s>>>(h->n_dof, T, h->As.p, h->copy_ptr.p, h->copy_idx.p, h->dtot.p);
+  h->dtot.alloc((size_t)std::max<int64_t>(1, h->n_loc));
+  h->sv2.alloc((size_t)ns);
+  if (weighting == CUTBDDC_WEIGHT_STIFFNESS) {  // Σ over every copy of the A^w diagonal
+    k_diag_slots<<<grid_for(ns, 256), 256, 0, s>>>(ns, T, h->As.p, h->sv2.p);
     CB_LAUNCH();
-    allreduce_sum(h, h->dtot.p, (size_t)h->n_dof);
+    iface_exchange(h, h->sv2.p, nullptr, nullptr);
+    iface_sum(h, h->sv2.p, nullptr, h->dtot.p, nullptr);
   }
-  k_weights<<<grid_for(ns, 256), 256, 0, s>>>(ns, T, weighting, h->slot_dof.p, h->ncount.p, h->As.p, h->dtot.p, h->w.p,
-                                              bad.p);
+  k_weights<<<grid_for(ns, 256), 256, 0, s>>>(ns, T, weighting, h->slot_dof.p, h->slot_loc.p, h->ncount.p, h->As.p,
+                                              h->dtot.p, h->w.p, bad.p);
   CB_LAUNCH();
-  h->mask_all.alloc((size_t)ns);
-  h->mask_int.alloc((size_t)ns);
-  k_masks<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->ncount.p, h->mask_all.p, h->mask_int.p);
-  CB_LAUNCH();
-  h->rho.alloc((size_t)nsd);
-  const size_t rho_shm = sizeof(double) * (size_t)T;
-  if (rho_shm > 48 * 1024) CB_CUDA(cudaFuncSetAttribute(k_rho, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rho_shm));
-  k_rho<<<nsd, 256, rho_shm, s>>>(nsd, T, h->slot_dof.p, h->As.p, h->rho.p);
-  CB_LAUNCH();
+  // Local failures (non-positive pivots, zero weight denominators, dependent
+  // constraints) must not leave other ranks waiting in a collective: each
+  // phase runs under `local`, then every rank learns the worst status
+  // (agree_status) before the next collective. One rank: no exchange.
+  int64_t upd_total = 1;
+  cutbddc_status fail_code = CUTBDDC_OK;
+  std::string fail_msg;
+  auto local = [&](auto&& fn) {
+    if (fail_code != CUTBDDC_OK) return;
+    try {
+      fn();
+    } catch (const Failure& e) {
+      fail_code = e.code;
+      fail_msg = e.what();
+    }
+  };
+  auto agree = [&](int extra) {  // returns the max over ranks of `extra` (0/1); throws on any failure
+    const int c = agree_status(h, ((int)fail_code << 1) | extra);
+    if (c >> 1) throw Failure((cutbddc_status)(c >> 1), fail_msg.empty() ? "setup_bddc: failed on another rank" : fail_msg);
+    return c & 1;
+  };
+  static const char* kSaddleMsg = "saddle: singular augmented system; constraints do not control the operator kernel";
+  h->rho.alloc((size_t)nsd);  // before the FactorInputs take their pointers
   h->diag_add.alloc((size_t)ns);
-  h->diag_add.zero(s);
-  k_diag_add<<<nsd, 128, 0, s>>>(nsd, T, h->m_off.p, h->c_ptr.p, h->c_slot.p, d_corner, h->rho.p, h->diag_add.p);
-  CB_LAUNCH();
-  int hbad = 0;
-  CB_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
-  CB_CUDA(cudaStreamSynchronize(s));
-  if (hbad) throw Failure(CUTBDDC_DEGENERATE, "weighting: zero total diagonal at an interface dof");
-  ps_host.next("setup 1 factorisations");
-  // ---- factorisations
-  if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);
   FactorInput fi{h->As.p, h->mask_int.p, nullptr, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  factor_symbolic(h, h->tI, fi, h->fI);
-  std::vector<FactorJob> jobs{FactorJob{&h->tI, &fi, &h->fI, "cholesky (interior problem)"}};
+  FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
+                 h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
+  FactorInput fk_c{h->As.p, h->mask_all.p, h->diag_add.p, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   // Without an interface (one subdomain) every dof is interior: the weighted
   // residual r_w is identically zero and the constrained Neumann solve drops
   // out of the apply ("preconditioner reduces to exact interior solve").
@@ -1041,85 +1041,112 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     return e && e[0] == '1';
   }();
   h->k_corner = !force_shell && m_max > 0;
-  FactorInput fk{h->As.p, h->mask_all.p, h->diag_add.p, T, b1,
-                 h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, d_corner, h->rho.p};
-  FactorInput fk_c{h->As.p, h->mask_all.p, h->diag_add.p, T, b1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  static const char* kSaddleMsg = "saddle: singular augmented system; constraints do not control the operator kernel";
-  bool k_failed = false;
-  if (h->has_K) {
-    if (h->k_corner) {
-      factor_symbolic(h, h->tI, fk_c, h->fK);
-      jobs.push_back(FactorJob{&h->tI, &fk_c, &h->fK, kSaddleMsg, &k_failed});
-    } else {
+  bool corner_bad = false;
+  local([&] {
+    const size_t rho_shm = sizeof(double) * (size_t)T;
+    if (rho_shm > 48 * 1024) CB_CUDA(cudaFuncSetAttribute(k_rho, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rho_shm));
+    k_rho<<<nsd, 256, rho_shm, s>>>(nsd, T, h->slot_dof.p, h->As.p, h->rho.p);
+    CB_LAUNCH();
+    h->diag_add.zero(s);
+    k_diag_add<<<nsd, 128, 0, s>>>(nsd, T, h->m_off.p, h->c_ptr.p, h->c_slot.p, d_corner, h->rho.p, h->diag_add.p);
+    CB_LAUNCH();
+    int hbad = 0;
+    CB_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
+    CB_CUDA(cudaStreamSynchronize(s));
+    if (hbad) throw Failure(CUTBDDC_DEGENERATE, "weighting: zero total diagonal at an interface dof");
+    ps_host.next("setup 1 factorisations");
+    // ---- factorisations
+    if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);
+    factor_symbolic(h, h->tI, fi, h->fI);
+    std::vector<FactorJob> jobs{FactorJob{&h->tI, &fi, &h->fI, "cholesky (interior problem)"}};
+    bool k_failed = false;
+    if (h->has_K) {
+      if (h->k_corner) {
+        factor_symbolic(h, h->tI, fk_c, h->fK);
+        jobs.push_back(FactorJob{&h->tI, &fk_c, &h->fK, kSaddleMsg, &k_failed});
+      } else {
+        if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
+        factor_symbolic(h, h->tK, fk, h->fK);
+        jobs.push_back(FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg});
+      }
+    }
+    factor_numeric(h, jobs);
+    corner_bad = h->has_K && h->k_corner && (k_failed || !corner_pivots_ok(h));
+  });
+  // a floating fragment (no corner, no Nitsche boundary) leaves K_c singular
+  // on some subdomain: the full augmented K on the shell-root template
+  // instead, on every rank (one formulation: the same numbers for any world size)
+  if (agree(corner_bad ? 1 : 0) && h->has_K && h->k_corner) {
+    h->k_corner = false;
+    local([&] {
       if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
       factor_symbolic(h, h->tK, fk, h->fK);
-      jobs.push_back(FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg});
+      factor_numeric(h, {FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg}});
+    });
+    agree(0);
+  }
+  upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, h->fK.upd_total));
+  local([&] {
+    // ---- coarse basis in the root space of K (see k_root_h): H, S, S^{-1},
+    // W_r and A_c,w = S^{-1} - rho I; the apply never forms Phi
+    h->ac_loc.alloc((size_t)(world * h->maxac));  // staged: this rank's blocks at rank * maxac
+    h->ac_loc.zero(s);
+    h->sinv.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
+    ps_host.next("setup 2 root-space coarse basis");
+    if (m_max > 0 && h->k_corner) {
+      coarse_basis_corner(h, m_off, s_off);
+    } else if (m_max > 0) {
+      if (!h->has_K) throw Failure(CUTBDDC_INTERNAL, "coarse space without an interface");
+      const int nsn = (int)h->tK.tpl.sn.size(), root = nsn - 1;
+      std::vector<int64_t> rinfo((size_t)4 * nsd);
+      int64_t wtot = 0;
+      int cr_max = 0;
+      for (int sd = 0; sd < nsd; ++sd) {
+        const size_t fs = (size_t)sd * nsn + root;
+        const int cr = h->fK.h_rc[fs].y;
+        if (h->fK.h_rc[fs].x != cr) throw Failure(CUTBDDC_INTERNAL, "shell root with update rows");
+        const int m = (int)(m_off[(size_t)sd + 1] - m_off[(size_t)sd]);
+        rinfo[4 * (size_t)sd] = cr;
+        rinfo[4 * (size_t)sd + 1] = h->fK.h_panel_off[fs];
+        rinfo[4 * (size_t)sd + 2] = h->fK.h_vec_off[fs];
+        rinfo[4 * (size_t)sd + 3] = wtot;
+        wtot += (int64_t)cr * m;
+        cr_max = std::max(cr_max, cr);
+      }
+      h->root_info.upload(rinfo, s);
+      h->hroot.alloc((size_t)std::max<int64_t>(1, wtot));
+      h->wroot.alloc((size_t)std::max<int64_t>(1, wtot));
+      const int32_t* pfx_root = h->fK.pfx.p + h->tK.tpl.sn[(size_t)root].rows_off;
+      const int64_t rows_total = (int64_t)h->tK.tpl.rows.size();
+      k_root_h<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
+                                                h->tK.root_pos.p, pfx_root, rows_total, h->fK.panel.p, h->hroot.p);
+      CB_LAUNCH();
+      DevBuf<double>& S = h->ws_s;
+      S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
+      k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
+      CB_LAUNCH();
+      k_root_w<<<dim3(nsd, (cr_max + 63) / 64), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.panel.p, h->hroot.p,
+                                                            h->wroot.p);
+      CB_LAUNCH();
+      invert_schur(h, S.p);
+      k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, nullptr, h->sinv.p,
+                                        h->ac_loc.p + (int64_t)h->dist_rank * h->maxac);
+      CB_LAUNCH();
     }
-  }
-  factor_numeric(h, jobs);
-  if (h->has_K && h->k_corner && (k_failed || !corner_pivots_ok(h))) {
-    // a floating fragment (no corner, no Nitsche boundary) leaves K_c
-    // singular: the full augmented K on the shell-root template instead
-    h->k_corner = false;
-    if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
-    factor_symbolic(h, h->tK, fk, h->fK);
-    factor_numeric(h, {FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg}});
-  }
-  const int64_t upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, h->fK.upd_total));
-  // ---- coarse basis in the root space of K (see k_root_h): H, S, S^{-1},
-  // W_r and A_c,w = S^{-1} - rho I; the apply never forms Phi
-  h->ac_loc.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
-  h->sinv.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
-  ps_host.next("setup 2 root-space coarse basis");
-  if (m_max > 0 && h->k_corner) {
-    coarse_basis_corner(h, m_off, s_off);
-  } else if (m_max > 0) {
-    if (!h->has_K) throw Failure(CUTBDDC_INTERNAL, "coarse space without an interface");
-    const int nsn = (int)h->tK.tpl.sn.size(), root = nsn - 1;
-    std::vector<int64_t> rinfo((size_t)4 * nsd);
-    int64_t wtot = 0;
-    int cr_max = 0;
-    for (int sd = 0; sd < nsd; ++sd) {
-      const size_t fs = (size_t)sd * nsn + root;
-      const int cr = h->fK.h_rc[fs].y;
-      if (h->fK.h_rc[fs].x != cr) throw Failure(CUTBDDC_INTERNAL, "shell root with update rows");
-      const int m = (int)(m_off[(size_t)sd + 1] - m_off[(size_t)sd]);
-      rinfo[4 * (size_t)sd] = cr;
-      rinfo[4 * (size_t)sd + 1] = h->fK.h_panel_off[fs];
-      rinfo[4 * (size_t)sd + 2] = h->fK.h_vec_off[fs];
-      rinfo[4 * (size_t)sd + 3] = wtot;
-      wtot += (int64_t)cr * m;
-      cr_max = std::max(cr_max, cr);
-    }
-    h->root_info.upload(rinfo, s);
-    h->hroot.alloc((size_t)std::max<int64_t>(1, wtot));
-    h->wroot.alloc((size_t)std::max<int64_t>(1, wtot));
-    const int32_t* pfx_root = h->fK.pfx.p + h->tK.tpl.sn[(size_t)root].rows_off;
-    const int64_t rows_total = (int64_t)h->tK.tpl.rows.size();
-    k_root_h<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
-                                              h->tK.root_pos.p, pfx_root, rows_total, h->fK.panel.p, h->hroot.p);
-    CB_LAUNCH();
-    DevBuf<double>& S = h->ws_s;
-    S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
-    k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
-    CB_LAUNCH();
-    k_root_w<<<dim3(nsd, (cr_max + 63) / 64), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.panel.p, h->hroot.p,
-                                                          h->wroot.p);
-    CB_LAUNCH();
-    invert_schur(h, S.p);
-    k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, nullptr, h->sinv.p, h->ac_loc.p);
-    CB_LAUNCH();
-  }
+  });
+  agree(0);
   // ---- coarse matrix + factorisation
   ps_host.next("setup 4 coarse assemble+chol+inverse");
   h->acoarse.alloc((size_t)std::max(1, nc * nc));
   h->acoarse_inv.alloc((size_t)std::max(1, nc * nc));
   if (nc > 0) {
     h->acoarse.zero(s);
-    k_coarse_assemble<<<nc, 128, 0, s>>>(nc, h->cg_ptr.p, h->cg_idx.p, h->row_sd.p, h->m_off.p, h->ac_off.p,
-                                         h->coarse_id.p, h->ac_loc.p, h->acoarse.p);
+    // every subdomain's A_c,w on every rank, then the same assembly in
+    // global subdomain order everywhere
+    gather_blocks(h);
+    k_coarse_assemble<<<nc, 128, 0, s>>>(nc, h->cg_ptr.p, h->cg_idx.p, h->srow.p, h->scoarse.p, h->ac_loc.p,
+                                         h->acoarse.p);
     CB_LAUNCH();
-    allreduce_sum(h, h->acoarse.p, (size_t)nc * nc);  // SPEC.md:386 sum over all subdomains
     // Cholesky of A_c and X = L^{-1} by the tiled dense DAG (A_c is
     // symmetric, so its row-major buffer is its column-major lower part);
     // the apply solves with X^T (X g): two triangular GEMVs.
@@ -1150,11 +1177,10 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->sv1.alloc((size_t)ns);
   h->upd.alloc((size_t)upd_total);
   h->ysave.alloc((size_t)ns);
-  h->gv0.alloc((size_t)h->n_dof);
-  h->gv1.alloc((size_t)h->n_dof);
-  h->gv2.alloc((size_t)h->n_dof);
-  if (distributed(h)) h->gv3.alloc((size_t)h->n_dof);
-  h->gl.alloc((size_t)std::max<int64_t>(1, h->m_total));
+  h->gv0.alloc((size_t)std::max<int64_t>(1, h->n_loc));
+  h->gv2.alloc((size_t)std::max<int64_t>(1, h->n_loc));
+  h->gl.alloc((size_t)(world * h->maxrows));
+  h->gl.zero(s);
   h->cy.alloc((size_t)std::max<int64_t>(1, h->m_total));
   h->uvec.alloc((size_t)std::max<int64_t>(1, h->m_total));
   h->zc.alloc((size_t)std::max(1, nc));
@@ -1164,26 +1190,28 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->bddc_ready = true;
 }
 
-// z = M r (device vectors of n_dof), enqueued on the handle's stream.
-void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip) {
+// z = M r (local dof vectors, dist.cuh), enqueued on the handle's stream.
+// rz_part: when not null, every local subdomain's partial of r.z (PCG).
+void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip, double* rz_part) {
   cudaStream_t s = h->stream;
-  const int64_t nd = h->n_dof, ns = (int64_t)h->nsd * h->slots;
+  const int64_t nl = h->n_loc, ns = (int64_t)h->nsd * h->slots;
   const int T = h->slots;
   ProfScope ps(h->prof, s, "apply vec 1 gather");
-  k_gather_masked<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->mask_int.p, r, h->sv0.p, skip);
+  k_gather_masked<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_loc.p, h->mask_int.p, r, h->sv0.p, skip);
   CB_LAUNCH();
   ps.close();
   solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, skip);
-  ps.next("apply vec 2 z0 r1 scatter phit");
-  k_z0<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv0.p, skip);
+  ps.next("apply vec 2 z0 r1 scatter");
+  k_z0<<<grid_for(nl, 256), 256, 0, s>>>(nl, h->lowner.p, h->sv0.p, h->gv0.p, skip);
   CB_LAUNCH();
-  allreduce_sum(h, h->gv0.p, (size_t)nd);  // one owner per interior dof: exact
-  k_r1<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->ncount.p, h->aval.p, h->acol.p, r, h->gv0.p, h->gv1.p, skip);
-  CB_LAUNCH();
-  k_scatter_weighted<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->w.p, h->gv1.p, h->sv1.p, skip);
+  // (Abar z0) on interface rows = Σ_w A_w,GI z0_w (z0 vanishes on the interface)
+  sub_apply(h, kSubInterface, nullptr, h->sv0.p, h->sv2.p, skip);
+  iface_exchange(h, h->sv2.p, nullptr, skip);
+  k_scatter_r1<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_loc.p, h->mask_int.p, h->w.p, r, h->lcopy_ptr.p,
+                                                 h->lcopy_src.p, h->sv2.p, h->recvbuf.p, h->sv1.p, skip);
   CB_LAUNCH();
   ps.close();
-  if (h->has_K && h->m_total > 0) {
+  if (h->has_K && h->m_total_g > 0) {  // uniform over ranks (collectives inside)
     // z~ = K^{-1}(r_w + C^T u), u = S^{-1}(zc - C K^{-1} r_w). Corner
     // formulation: the forward sweep (y' = L^{-1} r_w in ysave), cy = H^T y',
     // the coarse problem, y' += H u, the backward sweep. Shell formulation:
@@ -1196,20 +1224,22 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepFwd);
     if (!corner) sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRoot);
     ps.next("apply vec 3 cy coarse root-correction");
-    const int cr_blocks = corner ? (h->np_max + 255) / 256 : (int)((h->tK.tpl.sn.back().ncols + 255) / 256);
-    if (!distributed(h) && h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
+    const int cr_blocks = std::max(1, corner ? (h->np_max + 255) / 256 : (int)((h->tK.tpl.sn.back().ncols + 255) / 256));
+    double* gl_loc = h->gl.p + (int64_t)h->dist_rank * h->maxrows;  // this rank's rows of the staged gl
+    if (h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
       if (corner) {  // cy = H^T y' (a warp per constraint row), gl = S^{-1} cy
-        k_h_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->root_info.p,
+        k_h_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->root_info.p,
                                                                h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
         CB_LAUNCH();
-        k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p,
-                                                               h->sinv.p, h->coarse_id.p, h->zc.p, h->cy.p, h->gl.p, 0,
+        k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p,
+                                                               h->sinv.p, h->coarse_id.p, h->zc.p, h->cy.p, gl_loc, 0,
                                                                skip);
       } else {
         k_coarse_in<<<h->nsd, 256, 0, s>>>(T, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, Yc, h->ac_off.p,
-                                           h->sinv.p, h->cy.p, h->gl.p, skip, h->root_info.p, nullptr, nullptr);
+                                           h->sinv.p, h->cy.p, gl_loc, skip, h->root_info.p, nullptr, nullptr);
       }
       CB_LAUNCH();
+      gather_rows(h);
       const size_t shm = sizeof(double) * ((size_t)h->n_coarse + 2 * kFusedCoarseM);
       if (shm > 48 * 1024)  // opt in once per device, to the largest size this kernel can ever need
         device_memo(kMemoCoarseOutShm, [] {
@@ -1223,19 +1253,19 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
       CB_LAUNCH();
     } else {
       if (corner) {
-        k_h_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->root_info.p,
+        k_h_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->root_info.p,
                                                                h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
       } else {
-        k_cy<<<grid_for(h->m_total * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p,
+        k_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p,
                                                            h->c_val.p, h->sv1.p, h->cy.p, skip);
       }
       CB_LAUNCH();
-      k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
-                                                             h->coarse_id.p, h->zc.p, h->cy.p, h->gl.p, 0, skip);
+      k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
+                                                             h->coarse_id.p, h->zc.p, h->cy.p, gl_loc, 0, skip);
       CB_LAUNCH();
+      gather_rows(h);
       k_coarse_rhs<<<grid_for(h->n_coarse, 128), 128, 0, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->gc.p, skip);
       CB_LAUNCH();
-      allreduce_sum(h, h->gc.p, (size_t)h->n_coarse);
       if (h->n_coarse <= kCoarseInverseMax) {
         k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_full.p, h->gc.p,
                                                                              h->zc.p, skip);
@@ -1250,7 +1280,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
         k_xty<<<grid_for((int64_t)nc * 32, 256), 256, 0, s>>>(nc, h->acoarse_inv.p, h->uvec_c.p, h->zc.p, skip);
         CB_LAUNCH();
       }
-      k_sinv_apply<<<grid_for(h->m_total, 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
+      k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
                                                              h->coarse_id.p, h->zc.p, h->cy.p, h->uvec.p, 1, skip);
       CB_LAUNCH();
       if (corner)
@@ -1268,25 +1298,17 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, skip);
     ps.next("apply vec 3b gather Av");
   }
-  k_gather_weighted<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->copy_ptr.p, h->copy_idx.p, h->w.p, h->sv1.p, h->gv2.p, skip);
-  CB_LAUNCH();
-  allreduce_sum(h, h->gv2.p, (size_t)nd);
-  k_interior_av<<<grid_for(ns, 256), 256, 0, s>>>(ns, nd, h->slot_dof.p, h->mask_int.p, h->aval.p, h->acol.p, h->gv2.p,
-                                                  h->sv0.p, skip);
-  CB_LAUNCH();
+  // v = Σ_copies w z~, every rank forms the same sum
+  iface_exchange(h, h->sv1.p, h->w.p, skip);
+  iface_sum(h, h->sv1.p, h->w.p, h->gv2.p, skip);
+  // harmonic correction: the interior rows of Abar v, one subdomain at a time
+  sub_apply(h, kSubInterior, h->gv2.p, nullptr, h->sv0.p, skip);
   ps.close();
   solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, skip);
   ps.next("apply vec 4 final");
-  if (distributed(h)) {
-    k_owned_neg<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->sv0.p, h->gv3.p, skip);
-    CB_LAUNCH();
-    allreduce_sum(h, h->gv3.p, (size_t)nd);
-    k_final_sum<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->gv0.p, h->gv2.p, h->gv3.p, z, skip);
-    CB_LAUNCH();
-  } else {
-    k_final_z<<<grid_for(nd, 256), 256, 0, s>>>(nd, h->owner_slot.p, h->gv0.p, h->gv2.p, h->sv0.p, z, skip);
-    CB_LAUNCH();
-  }
+  k_final_z<<<seg_grid(h), kSegThreads, 0, s>>>(seg_args(h, rz_part), h->lowner.p, h->gv0.p, h->gv2.p, h->sv0.p, z,
+                                                rz_part ? r : nullptr, skip);
+  CB_LAUNCH();
 }
 
 }  // namespace cutbddc_b200

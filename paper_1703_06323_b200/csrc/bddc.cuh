@@ -7,11 +7,13 @@
 namespace cutbddc_b200 {
 
 void classify_device(cutbddc_gpu* h, const cutbddc_geometry* g);
-void assemble_device(cutbddc_gpu* h, int block, int nsd, const int64_t* block_ids);
+void assemble_device(cutbddc_gpu* h, const cutbddc_partition_view* part);
 cutbddc_objects* classify_objects_device(cutbddc_gpu* h, int objects);
 void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weighting);
-void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip);
+// rz_part: when not null, per-subdomain partials of r.z (gathered layout, dist.cuh)
+void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip, double* rz_part = nullptr);
 void spmv_device(cutbddc_gpu* h, const double* x, double* y);
-void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, cutbddc_solve_report* rep);
+// b_loc, h->px: local dof vectors (dist.cuh)
+void pcg_device(cutbddc_gpu* h, const double* b_loc, double rtol, int max_iter, cutbddc_solve_report* rep);
 
 }  // namespace cutbddc_b200

@@ -7,6 +7,7 @@
 
 #include "bddc.cuh"
 #include "comm.cuh"
+#include "dist.cuh"
 #include "factor.cuh"
 
 namespace cutbddc_b200 {
@@ -91,6 +92,7 @@ void cutbddc_gpu_destroy(cutbddc_gpu* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  if (h->graph_exec_ref) cudaGraphExecDestroy(h->graph_exec_ref);
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->prof.dump();
   for (cudaEvent_t e : h->dag_ev) cudaEventDestroy(e);
@@ -109,20 +111,62 @@ cutbddc_status cutbddc_nccl_unique_id(void* id128) {
   });
 }
 
-cutbddc_status cutbddc_gpu_set_global_ids(cutbddc_gpu* h, int n_sd_global, const int32_t* global_of_local) {
+cutbddc_status cutbddc_gpu_set_distribution(cutbddc_gpu* h, const cutbddc_partition_view* part,
+                                            const int32_t* rank_of_sd, int rank, int world) {
   return guard([&] {
     need(h);
+    if (!rank_of_sd) throw Failure(CUTBDDC_INVALID_ARGUMENT, "distribution: null rank_of_sd");
     std::lock_guard<std::mutex> lk(h->mu);
-    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "set_global_ids: assemble first");
-    if (!global_of_local || n_sd_global < h->nsd) throw Failure(CUTBDDC_INVALID_ARGUMENT, "set_global_ids: bad ids");
-    std::vector<int32_t> g(global_of_local, global_of_local + h->nsd);
-    for (int i = 0; i < h->nsd; ++i)
-      if (g[(size_t)i] < 0 || g[(size_t)i] >= n_sd_global || (i && g[(size_t)i] <= g[(size_t)i - 1]))
-        throw Failure(CUTBDDC_INVALID_ARGUMENT, "set_global_ids: ids must ascend within [0, n_sd_global)");
-    h->nsd_global = n_sd_global;
-    h->global_of_local = std::move(g);
+    dist_set(h, part, rank_of_sd, rank, world);
+    h->assembled = false;
     h->bddc_ready = false;
   });
+}
+
+cutbddc_status cutbddc_gpu_exchange_plan(cutbddc_gpu* h, cutbddc_exchange_plan** out) {
+  return guard([&] {
+    need(h);
+    if (!out) throw Failure(CUTBDDC_INVALID_ARGUMENT, "exchange plan: null output");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "exchange plan: assemble first");
+    cudaStream_t s = h->stream;
+    auto* p = new cutbddc_exchange_plan();
+    p->n_loc = h->n_loc;
+    p->n_own = h->n_own;
+    p->n_sd_local = h->nsd;
+    p->n_nbr = (int)h->nbr.size();
+    p->loc_glob = new int32_t[(size_t)h->n_loc + 1];
+    p->seg_ptr = new int32_t[(size_t)h->nsd + 1];
+    p->copy_ptr = new int32_t[(size_t)h->n_loc + 1];
+    p->copy_src = new int32_t[(size_t)h->n_copies + 1];
+    p->nbr = new int32_t[h->nbr.size() + 1];
+    p->send_ptr = new int64_t[h->send_ptr.size()];
+    p->recv_ptr = new int64_t[h->recv_ptr.size()];
+    p->send_src = new int32_t[(size_t)h->send_ptr.back() + 1];
+    h->loc_glob.download(p->loc_glob, (size_t)h->n_loc, s);
+    h->seg_ptr.download(p->seg_ptr, (size_t)h->nsd + 1, s);
+    h->lcopy_ptr.download(p->copy_ptr, (size_t)h->n_loc + 1, s);
+    h->lcopy_src.download(p->copy_src, (size_t)h->n_copies, s);
+    h->send_src.download(p->send_src, (size_t)h->send_ptr.back(), s);
+    CB_CUDA(cudaStreamSynchronize(s));
+    std::copy(h->nbr.begin(), h->nbr.end(), p->nbr);
+    std::copy(h->send_ptr.begin(), h->send_ptr.end(), p->send_ptr);
+    std::copy(h->recv_ptr.begin(), h->recv_ptr.end(), p->recv_ptr);
+    *out = p;
+  });
+}
+
+void cutbddc_exchange_plan_free(cutbddc_exchange_plan* p) {
+  if (!p) return;
+  delete[] p->loc_glob;
+  delete[] p->seg_ptr;
+  delete[] p->copy_ptr;
+  delete[] p->copy_src;
+  delete[] p->nbr;
+  delete[] p->send_ptr;
+  delete[] p->send_src;
+  delete[] p->recv_ptr;
+  delete p;
 }
 
 cutbddc_status cutbddc_gpu_classify(cutbddc_gpu* h, const cutbddc_geometry* g, double* phi, uint8_t* cls,
@@ -174,7 +218,7 @@ cutbddc_status cutbddc_gpu_assemble(cutbddc_gpu* h, const cutbddc_mesh_view* mes
       h->mesh_ready = true;
     }
     if (!h->mesh_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble: no mesh (classify first or pass a view)");
-    assemble_device(h, part->block, part->n_sd, part->block_ids);
+    assemble_device(h, part);
     h->t_assembly = tm.stop();
     if (dirichlet) {
       h->orphan.download(dirichlet, (size_t)h->n_dof, h->stream);
@@ -230,6 +274,32 @@ cutbddc_status cutbddc_gpu_setup_bddc(cutbddc_gpu* h, const cutbddc_coarse_view*
   });
 }
 
+// boundary vectors (global numbering) <-> the handle's local dof space
+namespace {
+void host_to_local(cutbddc_gpu* h, const double* x, DevBuf<double>& loc) {
+  DevBuf<double> g;
+  g.upload(x, (size_t)h->n_dof, h->stream);
+  loc.alloc((size_t)std::max<int64_t>(1, h->n_loc));
+  to_local(h, g.p, loc.p);
+  CB_CUDA(cudaStreamSynchronize(h->stream));
+}
+// owned entries into the caller's n_dof buffer (others untouched)
+void local_to_host(cutbddc_gpu* h, const double* loc, double* x) {
+  DevBuf<double> g;
+  if (h->n_own == h->n_dof) {
+    g.alloc((size_t)h->n_dof);
+  } else {
+    g.upload(x, (size_t)h->n_dof, h->stream);
+  }
+  to_global_owned(h, loc, g.p);
+  g.download(x, (size_t)h->n_dof, h->stream);
+  CB_CUDA(cudaStreamSynchronize(h->stream));
+}
+void need_numeric(cutbddc_gpu* h) {
+  if (h->plan_only) throw Failure(CUTBDDC_CONFIG, "plan-only distribution (no communicator): no numerical calls");
+}
+}  // namespace
+
 cutbddc_status cutbddc_gpu_pcg(cutbddc_gpu* h, const double* b, double* x, double rtol, int max_iter,
                                cutbddc_solve_report* report) {
   return guard([&] {
@@ -239,14 +309,11 @@ cutbddc_status cutbddc_gpu_pcg(cutbddc_gpu* h, const double* b, double* x, doubl
     const double* bd = h->b.p;
     DevBuf<double> bbuf;
     if (b) {
-      bbuf.upload(b, (size_t)h->n_dof, h->stream);
+      host_to_local(h, b, bbuf);
       bd = bbuf.p;
     }
     pcg_device(h, bd, rtol, max_iter, report);
-    if (x) {
-      h->px.download(x, (size_t)h->n_dof, h->stream);
-      CB_CUDA(cudaStreamSynchronize(h->stream));
-    }
+    if (x) local_to_host(h, h->px.p, x);
   });
 }
 
@@ -255,12 +322,12 @@ cutbddc_status cutbddc_gpu_spmv(cutbddc_gpu* h, const double* x, double* y) {
     need(h);
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble first");
+    need_numeric(h);
     DevBuf<double> dx, dy;
-    dx.upload(x, (size_t)h->n_dof, h->stream);
-    dy.alloc((size_t)h->n_dof);
+    host_to_local(h, x, dx);
+    dy.alloc((size_t)std::max<int64_t>(1, h->n_loc));
     spmv_device(h, dx.p, dy.p);
-    dy.download(y, (size_t)h->n_dof, h->stream);
-    CB_CUDA(cudaStreamSynchronize(h->stream));
+    local_to_host(h, dy.p, y);
   });
 }
 
@@ -270,11 +337,10 @@ cutbddc_status cutbddc_gpu_apply_bddc(cutbddc_gpu* h, const double* r, double* z
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "apply: setup_bddc first");
     DevBuf<double> dr, dz;
-    dr.upload(r, (size_t)h->n_dof, h->stream);
-    dz.alloc((size_t)h->n_dof);
+    host_to_local(h, r, dr);
+    dz.alloc((size_t)std::max<int64_t>(1, h->n_loc));
     apply_bddc_device(h, dr.p, dz.p, nullptr);
-    dz.download(z, (size_t)h->n_dof, h->stream);
-    CB_CUDA(cudaStreamSynchronize(h->stream));
+    local_to_host(h, dz.p, z);
   });
 }
 
@@ -283,8 +349,8 @@ cutbddc_status cutbddc_gpu_rhs(cutbddc_gpu* h, double* b) {
     need(h);
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble first");
-    h->b.download(b, (size_t)h->n_dof, h->stream);
-    CB_CUDA(cudaStreamSynchronize(h->stream));
+    need_numeric(h);
+    local_to_host(h, h->b.p, b);
   });
 }
 

@@ -1,0 +1,597 @@
+// dist.cu — subdomains over ranks: the local dof space, the
+// interface exchange plan and the exchange itself, segment partials, and the
+// matrix-free sub-assembled operator (one constant Q1
+// stencil for interior cells plus the stored 8x8 matrix of each cut cell;
+// no assembled global matrix anywhere).
+//
+// Reference: the sum over subdomain copies is SPEC.md:393 ("sum the weighted
+// subdomain corrections") and Abar = Σ_w R_w^T A_w R_w; the
+// parallel contract is "independent parallel tasks joined by global
+// reductions". The plan is built on the device from the mesh
+// and the global partition every rank holds; host_partition.cpp has the same
+// plan as host C++ (cutbddc_build_exchange_plan) for the CPU multi-process
+// tests, and tests/test_gpu_dist.py checks the two agree entry for entry.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "comm.cuh"
+#include "dist.cuh"
+
+namespace cutbddc_b200 {
+namespace {
+
+constexpr int kMaxRanks = 32;  // rank masks are 32-bit
+
+// ---------------------------------------------------------------- plan kernels
+struct PlanArgs {
+  int n, B, nb, b1, T, rank;
+  const uint8_t* cls;
+  const int64_t* node_of_dof;
+  const int32_t* gsd_of_block;   // nb^3: global subdomain or -1
+  const int32_t* rank_of_gsd;
+  const int32_t* lsd_of_gsd;     // local subdomain index or -1
+  const int64_t* gblock;         // nsd_g: block id of each global subdomain
+};
+
+// per global dof: subdomains of its active cells (global ids ascending,
+// padded with -1), whether this rank has a copy, its segment (local index of
+// its lowest subdomain, or nsd for the ghost segment) and the rank mask
+__global__ void k_dof_sds(int64_t nd, PlanArgs a, int nsd, int32_t* __restrict__ sds, uint8_t* __restrict__ nsds,
+                          uint8_t* __restrict__ local, int32_t* __restrict__ seg, uint32_t* __restrict__ rmask) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  const int n = a.n;
+  const int64_t v = a.node_of_dof[d];
+  const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
+  int32_t s[8];
+  int m = 0;
+  for (int dx = 0; dx < 2; ++dx)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dz = 0; dz < 2; ++dz) {
+        const int ci = i - 1 + dx, cj = j - 1 + dy, ck = k - 1 + dz;
+        if (ci < 0 || cj < 0 || ck < 0 || ci >= n || cj >= n || ck >= n) continue;
+        if (a.cls[((int64_t)ci * n + cj) * n + ck] == CUTBDDC_EXTERIOR) continue;
+        const int32_t g = a.gsd_of_block[((int64_t)(ci / a.B) * a.nb + cj / a.B) * a.nb + ck / a.B];
+        bool seen = false;
+        for (int q = 0; q < m; ++q) seen |= s[q] == g;
+        if (!seen) s[m++] = g;
+      }
+  for (int x = 1; x < m; ++x)  // ascending block id == ascending global subdomain
+    for (int y = x; y > 0 && s[y - 1] > s[y]; --y) {
+      const int32_t t = s[y];
+      s[y] = s[y - 1];
+      s[y - 1] = t;
+    }
+  uint32_t mask = 0;
+  for (int q = 0; q < m; ++q) mask |= 1u << a.rank_of_gsd[s[q]];
+  for (int q = 0; q < 8; ++q) sds[d * 8 + q] = q < m ? s[q] : -1;
+  nsds[d] = (uint8_t)m;
+  const bool loc = (mask >> a.rank) & 1u;
+  local[d] = loc;
+  seg[d] = m > 0 && a.rank_of_gsd[s[0]] == a.rank ? a.lsd_of_gsd[s[0]] : nsd;
+  rmask[d] = loc ? mask : 0u;
+}
+
+__global__ void k_gather_i32(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ src,
+                             int32_t* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+__global__ void k_scatter_pos(int64_t n, const int32_t* __restrict__ idx, int32_t* __restrict__ pos) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) pos[idx[i]] = (int32_t)i;
+}
+
+// seg_ptr[s] = first position with key >= s (keys sorted)
+__global__ void k_seg_ptr(int nseg, int64_t n, const int32_t* __restrict__ keys, int32_t* __restrict__ seg_ptr) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > nseg) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < s) lo = mid + 1;
+    else hi = mid;
+  }
+  seg_ptr[s] = (int32_t)lo;
+}
+
+__global__ void k_or_mask(int64_t nd, const uint32_t* __restrict__ rmask, unsigned int* __restrict__ out) {
+  __shared__ unsigned int sm;
+  if (threadIdx.x == 0) sm = 0;
+  __syncthreads();
+  unsigned int m = 0;
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < nd; d += (int64_t)gridDim.x * blockDim.x)
+    m |= rmask[d];
+  atomicOr(&sm, m);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicOr(out, sm);
+}
+
+__device__ inline int count_rank(const int32_t* s, const int32_t* rank_of_gsd, int q) {
+  int c = 0;
+  for (int x = 0; x < 8 && s[x] >= 0; ++x) c += rank_of_gsd[s[x]] == q;
+  return c;
+}
+
+// per neighbour k, in ascending-global order j of the local dofs:
+//   rc = copies on q (message q -> rank), sc = copies here if q has a copy (message rank -> q)
+__global__ void k_nbr_counts(int64_t nloc, int nnbr, const int32_t* __restrict__ glist, const int32_t* __restrict__ sds,
+                             const int32_t* __restrict__ rank_of_gsd, const int32_t* __restrict__ nbr, int rank,
+                             int32_t* __restrict__ rc, int32_t* __restrict__ sc) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nloc) return;
+  const int32_t* s = sds + (int64_t)glist[j] * 8;
+  const int mine = count_rank(s, rank_of_gsd, rank);
+  for (int k = 0; k < nnbr; ++k) {
+    const int c = count_rank(s, rank_of_gsd, nbr[k]);
+    rc[(int64_t)k * nloc + j] = c;
+    sc[(int64_t)k * nloc + j] = c > 0 ? mine : 0;
+  }
+}
+
+__global__ void k_copy_count(int64_t nloc, const int32_t* __restrict__ loc_glob, const uint8_t* __restrict__ nsds,
+                             int32_t* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nloc) cnt[i] = nsds[loc_glob[i]];
+}
+
+__device__ inline int32_t slot_of(const PlanArgs& a, int64_t node, int32_t gsd) {
+  const int n = a.n, B = a.B, b1 = a.b1;
+  const int k = (int)(node % (n + 1)), j = (int)((node / (n + 1)) % (n + 1)), i = (int)(node / (n + 1) / (n + 1));
+  const int64_t bid = a.gblock[gsd];
+  const int bi = (int)(bid / a.nb / a.nb), bj = (int)((bid / a.nb) % a.nb), bk = (int)(bid % a.nb);
+  return ((i - bi * B) * b1 + (j - bj * B)) * b1 + (k - bk * B);
+}
+
+// copy sources (ascending global subdomain) of every local dof, the send
+// lists, and the owner slot of interior dofs; thread per local dof in
+// ascending-global order j
+__global__ void k_fill_plan(int64_t nloc, int nnbr, PlanArgs a, const int32_t* __restrict__ glist,
+                            const int32_t* __restrict__ loc_of_dof, const int32_t* __restrict__ sds,
+                            const int32_t* __restrict__ nbr_of_rank, const int32_t* __restrict__ rinc,
+                            const int32_t* __restrict__ rcnt, const int32_t* __restrict__ sinc,
+                            const int32_t* __restrict__ scnt, const int64_t* __restrict__ rbase,
+                            const int64_t* __restrict__ sbase, const int32_t* __restrict__ cptr,
+                            int32_t* __restrict__ csrc, int32_t* __restrict__ send_src, int32_t* __restrict__ lowner) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nloc) return;
+  const int32_t d = glist[j];
+  const int32_t i = loc_of_dof[d];
+  const int32_t* s = sds + (int64_t)d * 8;
+  const int64_t node = a.node_of_dof[d];
+  int pos_q[kMaxRanks];
+  for (int q = 0; q < kMaxRanks; ++q) pos_q[q] = 0;
+  int m = 0, mloc = 0;
+  int32_t p = cptr[i];
+  int32_t first_local = -1;
+  for (; m < 8 && s[m] >= 0; ++m) {
+    const int32_t g = s[m];
+    const int q = a.rank_of_gsd[g];
+    if (q == a.rank) {
+      const int32_t src = a.lsd_of_gsd[g] * a.T + slot_of(a, node, g);
+      csrc[p++] = src;
+      if (first_local < 0) first_local = src;
+      // this copy goes to every neighbour holding a copy, at position mloc
+      for (int k = 0; k < nnbr; ++k) {
+        const int64_t jj = (int64_t)k * nloc + j;
+        if (scnt[jj] > 0) send_src[sbase[k] + (sinc[jj] - scnt[jj]) + mloc] = src;
+      }
+      ++mloc;
+    } else {
+      const int k = nbr_of_rank[q];
+      const int64_t jj = (int64_t)k * nloc + j;
+      csrc[p++] = -1 - (int32_t)(rbase[k] + (rinc[jj] - rcnt[jj]) + pos_q[q]);
+      ++pos_q[q];
+    }
+  }
+  lowner[i] = m == 1 ? first_local : -1;
+}
+
+__global__ void k_slot_loc(int64_t ns, const int32_t* __restrict__ slot_dof, const int32_t* __restrict__ loc_of_dof,
+                           int32_t* __restrict__ slot_loc) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  const int32_t d = slot_dof[g];
+  slot_loc[g] = d >= 0 ? loc_of_dof[d] : -1;
+}
+
+// ---------------------------------------------------------------- exchange / sums
+__global__ void k_pack(int64_t n, const int32_t* __restrict__ src, const double* __restrict__ w,
+                       const double* __restrict__ Y, double* __restrict__ buf, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t s = src[k];
+  buf[k] = w ? w[s] * Y[s] : Y[s];
+}
+
+__global__ void k_isum(int64_t nloc, const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
+                       const double* __restrict__ w, const double* __restrict__ Y, const double* __restrict__ recv,
+                       double* __restrict__ out, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  double s = 0.0;
+  for (int32_t p = cptr[i]; p < cptr[i + 1]; ++p) {
+    const int32_t c = csrc[p];
+    s += c >= 0 ? (w ? w[c] * Y[c] : Y[c]) : recv[-1 - c];
+  }
+  out[i] = s;
+}
+
+__global__ void k_to_local(int64_t nloc, const int32_t* __restrict__ loc_glob, const double* __restrict__ xg,
+                           double* __restrict__ xl) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nloc) xl[i] = xg[loc_glob[i]];
+}
+
+__global__ void k_to_global(int64_t nown, const int32_t* __restrict__ loc_glob, const double* __restrict__ xl,
+                            double* __restrict__ xg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nown) xg[loc_glob[i]] = xl[i];
+}
+
+// ---------------------------------------------------------------- matrix-free operator
+struct SubArgs {
+  int n, B, b1, T, nb;
+  const int64_t* block_ids;   // local subdomain -> block id
+  const int32_t* eoc;         // per cell: -2 exterior, -1 interior, >= 0 local cut index
+  const double* ke;           // 8x8 row-major per local cut cell
+  const uint8_t* empty;
+  const double* kint;         // constant interior element matrix
+  const int32_t* slot_loc;
+  const uint8_t* mask_int;
+  const double* odiag;        // per slot: 1/|neigh| at strong-Dirichlet slots, else 0
+};
+
+// one CTA per subdomain: the subdomain's input values and cell codes in
+// shared memory, a thread per slot sums its <= 8 cells' element rows
+template <int MODE>
+__global__ void __launch_bounds__(512) k_sub_apply(SubArgs a, const double* __restrict__ xloc,
+                                                   const double* __restrict__ Xslot, double* __restrict__ Y,
+                                                   const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double xs[];
+  int32_t* cc = reinterpret_cast<int32_t*>(xs + a.T);
+  __shared__ double ks[64];
+  const int sd = blockIdx.x, T = a.T, B = a.B, b1 = a.b1, n = a.n;
+  const int64_t base = (int64_t)sd * T;
+  const int64_t bid = a.block_ids[sd];
+  const int bi = (int)(bid / a.nb / a.nb), bj = (int)((bid / a.nb) % a.nb), bk = (int)(bid % a.nb);
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    double v;
+    if (Xslot) {
+      v = Xslot[base + t];
+    } else {
+      const int32_t l = a.slot_loc[base + t];
+      v = l >= 0 ? xloc[l] : 0.0;
+    }
+    xs[t] = v;
+  }
+  for (int c = threadIdx.x; c < B * B * B; c += blockDim.x) {
+    const int cx = c / (B * B), cy = (c / B) % B, cz = c % B;
+    int32_t e = a.eoc[((int64_t)(bi * B + cx) * n + bj * B + cy) * n + bk * B + cz];
+    if (e >= 0 && a.empty[e]) e = -2;
+    cc[c] = e;
+  }
+  if (threadIdx.x < 64) ks[threadIdx.x] = a.kint[threadIdx.x];
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const int64_t g = base + t;
+    const bool present = a.slot_loc[g] >= 0;
+    const bool interior = a.mask_int[g] != 0;
+    const bool row = MODE == kSubAll ? present : (MODE == kSubInterface ? present && !interior : interior);
+    if (!row) {
+      Y[g] = 0.0;
+      continue;
+    }
+    const int lx = t / (b1 * b1), ly = (t / b1) % b1, lz = t % b1;
+    double acc = 0.0;
+    for (int dx = 0; dx < 2; ++dx)
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dz = 0; dz < 2; ++dz) {
+          const int cx = lx - 1 + dx, cy = ly - 1 + dy, cz = lz - 1 + dz;
+          if (cx < 0 || cy < 0 || cz < 0 || cx >= B || cy >= B || cz >= B) continue;
+          const int32_t e = cc[(cx * B + cy) * B + cz];
+          if (e == -2) continue;
+          const int lv = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+          const double* K = (e == -1 ? ks : a.ke + (int64_t)e * 64) + lv * 8;
+          const int n0 = (cx * b1 + cy) * b1 + cz;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) acc += K[w] * xs[n0 + ((w >> 2) & 1) + ((w >> 1) & 1) * b1 + (w & 1) * b1 * b1];
+        }
+    if (a.odiag) acc += a.odiag[g] * xs[t];
+    Y[g] = acc;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- distribution
+static void dist_common(cutbddc_gpu* h, int block, int nsd_g, const int64_t* bids, const int32_t* rank_of_sd, int rank,
+                        int world) {
+  if (world < 1 || world > kMaxRanks) throw Failure(CUTBDDC_INVALID_ARGUMENT, "distribution: world size out of range");
+  if (rank < 0 || rank >= world) throw Failure(CUTBDDC_INVALID_ARGUMENT, "distribution: rank out of range");
+  if (block < 1 || nsd_g < 1 || !bids) throw Failure(CUTBDDC_INVALID_ARGUMENT, "distribution: empty partition");
+  h->dist_block = block;
+  h->dist_rank = rank;
+  h->dist_world = world;
+  h->nsd_g = nsd_g;
+  h->g_block_ids.assign(bids, bids + nsd_g);
+  h->rank_of_gsd.assign((size_t)nsd_g, 0);
+  for (int g = 0; g < nsd_g; ++g) {
+    if (g && bids[g] <= bids[g - 1]) throw Failure(CUTBDDC_INVALID_ARGUMENT, "partition: block ids must ascend");
+    const int r = rank_of_sd ? rank_of_sd[g] : 0;
+    if (r < 0 || r >= world) throw Failure(CUTBDDC_INVALID_ARGUMENT, "distribution: rank_of_sd out of range");
+    h->rank_of_gsd[(size_t)g] = r;
+  }
+  std::vector<int> per(world, 0);
+  h->lidx_of_gsd.assign((size_t)nsd_g, 0);
+  h->global_of_local.clear();
+  for (int g = 0; g < nsd_g; ++g) {
+    const int r = h->rank_of_gsd[(size_t)g];
+    h->lidx_of_gsd[(size_t)g] = per[(size_t)r]++;
+    if (r == rank) h->global_of_local.push_back(g);
+  }
+  if (h->global_of_local.empty())
+    throw Failure(CUTBDDC_CONFIG, "distribution: rank " + std::to_string(rank) + " received no subdomain");
+  h->maxloc = *std::max_element(per.begin(), per.end());
+  std::vector<int32_t> gpos((size_t)nsd_g);
+  for (int g = 0; g < nsd_g; ++g) gpos[(size_t)g] = h->rank_of_gsd[(size_t)g] * h->maxloc + h->lidx_of_gsd[(size_t)g];
+  h->d_gpos.upload(gpos, h->stream);
+  h->dist_set = true;
+}
+
+void dist_set(cutbddc_gpu* h, const cutbddc_partition_view* part, const int32_t* rank_of_sd, int rank, int world) {
+  if (!part) throw Failure(CUTBDDC_INVALID_ARGUMENT, "distribution: null partition");
+  if (h->comm && (rank != h->rank || world != h->world))
+    throw Failure(CUTBDDC_INVALID_ARGUMENT, "distribution: rank / world differ from the handle's communicator");
+  dist_common(h, part->block, part->n_sd, part->block_ids, rank_of_sd, rank, world);
+  h->dist_explicit = true;
+}
+
+void dist_default(cutbddc_gpu* h, const cutbddc_partition_view* part) {
+  dist_common(h, part->block, part->n_sd, part->block_ids, nullptr, 0, 1);
+  h->dist_explicit = false;
+}
+
+// ---------------------------------------------------------------- plan
+void build_plan_device(cutbddc_gpu* h) {
+  cudaStream_t s = h->stream;
+  const int64_t nd = h->n_dof;
+  const int nsd = h->nsd, nsd_g = h->nsd_g, rank = h->dist_rank;
+  const int nb = h->nb, T = h->slots;
+  if (nd >= (1ll << 31)) throw Failure(CUTBDDC_INVALID_ARGUMENT, "distribution: more than 2^31 dofs");
+  // global subdomain maps on the device
+  std::vector<int32_t> gsd_of_block((size_t)nb * nb * nb, -1), lsd_of_gsd((size_t)nsd_g, -1);
+  for (int g = 0; g < nsd_g; ++g) {
+    gsd_of_block[(size_t)h->g_block_ids[(size_t)g]] = g;
+    if (h->rank_of_gsd[(size_t)g] == rank) lsd_of_gsd[(size_t)g] = h->lidx_of_gsd[(size_t)g];
+  }
+  h->d_gsd_of_block.upload(gsd_of_block, s);
+  h->d_rank_of_gsd.upload(h->rank_of_gsd, s);
+  h->d_lsd_of_gsd.upload(lsd_of_gsd, s);
+  h->d_gblock.upload(h->g_block_ids, s);
+  PlanArgs a{h->n, h->block, nb, h->b1, T, rank, h->cls.p, h->node_of_dof.p, h->d_gsd_of_block.p,
+             h->d_rank_of_gsd.p, h->d_lsd_of_gsd.p, h->d_gblock.p};
+  DevBuf<int32_t>& sds = h->ws_sds;
+  DevBuf<uint8_t>& nsds = h->ws_nsds;
+  DevBuf<uint8_t>& local = h->ws_local;
+  DevBuf<int32_t>& seg = h->ws_seg;
+  DevBuf<uint32_t>& rmask = h->ws_rmask;
+  sds.alloc((size_t)nd * 8);
+  nsds.alloc((size_t)nd);
+  local.alloc((size_t)nd);
+  seg.alloc((size_t)nd);
+  rmask.alloc((size_t)nd);
+  k_dof_sds<<<grid_for(nd, 256), 256, 0, s>>>(nd, a, nsd, sds.p, nsds.p, local.p, seg.p, rmask.p);
+  CB_LAUNCH();
+  // local dofs, ascending global
+  DevBuf<int32_t>& glist = h->ws_glist;
+  glist.alloc((size_t)nd);
+  DevBuf<int64_t>& cnt = h->ws_cnt;
+  cnt.alloc(2);
+  DevBuf<uint8_t>& tmp = h->ws_tmp;
+  size_t tb = 0;
+  cub::CountingInputIterator<int32_t> it(0);
+  CB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, local.p, glist.p, cnt.p, (int)nd, s));
+  tmp.alloc(std::max(tmp.n, tb));
+  CB_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, local.p, glist.p, cnt.p, (int)nd, s));
+  int64_t nloc = 0;
+  CB_CUDA(cudaMemcpyAsync(&nloc, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+  CB_CUDA(cudaStreamSynchronize(s));
+  h->n_loc = nloc;
+  // local numbering: stable sort by segment (ascending global within a segment)
+  DevBuf<int32_t>& keys = h->ws_keys;
+  keys.alloc((size_t)2 * nloc);
+  k_gather_i32<<<grid_for(nloc, 256), 256, 0, s>>>(nloc, glist.p, seg.p, keys.p);
+  CB_LAUNCH();
+  h->loc_glob.alloc((size_t)nloc);
+  int bits = 1;
+  while ((1 << bits) <= nsd) ++bits;
+  tb = 0;
+  CB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys.p + nloc, glist.p, h->loc_glob.p, (int)nloc, 0,
+                                          bits, s));
+  tmp.alloc(std::max(tmp.n, tb));
+  CB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys.p + nloc, glist.p, h->loc_glob.p, (int)nloc, 0, bits,
+                                          s));
+  h->seg_ptr.alloc((size_t)nsd + 1);
+  k_seg_ptr<<<grid_for(nsd + 1, 128), 128, 0, s>>>(nsd, nloc, keys.p + nloc, h->seg_ptr.p);
+  CB_LAUNCH();
+  h->loc_of_dof.alloc((size_t)nd);
+  CB_CUDA(cudaMemsetAsync(h->loc_of_dof.p, 0xff, sizeof(int32_t) * nd, s));
+  k_scatter_pos<<<grid_for(nloc, 256), 256, 0, s>>>(nloc, h->loc_glob.p, h->loc_of_dof.p);
+  CB_LAUNCH();
+  int32_t own = 0;
+  CB_CUDA(cudaMemcpyAsync(&own, h->seg_ptr.p + nsd, 4, cudaMemcpyDeviceToHost, s));
+  // neighbour ranks
+  DevBuf<unsigned int>& om = h->ws_omask;
+  om.alloc(1);
+  om.zero(s);
+  k_or_mask<<<148, 256, 0, s>>>(nd, rmask.p, om.p);
+  CB_LAUNCH();
+  unsigned int mask = 0;
+  CB_CUDA(cudaMemcpyAsync(&mask, om.p, 4, cudaMemcpyDeviceToHost, s));
+  CB_CUDA(cudaStreamSynchronize(s));
+  h->n_own = own;
+  h->nbr.clear();
+  std::vector<int32_t> nbr_of_rank(kMaxRanks, -1);
+  for (int q = 0; q < h->dist_world; ++q)
+    if (q != rank && ((mask >> q) & 1u)) {
+      nbr_of_rank[(size_t)q] = (int32_t)h->nbr.size();
+      h->nbr.push_back(q);
+    }
+  const int nnbr = (int)h->nbr.size();
+  h->d_nbr.upload(h->nbr.empty() ? std::vector<int32_t>{0} : h->nbr, s);
+  h->d_nbr_of_rank.upload(nbr_of_rank, s);
+  // per-neighbour message layouts (inclusive scans in ascending-global order)
+  DevBuf<int32_t>& rc = h->ws_rc;
+  DevBuf<int32_t>& sc = h->ws_sc;
+  const size_t nn = (size_t)std::max(1, nnbr) * (size_t)nloc;
+  rc.alloc(2 * nn);
+  sc.alloc(2 * nn);
+  std::vector<int64_t> sbase(1, 0), rbase(1, 0);
+  if (nnbr > 0) {
+    k_nbr_counts<<<grid_for(nloc, 256), 256, 0, s>>>(nloc, nnbr, glist.p, sds.p, h->d_rank_of_gsd.p, h->d_nbr.p, rank,
+                                                     rc.p, sc.p);
+    CB_LAUNCH();
+    tb = 0;
+    CB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, rc.p, rc.p + nn, (int)nloc, s));
+    tmp.alloc(std::max(tmp.n, tb));
+    std::vector<int32_t> tot((size_t)2 * nnbr);
+    for (int k = 0; k < nnbr; ++k) {
+      const size_t o = (size_t)k * nloc;
+      CB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, rc.p + o, rc.p + nn + o, (int)nloc, s));
+      CB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, sc.p + o, sc.p + nn + o, (int)nloc, s));
+      CB_CUDA(cudaMemcpyAsync(&tot[(size_t)2 * k], rc.p + nn + o + nloc - 1, 4, cudaMemcpyDeviceToHost, s));
+      CB_CUDA(cudaMemcpyAsync(&tot[(size_t)2 * k + 1], sc.p + nn + o + nloc - 1, 4, cudaMemcpyDeviceToHost, s));
+    }
+    CB_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k < nnbr; ++k) {
+      rbase.push_back(rbase.back() + tot[(size_t)2 * k]);
+      sbase.push_back(sbase.back() + tot[(size_t)2 * k + 1]);
+    }
+  }
+  h->recv_ptr = rbase;
+  h->send_ptr = sbase;
+  h->d_rbase.upload(rbase, s);
+  h->d_sbase.upload(sbase, s);
+  h->send_src.alloc((size_t)std::max<int64_t>(1, sbase.back()));
+  h->sendbuf.alloc((size_t)std::max<int64_t>(1, sbase.back()));
+  h->recvbuf.alloc((size_t)std::max<int64_t>(1, rbase.back()));
+  // copy lists (local numbering)
+  h->lcopy_ptr.alloc((size_t)nloc + 1);
+  DevBuf<int32_t>& cc = h->ws_ccount;
+  cc.alloc((size_t)std::max<int64_t>(1, nloc));
+  k_copy_count<<<grid_for(nloc, 256), 256, 0, s>>>(nloc, h->loc_glob.p, nsds.p, cc.p);
+  CB_LAUNCH();
+  CB_CUDA(cudaMemsetAsync(h->lcopy_ptr.p, 0, 4, s));
+  tb = 0;
+  CB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, cc.p, h->lcopy_ptr.p + 1, (int)nloc, s));
+  tmp.alloc(std::max(tmp.n, tb));
+  CB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, cc.p, h->lcopy_ptr.p + 1, (int)nloc, s));
+  int32_t ncopy = 0;
+  CB_CUDA(cudaMemcpyAsync(&ncopy, h->lcopy_ptr.p + nloc, 4, cudaMemcpyDeviceToHost, s));
+  CB_CUDA(cudaStreamSynchronize(s));
+  h->n_copies = ncopy;
+  h->lcopy_src.alloc((size_t)std::max(1, ncopy));
+  h->lowner.alloc((size_t)std::max<int64_t>(1, nloc));
+  k_fill_plan<<<grid_for(nloc, 128), 128, 0, s>>>(nloc, nnbr, a, glist.p, h->loc_of_dof.p, sds.p, h->d_nbr_of_rank.p,
+                                                  rc.p + nn, rc.p, sc.p + nn, sc.p, h->d_rbase.p, h->d_sbase.p,
+                                                  h->lcopy_ptr.p, h->lcopy_src.p, h->send_src.p, h->lowner.p);
+  CB_LAUNCH();
+  const int64_t ns = (int64_t)nsd * T;
+  h->slot_loc.alloc((size_t)ns);
+  k_slot_loc<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->loc_of_dof.p, h->slot_loc.p);
+  CB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- exchange
+void iface_exchange(cutbddc_gpu* h, const double* Y, const double* w, const int* skip) {
+  const int nnbr = (int)h->nbr.size();
+  if (nnbr == 0) return;
+  if (!h->comm) throw Failure(CUTBDDC_CONFIG, "interface exchange: the handle has no communicator (plan-only distribution)");
+  cudaStream_t s = h->stream;
+  const int64_t nsend = h->send_ptr.back();
+  k_pack<<<grid_for(std::max<int64_t>(1, nsend), 256), 256, 0, s>>>(nsend, h->send_src.p, w, Y, h->sendbuf.p, skip);
+  CB_LAUNCH();
+  nccl_check(ncclGroupStart(), "group start");
+  for (int k = 0; k < nnbr; ++k) {
+    const size_t ns = (size_t)(h->send_ptr[(size_t)k + 1] - h->send_ptr[(size_t)k]);
+    const size_t nr = (size_t)(h->recv_ptr[(size_t)k + 1] - h->recv_ptr[(size_t)k]);
+    if (ns) nccl_check(ncclSend(h->sendbuf.p + h->send_ptr[(size_t)k], ns, ncclDouble, h->nbr[(size_t)k], h->comm, s), "send");
+    if (nr) nccl_check(ncclRecv(h->recvbuf.p + h->recv_ptr[(size_t)k], nr, ncclDouble, h->nbr[(size_t)k], h->comm, s), "recv");
+  }
+  nccl_check(ncclGroupEnd(), "group end");
+}
+
+void iface_sum(cutbddc_gpu* h, const double* Y, const double* w, double* out, const int* skip) {
+  k_isum<<<grid_for(std::max<int64_t>(1, h->n_loc), 256), 256, 0, h->stream>>>(h->n_loc, h->lcopy_ptr.p, h->lcopy_src.p,
+                                                                                w, Y, h->recvbuf.p, out, skip);
+  CB_LAUNCH();
+}
+
+void gather_partials(cutbddc_gpu* h, double* part) {
+  if (h->dist_world == 1) return;
+  if (!h->comm) throw Failure(CUTBDDC_CONFIG, "partials: the handle has no communicator (plan-only distribution)");
+  nccl_check(ncclAllGather(part + (int64_t)h->dist_rank * h->maxloc, part, (size_t)h->maxloc, ncclDouble, h->comm,
+                           h->stream),
+             "all-gather");
+}
+
+void gather_rows(cutbddc_gpu* h) {
+  if (h->dist_world == 1) return;
+  if (!h->comm) throw Failure(CUTBDDC_CONFIG, "coarse rows: the handle has no communicator (plan-only distribution)");
+  nccl_check(ncclAllGather(h->gl.p + (int64_t)h->dist_rank * h->maxrows, h->gl.p, (size_t)h->maxrows, ncclDouble,
+                           h->comm, h->stream),
+             "all-gather");
+}
+
+void gather_blocks(cutbddc_gpu* h) {
+  if (h->dist_world == 1) return;
+  if (!h->comm) throw Failure(CUTBDDC_CONFIG, "coarse blocks: the handle has no communicator (plan-only distribution)");
+  nccl_check(ncclAllGather(h->ac_loc.p + (int64_t)h->dist_rank * h->maxac, h->ac_loc.p, (size_t)h->maxac, ncclDouble,
+                           h->comm, h->stream),
+             "all-gather");
+}
+
+int agree_status(cutbddc_gpu* h, int code) {
+  if (h->dist_world == 1 || !h->comm) return code;
+  DevBuf<int>& f = h->ws_flag;
+  f.alloc(1);
+  CB_CUDA(cudaMemcpyAsync(f.p, &code, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  nccl_check(ncclAllReduce(f.p, f.p, 1, ncclInt32, ncclMax, h->comm, h->stream), "status");
+  int out = 0;
+  CB_CUDA(cudaMemcpyAsync(&out, f.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CB_CUDA(cudaStreamSynchronize(h->stream));
+  return out;
+}
+
+void sub_apply(cutbddc_gpu* h, int mode, const double* xloc, const double* Xslot, double* Y, const int* skip) {
+  const size_t shm = sizeof(double) * (size_t)h->slots + sizeof(int32_t) * (size_t)h->block * h->block * h->block;
+  if (shm > 200 * 1024) throw Failure(CUTBDDC_CONFIG, "matrix-free operator: block too large for shared memory");
+  SubArgs a{h->n, h->block, h->b1, h->slots, h->nb, h->block_ids.p, h->elem_of_cell.p, h->ke.p, h->empty.p,
+            h->ws_kint.p, h->slot_loc.p, h->mask_int.p, h->odiag.p};
+  auto launch = [&](auto kern) {
+    if (shm > 48 * 1024) CB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    kern<<<h->nsd, 512, shm, h->stream>>>(a, xloc, Xslot, Y, skip);
+  };
+  if (mode == kSubAll) launch(k_sub_apply<kSubAll>);
+  else if (mode == kSubInterface) launch(k_sub_apply<kSubInterface>);
+  else launch(k_sub_apply<kSubInterior>);
+  CB_LAUNCH();
+}
+
+void to_local(cutbddc_gpu* h, const double* xglob, double* xloc) {
+  k_to_local<<<grid_for(std::max<int64_t>(1, h->n_loc), 256), 256, 0, h->stream>>>(h->n_loc, h->loc_glob.p, xglob, xloc);
+  CB_LAUNCH();
+}
+
+void to_global_owned(cutbddc_gpu* h, const double* xloc, double* xglob) {
+  k_to_global<<<grid_for(std::max<int64_t>(1, h->n_own), 256), 256, 0, h->stream>>>(h->n_own, h->loc_glob.p, xloc, xglob);
+  CB_LAUNCH();
+}
+
+}  // namespace cutbddc_b200

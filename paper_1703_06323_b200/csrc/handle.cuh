@@ -6,7 +6,8 @@
 //   cut cells:   ke[ncut][64] f64, fe[ncut][8] f64, beta[ncut], empty[ncut]
 //   subdomains:  slot space of the (B+1)^3 block lattice, T slots per subdomain:
 //                slot_dof[nsd][T] i32, As[nsd][27][T] f64 (stencil of A^w, SoA over slots)
-//   Abar:        ELL-27, aval[27][n_dof] f64, acol[27][n_dof] i32 (SoA, coalesced by row)
+//   Abar:        never assembled (matrix-free Σ_w R_w^T A_w R_w, dist.cu)
+//   vectors:     local dof space of the rank (segments per subdomain + ghosts, dist.cuh)
 //   bddc:        weights w[nsd][T], interior/present masks, factor panels
 //                GI/GK[nsd][panel_total] (column-major per supernode), Phi[sum m][T]
 #pragma once
@@ -81,12 +82,37 @@ struct cutbddc_gpu {
   std::mutex mu;
   cutbddc_b200::Prof prof;                       // CUTBDDC_PROFILE=1 phase timing
 
-  // ---------------------------------------------------------------- multi-GPU
-  // Subdomains are distributed over ranks; global dof vectors are replicated.
-  // comm == nullptr: one process owns every subdomain (no collectives).
+  // ---------------------------------------------------------------- multi-GPU (dist.cu)
+  // Subdomains are distributed over ranks; each rank holds the vectors of
+  // its local dof space (its subdomains' dofs, dist.cuh). comm == nullptr:
+  // no collectives (one rank, or a plan-only distribution).
   ncclComm_t comm = nullptr;
-  int nsd_global = 0;                            // 0: local == global numbering
+  bool dist_set = false, dist_explicit = false;  // distribution known / set by the caller
+  bool plan_only = false;                        // world > 1 without a communicator: plan inspection only
+  int dist_block = 0, dist_rank = 0, dist_world = 1;
+  int nsd_g = 0;                                 // subdomains of the global partition
+  std::vector<int64_t> g_block_ids;              // nsd_g, ascending
+  std::vector<int32_t> rank_of_gsd;              // nsd_g
+  std::vector<int32_t> lidx_of_gsd;              // nsd_g: index among its rank's subdomains
   std::vector<int32_t> global_of_local;          // nsd
+  int maxloc = 0;                                // most subdomains on one rank (stride of gathered partials)
+  cutbddc_b200::DevBuf<int32_t> d_gpos;          // nsd_g: position of each subdomain's gathered partial
+  cutbddc_b200::DevBuf<int32_t> d_gsd_of_block, d_rank_of_gsd, d_lsd_of_gsd, d_nbr, d_nbr_of_rank;
+  cutbddc_b200::DevBuf<int64_t> d_gblock, d_rbase, d_sbase;
+  // local dof space: segments of owned dofs per local subdomain, then ghosts
+  int64_t n_loc = 0, n_own = 0;
+  cutbddc_b200::DevBuf<int32_t> loc_glob;        // n_loc: global dof of each local dof
+  cutbddc_b200::DevBuf<int32_t> loc_of_dof;      // n_dof: local dof or -1
+  cutbddc_b200::DevBuf<int32_t> seg_ptr;         // nsd + 1
+  cutbddc_b200::DevBuf<int32_t> slot_loc;        // nsd*T: local dof of each slot or -1
+  cutbddc_b200::DevBuf<int32_t> lcopy_ptr;       // n_loc + 1
+  cutbddc_b200::DevBuf<int32_t> lcopy_src;       // copies, ascending global sd: >= 0 slot (sd*T+slot), < 0: -1 - receive index
+  cutbddc_b200::DevBuf<int32_t> lowner;          // n_loc: slot of an interior dof (one copy), else -1
+  // interface exchange: one message per neighbour rank and direction
+  std::vector<int32_t> nbr;                      // neighbour ranks, ascending
+  std::vector<int64_t> send_ptr, recv_ptr;       // nbr + 1 offsets into sendbuf / recvbuf
+  cutbddc_b200::DevBuf<int32_t> send_src;        // slot of every sent value
+  cutbddc_b200::DevBuf<double> sendbuf, recvbuf;
 
   // ---------------------------------------------------------------- mesh
   int n = 0;                   // cells per axis
@@ -113,19 +139,17 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int32_t> sd_of_block;     // nb^3, -1 for empty blocks
   cutbddc_b200::DevBuf<int32_t> slot_dof;        // nsd*T
   cutbddc_b200::DevBuf<double> As;               // nsd*27*T
-  cutbddc_b200::DevBuf<uint8_t> ncount, orphan;  // per dof (ncount over all ranks' subdomains)
-  cutbddc_b200::DevBuf<uint8_t> lcount;          // per dof: copies in this rank's subdomains
-  cutbddc_b200::DevBuf<double> dtot;             // per dof: sum of A^w diagonals over all copies
-  cutbddc_b200::DevBuf<int64_t> copy_ptr;        // n_dof+1
-  cutbddc_b200::DevBuf<int64_t> copy_idx;        // sd*T + slot, ascending sd
+  cutbddc_b200::DevBuf<uint8_t> ncount, orphan;  // per global dof: |neigh| over all ranks, strong-Dirichlet flag
+  cutbddc_b200::DevBuf<uint8_t> vcell;           // per cell: void cut cell (empty volume rule), all ranks
+  cutbddc_b200::DevBuf<double> dtot;             // per local dof: sum of A^w diagonals over all copies
+  cutbddc_b200::DevBuf<double> odiag;            // per slot: 1/|neigh| at strong-Dirichlet slots, else 0
+  cutbddc_b200::DevBuf<double> fs;               // per slot: sub-assembled load vector
   int64_t n_copies = 0;
-  cutbddc_b200::DevBuf<int32_t> if_dofs;         // dofs with ncount >= 2
-  int64_t n_if = 0;
-  cutbddc_b200::DevBuf<int64_t> owner_slot;      // per dof: sd*T+slot if interior, -1 else
+  int64_t n_if = 0;                              // interface dofs of the global problem
 
-  // ---------------------------------------------------------------- global operator
-  cutbddc_b200::DevBuf<double> aval, b;
-  cutbddc_b200::DevBuf<int32_t> acol;
+  // ---------------------------------------------------------------- operator
+  // Abar is never assembled: Abar x = Σ_w R_w^T A_w R_w x, matrix-free (dist.cu sub_apply)
+  cutbddc_b200::DevBuf<double> b;                // assembled rhs, local dofs
   bool assembled = false;
   double t_assembly = 0;
 
@@ -158,10 +182,15 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int32_t> coarse_id;        // m_total
   cutbddc_b200::DevBuf<int32_t> row_sd;           // m_total: owning subdomain of each constraint row
   cutbddc_b200::DevBuf<int64_t> cg_ptr;           // n_coarse+1
-  cutbddc_b200::DevBuf<int64_t> cg_idx;           // row index into m_total, ascending sd
+  cutbddc_b200::DevBuf<int64_t> cg_idx;           // staged row position (dist.cuh), ascending global sd
+  // staged coarse layout: rows (and m x m blocks) of every subdomain at
+  // rank * maxrows (rank * maxac) + the rank's earlier subdomains' share
+  int64_t maxrows = 1, maxac = 1, m_total_g = 0;
+  cutbddc_b200::DevBuf<int64_t> srow;             // 3 per staged row: first row of its sd, m, block offset
+  cutbddc_b200::DevBuf<int32_t> scoarse;          // coarse id of every staged row
   cutbddc_b200::DevBuf<double> w;                 // nsd*T
   cutbddc_b200::DevBuf<double> rho;               // nsd
-  cutbddc_b200::DevBuf<double> ac_loc;            // per sd m*m (offsets m_off^2 prefix)
+  cutbddc_b200::DevBuf<double> ac_loc;            // staged m x m blocks A_c,w (this rank's at rank * maxac + ac_off)
   cutbddc_b200::DevBuf<int64_t> ac_off;           // nsd+1
   cutbddc_b200::DevBuf<double> acoarse;
   cutbddc_b200::DevBuf<double> acoarse_inv;       // X = L_c^{-1} (lower, column-major n_c x n_c)
@@ -186,7 +215,7 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<double> sv0, sv1, sv2;     // slot vectors nsd*T
   cutbddc_b200::DevBuf<double> ysave;             // big-front forward results, nsd*T
   cutbddc_b200::DevBuf<double> upd;               // solve workspace nsd*upd_total (x nrhs for setup)
-  cutbddc_b200::DevBuf<double> gv0, gv1, gv2, gv3;  // global vectors n_dof
+  cutbddc_b200::DevBuf<double> gv0, gv2;         // local dof vectors (z0, v)
   cutbddc_b200::DevBuf<double> gl, cy, zc, gc;    // m_total, m_total, n_coarse, n_coarse
   cutbddc_b200::DevBuf<double> partials;          // reduction partials
   cutbddc_b200::DevBuf<double> scal;              // device scalars (pcg)
@@ -196,6 +225,10 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<double> ws_front, ws_upd, ws_s, ws_lc, ws_cpart, ws_q8, ws_kint;
   cutbddc_b200::DevBuf<unsigned long long> ws_fail;
   cutbddc_b200::DevBuf<int64_t> ws_cnt, ws_nc64;
+  cutbddc_b200::DevBuf<int32_t> ws_sds, ws_seg, ws_glist, ws_keys, ws_rc, ws_sc, ws_ccount;  // plan scratch (dist.cu)
+  cutbddc_b200::DevBuf<uint8_t> ws_nsds, ws_local;
+  cutbddc_b200::DevBuf<uint32_t> ws_rmask;
+  cutbddc_b200::DevBuf<unsigned int> ws_omask;
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp, ws_obj;
   cutbddc_b200::DevBuf<int> ws_flag;
   cutbddc_b200::DevBuf<int32_t> ws_coff;                       // corner coarse basis: front column offsets
@@ -207,6 +240,8 @@ struct cutbddc_gpu {
   // pcg vectors
   cutbddc_b200::DevBuf<double> px, pr, pz, pp, pq, pb, hist, lal, lbe;
   cudaGraphExec_t graph_exec = nullptr;
+  cudaGraphExec_t graph_exec_ref = nullptr;      // several ranks: the iteration with the k % 50 refresh
+  long long graph_nodes_ref = 0;
   int graph_max_iter = -1;
   long long graph_nodes = 0;                      // kernel nodes per PCG-iteration graph
   bool graph_while = false;                       // graph_exec runs the whole loop (conditional WHILE node)

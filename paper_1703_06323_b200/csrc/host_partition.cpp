@@ -13,6 +13,7 @@
 // ordered by smallest global dof, nodes ascending; singletons -> Corner;
 // strong-Dirichlet (orphan) dofs excluded.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -434,5 +435,161 @@ extern "C" cutbddc_status cutbddc_assign_subdomains(const cutbddc_partition_view
       rank_of_sd[s] = std::min(world - 1, std::max(0, r));
       acc += c;
     }
+  });
+}
+
+// Interface exchange plan of one rank, on the host: the same arrays, in the
+// same order, as the device plan (dist.cu build_plan_device; compared entry
+// for entry by tests/test_gpu_dist.py). Used by the multi-process CPU tests
+// (tests/test_multigpu_gloo.py) to drive real exchanges with product lists.
+extern "C" cutbddc_status cutbddc_build_exchange_plan(const cutbddc_mesh_view* mesh, const cutbddc_partition_view* part,
+                                                      const int32_t* rank_of_sd, int rank, int world,
+                                                      cutbddc_exchange_plan** out) {
+  using namespace cutbddc_b200;
+  return guard([&] {
+    check_mesh(mesh);
+    if (!part || !part->block_ids || part->n_sd < 1 || !rank_of_sd || !out)
+      throw Failure(CUTBDDC_INVALID_ARGUMENT, "exchange plan: null argument");
+    if (world < 1 || world > 32 || rank < 0 || rank >= world)
+      throw Failure(CUTBDDC_INVALID_ARGUMENT, "exchange plan: rank / world out of range");
+    const int n = mesh->cells[0], B = part->block;
+    if (B < 1 || n % B) throw Failure(CUTBDDC_INVALID_ARGUMENT, "partition: mesh dims not divisible by H/h");
+    const int nb = n / B, b1 = B + 1, T = b1 * b1 * b1, nsd_g = part->n_sd;
+    Lattice L{n, mesh->cls, mesh->dof_of_node};
+    std::vector<int32_t> gsd_of_block((size_t)nb * nb * nb, -1), lsd((size_t)nsd_g, -1);
+    int nsd = 0;
+    for (int g = 0; g < nsd_g; ++g) {
+      gsd_of_block[(size_t)part->block_ids[g]] = g;
+      if (rank_of_sd[g] < 0 || rank_of_sd[g] >= world) throw Failure(CUTBDDC_INVALID_ARGUMENT, "exchange plan: bad rank_of_sd");
+      if (rank_of_sd[g] == rank) lsd[(size_t)g] = nsd++;
+    }
+    const int64_t nd = mesh->n_dof;
+    std::vector<int64_t> node_of_dof((size_t)nd);
+    for (int64_t v = 0; v < (int64_t)(n + 1) * (n + 1) * (n + 1); ++v)
+      if (mesh->dof_of_node[v] >= 0) node_of_dof[(size_t)mesh->dof_of_node[v]] = v;
+    // subdomains of every dof (ascending), local dofs
+    std::vector<std::array<int32_t, 8>> sds((size_t)nd);
+    std::vector<uint8_t> ns((size_t)nd);
+    std::vector<int32_t> glist;
+    for (int64_t d = 0; d < nd; ++d) {
+      int c[3];
+      L.node_ijk(node_of_dof[(size_t)d], c);
+      int m = 0;
+      std::array<int32_t, 8>& s = sds[(size_t)d];
+      for (int dx = 0; dx < 2; ++dx)
+        for (int dy = 0; dy < 2; ++dy)
+          for (int dz = 0; dz < 2; ++dz) {
+            const int ci = c[0] - 1 + dx, cj = c[1] - 1 + dy, ck = c[2] - 1 + dz;
+            if (ci < 0 || cj < 0 || ck < 0 || ci >= n || cj >= n || ck >= n) continue;
+            if (mesh->cls[L.cell(ci, cj, ck)] == CUTBDDC_EXTERIOR) continue;
+            const int32_t g = gsd_of_block[((size_t)(ci / B) * nb + cj / B) * nb + ck / B];
+            if (std::find(s.begin(), s.begin() + m, g) == s.begin() + m) s[(size_t)m++] = g;
+          }
+      std::sort(s.begin(), s.begin() + m);
+      ns[(size_t)d] = (uint8_t)m;
+      bool loc = false;
+      for (int q = 0; q < m; ++q) loc |= rank_of_sd[s[(size_t)q]] == rank;
+      if (loc) glist.push_back((int32_t)d);
+    }
+    const int64_t nloc = (int64_t)glist.size();
+    auto seg = [&](int32_t d) {
+      const int32_t g0 = sds[(size_t)d][0];
+      return rank_of_sd[g0] == rank ? lsd[(size_t)g0] : nsd;
+    };
+    std::vector<int32_t> loc_glob(glist);
+    std::stable_sort(loc_glob.begin(), loc_glob.end(), [&](int32_t a, int32_t b) { return seg(a) < seg(b); });
+    std::vector<int32_t> seg_ptr((size_t)nsd + 1, 0), loc_of_dof((size_t)nd, -1);
+    for (int64_t i = 0; i < nloc; ++i) loc_of_dof[(size_t)loc_glob[(size_t)i]] = (int32_t)i;
+    for (int s2 = 0; s2 <= nsd; ++s2)
+      seg_ptr[(size_t)s2] = (int32_t)(std::lower_bound(loc_glob.begin(), loc_glob.end(), s2,
+                                                       [&](int32_t d, int key) { return seg(d) < key; }) -
+                                      loc_glob.begin());
+    auto count_rank = [&](int32_t d, int q) {
+      int c = 0;
+      for (int x = 0; x < ns[(size_t)d]; ++x) c += rank_of_sd[sds[(size_t)d][(size_t)x]] == q;
+      return c;
+    };
+    std::vector<int32_t> nbr;
+    std::vector<int> nbr_of_rank((size_t)world, -1);
+    {
+      std::vector<uint8_t> seen((size_t)world, 0);
+      for (int32_t d : glist)
+        for (int x = 0; x < ns[(size_t)d]; ++x) seen[(size_t)rank_of_sd[sds[(size_t)d][(size_t)x]]] = 1;
+      for (int q = 0; q < world; ++q)
+        if (q != rank && seen[(size_t)q]) {
+          nbr_of_rank[(size_t)q] = (int)nbr.size();
+          nbr.push_back(q);
+        }
+    }
+    const int nn = (int)nbr.size();
+    // message offsets of every dof (ascending global order)
+    std::vector<int64_t> send_ptr(1, 0), recv_ptr(1, 0);
+    std::vector<std::vector<int64_t>> roff((size_t)nn, std::vector<int64_t>((size_t)nloc)),
+        soff((size_t)nn, std::vector<int64_t>((size_t)nloc));
+    for (int k = 0; k < nn; ++k) {
+      int64_t r = 0, sacc = 0;
+      for (int64_t j = 0; j < nloc; ++j) {
+        const int32_t d = glist[(size_t)j];
+        const int cq = count_rank(d, nbr[(size_t)k]);
+        roff[(size_t)k][(size_t)j] = r;
+        soff[(size_t)k][(size_t)j] = sacc;
+        r += cq;
+        sacc += cq > 0 ? count_rank(d, rank) : 0;
+      }
+      recv_ptr.push_back(recv_ptr.back() + r);
+      send_ptr.push_back(send_ptr.back() + sacc);
+    }
+    std::vector<int32_t> copy_ptr((size_t)nloc + 1, 0);
+    for (int64_t i = 0; i < nloc; ++i) copy_ptr[(size_t)i + 1] = copy_ptr[(size_t)i] + ns[(size_t)loc_glob[(size_t)i]];
+    std::vector<int32_t> copy_src((size_t)copy_ptr[(size_t)nloc]), send_src((size_t)send_ptr.back());
+    for (int64_t j = 0; j < nloc; ++j) {
+      const int32_t d = glist[(size_t)j];
+      const int32_t i = loc_of_dof[(size_t)d];
+      int c[3];
+      L.node_ijk(node_of_dof[(size_t)d], c);
+      std::vector<int> pos_q((size_t)world, 0);
+      int32_t p = copy_ptr[(size_t)i];
+      int mloc = 0;
+      for (int x = 0; x < ns[(size_t)d]; ++x) {
+        const int32_t g = sds[(size_t)d][(size_t)x];
+        const int q = rank_of_sd[g];
+        if (q == rank) {
+          const int64_t bid = part->block_ids[g];
+          const int bi = (int)(bid / nb / nb), bj = (int)((bid / nb) % nb), bk = (int)(bid % nb);
+          const int32_t src = lsd[(size_t)g] * T + ((c[0] - bi * B) * b1 + (c[1] - bj * B)) * b1 + (c[2] - bk * B);
+          copy_src[(size_t)p++] = src;
+          for (int k = 0; k < nn; ++k)
+            if (count_rank(d, nbr[(size_t)k]) > 0) send_src[(size_t)(send_ptr[(size_t)k] + soff[(size_t)k][(size_t)j] + mloc)] = src;
+          ++mloc;
+        } else {
+          const int k = nbr_of_rank[(size_t)q];
+          copy_src[(size_t)p++] = -1 - (int32_t)(recv_ptr[(size_t)k] + roff[(size_t)k][(size_t)j] + pos_q[(size_t)q]++);
+        }
+      }
+    }
+    auto* r = new cutbddc_exchange_plan();
+    r->n_loc = nloc;
+    r->n_own = seg_ptr[(size_t)nsd];
+    r->n_sd_local = nsd;
+    r->n_nbr = nn;
+    auto dup32 = [](const std::vector<int32_t>& v) {
+      auto* a = new int32_t[v.size() + 1];
+      std::copy(v.begin(), v.end(), a);
+      return a;
+    };
+    auto dup64 = [](const std::vector<int64_t>& v) {
+      auto* a = new int64_t[v.size() + 1];
+      std::copy(v.begin(), v.end(), a);
+      return a;
+    };
+    r->loc_glob = dup32(loc_glob);
+    r->seg_ptr = dup32(seg_ptr);
+    r->copy_ptr = dup32(copy_ptr);
+    r->copy_src = dup32(copy_src);
+    r->nbr = dup32(nbr);
+    r->send_ptr = dup64(send_ptr);
+    r->send_src = dup32(send_src);
+    r->recv_ptr = dup64(recv_ptr);
+    *out = r;
   });
 }

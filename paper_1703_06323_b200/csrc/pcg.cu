@@ -7,11 +7,17 @@
 // non-converged report. Lanczos alpha/beta are recorded for
 // condition_estimate (evaluated on the host).
 //
-// The whole iteration (SpMV, dots, axpys, BDDC apply) is one CUDA graph with
-// all scalars on the device; a device "done" flag turns the remaining
-// kernels of a converged solve into no-ops, so the host only polls the flag
-// every few graph launches (no per-iteration host round trip). Dots are
-// two-stage fixed-order reductions: bit-reproducible run to run.
+// Vectors live in the rank's local dof space (dist.cuh). Abar p is the
+// matrix-free sub-assembled product plus the interface sum. Every dot is a
+// per-subdomain partial over the subdomain's owned segment, all-gathered
+// over ranks and summed in global subdomain order inside each consumer
+// kernel: the scalars are the same bits on 1, 2, 4 or 8 GPUs, so every rank
+// takes the same branch at the same iteration.
+//
+// One GPU: the whole loop is one CUDA graph with a conditional WHILE node,
+// all scalars on the device. Several GPUs: one captured graph per iteration
+// (with or without the k % 50 refresh), launched in batches by the host; a
+// device "done" flag turns the kernels of a finished solve into no-ops.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -19,130 +25,134 @@
 
 #include "bddc.cuh"
 #include "comm.cuh"
+#include "dist.cuh"
 
 namespace cutbddc_b200 {
 namespace {
-
-constexpr int kRedBlocks = 592;  // 4 x 148 SMs, fixed for deterministic reductions
-constexpr int kRedThreads = 256;
 
 // rz ping-pongs between S_RZ (even iterations) and S_RZ1 (odd): the fused
 // beta/p-update kernel reads the old value in every block while block 0
 // stores the new one.
 enum { S_RZ = 0, S_PQ, S_ALPHA, S_BETA, S_STOP, S_RN, S_RZ1, S_COUNT };
 __device__ __forceinline__ int rz_slot(int k) { return (k & 1) ? S_RZ1 : S_RZ; }
-enum { I_DONE = 0, I_ITER, I_ERR, I_ITERS, I_CONV, I_MAXIT, I_COUNT };
+// I_NOREF: 1 unless this iteration replaces r by b - Abar x (k % 50 == 0)
+enum { I_DONE = 0, I_ITER, I_ERR, I_ITERS, I_CONV, I_MAXIT, I_NOREF, I_COUNT };
 
-__global__ void __launch_bounds__(kRedThreads) k_spmv_dot(int64_t nd, const double* __restrict__ aval,
-                                                          const int32_t* __restrict__ acol, const double* __restrict__ x,
-                                                          double* __restrict__ y, double* __restrict__ partial,
-                                                          const int* __restrict__ skip) {
+struct Fin {  // where the gathered partials are summed from
+  const int32_t* gpos;
+  int nsd_g;
+};
+
+// q = Σ_copies Y (Abar p), and the p.q partials
+__global__ void __launch_bounds__(kSegThreads) k_spmv_dot(SegArgs a, const int32_t* __restrict__ cptr,
+                                                          const int32_t* __restrict__ csrc, const double* __restrict__ Y,
+                                                          const double* __restrict__ recv, const double* __restrict__ p,
+                                                          double* __restrict__ q, const int* __restrict__ skip) {
   if (skip && *skip) return;
   __shared__ double sh[32];
+  int lo, hi;
+  const bool part = seg_range(a, lo, hi);
   double acc = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < 27; ++k) s += aval[(int64_t)k * nd + i] * x[acol[(int64_t)k * nd + i]];
-    y[i] = s;
-    acc += x[i] * s;
+  for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
+    double v = 0.0;
+    for (int32_t c = cptr[i]; c < cptr[i + 1]; ++c) {
+      const int32_t src = csrc[c];
+      v += src >= 0 ? Y[src] : recv[-1 - src];
+    }
+    q[i] = v;
+    acc += p[i] * v;
   }
-  acc = block_sum<kRedThreads>(acc, sh);
-  if (partial && threadIdx.x == 0) partial[blockIdx.x] = acc;
+  if (!part || !a.part) return;
+  acc = block_sum<kSegThreads>(acc, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
 }
 
-__global__ void __launch_bounds__(kRedThreads) k_dot(int64_t nd, const double* __restrict__ a, const double* __restrict__ b,
-                                                     double* __restrict__ partial, const int* __restrict__ skip) {
-  if (skip && *skip) return;
+// partials of a.b
+__global__ void __launch_bounds__(kSegThreads) k_seg_dot(SegArgs a, const double* __restrict__ x,
+                                                         const double* __restrict__ y) {
   __shared__ double sh[32];
+  int lo, hi;
+  if (!seg_range(a, lo, hi)) return;
   double acc = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x)
-    acc += a[i] * b[i];
-  acc = block_sum<kRedThreads>(acc, sh);
-  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+  for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) acc += x[i] * y[i];
+  acc = block_sum<kSegThreads>(acc, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
 }
 
-__device__ inline double finish_sum(const double* partial, double* sh) {
-  double v = 0.0;
-  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) v += partial[i];
-  return block_sum<kRedThreads>(v, sh);
-}
-
-// finish_sum, the total broadcast to every thread of the block
-__device__ inline double finish_sum_all(const double* partial, double* sh) {
-  __shared__ double tot;
-  const double v = finish_sum(partial, sh);
-  if (threadIdx.x == 0) tot = v;
-  __syncthreads();
-  return tot;
-}
-
-// alpha = rz / pq (every block from the same fixed-order sum of `partial`),
-// x += alpha p, r -= alpha q, and the partials of r.r for k_check in `rpart`
-// (k_dot's mapping; at a refresh iteration k_refresh writes them instead)
-__global__ void __launch_bounds__(kRedThreads) k_update_xr(int64_t nd, double* __restrict__ sc,
-                                                           const double* __restrict__ p, const double* __restrict__ q,
-                                                           double* __restrict__ x, double* __restrict__ r,
-                                                           double* __restrict__ lal, const double* __restrict__ partial,
-                                                           double* __restrict__ rpart, int* __restrict__ is) {
+// alpha = rz / pq (pq from the gathered partials, the same in every block),
+// x += alpha p, r -= alpha q, and the r.r partials (not at a refresh
+// iteration: k_refresh replaces r and writes them)
+__global__ void __launch_bounds__(kSegThreads) k_update_xr(SegArgs a, Fin f, const double* __restrict__ pq_part,
+                                                           double* __restrict__ sc, const double* __restrict__ p,
+                                                           const double* __restrict__ q, double* __restrict__ x,
+                                                           double* __restrict__ r, double* __restrict__ lal,
+                                                           int* __restrict__ is) {
   if (is[I_DONE]) return;
   __shared__ double sh[32];
   const int k = is[I_ITER];
-  const double pq = finish_sum_all(partial, sh);
+  const double pq = finish_partials(pq_part, f.gpos, f.nsd_g);
   if (!(pq > 0.0)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       sc[S_PQ] = pq;
       is[I_ERR] = 1;
       is[I_DONE] = 1;
+      is[I_NOREF] = 1;
       is[I_ITERS] = k;
     }
     return;
   }
-  const double a = sc[rz_slot(k)] / pq;
-  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i0 == 0) {
+  const double al = sc[rz_slot(k)] / pq;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     sc[S_PQ] = pq;
-    sc[S_ALPHA] = a;
-    lal[k - 1] = a;
+    sc[S_ALPHA] = al;
+    lal[k - 1] = al;
   }
+  int lo, hi;
+  const bool part = seg_range(a, lo, hi);
   double acc = 0.0;
-  for (int64_t i = i0; i < nd; i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] += a * p[i];
-    const double ri = r[i] - a * q[i];
+  for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
+    x[i] += al * p[i];
+    const double ri = r[i] - al * q[i];
     r[i] = ri;
     acc += ri * ri;
   }
-  if (k % 50 == 0) return;  // k_refresh replaces r and its partials
-  acc = block_sum<kRedThreads>(acc, sh);
-  if (threadIdx.x == 0) rpart[blockIdx.x] = acc;
+  if (!part || k % 50 == 0) return;
+  acc = block_sum<kSegThreads>(acc, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
 }
 
-// true residual refresh at k % 50 == 0: r = b - Abar x, and the r.r partials
-__global__ void __launch_bounds__(kRedThreads) k_refresh(int64_t nd, const double* __restrict__ aval,
-                                                         const int32_t* __restrict__ acol, const double* __restrict__ x,
-                                                         const double* __restrict__ b, double* __restrict__ r,
-                                                         double* __restrict__ rpart, const int* __restrict__ is) {
-  if (is[I_DONE] || is[I_ITER] % 50 != 0) return;
+// true residual refresh at k % 50 == 0: r = b - Σ_copies Y (Y = A_w x_w),
+// and the r.r partials
+__global__ void __launch_bounds__(kSegThreads) k_refresh(SegArgs a, const int32_t* __restrict__ cptr,
+                                                         const int32_t* __restrict__ csrc, const double* __restrict__ Y,
+                                                         const double* __restrict__ recv, const double* __restrict__ b,
+                                                         double* __restrict__ r, const int* __restrict__ is) {
+  if (is[I_NOREF]) return;
   __shared__ double sh[32];
+  int lo, hi;
+  const bool part = seg_range(a, lo, hi);
   double acc = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < 27; ++k) s += aval[(int64_t)k * nd + i] * x[acol[(int64_t)k * nd + i]];
-    const double ri = b[i] - s;
+  for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
+    double v = 0.0;
+    for (int32_t c = cptr[i]; c < cptr[i + 1]; ++c) {
+      const int32_t src = csrc[c];
+      v += src >= 0 ? Y[src] : recv[-1 - src];
+    }
+    const double ri = b[i] - v;
     r[i] = ri;
     acc += ri * ri;
   }
-  acc = block_sum<kRedThreads>(acc, sh);
-  if (threadIdx.x == 0) rpart[blockIdx.x] = acc;
+  if (!part) return;
+  acc = block_sum<kSegThreads>(acc, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
 }
 
 // |r| -> history, convergence / max_iter test
-__global__ void k_check(const double* __restrict__ partial, double* __restrict__ sc, int* __restrict__ is,
-                        double* __restrict__ hist) {
+__global__ void __launch_bounds__(kSegThreads) k_check(Fin f, const double* __restrict__ rr_part,
+                                                       double* __restrict__ sc, int* __restrict__ is,
+                                                       double* __restrict__ hist) {
   if (is[I_DONE]) return;
-  __shared__ double sh[32];
-  const double rr = finish_sum(partial, sh);
+  const double rr = finish_partials(rr_part, f.gpos, f.nsd_g);
   if (threadIdx.x == 0) {
     const double rn = sqrt(rr);
     const int k = is[I_ITER];
@@ -160,20 +170,20 @@ __global__ void k_check(const double* __restrict__ partial, double* __restrict__
   }
 }
 
-// beta = rz_new / rz (every block from the same fixed-order sum; rz_new to
+// beta = rz_new / rz (every block from the same gathered partials; rz_new to
 // the other ping-pong slot), p = z + beta p
-__global__ void __launch_bounds__(kRedThreads) k_update_p(int64_t nd, const double* __restrict__ partial,
+__global__ void __launch_bounds__(kSegThreads) k_update_p(int64_t nloc, Fin f, const double* __restrict__ rz_part,
                                                           double* __restrict__ sc, const double* __restrict__ z,
                                                           double* __restrict__ p, double* __restrict__ lbe,
                                                           int* __restrict__ is) {
   if (is[I_DONE]) return;
-  __shared__ double sh[32];
   const int k = is[I_ITER];
-  const double rz = finish_sum_all(partial, sh);
+  const double rz = finish_partials(rz_part, f.gpos, f.nsd_g);
   if (!(rz > 0.0)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       is[I_ERR] = 2;
       is[I_DONE] = 1;
+      is[I_NOREF] = 1;
       is[I_ITERS] = k;
     }
     return;
@@ -185,30 +195,44 @@ __global__ void __launch_bounds__(kRedThreads) k_update_p(int64_t nd, const doub
     sc[rz_slot(k + 1)] = rz;
     lbe[k - 1] = beta;
   }
-  for (int64_t i = i0; i < nd; i += (int64_t)gridDim.x * blockDim.x) p[i] = z[i] + beta * p[i];
+  for (int64_t i = i0; i < nloc; i += (int64_t)gridDim.x * blockDim.x) p[i] = z[i] + beta * p[i];
 }
 
 __global__ void k_next(int* __restrict__ is) {
   if (is[I_DONE]) return;
-  is[I_ITER] += 1;
+  const int k = is[I_ITER] + 1;
+  is[I_ITER] = k;
+  is[I_NOREF] = k % 50 != 0;
+}
+
+// |b| -> residuals[0] and the stop threshold rtol |b|
+__global__ void __launch_bounds__(kSegThreads) k_init_norm(Fin f, const double* __restrict__ bb_part, double rtol,
+                                                           double* __restrict__ sc, double* __restrict__ hist) {
+  const double bb = finish_partials(bb_part, f.gpos, f.nsd_g);
+  if (threadIdx.x == 0) {
+    const double bn = sqrt(bb);
+    hist[0] = bn;
+    sc[S_STOP] = rtol * bn;
+  }
 }
 
 // initial: rz = r.z (after z = M r), p = z
-__global__ void k_init_rz(const double* __restrict__ partial, double* __restrict__ sc, int* __restrict__ is) {
-  __shared__ double sh[32];
-  const double rz = finish_sum(partial, sh);
+__global__ void __launch_bounds__(kSegThreads) k_init_rz(Fin f, const double* __restrict__ rz_part,
+                                                         double* __restrict__ sc, int* __restrict__ is) {
+  const double rz = finish_partials(rz_part, f.gpos, f.nsd_g);
   if (threadIdx.x == 0) {
     sc[rz_slot(1)] = rz;
     if (!(rz > 0.0)) {
       is[I_ERR] = 2;
       is[I_DONE] = 1;
+      is[I_NOREF] = 1;
       is[I_ITERS] = 0;
     }
   }
 }
 
-__global__ void k_copy(int64_t nd, const double* __restrict__ a, double* __restrict__ b) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
+__global__ void k_copy(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
 // Loop condition of the whole-solve graph: another iteration unless done.
@@ -216,7 +240,47 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle hc, const int* __restrict
   cudaGraphSetConditional(hc, is[I_DONE] ? 0u : 1u);
 }
 
-void enqueue_iteration(cutbddc_gpu* h);
+constexpr int kFlatBlocks = 592;  // 4 x 148 SMs for the flat vector kernels
+
+Fin fin(const cutbddc_gpu* h) { return Fin{h->d_gpos.p, h->nsd_g}; }
+double* part0(cutbddc_gpu* h) { return h->partials.p; }
+double* part1(cutbddc_gpu* h) { return h->partials.p + (int64_t)h->dist_world * h->maxloc; }
+
+// One iteration; refresh: include the k % 50 replacement of r (its kernels
+// check the device flag; with several ranks it is its own graph, so its
+// exchange runs only where it is needed)
+void enqueue_iteration(cutbddc_gpu* h, bool refresh) {
+  cudaStream_t s = h->stream;
+  int* is = h->iscal.p;
+  double* sc = h->scal.p;
+  const int sg = seg_grid(h);
+  // q = Abar p
+  sub_apply(h, kSubAll, h->pp.p, nullptr, h->sv2.p, is);
+  iface_exchange(h, h->sv2.p, nullptr, is);
+  k_spmv_dot<<<sg, kSegThreads, 0, s>>>(seg_args(h, part0(h)), h->lcopy_ptr.p, h->lcopy_src.p, h->sv2.p, h->recvbuf.p,
+                                        h->pp.p, h->pq.p, is);
+  CB_LAUNCH();
+  gather_partials(h, part0(h));
+  k_update_xr<<<sg, kSegThreads, 0, s>>>(seg_args(h, part1(h)), fin(h), part0(h), sc, h->pp.p, h->pq.p, h->px.p,
+                                         h->pr.p, h->lal.p, is);
+  CB_LAUNCH();
+  if (refresh) {
+    sub_apply(h, kSubAll, h->px.p, nullptr, h->sv2.p, is + I_NOREF);
+    iface_exchange(h, h->sv2.p, nullptr, is + I_NOREF);
+    k_refresh<<<sg, kSegThreads, 0, s>>>(seg_args(h, part1(h)), h->lcopy_ptr.p, h->lcopy_src.p, h->sv2.p,
+                                         h->recvbuf.p, h->pb.p, h->pr.p, is);
+    CB_LAUNCH();
+  }
+  gather_partials(h, part1(h));
+  k_check<<<1, kSegThreads, 0, s>>>(fin(h), part1(h), sc, is, h->hist.p);
+  CB_LAUNCH();
+  apply_bddc_device(h, h->pr.p, h->pz.p, is, part0(h));
+  gather_partials(h, part0(h));
+  k_update_p<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, fin(h), part0(h), sc, h->pz.p, h->pp.p, h->lbe.p, is);
+  CB_LAUNCH();
+  k_next<<<1, 1, 0, s>>>(is);
+  CB_LAUNCH();
+}
 
 // One graph for the whole PCG loop on one GPU: a conditional WHILE node whose
 // body is the captured iteration plus k_loop_cond. No host polling and no
@@ -244,7 +308,7 @@ bool build_while_graph(cutbddc_gpu* h) {
   const long long c0 = g_kernel_launches.load();
   if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
     return fail();
-  enqueue_iteration(h);
+  enqueue_iteration(h, true);
   k_loop_cond<<<1, 1, 0, s>>>(hc, h->iscal.p);
   const cudaError_t launch_err = cudaGetLastError();
   const cudaError_t cap_err = cudaStreamEndCapture(s, &body);
@@ -262,22 +326,22 @@ bool build_while_graph(cutbddc_gpu* h) {
   return true;
 }
 
-void enqueue_iteration(cutbddc_gpu* h) {
+// per-iteration graph (several ranks: NCCL calls inside)
+cudaGraphExec_t capture_iteration(cutbddc_gpu* h, bool refresh, long long* nodes) {
   cudaStream_t s = h->stream;
-  const int64_t nd = h->n_dof;
-  int* is = h->iscal.p;
-  double* sc = h->scal.p;
-  k_spmv_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->aval.p, h->acol.p, h->pp.p, h->pq.p, h->partials.p, is);
-  k_update_xr<<<kRedBlocks, kRedThreads, 0, s>>>(nd, sc, h->pp.p, h->pq.p, h->px.p, h->pr.p, h->lal.p, h->partials.p,
-                                                 h->partials.p + kRedBlocks, is);
-  k_refresh<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->aval.p, h->acol.p, h->px.p, h->pb.p, h->pr.p,
-                                               h->partials.p + kRedBlocks, is);
-  k_check<<<1, kRedThreads, 0, s>>>(h->partials.p + kRedBlocks, sc, is, h->hist.p);
-  apply_bddc_device(h, h->pr.p, h->pz.p, is);
-  k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pr.p, h->pz.p, h->partials.p, is);
-  k_update_p<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->partials.p, sc, h->pz.p, h->pp.p, h->lbe.p, is);
-  k_next<<<1, 1, 0, s>>>(is);
-  CB_LAUNCH();
+  cudaGraph_t g;
+  cudaGraphExec_t ex;
+  const long long c0 = g_kernel_launches.load();
+  CB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  enqueue_iteration(h, refresh);
+  CB_CUDA(cudaStreamEndCapture(s, &g));
+  CB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  size_t n = 0;
+  CB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+  *nodes = (long long)n;
+  g_kernel_launches.store(c0);  // captured, not executed
+  CB_CUDA(cudaGraphDestroy(g));
+  return ex;
 }
 
 // SPEC.md:440-448 on the host: extreme eigenvalues of the Lanczos tridiagonal
@@ -320,81 +384,79 @@ void lanczos_extremes(const std::vector<double>& al, const std::vector<double>& 
 }  // namespace
 
 void spmv_device(cutbddc_gpu* h, const double* x, double* y) {
-  k_spmv_dot<<<kRedBlocks, kRedThreads, 0, h->stream>>>(h->n_dof, h->aval.p, h->acol.p, x, y, nullptr, nullptr);
-  CB_LAUNCH();
+  if (h->plan_only) throw Failure(CUTBDDC_CONFIG, "spmv: plan-only distribution (no communicator)");
+  h->sv2.alloc((size_t)h->nsd * h->slots);
+  sub_apply(h, kSubAll, x, nullptr, h->sv2.p, nullptr);
+  iface_exchange(h, h->sv2.p, nullptr, nullptr);
+  iface_sum(h, h->sv2.p, nullptr, y, nullptr);
 }
 
-void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, cutbddc_solve_report* rep) {
+void pcg_device(cutbddc_gpu* h, const double* b_loc, double rtol, int max_iter, cutbddc_solve_report* rep) {
   if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "pcg: setup_bddc first");
   if (max_iter < 1) throw Failure(CUTBDDC_INVALID_ARGUMENT, "pcg: max_iter must be >= 1");
   cudaStream_t s = h->stream;
-  const int64_t nd = h->n_dof;
-  for (auto* v : {&h->px, &h->pr, &h->pz, &h->pp, &h->pq, &h->pb}) v->alloc((size_t)nd);
+  const int64_t nl = std::max<int64_t>(1, h->n_loc);
+  for (auto* v : {&h->px, &h->pr, &h->pz, &h->pp, &h->pq, &h->pb}) v->alloc((size_t)nl);
   h->hist.alloc((size_t)max_iter + 1);
   h->lal.alloc((size_t)max_iter + 1);
   h->lbe.alloc((size_t)max_iter + 1);
-  h->partials.alloc(2 * kRedBlocks);  // p.q / r.z partials, then r.r
+  h->partials.alloc((size_t)2 * h->dist_world * h->maxloc);  // p.q / r.z, then r.r (gathered layout)
+  h->partials.zero(s);
   h->scal.alloc(S_COUNT);
   h->iscal.alloc(I_COUNT);
   cudaEvent_t e0, e1;
   CB_CUDA(cudaEventCreate(&e0));
   CB_CUDA(cudaEventCreate(&e1));
   CB_CUDA(cudaEventRecord(e0, s));
-  k_copy<<<kRedBlocks, kRedThreads, 0, s>>>(nd, b_dev, h->pb.p);
+  const int sg = seg_grid(h);
+  k_copy<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, b_loc, h->pb.p);
   CB_LAUNCH();
-  k_copy<<<kRedBlocks, kRedThreads, 0, s>>>(nd, b_dev, h->pr.p);
+  k_copy<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, b_loc, h->pr.p);
   CB_LAUNCH();
   h->px.zero(s);
   h->iscal.zero(s);
-  k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pb.p, h->pb.p, h->partials.p, nullptr);
+  h->scal.zero(s);
+  k_seg_dot<<<sg, kSegThreads, 0, s>>>(seg_args(h, part1(h)), h->pb.p, h->pb.p);
   CB_LAUNCH();
-  std::vector<double> part(kRedBlocks);
-  CB_CUDA(cudaMemcpyAsync(part.data(), h->partials.p, sizeof(double) * kRedBlocks, cudaMemcpyDeviceToHost, s));
+  gather_partials(h, part1(h));
+  k_init_norm<<<1, kSegThreads, 0, s>>>(fin(h), part1(h), rtol, h->scal.p, h->hist.p);
+  CB_LAUNCH();
+  double bnorm = 0.0;
+  CB_CUDA(cudaMemcpyAsync(&bnorm, h->hist.p, sizeof(double), cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
-  // same fixed-order tree as the device finish (block_sum over 256 threads)
-  // is not needed for |b|: the host value only seeds the stop threshold.
-  double bb = 0.0;
-  for (double v : part) bb += v;
-  const double bnorm = std::sqrt(bb);
-  CB_CUDA(cudaMemcpyAsync(h->hist.p, &bnorm, sizeof(double), cudaMemcpyHostToDevice, s));
   int conv = 0, iters = 0, err = 0;
   if (bnorm == 0.0) {
     h->px.zero(s);
     conv = 1;
   } else {
-    const double host_sc[S_COUNT] = {0, 0, 0, 0, rtol * bnorm, 0, 0};
-    CB_CUDA(cudaMemcpyAsync(h->scal.p, host_sc, sizeof(host_sc), cudaMemcpyHostToDevice, s));
-    const int host_is[I_COUNT] = {0, 1, 0, 0, 0, max_iter};
+    const int host_is[I_COUNT] = {0, 1, 0, 0, 0, max_iter, 1};
     CB_CUDA(cudaMemcpyAsync(h->iscal.p, host_is, sizeof(host_is), cudaMemcpyHostToDevice, s));
-    apply_bddc_device(h, h->pr.p, h->pz.p, nullptr);
-    k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pr.p, h->pz.p, h->partials.p, nullptr);
+    apply_bddc_device(h, h->pr.p, h->pz.p, nullptr, part0(h));
+    gather_partials(h, part0(h));
+    k_init_rz<<<1, kSegThreads, 0, s>>>(fin(h), part0(h), h->scal.p, h->iscal.p);
     CB_LAUNCH();
-    k_init_rz<<<1, kRedThreads, 0, s>>>(h->partials.p, h->scal.p, h->iscal.p);
-    CB_LAUNCH();
-    k_copy<<<kRedBlocks, kRedThreads, 0, s>>>(nd, h->pz.p, h->pp.p);
+    k_copy<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, h->pz.p, h->pp.p);
     CB_LAUNCH();
     if (h->graph_exec && h->graph_max_iter != max_iter) {
       cudaGraphExecDestroy(h->graph_exec);
       h->graph_exec = nullptr;
     }
-    if (!h->graph_exec && !distributed(h) && !std::getenv("CUTBDDC_NO_WHILE_GRAPH")) {
+    if (h->graph_exec_ref && h->graph_max_iter != max_iter) {
+      cudaGraphExecDestroy(h->graph_exec_ref);
+      h->graph_exec_ref = nullptr;
+    }
+    const bool one_rank = h->dist_world == 1;
+    if (!h->graph_exec && one_rank && !std::getenv("CUTBDDC_NO_WHILE_GRAPH")) {
       h->graph_max_iter = max_iter;
       build_while_graph(h);
     }
     if (!h->graph_exec) {
       h->graph_max_iter = max_iter;
       h->graph_while = false;
-      cudaGraph_t g;
-      const long long c0 = g_kernel_launches.load();
-      CB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      enqueue_iteration(h);
-      CB_CUDA(cudaStreamEndCapture(s, &g));
-      CB_CUDA(cudaGraphInstantiate(&h->graph_exec, g, 0));
-      size_t nodes = 0;
-      CB_CUDA(cudaGraphGetNodes(g, nullptr, &nodes));
-      h->graph_nodes = (long long)nodes;
-      g_kernel_launches.store(c0);  // captured, not executed
-      CB_CUDA(cudaGraphDestroy(g));
+      // one rank: the refresh kernels check the device flag; several ranks:
+      // a second graph carries the refresh (and its exchange)
+      h->graph_exec = capture_iteration(h, one_rank, &h->graph_nodes);
+      if (!one_rank) h->graph_exec_ref = capture_iteration(h, true, &h->graph_nodes_ref);
     }
     int is_host[I_COUNT] = {0};
     int launched = 0, batch = 4;
@@ -406,8 +468,9 @@ void pcg_device(cutbddc_gpu* h, const double* b_dev, double rtol, int max_iter, 
     }
     while (!h->graph_while) {
       for (int q = 0; q < batch && launched < max_iter; ++q, ++launched) {
-        CB_CUDA(cudaGraphLaunch(h->graph_exec, s));
-        g_kernel_launches.fetch_add(h->graph_nodes);
+        const bool ref = !one_rank && (launched + 1) % 50 == 0;  // iteration k = launched + 1
+        CB_CUDA(cudaGraphLaunch(ref ? h->graph_exec_ref : h->graph_exec, s));
+        g_kernel_launches.fetch_add(ref ? h->graph_nodes_ref : h->graph_nodes);
       }
       CB_CUDA(cudaMemcpyAsync(is_host, h->iscal.p, sizeof(is_host), cudaMemcpyDeviceToHost, s));
       CB_CUDA(cudaStreamSynchronize(s));

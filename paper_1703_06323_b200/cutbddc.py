@@ -63,6 +63,14 @@ class _Objects(C.Structure):
                 ("neigh_ptr", C.POINTER(C.c_int64)), ("neigh", C.POINTER(C.c_int32))]
 
 
+class _Plan(C.Structure):
+    _fields_ = [("n_loc", C.c_int64), ("n_own", C.c_int64), ("n_sd_local", C.c_int), ("n_nbr", C.c_int),
+                ("loc_glob", C.POINTER(C.c_int32)), ("seg_ptr", C.POINTER(C.c_int32)),
+                ("copy_ptr", C.POINTER(C.c_int32)), ("copy_src", C.POINTER(C.c_int32)), ("nbr", C.POINTER(C.c_int32)),
+                ("send_ptr", C.POINTER(C.c_int64)), ("send_src", C.POINTER(C.c_int32)),
+                ("recv_ptr", C.POINTER(C.c_int64))]
+
+
 class _Report(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("cond_estimate", C.c_double),
                 ("lambda_min", C.c_double), ("lambda_max", C.c_double), ("residuals", C.POINTER(C.c_double)),
@@ -75,8 +83,8 @@ EXPORTS = [
     "cutbddc_gpu_apply_bddc", "cutbddc_gpu_rhs", "cutbddc_gpu_coarse_matrix", "cutbddc_gpu_cells", "cutbddc_gpu_stats",
     "cutbddc_gpu_cut_elements", "cutbddc_gpu_local_system", "cutbddc_gpu_local_solve", "cutbddc_gpu_time_solves",
     "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free", "cutbddc_gpu_classify_objects",
-    "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_global_ids", "cutbddc_gpu_time_factor",
-    "cutbddc_fp64_peak",
+    "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_distribution", "cutbddc_gpu_time_factor",
+    "cutbddc_fp64_peak", "cutbddc_build_exchange_plan", "cutbddc_gpu_exchange_plan", "cutbddc_exchange_plan_free",
 ]
 
 
@@ -89,6 +97,7 @@ def lib():
         _lib.cutbddc_last_error.restype = C.c_char_p
         _lib.cutbddc_gpu_destroy.restype = None
         _lib.cutbddc_objects_free.restype = None
+        _lib.cutbddc_exchange_plan_free.restype = None
     return _lib
 
 
@@ -204,6 +213,46 @@ def fp64_peak(device: int = 0) -> dict:
     return dict(dmma_tflops=a.value, dfma_tflops=b.value)
 
 
+@dataclass
+class ExchangePlan:
+    """Interface exchange plan of one rank (include/cutbddc.h cutbddc_exchange_plan)."""
+    n_loc: int
+    n_own: int
+    loc_glob: np.ndarray      # global dof of every local dof (segments, then ghosts)
+    seg_ptr: np.ndarray       # n_sd_local + 1
+    copy_ptr: np.ndarray      # n_loc + 1
+    copy_src: np.ndarray      # >= 0 local slot, < 0: -1 - receive index
+    nbr: np.ndarray           # neighbour ranks
+    send_ptr: np.ndarray      # n_nbr + 1
+    send_src: np.ndarray      # local slots of the sent values
+    recv_ptr: np.ndarray      # n_nbr + 1
+
+
+def _take_plan(out) -> ExchangePlan:
+    p = out.contents
+    nl, ns, nn = p.n_loc, p.n_sd_local, p.n_nbr
+    a32 = lambda ptr, n: np.ctypeslib.as_array(ptr, shape=(max(n, 1),))[:n].copy()  # noqa: E731
+    ncopy = int(p.copy_ptr[nl]) if nl else 0
+    r = ExchangePlan(nl, p.n_own, a32(p.loc_glob, nl), a32(p.seg_ptr, ns + 1), a32(p.copy_ptr, nl + 1),
+                     a32(p.copy_src, ncopy), a32(p.nbr, nn), a32(p.send_ptr, nn + 1),
+                     np.zeros(0, np.int32), a32(p.recv_ptr, nn + 1))
+    r.send_src = a32(p.send_src, int(r.send_ptr[-1]))
+    lib().cutbddc_exchange_plan_free(out)
+    return r
+
+
+def exchange_plan(mesh: Mesh, block: int, block_ids: np.ndarray, rank_of_sd: np.ndarray, rank: int,
+                  world: int) -> ExchangePlan:
+    """Host-built exchange plan of `rank` (the same arrays as the device plan)."""
+    block_ids = np.ascontiguousarray(block_ids, np.int64)
+    ros = np.ascontiguousarray(rank_of_sd, np.int32)
+    pv = _PartView(block, len(block_ids), _p(block_ids, C.c_int64))
+    mv = mesh.view()
+    out = C.POINTER(_Plan)()
+    _check(lib().cutbddc_build_exchange_plan(C.byref(mv), C.byref(pv), _p(ros, C.c_int32), rank, world, C.byref(out)))
+    return _take_plan(out)
+
+
 def nccl_unique_id() -> bytes:
     """Rank 0 creates the 128-byte NCCL id; the caller broadcasts it."""
     buf = C.create_string_buffer(128)
@@ -214,9 +263,11 @@ def nccl_unique_id() -> bytes:
 class GpuSolver:
     """One device handle: geometry -> classify -> assemble -> setup -> pcg.
 
-    Multi-GPU: one handle per rank, created with the rank-0 NCCL id; each
-    rank assembles its own subdomains (assemble with the local block ids, then
-    set_global_ids) and every call is collective over the ranks."""
+    Multi-GPU: one handle per rank, created with the rank-0 NCCL id; every
+    rank sets the same distribution (global partition + rank of each
+    subdomain) and then assembles, sets up and solves its own subdomains;
+    every call is collective over the ranks. Vectors are global-numbered
+    (each rank writes the dofs it owns)."""
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
@@ -227,9 +278,23 @@ class GpuSolver:
         self.n_dof = 0
         self.rank, self.world = rank, world
 
-    def set_global_ids(self, n_sd_global: int, global_of_local: np.ndarray):
-        g = np.ascontiguousarray(global_of_local, np.int32)
-        _check(lib().cutbddc_gpu_set_global_ids(self.h, n_sd_global, _p(g, C.c_int32)))
+    def set_distribution(self, block: int, block_ids: np.ndarray, rank_of_sd: np.ndarray, rank: int | None = None,
+                         world: int | None = None):
+        """Global partition and the rank of each subdomain (every rank passes
+        the same). rank/world default to the handle's; a handle without a
+        communicator may take any rank's view (plan inspection only)."""
+        self._bids = np.ascontiguousarray(block_ids, np.int64)
+        self._ros = np.ascontiguousarray(rank_of_sd, np.int32)
+        pv = _PartView(block, len(self._bids), _p(self._bids, C.c_int64))
+        _check(lib().cutbddc_gpu_set_distribution(self.h, C.byref(pv), _p(self._ros, C.c_int32),
+                                                  self.rank if rank is None else rank,
+                                                  self.world if world is None else world))
+
+    def exchange_plan(self) -> ExchangePlan:
+        """The device-built exchange plan of this handle's rank."""
+        out = C.POINTER(_Plan)()
+        _check(lib().cutbddc_gpu_exchange_plan(self.h, C.byref(out)))
+        return _take_plan(out)
 
     def close(self):
         if getattr(self, "h", None):
@@ -261,7 +326,8 @@ class GpuSolver:
         self.n_dof = nd.value
         return Mesh(n, origin, h, phi, cls, dof, nd.value)
 
-    # assemble_subassembled + assemble_global on the device
+    # assemble_subassembled on the device (block_ids: the GLOBAL partition;
+    # a distributed handle assembles its own subdomains)
     def assemble(self, block: int, block_ids: np.ndarray, mesh: Mesh | None = None) -> np.ndarray:
         pv = _PartView(block, len(block_ids), _p(block_ids, C.c_int64))
         mv = mesh.view() if mesh is not None else None
@@ -424,16 +490,16 @@ def local_part(block: int, block_ids: np.ndarray, cells: int, rank: int, world: 
 
 
 def prepare_distributed(solver: GpuSolver, cfg) -> tuple[Problem, LocalPart]:
-    """prepare() for one rank of a multi-GPU solve: the mesh, partition and
-    objects are built identically on every rank (host work, replicated);
-    the device work is split by subdomain."""
+    """prepare() for one rank of a multi-GPU solve: the mesh, partition,
+    assignment and objects are built identically on every rank (host work,
+    replicated); the device work is split by subdomain."""
     if cfg.variant == _cfg.V2:
         raise CutbddcError(CONFIG, "variant v2 needs every subdomain's diagonals; not supported distributed")
     mesh = solver.classify(cfg)
     block_ids = build_partition(mesh, cfg.block)
     lp = local_part(cfg.block, block_ids, cfg.cells, solver.rank, solver.world)
-    dirichlet = solver.assemble(cfg.block, lp.local_block_ids)
-    solver.set_global_ids(len(block_ids), lp.local_sd)
+    solver.set_distribution(cfg.block, block_ids, lp.rank_of_sd)
+    dirichlet = solver.assemble(cfg.block, block_ids)
     objs = classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, None)
     return Problem(cfg, mesh, block_ids, dirichlet, objs), lp
 
