@@ -176,6 +176,13 @@ cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
  * their algorithmic bytes (panel lower parts + front vectors). */
 cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds, double* bytes);
 
+/* Measurement hook: warm average device time (microseconds, `reps`
+ * back-to-back calls) of the pieces of one PCG iteration: us[0] the
+ * matrix-free operator on every row, [1] on interface rows, [2] on
+ * interior rows, [3] one interface sum, [4] one BDDC apply, [5] its three
+ * triangular solves, [6] one SpMV (operator + interface sum), [7] unused. */
+cutbddc_status cutbddc_gpu_time_parts(cutbddc_gpu* h, int reps, double* us);
+
 /* Measurement hook: device time of the numeric factorisation launch(es)
  * (k_dense_dag) of the last setup, its partial-Cholesky flops
  * (sum over fronts of c^3/3 + (r-c)c^2 + (r-c)^2 c; the reference op is

@@ -250,6 +250,7 @@ void assemble_device(cutbddc_gpu* h, const cutbddc_partition_view* part) {
   // element matrices of this rank's cut cells
   ps.next("assembly 2 cut elements");
   cut_elements_device(h);
+  pack_cut_matrices(h);
   DevBuf<double>& kint = h->ws_kint;
   kint.alloc(72);
   interior_element_device(h, kint.p, kint.p + 64);
@@ -285,8 +286,9 @@ void assemble_device(cutbddc_gpu* h, const cutbddc_partition_view* part) {
   h->mask_int.alloc((size_t)ns);
   k_masks<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_dof.p, h->ncount.p, h->mask_all.p, h->mask_int.p);
   CB_LAUNCH();
-  // local dof space, copy and exchange lists
+  // local dof space, copy and exchange lists; the operator's rows
   build_plan_device(h);
+  build_operator_rows(h);
   // load vector: interface sum of the sub-assembled ones
   h->b.alloc((size_t)std::max<int64_t>(1, h->n_loc));
   h->plan_only = plan_only;

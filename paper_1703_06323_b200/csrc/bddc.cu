@@ -181,16 +181,6 @@ __global__ void k_gather_masked(int64_t ns, const int32_t* __restrict__ slot_loc
   X[g] = mask[g] ? r[slot_loc[g]] : 0.0;
 }
 
-// z0 = the interior solution at interior dofs (one copy), 0 elsewhere
-__global__ void k_z0(int64_t nloc, const int32_t* __restrict__ owner, const double* __restrict__ X,
-                     double* __restrict__ z0, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nloc) return;
-  const int32_t o = owner[i];
-  z0[i] = o >= 0 ? X[o] : 0.0;
-}
-
 // X[slot] = w * r1[dof] with r1 = r - Abar z0 on interface rows and 0 on
 // interior rows; (Abar z0)[dof] = Σ over the copies,
 // ascending global sd, of (A_w z0_w)[slot] (Y, remote copies from recv)
@@ -355,11 +345,12 @@ __global__ void k_xty(int n, const double* __restrict__ X, const double* __restr
   if (lane == 0) z[j] = s;
 }
 
-// z = z0 + v - X[owner] over the local dofs (interior dofs: minus the
-// harmonic correction), a block per segment (dist.cuh); with r, every local
+// z = z0 + v - X[owner] over the local dofs (z0 = Z0[owner], the first
+// interior solve; interior dofs: minus the harmonic correction X), a block
+// per segment (dist.cuh); with r, every local
 // subdomain's partial of r.z for the PCG (bit-reproducible for any world size)
 __global__ void __launch_bounds__(kSegThreads) k_final_z(SegArgs a, const int32_t* __restrict__ owner,
-                                                         const double* __restrict__ z0, const double* __restrict__ v,
+                                                         const double* __restrict__ Z0, const double* __restrict__ v,
                                                          const double* __restrict__ X, double* __restrict__ z,
                                                          const double* __restrict__ r, const int* __restrict__ skip) {
   if (skip && *skip) return;
@@ -369,7 +360,7 @@ __global__ void __launch_bounds__(kSegThreads) k_final_z(SegArgs a, const int32_
   double acc = 0.0;
   for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
     const int32_t o = owner[i];
-    const double zi = z0[i] + v[i] - (o >= 0 ? X[o] : 0.0);
+    const double zi = (o >= 0 ? Z0[o] : 0.0) + v[i] - (o >= 0 ? X[o] : 0.0);
     z[i] = zi;
     if (r) acc += r[i] * zi;
   }
@@ -521,30 +512,37 @@ __global__ void k_pivot_check(int nsn, int T, const FrontDesc* __restrict__ desc
   }
 }
 
-// cy[row] = (H^T y')[row]: warp per constraint row, y' the forward sweep's
-// column values in slot space
-__global__ void k_h_cy(int64_t mtot, const int32_t* __restrict__ row_sd, const int64_t* __restrict__ m_off,
-                       const int64_t* __restrict__ rinfo, const double* __restrict__ H, const int32_t* __restrict__ hslot,
-                       const double* __restrict__ Y, double* __restrict__ cy, const int* __restrict__ skip) {
+// cy[row] = (H^T y')[row]: blocks (subdomain, row group); the subdomain's
+// y' values are gathered into shared memory once (not once per row), then a
+// warp per constraint row streams its H column (coalesced)
+constexpr int kHcySplit = 4;
+__global__ void __launch_bounds__(256) k_h_cy(const int64_t* __restrict__ m_off, const int64_t* __restrict__ rinfo,
+                                              const double* __restrict__ H, const int32_t* __restrict__ hslot,
+                                              const double* __restrict__ Y, double* __restrict__ cy,
+                                              const int* __restrict__ skip) {
   if (skip && *skip) return;
-  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= mtot) return;
-  const int sd = row_sd[row];
-  const int a = (int)(row - m_off[sd]), np = (int)rinfo[4 * sd];
-  const double* hc = H + rinfo[4 * sd + 3] + (int64_t)a * np;
+  extern __shared__ double ys[];
+  const int sd = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t b0 = m_off[sd];
+  const int m = (int)(m_off[sd + 1] - b0), np = (int)rinfo[4 * sd];
+  if (m == 0) return;
   const int32_t* hs = hslot + rinfo[4 * sd + 1];
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four independent load chains per lane
-  int k = lane;
-  for (; k + 96 < np; k += 128) {
-    s0 += hc[k] * Y[hs[k]];
-    s1 += hc[k + 32] * Y[hs[k + 32]];
-    s2 += hc[k + 64] * Y[hs[k + 64]];
-    s3 += hc[k + 96] * Y[hs[k + 96]];
+  for (int k = threadIdx.x; k < np; k += blockDim.x) ys[k] = Y[hs[k]];
+  __syncthreads();
+  for (int a = blockIdx.y + gridDim.y * wid; a < m; a += gridDim.y * (blockDim.x >> 5)) {
+    const double* hc = H + rinfo[4 * sd + 3] + (int64_t)a * np;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four independent load chains per lane
+    int k = lane;
+    for (; k + 96 < np; k += 128) {
+      s0 += hc[k] * ys[k];
+      s1 += hc[k + 32] * ys[k + 32];
+      s2 += hc[k + 64] * ys[k + 64];
+      s3 += hc[k + 96] * ys[k + 96];
+    }
+    for (; k < np; k += 32) s0 += hc[k] * ys[k];
+    const double v = warp_sum((s0 + s1) + (s2 + s3));
+    if (lane == 0) cy[b0 + a] = v;
   }
-  for (; k < np; k += 32) s0 += hc[k] * Y[hs[k]];
-  const double s = warp_sum((s0 + s1) + (s2 + s3));
-  if (lane == 0) cy[row] = s;
 }
 
 // y'[slot_k] += (H u)[k]: blocks (subdomain, 256 compact positions)
@@ -1175,6 +1173,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   ps_host.next("setup 5 work vectors");
   h->sv0.alloc((size_t)ns);
   h->sv1.alloc((size_t)ns);
+  h->sx.alloc((size_t)ns);  // operator input (allocated here: never inside a graph capture)
   h->upd.alloc((size_t)upd_total);
   h->ysave.alloc((size_t)ns);
   h->gv0.alloc((size_t)std::max<int64_t>(1, h->n_loc));
@@ -1200,10 +1199,8 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
   k_gather_masked<<<grid_for(ns, 256), 256, 0, s>>>(ns, h->slot_loc.p, h->mask_int.p, r, h->sv0.p, skip);
   CB_LAUNCH();
   ps.close();
-  solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, skip);
-  ps.next("apply vec 2 z0 r1 scatter");
-  k_z0<<<grid_for(nl, 256), 256, 0, s>>>(nl, h->lowner.p, h->sv0.p, h->gv0.p, skip);
-  CB_LAUNCH();
+  solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, skip);  // sv0 keeps z0 (interior slots)
+  ps.next("apply vec 2 r1 scatter");
   // (Abar z0) on interface rows = Σ_w A_w,GI z0_w (z0 vanishes on the interface)
   sub_apply(h, kSubInterface, nullptr, h->sv0.p, h->sv2.p, skip);
   iface_exchange(h, h->sv2.p, nullptr, skip);
@@ -1228,8 +1225,13 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     double* gl_loc = h->gl.p + (int64_t)h->dist_rank * h->maxrows;  // this rank's rows of the staged gl
     if (h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
       if (corner) {  // cy = H^T y' (a warp per constraint row), gl = S^{-1} cy
-        k_h_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->root_info.p,
-                                                               h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
+        if (sizeof(double) * h->np_max > 48 * 1024)
+          device_memo(kMemoHcyShm, [] {
+            CB_CUDA(cudaFuncSetAttribute(k_h_cy, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            return 1ll;
+          });
+        k_h_cy<<<dim3(h->nsd, kHcySplit), 256, sizeof(double) * std::max(1, h->np_max), s>>>(
+            h->m_off.p, h->root_info.p, h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
         CB_LAUNCH();
         k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p,
                                                                h->sinv.p, h->coarse_id.p, h->zc.p, h->cy.p, gl_loc, 0,
@@ -1253,8 +1255,13 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
       CB_LAUNCH();
     } else {
       if (corner) {
-        k_h_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->root_info.p,
-                                                               h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
+        if (sizeof(double) * h->np_max > 48 * 1024)
+          device_memo(kMemoHcyShm, [] {
+            CB_CUDA(cudaFuncSetAttribute(k_h_cy, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            return 1ll;
+          });
+        k_h_cy<<<dim3(h->nsd, kHcySplit), 256, sizeof(double) * std::max(1, h->np_max), s>>>(
+            h->m_off.p, h->root_info.p, h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
       } else {
         k_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p,
                                                            h->c_val.p, h->sv1.p, h->cy.p, skip);
@@ -1298,15 +1305,18 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, skip);
     ps.next("apply vec 3b gather Av");
   }
-  // v = Σ_copies w z~, every rank forms the same sum
+  // v = Σ_copies w z~, every rank forms the same sum, also
+  // scattered to the slots (sx) for the operator
   iface_exchange(h, h->sv1.p, h->w.p, skip);
-  iface_sum(h, h->sv1.p, h->w.p, h->gv2.p, skip);
-  // harmonic correction: the interior rows of Abar v, one subdomain at a time
-  sub_apply(h, kSubInterior, h->gv2.p, nullptr, h->sv0.p, skip);
+  h->sx.alloc((size_t)ns);
+  iface_sum(h, h->sv1.p, h->w.p, h->gv2.p, skip, h->sx.p);
+  // harmonic correction: the interior rows of Abar v, one subdomain at a
+  // time, and their interior solve (sv2; sv0 still holds z0)
+  sub_apply(h, kSubInterior, nullptr, h->sx.p, h->sv2.p, skip);
   ps.close();
-  solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, skip);
+  solve_device(h, h->tI, h->fI, h->sv2.p, h->upd.p, h->ysave.p, skip);
   ps.next("apply vec 4 final");
-  k_final_z<<<seg_grid(h), kSegThreads, 0, s>>>(seg_args(h, rz_part), h->lowner.p, h->gv0.p, h->gv2.p, h->sv0.p, z,
+  k_final_z<<<seg_grid(h), kSegThreads, 0, s>>>(seg_args(h, rz_part), h->lowner.p, h->sv0.p, h->gv2.p, h->sv2.p, z,
                                                 rz_part ? r : nullptr, skip);
   CB_LAUNCH();
 }

@@ -450,6 +450,40 @@ cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds
   });
 }
 
+cutbddc_status cutbddc_gpu_time_parts(cutbddc_gpu* h, int reps, double* us) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bddc_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "setup_bddc first");
+    need_numeric(h);
+    if (reps < 1) reps = 1;
+    cudaStream_t s = h->stream;
+    const int64_t nl = std::max<int64_t>(1, h->n_loc);
+    DevBuf<double> x, y;
+    x.alloc((size_t)nl);
+    y.alloc((size_t)nl);
+    CB_CUDA(cudaMemcpyAsync(x.p, h->b.p, sizeof(double) * nl, cudaMemcpyDeviceToDevice, s));
+    auto timed = [&](auto fn) {
+      fn();  // warm
+      Timer tm(s);
+      for (int r = 0; r < reps; ++r) fn();
+      return 1e6 * tm.stop() / reps;
+    };
+    us[0] = timed([&] { sub_apply(h, kSubAll, x.p, nullptr, h->sv2.p, nullptr); });
+    us[1] = timed([&] { sub_apply(h, kSubInterface, nullptr, h->sv0.p, h->sv2.p, nullptr); });
+    us[2] = timed([&] { sub_apply(h, kSubInterior, x.p, nullptr, h->sv2.p, nullptr); });
+    us[3] = timed([&] { iface_sum(h, h->sv2.p, nullptr, y.p, nullptr); });
+    us[4] = timed([&] { apply_bddc_device(h, x.p, y.p, nullptr); });
+    us[5] = timed([&] {
+      solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
+      if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, nullptr);
+      solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
+    });
+    us[6] = timed([&] { spmv_device(h, x.p, y.p); });
+    us[7] = 0.0;
+  });
+}
+
 cutbddc_status cutbddc_gpu_time_factor(cutbddc_gpu* h, double* seconds, double* flops_cholesky, double* flops_inverse) {
   return guard([&] {
     need(h);

@@ -78,7 +78,7 @@ struct DevBuf {
 // value computed (or an attribute set) on one device must not be reused on
 // another. `fn` runs once per (slot, device) under a mutex; later calls on the
 // same device read the stored value. Slots name the call sites.
-enum DeviceMemoSlot { kMemoSweepFwd = 0, kMemoSweepBwd, kMemoSweepAttr, kMemoDagGrid, kMemoCoarseOutShm, kMemoSweepMulti, kMemoCoarseInShm, kMemoSlots };
+enum DeviceMemoSlot { kMemoSweepFwd = 0, kMemoSweepBwd, kMemoSweepAttr, kMemoDagGrid, kMemoCoarseOutShm, kMemoSweepMulti, kMemoCoarseInShm, kMemoHcyShm, kMemoSlots };
 template <typename Fn>
 long long device_memo(int slot, Fn fn) {
   constexpr int kMaxDev = 64;

@@ -207,18 +207,26 @@ __global__ void k_pack(int64_t n, const int32_t* __restrict__ src, const double*
   buf[k] = w ? w[s] * Y[s] : Y[s];
 }
 
+// out[i] = Σ copies (ascending global sd); with Xs, the sum is also written
+// to every local slot copy (the slot vector the operator reads next)
 __global__ void k_isum(int64_t nloc, const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
                        const double* __restrict__ w, const double* __restrict__ Y, const double* __restrict__ recv,
-                       double* __restrict__ out, const int* __restrict__ skip) {
+                       double* __restrict__ out, double* __restrict__ Xs, const int* __restrict__ skip) {
   if (skip && *skip) return;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nloc) return;
   double s = 0.0;
-  for (int32_t p = cptr[i]; p < cptr[i + 1]; ++p) {
+  const int32_t p0 = cptr[i], p1 = cptr[i + 1];
+  for (int32_t p = p0; p < p1; ++p) {
     const int32_t c = csrc[p];
     s += c >= 0 ? (w ? w[c] * Y[c] : Y[c]) : recv[-1 - c];
   }
   out[i] = s;
+  if (Xs)
+    for (int32_t p = p0; p < p1; ++p) {
+      const int32_t c = csrc[p];
+      if (c >= 0) Xs[c] = s;
+    }
 }
 
 __global__ void k_to_local(int64_t nloc, const int32_t* __restrict__ loc_glob, const double* __restrict__ xg,
@@ -235,76 +243,185 @@ __global__ void k_to_global(int64_t nown, const int32_t* __restrict__ loc_glob, 
 
 // ---------------------------------------------------------------- matrix-free operator
 struct SubArgs {
-  int n, B, b1, T, nb;
+  int n, B, b1, T, nb, nsd;
   const int64_t* block_ids;   // local subdomain -> block id
   const int32_t* eoc;         // per cell: -2 exterior, -1 interior, >= 0 local cut index
-  const double* ke;           // 8x8 row-major per local cut cell
-  const uint8_t* empty;
+  const double* keS;          // cut-cell matrices, packed upper triangle, SoA: keS[36][ncut] (empty cells: 0)
+  int64_t ncut;
   const double* kint;         // constant interior element matrix
   const int32_t* slot_loc;
   const uint8_t* mask_int;
   const double* odiag;        // per slot: 1/|neigh| at strong-Dirichlet slots, else 0
 };
 
-// one CTA per subdomain: the subdomain's input values and cell codes in
-// shared memory, a thread per slot sums its <= 8 cells' element rows
-template <int MODE>
-__global__ void __launch_bounds__(512) k_sub_apply(SubArgs a, const double* __restrict__ xloc,
-                                                   const double* __restrict__ Xslot, double* __restrict__ Y,
-                                                   const int* __restrict__ skip) {
+// cut-cell matrices (8x8 row-major per cell, symmetric) -> packed upper
+// triangle SoA keS[36][ncut]
+__global__ void k_pack_ke(int64_t ncut, const double* __restrict__ ke, double* __restrict__ keS) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= ncut) return;
+  int p = 0;
+  for (int i = 0; i < 8; ++i)
+    for (int j = i; j < 8; ++j) keS[(int64_t)(p++) * ncut + e] = ke[e * 64 + i * 8 + j];
+}
+
+__global__ void k_iota(int64_t n, int32_t* __restrict__ a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (int32_t)i;
+}
+
+// end of the kind 0 / 1 / 2 ranges in a sorted kind array (binary search)
+__global__ void k_kind_counts(int64_t n, const uint8_t* __restrict__ kind, int64_t* __restrict__ out) {
+  const int k = threadIdx.x;
+  if (k >= 3) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (kind[mid] <= k) lo = mid + 1;
+    else hi = mid;
+  }
+  out[k] = lo;
+}
+
+// slot vector of a local dof vector (0 at absent slots)
+__global__ void k_gather_slots(int64_t ns, const int32_t* __restrict__ slot_loc, const double* __restrict__ x,
+                               double* __restrict__ X, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  extern __shared__ double xs[];
-  int32_t* cc = reinterpret_cast<int32_t*>(xs + a.T);
-  __shared__ double ks[64];
-  const int sd = blockIdx.x, T = a.T, B = a.B, b1 = a.b1, n = a.n;
-  const int64_t base = (int64_t)sd * T;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  const int32_t l = slot_loc[g];
+  X[g] = l >= 0 ? x[l] : 0.0;
+}
+
+// Rows of the operator as one list of slots, [interior regular | interior
+// irregular | interface] (ascending slots within each): a regular slot has
+// all 8 cells inside its block and interior (the bulk), so its row is the
+// constant 27-point stencil S27 of the Q1 element; every other row sums its
+// cells' element rows. kSubInterior = [0, n_int), kSubInterface =
+// [n_int, n_rows), kSubAll = [0, n_rows).
+__global__ void k_slot_kind(int64_t ns, int T, int B, int b1, int n, int nb, const int64_t* __restrict__ block_ids,
+                            const int32_t* __restrict__ eoc, const int32_t* __restrict__ slot_loc,
+                            const uint8_t* __restrict__ mask_int, const double* __restrict__ odiag,
+                            uint8_t* __restrict__ kind) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ns) return;
+  if (slot_loc[g] < 0) {
+    kind[g] = 3;
+    return;
+  }
+  if (!mask_int[g]) {
+    kind[g] = 2;
+    return;
+  }
+  const int sd = (int)(g / T), t = (int)(g - (int64_t)sd * T);
+  const int P = b1 * b1, lx = t / P, ly = (t / b1) % b1, lz = t % b1;
+  const int64_t bid = block_ids[sd];
+  const int bi = (int)(bid / nb / nb), bj = (int)((bid / nb) % nb), bk = (int)(bid % nb);
+  bool reg = odiag[g] == 0.0 && lx > 0 && ly > 0 && lz > 0 && lx < B && ly < B && lz < B;
+  for (int c = 0; c < 8 && reg; ++c) {
+    const int cx = lx - 1 + (c >> 2), cy = ly - 1 + ((c >> 1) & 1), cz = lz - 1 + (c & 1);
+    reg = eoc[((int64_t)(bi * B + cx) * n + bj * B + cy) * n + bk * B + cz] == -1;
+  }
+  kind[g] = reg ? 0 : 1;
+}
+
+// S27[q]: the interior element rows summed onto the 27-point stencil (cells
+// in (dx,dy,dz) order, nodes in bit order: a fixed order)
+__global__ void k_stencil27(const double* __restrict__ kint, double* __restrict__ s27) {
+  if (threadIdx.x != 0) return;
+  for (int q = 0; q < 27; ++q) s27[q] = 0.0;
+  for (int c = 0; c < 8; ++c) {
+    const int dx = c >> 2, dy = (c >> 1) & 1, dz = c & 1;
+    const int lv = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+    for (int w = 0; w < 8; ++w) s27[(dx + (w & 1)) * 9 + (dy + ((w >> 1) & 1)) * 3 + (dz + ((w >> 2) & 1))] += kint[lv * 8 + w];
+  }
+}
+
+// partial of cell c (0..7, (dx,dy,dz) order) of the row at slot g: the
+// cell's element row times its 8 node values (constant Q1 matrix for
+// interior cells, the packed matrix of cut cells, 0 for exterior cells)
+__device__ __forceinline__ double cell_part(const SubArgs& a, const double* __restrict__ ks, int64_t g, int c,
+                                            const double* __restrict__ X) {
+  const int T = a.T, B = a.B, b1 = a.b1, n = a.n, P = b1 * b1;
+  const int sd = (int)(g / T), t = (int)(g - (int64_t)sd * T);
+  const int lx = t / P, ly = (t / b1) % b1, lz = t % b1;
+  const int dx = c >> 2, dy = (c >> 1) & 1, dz = c & 1;
+  const int cx = lx - 1 + dx, cy = ly - 1 + dy, cz = lz - 1 + dz;
+  double v = 0.0;
+  if (cx < 0 || cy < 0 || cz < 0 || cx >= B || cy >= B || cz >= B) return v;
   const int64_t bid = a.block_ids[sd];
   const int bi = (int)(bid / a.nb / a.nb), bj = (int)((bid / a.nb) % a.nb), bk = (int)(bid % a.nb);
-  for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    double v;
-    if (Xslot) {
-      v = Xslot[base + t];
-    } else {
-      const int32_t l = a.slot_loc[base + t];
-      v = l >= 0 ? xloc[l] : 0.0;
+  const int32_t e = a.eoc[((int64_t)(bi * B + cx) * n + bj * B + cy) * n + bk * B + cz];
+  const int lv = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+  const int64_t n0 = g + (dx - 1) * P + (dy - 1) * b1 + (dz - 1);  // node 0 of the cell
+  if (e == -1) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += ks[lv * 8 + w] * X[n0 + (w & 1) * P + ((w >> 1) & 1) * b1 + ((w >> 2) & 1)];
+  } else if (e >= 0) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const int i = lv < w ? lv : w, k = lv < w ? w : lv;  // packed upper-triangle index of (lv, w)
+      v += a.keS[(int64_t)(i * 8 - i * (i - 1) / 2 + (k - i)) * a.ncut + e] *
+           X[n0 + (w & 1) * P + ((w >> 1) & 1) * b1 + ((w >> 2) & 1)];
     }
-    xs[t] = v;
   }
-  for (int c = threadIdx.x; c < B * B * B; c += blockDim.x) {
-    const int cx = c / (B * B), cy = (c / B) % B, cz = c % B;
-    int32_t e = a.eoc[((int64_t)(bi * B + cx) * n + bj * B + cy) * n + bk * B + cz];
-    if (e >= 0 && a.empty[e]) e = -2;
-    cc[c] = e;
-  }
+  return v;
+}
+
+// regular rows, a thread each: S27 on the 27 lattice neighbours (all 8
+// cells interior, so every neighbour lies in the lattice)
+__global__ void __launch_bounds__(256) k_sub_regular(const int32_t* __restrict__ rows, int64_t nreg, int P, int b1,
+                                                     const double* __restrict__ s27, const double* __restrict__ X,
+                                                     double* __restrict__ Y, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double ss[27];
+  if (threadIdx.x < 27) ss[threadIdx.x] = s27[threadIdx.x];
+  __syncthreads();
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nreg) return;
+  const int64_t g = rows[j];
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < 27; ++q) acc += ss[q] * X[g + (q / 9 - 1) * P + ((q / 3) % 3 - 1) * b1 + (q % 3 - 1)];
+  Y[g] = acc;
+}
+
+// The other rows: the 8 cell partials combined by one fixed tree,
+// ((p0+p4)+(p2+p6)) + ((p1+p5)+(p3+p7)). k_sub_cells8 runs 8 lanes per row
+// (the xor tree; many-SM parallelism for few rows), k_sub_cells1 a thread
+// per row: the same bits either way, so each rank may pick by its row count.
+__global__ void __launch_bounds__(256) k_sub_cells8(SubArgs a, const int32_t* __restrict__ rows, int64_t lo, int64_t hi,
+                                                    const double* __restrict__ X, double* __restrict__ Y,
+                                                    const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double ks[64];
   if (threadIdx.x < 64) ks[threadIdx.x] = a.kint[threadIdx.x];
   __syncthreads();
-  for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    const int64_t g = base + t;
-    const bool present = a.slot_loc[g] >= 0;
-    const bool interior = a.mask_int[g] != 0;
-    const bool row = MODE == kSubAll ? present : (MODE == kSubInterface ? present && !interior : interior);
-    if (!row) {
-      Y[g] = 0.0;
-      continue;
-    }
-    const int lx = t / (b1 * b1), ly = (t / b1) % b1, lz = t % b1;
-    double acc = 0.0;
-    for (int dx = 0; dx < 2; ++dx)
-      for (int dy = 0; dy < 2; ++dy)
-        for (int dz = 0; dz < 2; ++dz) {
-          const int cx = lx - 1 + dx, cy = ly - 1 + dy, cz = lz - 1 + dz;
-          if (cx < 0 || cy < 0 || cz < 0 || cx >= B || cy >= B || cz >= B) continue;
-          const int32_t e = cc[(cx * B + cy) * B + cz];
-          if (e == -2) continue;
-          const int lv = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
-          const double* K = (e == -1 ? ks : a.ke + (int64_t)e * 64) + lv * 8;
-          const int n0 = (cx * b1 + cy) * b1 + cz;
+  const int64_t j = lo + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 8;
+  const int c = threadIdx.x & 7;
+  const bool live = j < hi;  // whole 8-lane groups are live or not: the shuffles stay convergent
+  const int64_t g = live ? rows[j] : 0;
+  double v = live ? cell_part(a, ks, g, c, X) : 0.0;
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  if (live && c == 0) Y[g] = a.odiag ? v + a.odiag[g] * X[g] : v;
+}
+
+__global__ void __launch_bounds__(256) k_sub_cells1(SubArgs a, const int32_t* __restrict__ rows, int64_t lo, int64_t hi,
+                                                    const double* __restrict__ X, double* __restrict__ Y,
+                                                    const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double ks[64];
+  if (threadIdx.x < 64) ks[threadIdx.x] = a.kint[threadIdx.x];
+  __syncthreads();
+  const int64_t j = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= hi) return;
+  const int64_t g = rows[j];
+  double p[8];
 #pragma unroll
-          for (int w = 0; w < 8; ++w) acc += K[w] * xs[n0 + ((w >> 2) & 1) + ((w >> 1) & 1) * b1 + (w & 1) * b1 * b1];
-        }
-    if (a.odiag) acc += a.odiag[g] * xs[t];
-    Y[g] = acc;
-  }
+  for (int c = 0; c < 8; ++c) p[c] = cell_part(a, ks, g, c, X);
+  const double v = ((p[0] + p[4]) + (p[2] + p[6])) + ((p[1] + p[5]) + (p[3] + p[7]));
+  Y[g] = a.odiag ? v + a.odiag[g] * X[g] : v;
 }
 
 }  // namespace
@@ -527,9 +644,9 @@ void iface_exchange(cutbddc_gpu* h, const double* Y, const double* w, const int*
   nccl_check(ncclGroupEnd(), "group end");
 }
 
-void iface_sum(cutbddc_gpu* h, const double* Y, const double* w, double* out, const int* skip) {
+void iface_sum(cutbddc_gpu* h, const double* Y, const double* w, double* out, const int* skip, double* Xs) {
   k_isum<<<grid_for(std::max<int64_t>(1, h->n_loc), 256), 256, 0, h->stream>>>(h->n_loc, h->lcopy_ptr.p, h->lcopy_src.p,
-                                                                                w, Y, h->recvbuf.p, out, skip);
+                                                                                w, Y, h->recvbuf.p, out, Xs, skip);
   CB_LAUNCH();
 }
 
@@ -569,18 +686,78 @@ int agree_status(cutbddc_gpu* h, int code) {
   return out;
 }
 
+constexpr int64_t kCells8Rows = 65536;  // fewer irregular rows: 8 lanes per row (latency), else a thread per row
+
 void sub_apply(cutbddc_gpu* h, int mode, const double* xloc, const double* Xslot, double* Y, const int* skip) {
-  const size_t shm = sizeof(double) * (size_t)h->slots + sizeof(int32_t) * (size_t)h->block * h->block * h->block;
-  if (shm > 200 * 1024) throw Failure(CUTBDDC_CONFIG, "matrix-free operator: block too large for shared memory");
-  SubArgs a{h->n, h->block, h->b1, h->slots, h->nb, h->block_ids.p, h->elem_of_cell.p, h->ke.p, h->empty.p,
-            h->ws_kint.p, h->slot_loc.p, h->mask_int.p, h->odiag.p};
-  auto launch = [&](auto kern) {
-    if (shm > 48 * 1024) CB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    kern<<<h->nsd, 512, shm, h->stream>>>(a, xloc, Xslot, Y, skip);
-  };
-  if (mode == kSubAll) launch(k_sub_apply<kSubAll>);
-  else if (mode == kSubInterface) launch(k_sub_apply<kSubInterface>);
-  else launch(k_sub_apply<kSubInterior>);
+  cudaStream_t st = h->stream;
+  const int64_t ns = (int64_t)h->nsd * h->slots;
+  if (!Xslot) {
+    h->sx.alloc((size_t)ns);
+    k_gather_slots<<<grid_for(ns, 256), 256, 0, st>>>(ns, h->slot_loc.p, xloc, h->sx.p, skip);
+    CB_LAUNCH();
+    Xslot = h->sx.p;
+  }
+  SubArgs a{h->n,    h->block, h->b1, h->slots, h->nb, h->nsd, h->block_ids.p, h->elem_of_cell.p, h->keS.p,
+            h->n_cut, h->ws_kint.p, h->slot_loc.p, h->mask_int.p, h->odiag.p};
+  const int64_t lo = mode == kSubInterface ? h->rows_nint : 0;
+  const int64_t hi = mode == kSubInterior ? h->rows_nint : h->rows_n;
+  const int64_t lo2 = std::max(lo, h->rows_nreg);  // irregular rows from here
+  if (lo < h->rows_nreg) {
+    k_sub_regular<<<grid_for(h->rows_nreg, 256), 256, 0, st>>>(h->op_rows.p, h->rows_nreg, h->b1 * h->b1, h->b1,
+                                                               h->s27.p, Xslot, Y, skip);
+    CB_LAUNCH();
+  }
+  if (hi > lo2) {
+    if (hi - lo2 < kCells8Rows)
+      k_sub_cells8<<<grid_for((hi - lo2) * 8, 256), 256, 0, st>>>(a, h->op_rows.p, lo2, hi, Xslot, Y, skip);
+    else
+      k_sub_cells1<<<grid_for(hi - lo2, 256), 256, 0, st>>>(a, h->op_rows.p, lo2, hi, Xslot, Y, skip);
+    CB_LAUNCH();
+  }
+}
+
+// the operator's row list (after the masks, odiag and slot_loc exist)
+void build_operator_rows(cutbddc_gpu* h) {
+  cudaStream_t st = h->stream;
+  const int64_t ns = (int64_t)h->nsd * h->slots;
+  DevBuf<uint8_t>& kind = h->ws_local;
+  kind.alloc((size_t)ns);
+  k_slot_kind<<<grid_for(ns, 256), 256, 0, st>>>(ns, h->slots, h->block, h->b1, h->n, h->nb, h->block_ids.p,
+                                                 h->elem_of_cell.p, h->slot_loc.p, h->mask_int.p, h->odiag.p, kind.p);
+  CB_LAUNCH();
+  h->op_rows.alloc((size_t)ns);
+  // stable sort of the slots by kind (radix sort over 2 bits)
+  DevBuf<uint8_t>& kind2 = h->ws_nsds;
+  kind2.alloc((size_t)ns);
+  cub::CountingInputIterator<int32_t> it(0);
+  DevBuf<int32_t>& idx = h->ws_glist;
+  idx.alloc((size_t)ns);
+  k_iota<<<grid_for(ns, 256), 256, 0, st>>>(ns, idx.p);
+  CB_LAUNCH();
+  size_t tb = 0;
+  CB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kind.p, kind2.p, idx.p, h->op_rows.p, (int)ns, 0, 2, st));
+  DevBuf<uint8_t>& tmp = h->ws_tmp;
+  tmp.alloc(std::max(tmp.n, tb));
+  CB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, kind.p, kind2.p, idx.p, h->op_rows.p, (int)ns, 0, 2, st));
+  DevBuf<int64_t>& cnt = h->ws_cnt;
+  cnt.alloc(4);
+  k_kind_counts<<<1, 32, 0, st>>>(ns, kind2.p, cnt.p);
+  CB_LAUNCH();
+  int64_t c[4];
+  CB_CUDA(cudaMemcpyAsync(c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+  h->s27.alloc(27);
+  k_stencil27<<<1, 32, 0, st>>>(h->ws_kint.p, h->s27.p);
+  CB_LAUNCH();
+  CB_CUDA(cudaStreamSynchronize(st));
+  h->rows_nreg = c[0];
+  h->rows_nint = c[1];
+  h->rows_n = c[2];
+}
+
+void pack_cut_matrices(cutbddc_gpu* h) {
+  h->keS.alloc((size_t)36 * std::max<int64_t>(1, h->n_cut));
+  if (h->n_cut == 0) return;
+  k_pack_ke<<<grid_for(h->n_cut, 256), 256, 0, h->stream>>>(h->n_cut, h->ke.p, h->keS.p);
   CB_LAUNCH();
 }
 

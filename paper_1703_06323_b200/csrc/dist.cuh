@@ -35,7 +35,8 @@ void build_plan_device(cutbddc_gpu* h);
 void iface_exchange(cutbddc_gpu* h, const double* Y, const double* w, const int* skip);
 // out[i] = Σ over the copies of local dof i, ascending global subdomain, of
 // (w ? w * Y : Y) (remote copies from h->recvbuf). Call iface_exchange first.
-void iface_sum(cutbddc_gpu* h, const double* Y, const double* w, double* out, const int* skip);
+// Xs (optional): the sums also land in every local slot copy.
+void iface_sum(cutbddc_gpu* h, const double* Y, const double* w, double* out, const int* skip, double* Xs = nullptr);
 // In-place all-gather of the per-subdomain partials (stride h->maxloc).
 void gather_partials(cutbddc_gpu* h, double* part);
 // Coarse staging (bddc.cu): every rank's constraint-row values h->gl
@@ -48,9 +49,14 @@ int agree_status(cutbddc_gpu* h, int code);
 // matrix for interior cells, the stored 8x8 matrix of each cut cell, the
 // 1/|neigh| diagonal of strong-Dirichlet dofs. Rows: every present slot
 // (kSubAll), interface slots only (kSubInterface) or interior slots only
-// (kSubInterior); other slots get 0. The input is the slot vector Xslot, or
+// (kSubInterior); other slots are not written. The input is the slot vector Xslot, or
 // the local dof vector xloc gathered through slot_loc when Xslot is null.
 enum { kSubAll = 0, kSubInterface = 1, kSubInterior = 2 };
+// the operator's copy of the cut-cell matrices: packed upper triangle, SoA
+// (36 doubles per cut cell, coalesced by neighbouring slots)
+void pack_cut_matrices(cutbddc_gpu* h);
+// the operator's row lists (assembly, after the plan)
+void build_operator_rows(cutbddc_gpu* h);
 void sub_apply(cutbddc_gpu* h, int mode, const double* xloc, const double* Xslot, double* Y, const int* skip);
 // Global <-> local vectors at the boundary: gather every local dof; scatter
 // the owned ones (segments, not the ghost segment).

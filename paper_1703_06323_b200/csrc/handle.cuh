@@ -130,6 +130,7 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int64_t> active_cells, cut_cells;
   cutbddc_b200::DevBuf<int32_t> elem_of_cell;
   cutbddc_b200::DevBuf<double> ke, fe, beta;
+  cutbddc_b200::DevBuf<double> keS;              // ke packed (upper triangle) SoA [36][ncut] for the operator
   cutbddc_b200::DevBuf<uint8_t> empty;
 
   // ---------------------------------------------------------------- subdomains
@@ -213,6 +214,10 @@ struct cutbddc_gpu {
 
   // ---------------------------------------------------------------- work vectors
   cutbddc_b200::DevBuf<double> sv0, sv1, sv2;     // slot vectors nsd*T
+  cutbddc_b200::DevBuf<double> sx;                // slot-vector input of the matrix-free operator (dist.cu)
+  cutbddc_b200::DevBuf<int32_t> op_rows;          // operator rows: [interior regular | interior | interface] slots
+  int64_t rows_nreg = 0, rows_nint = 0, rows_n = 0;
+  cutbddc_b200::DevBuf<double> s27;               // constant 27-point stencil of interior cells
   cutbddc_b200::DevBuf<double> ysave;             // big-front forward results, nsd*T
   cutbddc_b200::DevBuf<double> upd;               // solve workspace nsd*upd_total (x nrhs for setup)
   cutbddc_b200::DevBuf<double> gv0, gv2;         // local dof vectors (z0, v)
@@ -239,6 +244,7 @@ struct cutbddc_gpu {
 
   // pcg vectors
   cutbddc_b200::DevBuf<double> px, pr, pz, pp, pq, pb, hist, lal, lbe;
+  cutbddc_b200::DevBuf<double> psl;               // p at every local slot copy (the SpMV's input)
   cudaGraphExec_t graph_exec = nullptr;
   cudaGraphExec_t graph_exec_ref = nullptr;      // several ranks: the iteration with the k % 50 refresh
   long long graph_nodes_ref = 0;

@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(kSegThreads) k_check(Fin f, const double* __re
 __global__ void __launch_bounds__(kSegThreads) k_update_p(int64_t nloc, Fin f, const double* __restrict__ rz_part,
                                                           double* __restrict__ sc, const double* __restrict__ z,
                                                           double* __restrict__ p, double* __restrict__ lbe,
+                                                          const int32_t* __restrict__ cptr,
+                                                          const int32_t* __restrict__ csrc, double* __restrict__ Ps,
                                                           int* __restrict__ is) {
   if (is[I_DONE]) return;
   const int k = is[I_ITER];
@@ -195,7 +197,22 @@ __global__ void __launch_bounds__(kSegThreads) k_update_p(int64_t nloc, Fin f, c
     sc[rz_slot(k + 1)] = rz;
     lbe[k - 1] = beta;
   }
-  for (int64_t i = i0; i < nloc; i += (int64_t)gridDim.x * blockDim.x) p[i] = z[i] + beta * p[i];
+  for (int64_t i = i0; i < nloc; i += (int64_t)gridDim.x * blockDim.x) {
+    const double pi = z[i] + beta * p[i];
+    p[i] = pi;
+    for (int32_t c = cptr[i]; c < cptr[i + 1]; ++c)  // p at its local slot copies (the next SpMV's input)
+      if (csrc[c] >= 0) Ps[csrc[c]] = pi;
+  }
+}
+
+// p = z and its slot copies
+__global__ void k_init_p(int64_t nloc, const double* __restrict__ z, double* __restrict__ p,
+                         const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc, double* __restrict__ Ps) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nloc; i += (int64_t)gridDim.x * blockDim.x) {
+    p[i] = z[i];
+    for (int32_t c = cptr[i]; c < cptr[i + 1]; ++c)
+      if (csrc[c] >= 0) Ps[csrc[c]] = z[i];
+  }
 }
 
 __global__ void k_next(int* __restrict__ is) {
@@ -254,8 +271,8 @@ void enqueue_iteration(cutbddc_gpu* h, bool refresh) {
   int* is = h->iscal.p;
   double* sc = h->scal.p;
   const int sg = seg_grid(h);
-  // q = Abar p
-  sub_apply(h, kSubAll, h->pp.p, nullptr, h->sv2.p, is);
+  // q = Abar p (p's slot copies kept by k_update_p / k_init_p)
+  sub_apply(h, kSubAll, nullptr, h->psl.p, h->sv2.p, is);
   iface_exchange(h, h->sv2.p, nullptr, is);
   k_spmv_dot<<<sg, kSegThreads, 0, s>>>(seg_args(h, part0(h)), h->lcopy_ptr.p, h->lcopy_src.p, h->sv2.p, h->recvbuf.p,
                                         h->pp.p, h->pq.p, is);
@@ -276,7 +293,8 @@ void enqueue_iteration(cutbddc_gpu* h, bool refresh) {
   CB_LAUNCH();
   apply_bddc_device(h, h->pr.p, h->pz.p, is, part0(h));
   gather_partials(h, part0(h));
-  k_update_p<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, fin(h), part0(h), sc, h->pz.p, h->pp.p, h->lbe.p, is);
+  k_update_p<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, fin(h), part0(h), sc, h->pz.p, h->pp.p, h->lbe.p,
+                                                 h->lcopy_ptr.p, h->lcopy_src.p, h->psl.p, is);
   CB_LAUNCH();
   k_next<<<1, 1, 0, s>>>(is);
   CB_LAUNCH();
@@ -397,6 +415,7 @@ void pcg_device(cutbddc_gpu* h, const double* b_loc, double rtol, int max_iter, 
   cudaStream_t s = h->stream;
   const int64_t nl = std::max<int64_t>(1, h->n_loc);
   for (auto* v : {&h->px, &h->pr, &h->pz, &h->pp, &h->pq, &h->pb}) v->alloc((size_t)nl);
+  h->psl.alloc((size_t)h->nsd * h->slots);
   h->hist.alloc((size_t)max_iter + 1);
   h->lal.alloc((size_t)max_iter + 1);
   h->lbe.alloc((size_t)max_iter + 1);
@@ -435,7 +454,7 @@ void pcg_device(cutbddc_gpu* h, const double* b_loc, double rtol, int max_iter, 
     gather_partials(h, part0(h));
     k_init_rz<<<1, kSegThreads, 0, s>>>(fin(h), part0(h), h->scal.p, h->iscal.p);
     CB_LAUNCH();
-    k_copy<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, h->pz.p, h->pp.p);
+    k_init_p<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, h->pz.p, h->pp.p, h->lcopy_ptr.p, h->lcopy_src.p, h->psl.p);
     CB_LAUNCH();
     if (h->graph_exec && h->graph_max_iter != max_iter) {
       cudaGraphExecDestroy(h->graph_exec);

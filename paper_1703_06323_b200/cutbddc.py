@@ -85,6 +85,7 @@ EXPORTS = [
     "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free", "cutbddc_gpu_classify_objects",
     "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_distribution", "cutbddc_gpu_time_factor",
     "cutbddc_fp64_peak", "cutbddc_build_exchange_plan", "cutbddc_gpu_exchange_plan", "cutbddc_exchange_plan_free",
+    "cutbddc_gpu_time_parts",
 ]
 
 
@@ -436,6 +437,13 @@ class GpuSolver:
         _check(lib().cutbddc_gpu_time_solves(self.h, reps, C.byref(sec), C.byref(byt)))
         return dict(kernel="k_sweep_fwd+k_sweep_bwd (3 triangular solves of one BDDC apply)",
                     seconds=sec.value, bytes=byt.value)
+
+    def time_parts(self, reps: int = 20) -> dict:
+        """Warm device time (us) of the pieces of one PCG iteration."""
+        us = np.zeros(8)
+        _check(lib().cutbddc_gpu_time_parts(self.h, reps, _p(us, C.c_double)))
+        keys = ["op_all", "op_interface", "op_interior", "iface_sum", "apply", "apply_solves", "spmv"]
+        return {k: float(v) for k, v in zip(keys, us)}
 
     def factor_timing(self):
         """Device time of the last setup's numeric factorisation launch(es)
