@@ -354,9 +354,8 @@ __global__ void __launch_bounds__(kSegThreads) k_final_z(SegArgs a, const int32_
                                                          const double* __restrict__ X, double* __restrict__ z,
                                                          const double* __restrict__ r, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  __shared__ double sh[32];
   int lo, hi;
-  const bool part = seg_range(a, lo, hi);
+  const int seg = seg_range(a, lo, hi);
   double acc = 0.0;
   for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
     const int32_t o = owner[i];
@@ -364,9 +363,8 @@ __global__ void __launch_bounds__(kSegThreads) k_final_z(SegArgs a, const int32_
     z[i] = zi;
     if (r) acc += r[i] * zi;
   }
-  if (!r || !part) return;
-  acc = block_sum<kSegThreads>(acc, sh);
-  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
+  if (!r || seg < 0) return;
+  seg_commit(a, seg, acc);
 }
 
 // ---------------------------------------------------------------- root-space coarse basis
@@ -512,37 +510,46 @@ __global__ void k_pivot_check(int nsn, int T, const FrontDesc* __restrict__ desc
   }
 }
 
-// cy[row] = (H^T y')[row]: blocks (subdomain, row group); the subdomain's
-// y' values are gathered into shared memory once (not once per row), then a
-// warp per constraint row streams its H column (coalesced)
-constexpr int kHcySplit = 4;
+// cy[row] = (H^T y')[row] in two steps. k_h_cy: blocks (subdomain, 256
+// compact positions k): one gather of y'[k] per thread, then every row's
+// H[a][k] y'[k] (coalesced across k), summed over the block in a fixed tree
+// into a per-chunk partial. k_h_cy_sum: cy = the chunk partials in chunk order.
+constexpr int kHcyMaxM = 128;  // constraint rows per subdomain of this path
 __global__ void __launch_bounds__(256) k_h_cy(const int64_t* __restrict__ m_off, const int64_t* __restrict__ rinfo,
                                               const double* __restrict__ H, const int32_t* __restrict__ hslot,
-                                              const double* __restrict__ Y, double* __restrict__ cy,
+                                              const double* __restrict__ Y, double* __restrict__ hp, int mmax,
                                               const int* __restrict__ skip) {
   if (skip && *skip) return;
-  extern __shared__ double ys[];
-  const int sd = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t b0 = m_off[sd];
-  const int m = (int)(m_off[sd + 1] - b0), np = (int)rinfo[4 * sd];
-  if (m == 0) return;
-  const int32_t* hs = hslot + rinfo[4 * sd + 1];
-  for (int k = threadIdx.x; k < np; k += blockDim.x) ys[k] = Y[hs[k]];
-  __syncthreads();
-  for (int a = blockIdx.y + gridDim.y * wid; a < m; a += gridDim.y * (blockDim.x >> 5)) {
-    const double* hc = H + rinfo[4 * sd + 3] + (int64_t)a * np;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four independent load chains per lane
-    int k = lane;
-    for (; k + 96 < np; k += 128) {
-      s0 += hc[k] * ys[k];
-      s1 += hc[k + 32] * ys[k + 32];
-      s2 += hc[k + 64] * ys[k + 64];
-      s3 += hc[k + 96] * ys[k + 96];
-    }
-    for (; k < np; k += 32) s0 += hc[k] * ys[k];
-    const double v = warp_sum((s0 + s1) + (s2 + s3));
-    if (lane == 0) cy[b0 + a] = v;
+  __shared__ double wsum[8][kHcyMaxM];
+  const int sd = blockIdx.x, ch = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int m = (int)(m_off[sd + 1] - m_off[sd]), np = (int)rinfo[4 * sd];
+  if (m == 0 || ch * 256 >= np) return;
+  const int k = ch * 256 + threadIdx.x;
+  const double y = k < np ? Y[hslot[rinfo[4 * sd + 1] + k]] : 0.0;
+  const double* hc = H + rinfo[4 * sd + 3] + k;
+  for (int a = 0; a < m; ++a) {
+    const double v = warp_sum(k < np ? hc[(int64_t)a * np] * y : 0.0);
+    if (lane == 0) wsum[wid][a] = v;
   }
+  __syncthreads();
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += wsum[w][a];
+    hp[((int64_t)sd * gridDim.y + ch) * mmax + a] = v;
+  }
+}
+
+__global__ void k_h_cy_sum(int64_t mtot, int nch, int mmax, const int32_t* __restrict__ row_sd,
+                           const int64_t* __restrict__ m_off, const int64_t* __restrict__ rinfo,
+                           const double* __restrict__ hp, double* __restrict__ cy, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= mtot) return;
+  const int sd = row_sd[row];
+  const int a = (int)(row - m_off[sd]), used = (int)((rinfo[4 * sd] + 255) / 256);
+  double v = 0.0;
+  for (int c = 0; c < used; ++c) v += hp[((int64_t)sd * nch + c) * mmax + a];
+  cy[row] = v;
 }
 
 // y'[slot_k] += (H u)[k]: blocks (subdomain, 256 compact positions)
@@ -1174,6 +1181,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->sv0.alloc((size_t)ns);
   h->sv1.alloc((size_t)ns);
   h->sx.alloc((size_t)ns);  // operator input (allocated here: never inside a graph capture)
+  h->hcy_part.alloc((size_t)std::max(1, nsd * std::max(1, (h->np_max + 255) / 256) * std::max(1, m_max)));
   h->upd.alloc((size_t)upd_total);
   h->ysave.alloc((size_t)ns);
   h->gv0.alloc((size_t)std::max<int64_t>(1, h->n_loc));
@@ -1187,6 +1195,20 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->gc.alloc((size_t)std::max(1, nc));
   CB_CUDA(cudaStreamSynchronize(s));
   h->bddc_ready = true;
+}
+
+// cy = H^T y' of every local constraint row (corner formulation)
+void h_cy(cutbddc_gpu* h, const double* Yc, const int* skip) {
+  if (h->m_total == 0) return;
+  if (h->m_max > kHcyMaxM) throw Failure(CUTBDDC_CONFIG, "coarse basis: more than 128 constraint rows in a subdomain");
+  const int nch = std::max(1, (h->np_max + 255) / 256);
+  h->hcy_part.alloc((size_t)h->nsd * nch * h->m_max);
+  k_h_cy<<<dim3(h->nsd, nch), 256, 0, h->stream>>>(h->m_off.p, h->root_info.p, h->hroot.p, h->hslot.p, Yc,
+                                                     h->hcy_part.p, h->m_max, skip);
+  CB_LAUNCH();
+  k_h_cy_sum<<<grid_for(h->m_total, 128), 128, 0, h->stream>>>(h->m_total, nch, h->m_max, h->row_sd.p, h->m_off.p,
+                                                              h->root_info.p, h->hcy_part.p, h->cy.p, skip);
+  CB_LAUNCH();
 }
 
 // z = M r (local dof vectors, dist.cuh), enqueued on the handle's stream.
@@ -1225,13 +1247,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     double* gl_loc = h->gl.p + (int64_t)h->dist_rank * h->maxrows;  // this rank's rows of the staged gl
     if (h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
       if (corner) {  // cy = H^T y' (a warp per constraint row), gl = S^{-1} cy
-        if (sizeof(double) * h->np_max > 48 * 1024)
-          device_memo(kMemoHcyShm, [] {
-            CB_CUDA(cudaFuncSetAttribute(k_h_cy, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            return 1ll;
-          });
-        k_h_cy<<<dim3(h->nsd, kHcySplit), 256, sizeof(double) * std::max(1, h->np_max), s>>>(
-            h->m_off.p, h->root_info.p, h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
+        h_cy(h, Yc, skip);
         CB_LAUNCH();
         k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p,
                                                                h->sinv.p, h->coarse_id.p, h->zc.p, h->cy.p, gl_loc, 0,
@@ -1255,13 +1271,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
       CB_LAUNCH();
     } else {
       if (corner) {
-        if (sizeof(double) * h->np_max > 48 * 1024)
-          device_memo(kMemoHcyShm, [] {
-            CB_CUDA(cudaFuncSetAttribute(k_h_cy, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            return 1ll;
-          });
-        k_h_cy<<<dim3(h->nsd, kHcySplit), 256, sizeof(double) * std::max(1, h->np_max), s>>>(
-            h->m_off.p, h->root_info.p, h->hroot.p, h->hslot.p, Yc, h->cy.p, skip);
+        h_cy(h, Yc, skip);
       } else {
         k_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p,
                                                            h->c_val.p, h->sv1.p, h->cy.p, skip);

@@ -541,8 +541,8 @@ void build_plan_device(cutbddc_gpu* h) {
   CB_CUDA(cudaMemsetAsync(h->loc_of_dof.p, 0xff, sizeof(int32_t) * nd, s));
   k_scatter_pos<<<grid_for(nloc, 256), 256, 0, s>>>(nloc, h->loc_glob.p, h->loc_of_dof.p);
   CB_LAUNCH();
-  int32_t own = 0;
-  CB_CUDA(cudaMemcpyAsync(&own, h->seg_ptr.p + nsd, 4, cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> hseg((size_t)nsd + 1);
+  CB_CUDA(cudaMemcpyAsync(hseg.data(), h->seg_ptr.p, sizeof(int32_t) * (nsd + 1), cudaMemcpyDeviceToHost, s));
   // neighbour ranks
   DevBuf<unsigned int>& om = h->ws_omask;
   om.alloc(1);
@@ -552,7 +552,26 @@ void build_plan_device(cutbddc_gpu* h) {
   unsigned int mask = 0;
   CB_CUDA(cudaMemcpyAsync(&mask, om.p, 4, cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
-  h->n_own = own;
+  h->n_own = hseg[(size_t)nsd];
+  {  // segment-kernel chunks (dist.cuh): per segment, then the ghosts
+    std::vector<int4> ch;
+    std::vector<int32_t> first((size_t)nsd + 1, 0);
+    for (int sd = 0; sd < nsd; ++sd) {
+      first[(size_t)sd] = (int32_t)ch.size();
+      for (int32_t lo = hseg[(size_t)sd]; lo < hseg[(size_t)sd + 1]; lo += kChunk)
+        ch.push_back(make_int4(sd, lo, std::min(lo + kChunk, hseg[(size_t)sd + 1]), 0));
+    }
+    first[(size_t)nsd] = (int32_t)ch.size();
+    for (int64_t lo = hseg[(size_t)nsd]; lo < nloc; lo += kChunk)
+      ch.push_back(make_int4(-1, (int)lo, (int)std::min<int64_t>(lo + kChunk, nloc), 0));
+    if (ch.empty()) ch.push_back(make_int4(-1, 0, 0, 0));
+    h->n_chunks = (int64_t)ch.size();
+    h->chunks.upload(ch, s);
+    h->seg_chunk.upload(first, s);
+    h->cpart.alloc(ch.size());
+    h->tickets.alloc((size_t)nsd);
+    h->tickets.zero(s);
+  }
   h->nbr.clear();
   std::vector<int32_t> nbr_of_rank(kMaxRanks, -1);
   for (int q = 0; q < h->dist_world; ++q)

@@ -21,7 +21,6 @@
 namespace cutbddc_b200 {
 
 constexpr int kSegThreads = 256;   // block size of every segment kernel (fixed: reductions are bit-reproducible)
-constexpr int kGhostChunk = 4096;  // ghost-segment dofs per block
 
 // Distribution set by the caller (cutbddc_gpu_set_distribution), or the
 // default one-rank distribution of `part` when none was set.
@@ -62,34 +61,54 @@ void sub_apply(cutbddc_gpu* h, int mode, const double* xloc, const double* Xslot
 // the owned ones (segments, not the ghost segment).
 void to_local(cutbddc_gpu* h, const double* xglob, double* xloc);
 void to_global_owned(cutbddc_gpu* h, const double* xloc, double* xglob);
-// grid of a segment kernel: one block per local subdomain + the ghost chunks
-inline int seg_grid(const cutbddc_gpu* h) {
-  return h->nsd + (int)((h->n_loc - h->n_own + kGhostChunk - 1) / kGhostChunk);
-}
+// Segment kernels run one block per chunk of kChunk local dofs: the chunks
+// of a subdomain's segment (its owned dofs), then the ghost chunks. A chunk
+// writes its partial; the last chunk of a segment to finish (ticket) adds
+// the segment's chunk partials in chunk order into the subdomain's partial.
+// Chunks depend only on the segment's length, so the partials are the same
+// bits for every world size.
+constexpr int kChunk = 256;
+inline int seg_grid(const cutbddc_gpu* h) { return (int)h->n_chunks; }
 
 struct SegArgs {
-  const int32_t* seg_ptr;  // nsd + 1
-  int nsd;
-  int64_t n_loc;
-  double* part;            // this rank's partials (h->partials + rank * maxloc)
+  const int4* chunks;       // per block: (local subdomain or -1 for ghosts, lo, hi, 0)
+  const int32_t* seg_chunk; // nsd + 1: first chunk of each segment
+  double* cpart;            // per chunk partial
+  int* tickets;             // per segment (0 between kernels)
+  double* part;             // this rank's subdomain partials (part_all + rank * maxloc)
 };
 inline SegArgs seg_args(const cutbddc_gpu* h, double* part_all) {
-  return SegArgs{h->seg_ptr.p, h->nsd, h->n_loc, part_all ? part_all + (int64_t)h->dist_rank * h->maxloc : nullptr};
+  return SegArgs{h->chunks.p, h->seg_chunk.p, h->cpart.p, h->tickets.p,
+                 part_all ? part_all + (int64_t)h->dist_rank * h->maxloc : nullptr};
 }
 
-// Range of the calling block: a subdomain's segment (returns true: the block
-// writes that subdomain's partial) or a ghost chunk (false).
-__device__ inline bool seg_range(const SegArgs& a, int& lo, int& hi) {
-  const int b = blockIdx.x;
-  if (b < a.nsd) {
-    lo = a.seg_ptr[b];
-    hi = a.seg_ptr[b + 1];
-    return true;
+// Range of the calling block; its subdomain (-1: a ghost chunk, no partial).
+__device__ inline int seg_range(const SegArgs& a, int& lo, int& hi) {
+  const int4 c = a.chunks[blockIdx.x];
+  lo = c.y;
+  hi = c.z;
+  return c.x;
+}
+
+// Every thread of a non-ghost chunk calls this with its accumulator.
+__device__ inline void seg_commit(const SegArgs& a, int seg, double acc) {
+  __shared__ double sh[32];
+  __shared__ int last;
+  acc = block_sum<kSegThreads>(acc, sh);
+  if (threadIdx.x == 0) {
+    a.cpart[blockIdx.x] = acc;
+    __threadfence();
+    const int n = a.seg_chunk[seg + 1] - a.seg_chunk[seg];
+    last = atomicAdd(&a.tickets[seg], 1) == n - 1;
   }
-  const int64_t g0 = a.seg_ptr[a.nsd] + (int64_t)(b - a.nsd) * kGhostChunk;
-  lo = (int)g0;
-  hi = (int)(g0 + kGhostChunk < a.n_loc ? g0 + kGhostChunk : a.n_loc);
-  return false;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (int k = a.seg_chunk[seg]; k < a.seg_chunk[seg + 1]; ++k) s += __ldcg(a.cpart + k);
+    a.part[seg] = s;
+    a.tickets[seg] = 0;
+  }
 }
 
 // Σ over global subdomains g (ascending, fixed thread mapping and tree) of

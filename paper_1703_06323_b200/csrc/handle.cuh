@@ -104,6 +104,11 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int32_t> loc_glob;        // n_loc: global dof of each local dof
   cutbddc_b200::DevBuf<int32_t> loc_of_dof;      // n_dof: local dof or -1
   cutbddc_b200::DevBuf<int32_t> seg_ptr;         // nsd + 1
+  cutbddc_b200::DevBuf<int4> chunks;             // segment-kernel blocks: (segment or -1, lo, hi, 0) (dist.cuh)
+  cutbddc_b200::DevBuf<int32_t> seg_chunk;       // nsd + 1: first chunk of each segment
+  cutbddc_b200::DevBuf<double> cpart;            // per chunk partial
+  cutbddc_b200::DevBuf<int> tickets;             // per segment
+  int64_t n_chunks = 0;
   cutbddc_b200::DevBuf<int32_t> slot_loc;        // nsd*T: local dof of each slot or -1
   cutbddc_b200::DevBuf<int32_t> lcopy_ptr;       // n_loc + 1
   cutbddc_b200::DevBuf<int32_t> lcopy_src;       // copies, ascending global sd: >= 0 slot (sd*T+slot), < 0: -1 - receive index
@@ -207,6 +212,7 @@ struct cutbddc_gpu {
   // front-column order (column-major, np_sd x m_sd at root_info[4 sd + 3]),
   // hslot[root_info[4 sd + 1] + k] = sd * T + slot of compact position k
   cutbddc_b200::DevBuf<int32_t> hslot;
+  cutbddc_b200::DevBuf<double> hcy_part;          // H^T y' chunk partials (bddc.cu h_cy)
   int np_max = 0;
   cutbddc_b200::DevBuf<double> uvec;              // m_total: S^{-1}(zc - cy) per constraint row
   bool bddc_ready = false;

@@ -49,9 +49,8 @@ __global__ void __launch_bounds__(kSegThreads) k_spmv_dot(SegArgs a, const int32
                                                           const double* __restrict__ recv, const double* __restrict__ p,
                                                           double* __restrict__ q, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  __shared__ double sh[32];
   int lo, hi;
-  const bool part = seg_range(a, lo, hi);
+  const int seg = seg_range(a, lo, hi);
   double acc = 0.0;
   for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
     double v = 0.0;
@@ -62,21 +61,19 @@ __global__ void __launch_bounds__(kSegThreads) k_spmv_dot(SegArgs a, const int32
     q[i] = v;
     acc += p[i] * v;
   }
-  if (!part || !a.part) return;
-  acc = block_sum<kSegThreads>(acc, sh);
-  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
+  if (seg < 0 || !a.part) return;
+  seg_commit(a, seg, acc);
 }
 
 // partials of a.b
 __global__ void __launch_bounds__(kSegThreads) k_seg_dot(SegArgs a, const double* __restrict__ x,
                                                          const double* __restrict__ y) {
-  __shared__ double sh[32];
   int lo, hi;
-  if (!seg_range(a, lo, hi)) return;
+  const int seg = seg_range(a, lo, hi);
+  if (seg < 0) return;
   double acc = 0.0;
   for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) acc += x[i] * y[i];
-  acc = block_sum<kSegThreads>(acc, sh);
-  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
+  seg_commit(a, seg, acc);
 }
 
 // alpha = rz / pq (pq from the gathered partials, the same in every block),
@@ -88,7 +85,6 @@ __global__ void __launch_bounds__(kSegThreads) k_update_xr(SegArgs a, Fin f, con
                                                            double* __restrict__ r, double* __restrict__ lal,
                                                            int* __restrict__ is) {
   if (is[I_DONE]) return;
-  __shared__ double sh[32];
   const int k = is[I_ITER];
   const double pq = finish_partials(pq_part, f.gpos, f.nsd_g);
   if (!(pq > 0.0)) {
@@ -108,7 +104,7 @@ __global__ void __launch_bounds__(kSegThreads) k_update_xr(SegArgs a, Fin f, con
     lal[k - 1] = al;
   }
   int lo, hi;
-  const bool part = seg_range(a, lo, hi);
+  const int seg = seg_range(a, lo, hi);
   double acc = 0.0;
   for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
     x[i] += al * p[i];
@@ -116,9 +112,8 @@ __global__ void __launch_bounds__(kSegThreads) k_update_xr(SegArgs a, Fin f, con
     r[i] = ri;
     acc += ri * ri;
   }
-  if (!part || k % 50 == 0) return;
-  acc = block_sum<kSegThreads>(acc, sh);
-  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
+  if (seg < 0 || k % 50 == 0) return;
+  seg_commit(a, seg, acc);
 }
 
 // true residual refresh at k % 50 == 0: r = b - Σ_copies Y (Y = A_w x_w),
@@ -128,9 +123,8 @@ __global__ void __launch_bounds__(kSegThreads) k_refresh(SegArgs a, const int32_
                                                          const double* __restrict__ recv, const double* __restrict__ b,
                                                          double* __restrict__ r, const int* __restrict__ is) {
   if (is[I_NOREF]) return;
-  __shared__ double sh[32];
   int lo, hi;
-  const bool part = seg_range(a, lo, hi);
+  const int seg = seg_range(a, lo, hi);
   double acc = 0.0;
   for (int i = lo + threadIdx.x; i < hi; i += kSegThreads) {
     double v = 0.0;
@@ -142,9 +136,8 @@ __global__ void __launch_bounds__(kSegThreads) k_refresh(SegArgs a, const int32_
     r[i] = ri;
     acc += ri * ri;
   }
-  if (!part) return;
-  acc = block_sum<kSegThreads>(acc, sh);
-  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
+  if (seg < 0) return;
+  seg_commit(a, seg, acc);
 }
 
 // |r| -> history, convergence / max_iter test
