@@ -309,12 +309,8 @@ def main():
         return rep
 
     def solve_e2e(s):
-        dirichlet = assemble(s, mesh)                                  # H2D of the mesh view
-        if cfg.variant == configs.V_STANDARD:                         # objects on the device
-            o2 = s.classify_objects(cfg.objects, cfg.variant)
-        else:                                                          # v1/v2 edge splits: host
-            diag = s.local_diagonals() if cfg.variant == configs.V2 else None
-            o2 = cb.classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, diag)
+        assemble(s, mesh)                                              # H2D of the mesh view
+        o2 = s.classify_objects(cfg.objects, cfg.variant)              # objects (+ v1/v2 splits) on the device
         s.setup_bddc(o2, cfg.weighting)
         return s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)             # D2H of x
 

@@ -215,10 +215,12 @@ cutbddc_status cutbddc_classify_objects(const cutbddc_mesh_view* mesh, const cut
                                         const uint8_t* dirichlet, int objects, int variant, const double* weights,
                                         cutbddc_objects** out);
 void cutbddc_objects_free(cutbddc_objects* o);
-/* classify_objects on the device from the mesh and
- * strong-Dirichlet mask left by cutbddc_gpu_assemble: the same objects,
- * bit for bit, as cutbddc_classify_objects with the standard variant
- * (v1/v2 return CUTBDDC_CONFIG). Free the result with cutbddc_objects_free. */
+/* classify_objects and the edge splits split_edges_v1 /
+ * split_edges_v2 on the device from the mesh, the
+ * strong-Dirichlet mask and (v2) the subdomain matrices left by
+ * cutbddc_gpu_assemble: the same objects, bit for bit, as
+ * cutbddc_classify_objects. v2 needs every subdomain on this handle
+ * (CUTBDDC_CONFIG on a distributed one). Free with cutbddc_objects_free. */
 cutbddc_status cutbddc_gpu_classify_objects(cutbddc_gpu* h, int objects, int variant, cutbddc_objects** out);
 
 /* Multi-GPU (one process and one handle per GPU). Subdomains are assigned

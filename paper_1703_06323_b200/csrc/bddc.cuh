@@ -8,7 +8,7 @@ namespace cutbddc_b200 {
 
 void classify_device(cutbddc_gpu* h, const cutbddc_geometry* g);
 void assemble_device(cutbddc_gpu* h, const cutbddc_partition_view* part);
-cutbddc_objects* classify_objects_device(cutbddc_gpu* h, int objects);
+cutbddc_objects* classify_objects_device(cutbddc_gpu* h, int objects, int variant);
 void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weighting);
 // rz_part: when not null, per-subdomain partials of r.z (gathered layout, dist.cuh)
 void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip, double* rz_part = nullptr);

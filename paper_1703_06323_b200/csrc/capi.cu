@@ -254,11 +254,11 @@ cutbddc_status cutbddc_gpu_classify_objects(cutbddc_gpu* h, int objects, int var
     if (!out) throw Failure(CUTBDDC_INVALID_ARGUMENT, "objects: null output");
     if (objects < CUTBDDC_OBJECTS_C || objects > CUTBDDC_OBJECTS_CEF)
       throw Failure(CUTBDDC_CONFIG, "bddc.objects must be c, ce or cef");
-    if (variant != CUTBDDC_VARIANT_STANDARD)
-      throw Failure(CUTBDDC_CONFIG, "device objects: standard variant only (v1/v2: cutbddc_classify_objects)");
+    if (variant < CUTBDDC_VARIANT_STANDARD || variant > CUTBDDC_VARIANT_V2)
+      throw Failure(CUTBDDC_CONFIG, "bddc.variant must be standard, v1 or v2");
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "objects: assemble first");
-    *out = classify_objects_device(h, objects);
+    *out = classify_objects_device(h, objects, variant);
   });
 }
 

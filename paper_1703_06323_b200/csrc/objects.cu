@@ -15,6 +15,12 @@
 //              its smallest dof (deterministic labels)
 //   kinds      singleton -> Corner, |neigh| = 2 -> Face, else Edge
 //   order      by smallest dof, dofs ascending (stable radix sort by label)
+//   variants   the paper's improved coarse edges: an edge
+//              lattice edge joins two nodes only if neither is a v1 cut node
+//              (an incident edge of the object changes the sign of phi,
+//              PAPER.md:585-590) / their stiffness weight tuples agree within
+//              1e-8 (v2; weights diag_w / Σ_w' diag_w' in
+//              ascending subdomain order, the host's summation order)
 #include <cub/cub.cuh>
 
 #include "handle.cuh"
@@ -93,14 +99,32 @@ __device__ __forceinline__ void uf_union(int32_t* p, int a, int b) {
   }
 }
 
+__device__ __forceinline__ bool edge_active(const uint8_t* __restrict__ cls, int n, const int c[3], int ax) {
+  // edge_active (mesh.cpp:74-108): one of the <= 4 cells around the edge is not exterior
+  const int o1 = ax == 0 ? 1 : 0, o2 = ax == 2 ? 1 : 2;
+  for (int da = -1; da <= 0; ++da)
+    for (int db = -1; db <= 0; ++db) {
+      int e[3] = {c[0], c[1], c[2]};
+      e[o1] += da;
+      e[o2] += db;
+      if (e[0] < 0 || e[1] < 0 || e[2] < 0 || e[0] >= n || e[1] >= n || e[2] >= n) continue;
+      if (cls[((int64_t)e[0] * n + e[1]) * n + e[2]] != CUTBDDC_EXTERIOR) return true;
+    }
+  return false;
+}
+
 // union along active +axis lattice edges between equal-key interface dofs
+// (edge keys: unless a variant splits them, see the header)
 __global__ void k_obj_union(int64_t nd, int n, const uint8_t* __restrict__ cls, const int32_t* __restrict__ dof_of_node,
                             const int64_t* __restrict__ node_of_dof, const uint64_t* __restrict__ key,
-                            int32_t* parent) {
+                            int32_t* parent, int variant, const uint8_t* __restrict__ cut,
+                            const double* __restrict__ w8) {
   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (d >= nd) return;
   const uint64_t kd = key[d];
   if (kd == kNoKey) return;
+  const bool edge = __popcll(kd & 0xff) > 2;
+  if (edge && variant == CUTBDDC_VARIANT_V1 && cut[d]) return;
   int c[3];
   node_ijk(node_of_dof[d], n, c);
   for (int ax = 0; ax < 3; ++ax) {
@@ -109,19 +133,66 @@ __global__ void k_obj_union(int64_t nd, int n, const uint8_t* __restrict__ cls, 
     cc[ax] += 1;
     const int32_t d2 = dof_of_node[((int64_t)cc[0] * (n + 1) + cc[1]) * (n + 1) + cc[2]];
     if (d2 < 0 || key[d2] != kd) continue;
-    // edge_active (mesh.cpp:74-108): one of the <= 4 cells around the edge is not exterior
-    const int o1 = ax == 0 ? 1 : 0, o2 = ax == 2 ? 1 : 2;
-    bool act = false;
-    for (int da = -1; da <= 0 && !act; ++da)
-      for (int db = -1; db <= 0 && !act; ++db) {
-        int e[3] = {c[0], c[1], c[2]};
-        e[o1] += da;
-        e[o2] += db;
-        if (e[0] < 0 || e[1] < 0 || e[2] < 0 || e[0] >= n || e[1] >= n || e[2] >= n) continue;
-        act = cls[((int64_t)e[0] * n + e[1]) * n + e[2]] != CUTBDDC_EXTERIOR;
+    if (edge && variant == CUTBDDC_VARIANT_V1 && cut[d2]) continue;
+    if (edge && variant == CUTBDDC_VARIANT_V2) {
+      bool same = true;
+      for (int q = 0; q < __popcll(kd & 0xff); ++q) {
+        const double wa = w8[d * 8 + q], wb = w8[(int64_t)d2 * 8 + q];
+        const double scale = fmax(1.0, fmax(fabs(wa), fabs(wb)));
+        if (fabs(wa - wb) > 1e-8 * scale) same = false;
       }
-    if (act) uf_union(parent, (int)d, (int)d2);
+      if (!same) continue;
+    }
+    if (edge_active(cls, n, c, ax)) uf_union(parent, (int)d, (int)d2);
   }
+}
+
+// v1: edge-key dofs with an incident active object edge across which phi
+// changes sign become corners
+__global__ void k_v1_cut(int64_t nd, int n, const uint8_t* __restrict__ cls, const int32_t* __restrict__ dof_of_node,
+                         const int64_t* __restrict__ node_of_dof, const uint64_t* __restrict__ key,
+                         const double* __restrict__ phi, uint8_t* __restrict__ cut) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  cut[d] = 0;
+  const uint64_t kd = key[d];
+  if (kd == kNoKey || __popcll(kd & 0xff) <= 2) return;
+  const int64_t v = node_of_dof[d];
+  int c[3];
+  node_ijk(v, n, c);
+  const bool neg = phi[v] < 0;
+  for (int ax = 0; ax < 3; ++ax)
+    for (int sgn = -1; sgn <= 1; sgn += 2) {
+      int cc[3] = {c[0], c[1], c[2]};
+      cc[ax] += sgn;
+      if (cc[ax] < 0 || cc[ax] > n) continue;
+      const int64_t v2 = ((int64_t)cc[0] * (n + 1) + cc[1]) * (n + 1) + cc[2];
+      const int32_t d2 = dof_of_node[v2];
+      if (d2 < 0 || key[d2] != kd) continue;
+      int lo[3] = {c[0], c[1], c[2]};
+      if (sgn < 0) lo[ax] -= 1;
+      if (!edge_active(cls, n, lo, ax)) continue;
+      if ((phi[v2] < 0) != neg) cut[d] = 1;
+    }
+}
+
+// v2: stiffness weight tuple of every interface dof (one rank holds every
+// copy): w_q = diag_q / Σ diag, copies in ascending subdomain order
+__global__ void k_v2_weights(int64_t nloc, int T, const int32_t* __restrict__ loc_glob,
+                             const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
+                             const double* __restrict__ As, double* __restrict__ w8) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  const int32_t p0 = cptr[i], k = cptr[i + 1] - p0;
+  if (k < 2) return;
+  double dg[8], tot = 0.0;
+  for (int q = 0; q < k; ++q) {
+    const int32_t c = csrc[p0 + q];
+    dg[q] = As[(int64_t)(c / T) * 27 * T + 13ll * T + c % T];
+    tot += dg[q];
+  }
+  const int64_t d = loc_glob[i];
+  for (int q = 0; q < k; ++q) w8[d * 8 + q] = dg[q] / tot;
 }
 
 __global__ void k_obj_label(int64_t nd, const uint64_t* __restrict__ key, int32_t* parent, int32_t* __restrict__ size) {
@@ -202,7 +273,7 @@ T* carve(DevBuf<uint8_t>& b, size_t& off, size_t count) {
 }  // namespace
 
 // Device objects -> host cutbddc_objects (arrays allocated with new[]).
-cutbddc_objects* classify_objects_device(cutbddc_gpu* h, int objects) {
+cutbddc_objects* classify_objects_device(cutbddc_gpu* h, int objects, int variant) {
   cudaStream_t s = h->stream;
   const int n = h->n, B = h->block;
   if (B < 1 || n % B != 0) throw Failure(CUTBDDC_INVALID_ARGUMENT, "objects: assemble a partition first");
@@ -269,7 +340,24 @@ cutbddc_objects* classify_objects_device(cutbddc_gpu* h, int objects) {
   k_obj_keys<<<grid_for(nd, 256), 256, 0, s>>>(nd, n, B, nb, h->cls.p, h->node_of_dof.p, h->orphan.p, key, parent,
                                                 size);
   CB_LAUNCH();
-  k_obj_union<<<grid_for(nd, 256), 256, 0, s>>>(nd, n, h->cls.p, h->dof_of_node.p, h->node_of_dof.p, key, parent);
+  uint8_t* cut = nullptr;
+  double* w8 = nullptr;
+  if (variant == CUTBDDC_VARIANT_V1) {
+    h->ws_cut.alloc((size_t)nd);
+    cut = h->ws_cut.p;
+    k_v1_cut<<<grid_for(nd, 256), 256, 0, s>>>(nd, n, h->cls.p, h->dof_of_node.p, h->node_of_dof.p, key, h->phi.p, cut);
+    CB_LAUNCH();
+  } else if (variant == CUTBDDC_VARIANT_V2) {
+    if (h->dist_world > 1)
+      throw Failure(CUTBDDC_CONFIG, "device objects v2: needs every subdomain's diagonals (one rank only)");
+    h->ws_w8.alloc((size_t)nd * 8);
+    w8 = h->ws_w8.p;
+    k_v2_weights<<<grid_for(h->n_loc, 256), 256, 0, s>>>(h->n_loc, h->slots, h->loc_glob.p, h->lcopy_ptr.p,
+                                                         h->lcopy_src.p, h->As.p, w8);
+    CB_LAUNCH();
+  }
+  k_obj_union<<<grid_for(nd, 256), 256, 0, s>>>(nd, n, h->cls.p, h->dof_of_node.p, h->node_of_dof.p, key, parent,
+                                                variant, cut, w8);
   CB_LAUNCH();
   k_obj_label<<<grid_for(nd, 256), 256, 0, s>>>(nd, key, parent, size);
   CB_LAUNCH();

@@ -340,8 +340,8 @@ class GpuSolver:
         return dirichlet
 
     def classify_objects(self, objects: int, variant: int = 0) -> Objects:
-        """classify_objects on the device from the assembled mesh (standard
-        variant; bit-identical to the host classify_objects)."""
+        """classify_objects (+ the v1 / v2 edge splits) on the device from the
+        assembled mesh; bit-identical to the host classify_objects."""
         out = C.POINTER(_Objects)()
         _check(lib().cutbddc_gpu_classify_objects(self.h, objects, variant, C.byref(out)))
         return _take_objects(out)

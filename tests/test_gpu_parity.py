@@ -280,15 +280,19 @@ def _objects_equal(a, b):
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
 def test_device_objects_bit_exact_vs_host(name):
     """classify_objects on the device (objects.cu) against the host
-    restatement (host_partition.cpp), every object level: identical kinds,
+    restatement (host_partition.cpp), every object level and every variant
+    (standard, v1 cut-edge corners, v2 weight-tuple splits): identical kinds,
     dofs, neighbour lists and order."""
     cfg = configs.get(name)
     s = cb.GpuSolver(0)
     pb = cb.prepare(s, cfg)
-    for level in (configs.OBJ_C, configs.OBJ_CE, configs.OBJ_CEF):
-        host = cb.classify_objects(pb.mesh, cfg.block, pb.block_ids, pb.dirichlet, level, 0, None)
-        dev = s.classify_objects(level, 0)
-        assert len(dev) == len(host) and _objects_equal(dev, host), (name, level)
+    diag = s.local_diagonals()
+    for variant in (configs.V_STANDARD, configs.V1, configs.V2):
+        for level in (configs.OBJ_C, configs.OBJ_CE, configs.OBJ_CEF):
+            host = cb.classify_objects(pb.mesh, cfg.block, pb.block_ids, pb.dirichlet, level, variant,
+                                       diag if variant == configs.V2 else None)
+            dev = s.classify_objects(level, variant)
+            assert len(dev) == len(host) and _objects_equal(dev, host), (name, variant, level)
     s.close()
 
 
