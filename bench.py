@@ -259,6 +259,26 @@ def _cfg5_leg(cb, args, hbm, peak_source, local):
     return out
 
 
+def _batch_leg(cfg, local, n_sys=8, conc=4):
+    """a translation sweep of n_sys
+    cfg4 systems, one at a time vs `conc` in flight (one handle and stream
+    each); wall clock of the whole batch including each system's classify,
+    partition, device objects, assembly, setup and PCG."""
+    from paper_1703_06323_b200 import batch
+    cfgs = batch.translation_sweep(cfg, n_sys)
+    out = {"workload": f"{n_sys} translated {cfg.name} systems (eps in [-h, h] along (1,1,1)), warm handles"}
+    for c in (1, conc):
+        runner = batch.BatchRunner(local, c)
+        runner.run(cfgs)  # warm: every handle's buffers and graphs exist
+        res, wall = runner.run(cfgs)
+        runner.close()
+        nd = sum(r.n_dof for r in res)
+        out[f"concurrency_{c}"] = {"value": nd / wall, "unit": "DOF/s", "wall_s": wall,
+                                   "iterations": [r.report["iterations"] for r in res]}
+    out["speedup"] = out[f"concurrency_{conc}"]["value"] / out["concurrency_1"]["value"]
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -269,6 +289,7 @@ def main():
     ap.add_argument("--variant", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 sub-measurement")
+    ap.add_argument("--no-batch", action="store_true", help="skip the batched translation-sweep sub-measurement")
     args = ap.parse_args()
     rank, world, local = _env_rank()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -388,6 +409,10 @@ def main():
     if world == 1 and not args.no_cfg5 and cfg.name == "cfg4":
         cfg5 = _cfg5_leg(cb, args, hbm, peak_source, local)
 
+    batch_leg = None
+    if world == 1 and not args.no_batch and cfg.name == "cfg4":
+        batch_leg = _batch_leg(cfg, local)
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -412,7 +437,7 @@ def main():
             "roofline": roof, "roofline_fp64": roof64, "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "DOF/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "stat": "median of 5 solves", "samples_ms": [round(1e3 * t, 3) for t in e2e_t]},
-            "e2e_fresh_handle": fresh, "cfg5": cfg5,
+            "e2e_fresh_handle": fresh, "cfg5": cfg5, "batch": batch_leg,
             "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
