@@ -836,6 +836,7 @@ void coarse_basis_corner(cutbddc_gpu* h, const std::vector<int64_t>& m_off, cons
   h->ws_y8.alloc((size_t)kSweepMultiRhs * ns);
   h->ws_u8.alloc((size_t)kSweepMultiRhs * std::max<int64_t>(1, f.upd_total));
   h->ws_v8.alloc((size_t)kSweepMultiRhs * std::max<size_t>(1, f.vbuf.n));
+  ProfScope pc(h->prof, s, "coarse basis H passes");
   for (int pass = 0; pass * kSweepMultiRhs < m_max; ++pass) {
     h->ws_x8.zero(s);
     k_ct_rhs<<<dim3(nsd, kSweepMultiRhs), 128, 0, s>>>(pass, ns, T, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
@@ -846,6 +847,7 @@ void coarse_basis_corner(cutbddc_gpu* h, const std::vector<int64_t>& m_off, cons
                                               dcoff.p, h->m_off.p, h->root_info.p, h->ws_y8.p, h->hroot.p, h->hslot.p);
     CB_LAUNCH();
   }
+  pc.next("coarse basis S, S^-1");
   DevBuf<double>& S = h->ws_s;
   S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
   k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
@@ -884,6 +886,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   const int nc = cv ? cv->n_objects : 0;
   const int nsd_g = h->nsd_g, world = h->dist_world, rank = h->dist_rank;
   std::vector<int64_t> node_of_dof = h->node_of_dof.to_host(s);
+  ps_host.next("setup 0a host rows");
   std::vector<std::vector<int>> obj_of_gsd((size_t)nsd_g);  // object ids per global sd (ascending)
   for (int o = 0; o < nc; ++o)
     for (int64_t p = cv->neigh_ptr[o]; p < cv->neigh_ptr[o + 1]; ++p) {
@@ -989,6 +992,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   h->row_sd.alloc((size_t)std::max<int64_t>(1, h->m_total));
   k_row_sd<<<nsd, 128, 0, s>>>(nsd, h->m_off.p, h->row_sd.p);
   CB_LAUNCH();
+  ps_host.next("setup 0b weights");
   // ---- weights, rho
   DevBuf<int>& bad = h->ws_flag;
   bad.alloc(1);
@@ -1075,7 +1079,10 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
         jobs.push_back(FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg});
       }
     }
-    factor_numeric(h, jobs);
+    factor_numeric(h, jobs, [&] {  // the sweep item lists on the host while the GPU factorises
+      build_sweep_items(h, h->tI, h->fI);
+      if (h->has_K) build_sweep_items(h, h->k_corner ? h->tI : h->tK, h->fK);
+    });
     corner_bad = h->has_K && h->k_corner && (k_failed || !corner_pivots_ok(h));
   });
   // a floating fragment (no corner, no Nitsche boundary) leaves K_c singular
@@ -1086,7 +1093,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     local([&] {
       if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
       factor_symbolic(h, h->tK, fk, h->fK);
-      factor_numeric(h, {FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg}});
+      factor_numeric(h, {FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg}}, [&] { build_sweep_items(h, h->tK, h->fK); });
     });
     agree(0);
   }

@@ -166,6 +166,7 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
   k_symbolic<<<dim3(nsn, nsd), kThreads, 0, s>>>(t, nsd, in.mask, f.pfx.p, f.tpos.p, f.rc.p);
   CB_LAUNCH();
   f.h_rc = f.rc.to_host(s);
+  pplan.next(std::string("factor") + tag_of(h, f) + " symbolic host");
   std::vector<int64_t> poff((size_t)nsd * nsn), uoff((size_t)nsd * nsn), foff((size_t)nsd * nsn);
   f.h_front_base.assign((size_t)nsd + 1, 0);
   int64_t pt = 0, ut = 0;
@@ -197,6 +198,7 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
   f.h_front_off = foff;
   f.upd_off.upload(uoff, s);
   f.panel.alloc((size_t)pt + 2);  // +2: the sweeps' 16-byte aligned bulk copies may read one double past the end
+  pplan.next(std::string("factor") + tag_of(h, f) + " sweep plan");
   build_sweep_plan(h, ts, f, poff, uoff);
 }
 
@@ -205,7 +207,7 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
 // all their fronts fit a workspace budget of half the free device memory;
 // otherwise each runs alone in subdomain chunks bounded by the budget (every
 // chunk repeats the tree's critical path).
-void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs) {
+void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const std::function<void()>& overlap) {
   cudaStream_t s = h->stream;
   const int nsd = h->nsd;
   DevBuf<unsigned long long>& fail = h->ws_fail;
@@ -250,6 +252,7 @@ void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs) {
     }
   }
   pnum.close();
+  if (overlap) overlap();
   std::vector<unsigned long long> fl(jobs.size());
   CB_CUDA(cudaMemcpyAsync(fl.data(), fail.p, 8 * jobs.size(), cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));

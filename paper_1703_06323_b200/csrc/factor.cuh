@@ -1,6 +1,8 @@
 // factor.cuh — interfaces of the batched multifrontal factorisation/solves.
 #pragma once
 
+#include <functional>
+
 #include "front_desc.cuh"
 #include "handle.cuh"
 
@@ -67,7 +69,9 @@ struct FactorJob {
   const char* what;       // error message prefix (non-positive pivot)
   bool* failed = nullptr;  // set: a non-positive pivot is reported here instead of thrown
 };
-void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs);
+// `overlap`: host work run after the factorisation is enqueued, before the
+// pivot check waits for it (the sweep item lists)
+void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const std::function<void()>& overlap = {});
 // ysave: nsd x T doubles of scratch (forward results of big fronts).
 void solve_device(cutbddc_gpu* h, const TplSet& t, const FactorSet& f, double* X, double* upd, double* ysave,
                   const int* skip);
@@ -76,6 +80,8 @@ double sweep_bytes(const FactorSet& f);
 // sweep.cu: dataflow sweeps for one right-hand side (plan built per factorisation)
 void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std::vector<int64_t>& poff,
                       const std::vector<int64_t>& uoff);
+// the sweeps' item lists (host; run while the GPU factorises: factor_numeric's overlap hook)
+void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f);
 void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip);
 enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3, kSweepAttrOnly = 4 };

@@ -69,6 +69,7 @@ struct FactorSet {
   int64_t vec_total = 0;
   int n_items_f = 0, n_items_b = 0;
   int n_items_b_root = 0;                      // leading backward items of the root level
+  bool items_ready = false;                    // item lists built (build_sweep_items)
   int fwd_cols = 256, bwd_cols = 32;           // sweep item sizes (sweep.cu choose_item_sizes)
   int small_work = 8192;                       // panel entries of the largest one-item forward front
   std::vector<int64_t> h_vec_off;              // nsd x nsn compact front vector offsets (host copy)

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -23,10 +24,12 @@ struct Prof {
   struct Rec {
     std::string name;
     cudaEvent_t a, b;
+    double host_ms;  // host wall time spent inside the scope (enqueue + host work)
   };
   std::vector<Rec> pending;
   std::map<std::string, std::pair<long long, double>> tot;  // name -> (count, ms)
   std::map<std::string, double> mx;                         // name -> max ms of one scope
+  std::map<std::string, double> host;                       // name -> host ms
 
   Prof() {
     const char* e = std::getenv("CUTBDDC_PROFILE");
@@ -41,6 +44,7 @@ struct Prof {
       t.first += 1;
       t.second += ms;
       mx[r.name] = std::max(mx[r.name], (double)ms);
+      host[r.name] += r.host_ms;
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
     }
@@ -51,11 +55,12 @@ struct Prof {
     flush();
     double all = 0;
     for (auto& kv : tot) all += kv.second.second;
-    std::fprintf(stderr, "[cutbddc profile] %-40s %8s %10s %10s %10s\n", "scope", "count", "total ms", "mean us",
-                 "max us");
+    std::fprintf(stderr, "[cutbddc profile] %-40s %8s %10s %10s %10s %12s\n", "scope", "count", "total ms", "mean us",
+                 "max us", "host mean us");
     for (auto& kv : tot)
-      std::fprintf(stderr, "[cutbddc profile] %-40s %8lld %10.3f %10.2f %10.2f\n", kv.first.c_str(), kv.second.first,
-                   kv.second.second, 1e3 * kv.second.second / (double)kv.second.first, 1e3 * mx[kv.first]);
+      std::fprintf(stderr, "[cutbddc profile] %-40s %8lld %10.3f %10.2f %10.2f %12.2f\n", kv.first.c_str(),
+                   kv.second.first, kv.second.second, 1e3 * kv.second.second / (double)kv.second.first,
+                   1e3 * mx[kv.first], 1e3 * host[kv.first] / (double)kv.second.first);
     std::fprintf(stderr, "[cutbddc profile] (scopes may nest; sum of all = %.3f ms)\n", all);
   }
   ~Prof() {
@@ -72,6 +77,7 @@ struct ProfScope {
   cudaStream_t s = nullptr;
   std::string name;
   cudaEvent_t a = nullptr;
+  std::chrono::steady_clock::time_point t0;
   ProfScope(Prof& prof, cudaStream_t st, std::string nm) {
     if (!prof.on) return;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -82,13 +88,15 @@ struct ProfScope {
     name = std::move(nm);
     cudaEventCreate(&a);
     cudaEventRecord(a, s);
+    t0 = std::chrono::steady_clock::now();
   }
   void close() {
     if (!p || !a) return;
     cudaEvent_t b;
     cudaEventCreate(&b);
     cudaEventRecord(b, s);
-    p->pending.push_back({name, a, b});
+    const double hm = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    p->pending.push_back({name, a, b, hm});
     if (p->pending.size() > 4096) p->flush();
     a = nullptr;
   }
@@ -99,6 +107,7 @@ struct ProfScope {
     name = std::move(nm);
     cudaEventCreate(&a);
     cudaEventRecord(a, s);
+    t0 = std::chrono::steady_clock::now();
   }
   ~ProfScope() {
     if (p && a) close();

@@ -758,6 +758,43 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
         d.pnb = nb[(size_t)d.pfs];
       }
     }
+  f.items_ready = false;
+  f.desc.upload(reinterpret_cast<const int4*>(desc.data()), desc.size() * 6, s);
+  f.cslot.alloc((size_t)std::max<int64_t>(1, tot));
+  f.umap.alloc((size_t)std::max<int64_t>(1, f.upd_total));
+  if (f.upd_total >= (1ll << 31)) throw Failure(CUTBDDC_CONFIG, "sweep: update workspace exceeds 32-bit indexing");
+  f.gmap.alloc((size_t)2 * std::max<int64_t>(1, tot));
+  CB_CUDA(cudaMemsetAsync(f.gmap.p, 0xff, sizeof(int32_t) * f.gmap.n, s));
+  f.vbuf.alloc((size_t)std::max<int64_t>(1, ptot));
+  f.counters.alloc((size_t)4 * nsd * nsn + 3 + nrb_tot);
+  const TplDev t = tpl_dev(ts, h->slots);
+  k_sweep_maps<<<dim3(nsn, nsd), 256, 0, s>>>(t, factor_dev(f), reinterpret_cast<const FrontDesc*>(f.desc.p),
+                                              f.cslot.p, f.umap.p, f.gmap.p);
+  CB_LAUNCH();
+  // no synchronisation: uploads from pageable host memory return once the
+  // data is staged, so the host vectors above may go out of scope
+}
+
+// The sweeps' work items in dependency (critical-path) order. Needed only by
+// the solves, so setup builds them on the host while the GPU factorises.
+void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f) {
+  cudaStream_t s = h->stream;
+  const Template& tp = ts.tpl;
+  const int nsd = h->nsd, nsn = (int)tp.sn.size();
+  const auto& lv = tp.levels;
+  const int nlev = (int)lv.size();
+  const int fc = f.fwd_cols, bc = f.bwd_cols;
+  auto is_small = [&f](int2 rc) { return rc.x <= kSmallRows && (int64_t)rc.x * rc.y <= f.small_work; };
+  std::vector<int32_t> nf((size_t)nsd * nsn, 0), nb((size_t)nsd * nsn, 0);
+  for (size_t i = 0; i < (size_t)nsd * nsn; ++i) {
+    const int2 v = f.h_rc[i];
+    nf[i] = v.x == 0 ? 0 : is_small(v) ? 1 : (v.x + kFwdRows - 1) / kFwdRows;
+    nb[i] = v.x == 0 ? 0 : std::max(1, (v.y + bc - 1) / bc);
+  }
+  auto mcb_of = [fc](int c) { return std::max(1, (c + fc - 1) / fc); };
+  auto ncb_of = [fc](int r, int c, int rb) {
+    return std::max(1, (std::min(c, std::min(r, (rb + 1) * kFwdRows)) + fc - 1) / fc);
+  };
   std::vector<int4> fw, bw;
   auto front_items = [&](int L, bool fwd, std::vector<int4>& out) {
     for (int sid : lv[(size_t)L])
@@ -873,22 +910,11 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   f.n_items_b = (int)bw.size();
   if (fw.empty()) fw.push_back(make_int4(0, 0, 0, 0));
   if (bw.empty()) bw.push_back(make_int4(0, 0, 0, 0));
-  f.desc.upload(reinterpret_cast<const int4*>(desc.data()), desc.size() * 6, s);
   f.items_f.upload(fw, s);
   f.items_b.upload(bw, s);
-  f.cslot.alloc((size_t)std::max<int64_t>(1, tot));
-  f.umap.alloc((size_t)std::max<int64_t>(1, f.upd_total));
-  if (f.upd_total >= (1ll << 31)) throw Failure(CUTBDDC_CONFIG, "sweep: update workspace exceeds 32-bit indexing");
-  f.gmap.alloc((size_t)2 * std::max<int64_t>(1, tot));
-  CB_CUDA(cudaMemsetAsync(f.gmap.p, 0xff, sizeof(int32_t) * f.gmap.n, s));
-  f.vbuf.alloc((size_t)std::max<int64_t>(1, ptot));
-  f.counters.alloc((size_t)4 * nsd * nsn + 3 + nrb_tot);
-  const TplDev t = tpl_dev(ts, h->slots);
-  k_sweep_maps<<<dim3(nsn, nsd), 256, 0, s>>>(t, factor_dev(f), reinterpret_cast<const FrontDesc*>(f.desc.p),
-                                              f.cslot.p, f.umap.p, f.gmap.p);
-  CB_LAUNCH();
-  CB_CUDA(cudaStreamSynchronize(s));  // the host vectors above are pageable and go out of scope
+  f.items_ready = true;
 }
+
 
 // In-place solve of one right-hand side X (nsd x T slot vector) in phases:
 // kSweepFwd resets the counters and runs the forward sweep; kSweepBwd the
@@ -896,6 +922,7 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
 // root level (the BDDC apply corrects the root solution in between).
 void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip, int phase) {
+  if (!f.items_ready) throw Failure(CUTBDDC_INTERNAL, "sweep: item lists not built");
   cudaStream_t s = h->stream;
   const int nsd = h->nsd, nsn = (int)ts.tpl.sn.size();
   const char* tp = trace_prefix();
@@ -940,6 +967,7 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
 void sweep_forward_multi(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const double* X, double* ysave,
                          double* upd, double* vbuf8) {
   static_assert(kMultiRhs == kSweepMultiRhs, "multi-RHS width");
+  if (!f.items_ready) throw Failure(CUTBDDC_INTERNAL, "sweep: item lists not built");
   cudaStream_t s = h->stream;
   const int nsd = h->nsd, nsn = (int)ts.tpl.sn.size();
   SweepDev p = sweep_dev(f, nsd, nsn, nullptr);

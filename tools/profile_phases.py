@@ -12,7 +12,7 @@ from paper_1703_06323_b200 import configs, cutbddc as cb  # noqa: E402
 cfg = configs.get(sys.argv[1] if len(sys.argv) > 1 else "cfg4")
 s = cb.GpuSolver(0)
 pb = cb.prepare(s, cfg)
-for _ in range(int(os.environ.get("PROFILE_REPS", "2"))):
+for _ in range(int(os.environ.get("PROFILE_REPS", "6"))):
     s.assemble(cfg.block, pb.block_ids)
     s.setup_bddc(pb.objects, cfg.weighting)
     x, rep = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
