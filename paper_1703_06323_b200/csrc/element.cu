@@ -10,7 +10,9 @@
 // (PAPER.md:315), f = 1, g = 0. A cut cell whose retained volume rule is
 // empty contributes nothing.
 // Compiled with -fmad=false: identical op order to the CPU restatement.
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "handle.cuh"
 
@@ -288,34 +290,29 @@ CB_HD int cut_element(const double q8[8], double h, double* K, double* F, double
 }
 
 // ---------------------------------------------------------------------------
-// Lane-group form of cut_element (same arithmetic, bit for bit): four cut
-// cells per warp, eight lanes per cell.
+// Two-kernel form of cut_element (same arithmetic, bit for bit).
 //
-// Lanes 0-5 of a group cut one Kuhn tet each and write its quadrature points
-// to shared memory (volume: x, y, z, w; surface: x, y, z, w, n). Every
-// accumulator of the sequential code (D, F, B, M, N: 180 unique entries) is
-// then owned by one lane, which sums its entry over the points in the
-// sequential order (tet, piece, point), so every sum sees the same operands
-// in the same order. The Q1 factors are rebuilt per point from f_d in {x_d,
-// 1 - x_d}: grad[l][0] = (+-1 * f1) * f2 = +-(f1 f2) exactly, so no product
-// differs from q1_eval. The Jacobi rotations of the 8x8 pencil run
-// lane-parallel over k (each k touches only its own row / column entries,
-// as in the sequential loops).
+// k_cut_acc, one warp per cut cell: lanes 0-5 cut one Kuhn tet each and
+// write its quadrature points to shared memory; then every accumulator of
+// the sequential code (D, F, B, M, N: 180 unique entries) is owned by one
+// lane, which sums it over the points in the sequential order (tet, piece,
+// point), so every sum sees the same operands in the same order. The Q1
+// factors are rebuilt per point from f_d in {x_d, 1 - x_d}: grad[l][0] =
+// (+-1 * f1) * f2 = +-(f1 f2) exactly, so no product differs from q1_eval.
+// The 180 sums go to global memory.
+//
+// k_cut_pencil, eight lanes per cell: beta_e from the deflated pencil
+// (gen_eigs_max) with the 8x8 matrices held in registers, lane k owning row
+// k (Jacobi rotations exchange rows by shuffles: no shared memory, so many
+// cells are in flight), then K_e and F_e.
 constexpr int kVolPts = 12;   // per tet: up to three sub-tets x 4 points
 constexpr int kSurfPts = 6;   // per tet: up to two triangles x 3 points
-constexpr int kCellWarps = 1; // warps per CTA (four cut cells per warp; shared memory bound)
+constexpr int kAccCells = 4;  // cells (warps) per CTA of k_cut_acc
+constexpr int kAcc = 180;     // accumulators per cell: 0-35 D (i <= j), 36-43 F, 44-79 B, 80-115 M (i <= j), 116-179 N
 
-struct CellSmem {
-  union {
-    struct {  // quadrature points (dead after the accumulation)
-      double vp[6][kVolPts][4];
-      double sp[6][kSurfPts][7];
-    };
-    struct {  // pencil scratch (gen_eigs_max)
-      double a[64], v[64], ev[8], bq[64], c[64], cv[64], cev[8];
-    };
-  };
-  double dr[64], br[64], mr[64], nr[64], fr[8];
+struct PointSmem {
+  double vp[6][kVolPts][4];
+  double sp[6][kSurfPts][7];
   int nv[6], ns[6];
 };
 
@@ -434,152 +431,57 @@ __device__ __forceinline__ void q1_gv(const double* x, int l, double g[3], doubl
   if (val) *val = f01 * f2;
 }
 
-// jacobi(n, a, v, ev) by a group of 8 lanes (gl = index within the group):
-// lane k owns index k of each rotation's row / column updates
-__device__ void grp_jacobi(int n, double* a, double* v, double* ev, int gl, unsigned gm) {
-  for (int k = gl; k < n * n; k += 8) v[k] = (k / n) == (k % n) ? 1.0 : 0.0;
-  __syncwarp(gm);
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0, diag = 0.0;
-    for (int i = 0; i < n; ++i) {
-      diag += a[i * n + i] * a[i * n + i];
-      for (int j = i + 1; j < n; ++j) off += a[i * n + j] * a[i * n + j];
+// accumulator `it` -> (kind, i, j): 0 D, 1 F, 2 B, 3 M, 4 N
+__device__ __forceinline__ void acc_index(int it, int& kind, int& i, int& j) {
+  if (it < 36 || (it >= 44 && it < 116)) {
+    int u = it < 36 ? it : (it - 44) % 36;
+    kind = it < 36 ? 0 : (it < 80 ? 2 : 3);
+    i = 0;
+    while (u >= 8 - i) {
+      u -= 8 - i;
+      ++i;
     }
-    if (off <= 1e-32 * diag || off < 1e-300) break;
-    for (int p = 0; p < n; ++p) {
-      for (int q = p + 1; q < n; ++q) {
-        const double apq = a[p * n + q];
-        if (apq == 0.0) continue;
-        const double app = a[p * n + p], aqq = a[q * n + q];
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(t * t + 1.0);
-        const double s = t * c;
-        __syncwarp(gm);
-        const int k = gl;
-        if (k < n) {
-          const double akp = a[k * n + p], akq = a[k * n + q];
-          a[k * n + p] = c * akp - s * akq;
-          a[k * n + q] = s * akp + c * akq;
-        }
-        __syncwarp(gm);
-        if (k < n) {
-          const double apk = a[p * n + k], aqk = a[q * n + k];
-          a[p * n + k] = c * apk - s * aqk;
-          a[q * n + k] = s * apk + c * aqk;
-          const double vkp = v[k * n + p], vkq = v[k * n + q];
-          v[k * n + p] = c * vkp - s * vkq;
-          v[k * n + q] = s * vkp + c * vkq;
-        }
-        __syncwarp(gm);
-        if (gl == 0) {
-          a[p * n + q] = 0.0;
-          a[q * n + p] = 0.0;
-        }
-        __syncwarp(gm);
-      }
-    }
+    j = i + u;
+  } else if (it < 44) {
+    kind = 1;
+    i = it - 36;
+    j = i;
+  } else {
+    kind = 4;
+    i = (it - 116) / 8;
+    j = (it - 116) % 8;
   }
-  for (int i = gl; i < n; i += 8) ev[i] = a[i * n + i];
-  __syncwarp(gm);
 }
 
-// gen_eigs_max (linalg.cpp:108-136) by a lane group: the same operations as
-// the sequential function above
-__device__ double grp_gen_eigs_max(CellSmem& S, int gl, unsigned gm) {
-  for (int i = gl; i < 64; i += 8) S.a[i] = S.dr[i];
-  __syncwarp(gm);
-  grp_jacobi(8, S.a, S.v, S.ev, gl, gm);
-  double lmax = S.ev[0];
-  for (int i = 1; i < 8; ++i) lmax = fmax(lmax, S.ev[i]);
-  if (!(lmax > 0.0)) return -1.0;
-  int m = 0;
-  int keep[8];
-  for (int k = 0; k < 8; ++k)
-    if (S.ev[k] >= 1e-12 * lmax) keep[m++] = k;
-  for (int e = gl; e < 8 * m; e += 8) {
-    const int i = e / m, k = e % m;
-    double s = 0;
-    for (int j = 0; j < 8; ++j) s += S.br[i * 8 + j] * S.v[j * 8 + keep[k]];
-    S.bq[i * m + k] = s;
-  }
-  __syncwarp(gm);
-  for (int e = gl; e < m * m; e += 8) {
-    const int k = e / m, l = e % m;
-    double s = 0;
-    for (int i = 0; i < 8; ++i) s += S.v[i * 8 + keep[k]] * S.bq[i * m + l];
-    S.c[k * m + l] = s / (sqrt(S.ev[keep[k]]) * sqrt(S.ev[keep[l]]));
-  }
-  __syncwarp(gm);
-  for (int e = gl; e < m * m; e += 8) {
-    const int k = e / m, l = e % m;
-    S.a[k * m + l] = l == k ? S.c[k * m + k] : 0.5 * (S.c[min(k, l) * m + max(k, l)] + S.c[max(k, l) * m + min(k, l)]);
-  }
-  __syncwarp(gm);
-  grp_jacobi(m, S.a, S.cv, S.cev, gl, gm);
-  double best = S.cev[0];
-  for (int k = 1; k < m; ++k) best = fmax(best, S.cev[k]);
-  return best;
-}
-
-// four cut cells per warp, eight lanes per cell
-__global__ void __launch_bounds__(32 * kCellWarps) k_cut_elements_warp(double h, int64_t ncut,
-                                                                       const double* __restrict__ q8all,
-                                                                       double* __restrict__ ke, double* __restrict__ fe,
-                                                                       double* __restrict__ beta,
-                                                                       uint8_t* __restrict__ empty,
-                                                                       int* __restrict__ degenerate) {
-  __shared__ CellSmem smem[4 * kCellWarps];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 3, gl = lane & 7;
-  const unsigned gm = 0xffu << (8 * g);
-  const int64_t e = ((int64_t)blockIdx.x * kCellWarps + wid) * 4 + g;
+__global__ void __launch_bounds__(32 * kAccCells) k_cut_acc(int64_t ncut, const double* __restrict__ q8all,
+                                                             double* __restrict__ accs, int* __restrict__ nvs) {
+  __shared__ PointSmem smem[kAccCells];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * kAccCells + wid;
   if (e >= ncut) return;
-  CellSmem& S = smem[4 * wid + g];
-  const double* q8 = q8all + e * 8;
-  if (gl < 6) {
-    PtList L{S.vp[gl], S.sp[gl], 0, 0};
+  PointSmem& S = smem[wid];
+  if (lane < 6) {
+    PtList L{S.vp[lane], S.sp[lane], 0, 0};
     double q[8];
-    for (int i = 0; i < 8; ++i) q[i] = q8[i];
-    tet_points(gl, q, L);
-    S.nv[gl] = L.nv;
-    S.ns[gl] = L.ns;
+    for (int i = 0; i < 8; ++i) q[i] = q8all[e * 8 + i];
+    tet_points(lane, q, L);
+    S.nv[lane] = L.nv;
+    S.ns[lane] = L.ns;
   }
-  __syncwarp(gm);
+  __syncwarp();
   int nvol = 0, nsurf = 0;
   for (int t = 0; t < 6; ++t) {
     nvol += S.nv[t];
     nsurf += S.ns[t];
   }
-  if (nvol == 0) {
-    for (int t = gl; t < 64; t += 8) ke[e * 64 + t] = 0.0;
-    fe[e * 8 + gl] = 0.0;
-    if (gl == 0) {
-      beta[e] = 0.0;
-      empty[e] = 1;
-    }
-    return;
+  if (lane == 0) {
+    nvs[2 * e] = nvol;
+    nvs[2 * e + 1] = nsurf;
   }
-  // accumulators: 0-35 D (i <= j), 36-43 F, 44-79 B (i <= j), 80-115 M (i <= j), 116-179 N
-  for (int it = gl; it < 180; it += 8) {
+  if (nvol == 0) return;
+  for (int it = lane; it < kAcc; it += 32) {
     int kind, i, j;
-    if (it < 36 || (it >= 44 && it < 116)) {
-      int u = it < 36 ? it : (it - 44) % 36;
-      kind = it < 36 ? 0 : (it < 80 ? 2 : 3);
-      i = 0;
-      while (u >= 8 - i) {
-        u -= 8 - i;
-        ++i;
-      }
-      j = i + u;
-    } else if (it < 44) {
-      kind = 1;
-      i = it - 36;
-      j = i;
-    } else {
-      kind = 4;
-      i = (it - 116) / 8;
-      j = (it - 116) % 8;
-    }
+    acc_index(it, kind, i, j);
     double acc = 0.0;
     if (kind <= 1) {
       for (int t = 0; t < 6; ++t)
@@ -615,36 +517,199 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_cut_elements_warp(double h,
           }
         }
     }
-    if (kind == 0) {
-      S.dr[i * 8 + j] = acc;
-      S.dr[j * 8 + i] = acc;
-    } else if (kind == 1) {
-      S.fr[i] = acc;
-    } else if (kind == 2) {
-      S.br[i * 8 + j] = acc;
-      S.br[j * 8 + i] = acc;
-    } else if (kind == 3) {
-      S.mr[i * 8 + j] = acc;
-      S.mr[j * 8 + i] = acc;
-    } else {
-      S.nr[i * 8 + j] = acc;
-    }
+    accs[e * kAcc + it] = acc;
   }
-  __syncwarp(gm);
+}
+
+__device__ __forceinline__ double gsh(double v, int src, unsigned gm) { return __shfl_sync(gm, v, src, 8); }
+// r[idx] with a runtime idx (no local-memory array)
+__device__ __forceinline__ double sel8(const double (&r)[8], int idx) {
+  double x = r[0];
+#pragma unroll
+  for (int j = 1; j < 8; ++j) x = idx == j ? r[j] : x;
+  return x;
+}
+// packed-upper index of (i, j), i <= j, in the D / B / M accumulator blocks
+__device__ __forceinline__ int tri(int i, int j) { return i * 8 - i * (i - 1) / 2 + (j - i); }
+
+// jacobi(n, a, v, ev) by the 8 lanes of a group, lane k holding row k of a
+// and of v in registers: the column update of a rotation is lane-local, the
+// row update exchanges rows p and q by shuffles. The operations and their
+// order are jacobi's (every update reads the same operands). The (p, q)
+// loops are unrolled so every register index is a compile-time constant
+// (measured: the rolled form with select chains is 10-60% slower).
+__device__ void reg_jacobi(int n, double (&a)[8], double (&v)[8], int gl, unsigned gm) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = j == gl ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, diag = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double aii = gsh(a[i], i, gm);
+      if (i < n) diag += aii * aii;
+#pragma unroll
+      for (int j = i + 1; j < 8; ++j) {
+        const double aij = gsh(a[j], i, gm);
+        if (j < n) off += aij * aij;
+      }
+    }
+    if (off <= 1e-32 * diag || off < 1e-300) break;
+#pragma unroll
+    for (int p = 0; p < 7; ++p)
+#pragma unroll
+      for (int q = p + 1; q < 8; ++q) {
+        if (q >= n) continue;  // n is uniform over the group
+        const double apq = gsh(a[q], p, gm);
+        if (apq == 0.0) continue;
+        const double app = gsh(a[p], p, gm), aqq = gsh(a[q], q, gm);
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0);
+        const double s = t * c;
+        if (gl < n) {  // column update, row k = gl
+          const double akp = a[p], akq = a[q];
+          a[p] = c * akp - s * akq;
+          a[q] = s * akp + c * akq;
+        }
+        double rp[8], rq[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          rp[j] = gsh(a[j], p, gm);
+          rq[j] = gsh(a[j], q, gm);
+        }
+        if (gl == p) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < n) a[j] = c * rp[j] - s * rq[j];
+          a[q] = 0.0;
+        } else if (gl == q) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < n) a[j] = s * rp[j] + c * rq[j];
+          a[p] = 0.0;
+        }
+        if (gl < n) {
+          const double vkp = v[p], vkq = v[q];
+          v[p] = c * vkp - s * vkq;
+          v[q] = s * vkp + c * vkq;
+        }
+      }
+  }
+}
+
+// gen_eigs_max (linalg.cpp:108-136) by a lane group with register rows: the
+// same operations as the sequential function above. d, b: row gl.
+__device__ double reg_gen_eigs_max(const double (&d)[8], const double (&b)[8], int gl, unsigned gm) {
+  double a[8], v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = d[j];
+  reg_jacobi(8, a, v, gl, gm);
+  double ev[8];
+  const double evk = sel8(a, gl);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ev[i] = gsh(evk, i, gm);
+  double lmax = ev[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) lmax = fmax(lmax, ev[i]);
+  if (!(lmax > 0.0)) return -1.0;
+  int keep[8], m = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (ev[k] >= 1e-12 * lmax) keep[m++] = k;
+  // bq row gl: bq[gl][k] = sum_j b[gl][j] v[j][keep[k]]
+  double bq[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int kk = k < m ? keep[k] : 0;
+    const double mine = sel8(v, kk);  // v[gl][keep[k]], sent to every lane below
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += b[j] * gsh(mine, j, gm);
+    bq[k] = s;
+  }
+  // c row gl (gl < m): c[gl][l] = sum_i v[i][keep[gl]] bq[i][l] / (sqrt(ev[keep[gl]]) sqrt(ev[keep[l]]))
+  const int kg = gl < m ? keep[gl] : 0;
+  double cs[8];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) cs[l] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double vi[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) vi[j] = gsh(v[j], i, gm);
+    const double vik = sel8(vi, kg);
+#pragma unroll
+    for (int l = 0; l < 8; ++l) cs[l] += vik * gsh(bq[l], i, gm);
+  }
+  const double ek = sel8(ev, kg);
+  double c[8];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) c[l] = cs[l] / (sqrt(ek) * sqrt(ev[l < m ? keep[l] : 0]));
+  // symmetrise: (k, l), k != l: 0.5 (c[min][max] + c[max][min])
+  double a2[8];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    double crow[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) crow[j] = gsh(c[j], l, gm);
+    const double clk = sel8(crow, gl);  // c[l][gl]
+    a2[l] = l == gl ? c[l] : (gl < l ? 0.5 * (c[l] + clk) : 0.5 * (clk + c[l]));
+  }
+  double cv[8];
+  reg_jacobi(m, a2, cv, gl, gm);
+  const double ck = sel8(a2, gl);
+  double best = gsh(ck, 0, gm);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {
+    const double x = gsh(ck, k, gm);
+    if (k < m) best = fmax(best, x);
+  }
+  return best;
+}
+
+// eight lanes per cut cell: beta_e, K_e = h (D + beta M - N - N^T), F_e = h^3 F
+__global__ void __launch_bounds__(256) k_cut_pencil(double h, int64_t ncut, const double* __restrict__ accs,
+                                                     const int* __restrict__ nvs, double* __restrict__ ke,
+                                                     double* __restrict__ fe, double* __restrict__ beta,
+                                                     uint8_t* __restrict__ empty, int* __restrict__ degenerate) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, gl = lane & 7;
+  const unsigned gm = 0xffu << (8 * g);
+  const int64_t e = (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) / 8;
+  if (e >= ncut) return;  // whole groups: ncut cells x 8 lanes
+  const int nvol = nvs[2 * e], nsurf = nvs[2 * e + 1];
+  if (nvol == 0) {
+    for (int t = gl; t < 64; t += 8) ke[e * 64 + t] = 0.0;
+    fe[e * 8 + gl] = 0.0;
+    if (gl == 0) {
+      beta[e] = 0.0;
+      empty[e] = 1;
+    }
+    return;
+  }
+  const double* A = accs + e * kAcc;
+  double d[8], b[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int i0 = gl < j ? gl : j, j0 = gl < j ? j : gl;
+    d[j] = A[tri(i0, j0)];
+    b[j] = A[44 + tri(i0, j0)];
+  }
   double lambda = 0.0;
   if (nsurf > 0) {
-    lambda = grp_gen_eigs_max(S, gl, gm);
+    lambda = reg_gen_eigs_max(d, b, gl, gm);
     if (lambda < 0) {
       if (gl == 0) atomicExch(degenerate, 1);
       lambda = 0.0;
     }
   }
   const double betar = 2.0 * lambda;
-  for (int t = gl; t < 64; t += 8) {
-    const int x = t / 8, y = t % 8;
-    ke[e * 64 + t] = h * (S.dr[x * 8 + y] + betar * S.mr[x * 8 + y] - (S.nr[x * 8 + y] + S.nr[y * 8 + x]));
+#pragma unroll
+  for (int y = 0; y < 8; ++y) {
+    const int i0 = gl < y ? gl : y, j0 = gl < y ? y : gl;
+    const double mxy = A[80 + tri(i0, j0)];
+    ke[e * 64 + gl * 8 + y] = h * (d[y] + betar * mxy - (A[116 + gl * 8 + y] + A[116 + y * 8 + gl]));
   }
-  fe[e * 8 + gl] = h * h * h * S.fr[gl];
+  fe[e * 8 + gl] = h * h * h * A[36 + gl];
   if (gl == 0) {
     beta[e] = betar / h;
     empty[e] = 0;
@@ -710,16 +775,25 @@ void cut_elements_device(cutbddc_gpu* h) {
   if (h->n_cut > 0) {
     DevBuf<double>& q8all = h->ws_q8;
     q8all.alloc((size_t)h->n_cut * 8);
+
     k_gather_q8<<<grid_for(h->n_cut, 256), 256, 0, h->stream>>>(h->n, h->n_cut, h->cut_cells.p, h->phi.p, q8all.p);
     CB_LAUNCH();
-    if (std::getenv("CUTBDDC_CUT_THREAD"))  // the thread-per-cell form (A/B reference)
+    if (std::getenv("CUTBDDC_CUT_THREAD")) {  // the thread-per-cell form (A/B reference)
       k_cut_elements<<<grid_for(h->n_cut, 64), 64, 0, h->stream>>>(h->h, h->n_cut, q8all.p, h->ke.p, h->fe.p,
                                                                     h->beta.p, h->empty.p, degen.p);
-    else
-      k_cut_elements_warp<<<(unsigned)((h->n_cut + 4 * kCellWarps - 1) / (4 * kCellWarps)), 32 * kCellWarps, 0,
-                            h->stream>>>(
-          h->h, h->n_cut, q8all.p, h->ke.p, h->fe.p, h->beta.p, h->empty.p, degen.p);
-    CB_LAUNCH();
+      CB_LAUNCH();
+    } else {
+      DevBuf<double>& accs = h->ws_acc;
+      DevBuf<int>& nvs = h->ws_nvs;
+      accs.alloc((size_t)h->n_cut * kAcc);
+      nvs.alloc((size_t)h->n_cut * 2);
+      k_cut_acc<<<(unsigned)((h->n_cut + kAccCells - 1) / kAccCells), 32 * kAccCells, 0, h->stream>>>(
+          h->n_cut, q8all.p, accs.p, nvs.p);
+      CB_LAUNCH();
+      k_cut_pencil<<<(unsigned)((h->n_cut * 8 + 255) / 256), 256, 0, h->stream>>>(
+          h->h, h->n_cut, accs.p, nvs.p, h->ke.p, h->fe.p, h->beta.p, h->empty.p, degen.p);
+      CB_LAUNCH();
+    }
   }
   int dg = 0;
   CB_CUDA(cudaMemcpyAsync(&dg, degen.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));

@@ -243,6 +243,8 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<unsigned int> ws_omask;
   cutbddc_b200::DevBuf<uint8_t> ws_act, ws_cut, ws_tmp, ws_obj;
   cutbddc_b200::DevBuf<double> ws_w8;             // device objects v2: weight tuples (8 per dof)
+  cutbddc_b200::DevBuf<double> ws_acc;            // cut cells: the 180 quadrature sums per cell (element.cu)
+  cutbddc_b200::DevBuf<int> ws_nvs;
   cutbddc_b200::DevBuf<int> ws_flag;
   cutbddc_b200::DevBuf<int32_t> ws_coff;                       // corner coarse basis: front column offsets
   cutbddc_b200::DevBuf<double> ws_x8, ws_y8, ws_u8, ws_v8;      // multi-RHS forward sweep vectors
