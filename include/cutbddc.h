@@ -249,6 +249,18 @@ cutbddc_status cutbddc_nccl_unique_id(void* id128);
 cutbddc_status cutbddc_gpu_set_distribution(cutbddc_gpu* h, const cutbddc_partition_view* part,
                                             const int32_t* rank_of_sd, int rank, int world);
 
+/* Problem data of the load vector: the BASELINE runs use
+ * f = 1 and g^D = 0 (CUTBDDC_PROBLEM_UNIT_LOAD, the default);
+ * CUTBDDC_PROBLEM_MANUFACTURED is manufactured(u-case) with u =
+ * sin(5 pi |x|) (§5.1): f = -lap u, g^D = u on the embedded
+ * boundary through the Nitsche terms. Set before cutbddc_gpu_assemble. */
+enum { CUTBDDC_PROBLEM_UNIT_LOAD = 0, CUTBDDC_PROBLEM_MANUFACTURED = 1 };
+cutbddc_status cutbddc_gpu_set_problem(cutbddc_gpu* h, int problem);
+/* error_norms of the manufactured problem: |u_h - u|_L2
+ * and the H1 seminorm |u_h - u|_H1 over the cut-aware volume rules. x:
+ * global-numbered nodal values (NULL: the last PCG solution). Collective. */
+cutbddc_status cutbddc_gpu_error_norms(cutbddc_gpu* h, const double* x, double* l2, double* h1);
+
 /* Interface exchange plan of one rank (dist.cu builds it on the device;
  * cutbddc_build_exchange_plan builds the same plan on the host):
  *   local dofs: loc_glob[n_loc] global dof ids, segment by segment — the

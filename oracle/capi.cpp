@@ -47,6 +47,7 @@ struct orc_config {
   int n_balls;
   const double* balls;  // 4 doubles per ball: cx, cy, cz, r
   int threads;
+  int problem;          // 0: f = 1, g = 0; 1: manufactured u = sin(5 pi |x|)
 };
 
 const char* orc_last_error() { return g_err.c_str(); }
@@ -65,6 +66,7 @@ int orc_create(const orc_config* cfg, void** out) {
       h->pb.geom.balls.push_back({cfg->balls[4 * i], cfg->balls[4 * i + 1], cfg->balls[4 * i + 2], cfg->balls[4 * i + 3]});
     double t0 = now();
     h->pb.mesh = classify(h->pb.params, h->pb.geom);
+    h->pb.mesh.problem = cfg->problem;
     double t1 = now();
     h->t_classify = t1 - t0;
     if (cfg->block > 0) {
@@ -175,6 +177,13 @@ int orc_cut_rule(const double* phiv, int full, double* vol, int vol_cap, double*
 
 int orc_gen_eigs(const double* b, const double* d, int n, double tol, double* out) {
   return guard([&] { *out = dense_generalized_eigs_max(b, d, n, tol); });
+}
+
+int orc_error_norms(void* hv, const double* x, double* out) {
+  return guard([&] {
+    auto* h = static_cast<Handle*>(hv);
+    error_norms(h->pb.mesh, x, out, out + 1);
+  });
 }
 
 int orc_rhs(void* hv, double* b) {

@@ -135,13 +135,25 @@ Element element_matrix(const Mesh& m, std::int64_t cell) {
     e.empty = true;
     return e;
   }
-  double dr[64] = {0}, br[64] = {0}, mr[64] = {0}, nr[64] = {0}, fr[8] = {0};
+  double dr[64] = {0}, br[64] = {0}, mr[64] = {0}, nr[64] = {0}, fr[8] = {0}, g1[8] = {0}, g2[8] = {0};
   double val[8], grad[8][3];
+  const bool mms = m.problem == kProblemManufactured;
+  int cc[3];
+  m.cell_coords(cell, cc);
+  auto phys = [&](const double* xi, double x[3]) {  // origin + (cell + xi) h
+    for (int d = 0; d < 3; ++d) x[d] = m.origin[d] + ((double)cc[d] + xi[d]) * h;
+  };
   for (const auto& p : rule.vol) {
     const double xi[3] = {p[0], p[1], p[2]};
     q1_eval(xi, val, grad);
+    double fx = 1.0;
+    if (mms) {
+      double x[3];
+      phys(xi, x);
+      fx = Manufactured::f(x);
+    }
     for (int a = 0; a < 8; ++a) {
-      fr[a] += p[3] * val[a];
+      fr[a] += mms ? p[3] * (fx * val[a]) : p[3] * val[a];
       for (int b = 0; b < 8; ++b)
         dr[a * 8 + b] += p[3] * (grad[a][0] * grad[b][0] + grad[a][1] * grad[b][1] + grad[a][2] * grad[b][2]);
     }
@@ -153,6 +165,15 @@ Element element_matrix(const Mesh& m, std::int64_t cell) {
       q1_eval(xi, val, grad);
       double gn[8];
       for (int a = 0; a < 8; ++a) gn[a] = p[4] * grad[a][0] + p[5] * grad[a][1] + p[6] * grad[a][2];
+      if (mms) {  // Nitsche load: beta g phi_a - g n.grad phi_a, g = u on the boundary
+        double x[3];
+        phys(xi, x);
+        const double gx = Manufactured::u(x);
+        for (int a = 0; a < 8; ++a) {
+          g1[a] += p[3] * (gx * val[a]);
+          g2[a] += p[3] * (gx * gn[a]);
+        }
+      }
       for (int a = 0; a < 8; ++a)
         for (int b = 0; b < 8; ++b) {
           br[a * 8 + b] += p[3] * (gn[a] * gn[b]);
@@ -166,10 +187,52 @@ Element element_matrix(const Mesh& m, std::int64_t cell) {
   for (int a = 0; a < 8; ++a)
     for (int b = 0; b < 8; ++b)
       e.k[a * 8 + b] = h * (dr[a * 8 + b] + betar * mr[a * 8 + b] - (nr[a * 8 + b] + nr[b * 8 + a]));
-  for (int a = 0; a < 8; ++a) e.f[a] = h * h * h * fr[a];
+  for (int a = 0; a < 8; ++a) e.f[a] = mms ? h * h * h * fr[a] + h * (betar * g1[a] - g2[a]) : h * h * h * fr[a];
   e.beta = betar / h;
   e.empty = false;
   return e;
+}
+
+void error_norms(const Mesh& m, const double* x, double* l2, double* h1) {
+  const double h = m.h[0];
+  double el2 = 0.0, eh1 = 0.0;
+  for (std::int64_t cell : m.active) {  // ascending cell id, sequential sums
+    std::int64_t nodes[8];
+    m.cell_nodes(cell, nodes);
+    double phiv[8], uh[8];
+    for (int l = 0; l < 8; ++l) {
+      phiv[l] = m.phi[(size_t)nodes[l]];
+      const std::int32_t d = m.dof_of_node[(size_t)nodes[l]];
+      uh[l] = d >= 0 ? x[d] : 0.0;
+    }
+    const CutRule rule = m.cls[(size_t)cell] == kCut ? cut_quadrature_ref(phiv) : full_quadrature_ref();
+    int cc[3];
+    m.cell_coords(cell, cc);
+    double val[8], grad[8][3];
+    for (const auto& p : rule.vol) {
+      const double xi[3] = {p[0], p[1], p[2]};
+      q1_eval(xi, val, grad);
+      double xp[3];
+      for (int d = 0; d < 3; ++d) xp[d] = m.origin[d] + ((double)cc[d] + xi[d]) * h;
+      double v = 0.0, g[3] = {0.0, 0.0, 0.0}, gu[3];
+      for (int l = 0; l < 8; ++l) {
+        v += uh[l] * val[l];
+        for (int d = 0; d < 3; ++d) g[d] += uh[l] * grad[l][d];
+      }
+      Manufactured::grad(xp, gu);
+      const double e = v - Manufactured::u(xp);
+      const double w = p[3] * (h * h * h);
+      el2 += w * (e * e);
+      double s = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        const double ed = g[d] / h - gu[d];
+        s += ed * ed;
+      }
+      eh1 += w * s;
+    }
+  }
+  *l2 = std::sqrt(el2);
+  *h1 = std::sqrt(eh1);
 }
 
 }  // namespace oracle

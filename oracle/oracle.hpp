@@ -24,6 +24,8 @@
 // parity is "pinned to SPEC known answers", not to reference outputs.
 #pragma once
 
+#include <cmath>
+
 #include <array>
 #include <cstdint>
 #include <stdexcept>
@@ -77,7 +79,26 @@ struct MeshParams {
 
 enum : std::uint8_t { kInterior = 0, kExterior = 1, kCut = 2 };
 
+// Problem data: 0 = the BASELINE runs (f = 1, g^D = 0);
+// 1 = manufactured(u-case), u = sin(5 pi |x|) (§5.1), f = -lap u,
+// g^D = u on the embedded boundary (Nitsche terms in the load vector).
+enum : int { kProblemUnitLoad = 0, kProblemManufactured = 1 };
+struct Manufactured {
+  static double r(const double x[3]) { return std::sqrt((x[0] * x[0] + x[1] * x[1]) + x[2] * x[2]); }
+  static double u(const double x[3]) { return std::sin(5.0 * M_PI * r(x)); }
+  // f = -(u'' + 2 u' / r), u' = 5 pi cos(5 pi r), u'' = -25 pi^2 sin(5 pi r)
+  static double f(const double x[3]) {
+    const double rr = r(x);
+    return 25.0 * M_PI * M_PI * std::sin(5.0 * M_PI * rr) - 10.0 * M_PI * std::cos(5.0 * M_PI * rr) / rr;
+  }
+  static void grad(const double x[3], double g[3]) {
+    const double rr = r(x), c = 5.0 * M_PI * std::cos(5.0 * M_PI * rr) / rr;
+    for (int d = 0; d < 3; ++d) g[d] = c * x[d];
+  }
+};
+
 struct Mesh {
+  int problem = kProblemUnitLoad;
   int n[3] = {0, 0, 0};
   double origin[3] = {0, 0, 0};
   double h[3] = {0, 0, 0};
@@ -125,6 +146,9 @@ struct Element {
 double dense_generalized_eigs_max(const double* b, const double* d, int n, double kernel_tol = 1e-12);
 void jacobi_eigs(int n, double* a, double* v, double* ev);
 Element element_matrix(const Mesh& m, std::int64_t cell);
+// error_norms: |u_h - u|_L2 and |u_h - u|_H1 (seminorm)
+// over the same cut-aware volume rules; x = nodal values per dof.
+void error_norms(const Mesh& m, const double* x, double* l2, double* h1);
 
 // ---------------------------------------------------------------- sparse
 struct Csr {

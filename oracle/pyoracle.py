@@ -32,6 +32,7 @@ class _Cfg(C.Structure):
         ("n_balls", C.c_int),
         ("balls", C.POINTER(C.c_double)),
         ("threads", C.c_int),
+        ("problem", C.c_int),
     ]
 
 
@@ -80,6 +81,7 @@ class Oracle:
         c.n_balls = len(cfg.balls)
         c.balls = _p(balls, D)
         c.threads = threads or os.cpu_count() or 1
+        c.problem = getattr(cfg, "problem", 0)
         self._balls = balls
         h = C.c_void_p()
         _check(L.orc_create(C.byref(c), C.byref(h)))
@@ -213,6 +215,13 @@ class Oracle:
         z = np.zeros(self.n_dof)
         _check(lib().orc_apply(self.h, _p(r, D), _p(z, D)))
         return z
+
+    def error_norms(self, x):
+        """(|u_h - u|_L2, |u_h - u|_H1) of the manufactured solution."""
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.zeros(2)
+        _check(lib().orc_error_norms(self.h, _p(x, D), _p(out, D)))
+        return float(out[0]), float(out[1])
 
     def pcg(self, b=None, rtol=None, max_iter=None, precond=True):
         b = self.rhs() if b is None else np.ascontiguousarray(b, np.float64)

@@ -112,6 +112,7 @@ class Config:
     lo: tuple = (0.0, 0.0, 0.0)
     hi: tuple = (1.0, 1.0, 1.0)
     translation: tuple = (0.0, 0.0, 0.0)
+    problem: int = 0  # 0: f = 1, g^D = 0 (BASELINE runs); 1: manufactured u = sin(5 pi |x|)
     extra: dict = field(default_factory=dict)
 
     def with_(self, **kw) -> "Config":

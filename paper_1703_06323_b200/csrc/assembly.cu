@@ -17,6 +17,7 @@
 #include "comm.cuh"
 #include "dist.cuh"
 #include "handle.cuh"
+#include "mms.cuh"
 
 namespace cutbddc_b200 {
 
@@ -61,6 +62,8 @@ __global__ void k_sd_of_block(int nsd, const int64_t* __restrict__ bids, int32_t
 
 struct MeshArgs {
   int n, B, nb, T;
+  int problem;          // kProblemManufactured: interior-cell loads from f at the Gauss points
+  double ox, oy, oz, h;
   const int32_t* eoc;
   const int32_t* dof_of_node;
   const int64_t* node_of_dof;
@@ -88,6 +91,23 @@ __device__ inline const double* elem_k(const MeshArgs& m, int64_t cell, const do
 
 // per dof: |neigh| (distinct blocks among incident active cells, every
 // rank's) and the orphan flag (every incident active cell void)
+// load of an interior cell at its local node lv, manufactured problem: the
+// 2x2x2 Gauss rule (full_quadrature_ref), h^3 sum_g 1/8 (f(x_g) phi_lv(xi_g))
+__device__ double interior_mms_load(const MeshArgs& m, int ci, int cj, int ck, int lv) {
+  const double g0 = 0.5 - 0.5 / sqrt(3.0), g1 = 0.5 + 0.5 / sqrt(3.0);
+  double s = 0.0;
+  for (int l = 0; l < 8; ++l) {
+    const double xi[3] = {(l & 1) ? g1 : g0, ((l >> 1) & 1) ? g1 : g0, ((l >> 2) & 1) ? g1 : g0};
+    double f[3];
+    for (int d = 0; d < 3; ++d) f[d] = ((lv >> d) & 1) ? xi[d] : 1.0 - xi[d];
+    const double val = f[0] * f[1] * f[2];
+    const double fx = mms_f(m.ox + ((double)ci + xi[0]) * m.h, m.oy + ((double)cj + xi[1]) * m.h,
+                            m.oz + ((double)ck + xi[2]) * m.h);
+    s += 0.125 * (fx * val);
+  }
+  return m.h * m.h * m.h * s;
+}
+
 __global__ void k_dof_info(int64_t ndof, MeshArgs m, const uint8_t* __restrict__ vcell, uint8_t* __restrict__ ncount,
                            uint8_t* __restrict__ orphan) {
   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -147,7 +167,9 @@ __global__ void k_subassemble(int nsd, MeshArgs m, const int64_t* __restrict__ b
         const double* K = elem_k(m, cell, &f);
         if (!K) continue;
         const int lv = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
-        bb += f[lv];
+        bb += (m.problem == kProblemManufactured && m.eoc[cell] == -1)
+                  ? interior_mms_load(m, bi * m.B + cx, bj * m.B + cy, bk * m.B + cz, lv)
+                  : f[lv];
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
           const int q = stencil_k((w & 1) - (lv & 1), ((w >> 1) & 1) - ((lv >> 1) & 1), ((w >> 2) & 1) - ((lv >> 2) & 1));
@@ -267,8 +289,9 @@ void assemble_device(cutbddc_gpu* h, const cutbddc_partition_view* part) {
   const bool plan_only = h->dist_world > 1 && !h->comm;
   if (h->dist_world > 1 && !plan_only)
     nccl_check(ncclAllReduce(h->vcell.p, h->vcell.p, (size_t)nc, ncclUint8, ncclMax, h->comm, s), "void cells");
-  MeshArgs m{n, block, h->nb, h->slots, h->elem_of_cell.p, h->dof_of_node.p, h->node_of_dof.p,
-             h->ke.p, h->fe.p, h->empty.p, kint.p, kint.p + 64, h->sd_of_block.p};
+  MeshArgs m{n,          block,         h->nb,         h->slots,      h->problem,      h->origin[0],
+             h->origin[1], h->origin[2], h->h,          h->elem_of_cell.p, h->dof_of_node.p, h->node_of_dof.p,
+             h->ke.p,      h->fe.p,       h->empty.p,    kint.p,        kint.p + 64,     h->sd_of_block.p};
   const int64_t nd = h->n_dof;
   h->ncount.alloc((size_t)nd);
   h->orphan.alloc((size_t)nd);

@@ -13,6 +13,8 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
 // rz_part: when not null, per-subdomain partials of r.z (gathered layout, dist.cuh)
 void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* skip, double* rz_part = nullptr);
 void spmv_device(cutbddc_gpu* h, const double* x, double* y);
+// squared error norms of the manufactured solution over this rank's cells (element.cu)
+void error_norms_device(cutbddc_gpu* h, const double* xloc, double* l2sq, double* h1sq);
 // b_loc, h->px: local dof vectors (dist.cuh)
 void pcg_device(cutbddc_gpu* h, const double* b_loc, double rtol, int max_iter, cutbddc_solve_report* rep);
 

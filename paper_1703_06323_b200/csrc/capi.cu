@@ -1,6 +1,7 @@
 // capi.cu — the extern "C" boundary declared in include/cutbddc.h.
 // Every entry point converts Failure / CUDA errors into cutbddc_status
 // (common.hpp:22-23: "the C boundary maps `code` onto cutbddc_status values").
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -111,6 +112,32 @@ cutbddc_status cutbddc_nccl_unique_id(void* id128) {
   });
 }
 
+// boundary vectors (global numbering) <-> the handle's local dof space
+namespace {
+void host_to_local(cutbddc_gpu* h, const double* x, DevBuf<double>& loc) {
+  DevBuf<double> g;
+  g.upload(x, (size_t)h->n_dof, h->stream);
+  loc.alloc((size_t)std::max<int64_t>(1, h->n_loc));
+  to_local(h, g.p, loc.p);
+  CB_CUDA(cudaStreamSynchronize(h->stream));
+}
+// owned entries into the caller's n_dof buffer (others untouched)
+void local_to_host(cutbddc_gpu* h, const double* loc, double* x) {
+  DevBuf<double> g;
+  if (h->n_own == h->n_dof) {
+    g.alloc((size_t)h->n_dof);
+  } else {
+    g.upload(x, (size_t)h->n_dof, h->stream);
+  }
+  to_global_owned(h, loc, g.p);
+  g.download(x, (size_t)h->n_dof, h->stream);
+  CB_CUDA(cudaStreamSynchronize(h->stream));
+}
+void need_numeric(cutbddc_gpu* h) {
+  if (h->plan_only) throw Failure(CUTBDDC_CONFIG, "plan-only distribution (no communicator): no numerical calls");
+}
+}  // namespace
+
 cutbddc_status cutbddc_gpu_set_distribution(cutbddc_gpu* h, const cutbddc_partition_view* part,
                                             const int32_t* rank_of_sd, int rank, int world) {
   return guard([&] {
@@ -120,6 +147,52 @@ cutbddc_status cutbddc_gpu_set_distribution(cutbddc_gpu* h, const cutbddc_partit
     dist_set(h, part, rank_of_sd, rank, world);
     h->assembled = false;
     h->bddc_ready = false;
+  });
+}
+
+cutbddc_status cutbddc_gpu_set_problem(cutbddc_gpu* h, int problem) {
+  return guard([&] {
+    need(h);
+    if (problem != CUTBDDC_PROBLEM_UNIT_LOAD && problem != CUTBDDC_PROBLEM_MANUFACTURED)
+      throw Failure(CUTBDDC_CONFIG, "problem must be the unit load or the manufactured solution");
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->problem = problem;
+    h->assembled = false;
+    h->bddc_ready = false;
+  });
+}
+
+cutbddc_status cutbddc_gpu_error_norms(cutbddc_gpu* h, const double* x, double* l2, double* h1) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->assembled) throw Failure(CUTBDDC_INVALID_ARGUMENT, "error norms: assemble first");
+    if (h->problem != CUTBDDC_PROBLEM_MANUFACTURED)
+      throw Failure(CUTBDDC_CONFIG, "error norms: the problem has no exact solution (set the manufactured problem)");
+    need_numeric(h);
+    DevBuf<double> xl;
+    const double* xp = h->px.p;
+    if (x) {
+      host_to_local(h, x, xl);
+      xp = xl.p;
+    } else if (!xp || h->px.n < (size_t)h->n_loc) {
+      throw Failure(CUTBDDC_INVALID_ARGUMENT, "error norms: no solution (pass x or solve first)");
+    }
+    double a = 0.0, b = 0.0;
+    error_norms_device(h, xp, &a, &b);
+    if (h->comm && h->dist_world > 1) {  // every rank's cells
+      DevBuf<double> t;
+      const double ab[2] = {a, b};
+      t.upload(ab, 2, h->stream);
+      nccl_check(ncclAllReduce(t.p, t.p, 2, ncclDouble, ncclSum, h->comm, h->stream), "error norms");
+      double r[2];
+      t.download(r, 2, h->stream);
+      CB_CUDA(cudaStreamSynchronize(h->stream));
+      a = r[0];
+      b = r[1];
+    }
+    if (l2) *l2 = std::sqrt(a);
+    if (h1) *h1 = std::sqrt(b);
   });
 }
 
@@ -274,31 +347,6 @@ cutbddc_status cutbddc_gpu_setup_bddc(cutbddc_gpu* h, const cutbddc_coarse_view*
   });
 }
 
-// boundary vectors (global numbering) <-> the handle's local dof space
-namespace {
-void host_to_local(cutbddc_gpu* h, const double* x, DevBuf<double>& loc) {
-  DevBuf<double> g;
-  g.upload(x, (size_t)h->n_dof, h->stream);
-  loc.alloc((size_t)std::max<int64_t>(1, h->n_loc));
-  to_local(h, g.p, loc.p);
-  CB_CUDA(cudaStreamSynchronize(h->stream));
-}
-// owned entries into the caller's n_dof buffer (others untouched)
-void local_to_host(cutbddc_gpu* h, const double* loc, double* x) {
-  DevBuf<double> g;
-  if (h->n_own == h->n_dof) {
-    g.alloc((size_t)h->n_dof);
-  } else {
-    g.upload(x, (size_t)h->n_dof, h->stream);
-  }
-  to_global_owned(h, loc, g.p);
-  g.download(x, (size_t)h->n_dof, h->stream);
-  CB_CUDA(cudaStreamSynchronize(h->stream));
-}
-void need_numeric(cutbddc_gpu* h) {
-  if (h->plan_only) throw Failure(CUTBDDC_CONFIG, "plan-only distribution (no communicator): no numerical calls");
-}
-}  // namespace
 
 cutbddc_status cutbddc_gpu_pcg(cutbddc_gpu* h, const double* b, double* x, double rtol, int max_iter,
                                cutbddc_solve_report* report) {

@@ -10,11 +10,14 @@
 // (PAPER.md:315), f = 1, g = 0. A cut cell whose retained volume rule is
 // empty contributes nothing.
 // Compiled with -fmad=false: identical op order to the CPU restatement.
+#include <cub/cub.cuh>
+
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 
 #include "handle.cuh"
+#include "mms.cuh"
 
 #ifndef CB_HD
 #define CB_HD __host__ __device__
@@ -308,7 +311,9 @@ CB_HD int cut_element(const double q8[8], double h, double* K, double* F, double
 constexpr int kVolPts = 12;   // per tet: up to three sub-tets x 4 points
 constexpr int kSurfPts = 6;   // per tet: up to two triangles x 3 points
 constexpr int kAccCells = 4;  // cells (warps) per CTA of k_cut_acc
-constexpr int kAcc = 180;     // accumulators per cell: 0-35 D (i <= j), 36-43 F, 44-79 B, 80-115 M (i <= j), 116-179 N
+constexpr int kAcc = 196;     // accumulators per cell: 0-35 D (i <= j), 36-43 F, 44-79 B, 80-115 M (i <= j), 116-179 N,
+                              // manufactured problem only: 180-187 G1 = sum g phi_a, 188-195 G2 = sum g n.grad phi_a
+constexpr int kAccBase = 180; // the accumulators of every problem
 
 struct PointSmem {
   double vp[6][kVolPts][4];
@@ -453,8 +458,17 @@ __device__ __forceinline__ void acc_index(int it, int& kind, int& i, int& j) {
   }
 }
 
+// Problem data of the load vector: f = 1, g = 0, or the manufactured u
+// evaluated at the physical point origin + (cell + xi) h (mms.cuh).
+struct LoadArgs {
+  int problem, n;
+  const int64_t* cells;  // cut cell ids
+  double ox, oy, oz, h;
+};
+
 __global__ void __launch_bounds__(32 * kAccCells) k_cut_acc(int64_t ncut, const double* __restrict__ q8all,
-                                                             double* __restrict__ accs, int* __restrict__ nvs) {
+                                                             double* __restrict__ accs, int* __restrict__ nvs,
+                                                             LoadArgs la) {
   __shared__ PointSmem smem[kAccCells];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * kAccCells + wid;
@@ -479,10 +493,38 @@ __global__ void __launch_bounds__(32 * kAccCells) k_cut_acc(int64_t ncut, const 
     nvs[2 * e + 1] = nsurf;
   }
   if (nvol == 0) return;
-  for (int it = lane; it < kAcc; it += 32) {
+  const bool mms = la.problem == kProblemManufactured;
+  double cx = 0, cy = 0, cz = 0;  // the cell's lattice coordinates
+  if (mms) {
+    const int64_t cell = la.cells[e], n = la.n;
+    cz = (double)(cell % n);
+    cy = (double)((cell / n) % n);
+    cx = (double)(cell / n / n);
+  }
+  for (int it = lane; it < (mms ? kAcc : kAccBase); it += 32) {
     int kind, i, j;
-    acc_index(it, kind, i, j);
     double acc = 0.0;
+    if (it >= kAccBase) {  // G1 / G2 of the Nitsche load
+      const int a = (it - kAccBase) & 7;
+      const bool g2 = it >= kAccBase + 8;
+      for (int t = 0; t < 6; ++t)
+        for (int pnt = 0; pnt < S.ns[t]; ++pnt) {
+          const double* P = S.sp[t][pnt];
+          const double w = P[3];
+          double ga[3], va;
+          q1_gv(P, a, ga, &va);
+          const double gx = mms_u(la.ox + (cx + P[0]) * la.h, la.oy + (cy + P[1]) * la.h, la.oz + (cz + P[2]) * la.h);
+          if (g2) {
+            const double na = P[4] * ga[0] + P[5] * ga[1] + P[6] * ga[2];
+            acc += w * (gx * na);
+          } else {
+            acc += w * (gx * va);
+          }
+        }
+      accs[e * kAcc + it] = acc;
+      continue;
+    }
+    acc_index(it, kind, i, j);
     if (kind <= 1) {
       for (int t = 0; t < 6; ++t)
         for (int pnt = 0; pnt < S.nv[t]; ++pnt) {
@@ -491,7 +533,10 @@ __global__ void __launch_bounds__(32 * kAccCells) k_cut_acc(int64_t ncut, const 
           double gi[3], gj[3], vi;
           q1_gv(P, i, gi, &vi);
           if (kind == 1) {
-            acc += w * vi;
+            if (mms)
+              acc += w * (mms_f(la.ox + (cx + P[0]) * la.h, la.oy + (cy + P[1]) * la.h, la.oz + (cz + P[2]) * la.h) * vi);
+            else
+              acc += w * vi;
           } else {
             q1_gv(P, j, gj, nullptr);
             acc += w * (gi[0] * gj[0] + gi[1] * gj[1] + gi[2] * gj[2]);
@@ -668,7 +713,7 @@ __device__ double reg_gen_eigs_max(const double (&d)[8], const double (&b)[8], i
 }
 
 // eight lanes per cut cell: beta_e, K_e = h (D + beta M - N - N^T), F_e = h^3 F
-__global__ void __launch_bounds__(256) k_cut_pencil(double h, int64_t ncut, const double* __restrict__ accs,
+__global__ void __launch_bounds__(256) k_cut_pencil(double h, int64_t ncut, int problem, const double* __restrict__ accs,
                                                      const int* __restrict__ nvs, double* __restrict__ ke,
                                                      double* __restrict__ fe, double* __restrict__ beta,
                                                      uint8_t* __restrict__ empty, int* __restrict__ degenerate) {
@@ -709,7 +754,9 @@ __global__ void __launch_bounds__(256) k_cut_pencil(double h, int64_t ncut, cons
     const double mxy = A[80 + tri(i0, j0)];
     ke[e * 64 + gl * 8 + y] = h * (d[y] + betar * mxy - (A[116 + gl * 8 + y] + A[116 + y * 8 + gl]));
   }
-  fe[e * 8 + gl] = h * h * h * A[36 + gl];
+  fe[e * 8 + gl] = problem == kProblemManufactured
+                      ? h * h * h * A[36 + gl] + h * (betar * A[kAccBase + gl] - A[kAccBase + 8 + gl])
+                      : h * h * h * A[36 + gl];
   if (gl == 0) {
     beta[e] = betar / h;
     empty[e] = 0;
@@ -757,7 +804,123 @@ __global__ void k_interior_element(double h, double* __restrict__ kint, double* 
   for (int t = 0; t < 8; ++t) fint[t] = h * h * h * a.fr[t];
 }
 
+// error_norms: per active cell of this rank, the volume
+// integrals of (u_h - u)^2 and |grad u_h - grad u|^2 over the cell's rule
+// (the cut rule of the element kernel, 2x2x2 Gauss for interior cells),
+// u_h from the local solution vector. One thread per cell, the oracle's
+// operation order (oracle/element.cpp error_norms).
+__global__ void k_error_cells(int64_t na, const int64_t* __restrict__ cells, int n, double ox, double oy, double oz,
+                              double h, const double* __restrict__ phi, const uint8_t* __restrict__ cls,
+                              const int32_t* __restrict__ dof_of_node, const int32_t* __restrict__ loc_of_dof,
+                              const double* __restrict__ x, double* __restrict__ out) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= na) return;
+  const int64_t cell = cells[a];
+  const int k = (int)(cell % n), j = (int)((cell / n) % n), i = (int)(cell / n / n);
+  double q[8], uh[8];
+  for (int l = 0; l < 8; ++l) {
+    const int64_t v = ((int64_t)(i + (l & 1)) * (n + 1) + j + ((l >> 1) & 1)) * (n + 1) + k + ((l >> 2) & 1);
+    q[l] = phi[v];
+    const int32_t d = dof_of_node[v];
+    const int32_t lo = d >= 0 ? loc_of_dof[d] : -1;
+    uh[l] = lo >= 0 ? x[lo] : 0.0;
+  }
+  double vp[6][kVolPts][4], sp[6][kSurfPts][7];
+  int nv[6];
+  const bool cut = cls[cell] == CUTBDDC_CUT;
+  if (cut) {
+    for (int t = 0; t < 6; ++t) {
+      PtList L{vp[t], sp[t], 0, 0};
+      tet_points(t, q, L);
+      nv[t] = L.nv;
+    }
+  } else {  // full_quadrature_ref: 2x2x2 Gauss, weight 1/8 (in tet slot 0)
+    const double g0 = 0.5 - 0.5 / sqrt(3.0), g1 = 0.5 + 0.5 / sqrt(3.0);
+    for (int l = 0; l < 8; ++l) {
+      vp[0][l][0] = (l & 1) ? g1 : g0;
+      vp[0][l][1] = ((l >> 1) & 1) ? g1 : g0;
+      vp[0][l][2] = ((l >> 2) & 1) ? g1 : g0;
+      vp[0][l][3] = 0.125;
+    }
+    nv[0] = 8;
+    for (int t = 1; t < 6; ++t) nv[t] = 0;
+  }
+  double el2 = 0.0, eh1 = 0.0;
+  for (int t = 0; t < 6; ++t)
+    for (int p = 0; p < nv[t]; ++p) {
+      const double* P = vp[t][p];
+      double v = 0.0, g[3] = {0.0, 0.0, 0.0};
+      for (int l = 0; l < 8; ++l) {
+        double gl[3], vl;
+        q1_gv(P, l, gl, &vl);
+        v += uh[l] * vl;
+        for (int d = 0; d < 3; ++d) g[d] += uh[l] * gl[d];
+      }
+      const double xp = ox + ((double)i + P[0]) * h, yp = oy + ((double)j + P[1]) * h, zp = oz + ((double)k + P[2]) * h;
+      double gu[3];
+      mms_grad(xp, yp, zp, gu);
+      const double e = v - mms_u(xp, yp, zp);
+      const double w = P[3] * (h * h * h);
+      el2 += w * (e * e);
+      double s = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        const double ed = g[d] / h - gu[d];
+        s += ed * ed;
+      }
+      eh1 += w * s;
+    }
+  out[2 * a] = el2;
+  out[2 * a + 1] = eh1;
+}
+
+__global__ void k_local_active(int64_t nc, int n, int B, int nb, const int64_t* __restrict__ active,
+                               const int32_t* __restrict__ sd_of_block, uint8_t* __restrict__ flag) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= nc) return;
+  const int64_t c = active[a];
+  const int64_t k = c % n, j = (c / n) % n, i = c / n / n;
+  flag[a] = sd_of_block[((i / B) * nb + j / B) * nb + k / B] >= 0;
+}
+
 }  // namespace
+
+// sum over this rank's active cells, ascending cell id (the oracle's order)
+void error_norms_device(cutbddc_gpu* h, const double* xloc, double* l2sq, double* h1sq) {
+  cudaStream_t s = h->stream;
+  const int64_t na = h->n_active;
+  DevBuf<uint8_t>& flag = h->ws_tmp2;
+  DevBuf<int64_t>& cells = h->ws_cells;
+  DevBuf<int64_t>& cnt = h->ws_cnt;
+  flag.alloc((size_t)std::max<int64_t>(1, na));
+  cells.alloc((size_t)std::max<int64_t>(1, na));
+  cnt.alloc(2);
+  k_local_active<<<grid_for(std::max<int64_t>(1, na), 256), 256, 0, s>>>(na, h->n, h->block, h->nb, h->active_cells.p,
+                                                                        h->sd_of_block.p, flag.p);
+  CB_LAUNCH();
+  size_t tb = 0;
+  CB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, h->active_cells.p, flag.p, cells.p, cnt.p, na, s));
+  DevBuf<uint8_t>& tmp = h->ws_tmp;
+  tmp.alloc(std::max(tmp.n, tb));
+  CB_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, h->active_cells.p, flag.p, cells.p, cnt.p, na, s));
+  int64_t nl = 0;
+  CB_CUDA(cudaMemcpyAsync(&nl, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+  CB_CUDA(cudaStreamSynchronize(s));
+  DevBuf<double> per;
+  per.alloc((size_t)std::max<int64_t>(1, 2 * nl));
+  if (nl > 0) {
+    k_error_cells<<<grid_for(nl, 64), 64, 0, s>>>(nl, cells.p, h->n, h->origin[0], h->origin[1], h->origin[2], h->h,
+                                                  h->phi.p, h->cls.p, h->dof_of_node.p, h->loc_of_dof.p, xloc, per.p);
+    CB_LAUNCH();
+  }
+  std::vector<double> hv = per.to_host(s);
+  double a = 0.0, b = 0.0;
+  for (int64_t c = 0; c < nl; ++c) {
+    a += hv[(size_t)(2 * c)];
+    b += hv[(size_t)(2 * c + 1)];
+  }
+  *l2sq = a;
+  *h1sq = b;
+}
 
 void interior_element_device(cutbddc_gpu* h, double* kint, double* fint) {
   k_interior_element<<<1, 1, 0, h->stream>>>(h->h, kint, fint);
@@ -778,7 +941,8 @@ void cut_elements_device(cutbddc_gpu* h) {
 
     k_gather_q8<<<grid_for(h->n_cut, 256), 256, 0, h->stream>>>(h->n, h->n_cut, h->cut_cells.p, h->phi.p, q8all.p);
     CB_LAUNCH();
-    if (std::getenv("CUTBDDC_CUT_THREAD")) {  // the thread-per-cell form (A/B reference)
+    if (std::getenv("CUTBDDC_CUT_THREAD")) {  // the thread-per-cell form (A/B reference, f = 1 only)
+      if (h->problem != kProblemUnitLoad) throw Failure(CUTBDDC_CONFIG, "CUTBDDC_CUT_THREAD: unit load only");
       k_cut_elements<<<grid_for(h->n_cut, 64), 64, 0, h->stream>>>(h->h, h->n_cut, q8all.p, h->ke.p, h->fe.p,
                                                                     h->beta.p, h->empty.p, degen.p);
       CB_LAUNCH();
@@ -787,11 +951,12 @@ void cut_elements_device(cutbddc_gpu* h) {
       DevBuf<int>& nvs = h->ws_nvs;
       accs.alloc((size_t)h->n_cut * kAcc);
       nvs.alloc((size_t)h->n_cut * 2);
+      const LoadArgs la{h->problem, h->n, h->cut_cells.p, h->origin[0], h->origin[1], h->origin[2], h->h};
       k_cut_acc<<<(unsigned)((h->n_cut + kAccCells - 1) / kAccCells), 32 * kAccCells, 0, h->stream>>>(
-          h->n_cut, q8all.p, accs.p, nvs.p);
+          h->n_cut, q8all.p, accs.p, nvs.p, la);
       CB_LAUNCH();
       k_cut_pencil<<<(unsigned)((h->n_cut * 8 + 255) / 256), 256, 0, h->stream>>>(
-          h->h, h->n_cut, accs.p, nvs.p, h->ke.p, h->fe.p, h->beta.p, h->empty.p, degen.p);
+          h->h, h->n_cut, h->problem, accs.p, nvs.p, h->ke.p, h->fe.p, h->beta.p, h->empty.p, degen.p);
       CB_LAUNCH();
     }
   }

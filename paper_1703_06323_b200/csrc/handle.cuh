@@ -122,6 +122,7 @@ struct cutbddc_gpu {
 
   // ---------------------------------------------------------------- mesh
   int n = 0;                   // cells per axis
+  int problem = 0;             // load data: 0 f = 1, g = 0; 1 manufactured (mms.cuh)
   double origin[3] = {0, 0, 0}, h = 0, tol = 0;
   int64_t n_nodes = 0, n_cells = 0, n_dof = 0;
   cutbddc_b200::DevBuf<double> phi;
@@ -245,6 +246,8 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<double> ws_w8;             // device objects v2: weight tuples (8 per dof)
   cutbddc_b200::DevBuf<double> ws_acc;            // cut cells: the 180 quadrature sums per cell (element.cu)
   cutbddc_b200::DevBuf<int> ws_nvs;
+  cutbddc_b200::DevBuf<uint8_t> ws_tmp2;
+  cutbddc_b200::DevBuf<int64_t> ws_cells;
   cutbddc_b200::DevBuf<int> ws_flag;
   cutbddc_b200::DevBuf<int32_t> ws_coff;                       // corner coarse basis: front column offsets
   cutbddc_b200::DevBuf<double> ws_x8, ws_y8, ws_u8, ws_v8;      // multi-RHS forward sweep vectors

@@ -85,7 +85,7 @@ EXPORTS = [
     "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free", "cutbddc_gpu_classify_objects",
     "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_distribution", "cutbddc_gpu_time_factor",
     "cutbddc_fp64_peak", "cutbddc_build_exchange_plan", "cutbddc_gpu_exchange_plan", "cutbddc_exchange_plan_free",
-    "cutbddc_gpu_time_parts",
+    "cutbddc_gpu_time_parts", "cutbddc_gpu_set_problem", "cutbddc_gpu_error_norms",
 ]
 
 
@@ -291,6 +291,17 @@ class GpuSolver:
                                                   self.rank if rank is None else rank,
                                                   self.world if world is None else world))
 
+    def set_problem(self, problem: int):
+        """0: f = 1, g = 0 (BASELINE runs); 1: manufactured u = sin(5 pi |x|). Before assemble."""
+        _check(lib().cutbddc_gpu_set_problem(self.h, int(problem)))
+
+    def error_norms(self, x=None) -> tuple:
+        """(|u_h - u|_L2, |u_h - u|_H1) of the manufactured problem."""
+        l2, h1 = C.c_double(), C.c_double()
+        xp = _p(np.ascontiguousarray(x, np.float64), C.c_double) if x is not None else None
+        _check(lib().cutbddc_gpu_error_norms(self.h, xp, C.byref(l2), C.byref(h1)))
+        return l2.value, h1.value
+
     def exchange_plan(self) -> ExchangePlan:
         """The device-built exchange plan of this handle's rank."""
         out = C.POINTER(_Plan)()
@@ -475,6 +486,7 @@ def prepare(solver: GpuSolver, cfg) -> Problem:
     (host), sub-assembly (device)."""
     mesh = solver.classify(cfg)
     block_ids = build_partition(mesh, cfg.block)
+    solver.set_problem(getattr(cfg, "problem", 0))
     dirichlet = solver.assemble(cfg.block, block_ids)
     diag = solver.local_diagonals() if cfg.variant == _cfg.V2 else None
     objs = classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, diag)
@@ -507,6 +519,7 @@ def prepare_distributed(solver: GpuSolver, cfg) -> tuple[Problem, LocalPart]:
     block_ids = build_partition(mesh, cfg.block)
     lp = local_part(cfg.block, block_ids, cfg.cells, solver.rank, solver.world)
     solver.set_distribution(cfg.block, block_ids, lp.rank_of_sd)
+    solver.set_problem(getattr(cfg, "problem", 0))
     dirichlet = solver.assemble(cfg.block, block_ids)
     objs = classify_objects(mesh, cfg.block, block_ids, dirichlet, cfg.objects, cfg.variant, None)
     return Problem(cfg, mesh, block_ids, dirichlet, objs), lp
