@@ -1066,6 +1066,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     ps_host.next("setup 1 factorisations");
     // ---- factorisations
     if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);
+    set_split_flags(h->tI, nsd);
     factor_symbolic(h, h->tI, fi, h->fI);
     std::vector<FactorJob> jobs{FactorJob{&h->tI, &fi, &h->fI, "cholesky (interior problem)"}};
     bool k_failed = false;
@@ -1075,6 +1076,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
         jobs.push_back(FactorJob{&h->tI, &fk_c, &h->fK, kSaddleMsg, &k_failed});
       } else {
         if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
+        set_split_flags(h->tK, nsd);
         factor_symbolic(h, h->tK, fk, h->fK);
         jobs.push_back(FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg});
       }
@@ -1092,6 +1094,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     h->k_corner = false;
     local([&] {
       if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
+      set_split_flags(h->tK, nsd);
       factor_symbolic(h, h->tK, fk, h->fK);
       factor_numeric(h, {FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg}}, [&] { build_sweep_items(h, h->tK, h->fK); });
     });

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) k_symbolic(TplDev t, int nsd, const 
 // The numeric factorisation is one dataflow launch over every front
 // (dense_dag.cu). Split fronts are cut into 64 x 64 tile tasks shared by many
 // CTAs; the others are factorised whole by one CTA (W task). A front is split
-// from kSplitRows template rows (cfg4: against 600 / 250 / 150) or
+// from kSplitRows template rows or
 // kSplitMflop template MFLOP of partial Cholesky (a dense root: one CTA would
 // run it alone for ~0.5 ms). CUTBDDC_SPLIT_ROWS / CUTBDDC_SPLIT_MFLOP
 // override, for measurements.
@@ -93,17 +93,27 @@ static const int kSplitRows = [] {
   const char* e = std::getenv("CUTBDDC_SPLIT_ROWS");
   return e ? std::max(64, std::atoi(e)) : 400;
 }();
-static const double kSplitMflop = [] {
-  const char* e = std::getenv("CUTBDDC_SPLIT_MFLOP");
-  return e ? std::atof(e) : 7.0;
-}();
-static bool is_split_front(const Supernode& sn) {
+// Split threshold in MFLOP: few subdomains (cfg4: 51) leave most SMs idle
+// unless the leaves are tiled too (7 -> 1 MFLOP: setup 4.8 -> 4.4 ms); many
+// (cfg5: 1 960) fill the GPU with whole fronts, where tiling only adds task
+// overhead (1 MFLOP: setup 607 -> 662 ms). profiles/r02_tune_split.txt.
+static double split_mflop(int nsd) {
+  static const char* e = std::getenv("CUTBDDC_SPLIT_MFLOP");
+  return e ? std::atof(e) : (nsd >= 256 ? 7.0 : 1.0);
+}
+static bool is_split_front(const Supernode& sn, int nsd) {
   const double r = sn.nrows, c = sn.ncols;
   const double mflop = (c * c * c / 3.0 + (r - c) * c * c + (r - c) * (r - c) * c) * 1e-6;
-  return sn.nrows >= kSplitRows || mflop >= kSplitMflop;
+  return sn.nrows >= kSplitRows || mflop >= split_mflop(nsd);
 }
 
+
 }  // namespace
+
+void set_split_flags(TplSet& ts, int nsd) {
+  ts.is_split.assign(ts.tpl.sn.size(), 0);
+  for (size_t sid = 0; sid < ts.tpl.sn.size(); ++sid) ts.is_split[sid] = is_split_front(ts.tpl.sn[sid], nsd);
+}
 
 TplDev tpl_dev(const TplSet& ts, int slots) {
   TplDev t;
@@ -142,8 +152,7 @@ void upload_template(cutbddc_gpu* h, TplSet& ts, bool shell_root) {
   ts.amap.upload(ts.tpl.amap, s);
   ts.emap.upload(ts.tpl.emap.empty() ? std::vector<int32_t>{0} : ts.tpl.emap, s);
   ts.root_pos.upload(ts.tpl.root_pos, s);
-  ts.is_split.assign(ts.tpl.sn.size(), 0);
-  for (size_t sid = 0; sid < ts.tpl.sn.size(); ++sid) ts.is_split[sid] = is_split_front(ts.tpl.sn[sid]);
+  set_split_flags(ts, h->nsd);
   ts.ready = true;
 }
 

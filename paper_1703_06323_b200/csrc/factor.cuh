@@ -57,6 +57,8 @@ struct FactorInput {
 TplDev tpl_dev(const TplSet& t, int slots);
 FactorDev factor_dev(const FactorSet& f);
 void upload_template(cutbddc_gpu* h, TplSet& t, bool shell_root);
+// which fronts the factorisation tiles (depends on the subdomain count)
+void set_split_flags(TplSet& ts, int nsd);
 // Symbolic phase of one factorisation: compact front sizes, panel / update /
 // front-workspace offsets, the sweep plan.
 void factor_symbolic(cutbddc_gpu* h, const TplSet& t, const FactorInput& in, FactorSet& f);

@@ -6,6 +6,6 @@ mkdir -p gpurun_out
 : > $out
 for v in "$@"; do
   echo "== ${v:-default}" >> $out
-  env $v timeout 300 python tools/setup_sweep.py cfg4 8 >> $out 2>&1
+  env $v timeout 600 python tools/setup_sweep.py ${TUNE_WORKLOAD:-cfg4} ${TUNE_REPS:-8} >> $out 2>&1
 done
 cat $out
