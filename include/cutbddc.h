@@ -162,14 +162,16 @@ cutbddc_status cutbddc_gpu_cut_elements(cutbddc_gpu* h, int64_t* cells, double* 
 cutbddc_status cutbddc_gpu_local_system(cutbddc_gpu* h, double* stencil, uint8_t* mask_interior, uint8_t* mask_present,
                                         double* diag_add, int32_t* slot_dof);
 cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x);
-/* Statistics (16 slots): [0]=n_dof [1]=n_sd [2]=n_coarse [3]=template slots
+/* Statistics (17 slots): [0]=n_dof [1]=n_sd [2]=n_coarse [3]=template slots
  * [4]=factor panel doubles (both factorisations, all subdomains)
  * [5]=supernodes (Neumann template) [6]=levels [7]=max m_w [8]=n_interface
  * [9]=kernel launches so far (process-wide) [10]/[11]=panel doubles of the
  * interior / Neumann factorisation [12]=partial-Cholesky flops of both
  * [13]=world size [14]=1 if the handle owns an NCCL communicator
  * [15]=1 if the constrained Neumann factor is the corner-augmented
- * K_c = A + rho C_corner^T C_corner (else K = A + rho C^T C). */
+ * K_c = A + rho C_corner^T C_corner (else K = A + rho C^T C)
+ * [16]=subdomains of this rank on K = A + rho C^T C while the others use K_c
+ * (a mixed K: K_c singular there, e.g. a floating fragment); counted in [11]/[12]. */
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
 /* Measurement hook: average device time of the triangular-solve sweeps of
  * one BDDC apply (interior, Neumann, interior) over `reps` repetitions, and

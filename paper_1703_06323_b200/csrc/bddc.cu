@@ -208,11 +208,12 @@ __global__ void k_scatter_r1(int64_t ns, const int32_t* __restrict__ slot_loc, c
 // cy[row] = C_row . y
 __global__ void k_cy(int64_t mtot, int T, const int32_t* __restrict__ row_sd, const int64_t* __restrict__ c_ptr,
                      const int32_t* __restrict__ c_slot, const double* __restrict__ c_val, const double* __restrict__ Y,
-                     double* __restrict__ cy, const int* __restrict__ skip) {
+                     double* __restrict__ cy, const int* __restrict__ skip, const uint8_t* __restrict__ skip_sd) {
   if (skip && *skip) return;
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= mtot) return;
+  if (skip_sd && skip_sd[row_sd[row]]) return;
   const double* y = Y + (int64_t)row_sd[row] * T;
   double s = 0.0;
   for (int64_t p = c_ptr[row] + lane; p < c_ptr[row + 1]; p += 32) s += c_val[p] * y[c_slot[p]];
@@ -414,8 +415,9 @@ __global__ void __launch_bounds__(256) k_root_h(const int64_t* __restrict__ rinf
 // S = H^T H per subdomain (both triangles): CTA per (sd, row a), warp per b <= a
 __global__ void __launch_bounds__(256) k_root_s(const int64_t* __restrict__ rinfo, const int64_t* __restrict__ m_off,
                                                 const int64_t* __restrict__ s_off, const double* __restrict__ H,
-                                                double* __restrict__ S) {
+                                                double* __restrict__ S, const uint8_t* __restrict__ skip_sd) {
   const int sd = blockIdx.x, a = blockIdx.y;
+  if (skip_sd && skip_sd[sd]) return;  // the other formulation's subdomain
   const int m = (int)(m_off[sd + 1] - m_off[sd]);
   if (a >= m) return;
   const int cr = (int)rinfo[4 * sd];
@@ -434,10 +436,12 @@ __global__ void __launch_bounds__(256) k_root_s(const int64_t* __restrict__ rinf
 
 // sinv = sym(S^{-1}); A_c,w = sinv - rho I (K = A + rho C^T C), or
 // sinv - rho I_corner (K_c = A + rho C_corner^T C_corner: corner_row != null)
+// A_c,w = S^{-1} - rho I_aug: the augmented rows are the corner rows (K_c)
+// or every row (K = A + rho C^T C: no corner_row, or shell_sd[sd] set)
 __global__ void k_root_coarse(const int64_t* __restrict__ m_off, const int64_t* __restrict__ s_off,
                               const double* __restrict__ Sinv, const double* __restrict__ rho,
                               const uint8_t* __restrict__ corner_row, double* __restrict__ sinv,
-                              double* __restrict__ ac) {
+                              double* __restrict__ ac, const uint8_t* __restrict__ shell_sd) {
   const int sd = blockIdx.x;
   const int m = (int)(m_off[sd + 1] - m_off[sd]);
   const int64_t o = s_off[sd];
@@ -445,7 +449,7 @@ __global__ void k_root_coarse(const int64_t* __restrict__ m_off, const int64_t* 
     const int a = q / m, b = q % m;
     const double v = 0.5 * (Sinv[o + (int64_t)a * m + b] + Sinv[o + (int64_t)b * m + a]);
     sinv[o + q] = v;
-    const bool shift = a == b && (!corner_row || corner_row[m_off[sd] + a]);
+    const bool shift = a == b && (!corner_row || (shell_sd && shell_sd[sd]) || corner_row[m_off[sd] + a]);
     ac[o + q] = v - (shift ? rho[sd] : 0.0);
   }
 }
@@ -480,6 +484,7 @@ __global__ void k_h_compact(int pass, int nsn, int64_t ns, const FrontDesc* __re
   const FrontDesc& d = desc[(int64_t)sd * nsn + sid];
   const int m = (int)(m_off[sd + 1] - m_off[sd]);
   const int np = (int)rinfo[4 * sd];
+  if (np == 0) return;  // a shell-formulation subdomain (mixed K): no corner H
   const int k0 = coff[(int64_t)sd * nsn + sid];
   double* hs = H + rinfo[4 * sd + 3];
   for (int j = threadIdx.x; j < d.c; j += blockDim.x) {
@@ -506,7 +511,7 @@ __global__ void k_pivot_check(int nsn, int T, const FrontDesc* __restrict__ desc
     const double piv = 1.0 / (g * g);
     const int sl = cslot[d.vo + j];
     const double orig = As[(int64_t)(sl / T) * 27 * T + 13ll * T + sl % T] + dadd[sl];
-    if (!(piv > 1e-12 * orig)) atomicExch(bad, 1);
+    if (!(piv > 1e-12 * orig)) bad[sd] = 1;  // per subdomain (benign race: every writer stores 1)
   }
 }
 
@@ -541,11 +546,13 @@ __global__ void __launch_bounds__(256) k_h_cy(const int64_t* __restrict__ m_off,
 
 __global__ void k_h_cy_sum(int64_t mtot, int nch, int mmax, const int32_t* __restrict__ row_sd,
                            const int64_t* __restrict__ m_off, const int64_t* __restrict__ rinfo,
-                           const double* __restrict__ hp, double* __restrict__ cy, const int* __restrict__ skip) {
+                           const double* __restrict__ hp, double* __restrict__ cy, const int* __restrict__ skip,
+                           const uint8_t* __restrict__ skip_sd) {
   if (skip && *skip) return;
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (row >= mtot) return;
   const int sd = row_sd[row];
+  if (skip_sd && skip_sd[sd]) return;
   const int a = (int)(row - m_off[sd]), used = (int)((rinfo[4 * sd] + 255) / 256);
   double v = 0.0;
   for (int c = 0; c < used; ++c) v += hp[((int64_t)sd * nch + c) * mmax + a];
@@ -760,21 +767,37 @@ __global__ void k_row_sd(int nsd, const int64_t* __restrict__ m_off, int32_t* __
   for (int64_t r = m_off[sd] + threadIdx.x; r < m_off[sd + 1]; r += blockDim.x) row_sd[r] = sd;
 }
 
-// K_c pivots against the original diagonal (k_pivot_check): false if any is tiny
-bool corner_pivots_ok(cutbddc_gpu* h) {
+// Subdomains whose K_c cannot be used: a non-positive pivot in the
+// factorisation (flagged by the DAG into bad_dev) or a pivot tiny against
+// the original diagonal (k_pivot_check). bad: per subdomain, host.
+int corner_bad_subdomains(cutbddc_gpu* h, int* bad_dev, std::vector<uint8_t>& bad) {
   cudaStream_t s = h->stream;
   const int nsn = (int)h->tI.tpl.sn.size();
-  DevBuf<int>& bad = h->ws_flag;
-  bad.alloc(1);
-  bad.zero(s);
   k_pivot_check<<<dim3(nsn, h->nsd), 128, 0, s>>>(nsn, h->slots, reinterpret_cast<const FrontDesc*>(h->fK.desc.p),
-                                                   h->fK.panel.p, h->fK.cslot.p, h->As.p, h->diag_add.p, bad.p);
+                                                   h->fK.panel.p, h->fK.cslot.p, h->As.p, h->diag_add.p, bad_dev);
   CB_LAUNCH();
-  int hb = 0;
-  CB_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  std::vector<int> hb((size_t)h->nsd);
+  CB_CUDA(cudaMemcpyAsync(hb.data(), bad_dev, sizeof(int) * h->nsd, cudaMemcpyDeviceToHost, s));
   CB_CUDA(cudaStreamSynchronize(s));
-  if (hb && std::getenv("CUTBDDC_K_STATS")) std::fprintf(stderr, "[cutbddc] tiny K_c pivot: shell-root K fallback\n");
-  return hb == 0;
+  bad.assign((size_t)h->nsd, 0);
+  // test hook: CUTBDDC_K_MIXED_EVERY=n puts every n-th subdomain on the
+  // shell-root K (the mixed path on meshes where K_c is never singular)
+  const int every = [] {
+    const char* e = std::getenv("CUTBDDC_K_MIXED_EVERY");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  int nb = 0;
+  for (int sd = 0; sd < h->nsd; ++sd)
+    nb += bad[(size_t)sd] = hb[(size_t)sd] != 0 || (every > 0 && sd % every == 0);
+  if (nb && std::getenv("CUTBDDC_K_STATS"))
+    std::fprintf(stderr, "[cutbddc] K_c unusable in %d of %d subdomains: shell-root K there\n", nb, h->nsd);
+  return nb;
+}
+
+__global__ void k_mask_sd(int64_t ns, int T, const uint8_t* __restrict__ mask, const uint8_t* __restrict__ sel,
+                          uint8_t* __restrict__ out) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g < ns) out[g] = mask[g] && sel[g / T];
 }
 
 // S^{-1} (symmetrised) of every subdomain's m x m block in place; a
@@ -800,7 +823,8 @@ void invert_schur(cutbddc_gpu* h, double* S) {
 // Coarse basis of the corner formulation: H = L^{-1} C^T by multi-RHS
 // forward sweeps (kSweepMultiRhs constraint rows of every subdomain per
 // pass), S = H^T H, S^{-1}, A_c,w = S^{-1} - rho I_corner.
-void coarse_basis_corner(cutbddc_gpu* h, const std::vector<int64_t>& m_off, const std::vector<int64_t>& s_off) {
+void coarse_basis_corner(cutbddc_gpu* h, const std::vector<int64_t>& m_off, const std::vector<int64_t>& s_off,
+                         const std::vector<uint8_t>& shell_sd, double* S) {
   cudaStream_t s = h->stream;
   const int nsd = h->nsd, T = h->slots, m_max = h->m_max;
   const TplSet& ts = h->tI;
@@ -816,6 +840,7 @@ void coarse_basis_corner(cutbddc_gpu* h, const std::vector<int64_t>& m_off, cons
       coff[(size_t)sd * nsn + sid] = k;
       k += f.h_rc[(size_t)sd * nsn + sid].y;
     }
+    if (!shell_sd.empty() && shell_sd[(size_t)sd]) k = 0;  // its K is the shell-root one
     const int64_t m = m_off[(size_t)sd + 1] - m_off[(size_t)sd];
     rinfo[4 * (size_t)sd] = k;
     rinfo[4 * (size_t)sd + 1] = hs;
@@ -847,14 +872,49 @@ void coarse_basis_corner(cutbddc_gpu* h, const std::vector<int64_t>& m_off, cons
                                               dcoff.p, h->m_off.p, h->root_info.p, h->ws_y8.p, h->hroot.p, h->hslot.p);
     CB_LAUNCH();
   }
-  pc.next("coarse basis S, S^-1");
-  DevBuf<double>& S = h->ws_s;
-  S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
-  k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
+  pc.next("coarse basis S");
+  k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S,
+                                            shell_sd.empty() ? nullptr : h->kform_shell.p);
   CB_LAUNCH();
-  invert_schur(h, S.p);
-  k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, h->corner_row.p, h->sinv.p,
-                                    h->ac_loc.p + (int64_t)h->dist_rank * h->maxac);
+}
+
+// Coarse basis of the shell-root formulation K = A + rho C^T C on the
+// subdomains factorised in fs (all, or the shell part of a mixed K): H =
+// G_r C_r^T, S = H^T H, W_r = G_r^T H in the root space (see k_root_h).
+void coarse_basis_shell(cutbddc_gpu* h, const std::vector<int64_t>& m_off, const FactorSet& fs, bool mixed,
+                        double* S) {
+  cudaStream_t s = h->stream;
+  const int nsd = h->nsd, m_max = h->m_max;
+  const int nsn = (int)h->tK.tpl.sn.size(), root = nsn - 1;
+  std::vector<int64_t> rinfo((size_t)4 * nsd);
+  int64_t wtot = 0;
+  int cr_max = 0;
+  for (int sd = 0; sd < nsd; ++sd) {
+    const size_t q = (size_t)sd * nsn + root;
+    const int cr = fs.h_rc[q].y;  // 0: not a shell subdomain (mixed)
+    if (fs.h_rc[q].x != cr) throw Failure(CUTBDDC_INTERNAL, "shell root with update rows");
+    const int m = (int)(m_off[(size_t)sd + 1] - m_off[(size_t)sd]);
+    rinfo[4 * (size_t)sd] = cr;
+    rinfo[4 * (size_t)sd + 1] = fs.h_panel_off[q];
+    rinfo[4 * (size_t)sd + 2] = fs.h_vec_off[q];
+    rinfo[4 * (size_t)sd + 3] = wtot;
+    wtot += (int64_t)cr * m;
+    cr_max = std::max(cr_max, cr);
+  }
+  h->root_info_s.upload(rinfo, s);
+  h->hroot_s.alloc((size_t)std::max<int64_t>(1, wtot));
+  h->wroot.alloc((size_t)std::max<int64_t>(1, wtot));
+  if (cr_max == 0) return;
+  const int32_t* pfx_root = fs.pfx.p + h->tK.tpl.sn[(size_t)root].rows_off;
+  const int64_t rows_total = (int64_t)h->tK.tpl.rows.size();
+  k_root_h<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info_s.p, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
+                                            h->tK.root_pos.p, pfx_root, rows_total, fs.panel.p, h->hroot_s.p);
+  CB_LAUNCH();
+  k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info_s.p, h->m_off.p, h->ac_off.p, h->hroot_s.p, S,
+                                            mixed ? h->kform_corner.p : nullptr);
+  CB_LAUNCH();
+  k_root_w<<<dim3(nsd, (cr_max + 63) / 64), 256, 0, s>>>(h->root_info_s.p, h->m_off.p, fs.panel.p, h->hroot_s.p,
+                                                        h->wroot.p);
   CB_LAUNCH();
 }
 
@@ -1042,15 +1102,20 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   // out of the apply ("preconditioner reduces to exact interior solve").
   h->has_K = h->n_if > 0;
   h->fK.upd_total = 0;
+  h->fKs.upd_total = 0;
   // K: corner-augmented K_c = A + rho sum_corners e e^T on the plain ND
   // template (no rho C^T C rows: fk_c has no constraint rows), else the full
   // K = A + rho C^T C on the shell-root template (PEN rows of the root).
-  static const bool force_shell = [] {
+  const bool force_shell = [] {
     const char* e = std::getenv("CUTBDDC_K_SHELL");
     return e && e[0] == '1';
   }();
   h->k_corner = !force_shell && m_max > 0;
-  bool corner_bad = false;
+  int n_bad = 0;                   // subdomains whose K_c is unusable (this rank)
+  std::vector<uint8_t> bad_sd;
+  DevBuf<int>& bad_dev = h->ws_badsd;
+  bad_dev.alloc((size_t)nsd);
+  bad_dev.zero(s);
   local([&] {
     const size_t rho_shm = sizeof(double) * (size_t)T;
     if (rho_shm > 48 * 1024) CB_CUDA(cudaFuncSetAttribute(k_rho, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rho_shm));
@@ -1073,7 +1138,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     if (h->has_K) {
       if (h->k_corner) {
         factor_symbolic(h, h->tI, fk_c, h->fK);
-        jobs.push_back(FactorJob{&h->tI, &fk_c, &h->fK, kSaddleMsg, &k_failed});
+        jobs.push_back(FactorJob{&h->tI, &fk_c, &h->fK, kSaddleMsg, &k_failed, bad_dev.p});
       } else {
         if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
         set_split_flags(h->tK, nsd);
@@ -1085,67 +1150,54 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
       build_sweep_items(h, h->tI, h->fI);
       if (h->has_K) build_sweep_items(h, h->k_corner ? h->tI : h->tK, h->fK);
     });
-    corner_bad = h->has_K && h->k_corner && (k_failed || !corner_pivots_ok(h));
+    if (h->has_K && h->k_corner) n_bad = corner_bad_subdomains(h, bad_dev.p, bad_sd);
   });
-  // a floating fragment (no corner, no Nitsche boundary) leaves K_c singular
-  // on some subdomain: the full augmented K on the shell-root template
-  // instead, on every rank (one formulation: the same numbers for any world size)
-  if (agree(corner_bad ? 1 : 0) && h->has_K && h->k_corner) {
-    h->k_corner = false;
+  // A floating fragment (no corner, no Nitsche boundary) leaves K_c singular
+  // on its subdomain: there K = A + rho C^T C on the shell-root template
+  // instead (a mixed K: the corner formulation everywhere else). The mode is
+  // agreed over the ranks (one apply path: the same numbers for any world size).
+  h->k_mixed = false;
+  h->n_shell_sd = n_bad;
+  if (agree(n_bad > 0 ? 1 : 0) && h->has_K && h->k_corner) {
+    h->k_mixed = true;
     local([&] {
+      std::vector<uint8_t> corner_sd((size_t)nsd);
+      for (int sd = 0; sd < nsd; ++sd) corner_sd[(size_t)sd] = !bad_sd[(size_t)sd];
+      h->kform_shell.upload(bad_sd, s);
+      h->kform_corner.upload(corner_sd, s);
+      build_sweep_items(h, h->tI, h->fK, &bad_sd);  // K_c sweeps skip the shell subdomains, fKs's the others
       if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
       set_split_flags(h->tK, nsd);
-      factor_symbolic(h, h->tK, fk, h->fK);
-      factor_numeric(h, {FactorJob{&h->tK, &fk, &h->fK, kSaddleMsg}}, [&] { build_sweep_items(h, h->tK, h->fK); });
+      DevBuf<uint8_t>& mask_s = h->mask_shell;
+      mask_s.alloc((size_t)ns);
+      k_mask_sd<<<grid_for(ns, 256), 256, 0, s>>>(ns, T, h->mask_all.p, h->kform_shell.p, mask_s.p);
+      CB_LAUNCH();
+      FactorInput fk_s = fk;
+      fk_s.mask = mask_s.p;
+      factor_symbolic(h, h->tK, fk_s, h->fKs);
+      factor_numeric(h, {FactorJob{&h->tK, &fk_s, &h->fKs, kSaddleMsg}}, [&] { build_sweep_items(h, h->tK, h->fKs, &corner_sd); }, true);
     });
     agree(0);
   }
-  upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, h->fK.upd_total));
+  upd_total = std::max<int64_t>(1, std::max(h->fI.upd_total, std::max(h->fK.upd_total, h->k_mixed ? h->fKs.upd_total : 0)));
   local([&] {
-    // ---- coarse basis in the root space of K (see k_root_h): H, S, S^{-1},
-    // W_r and A_c,w = S^{-1} - rho I; the apply never forms Phi
+    // ---- coarse basis: S = C K^{-1} C^T per subdomain in the formulation's
+    // factor space (corner: H = L^{-1} C^T; shell: the root space), then
+    // S^{-1} and A_c,w = S^{-1} - rho I_aug; the apply never forms Phi
     h->ac_loc.alloc((size_t)(world * h->maxac));  // staged: this rank's blocks at rank * maxac
     h->ac_loc.zero(s);
     h->sinv.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
     ps_host.next("setup 2 root-space coarse basis");
-    if (m_max > 0 && h->k_corner) {
-      coarse_basis_corner(h, m_off, s_off);
-    } else if (m_max > 0) {
+    if (m_max > 0) {
       if (!h->has_K) throw Failure(CUTBDDC_INTERNAL, "coarse space without an interface");
-      const int nsn = (int)h->tK.tpl.sn.size(), root = nsn - 1;
-      std::vector<int64_t> rinfo((size_t)4 * nsd);
-      int64_t wtot = 0;
-      int cr_max = 0;
-      for (int sd = 0; sd < nsd; ++sd) {
-        const size_t fs = (size_t)sd * nsn + root;
-        const int cr = h->fK.h_rc[fs].y;
-        if (h->fK.h_rc[fs].x != cr) throw Failure(CUTBDDC_INTERNAL, "shell root with update rows");
-        const int m = (int)(m_off[(size_t)sd + 1] - m_off[(size_t)sd]);
-        rinfo[4 * (size_t)sd] = cr;
-        rinfo[4 * (size_t)sd + 1] = h->fK.h_panel_off[fs];
-        rinfo[4 * (size_t)sd + 2] = h->fK.h_vec_off[fs];
-        rinfo[4 * (size_t)sd + 3] = wtot;
-        wtot += (int64_t)cr * m;
-        cr_max = std::max(cr_max, cr);
-      }
-      h->root_info.upload(rinfo, s);
-      h->hroot.alloc((size_t)std::max<int64_t>(1, wtot));
-      h->wroot.alloc((size_t)std::max<int64_t>(1, wtot));
-      const int32_t* pfx_root = h->fK.pfx.p + h->tK.tpl.sn[(size_t)root].rows_off;
-      const int64_t rows_total = (int64_t)h->tK.tpl.rows.size();
-      k_root_h<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p,
-                                                h->tK.root_pos.p, pfx_root, rows_total, h->fK.panel.p, h->hroot.p);
-      CB_LAUNCH();
       DevBuf<double>& S = h->ws_s;
       S.alloc((size_t)std::max<int64_t>(1, s_off[(size_t)nsd]));
-      k_root_s<<<dim3(nsd, m_max), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->ac_off.p, h->hroot.p, S.p);
-      CB_LAUNCH();
-      k_root_w<<<dim3(nsd, (cr_max + 63) / 64), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.panel.p, h->hroot.p,
-                                                            h->wroot.p);
-      CB_LAUNCH();
+      if (h->k_corner) coarse_basis_corner(h, m_off, s_off, h->k_mixed ? bad_sd : std::vector<uint8_t>{}, S.p);
+      if (!h->k_corner || h->k_mixed) coarse_basis_shell(h, m_off, h->k_mixed ? h->fKs : h->fK, h->k_mixed, S.p);
       invert_schur(h, S.p);
-      k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, nullptr, h->sinv.p,
-                                        h->ac_loc.p + (int64_t)h->dist_rank * h->maxac);
+      k_root_coarse<<<nsd, 256, 0, s>>>(h->m_off.p, h->ac_off.p, S.p, h->rho.p, h->k_corner ? h->corner_row.p : nullptr,
+                                        h->sinv.p, h->ac_loc.p + (int64_t)h->dist_rank * h->maxac,
+                                        h->k_mixed ? h->kform_shell.p : nullptr);
       CB_LAUNCH();
     }
   });
@@ -1217,7 +1269,8 @@ void h_cy(cutbddc_gpu* h, const double* Yc, const int* skip) {
                                                      h->hcy_part.p, h->m_max, skip);
   CB_LAUNCH();
   k_h_cy_sum<<<grid_for(h->m_total, 128), 128, 0, h->stream>>>(h->m_total, nch, h->m_max, h->row_sd.p, h->m_off.p,
-                                                              h->root_info.p, h->hcy_part.p, h->cy.p, skip);
+                                                              h->root_info.p, h->hcy_part.p, h->cy.p, skip,
+                                                              h->k_mixed ? h->kform_shell.p : nullptr);
   CB_LAUNCH();
 }
 
@@ -1246,16 +1299,23 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     // the coarse problem, y' += H u, the backward sweep. Shell formulation:
     // the forward sweep, the root's backward step, the coarse problem, the
     // root correction W_r u, then the backward sweep below the root (k_root_h).
-    const bool corner = h->k_corner;
-    const TplSet& tk = h->tplK();
-    double* Yc = corner ? h->ysave.p : h->sv1.p;  // where cy is read and the correction lands
-    const double* Hc = corner ? h->hroot.p : nullptr;
-    sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepFwd);
-    if (!corner) sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRoot);
+    // Mixed K: the corner formulation's sweeps skip the shell subdomains and
+    // the shell factor fKs holds only those; each subdomain takes one path.
+    const bool corner = h->k_corner, mixed = h->k_mixed, shell = !corner || mixed;
+    const FactorSet& fs = mixed ? h->fKs : h->fK;  // the shell-root factor
+    if (corner) sweep_phase(h, h->tI, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepFwd);
+    if (shell) {
+      sweep_phase(h, h->tK, fs, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepFwd);
+      sweep_phase(h, h->tK, fs, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRoot);
+    }
     ps.next("apply vec 3 cy coarse root-correction");
-    const int cr_blocks = std::max(1, corner ? (h->np_max + 255) / 256 : (int)((h->tK.tpl.sn.back().ncols + 255) / 256));
+    const int cr_corner = corner ? (h->np_max + 255) / 256 : 0;
+    const int cr_shell = shell ? (int)((h->tK.tpl.sn.back().ncols + 255) / 256) : 0;
+    const int cr_blocks = std::max(1, std::max(cr_corner, cr_shell));
     double* gl_loc = h->gl.p + (int64_t)h->dist_rank * h->maxrows;  // this rank's rows of the staged gl
-    if (h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
+    if (!mixed && h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
+      double* Yc = corner ? h->ysave.p : h->sv1.p;  // where cy is read and the correction lands
+      const int64_t* rinfo = corner ? h->root_info.p : h->root_info_s.p;
       if (corner) {  // cy = H^T y' (a warp per constraint row), gl = S^{-1} cy
         h_cy(h, Yc, skip);
         CB_LAUNCH();
@@ -1264,7 +1324,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
                                                                skip);
       } else {
         k_coarse_in<<<h->nsd, 256, 0, s>>>(T, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, Yc, h->ac_off.p,
-                                           h->sinv.p, h->cy.p, gl_loc, skip, h->root_info.p, nullptr, nullptr);
+                                           h->sinv.p, h->cy.p, gl_loc, skip, rinfo, nullptr, nullptr);
       }
       CB_LAUNCH();
       gather_rows(h);
@@ -1277,15 +1337,14 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
         });
       k_coarse_out<<<dim3(h->nsd, cr_blocks), 256, shm, s>>>(
           h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->acoarse_full.p, h->coarse_id.p, h->m_off.p, h->ac_off.p,
-          h->sinv.p, h->cy.p, h->root_info.p, h->fK.cslot.p, h->wroot.p, Yc, skip, Hc, h->hslot.p);
+          h->sinv.p, h->cy.p, rinfo, fs.cslot.p, h->wroot.p, Yc, skip, corner ? h->hroot.p : nullptr, h->hslot.p);
       CB_LAUNCH();
     } else {
-      if (corner) {
-        h_cy(h, Yc, skip);
-      } else {
-        k_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p,
-                                                           h->c_val.p, h->sv1.p, h->cy.p, skip);
-      }
+      if (corner) h_cy(h, h->ysave.p, skip);
+      if (shell)
+        k_cy<<<grid_for(std::max<int64_t>(1, h->m_total) * 32, 256), 256, 0, s>>>(
+            h->m_total, T, h->row_sd.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, h->sv1.p, h->cy.p, skip,
+            mixed ? h->kform_corner.p : nullptr);
       CB_LAUNCH();
       k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
                                                              h->coarse_id.p, h->zc.p, h->cy.p, gl_loc, 0, skip);
@@ -1310,19 +1369,23 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
       k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p,
                                                              h->coarse_id.p, h->zc.p, h->cy.p, h->uvec.p, 1, skip);
       CB_LAUNCH();
-      if (corner)
-        k_h_correct<<<dim3(h->nsd, cr_blocks), 256, 0, s>>>(h->m_off.p, h->root_info.p, h->hroot.p, h->hslot.p,
-                                                            h->uvec.p, Yc, skip);
-      else
-        k_root_correct<<<dim3(h->nsd, cr_blocks), 256, 0, s>>>(h->root_info.p, h->m_off.p, h->fK.cslot.p, h->wroot.p,
-                                                               h->uvec.p, h->sv1.p, skip);
-      CB_LAUNCH();
+      if (corner) {  // shell subdomains of a mixed K have no H columns (np = 0)
+        k_h_correct<<<dim3(h->nsd, std::max(1, cr_corner)), 256, 0, s>>>(h->m_off.p, h->root_info.p, h->hroot.p,
+                                                                         h->hslot.p, h->uvec.p, h->ysave.p, skip);
+        CB_LAUNCH();
+      }
+      if (shell) {  // corner subdomains of a mixed K have no root columns in fKs
+        k_root_correct<<<dim3(h->nsd, std::max(1, cr_shell)), 256, 0, s>>>(h->root_info_s.p, h->m_off.p, fs.cslot.p,
+                                                                          h->wroot.p, h->uvec.p, h->sv1.p, skip);
+        CB_LAUNCH();
+      }
     }
     ps.close();
-    sweep_phase(h, tk, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, corner ? kSweepBwd : kSweepBwdRest);
+    if (corner) sweep_phase(h, h->tI, h->fK, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwd);
+    if (shell) sweep_phase(h, h->tK, fs, h->sv1.p, h->ysave.p, h->upd.p, skip, kSweepBwdRest);
     ps.next("apply vec 3b gather Av");
   } else {
-    if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, skip);
+    if (h->has_K) solve_k_device(h, h->sv1.p, skip);
     ps.next("apply vec 3b gather Av");
   }
   // v = Σ_copies w z~, every rank forms the same sum, also

@@ -472,7 +472,10 @@ cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x) {
     if (which != 0 && !h->has_K) throw Failure(CUTBDDC_INVALID_ARGUMENT, "no constrained Neumann factor (no interface)");
     DevBuf<double> X;
     X.upload(x, ns, h->stream);
-    solve_device(h, which == 0 ? h->tI : h->tplK(), which == 0 ? h->fI : h->fK, X.p, h->upd.p, h->ysave.p, nullptr);
+    if (which == 0)
+      solve_device(h, h->tI, h->fI, X.p, h->upd.p, h->ysave.p, nullptr);
+    else
+      solve_k_device(h, X.p, nullptr);
     X.download(x, ns, h->stream);
     CB_CUDA(cudaStreamSynchronize(h->stream));
   });
@@ -486,15 +489,15 @@ cutbddc_status cutbddc_gpu_time_solves(cutbddc_gpu* h, int reps, double* seconds
     if (reps < 1) reps = 1;
     // warm
     solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
-    if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, nullptr);
+    if (h->has_K) solve_k_device(h, h->sv1.p, nullptr);
     Timer tm(h->stream);
     for (int r = 0; r < reps; ++r) {
       solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
-      if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, nullptr);
+      if (h->has_K) solve_k_device(h, h->sv1.p, nullptr);
       solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
     }
     *seconds = tm.stop() / reps;
-    *bytes = 2.0 * sweep_bytes(h->fI) + (h->has_K ? sweep_bytes(h->fK) : 0.0);
+    *bytes = 2.0 * sweep_bytes(h->fI) + (h->has_K ? sweep_bytes(h->fK) + (h->k_mixed ? sweep_bytes(h->fKs) : 0.0) : 0.0);
   });
 }
 
@@ -524,7 +527,7 @@ cutbddc_status cutbddc_gpu_time_parts(cutbddc_gpu* h, int reps, double* us) {
     us[4] = timed([&] { apply_bddc_device(h, x.p, y.p, nullptr); });
     us[5] = timed([&] {
       solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
-      if (h->has_K) solve_device(h, h->tplK(), h->fK, h->sv1.p, h->upd.p, h->ysave.p, nullptr);
+      if (h->has_K) solve_k_device(h, h->sv1.p, nullptr);
       solve_device(h, h->tI, h->fI, h->sv0.p, h->upd.p, h->ysave.p, nullptr);
     });
     us[6] = timed([&] { spmv_device(h, x.p, y.p); });
@@ -545,8 +548,9 @@ cutbddc_status cutbddc_gpu_time_factor(cutbddc_gpu* h, double* seconds, double* 
       t += ms * 1e-3;
     }
     *seconds = t;
-    *flops_cholesky = h->fI.flops + (h->has_K ? h->fK.flops : 0.0);
-    *flops_inverse = h->fI.flops_inv + (h->has_K ? h->fK.flops_inv : 0.0);
+    const bool ks = h->has_K && h->k_mixed;
+    *flops_cholesky = h->fI.flops + (h->has_K ? h->fK.flops : 0.0) + (ks ? h->fKs.flops : 0.0);
+    *flops_inverse = h->fI.flops_inv + (h->has_K ? h->fK.flops_inv : 0.0) + (ks ? h->fKs.flops_inv : 0.0);
   });
 }
 
@@ -561,18 +565,20 @@ cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {
     st[1] = h->nsd;
     st[2] = h->n_coarse;
     st[3] = h->slots;
-    st[4] = h->fI.panel_total + h->fK.panel_total;
+    const int64_t pks = h->k_mixed ? h->fKs.panel_total : 0;
+    st[4] = h->fI.panel_total + h->fK.panel_total + pks;
     st[5] = (int64_t)h->tplK().tpl.sn.size();
     st[6] = (int64_t)h->tplK().tpl.levels.size();
     st[7] = h->m_max;
     st[8] = h->n_if;
     st[9] = g_kernel_launches.load();
     st[10] = h->fI.panel_total;
-    st[11] = h->fK.panel_total;
-    st[12] = (int64_t)(h->fI.flops + h->fK.flops);
+    st[11] = h->fK.panel_total + pks;
+    st[12] = (int64_t)(h->fI.flops + h->fK.flops + (h->k_mixed ? h->fKs.flops : 0.0));
     st[13] = h->world;
     st[14] = h->comm != nullptr;
     st[15] = h->has_K && h->k_corner;
+    st[16] = h->has_K && h->k_mixed ? h->n_shell_sd : 0;
   });
 }
 

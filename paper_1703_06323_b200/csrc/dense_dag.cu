@@ -62,6 +62,7 @@ struct DagGroup {
   FactorInput in;
   double* panel;
   unsigned long long* fail;
+  int* fail_sd;  // optional: per subdomain, set when one of its pivots is non-positive
 };
 
 constexpr int kMaxGroups = 2;
@@ -283,6 +284,7 @@ __device__ void tile_task(const DagArgs& a, const DagFront& d, int kind, int i, 
       const Supernode s = G.t.sn[d.sid];
       const int q = G.f.tpos[(int64_t)d.sd * G.t.rows_total + s.rows_off + col0 + jj];
       atomicMin(G.fail, (unsigned long long)((int64_t)d.sd * G.t.T + G.t.rows[s.rows_off + q]));
+      if (G.fail_sd) G.fail_sd[d.sd] = 1;
     });
     // (the panel above this diagonal tile is never read: the sweeps start
     // every column at the 32-row block holding its diagonal)
@@ -851,7 +853,7 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
   }
   std::vector<DagGroup> groups;
   for (const FactorSpan& sp : spans)
-    groups.push_back(DagGroup{tpl_dev(*sp.ts, h->slots), factor_dev(*sp.f), *sp.in, sp.f->panel.p, sp.fail});
+    groups.push_back(DagGroup{tpl_dev(*sp.ts, h->slots), factor_dev(*sp.f), *sp.in, sp.f->panel.p, sp.fail, sp.fail_sd});
   launch_dag(h, plan, front, groups, hit ? nullptr : &tasks);
 }
 
@@ -877,7 +879,7 @@ void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long
   fr[0].d.ntask = (int)kept.size();
   upload_plan(h, h->dag_dense, fr, kept);
   ps.close();
-  launch_dag(h, h->dag_dense, A, {DagGroup{TplDev{}, FactorDev{}, FactorInput{}, X, fail}}, &kept);
+  launch_dag(h, h->dag_dense, A, {DagGroup{TplDev{}, FactorDev{}, FactorInput{}, X, fail, nullptr}}, &kept);
 }
 
 }  // namespace cutbddc_b200

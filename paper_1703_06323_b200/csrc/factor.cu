@@ -216,15 +216,18 @@ void factor_symbolic(cutbddc_gpu* h, const TplSet& ts, const FactorInput& in, Fa
 // all their fronts fit a workspace budget of half the free device memory;
 // otherwise each runs alone in subdomain chunks bounded by the budget (every
 // chunk repeats the tree's critical path).
-void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const std::function<void()>& overlap) {
+void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const std::function<void()>& overlap,
+                    bool append_events) {
   cudaStream_t s = h->stream;
   const int nsd = h->nsd;
   DevBuf<unsigned long long>& fail = h->ws_fail;
   fail.alloc(jobs.size());
   CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8 * jobs.size(), s));
   DevBuf<double>& front = h->ws_front;
-  for (cudaEvent_t e : h->dag_ev) cudaEventDestroy(e);
-  h->dag_ev.clear();
+  if (!append_events) {
+    for (cudaEvent_t e : h->dag_ev) cudaEventDestroy(e);
+    h->dag_ev.clear();
+  }
   ProfScope pnum(h->prof, s, "factor numeric");
   int64_t all = 0;
   for (const FactorJob& j : jobs) all += j.f->h_front_base[(size_t)nsd];
@@ -241,7 +244,7 @@ void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const st
     std::vector<FactorSpan> spans;
     int64_t off = 0;
     for (size_t g = 0; g < jobs.size(); ++g) {
-      spans.push_back(FactorSpan{jobs[g].ts, jobs[g].in, jobs[g].f, 0, nsd, off, fail.p + g});
+      spans.push_back(FactorSpan{jobs[g].ts, jobs[g].in, jobs[g].f, 0, nsd, off, fail.p + g, jobs[g].fail_sd});
       off += jobs[g].f->h_front_base[(size_t)nsd];
     }
     if ((int64_t)front.n < all) front.alloc((size_t)std::max<int64_t>(1, all));
@@ -255,7 +258,8 @@ void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const st
         while (sd1 < nsd && f.h_front_base[(size_t)sd1 + 1] - f.h_front_base[(size_t)sd0] <= budget) ++sd1;
         const int64_t need = f.h_front_base[(size_t)sd1] - f.h_front_base[(size_t)sd0];
         if ((int64_t)front.n < need) front.alloc((size_t)need);
-        dense_dag_factor(h, {FactorSpan{jobs[g].ts, jobs[g].in, jobs[g].f, sd0, sd1, 0, fail.p + g}}, front.p);
+        dense_dag_factor(h, {FactorSpan{jobs[g].ts, jobs[g].in, jobs[g].f, sd0, sd1, 0, fail.p + g, jobs[g].fail_sd}},
+                         front.p);
         sd0 = sd1;
       }
     }
@@ -286,6 +290,13 @@ void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const st
 void solve_device(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* upd, double* ysave,
                   const int* skip) {
   sweep_solve(h, ts, f, X, ysave, upd, skip);
+}
+
+// The constrained Neumann solve of every subdomain: K_c (corner
+// formulation) or K (shell root); a mixed K takes each subdomain's own.
+void solve_k_device(cutbddc_gpu* h, double* X, const int* skip) {
+  solve_device(h, h->tplK(), h->fK, X, h->upd.p, h->ysave.p, skip);
+  if (h->k_mixed) solve_device(h, h->tK, h->fKs, X, h->upd.p, h->ysave.p, skip);
 }
 
 }  // namespace cutbddc_b200

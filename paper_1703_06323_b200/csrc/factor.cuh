@@ -70,20 +70,25 @@ struct FactorJob {
   FactorSet* f;
   const char* what;       // error message prefix (non-positive pivot)
   bool* failed = nullptr;  // set: a non-positive pivot is reported here instead of thrown
+  int* fail_sd = nullptr;  // device, optional: per subdomain, 1 where a pivot was non-positive
 };
 // `overlap`: host work run after the factorisation is enqueued, before the
-// pivot check waits for it (the sweep item lists)
-void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const std::function<void()>& overlap = {});
+// pivot check waits for it (the sweep item lists). append_events: keep the
+// previous call's timing events (a second factorisation of the same setup)
+void factor_numeric(cutbddc_gpu* h, const std::vector<FactorJob>& jobs, const std::function<void()>& overlap = {},
+                    bool append_events = false);
 // ysave: nsd x T doubles of scratch (forward results of big fronts).
 void solve_device(cutbddc_gpu* h, const TplSet& t, const FactorSet& f, double* X, double* upd, double* ysave,
                   const int* skip);
+void solve_k_device(cutbddc_gpu* h, double* X, const int* skip);
 // algorithmic bytes of one forward + backward sweep (panel lower parts + front vectors)
 double sweep_bytes(const FactorSet& f);
 // sweep.cu: dataflow sweeps for one right-hand side (plan built per factorisation)
 void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std::vector<int64_t>& poff,
                       const std::vector<int64_t>& uoff);
 // the sweeps' item lists (host; run while the GPU factorises: factor_numeric's overlap hook)
-void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f);
+// exclude (optional, per subdomain): subdomains whose fronts get no items
+void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std::vector<uint8_t>* exclude = nullptr);
 void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip);
 enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3, kSweepAttrOnly = 4 };
@@ -101,6 +106,7 @@ struct FactorSpan {
   int sd0, sd1;                // subdomains of this factorisation in the launch
   int64_t front_off;           // their front workspace offset in the launch's workspace
   unsigned long long* fail;    // pivot failure report
+  int* fail_sd = nullptr;      // per-subdomain failure flags (optional)
 };
 void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, double* front);
 // dense_dag.cu: Cholesky (A, column-major lower, overwritten) and X = L^{-1}

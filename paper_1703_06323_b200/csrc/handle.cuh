@@ -173,6 +173,14 @@ struct cutbddc_gpu {
   // K_c pivot is tiny or non-positive, or CUTBDDC_K_SHELL=1)
   bool k_corner = true;
   const TplSet& tplK() const { return k_corner ? tI : tK; }
+  // mixed K: the corner formulation on most subdomains, the shell-root K on
+  // the subdomains whose K_c is singular (floating fragments), factorised in fKs
+  bool k_mixed = false;
+  int n_shell_sd = 0;  // this rank's subdomains on the shell-root K (mixed)
+  FactorSet fKs;
+  cutbddc_b200::DevBuf<uint8_t> kform_shell, kform_corner;  // per subdomain (mixed K)
+  cutbddc_b200::DevBuf<uint8_t> mask_shell;                 // per slot: present slots of the shell subdomains
+  cutbddc_b200::DevBuf<int> ws_badsd;                       // per subdomain: K_c unusable
   cutbddc_b200::DevBuf<uint8_t> mask_int, mask_all;  // per (sd, slot)
   cutbddc_b200::DevBuf<double> diag_add;         // per (sd, slot): rho at corner slots
   cutbddc_b200::DevBuf<uint8_t> corner_row;      // per constraint row: 1 if a corner
@@ -209,7 +217,9 @@ struct cutbddc_gpu {
   // W_r = (K^{-1})_rr C_r^T (c_r x m, column-major); root_info[sd] =
   // {c_r, root panel offset, root vector offset (sweep), W_r offset}
   cutbddc_b200::DevBuf<double> sinv, wroot, hroot;
-  cutbddc_b200::DevBuf<int64_t> root_info;
+  cutbddc_b200::DevBuf<int64_t> root_info;       // corner formulation (see below)
+  cutbddc_b200::DevBuf<int64_t> root_info_s;     // shell formulation: {c_r, root panel off, root vec off, W_r off}
+  cutbddc_b200::DevBuf<double> hroot_s;          // shell formulation: H = G_r C_r^T
   // corner formulation: H = L^{-1} C^T over each subdomain's present slots in
   // front-column order (column-major, np_sd x m_sd at root_info[4 sd + 3]),
   // hslot[root_info[4 sd + 1] + k] = sd * T + slot of compact position k

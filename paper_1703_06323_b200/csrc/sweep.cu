@@ -777,7 +777,7 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
 
 // The sweeps' work items in dependency (critical-path) order. Needed only by
 // the solves, so setup builds them on the host while the GPU factorises.
-void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f) {
+void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std::vector<uint8_t>* exclude) {
   cudaStream_t s = h->stream;
   const Template& tp = ts.tpl;
   const int nsd = h->nsd, nsn = (int)tp.sn.size();
@@ -799,11 +799,13 @@ void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f) {
   auto front_items = [&](int L, bool fwd, std::vector<int4>& out) {
     for (int sid : lv[(size_t)L])
       for (int sd = 0; sd < nsd; ++sd) {
+        if (exclude && (*exclude)[(size_t)sd]) continue;
         const int2 v = f.h_rc[(size_t)sd * nsn + sid];
         if (v.x > 0 && (fwd ? is_small(v) : v.y == 0)) out.push_back(make_int4(kItemS, sid, sd, 0));
       }
     for (int sid : lv[(size_t)L])
       for (int sd = 0; sd < nsd; ++sd) {
+        if (exclude && (*exclude)[(size_t)sd]) continue;
         const size_t i = (size_t)sd * nsn + sid;
         const int2 v = f.h_rc[i];
         if (fwd && is_small(v)) continue;

@@ -465,10 +465,11 @@ class GpuSolver:
                     flops_cholesky=fc.value, flops_inverse=fi.value)
 
     def stats(self):
-        st = np.zeros(16, np.int64)
+        st = np.zeros(17, np.int64)
         _check(lib().cutbddc_gpu_stats(self.h, _p(st, C.c_int64)))
         keys = ["n_dof", "n_sd", "n_coarse", "slots", "panel_total", "n_supernodes", "levels", "m_max", "n_if",
-                "launches", "panel_interior", "panel_neumann", "factor_flops", "world", "has_comm", "k_corner"]
+                "launches", "panel_interior", "panel_neumann", "factor_flops", "world", "has_comm", "k_corner",
+                "k_shell_subdomains"]
         return {k: int(st[i]) for i, k in enumerate(keys)}
 
 
