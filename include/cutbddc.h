@@ -162,6 +162,15 @@ cutbddc_status cutbddc_gpu_cut_elements(cutbddc_gpu* h, int64_t* cells, double* 
 cutbddc_status cutbddc_gpu_local_system(cutbddc_gpu* h, double* stencil, uint8_t* mask_interior, uint8_t* mask_present,
                                         double* diag_add, int32_t* slot_dof);
 cutbddc_status cutbddc_gpu_local_solve(cutbddc_gpu* h, int which, double* x);
+/* Test hook: the tiled dense factorisation the coarse problem uses (one
+ * dataflow launch of 64 x 64 tile tasks, POTRF / TRSM / GEMM on DMMA and the
+ * explicit inverse) on a plain n x n SPD matrix a (column-major; the lower
+ * part is read): l = L (a = L L^T), x = L^{-1}, column-major in their lower
+ * parts (the strict upper parts are unspecified); either may be NULL. A non-positive pivot returns
+ * CUTBDDC_SINGULAR with its index in *pivot (-1 otherwise). Replaces, for
+ * dense matrices, SparseCholesky::compute (linalg.cpp:34-62). */
+cutbddc_status cutbddc_gpu_dense_cholesky(cutbddc_gpu* h, int n, const double* a, double* l, double* x,
+                                          int64_t* pivot);
 /* Statistics (17 slots): [0]=n_dof [1]=n_sd [2]=n_coarse [3]=template slots
  * [4]=factor panel doubles (both factorisations, all subdomains)
  * [5]=supernodes (Neumann template) [6]=levels [7]=max m_w [8]=n_interface

@@ -415,6 +415,34 @@ cutbddc_status cutbddc_gpu_coarse_matrix(cutbddc_gpu* h, double* ac, int* n_coar
   });
 }
 
+cutbddc_status cutbddc_gpu_dense_cholesky(cutbddc_gpu* h, int n, const double* a, double* l, double* x,
+                                          int64_t* pivot) {
+  return guard([&] {
+    need(h);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (n < 0 || (n > 0 && !a)) throw Failure(CUTBDDC_INVALID_ARGUMENT, "dense_cholesky: bad matrix");
+    if (pivot) *pivot = -1;
+    if (n == 0) return;
+    const size_t nn = (size_t)n * n;
+    DevBuf<double> A, X;
+    DevBuf<unsigned long long> fail;
+    A.upload(a, nn, h->stream);
+    X.alloc(nn);
+    fail.alloc(1);
+    CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, h->stream));
+    dense_dag_matrix(h, A.p, X.p, n, fail.p);
+    unsigned long long f = 0;
+    CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, h->stream));
+    if (l) A.download(l, nn, h->stream);
+    if (x) X.download(x, nn, h->stream);
+    CB_CUDA(cudaStreamSynchronize(h->stream));
+    if (f != ~0ull) {
+      if (pivot) *pivot = (int64_t)f;
+      throw Failure(CUTBDDC_SINGULAR, "dense_cholesky: not positive definite (pivot " + std::to_string(f) + ")");
+    }
+  });
+}
+
 cutbddc_status cutbddc_gpu_cells(cutbddc_gpu* h, double* beta, uint8_t* empty, int64_t* n_active) {
   return guard([&] {
     need(h);

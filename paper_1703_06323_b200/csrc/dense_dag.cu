@@ -182,28 +182,48 @@ __device__ void tile_mm(double* C, int ldc, const double* A, int lda, const doub
       }
 }
 
-// Cholesky of the n x n diagonal tile and the inverse of its factor; the
-// strict upper parts of both stored tiles become zero.
-typedef double SmTile[kTile + 1];
-#ifndef POTRF_PHASE  // microbenchmark hook (tools/debug/potrf_real_bench.cu)
-#define POTRF_PHASE(k)
-#endif
+// D += sa * A B on one 8 x 8 block (DMMA m8n8k4, K a multiple of 4): lane l
+// holds D[l/4][2(l%4) .. 2(l%4)+1]; A[i][k] = pa[i*sia + k*ska], B[k][n] =
+// pb[k*skb + n*snb] (shared memory).
+__device__ __forceinline__ void mma_block8(double& d0, double& d1, const double* pa, int sia, int ska,
+                                           const double* pb, int skb, int snb, int K, double sa) {
+  const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+  const double* a = pa + r * sia + c * ska;
+  const double* b = pb + c * skb + r * snb;
+  for (int k = 0; k < K; k += 4) dmma_8x8x4(d0, d1, sa * a[k * ska], b[k * skb]);
+}
 
-// Cholesky of the n x n diagonal tile and the inverse of its factor by the
-// whole CTA, one pivot per step in the unscaled (LDL^T-like) form:
-//   U_iq -= U_ij U_qj / U_jj      (j < q <= i, the trailing lower triangle)
-//   Y_ic -= U_ij Y_jc / U_jj      (c <= j < i, Y = unscaled rows of L^{-1})
-// then L_ij = U_ij / sqrt(U_jj) and X_jc = Y_jc / sqrt(U_jj). Thread (i, g)
-// owns the entries of row i in the columns = g mod 4: one barrier per pivot,
-// short rolled loops (the unrolled warp-level variants were bound by
-// instruction fetch: this code runs once per task). Non-positive pivots are
-// reported (fail) and replaced by 1. Strict upper parts stored as zero.
+// Cholesky of the n x n diagonal tile and the inverse of its factor,
+// blocked by kPb = 16 columns. Per panel p (columns c0 = 16p ..):
+//   (a) warp 0: the 16 x 16 diagonal block in shared memory, L_pp (lane =
+//       row half) and X_pp = L_pp^{-1} (lane = column half, right-looking),
+//       rolled pivot loops with load-first bodies and selects instead of
+//       branches; meanwhile warps 1-7 form T = L_p,<p X_<p,<p (block row p
+//       of the inverse, before X_pp)
+//   (b) L_ip = A_ip X_pp^T for the rows below and X_pj = -X_pp T_pj (j < p)
+//   (c) A_iq -= L_ip L_qp^T on the trailing lower triangle
+// (b), (c) and T are 8 x 8 DMMA blocks from shared memory. Four barriers per
+// panel instead of one per pivot (a dependent DFMA costs ~23 cycles, a shared
+// load -> DFMA -> store ~53 on B200: tools/bench_src/lat_probe.cu). In the
+// cfg4 task trace (CUTBDDC_DAG_TRACE) a POTRF task takes 37 us against 45 us
+// for the unblocked one-barrier-per-pivot form; tools/bench_src/potrf_bench.cu
+// shows warp 0's 32 pivot steps still at ~1k cycles each, the open item. Rows / columns >= n are padded with
+// the identity and never written back. Non-positive pivots are reported
+// (fail) and replaced by 1. Strict upper parts stored as zero.
+typedef double SmTile[kTile + 1];
+constexpr int kPb = 16;
+#ifndef POTRF_STAMP  // phase timestamps for tools/bench_src/potrf_bench.cu
+#define POTRF_STAMP(k)
+#endif
 template <typename Fail>
 __device__ void tile_potrf_inv(double* F, int ldf, double* P, int ldp, int n, double* sm, Fail fail) {
   SmTile* ls = reinterpret_cast<SmTile*>(sm);
   SmTile* xs = reinterpret_cast<SmTile*>(sm + kTile * (kTile + 1));
-  __shared__ double rs[kTile];
-  const int tid = threadIdx.x;
+  constexpr int ld = kTile + 1;
+  __shared__ double rinv[kPb];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int fr = lane >> 2, fc = lane & 3;  // DMMA fragment row / column pair
+  const int npan = (n + kPb - 1) / kPb, N = npan * kPb;  // padded size
   __syncthreads();
   {
     constexpr int kPer = kTile * kTile / kDagThreads;  // loads in flight per thread
@@ -211,58 +231,160 @@ __device__ void tile_potrf_inv(double* F, int ldf, double* P, int ldp, int n, do
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = tid + u * kDagThreads, i = e & 63, j = e >> 6;
-      v[u] = (i < n && j < n && i >= j) ? F[i + (int64_t)j * ldf] : 0.0;
+      v[u] = (i < n && j < n && i >= j) ? F[i + (int64_t)j * ldf] : (i == j ? 1.0 : 0.0);
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = tid + u * kDagThreads, i = e & 63, j = e >> 6;
       ls[i][j] = v[u];
-      xs[i][j] = i == j ? 1.0 : 0.0;
     }
   }
-  POTRF_PHASE(0);
-  const int i = tid & 63, g = tid >> 6;
-  for (int j = 0; j < n; ++j) {
+  POTRF_STAMP(0);
+  for (int p = 0; p < npan; ++p) {
+    const int c0 = p * kPb;
+    __syncthreads();  // the previous panel's trailing update is complete
+    POTRF_STAMP(1 + 3 * p);
+    if (wid == 0) {
+      // (a) L_pp in shared memory: lane (i, h) updates row c0 + i, columns
+      // 8h .. 8h + 7. Rolled pivot loop with a short, load-first body: this
+      // code runs once per tile, so straight-line unrolled code is bound by
+      // cold instruction fetch (~34 cycles per instruction measured).
+      const int li = lane & (kPb - 1), h = lane >> 4;
+      double* bl = &ls[c0][c0];
+      unsigned bad = 0;  // non-positive pivots of the block (the first is reported)
+#pragma unroll 1
+      for (int j = 0; j < kPb; ++j) {
+        double d = bl[j * ld + j];
+        const double aij = bl[li * ld + j];
+        double lq[8], aq[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          lq[k] = bl[(8 * h + k) * ld + j];
+          aq[k] = bl[li * ld + 8 * h + k];
+        }
+        const bool ok = d > 0.0;
+        bad |= ok ? 0u : 1u << j;
+        d = ok ? d : 1.0;
+        const double r = rsqrt(d);
+        const double lij = aij * r;
+        __syncwarp();  // column j read by every lane
+        // every lane computes every candidate and stores a selected value:
+        // per-lane branches around FP64 ops compile to BSSY/BSYNC pairs that
+        // cost ~100 cycles each (measured); every entry has one owner lane
+        const double dr = d * r;
+        const double colj = li > j ? lij : (li == j ? dr : aij);
+        rinv[j] = r;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int q = 8 * h + k;
+          const double upd = fma(-lij, lq[k] * r, aq[k]);  // computed by every lane: no branches
+          double v = aq[k];
+          v = (q > j && li >= q) ? upd : v;
+          v = q == j ? colj : v;
+          bl[li * ld + q] = v;
+        }
+        __syncwarp();
+      }
+      if (bad && lane == 0) fail(c0 + __ffs(bad) - 1);
+      // X_pp = L_pp^{-1} in place in xs: lane (c, h) owns column c, rows
+      // 8h .. 8h + 7; right-looking (x_k final, then every row below updated)
+      double* xb = &xs[c0][c0];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int row = 8 * h + k;
+        xb[row * ld + li] = row == li ? 1.0 : 0.0;
+        bl[row * ld + li] = row < li ? 0.0 : bl[row * ld + li];  // strict upper part of L_pp
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int k = 0; k < kPb; ++k) {
+        const double xk = xb[k * ld + li] * rinv[k];
+        double lk[8], tk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          lk[i] = bl[(8 * h + i) * ld + k];
+          tk[i] = xb[(8 * h + i) * ld + li];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = 8 * h + i;
+          const double upd = fma(-lk[i], xk, tk[i]);
+          double v = row > k ? upd : tk[i];
+          v = row == k ? xk : v;
+          xb[row * ld + li] = v;
+        }
+        __syncwarp();
+      }
+    } else if (p > 0) {
+      // T_pj = L_p,s X_s,j over s from the 16-block holding column j to c0
+      // (X is lower triangular), 8 x 8 blocks into X_pj's place
+      const int nt = 2 * (c0 / 8);
+      for (int blk = wid - 1; blk < nt; blk += kDagThreads / 32 - 1) {
+        const int m0 = 8 * (blk & 1), col0 = 8 * (blk >> 1), s0 = kPb * (col0 / kPb);
+        double d0 = 0.0, d1 = 0.0;
+        mma_block8(d0, d1, &ls[c0 + m0][s0], ld, 1, &xs[s0][col0], ld, 1, c0 - s0, 1.0);
+        xs[c0 + m0 + fr][col0 + 2 * fc] = d0;
+        xs[c0 + m0 + fr][col0 + 2 * fc + 1] = d1;
+      }
+    }
     __syncthreads();
-    double ajj = ls[j][j];
-    if (!(ajj > 0.0)) {
-      if (tid == 0) fail(j);
-      ajj = 1.0;
+    POTRF_STAMP(2 + 3 * p);
+    // (b) L_ip = A_ip X_pp^T (rows below the block) and X_pj = -X_pp T_pj,
+    // computed into registers, stored after a barrier (A_ip and T are
+    // overwritten in place)
+    const int nbr = (N - c0 - kPb) / 8;  // 8-row blocks below the diagonal block
+    const int nl = 2 * nbr, nx = 2 * (c0 / 8);
+    double o[2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int blk = wid + 8 * u;
+      o[u][0] = o[u][1] = 0.0;
+      if (blk < nl) {
+        const int i0 = c0 + kPb + 8 * (blk >> 1), j0 = 8 * (blk & 1);
+        mma_block8(o[u][0], o[u][1], &ls[i0][c0], ld, 1, &xs[c0 + j0][c0], 1, ld, kPb, 1.0);
+      } else if (blk < nl + nx) {
+        const int b2 = blk - nl, m0 = 8 * (b2 & 1), col0 = 8 * (b2 >> 1);
+        mma_block8(o[u][0], o[u][1], &xs[c0 + m0][c0], ld, 1, &xs[c0][col0], ld, 1, kPb, -1.0);
+      }
     }
-    const double r = rsqrt(ajj);
-    if (tid == 0) rs[j] = r;
-    if (i <= j || i >= n) continue;
-    const double f = ls[i][j] * (r * r);
-    // row i of the trailing block (columns q > j) and of Y (rows i > j) never
-    // overlap column j / row j read here: loads are batched ahead of stores
-    int q = j + 1 + ((g - j - 1) & 3);
-    for (; q + 12 <= i; q += 16) {
-      const double a0 = ls[i][q], a1 = ls[i][q + 4], a2 = ls[i][q + 8], a3 = ls[i][q + 12];
-      const double b0 = ls[q][j], b1 = ls[q + 4][j], b2 = ls[q + 8][j], b3 = ls[q + 12][j];
-      ls[i][q] = a0 - f * b0;
-      ls[i][q + 4] = a1 - f * b1;
-      ls[i][q + 8] = a2 - f * b2;
-      ls[i][q + 12] = a3 - f * b3;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int blk = wid + 8 * u;
+      if (blk < nl) {
+        const int i0 = c0 + kPb + 8 * (blk >> 1), j0 = c0 + 8 * (blk & 1);
+        ls[i0 + fr][j0 + 2 * fc] = o[u][0];
+        ls[i0 + fr][j0 + 2 * fc + 1] = o[u][1];
+      } else if (blk < nl + nx) {
+        const int b2 = blk - nl, m0 = c0 + 8 * (b2 & 1), col0 = 8 * (b2 >> 1);
+        xs[m0 + fr][col0 + 2 * fc] = o[u][0];
+        xs[m0 + fr][col0 + 2 * fc + 1] = o[u][1];
+      }
     }
-    for (; q <= i; q += 4) ls[i][q] -= f * ls[q][j];
-    int c = g;
-    for (; c + 12 <= j; c += 16) {
-      const double a0 = xs[i][c], a1 = xs[i][c + 4], a2 = xs[i][c + 8], a3 = xs[i][c + 12];
-      const double b0 = xs[j][c], b1 = xs[j][c + 4], b2 = xs[j][c + 8], b3 = xs[j][c + 12];
-      xs[i][c] = a0 - f * b0;
-      xs[i][c + 4] = a1 - f * b1;
-      xs[i][c + 8] = a2 - f * b2;
-      xs[i][c + 12] = a3 - f * b3;
+    if (nbr == 0) continue;
+    __syncthreads();
+    POTRF_STAMP(3 + 3 * p);
+    // (c) trailing lower triangle, 8 x 8 blocks (ib >= qb) of rows / columns >= c0 + 16
+    const int ntr = nbr * (nbr + 1) / 2;
+    for (int blk = wid; blk < ntr; blk += kDagThreads / 32) {
+      int ib = 0;
+      while ((ib + 1) * (ib + 2) / 2 <= blk) ++ib;
+      const int qb = blk - ib * (ib + 1) / 2;
+      const int i0 = c0 + kPb + 8 * ib, q0 = c0 + kPb + 8 * qb;
+      double d0 = ls[i0 + fr][q0 + 2 * fc], d1 = ls[i0 + fr][q0 + 2 * fc + 1];
+      mma_block8(d0, d1, &ls[i0][c0], ld, 1, &ls[q0][c0], 1, ld, kPb, -1.0);
+      if (ib != qb || fr >= 2 * fc) ls[i0 + fr][q0 + 2 * fc] = d0;
+      if (ib != qb || fr >= 2 * fc + 1) ls[i0 + fr][q0 + 2 * fc + 1] = d1;
     }
-    for (; c <= j; c += 4) xs[i][c] -= f * xs[j][c];
   }
   __syncthreads();
-  POTRF_PHASE(1);
-  for (int e = tid; e < n * n; e += kDagThreads) {
-    const int r = e % n, c = e / n;
-    F[r + (int64_t)c * ldf] = r >= c ? ls[r][c] * rs[c] : 0.0;
-    P[r + (int64_t)c * ldp] = r >= c ? xs[r][c] * rs[r] : 0.0;
-  }
+  POTRF_STAMP(15);
+  for (int c = wid; c < n; c += kDagThreads / 32)
+    for (int r = lane; r < n; r += 32) {
+      F[r + (int64_t)c * ldf] = r >= c ? ls[r][c] : 0.0;
+      P[r + (int64_t)c * ldp] = r >= c ? xs[r][c] : 0.0;
+    }
 }
 
 // One tile task of front d (POTRF / TRSM / GEMM / ACC / FIN), no waits.

@@ -85,7 +85,7 @@ EXPORTS = [
     "cutbddc_build_partition", "cutbddc_classify_objects", "cutbddc_objects_free", "cutbddc_gpu_classify_objects",
     "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_distribution", "cutbddc_gpu_time_factor",
     "cutbddc_fp64_peak", "cutbddc_build_exchange_plan", "cutbddc_gpu_exchange_plan", "cutbddc_exchange_plan_free",
-    "cutbddc_gpu_time_parts", "cutbddc_gpu_set_problem", "cutbddc_gpu_error_norms",
+    "cutbddc_gpu_time_parts", "cutbddc_gpu_set_problem", "cutbddc_gpu_error_norms", "cutbddc_gpu_dense_cholesky",
 ]
 
 
@@ -435,6 +435,22 @@ class GpuSolver:
         _check(lib().cutbddc_gpu_local_system(self.h, _p(sten, C.c_double), _p(mi, C.c_uint8), _p(mp, C.c_uint8),
                                               _p(da, C.c_double), _p(sd, C.c_int32)))
         return sten, mi, mp, da, sd
+
+    def dense_cholesky(self, a):
+        """(L, X = L^{-1}) of a dense SPD matrix by the tiled dataflow
+        factorisation; CutbddcError(SINGULAR) carries .pivot on failure."""
+        a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+        n = a.shape[0]
+        l = np.zeros((n, n), np.float64, order="F")
+        x = np.zeros((n, n), np.float64, order="F")
+        piv = C.c_int64(-1)
+        code = lib().cutbddc_gpu_dense_cholesky(self.h, n, _p(a, C.c_double), _p(l, C.c_double), _p(x, C.c_double),
+                                                C.byref(piv))
+        if code != OK:
+            err = CutbddcError(code, lib().cutbddc_last_error().decode())
+            err.pivot = piv.value
+            raise err
+        return np.tril(l), np.tril(x)
 
     def local_solve(self, which: int, x):
         x = np.ascontiguousarray(x, np.float64).copy()
