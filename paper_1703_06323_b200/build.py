@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libcutbddc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NO_FMA = {"geometry.cu", "element.cu"}
-CU = ["geometry.cu", "element.cu", "assembly.cu", "dist.cu", "factor.cu", "sweep.cu", "dense_dag.cu", "bddc.cu", "pcg.cu",
+CU = ["geometry.cu", "element.cu", "assembly.cu", "dist.cu", "factor.cu", "sweep.cu", "dense_dag.cu", "coarse_sparse.cu", "bddc.cu", "pcg.cu",
       "objects.cu", "peak.cu", "capi.cu"]
 CPP = ["nd_template.cpp", "host_partition.cpp"]
 def _nccl_dir() -> str:

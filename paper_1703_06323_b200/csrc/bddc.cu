@@ -1205,7 +1205,12 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   // ---- coarse matrix + factorisation
   ps_host.next("setup 4 coarse assemble+chol+inverse");
   h->acoarse.alloc((size_t)std::max(1, nc * nc));
-  h->acoarse_inv.alloc((size_t)std::max(1, nc * nc));
+  // n_c <= kCoarseInverseMax: dense Cholesky + explicit inverse (one GEMV per
+  // apply); larger: the nested-dissection factor (coarse_sparse.cu)
+  // (CUTBDDC_COARSE=dense / sparse forces one path: A/B runs, tests)
+  const char* coarse_env = std::getenv("CUTBDDC_COARSE");
+  const std::string coarse_mode = coarse_env ? coarse_env : "";
+  h->coarse_sparse = coarse_mode == "sparse" || (nc > kCoarseInverseMax && coarse_mode != "dense");
   if (nc > 0) {
     h->acoarse.zero(s);
     // every subdomain's A_c,w on every rank, then the same assembly in
@@ -1214,23 +1219,29 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     k_coarse_assemble<<<nc, 128, 0, s>>>(nc, h->cg_ptr.p, h->cg_idx.p, h->srow.p, h->scoarse.p, h->ac_loc.p,
                                          h->acoarse.p);
     CB_LAUNCH();
-    // Cholesky of A_c and X = L^{-1} by the tiled dense DAG (A_c is
-    // symmetric, so its row-major buffer is its column-major lower part);
-    // the apply solves with X^T (X g): two triangular GEMVs.
-    DevBuf<double>& Lc = h->ws_lc;
-    Lc.alloc((size_t)nc * nc);
-    CB_CUDA(cudaMemcpyAsync(Lc.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
     DevBuf<unsigned long long>& fail = h->ws_fail;
     fail.alloc(1);
     CB_CUDA(cudaMemsetAsync(fail.p, 0xff, 8, s));
-    dense_dag_matrix(h, Lc.p, h->acoarse_inv.p, nc, fail.p);
-    if (nc <= kCoarseInverseMax) {
-      h->acoarse_full.alloc((size_t)nc * nc);
-      const int nb64 = (nc + 63) / 64;
-      k_xtx<<<dim3(nb64, nb64), 256, 0, s>>>(nc, h->acoarse_inv.p, h->acoarse_full.p);
-      CB_LAUNCH();
+    if (h->coarse_sparse) {
+      coarse_sparse_setup(h, nc, obj_of_gsd);
+      coarse_sparse_factor(h, h->acoarse.p, nc, fail.p);
     } else {
-      h->ws_cpart.alloc((size_t)((nc + 63) / 64) * nc);
+      // Cholesky of A_c and X = L^{-1} by the tiled dense DAG (A_c is
+      // symmetric, so its row-major buffer is its column-major lower part);
+      // the apply solves with X^T (X g): two triangular GEMVs.
+      h->acoarse_inv.alloc((size_t)std::max(1, nc * nc));
+      DevBuf<double>& Lc = h->ws_lc;
+      Lc.alloc((size_t)nc * nc);
+      CB_CUDA(cudaMemcpyAsync(Lc.p, h->acoarse.p, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, s));
+      dense_dag_matrix(h, Lc.p, h->acoarse_inv.p, nc, fail.p);
+      if (nc <= kCoarseInverseMax) {
+        h->acoarse_full.alloc((size_t)nc * nc);
+        const int nb64 = (nc + 63) / 64;
+        k_xtx<<<dim3(nb64, nb64), 256, 0, s>>>(nc, h->acoarse_inv.p, h->acoarse_full.p);
+        CB_LAUNCH();
+      } else {
+        h->ws_cpart.alloc((size_t)((nc + 63) / 64) * nc);
+      }
     }
     unsigned long long f = 0;
     CB_CUDA(cudaMemcpyAsync(&f, fail.p, 8, cudaMemcpyDeviceToHost, s));
@@ -1313,7 +1324,7 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
     const int cr_shell = shell ? (int)((h->tK.tpl.sn.back().ncols + 255) / 256) : 0;
     const int cr_blocks = std::max(1, std::max(cr_corner, cr_shell));
     double* gl_loc = h->gl.p + (int64_t)h->dist_rank * h->maxrows;  // this rank's rows of the staged gl
-    if (!mixed && h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
+    if (!mixed && !h->coarse_sparse && h->n_coarse <= kCoarseInverseMax && h->m_max <= kFusedCoarseM) {
       double* Yc = corner ? h->ysave.p : h->sv1.p;  // where cy is read and the correction lands
       const int64_t* rinfo = corner ? h->root_info.p : h->root_info_s.p;
       if (corner) {  // cy = H^T y' (a warp per constraint row), gl = S^{-1} cy
@@ -1352,7 +1363,9 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
       gather_rows(h);
       k_coarse_rhs<<<grid_for(h->n_coarse, 128), 128, 0, s>>>(h->n_coarse, h->cg_ptr.p, h->cg_idx.p, h->gl.p, h->gc.p, skip);
       CB_LAUNCH();
-      if (h->n_coarse <= kCoarseInverseMax) {
+      if (h->coarse_sparse) {  // the nested-dissection factor's two level sweeps
+        coarse_sparse_solve(h, h->gc.p, h->zc.p, skip);
+      } else if (h->n_coarse <= kCoarseInverseMax) {
         k_coarse_gemv<<<grid_for((int64_t)h->n_coarse * 32, 256), 256, 0, s>>>(h->n_coarse, h->acoarse_full.p, h->gc.p,
                                                                              h->zc.p, skip);
         CB_LAUNCH();

@@ -1004,4 +1004,40 @@ void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long
   launch_dag(h, h->dag_dense, A, {DagGroup{TplDev{}, FactorDev{}, FactorInput{}, X, fail, nullptr}}, &kept);
 }
 
+void dense_dag_fronts(cutbddc_gpu* h, DagPlan& plan, double* F, double* X, const std::vector<DenseFront>& fronts,
+                      unsigned long long* fail) {
+  if (fronts.empty()) return;
+  ProfScope ps(h->prof, h->stream, "dense dag host+upload");
+  std::vector<HostFront> fr(fronts.size());
+  for (size_t q = 0; q < fronts.size(); ++q) {
+    HostFront& hf = fr[q];
+    hf = HostFront{};
+    DagFront& d = hf.d;
+    d.fo = fronts[q].fo;
+    d.po = fronts[q].po;
+    d.r = fronts[q].r;
+    d.c = fronts[q].c;
+    d.np = (d.c + kTile - 1) / kTile;
+    d.nt = d.np + (d.r - d.c + kTile - 1) / kTile;
+    d.sd = d.sid = -1;
+    d.ch0 = d.ch1 = -1;
+    hf.parent = -1;
+  }
+  std::vector<int4> tasks = build_tasks(fr);
+  std::vector<int4> kept;
+  std::vector<int> ntask(fr.size(), 0);
+  for (const int4& tk : tasks)
+    if ((tk.x >> 24) != kAsm) {
+      kept.push_back(tk);
+      ++ntask[(size_t)(tk.x & 0xffffff)];
+    }
+  for (size_t q = 0; q < fr.size(); ++q) {  // assembled in place: no ASM tasks
+    fr[q].d.nasm = 0;
+    fr[q].d.ntask = ntask[q];
+  }
+  upload_plan(h, plan, fr, kept);
+  ps.close();
+  launch_dag(h, plan, F, {DagGroup{TplDev{}, FactorDev{}, FactorInput{}, X, fail, nullptr}}, &kept);
+}
+
 }  // namespace cutbddc_b200

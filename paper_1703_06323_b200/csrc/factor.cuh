@@ -112,6 +112,17 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
 // dense_dag.cu: Cholesky (A, column-major lower, overwritten) and X = L^{-1}
 // of one dense SPD matrix; a failing pivot index goes to *fail
 void dense_dag_matrix(cutbddc_gpu* h, double* A, double* X, int n, unsigned long long* fail);
+// dense_dag.cu: partial Cholesky of independent dense fronts in one launch:
+// front q is r x r (column-major lower at F + fo), its first c columns are
+// eliminated, the panel [L11^{-1}; L21 L11^{-1}] (r x c, ld r) goes to
+// X + po and the trailing (r - c) block becomes the update matrix
+void dense_dag_fronts(cutbddc_gpu* h, DagPlan& plan, double* F, double* X, const std::vector<DenseFront>& fronts,
+                      unsigned long long* fail);
+// coarse_sparse.cu: symbolic (nested dissection on the subdomain lattice),
+// numeric factorisation of the dense-stored A_c, and z = A_c^{-1} g
+void coarse_sparse_setup(cutbddc_gpu* h, int nc, const std::vector<std::vector<int>>& obj_of_gsd);
+void coarse_sparse_factor(cutbddc_gpu* h, const double* Ac, int nc, unsigned long long* fail);
+void coarse_sparse_solve(cutbddc_gpu* h, const double* g, double* z, const int* skip);
 // peak.cu: FP64 tensor (DMMA) and FP64 FMA throughput microbenchmarks, TFLOP/s
 void fp64_peaks(int device, double* dmma_tflops, double* dfma_tflops);
 

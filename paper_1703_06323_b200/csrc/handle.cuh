@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -41,6 +42,28 @@ struct DagPlan {
   std::vector<int2> key;                       // spans + compact front sizes the list was built for
   int n_tasks = 0;
   int64_t n_counters = 0;
+};
+
+// dense_dag.cu: one dense front of a dense_dag_fronts launch (factor.cuh)
+struct DenseFront {
+  int64_t fo, po;
+  int r, c;
+};
+
+// coarse_sparse.cu: the nested-dissection multifrontal factor of A_c
+// (n_c > kCoarseInverseMax)
+struct CoarseSparse {
+  bool ready = false;
+  int nlev = 0, rt_max = 0, n_fronts = 0;
+  double flops = 0.0;
+  std::vector<int> level_ptr;                   // fronts of level l: flist[level_ptr[l] ..)
+  std::vector<int> level_rt, level_c;           // per level: largest front / pivot block (solve grids)
+  std::vector<std::vector<DenseFront>> dense;  // per level, for dense_dag_fronts
+  std::vector<std::unique_ptr<DagPlan>> plans;  // per level
+  cutbddc_b200::DevBuf<long long> fronts;      // CsFront records
+  cutbddc_b200::DevBuf<int32_t> idx, cmap;     // per front: coarse ids (columns, rows); children's row maps
+  cutbddc_b200::DevBuf<int> flist;             // front ids by level
+  cutbddc_b200::DevBuf<double> F, P, ybuf, ubuf;
 };
 
 // One factorisation over a template, compacted per subdomain (masked-out
@@ -264,6 +287,8 @@ struct cutbddc_gpu {
   DagPlan dag_factor;                              // dense_dag.cu: the subdomain factorisations (one launch)
   std::vector<cudaEvent_t> dag_ev;                 // start/stop event pairs of the last numeric factorisation's launches
   DagPlan dag_dense;                               // dense_dag.cu: the coarse matrix factorisation
+  CoarseSparse csparse;                            // coarse_sparse.cu: sparse A_c factor (large n_c)
+  bool coarse_sparse = false;                      // the apply solves A_c by csparse
 
   // pcg vectors
   cutbddc_b200::DevBuf<double> px, pr, pz, pp, pq, pb, hist, lal, lbe;
