@@ -29,10 +29,13 @@
 #include <algorithm>
 #include <chrono>
 #include <map>
+#include <memory>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+
+#include <cub/cub.cuh>
 
 #include "factor.cuh"
 #include "front_asm.cuh"
@@ -659,35 +662,38 @@ struct SplitShape {
   std::vector<int4> ft;  // (kind << 24, i, j, k); the front id is or-ed in per front
   std::vector<int> bl;
   int top = 0;           // bottom level of the first POTRF (bl_p[0])
+  int maxbl = 0;         // largest entry of bl
+  int dev = -1;          // index in the device template table (dense_dag_factor)
 };
 
-std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
-  std::vector<int4> all;  // every task, front by front
-  std::vector<int> all_bl;
-  std::vector<int> entry(fr.size(), 0);  // bottom level of a front's first (children-waiting) tasks
+int g_shape_builds = 0;  // CUTBDDC_DAG_STATS: split shapes built by the last task list
+std::chrono::steady_clock::time_point g_bt_sort_t0;  // start of its sort (stats)
+
+// The tile tasks of a split front with np pivot / nt tile blocks and their
+// bottom levels relative to the front's parent entry: a pure function of
+// (np, nt), kept across calls (per host thread: batched handles run on
+// several).
+SplitShape& split_shape(int np, int nt) {
+  constexpr int kShapeDim = 64;
+  thread_local std::vector<std::unique_ptr<SplitShape>> shape_tab((size_t)kShapeDim * kShapeDim);
+  thread_local std::map<std::pair<int, int>, SplitShape> shapes;  // (larger fronts)
+  SplitShape* shp;
+  if (np < kShapeDim && nt < kShapeDim) {
+    std::unique_ptr<SplitShape>& u = shape_tab[(size_t)np * kShapeDim + nt];
+    if (!u) u = std::make_unique<SplitShape>();
+    shp = u.get();
+  } else {
+    shp = &shapes[std::make_pair(np, nt)];
+  }
+  SplitShape& sh = *shp;
+  if (!sh.ft.empty() || np == 0) return sh;
+  ++g_shape_builds;
   std::vector<int4> ft;
   std::vector<int> bl, bl_p, bl_t, bl_g, bl_a, bl_f;
-  std::map<std::pair<int, int>, SplitShape> shapes;
-  for (size_t q = fr.size(); q-- > 0;) {  // parents before children
-    HostFront& hf = fr[q];
-    DagFront& d = hf.d;
-    const int id = (int)q, np = d.np, nt = d.nt;
-    const int off = hf.parent >= 0 ? entry[(size_t)hf.parent] : 0;
-    ft.clear();
-    bl.clear();
-    auto push = [&](int kind, int i, int j, int kk, int b) {
-      ft.push_back(make_int4((kind << 24) | id, i, j, kk));
-      bl.push_back(b);
-    };
-    if (d.whole) {
-      int w = 1;  // assembly, then the tile tasks in list order (POTRF ~3 tile updates)
-      for (int k = 0; k < np; ++k) w += 3 + (nt - k - 1) * (1 + (nt - k) / 2) + k + (k + 1) * (nt - k - 1);
-      push(kWhole, 0, 0, 0, off + w);
-      entry[q] = off + w;
-      d.ntask = 1;
-    } else {
-      SplitShape& sh = shapes[std::make_pair(np, nt)];
-      if (sh.ft.empty() && np > 0) {
+  auto push = [&](int kind, int i, int j, int kk, int b) {
+    ft.push_back(make_int4(kind << 24, i, j, kk));
+    bl.push_back(b);
+  };
       for (int k = 0; k < np; ++k) {  // per front, step by step (successors later)
         push(kPotrf, k, k, k, 0);
         for (int i = k + 1; i < nt; ++i) push(kTrsm, i, k, k, 0);
@@ -746,7 +752,7 @@ std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
         for (size_t x = 0; x < ft.size(); ++x) {
           const int kind = ft[x].x >> 24, i = ft[x].y, j = ft[x].z, k = ft[x].w;
           if (kind == kTrsm && i == k + 1 && i < np) {
-            ft[x].x = (kDiag << 24) | id;
+            ft[x].x = (kDiag << 24);
           } else if ((kind == kGemm && i == j && i == k + 1 && i < np) || (kind == kPotrf && k > 0)) {
             continue;
           }
@@ -761,38 +767,101 @@ std::vector<int4> build_tasks(std::vector<HostFront>& fr) {
       for (int4& t : sh.ft) t.x &= ~0xffffff;  // kind only: the front id is or-ed in per front
       sh.bl = bl;
       sh.top = np > 0 ? bl_p[0] : 0;
-      }
-      ft.clear();
-      bl.clear();
-      for (size_t x = 0; x < sh.ft.size(); ++x) {
-        const int4 t = sh.ft[x];
-        ft.push_back(make_int4(t.x | (int)q, t.y, t.z, t.w));
-        bl.push_back(sh.bl[x] + off);
-      }
-      // assembly: ASM tiles, then the PEN rows, before every k = 0 task
+  for (int b2 : sh.bl) sh.maxbl = std::max(sh.maxbl, b2);
+  return sh;
+}
+
+// Per-front task bookkeeping in emission order (fronts from last to first:
+// parents before children): bottom-level offsets, task counts and offsets.
+struct FrontPlan {
+  int q;          // front index
+  SplitShape* sh;  // null: one W task
+  int off, lvl;   // parent entry offset; W task / ASM bottom level
+  int npen;
+  int64_t pen0, task_off;
+};
+int64_t plan_front_tasks(std::vector<HostFront>& fr, std::vector<FrontPlan>& fp, int& maxbl) {
+  std::vector<int> entry(fr.size(), 0);  // bottom level of a front's first (children-waiting) tasks
+  fp.clear();
+  fp.reserve(fr.size());
+  maxbl = 0;
+  int64_t tot = 0;
+  for (size_t q = fr.size(); q-- > 0;) {
+    HostFront& hf = fr[q];
+    DagFront& d = hf.d;
+    const int np = d.np, nt = d.nt;
+    const int off = hf.parent >= 0 ? entry[(size_t)hf.parent] : 0;
+    FrontPlan f{(int)q, nullptr, off, 0, 0, 0, tot};
+    if (d.whole) {
+      int w = 1;  // assembly, then the tile tasks in list order (POTRF ~3 tile updates)
+      for (int k = 0; k < np; ++k) w += 3 + (nt - k - 1) * (1 + (nt - k) / 2) + k + (k + 1) * (nt - k - 1);
+      f.lvl = entry[q] = off + w;
+      d.ntask = 1;
+      maxbl = std::max(maxbl, f.lvl);
+    } else {
+      SplitShape& sh = split_shape(np, nt);
+      f.sh = &sh;
       const int top = sh.top + off;
-      const int npen = (int)(hf.pen1 - hf.pen0);
-      const int asm_bl = 1 + top + (npen > 0 ? 1 : 0);
-      for (int i = 0; i < nt; ++i)
-        for (int j = 0; j <= i; ++j) push(kAsm, i, j, 0, asm_bl);
-      for (int64_t row = hf.pen0; row < hf.pen1; ++row) push(kPen, (int)row, 0, 0, top + 1);
+      f.npen = (int)(hf.pen1 - hf.pen0);
+      f.pen0 = hf.pen0;
+      f.lvl = entry[q] = 1 + top + (f.npen > 0 ? 1 : 0);  // ASM tiles, then PEN rows, before every k = 0 task
       d.ntile = nt * (nt + 1) / 2;
-      d.nasm = d.ntile + npen;
-      d.ntask = (int)ft.size();
-      entry[q] = asm_bl;
+      d.nasm = d.ntile + f.npen;
+      d.ntask = (int)sh.ft.size() + d.nasm;
+      maxbl = std::max(maxbl, std::max(sh.maxbl + off, f.lvl));
     }
-    all.insert(all.end(), ft.begin(), ft.end());
-    all_bl.insert(all_bl.end(), bl.begin(), bl.end());
+    tot += d.ntask;
+    fp.push_back(f);
   }
-  // decreasing bottom level, stable (counting sort)
+  return tot;
+}
+
+// Host task list (the small launches: dense matrices, coarse fronts): every
+// front's tasks in emission order, then decreasing bottom level, stable
+// (counting sort). The buffers persist per host thread.
+std::vector<int4>& build_tasks(std::vector<HostFront>& fr) {
+  g_shape_builds = 0;
+  thread_local std::vector<int4> all;
+  thread_local std::vector<int> all_bl;
+  thread_local std::vector<int4> tasks_out;
+  thread_local std::vector<FrontPlan> fp;
   int maxbl = 0;
-  for (int b : all_bl) maxbl = std::max(maxbl, b);
-  std::vector<int64_t> start((size_t)maxbl + 2, 0);
-  for (int b : all_bl) ++start[(size_t)(maxbl - b) + 1];
-  for (size_t b = 1; b < start.size(); ++b) start[b] += start[b - 1];
-  std::vector<int4> tasks(all.size());
-  for (size_t x = 0; x < all.size(); ++x) tasks[(size_t)start[(size_t)(maxbl - all_bl[x])]++] = all[x];
-  return tasks;
+  const int64_t tot = plan_front_tasks(fr, fp, maxbl);
+  all.resize((size_t)tot);
+  all_bl.resize((size_t)tot);
+  for (const FrontPlan& f : fp) {
+    const int id = f.q;
+    size_t x = (size_t)f.task_off;
+    if (!f.sh) {
+      all[x] = make_int4((kWhole << 24) | id, 0, 0, 0);
+      all_bl[x] = f.lvl;
+      continue;
+    }
+    const SplitShape& sh = *f.sh;
+    for (size_t t = 0; t < sh.ft.size(); ++t, ++x) {
+      const int4 v = sh.ft[t];
+      all[x] = make_int4(v.x | id, v.y, v.z, v.w);
+      all_bl[x] = sh.bl[t] + f.off;
+    }
+    const int nt = fr[(size_t)id].d.nt;
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i; ++j, ++x) {
+        all[x] = make_int4((kAsm << 24) | id, i, j, 0);
+        all_bl[x] = f.lvl;
+      }
+    for (int t = 0; t < f.npen; ++t, ++x) {
+      all[x] = make_int4((kPen << 24) | id, (int)(f.pen0 + t), 0, 0);
+      all_bl[x] = sh.top + f.off + 1;
+    }
+  }
+  g_bt_sort_t0 = std::chrono::steady_clock::now();
+  thread_local std::vector<int64_t> start;
+  start.assign((size_t)maxbl + 2, 0);
+  for (int b2 : all_bl) ++start[(size_t)(maxbl - b2) + 1];
+  for (size_t b2 = 1; b2 < start.size(); ++b2) start[b2] += start[b2 - 1];
+  tasks_out.resize(all.size());
+  for (size_t x = 0; x < all.size(); ++x) tasks_out[(size_t)start[(size_t)(maxbl - all_bl[x])]++] = all[x];
+  return tasks_out;
 }
 
 // One persistent launch over the plan's task list.
@@ -863,7 +932,12 @@ void launch_dag(cutbddc_gpu* h, DagPlan& plan, double* front, const std::vector<
 
 // Device copy of a host front list + task list (counters: per front done,
 // assembled, then the A and X tile triangles of a split front).
+void upload_plan_fronts(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, int64_t n_tasks);
 void upload_plan(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, const std::vector<int4>& tasks) {
+  upload_plan_fronts(h, plan, fr, (int64_t)tasks.size());
+  plan.tasks.upload(tasks, h->stream);
+}
+void upload_plan_fronts(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, int64_t n_tasks) {
   cudaStream_t s = h->stream;
   if (fr.size() >= (1u << 24)) throw Failure(CUTBDDC_CONFIG, "dense dag: too many fronts");
   std::vector<DagFront> dv(fr.size());
@@ -876,10 +950,104 @@ void upload_plan(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, cons
   }
   static_assert(sizeof(DagFront) == 10 * sizeof(long long), "DagFront layout");
   plan.fronts.upload(reinterpret_cast<const long long*>(dv.data()), dv.size() * 10, s);
-  plan.tasks.upload(tasks, s);
-  plan.n_tasks = (int)tasks.size();
+  if (n_tasks >= (1ll << 31)) throw Failure(CUTBDDC_CONFIG, "dense dag: too many tasks");
+  plan.n_tasks = (int)n_tasks;
   plan.n_counters = cnt;
   plan.counters.alloc((size_t)cnt + 1);
+}
+
+// Device task list (the subdomain factorisation: up to ~1e6 tasks). The
+// host keeps the per-front bookkeeping (plan_front_tasks) and the (np, nt)
+// shape templates; one block per front writes its tasks in emission order
+// with sort keys maxbl - bottom level, and a stable radix sort gives the
+// same list as the host counting sort (build_tasks).
+struct DevFrontPlan {
+  long long task_off, pen0;
+  int q, shape, off, lvl, npen, nt, top, pad_;
+};
+__global__ void k_expand_tasks(const DevFrontPlan* __restrict__ fp, const int4* __restrict__ tpl,
+                               const int* __restrict__ tpl_bl, const int2* __restrict__ tpl_rng, int maxbl,
+                               int4* __restrict__ out, unsigned* __restrict__ keys) {
+  const DevFrontPlan f = fp[blockIdx.x];
+  const long long o = f.task_off;
+  if (f.shape < 0) {
+    if (threadIdx.x == 0) {
+      out[o] = make_int4((kWhole << 24) | f.q, 0, 0, 0);
+      keys[o] = (unsigned)(maxbl - f.lvl);
+    }
+    return;
+  }
+  const int2 rg = tpl_rng[f.shape];  // (first, count)
+  for (int x = threadIdx.x; x < rg.y; x += blockDim.x) {
+    const int4 t = tpl[rg.x + x];
+    out[o + x] = make_int4(t.x | f.q, t.y, t.z, t.w);
+    keys[o + x] = (unsigned)(maxbl - (tpl_bl[rg.x + x] + f.off));
+  }
+  const int na = f.nt * (f.nt + 1) / 2;
+  for (int x = threadIdx.x; x < na; x += blockDim.x) {  // ASM tile (i, j <= i), row-major over the lower triangle
+    int i = (int)((sqrt(8.0 * x + 1.0) - 1.0) * 0.5);
+    while ((i + 1) * (i + 2) / 2 <= x) ++i;
+    while (i * (i + 1) / 2 > x) --i;
+    out[o + rg.y + x] = make_int4((kAsm << 24) | f.q, i, x - i * (i + 1) / 2, 0);
+    keys[o + rg.y + x] = (unsigned)(maxbl - f.lvl);
+  }
+  for (int t = threadIdx.x; t < f.npen; t += blockDim.x) {
+    out[o + rg.y + na + t] = make_int4((kPen << 24) | f.q, (int)(f.pen0 + t), 0, 0);
+    keys[o + rg.y + na + t] = (unsigned)(maxbl - (f.top + f.off + 1));
+  }
+}
+
+void build_tasks_device(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr) {
+  cudaStream_t s = h->stream;
+  g_shape_builds = 0;
+  thread_local std::vector<FrontPlan> fp;
+  int maxbl = 0;
+  const int64_t tot = plan_front_tasks(fr, fp, maxbl);
+  // shape templates used by this list
+  std::map<SplitShape*, int> sid;
+  std::vector<int4> tpl;
+  std::vector<int> tpl_bl;
+  std::vector<int2> rng;
+  std::vector<DevFrontPlan> dfp(fp.size());
+  for (size_t x = 0; x < fp.size(); ++x) {
+    const FrontPlan& f = fp[x];
+    int id = -1;
+    if (f.sh) {
+      auto it = sid.find(f.sh);
+      if (it == sid.end()) {
+        id = (int)rng.size();
+        sid[f.sh] = id;
+        rng.push_back(make_int2((int)tpl.size(), (int)f.sh->ft.size()));
+        tpl.insert(tpl.end(), f.sh->ft.begin(), f.sh->ft.end());
+        tpl_bl.insert(tpl_bl.end(), f.sh->bl.begin(), f.sh->bl.end());
+      } else {
+        id = it->second;
+      }
+    }
+    dfp[x] = DevFrontPlan{f.task_off, f.pen0, f.q, id, f.off, f.lvl, f.npen, fr[(size_t)f.q].d.nt,
+                          f.sh ? f.sh->top : 0, 0};
+  }
+  upload_plan_fronts(h, plan, fr, tot);
+  static_assert(sizeof(DevFrontPlan) == 48, "DevFrontPlan layout");
+  plan.d_fplan.upload(reinterpret_cast<const long long*>(dfp.data()), dfp.size() * 6, s);
+  plan.d_tpl.upload(tpl.empty() ? std::vector<int4>{make_int4(0, 0, 0, 0)} : tpl, s);
+  plan.d_tpl_bl.upload(tpl_bl.empty() ? std::vector<int>{0} : tpl_bl, s);
+  plan.d_tpl_rng.upload(rng.empty() ? std::vector<int2>{make_int2(0, 0)} : rng, s);
+  plan.keys.alloc((size_t)2 * std::max<int64_t>(1, tot));
+  plan.unsorted.alloc((size_t)std::max<int64_t>(1, tot));
+  plan.tasks.alloc((size_t)std::max<int64_t>(1, tot));
+  k_expand_tasks<<<(unsigned)fp.size(), 128, 0, s>>>(reinterpret_cast<const DevFrontPlan*>(plan.d_fplan.p), plan.d_tpl.p,
+                                                     plan.d_tpl_bl.p, plan.d_tpl_rng.p, maxbl, plan.unsorted.p,
+                                                     plan.keys.p);
+  CB_LAUNCH();
+  int bits = 1;
+  while (bits < 32 && (maxbl >> bits) != 0) ++bits;
+  size_t tmp = 0;
+  CB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, plan.keys.p, plan.keys.p + tot, plan.unsorted.p, plan.tasks.p,
+                                          (int)tot, 0, bits, s));
+  plan.sort_tmp.alloc(std::max<size_t>(1, tmp));
+  CB_CUDA(cub::DeviceRadixSort::SortPairs(plan.sort_tmp.p, tmp, plan.keys.p, plan.keys.p + tot, plan.unsorted.p,
+                                          plan.tasks.p, (int)tot, 0, bits, s));
 }
 
 }  // namespace
@@ -915,7 +1083,7 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
   const bool hit = plan.key.size() == key.size() &&
                    std::memcmp(plan.key.data(), key.data(), sizeof(int2) * key.size()) == 0 &&
                    !std::getenv("CUTBDDC_DAG_TRACE") && !std::getenv("CUTBDDC_NO_PLAN_CACHE");
-  std::vector<int4> tasks;
+  const std::vector<int4>* tasks = nullptr;
   if (!hit) {
     ProfScope ps(h->prof, s, "dense dag host+upload");
     std::vector<HostFront> fr;
@@ -962,13 +1130,26 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
     }
     if (fr.empty()) return;
     const auto t0 = std::chrono::steady_clock::now();
-    tasks = build_tasks(fr);
+    build_tasks_device(h, plan, fr);
     const auto t1 = std::chrono::steady_clock::now();
-    upload_plan(h, plan, fr, tasks);
+    if (std::getenv("CUTBDDC_DAG_CHECK")) {  // test hook: the device list equals the host list
+      std::vector<int4> dl = plan.tasks.to_host(s);
+      const std::vector<int4>& hl = build_tasks(fr);
+      dl.resize((size_t)plan.n_tasks);
+      if (dl.size() != hl.size() || std::memcmp(dl.data(), hl.data(), sizeof(int4) * hl.size()) != 0)
+        throw Failure(CUTBDDC_INTERNAL, "dense dag: device task list differs from the host list");
+    }
+    if (std::getenv("CUTBDDC_DAG_TRACE")) {  // the trace dump wants the list on the host
+      thread_local std::vector<int4> tl;
+      tl = plan.tasks.to_host(s);
+      tl.resize((size_t)plan.n_tasks);
+      tasks = &tl;
+    }
     plan.key = key;
     if (std::getenv("CUTBDDC_DAG_STATS")) {
       const auto t2 = std::chrono::steady_clock::now();
-      std::fprintf(stderr, "[dag stats] fronts %zu tasks %zu build %.2f ms upload %.2f ms\n", fr.size(), tasks.size(),
+      std::fprintf(stderr, "[dag stats] fronts %zu tasks %d shapes %d build+enqueue %.2f ms, then %.2f ms\n",
+                   fr.size(), plan.n_tasks, g_shape_builds,
                    std::chrono::duration<double, std::milli>(t1 - t0).count(),
                    std::chrono::duration<double, std::milli>(t2 - t1).count());
     }
@@ -976,7 +1157,7 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
   std::vector<DagGroup> groups;
   for (const FactorSpan& sp : spans)
     groups.push_back(DagGroup{tpl_dev(*sp.ts, h->slots), factor_dev(*sp.f), *sp.in, sp.f->panel.p, sp.fail, sp.fail_sd});
-  launch_dag(h, plan, front, groups, hit ? nullptr : &tasks);
+  launch_dag(h, plan, front, groups, hit ? nullptr : tasks);
 }
 
 // Cholesky + explicit inverse factor of one dense SPD n x n matrix (A:

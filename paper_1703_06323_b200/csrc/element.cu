@@ -713,7 +713,10 @@ __device__ double reg_gen_eigs_max(const double (&d)[8], const double (&b)[8], i
 }
 
 // eight lanes per cut cell: beta_e, K_e = h (D + beta M - N - N^T), F_e = h^3 F
-__global__ void __launch_bounds__(256) k_cut_pencil(double h, int64_t ncut, int problem, const double* __restrict__ accs,
+#ifndef CB_PENCIL_MINB
+#define CB_PENCIL_MINB 1
+#endif
+__global__ void __launch_bounds__(256, CB_PENCIL_MINB) k_cut_pencil(double h, int64_t ncut, int problem, const double* __restrict__ accs,
                                                      const int* __restrict__ nvs, double* __restrict__ ke,
                                                      double* __restrict__ fe, double* __restrict__ beta,
                                                      uint8_t* __restrict__ empty, int* __restrict__ degenerate) {

@@ -40,6 +40,13 @@ struct DagPlan {
   cutbddc_b200::DevBuf<int4> tasks;            // (kind << 24 | front, i, j, k) in ticket order
   cutbddc_b200::DevBuf<int> counters;          // per front: done, assembled, tile counters; then the ticket
   std::vector<int2> key;                       // spans + compact front sizes the list was built for
+  // device-built task lists (dense_dag.cu build_tasks_device)
+  cutbddc_b200::DevBuf<long long> d_fplan;     // per front: DevFrontPlan
+  cutbddc_b200::DevBuf<int4> d_tpl, unsorted;  // shape templates; the list before the sort
+  cutbddc_b200::DevBuf<int> d_tpl_bl;
+  cutbddc_b200::DevBuf<int2> d_tpl_rng;
+  cutbddc_b200::DevBuf<unsigned> keys;         // sort keys in / out
+  cutbddc_b200::DevBuf<uint8_t> sort_tmp;
   int n_tasks = 0;
   int64_t n_counters = 0;
 };

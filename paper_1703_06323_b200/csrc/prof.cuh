@@ -24,8 +24,12 @@ struct Prof {
   struct Rec {
     std::string name;
     cudaEvent_t a, b;
-    double host_ms;  // host wall time spent inside the scope (enqueue + host work)
+    double host_ms;     // host wall time spent inside the scope (enqueue + host work)
+    double host_start;  // host ms since the first scope (timeline mode)
   };
+  bool timeline = false;  // CUTBDDC_PROFILE=2: also print every scope in order
+  cudaEvent_t base = nullptr;
+  std::chrono::steady_clock::time_point hbase;
   std::vector<Rec> pending;
   std::map<std::string, std::pair<long long, double>> tot;  // name -> (count, ms)
   std::map<std::string, double> mx;                         // name -> max ms of one scope
@@ -33,13 +37,20 @@ struct Prof {
 
   Prof() {
     const char* e = std::getenv("CUTBDDC_PROFILE");
-    on = e && e[0] == '1';
+    on = e && (e[0] == '1' || e[0] == '2');
+    timeline = e && e[0] == '2';
   }
   void flush() {
     for (auto& r : pending) {
       cudaEventSynchronize(r.b);
       float ms = 0;
       cudaEventElapsedTime(&ms, r.a, r.b);
+      if (timeline && base) {  // device start / duration and host start, ms from the first scope
+        float st = 0;
+        cudaEventElapsedTime(&st, base, r.a);
+        std::fprintf(stderr, "[cutbddc timeline] %-40s dev %9.3f +%8.3f  host %9.3f +%8.3f\n", r.name.c_str(), st, ms,
+                     r.host_start, r.host_ms);
+      }
       auto& t = tot[r.name];
       t.first += 1;
       t.second += ms;
@@ -89,6 +100,11 @@ struct ProfScope {
     cudaEventCreate(&a);
     cudaEventRecord(a, s);
     t0 = std::chrono::steady_clock::now();
+    if (prof.timeline && !prof.base) {
+      cudaEventCreate(&prof.base);
+      cudaEventRecord(prof.base, s);
+      prof.hbase = t0;
+    }
   }
   void close() {
     if (!p || !a) return;
@@ -96,7 +112,7 @@ struct ProfScope {
     cudaEventCreate(&b);
     cudaEventRecord(b, s);
     const double hm = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    p->pending.push_back({name, a, b, hm});
+    p->pending.push_back({name, a, b, hm, std::chrono::duration<double, std::milli>(t0 - p->hbase).count()});
     if (p->pending.size() > 4096) p->flush();
     a = nullptr;
   }

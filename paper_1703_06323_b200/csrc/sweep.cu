@@ -46,6 +46,12 @@ namespace {
 #ifndef CUTBDDC_SWEEP_MIN_BLOCKS
 #define CUTBDDC_SWEEP_MIN_BLOCKS 4
 #endif
+#ifndef CUTBDDC_SWEEP_BWD_ROWS
+#define CUTBDDC_SWEEP_BWD_ROWS 64
+#endif
+#ifndef CUTBDDC_SWEEP_SLOT_DOUBLES
+#define CUTBDDC_SWEEP_SLOT_DOUBLES 2176
+#endif
 // (the CUTBDDC_SWEEP_* macros exist for tools/tune_sweep.sh)
 constexpr int kSmallRows = 256;                     // fronts with at most this many rows: one forward item
 constexpr int kFwdRows = CUTBDDC_SWEEP_FWD_ROWS;    // forward items of larger fronts: row blocks ...
@@ -57,8 +63,8 @@ constexpr int kSlots = CUTBDDC_SWEEP_SLOTS;         // staging ring depth (chunk
 constexpr int kMinBlocks = CUTBDDC_SWEEP_MIN_BLOCKS;
 constexpr int kThreadsSweep = 256;                  // consumer threads (+ one producer warp)
 constexpr int kWarps = kThreadsSweep / 32;
-constexpr int kBwdRowsChunk = 64;                   // backward chunk: bwd_cols columns x 64 rows
-constexpr int kSlot = 2176;                         // doubles per ring slot (17 KB)
+constexpr int kBwdRowsChunk = CUTBDDC_SWEEP_BWD_ROWS;  // backward chunk: bwd_cols columns x 64 rows
+constexpr int kSlot = CUTBDDC_SWEEP_SLOT_DOUBLES;       // doubles per ring slot (17 KB)
 constexpr int kMaxSegs = 32;                        // column segments per chunk
 constexpr int kVecDoubles = 2048;                   // front vector: >= every template front
 constexpr int kItems = 1;                           // item records (consumers release theirs once its dependencies are met)

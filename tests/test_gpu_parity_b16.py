@@ -174,3 +174,25 @@ def test_cfg5_matches_golden():
     """BASELINE.json configs[4] (256^3, {stiffness, cef}) against the oracle's
     golden result."""
     _check_golden(_golden("solve_cfg5.json"), configs.get("cfg5"))
+
+
+def test_device_task_list_equals_host(monkeypatch):
+    """The factorisation's task list is expanded and radix-sorted on the
+    device (dense_dag.cu build_tasks_device); CUTBDDC_DAG_CHECK=1 rebuilds it
+    on the host (plan_front_tasks + counting sort) and fails setup on any
+    difference. cfg4 (43k tasks) with the constraint-row PEN tasks of the
+    shell K (CUTBDDC_K_MIXED_EVERY), and cfg2."""
+    monkeypatch.setenv("CUTBDDC_DAG_CHECK", "1")
+    monkeypatch.setenv("CUTBDDC_NO_PLAN_CACHE", "1")
+    for name, env in (("cfg4", {}), ("cfg4", {"CUTBDDC_K_MIXED_EVERY": "3"}), ("cfg2", {})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        cfg = configs.get(name)
+        s = cb.GpuSolver(0)
+        pb = cb.prepare(s, cfg)
+        s.setup_bddc(pb.objects, cfg.weighting)
+        x, rep = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
+        assert rep["converged"]
+        s.close()
+        for k in env:
+            monkeypatch.delenv(k)
