@@ -716,7 +716,10 @@ __device__ double reg_gen_eigs_max(const double (&d)[8], const double (&b)[8], i
 #ifndef CB_PENCIL_MINB
 #define CB_PENCIL_MINB 1
 #endif
-__global__ void __launch_bounds__(256, CB_PENCIL_MINB) k_cut_pencil(double h, int64_t ncut, int problem, const double* __restrict__ accs,
+#ifndef CB_PENCIL_THREADS
+#define CB_PENCIL_THREADS 256
+#endif
+__global__ void __launch_bounds__(CB_PENCIL_THREADS, CB_PENCIL_MINB) k_cut_pencil(double h, int64_t ncut, int problem, const double* __restrict__ accs,
                                                      const int* __restrict__ nvs, double* __restrict__ ke,
                                                      double* __restrict__ fe, double* __restrict__ beta,
                                                      uint8_t* __restrict__ empty, int* __restrict__ degenerate) {
@@ -958,7 +961,8 @@ void cut_elements_device(cutbddc_gpu* h) {
       k_cut_acc<<<(unsigned)((h->n_cut + kAccCells - 1) / kAccCells), 32 * kAccCells, 0, h->stream>>>(
           h->n_cut, q8all.p, accs.p, nvs.p, la);
       CB_LAUNCH();
-      k_cut_pencil<<<(unsigned)((h->n_cut * 8 + 255) / 256), 256, 0, h->stream>>>(
+      k_cut_pencil<<<(unsigned)((h->n_cut * 8 + CB_PENCIL_THREADS - 1) / CB_PENCIL_THREADS), CB_PENCIL_THREADS, 0,
+                     h->stream>>>(
           h->h, h->n_cut, h->problem, accs.p, nvs.p, h->ke.p, h->fe.p, h->beta.p, h->empty.p, degen.p);
       CB_LAUNCH();
     }

@@ -93,6 +93,7 @@ struct SweepDev {
   int32_t* rbcnt;   // forward range arrivals per (chunked front, row block)
   double* vbuf;
   int fwd_cols, bwd_cols;  // item sizes of this factorisation's plan
+  int l2_policy;           // panel loads: 0 default, 1 L2 evict_last (keep resident), 2 L2 evict_first (stream)
   unsigned long long* trace;  // CUTBDDC_SWEEP_TRACE: per item {grab, deps met, done, sm}, else null
 };
 
@@ -139,6 +140,21 @@ __device__ __forceinline__ void bulk_g2s(double* dst, const double* src, uint32_
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(b))
                : "memory");
+}
+// the same with an L2 eviction-priority hint (createpolicy)
+__device__ __forceinline__ void bulk_g2s_hint(double* dst, const double* src, uint32_t bytes, uint64_t* b,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_of(int kind) {
+  uint64_t pol = 0;
+  if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 
 // The consumer warps synchronise among themselves with named barrier 1: the
@@ -233,7 +249,7 @@ struct SlotRec {
 // per column segment, 16-byte aligned: a segment starting at an odd element
 // copies one leading double more; rows past a segment's end are never read).
 __device__ __forceinline__ void produce_chunk(const FrontDesc& d, const Chunk& ch, const double* __restrict__ panel,
-                                              double* buf, int* segoff, SlotRec& sr) {
+                                              double* buf, int* segoff, SlotRec& sr, int l2_kind, uint64_t pol) {
   const int lane = threadIdx.x & 31;
   const int stride = seg_stride(ch.hi - ch.lo);
   const int jj = lane;
@@ -254,7 +270,12 @@ __device__ __forceinline__ void produce_chunk(const FrontDesc& d, const Chunk& c
     mbar_expect_tx(&sr.full, bytes);
   }
   __syncwarp();
-  if (n > 0) bulk_g2s(buf + jj * stride, panel + a, (uint32_t)(8 * n), &sr.full);
+  if (n > 0) {
+    if (l2_kind)
+      bulk_g2s_hint(buf + jj * stride, panel + a, (uint32_t)(8 * n), &sr.full, pol);
+    else
+      bulk_g2s(buf + jj * stride, panel + a, (uint32_t)(8 * n), &sr.full);
+  }
 }
 
 // Producer warp main loop: take tickets in order, publish each item, stream
@@ -263,6 +284,7 @@ __device__ void producer(const SweepDev& p, const int4* __restrict__ items, int 
                          const double* __restrict__ panel, ItemRec* rec, SlotRec* sr, double* ring, int* segoff,
                          bool fwd) {
   const int lane = threadIdx.x & 31;
+  const uint64_t pol = l2_policy_of(p.l2_policy);
   int chunk_seq = 0;
   for (int k = 0;; ++k) {
     ItemRec& R = rec[k % kItems];
@@ -302,7 +324,8 @@ __device__ void producer(const SweepDev& p, const int4* __restrict__ items, int 
     for (int q = 0; q < g.nchunk; ++q, ++chunk_seq) {
       const int slot = chunk_seq % kSlots;
       if (chunk_seq >= kSlots) mbar_wait(&sr[slot].empty, ((chunk_seq / kSlots) - 1) & 1);
-      produce_chunk(d, chunk_of(g, q, fwd), panel, ring + slot * kSlot, segoff + slot * kMaxSegs, sr[slot]);
+      produce_chunk(d, chunk_of(g, q, fwd), panel, ring + slot * kSlot, segoff + slot * kMaxSegs, sr[slot],
+                    p.l2_policy, pol);
     }
   }
 }
@@ -619,6 +642,7 @@ SweepDev sweep_dev(const FactorSet& f, int nsd, int nsn, unsigned long long* tra
                   const_cast<double*>(f.vbuf.p),
                   f.fwd_cols,
                   f.bwd_cols,
+                  f.l2_policy_f,
                   trace};
 }
 
@@ -673,6 +697,17 @@ void choose_item_sizes(cutbddc_gpu* h, FactorSet& f) {
   f.fwd_cols = std::max(16, std::min(kSmallRows, fc));  // <= kSmallRows: the multi-RHS front vector fits
   f.bwd_cols = bc;
   f.small_work = std::max(1, sw);
+  // L2 eviction priority of the panel loads (0 default, 1 evict_last, 2
+  // evict_first). The panels (172 MB at cfg4) do not fit the 126 MB L2, and
+  // streaming them evict_first keeps the apply's vectors, maps and coarse
+  // basis resident: measured on B200, cfg4 PCG 6.25 -> 5.96 ms, cfg5 239 ->
+  // 235 ms. CUTBDDC_SWEEP_L2=iF,iB,kF,kB overrides (interior / Neumann
+  // factor, forward / backward sweep).
+  int pol[4] = {2, 2, 2, 2};
+  if (const char* e = std::getenv("CUTBDDC_SWEEP_L2")) std::sscanf(e, "%d,%d,%d,%d", pol, pol + 1, pol + 2, pol + 3);
+  const bool interior = &f == &h->fI;
+  f.l2_policy_f = interior ? pol[0] : pol[2];
+  f.l2_policy_b = interior ? pol[1] : pol[3];
 }
 
 void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std::vector<int64_t>& poff,
@@ -961,9 +996,11 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
   if (phase == kSweepBwdRoot) b1 = f.n_items_b_root;
   if (phase == kSweepBwdRest) b0 = f.n_items_b_root, slot = 2;
   ProfScope ps(h->prof, s, tag + " bwd");
+  SweepDev pb = p;
+  pb.l2_policy = f.l2_policy_b;
   if (b1 > b0) {
     const int g = std::min(b1 - b0, sweep_grid((const void*)k_sweep_bwd));
-    k_sweep_bwd<<<g, kThreadsSweep + 32, shm, s>>>(p, f.items_b.p + b0, b1 - b0, f.panel.p, X, ysave, skip, slot);
+    k_sweep_bwd<<<g, kThreadsSweep + 32, shm, s>>>(pb, f.items_b.p + b0, b1 - b0, f.panel.p, X, ysave, skip, slot);
     CB_LAUNCH();
   }
   if (tp && phase == kSweepBwd) dump_trace(std::string(tp) + "_" + tag + "_bwd.bin", f, false, s);
