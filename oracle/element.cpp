@@ -18,13 +18,44 @@
 
 namespace oracle {
 
-// Cyclic Jacobi: a (n x n row-major, destroyed) -> eigenvalues ev, vectors v
-// (columns, row-major storage v[i*n+k]). Sweep order p<q row-wise; stop when
-// the off-diagonal Frobenius norm is <= 1e-300 or after 100 sweeps; rotations
-// skipped when |a_pq| is exactly zero.
+// Jacobi rotation (c, s) annihilating a_pq from h = a_qq - a_pp, g = 2 a_pq
+// (g != 0): t = tan = sgn / (|theta| + sqrt(theta^2 + 1)) with theta = h / g,
+// c = 1 / sqrt(t^2 + 1), s = t c, evaluated without theta as c = d / w,
+// s = sgn |g| / w with d = |h| + sqrt(h^2 + g^2), w = sqrt(d^2 + g^2) (two
+// square roots and one division deep instead of two and three); the theta
+// form is the fallback when the squares under- or overflow.
+void jacobi_rotation(double h, double g, double* c, double* s) {
+  const double sgn = (h == 0.0 || (h > 0.0) == (g > 0.0)) ? 1.0 : -1.0;
+  const double rho = std::sqrt(h * h + g * g);
+  const double d = std::fabs(h) + rho;
+  const double w = std::sqrt(d * d + g * g);
+  if (w > 0.0 && w <= 1.7976931348623157e308) {
+    *c = d / w;
+    *s = sgn * std::fabs(g) / w;
+    return;
+  }
+  const double theta = h / g;
+  const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+  *c = 1.0 / std::sqrt(t * t + 1.0);
+  *s = t * *c;
+}
+
+// Parallel-order cyclic Jacobi: a (n x n row-major, destroyed) -> eigenvalues
+// ev, vectors v (columns, row-major storage v[i*n+k]). A sweep visits every
+// pair (p, q), p < q, once, in round-robin (tournament) rounds of disjoint
+// pairs: N = 8 players for n <= 8, else 16 (indices >= n sit out); round
+// r = 0 .. N-2 pairs player N-1 with r and (r + k) mod (N-1) with (r - k) mod
+// (N-1), k = 1 .. N/2-1. A round takes its rotations J_k from the matrix at
+// the start of the round (the pairs are disjoint, so the angles do not depend
+// on one another: the device computes them side by side), then A <- A J
+// (column rotations, pairs in order), A <- J^T A (row rotations), a_pq =
+// a_qp = 0, V <- V J. A pair whose a_pq is exactly zero is skipped. Stop when
+// the off-diagonal Frobenius norm is <= 1e-16 of the diagonal's (or <= 1e-150)
+// or after 100 sweeps.
 void jacobi_eigs(int n, double* a, double* v, double* ev) {
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) v[i * n + j] = i == j ? 1.0 : 0.0;
+  const int N = n <= 8 ? 8 : 16;
   for (int sweep = 0; sweep < 100; ++sweep) {
     double off = 0.0, diag = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -32,33 +63,44 @@ void jacobi_eigs(int n, double* a, double* v, double* ev) {
       for (int j = i + 1; j < n; ++j) off += a[i * n + j] * a[i * n + j];
     }
     if (off <= 1e-32 * diag || off < 1e-300) break;
-    for (int p = 0; p < n; ++p) {
-      for (int q = p + 1; q < n; ++q) {
-        const double apq = a[p * n + q];
-        if (apq == 0.0) continue;
-        const double app = a[p * n + p], aqq = a[q * n + q];
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
-        const double c = 1.0 / std::sqrt(t * t + 1.0);
-        const double s = t * c;
-        for (int k = 0; k < n; ++k) {
-          const double akp = a[k * n + p], akq = a[k * n + q];
-          a[k * n + p] = c * akp - s * akq;
-          a[k * n + q] = s * akp + c * akq;
-        }
-        for (int k = 0; k < n; ++k) {
-          const double apk = a[p * n + k], aqk = a[q * n + k];
-          a[p * n + k] = c * apk - s * aqk;
-          a[q * n + k] = s * apk + c * aqk;
-        }
-        a[p * n + q] = 0.0;
-        a[q * n + p] = 0.0;
-        for (int k = 0; k < n; ++k) {
-          const double vkp = v[k * n + p], vkq = v[k * n + q];
-          v[k * n + p] = c * vkp - s * vkq;
-          v[k * n + q] = s * vkp + c * vkq;
+    for (int r = 0; r < N - 1; ++r) {
+      int P[8], Q[8];
+      double C[8], S[8];
+      bool act[8];
+      for (int k = 0; k < N / 2; ++k) {
+        const int x = k == 0 ? N - 1 : (r + k) % (N - 1);
+        const int y = k == 0 ? r : (r - k + (N - 1)) % (N - 1);
+        P[k] = x < y ? x : y;
+        Q[k] = x < y ? y : x;
+        act[k] = Q[k] < n && a[P[k] * n + Q[k]] != 0.0;
+        if (act[k])
+          jacobi_rotation(a[Q[k] * n + Q[k]] - a[P[k] * n + P[k]], 2.0 * a[P[k] * n + Q[k]], &C[k], &S[k]);
+      }
+      for (int k = 0; k < N / 2; ++k) {  // A <- A J, V <- V J
+        if (!act[k]) continue;
+        const int p = P[k], q = Q[k];
+        const double c = C[k], s = S[k];
+        for (int i = 0; i < n; ++i) {
+          const double aip = a[i * n + p], aiq = a[i * n + q];
+          a[i * n + p] = c * aip - s * aiq;
+          a[i * n + q] = s * aip + c * aiq;
+          const double vip = v[i * n + p], viq = v[i * n + q];
+          v[i * n + p] = c * vip - s * viq;
+          v[i * n + q] = s * vip + c * viq;
         }
       }
+      for (int k = 0; k < N / 2; ++k) {  // A <- J^T A
+        if (!act[k]) continue;
+        const int p = P[k], q = Q[k];
+        const double c = C[k], s = S[k];
+        for (int j = 0; j < n; ++j) {
+          const double apj = a[p * n + j], aqj = a[q * n + j];
+          a[p * n + j] = c * apj - s * aqj;
+          a[q * n + j] = s * apj + c * aqj;
+        }
+      }
+      for (int k = 0; k < N / 2; ++k)
+        if (act[k]) a[P[k] * n + Q[k]] = a[Q[k] * n + P[k]] = 0.0;
     }
   }
   for (int i = 0; i < n; ++i) ev[i] = a[i * n + i];

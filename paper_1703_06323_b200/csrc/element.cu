@@ -124,7 +124,28 @@ CB_HD inline void add_prism(Acc& a, P3 A, P3 B, P3 C, P3 A2, P3 B2, P3 C2) {
   add_tet(a, C, A2, B2, C2);
 }
 
-// Cyclic Jacobi, same sweep order / thresholds as the CPU restatement.
+// Jacobi rotation (c, s) from h = a_qq - a_pp, g = 2 a_pq (oracle/element.cpp
+// jacobi_rotation, the same operations).
+CB_HD inline void jacobi_rotation(double h, double g, double& c, double& s) {
+  const double sgn = (h == 0.0 || (h > 0.0) == (g > 0.0)) ? 1.0 : -1.0;
+  const double rho = sqrt(h * h + g * g);
+  const double d = fabs(h) + rho;
+  const double w = sqrt(d * d + g * g);
+  if (w > 0.0 && w <= 1.7976931348623157e308) {
+    c = d / w;
+    s = sgn * fabs(g) / w;
+    return;
+  }
+  const double theta = h / g;
+  const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+  c = 1.0 / sqrt(t * t + 1.0);
+  s = t * c;
+}
+
+// Parallel-order cyclic Jacobi (n <= 8): round-robin rounds of four disjoint
+// pairs, per round A <- A J, A <- J^T A, V <- V J with the rotations taken
+// from the matrix at the start of the round; same order / thresholds as the
+// CPU restatement (oracle/element.cpp jacobi_eigs).
 CB_HD void jacobi(int n, double* a, double* v, double* ev) {
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) v[i * n + j] = i == j ? 1.0 : 0.0;
@@ -135,33 +156,46 @@ CB_HD void jacobi(int n, double* a, double* v, double* ev) {
       for (int j = i + 1; j < n; ++j) off += a[i * n + j] * a[i * n + j];
     }
     if (off <= 1e-32 * diag || off < 1e-300) break;
-    for (int p = 0; p < n; ++p) {
-      for (int q = p + 1; q < n; ++q) {
-        const double apq = a[p * n + q];
-        if (apq == 0.0) continue;
-        const double app = a[p * n + p], aqq = a[q * n + q];
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(t * t + 1.0);
-        const double s = t * c;
-        for (int k = 0; k < n; ++k) {
-          const double akp = a[k * n + p], akq = a[k * n + q];
-          a[k * n + p] = c * akp - s * akq;
-          a[k * n + q] = s * akp + c * akq;
-        }
-        for (int k = 0; k < n; ++k) {
-          const double apk = a[p * n + k], aqk = a[q * n + k];
-          a[p * n + k] = c * apk - s * aqk;
-          a[q * n + k] = s * apk + c * aqk;
-        }
-        a[p * n + q] = 0.0;
-        a[q * n + p] = 0.0;
-        for (int k = 0; k < n; ++k) {
-          const double vkp = v[k * n + p], vkq = v[k * n + q];
-          v[k * n + p] = c * vkp - s * vkq;
-          v[k * n + q] = s * vkp + c * vkq;
+    for (int r = 0; r < 7; ++r) {
+      int P[4], Q[4];
+      double C[4], S[4];
+      bool act[4];
+      for (int k = 0; k < 4; ++k) {
+        const int x = k == 0 ? 7 : (r + k) % 7;
+        const int y = k == 0 ? r : (r - k + 7) % 7;
+        P[k] = x < y ? x : y;
+        Q[k] = x < y ? y : x;
+        act[k] = Q[k] < n && a[P[k] * n + Q[k]] != 0.0;
+        C[k] = 1.0;
+        S[k] = 0.0;
+        if (act[k])
+          jacobi_rotation(a[Q[k] * n + Q[k]] - a[P[k] * n + P[k]], 2.0 * a[P[k] * n + Q[k]], C[k], S[k]);
+      }
+      for (int k = 0; k < 4; ++k) {
+        if (!act[k]) continue;
+        const int p = P[k], q = Q[k];
+        const double c = C[k], s = S[k];
+        for (int i = 0; i < n; ++i) {
+          const double aip = a[i * n + p], aiq = a[i * n + q];
+          a[i * n + p] = c * aip - s * aiq;
+          a[i * n + q] = s * aip + c * aiq;
+          const double vip = v[i * n + p], viq = v[i * n + q];
+          v[i * n + p] = c * vip - s * viq;
+          v[i * n + q] = s * vip + c * viq;
         }
       }
+      for (int k = 0; k < 4; ++k) {
+        if (!act[k]) continue;
+        const int p = P[k], q = Q[k];
+        const double c = C[k], s = S[k];
+        for (int j = 0; j < n; ++j) {
+          const double apj = a[p * n + j], aqj = a[q * n + j];
+          a[p * n + j] = c * apj - s * aqj;
+          a[q * n + j] = s * apj + c * aqj;
+        }
+      }
+      for (int k = 0; k < 4; ++k)
+        if (act[k]) a[P[k] * n + Q[k]] = a[Q[k] * n + P[k]] = 0.0;
     }
   }
   for (int i = 0; i < n; ++i) ev[i] = a[i * n + i];
@@ -577,15 +611,26 @@ __device__ __forceinline__ double sel8(const double (&r)[8], int idx) {
 // packed-upper index of (i, j), i <= j, in the D / B / M accumulator blocks
 __device__ __forceinline__ int tri(int i, int j) { return i * 8 - i * (i - 1) / 2 + (j - i); }
 
+// The round-robin pair (p < q) number k of round r over 8 players (the order
+// of jacobi above).
+__host__ __device__ constexpr int rr_x(int r, int k) { return k == 0 ? 7 : (r + k) % 7; }
+__host__ __device__ constexpr int rr_y(int r, int k) { return k == 0 ? r : (r - k + 7) % 7; }
+__host__ __device__ constexpr int rr_p(int r, int k) { return rr_x(r, k) < rr_y(r, k) ? rr_x(r, k) : rr_y(r, k); }
+__host__ __device__ constexpr int rr_q(int r, int k) { return rr_x(r, k) < rr_y(r, k) ? rr_y(r, k) : rr_x(r, k); }
+
 // jacobi(n, a, v, ev) by the 8 lanes of a group, lane k holding row k of a
-// and of v in registers: the column update of a rotation is lane-local, the
-// row update exchanges rows p and q by shuffles. The operations and their
-// order are jacobi's (every update reads the same operands). The (p, q)
-// loops are unrolled so every register index is a compile-time constant
-// (measured: the rolled form with select chains is 10-60% slower).
+// and of v in registers. Per round: lane l computes the rotation of pair
+// l & 3 (the sqrt / div chains of the four pairs run side by side in
+// different lanes) and the (c, s) are broadcast; A <- A J and V <- V J are
+// lane-local (four disjoint column pairs of the lane's row); A <- J^T A
+// exchanges the lane's row with its partner's by one round of shuffles.
+// Every entry sees jacobi's operations on the same operands, so the result
+// is bit-identical. Rounds and pairs are unrolled: every register index is a
+// compile-time constant.
 __device__ void reg_jacobi(int n, double (&a)[8], double (&v)[8], int gl, unsigned gm) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) v[j] = j == gl ? 1.0 : 0.0;
+  const int k4 = gl & 3;
   for (int sweep = 0; sweep < 100; ++sweep) {
     double off = 0.0, diag = 0.0;
 #pragma unroll
@@ -600,45 +645,82 @@ __device__ void reg_jacobi(int n, double (&a)[8], double (&v)[8], int gl, unsign
     }
     if (off <= 1e-32 * diag || off < 1e-300) break;
 #pragma unroll
-    for (int p = 0; p < 7; ++p)
+    for (int r = 0; r < 7; ++r) {
+      // the pair whose rotation this lane computes (mp, mq); this lane's own
+      // pair number, partner and side
+      int mp = rr_p(r, 0), mq = rr_q(r, 0), mate = 0, mypair = 0;
+      bool is_p = false;
 #pragma unroll
-      for (int q = p + 1; q < 8; ++q) {
-        if (q >= n) continue;  // n is uniform over the group
-        const double apq = gsh(a[q], p, gm);
-        if (apq == 0.0) continue;
-        const double app = gsh(a[p], p, gm), aqq = gsh(a[q], q, gm);
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(t * t + 1.0);
-        const double s = t * c;
-        if (gl < n) {  // column update, row k = gl
-          const double akp = a[p], akq = a[q];
-          a[p] = c * akp - s * akq;
-          a[q] = s * akp + c * akq;
+      for (int kk = 0; kk < 4; ++kk) {
+        if (k4 == kk) {
+          mp = rr_p(r, kk);
+          mq = rr_q(r, kk);
         }
-        double rp[8], rq[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          rp[j] = gsh(a[j], p, gm);
-          rq[j] = gsh(a[j], q, gm);
+        if (gl == rr_p(r, kk)) {
+          mate = rr_q(r, kk);
+          mypair = kk;
+          is_p = true;
         }
-        if (gl == p) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (j < n) a[j] = c * rp[j] - s * rq[j];
-          a[q] = 0.0;
-        } else if (gl == q) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (j < n) a[j] = s * rp[j] + c * rq[j];
-          a[p] = 0.0;
-        }
-        if (gl < n) {
-          const double vkp = v[p], vkq = v[q];
-          v[p] = c * vkp - s * vkq;
-          v[q] = s * vkp + c * vkq;
+        if (gl == rr_q(r, kk)) {
+          mate = rr_p(r, kk);
+          mypair = kk;
         }
       }
+      const double dg = sel8(a, gl);    // A[gl][gl]
+      const double om = sel8(a, mate);  // A[gl][mate]
+      const double app = gsh(dg, mp, gm), aqq = gsh(dg, mq, gm), apq = gsh(om, mp, gm);
+      const bool act = mq < n && apq != 0.0;
+      double c = 1.0, s = 0.0;
+      if (act) jacobi_rotation(aqq - app, 2.0 * apq, c, s);
+      double C[4], S[4];
+      bool A[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        C[kk] = gsh(c, kk, gm);
+        S[kk] = gsh(s, kk, gm);
+        A[kk] = __shfl_sync(gm, (int)act, kk, 8) != 0;
+      }
+      // A <- A J, V <- V J: this lane's row, four disjoint column pairs
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int p = rr_p(r, kk), q = rr_q(r, kk);
+        if (A[kk] && gl < n) {
+          const double aip = a[p], aiq = a[q];
+          a[p] = C[kk] * aip - S[kk] * aiq;
+          a[q] = S[kk] * aip + C[kk] * aiq;
+          const double vip = v[p], viq = v[q];
+          v[p] = C[kk] * vip - S[kk] * viq;
+          v[q] = S[kk] * vip + C[kk] * viq;
+        }
+      }
+      // A <- J^T A: row p = c row p - s row q, row q = s row p + c row q
+      double other[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) other[j] = gsh(a[j], mate, gm);
+      bool mine = false;
+      double cm = 1.0, sm = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        if (mypair == kk) {
+          mine = A[kk];
+          cm = C[kk];
+          sm = S[kk];
+        }
+      if (mine) {
+        if (is_p) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < n) a[j] = cm * a[j] - sm * other[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < n) a[j] = sm * other[j] + cm * a[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j == mate) a[j] = 0.0;
+      }
+    }
   }
 }
 

@@ -28,6 +28,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "factor.cuh"
 #include "front_desc.cuh"
@@ -53,7 +56,11 @@ namespace {
 #define CUTBDDC_SWEEP_SLOT_DOUBLES 2176
 #endif
 // (the CUTBDDC_SWEEP_* macros exist for tools/tune_sweep.sh)
-constexpr int kSmallRows = 256;                     // fronts with at most this many rows: one forward item
+#ifndef CUTBDDC_SWEEP_THREADS
+#define CUTBDDC_SWEEP_THREADS 256
+#endif
+constexpr int kThreadsSweep = CUTBDDC_SWEEP_THREADS;  // consumer threads (+ one producer warp)
+constexpr int kSmallRows = kThreadsSweep;           // fronts with at most this many rows: one forward item
 constexpr int kFwdRows = CUTBDDC_SWEEP_FWD_ROWS;    // forward items of larger fronts: row blocks ...
 // ... cut into column ranges of SweepDev::fwd_cols columns; backward items:
 // column blocks of SweepDev::bwd_cols (<= kMaxBwdCols) columns, all rows
@@ -61,15 +68,14 @@ constexpr int kFwdRows = CUTBDDC_SWEEP_FWD_ROWS;    // forward items of larger f
 constexpr int kMaxBwdCols = 32;
 constexpr int kSlots = CUTBDDC_SWEEP_SLOTS;         // staging ring depth (chunks in flight per CTA)
 constexpr int kMinBlocks = CUTBDDC_SWEEP_MIN_BLOCKS;
-constexpr int kThreadsSweep = 256;                  // consumer threads (+ one producer warp)
 constexpr int kWarps = kThreadsSweep / 32;
 constexpr int kBwdRowsChunk = CUTBDDC_SWEEP_BWD_ROWS;  // backward chunk: bwd_cols columns x 64 rows
 constexpr int kSlot = CUTBDDC_SWEEP_SLOT_DOUBLES;       // doubles per ring slot (17 KB)
 constexpr int kMaxSegs = 32;                        // column segments per chunk
-constexpr int kVecDoubles = 2048;                   // front vector: >= every template front
+constexpr int kVecMax = 2048;                       // front vector (shared): at most this many rows per front
 constexpr int kItems = 1;                           // item records (consumers release theirs once its dependencies are met)
-constexpr int kShmDoubles = kSlots * kSlot + kVecDoubles + kThreadsSweep;
-constexpr int kShmBytes = 8 * kShmDoubles + 4 * kSlots * kMaxSegs;
+// dynamic shared memory of a sweep CTA: ring | front vector (vec doubles) | partials | segment offsets
+inline size_t sweep_shm_bytes(int vec) { return 8 * (size_t)(kSlots * kSlot + vec + kThreadsSweep) + 4 * kSlots * kMaxSegs; }
 static_assert(kThreadsSweep % kFwdRows == 0 && kFwdRows % 32 == 0, "forward row blocks");
 static_assert(kMaxBwdCols <= kMaxSegs && kMaxBwdCols % kWarps == 0, "backward column blocks");
 static_assert(kMaxBwdCols * (kBwdRowsChunk + 2) <= kSlot && 16 * (kFwdRows + 2) <= kSlot, "chunk sizes");
@@ -93,6 +99,7 @@ struct SweepDev {
   int32_t* rbcnt;   // forward range arrivals per (chunked front, row block)
   double* vbuf;
   int fwd_cols, bwd_cols;  // item sizes of this factorisation's plan
+  int vec;                 // doubles of the shared front vector (this launch)
   int l2_policy;           // panel loads: 0 default, 1 L2 evict_last (keep resident), 2 L2 evict_first (stream)
   unsigned long long* trace;  // CUTBDDC_SWEEP_TRACE: per item {grab, deps met, done, sm}, else null
 };
@@ -526,7 +533,7 @@ __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __rest
   extern __shared__ __align__(128) double shm[];
   double* ring = shm;
   double* vec = shm + kSlots * kSlot;
-  double* part = vec + kVecDoubles;
+  double* part = vec + p.vec;
   int* segoff = reinterpret_cast<int*>(part + kThreadsSweep);  // kSlots x kMaxSegs
   __shared__ ItemRec rec[kItems];
   __shared__ SlotRec sr[kSlots];
@@ -580,7 +587,7 @@ __global__ void __launch_bounds__(kThreadsSweep + 32, kMinBlocks) k_sweep_fwd(Sw
 // Forward sweep of kMultiRhs right-hand sides at once (the coarse-basis
 // setup: H = L^{-1} C^T), same items and schedule as k_sweep_fwd.
 constexpr int kMultiRhs = 8;
-static_assert(kMultiRhs * kSmallRows <= kVecDoubles, "multi-RHS front vector");
+static_assert(kMultiRhs * kSmallRows <= 4096, "multi-RHS front vector");
 __global__ void __launch_bounds__(kThreadsSweep + 32, 1) k_sweep_fwd_multi(SweepDev p, const int4* __restrict__ items, int n_items,
                                                              const double* __restrict__ panel,
                                                              const double* __restrict__ X, double* __restrict__ ysave,
@@ -642,6 +649,7 @@ SweepDev sweep_dev(const FactorSet& f, int nsd, int nsn, unsigned long long* tra
                   const_cast<double*>(f.vbuf.p),
                   f.fwd_cols,
                   f.bwd_cols,
+                  f.sweep_vec,
                   f.l2_policy_f,
                   trace};
 }
@@ -666,17 +674,23 @@ void dump_trace(const std::string& path, const FactorSet& f, bool fwd, cudaStrea
   std::fclose(fp);
 }
 
-int sweep_grid(const void* fn) {
-  const int slot = fn == (const void*)k_sweep_fwd ? kMemoSweepFwd
-                   : fn == (const void*)k_sweep_bwd ? kMemoSweepBwd : kMemoSweepMulti;
-  return (int)device_memo(slot, [&] {
-    int per_sm = 0;
-    CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsSweep + 32, kShmBytes));
-    int dev = 0, sms = 0;
-    CB_CUDA(cudaGetDevice(&dev));
-    CB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    return (long long)std::max(1, per_sm) * sms;
-  });
+// CTAs of a persistent sweep launch: every SM filled at the occupancy of
+// (kernel, shared-memory size); memoised per device for the sizes in use.
+int sweep_grid(const void* fn, size_t shm) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, size_t>, int> memo;
+  int dev = 0;
+  CB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, fn, shm);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  int per_sm = 0, sms = 0;
+  CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsSweep + 32, shm));
+  CB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int g = std::max(1, per_sm) * sms;
+  memo[key] = g;
+  return g;
 }
 
 }  // namespace
@@ -717,8 +731,11 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   const int nsd = h->nsd, nsn = (int)tp.sn.size();
   const auto& lv = tp.levels;
   const int nlev = (int)lv.size();
-  if (tp.max_rows > kVecDoubles) throw Failure(CUTBDDC_CONFIG, "sweep: front larger than the shared vector");
+  if (tp.max_rows > kVecMax) throw Failure(CUTBDDC_CONFIG, "sweep: front larger than the shared vector");
   choose_item_sizes(h, f);
+  // shared front vector of this factorisation's sweeps: its largest front
+  // (backward) or one column range (forward), 64-double granules
+  f.sweep_vec = (std::max({tp.max_rows, f.fwd_cols, kSmallRows}) + 63) & ~63;
   const int fc = f.fwd_cols, bc = f.bwd_cols;
   // S item: a front whose whole forward is one item (one row block, at most
   // small_work panel entries); larger fronts: row blocks x column ranges
@@ -972,11 +989,12 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
   FactorSet& fm = const_cast<FactorSet&>(f);
   if (tp) fm.trace.alloc((size_t)4 * std::max(f.n_items_f, f.n_items_b) + 4);
   const SweepDev p = sweep_dev(f, nsd, nsn, tp ? fm.trace.p : nullptr);
-  const size_t shm = kShmBytes;
+  const size_t shm = sweep_shm_bytes(f.sweep_vec);
   device_memo(kMemoSweepAttr, [&] {
-    CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    CB_CUDA(cudaFuncSetAttribute(k_sweep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    const int mx = (int)sweep_shm_bytes(kMultiRhs * std::max(kVecMax / kMultiRhs, kSmallRows));
+    CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CB_CUDA(cudaFuncSetAttribute(k_sweep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     return 1ll;
   });
   if (phase == kSweepAttrOnly) return;
@@ -985,7 +1003,7 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
     CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
     ProfScope ps(h->prof, s, tag + " fwd");
     if (f.n_items_f > 0) {
-      const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd));
+      const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd, shm));
       k_sweep_fwd<<<g, kThreadsSweep + 32, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, skip);
       CB_LAUNCH();
     }
@@ -999,7 +1017,7 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
   SweepDev pb = p;
   pb.l2_policy = f.l2_policy_b;
   if (b1 > b0) {
-    const int g = std::min(b1 - b0, sweep_grid((const void*)k_sweep_bwd));
+    const int g = std::min(b1 - b0, sweep_grid((const void*)k_sweep_bwd, shm));
     k_sweep_bwd<<<g, kThreadsSweep + 32, shm, s>>>(pb, f.items_b.p + b0, b1 - b0, f.panel.p, X, ysave, skip, slot);
     CB_LAUNCH();
   }
@@ -1017,12 +1035,13 @@ void sweep_forward_multi(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, c
   const int nsd = h->nsd, nsn = (int)ts.tpl.sn.size();
   SweepDev p = sweep_dev(f, nsd, nsn, nullptr);
   p.vbuf = vbuf8;
-  const size_t shm = kShmBytes;
+  p.vec = (std::max(f.sweep_vec, kMultiRhs * std::max(f.fwd_cols, kSmallRows)) + 63) & ~63;
+  const size_t shm = sweep_shm_bytes(p.vec);
   sweep_phase(h, ts, f, nullptr, nullptr, nullptr, nullptr, kSweepAttrOnly);
   CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
   if (f.n_items_f == 0) return;
   const RhsStride rs{(int64_t)nsd * h->slots, f.upd_total, (int64_t)f.vbuf.n};
-  const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd_multi));
+  const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd_multi, shm));
   k_sweep_fwd_multi<<<g, kThreadsSweep + 32, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, rs);
   CB_LAUNCH();
 }
