@@ -103,6 +103,7 @@ struct FactorSet {
   int fwd_cols = 256, bwd_cols = 32;           // sweep item sizes (sweep.cu choose_item_sizes)
   int small_work = 8192;                       // panel entries of the largest one-item forward front
   int sweep_vec = 2048;                        // doubles of the sweeps' shared front vector (largest front, sweep.cu)
+  int sweep_slot = 2560, sweep_bwd_rows = 78;  // ring slot doubles / backward chunk rows (sweep.cu build_sweep_plan)
   int l2_policy_f = 2, l2_policy_b = 2;        // panel loads of the forward / backward sweeps: L2 eviction priority
                                                // (0 default, 1 evict_last, 2 evict_first; sweep.cu choose_item_sizes)
   std::vector<int64_t> h_vec_off;              // nsd x nsn compact front vector offsets (host copy)

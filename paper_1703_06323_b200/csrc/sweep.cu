@@ -49,12 +49,6 @@ namespace {
 #ifndef CUTBDDC_SWEEP_MIN_BLOCKS
 #define CUTBDDC_SWEEP_MIN_BLOCKS 4
 #endif
-#ifndef CUTBDDC_SWEEP_BWD_ROWS
-#define CUTBDDC_SWEEP_BWD_ROWS 64
-#endif
-#ifndef CUTBDDC_SWEEP_SLOT_DOUBLES
-#define CUTBDDC_SWEEP_SLOT_DOUBLES 2176
-#endif
 // (the CUTBDDC_SWEEP_* macros exist for tools/tune_sweep.sh)
 #ifndef CUTBDDC_SWEEP_THREADS
 #define CUTBDDC_SWEEP_THREADS 256
@@ -69,16 +63,28 @@ constexpr int kMaxBwdCols = 32;
 constexpr int kSlots = CUTBDDC_SWEEP_SLOTS;         // staging ring depth (chunks in flight per CTA)
 constexpr int kMinBlocks = CUTBDDC_SWEEP_MIN_BLOCKS;
 constexpr int kWarps = kThreadsSweep / 32;
-constexpr int kBwdRowsChunk = CUTBDDC_SWEEP_BWD_ROWS;  // backward chunk: bwd_cols columns x 64 rows
-constexpr int kSlot = CUTBDDC_SWEEP_SLOT_DOUBLES;       // doubles per ring slot (17 KB)
+// Ring slot size (doubles) and backward chunk height (rows), chosen per
+// factorisation (SweepDev::slot, ::bwd_rows): many subdomains -> 4 CTAs per
+// SM with 20 KB slots, few -> 3 CTAs with 28 KB slots (fewer, longer chunks
+// per item). The macros override both.
+constexpr int kSlotWide = 2560, kBwdRowsWide = 78;      // nsd >= 256 (tuned on cfg5)
+constexpr int kSlotFew = 3584, kBwdRowsFew = 110;       // fewer subdomains (tuned on cfg4)
 constexpr int kMaxSegs = 32;                        // column segments per chunk
 constexpr int kVecMax = 2048;                       // front vector (shared): at most this many rows per front
-constexpr int kItems = 1;                           // item records (consumers release theirs once its dependencies are met)
-// dynamic shared memory of a sweep CTA: ring | front vector (vec doubles) | partials | segment offsets
-inline size_t sweep_shm_bytes(int vec) { return 8 * (size_t)(kSlots * kSlot + vec + kThreadsSweep) + 4 * kSlots * kMaxSegs; }
+#ifndef CUTBDDC_SWEEP_ITEMS_IN_FLIGHT
+#define CUTBDDC_SWEEP_ITEMS_IN_FLIGHT 2
+#endif
+constexpr int kItems = CUTBDDC_SWEEP_ITEMS_IN_FLIGHT;  // item records in flight per CTA: one computing, the others being prepared
+constexpr int kBlockSweep = kThreadsSweep + 64;     // consumers + producer warp + preparation warp
+constexpr int kColsPerLane = kSmallRows / 32;       // forward item columns per preparation lane
+// dynamic shared memory of a sweep CTA: ring | kItems front vectors (vec doubles each) | partials | segment offsets
+inline size_t sweep_shm_bytes(int slot, int vec) {
+  return 8 * (size_t)(kSlots * slot + kItems * vec + kThreadsSweep) + 4 * kSlots * kMaxSegs;
+}
 static_assert(kThreadsSweep % kFwdRows == 0 && kFwdRows % 32 == 0, "forward row blocks");
 static_assert(kMaxBwdCols <= kMaxSegs && kMaxBwdCols % kWarps == 0, "backward column blocks");
-static_assert(kMaxBwdCols * (kBwdRowsChunk + 2) <= kSlot && 16 * (kFwdRows + 2) <= kSlot, "chunk sizes");
+static_assert(kMaxBwdCols * (kBwdRowsWide + 2) <= kSlotWide && 16 * (kFwdRows + 2) <= kSlotWide, "chunk sizes");
+static_assert(kMaxBwdCols * (kBwdRowsFew + 2) <= kSlotFew && 16 * (kFwdRows + 2) <= kSlotFew, "chunk sizes");
 enum { kItemS = 0, kItemC = 2 };
 
 // column stride (doubles, even: every staged column starts 16-byte aligned)
@@ -100,6 +106,7 @@ struct SweepDev {
   double* vbuf;
   int fwd_cols, bwd_cols;  // item sizes of this factorisation's plan
   int vec;                 // doubles of the shared front vector (this launch)
+  int slot, bwd_rows;      // doubles per ring slot, rows per backward chunk
   int l2_policy;           // panel loads: 0 default, 1 L2 evict_last (keep resident), 2 L2 evict_first (stream)
   unsigned long long* trace;  // CUTBDDC_SWEEP_TRACE: per item {grab, deps met, done, sm}, else null
 };
@@ -197,7 +204,7 @@ struct Chunk {
 // Item geometry, computed identically by the producer and the consumers.
 // Forward: rows [i0, i1) (one row block) x columns [jlo, jhi) (one column
 // range), chunks of `cw` columns. Backward: columns [jlo, jhi) x rows
-// [jlo, r), chunks of kBwdRowsChunk rows.
+// [jlo, r), chunks of SweepDev::bwd_rows rows.
 struct ItemGeom {
   int i0, i1, jlo, jhi, nchunk, cw;
   int rb, cb, mcb;
@@ -222,30 +229,31 @@ __device__ __forceinline__ ItemGeom item_geom(const SweepDev& p, const FrontDesc
       g.jlo = g.cb * kFwdCols;
       g.jhi = min(min(c, g.i1), g.jlo + kFwdCols);
     }
-    g.cw = max(1, min(kMaxSegs, kSlot / seg_stride(g.i1 - g.i0)));
+    g.cw = max(1, min(kMaxSegs, p.slot / seg_stride(g.i1 - g.i0)));
     g.nchunk = g.jhi > g.jlo ? (g.jhi - g.jlo + g.cw - 1) / g.cw : 0;
   } else {
     g.jlo = chunk * kBwdCols;
     g.jhi = min(c, g.jlo + kBwdCols);
     g.i0 = g.jlo;
     g.i1 = r;
-    g.nchunk = g.jhi > g.jlo ? (r - g.jlo + kBwdRowsChunk - 1) / kBwdRowsChunk : 0;
+    g.nchunk = g.jhi > g.jlo ? (r - g.jlo + p.bwd_rows - 1) / p.bwd_rows : 0;
+    g.cw = p.bwd_rows;
   }
   return g;
 }
 __device__ __forceinline__ Chunk chunk_of(const ItemGeom& g, int q, bool fwd) {
   if (fwd) return Chunk{g.jlo + q * g.cw, min(g.jhi, g.jlo + (q + 1) * g.cw), g.i0, g.i1};
-  const int lo = g.i0 + q * kBwdRowsChunk;
-  return Chunk{g.jlo, g.jhi, lo, min(g.i1, lo + kBwdRowsChunk)};
+  const int lo = g.i0 + q * g.cw;  // backward: cw = rows per chunk
+  return Chunk{g.jlo, g.jhi, lo, min(g.i1, lo + g.cw)};
 }
 
 // Per-CTA shared state.
 struct ItemRec {
   int4 item;  // (kind, sid, sd, chunk); kind < 0: no more items
   FrontDesc d;
-  uint64_t info, empty;
+  uint64_t info, ready, empty;  // published by the producer / prepared (dependencies met, vector filled) / released
   int tk;
-  unsigned long long t_grab;
+  unsigned long long t_grab, t_dep;
 };
 struct SlotRec {
   uint64_t full, empty;
@@ -331,7 +339,7 @@ __device__ void producer(const SweepDev& p, const int4* __restrict__ items, int 
     for (int q = 0; q < g.nchunk; ++q, ++chunk_seq) {
       const int slot = chunk_seq % kSlots;
       if (chunk_seq >= kSlots) mbar_wait(&sr[slot].empty, ((chunk_seq / kSlots) - 1) & 1);
-      produce_chunk(d, chunk_of(g, q, fwd), panel, ring + slot * kSlot, segoff + slot * kMaxSegs, sr[slot],
+      produce_chunk(d, chunk_of(g, q, fwd), panel, ring + slot * p.slot, segoff + slot * kMaxSegs, sr[slot],
                     p.l2_policy, pol);
     }
   }
@@ -343,18 +351,154 @@ struct RhsStride {
   int64_t x, u, v;
 };
 
+// every lane waits until *p >= target (acquire: its later loads see the
+// signaller's writes)
+__device__ __forceinline__ void lane_wait(const int32_t* p, int target) {
+  while (ld_acquire(p) < target) __nanosleep(32);
+}
+
+// Preparation warp: for every item the producer publishes, everything its
+// consumers need besides the panel, into the item's own shared front vector
+// V: the static part first (b or y at the columns, slots and gather maps),
+// then the dependency wait, then the part other items produce (the
+// children's updates, the parents' solution). The consumers of the CTA are
+// still computing the previous item meanwhile, so these global-memory round
+// trips are off their path.
+template <bool kFwd, int NR>
+__device__ void preparer(const SweepDev& p, ItemRec* rec, double* vecs, const double* __restrict__ X,
+                         const double* __restrict__ ysave, const double* upd, const double* Xw, RhsStride rs) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0;; ++k) {
+    ItemRec& R = rec[k % kItems];
+    double* V = vecs + (size_t)(k % kItems) * p.vec;
+    mbar_wait(&R.info, (k / kItems) & 1);
+    if (R.item.x < 0) {
+      mbar_arrive(&R.ready);
+      return;
+    }
+    const FrontDesc d = R.d;
+    const ItemGeom g = item_geom(p, d, R.item.x, R.item.w, kFwd);
+    const int32_t* cs = p.cslot + d.vo;
+    if (kFwd) {
+      const int ncol = g.jhi - g.jlo;  // <= kSmallRows
+      // every batch of loads is issued before its first use (memory-level
+      // parallelism: one warp does what 256 threads did)
+      int sl[kColsPerLane];
+      int2 gc[kColsPerLane];
+#pragma unroll
+      for (int u = 0; u < kColsPerLane; ++u) {
+        const int q = lane + 32 * u;
+        sl[u] = q < ncol ? cs[g.jlo + q] : -1;
+        gc[u] = q < ncol ? reinterpret_cast<const int2*>(p.gmap)[d.vo + g.jlo + q] : make_int2(-1, -1);
+      }
+      if (NR == 1) {
+        double x[kColsPerLane];
+#pragma unroll
+        for (int u = 0; u < kColsPerLane; ++u) x[u] = sl[u] >= 0 ? X[sl[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < kColsPerLane; ++u)
+          if (sl[u] >= 0) V[lane + 32 * u] = x[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < kColsPerLane; ++u)
+          if (sl[u] >= 0) {
+            double x[NR];
+#pragma unroll
+            for (int rr = 0; rr < NR; ++rr) x[rr] = X[rr * rs.x + sl[u]];
+#pragma unroll
+            for (int rr = 0; rr < NR; ++rr) V[(lane + 32 * u) * NR + rr] = x[rr];
+          }
+      }
+      if (d.nch > 0) lane_wait(p.done_f + d.cfs0, d.cnf0);
+      if (d.nch > 1) lane_wait(p.done_f + d.cfs1, d.cnf1);
+      if (lane == 0 && p.trace) R.t_dep = gtimer();
+      // the children's updates at the columns: x = v (+ child 0) (+ child 1)
+      if (NR == 1) {
+        double a0[kColsPerLane], a1[kColsPerLane];
+#pragma unroll
+        for (int u = 0; u < kColsPerLane; ++u) {
+          a0[u] = gc[u].x >= 0 ? __ldcg(upd + gc[u].x) : 0.0;
+          a1[u] = gc[u].y >= 0 ? __ldcg(upd + gc[u].y) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kColsPerLane; ++u)
+          if (gc[u].x >= 0 || gc[u].y >= 0) {
+            double x = V[lane + 32 * u];
+            if (gc[u].x >= 0) x += a0[u];
+            if (gc[u].y >= 0) x += a1[u];
+            V[lane + 32 * u] = x;
+          }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kColsPerLane; ++u)
+          if (gc[u].x >= 0 || gc[u].y >= 0) {
+            double a0[NR], a1[NR];
+#pragma unroll
+            for (int rr = 0; rr < NR; ++rr) {
+              a0[rr] = gc[u].x >= 0 ? __ldcg(upd + rr * rs.u + gc[u].x) : 0.0;
+              a1[rr] = gc[u].y >= 0 ? __ldcg(upd + rr * rs.u + gc[u].y) : 0.0;
+            }
+#pragma unroll
+            for (int rr = 0; rr < NR; ++rr) {
+              double x = V[(lane + 32 * u) * NR + rr];
+              if (gc[u].x >= 0) x += a0[rr];
+              if (gc[u].y >= 0) x += a1[rr];
+              V[(lane + 32 * u) * NR + rr] = x;
+            }
+          }
+      }
+    } else {
+      const int r = d.r, c = d.c;
+      constexpr int kB = 8;  // rows per lane and batch
+      for (int q0 = g.jlo; q0 < r; q0 += 32 * kB) {  // static: y at the columns, the update rows' slots
+        int sl[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int q = q0 + lane + 32 * u;
+          sl[u] = q < r ? cs[q] : 0;
+        }
+        double y[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int q = q0 + lane + 32 * u;
+          y[u] = q < c ? ysave[sl[u]] : __longlong_as_double((long long)sl[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int q = q0 + lane + 32 * u;
+          if (q < r) V[q] = y[u];
+        }
+      }
+      if (d.pfs >= 0) lane_wait(p.done_b + d.pfs, d.pnb);
+      if (lane == 0 && p.trace) R.t_dep = gtimer();
+      for (int q0 = max(c, g.jlo); q0 < r; q0 += 32 * kB) {  // the parents' solution at the update rows
+        double x[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int q = q0 + lane + 32 * u;
+          x[u] = q < r ? __ldcg(Xw + (int)__double_as_longlong(V[q])) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int q = q0 + lane + 32 * u;
+          if (q < r) V[q] = -x[u];
+        }
+      }
+    }
+    mbar_arrive(&R.ready);  // every lane: its writes to V are published
+  }
+}
+
 // Forward of one item: o[i] = sum_j G[i, j] v[j] over the item's rows and
 // column range for NR right-hand sides at once (rows split over thread
 // groups, columns interleaved over the groups: every row's sum has a fixed
 // order). One column range: the item writes y (column rows) and the
 // parent's update v_rest - o (update rows); several: partial sums to vbuf,
 // the last range of a row block to arrive sums them in range order.
-// Everything static (b at the columns, gmap rows) is loaded before the
-// dependency wait.
+// v (the assembled right-hand side at the item's columns) comes prepared.
 template <int NR>
-__device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, const int* segoff, SlotRec* sr,
-                         int& chunk_seq, const double* __restrict__ X, double* ysave, double* upd, double* v,
-                         double* part, unsigned long long& t_dep, RhsStride rs) {
+__device__ void fwd_item(const SweepDev& p, const ItemRec& R, const double* ring, const int* segoff, SlotRec* sr,
+                         int& chunk_seq, double* ysave, double* upd, const double* v, double* part, RhsStride rs) {
   const int tid = threadIdx.x;
   const FrontDesc d = R.d;
   const int kind = R.item.x;
@@ -363,40 +507,19 @@ __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
   const int32_t* cs = p.cslot + d.vo;
   const ItemGeom g = item_geom(p, d, kind, R.item.w, true);
   const int nrow = g.i1 - g.i0;
-  // static loads: b at the item's columns (v), the gmap of its columns and rows
-  for (int q = tid; q < g.jhi - g.jlo; q += kThreadsSweep) {
-    const int sl = cs[g.jlo + q];
+  const int qr = g.i0 + tid;  // this thread's row (rows <= kThreadsSweep)
+  double cu[NR];  // the children's updates at row qr (update rows); the loads overlap the chunk loop
 #pragma unroll
-    for (int rr = 0; rr < NR; ++rr) v[q * NR + rr] = X[rr * rs.x + sl];
-  }
-  const int qr = g.i0 + tid;  // this thread's row (rows <= 256)
-  const int2 gr = (tid < nrow && qr >= c) ? reinterpret_cast<const int2*>(p.gmap)[d.vo + qr] : make_int2(-1, -1);
-  if (d.nch > 0) cta_wait(p.done_f + d.cfs0, d.cnf0);
-  if (d.nch > 1) cta_wait(p.done_f + d.cfs1, d.cnf1);
-  csync();  // every consumer has its copy of the record: the producer may take the next ticket
-  if (tid == 0) {
-    if (p.trace) t_dep = gtimer();
-    mbar_arrive(&R.empty);
-  }
-  for (int q = tid; q < g.jhi - g.jlo; q += kThreadsSweep) {  // the children's updates at the columns
-    const int2 gc = reinterpret_cast<const int2*>(p.gmap)[d.vo + g.jlo + q];
+  for (int rr = 0; rr < NR; ++rr) cu[rr] = 0.0;
+  if (tid < nrow && qr >= c) {
+    const int2 gr = reinterpret_cast<const int2*>(p.gmap)[d.vo + qr];
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) {
-      double x = v[q * NR + rr];
-      if (gc.x >= 0) x += __ldcg(upd + rr * rs.u + gc.x);
-      if (gc.y >= 0) x += __ldcg(upd + rr * rs.u + gc.y);
-      v[q * NR + rr] = x;
+      if (gr.x >= 0) cu[rr] += __ldcg(upd + rr * rs.u + gr.x);
+      if (gr.y >= 0) cu[rr] += __ldcg(upd + rr * rs.u + gr.y);
     }
   }
-  double cu[NR];  // the children's updates at row qr (update rows)
-#pragma unroll
-  for (int rr = 0; rr < NR; ++rr) {
-    cu[rr] = 0.0;
-    if (gr.x >= 0) cu[rr] += __ldcg(upd + rr * rs.u + gr.x);
-    if (gr.y >= 0) cu[rr] += __ldcg(upd + rr * rs.u + gr.y);
-  }
-  csync();
-  const int Rw = (nrow + 31) & ~31, ng = kThreadsSweep / Rw;  // Rw <= 256 rows per group, ng groups
+  const int Rw = (nrow + 31) & ~31, ng = kThreadsSweep / Rw;  // Rw <= kThreadsSweep rows per group, ng groups
   const int row = tid % Rw, grp = tid / Rw, i = g.i0 + row;
   double acc[NR];
 #pragma unroll
@@ -405,7 +528,7 @@ __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
     const int slot = chunk_seq % kSlots;
     const Chunk ch = chunk_of(g, q, true);
     mbar_wait(&sr[slot].full, (chunk_seq / kSlots) & 1);
-    const double* S = ring + slot * kSlot;
+    const double* S = ring + slot * p.slot;
     const int* so = segoff + slot * kMaxSegs;
     if (grp < ng && row < nrow) {
       const int jend = min(ch.jb, i + 1);
@@ -419,14 +542,19 @@ __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
     if ((threadIdx.x & 31) == 0) mbar_arrive(&sr[slot].empty);
   }
   double o[NR];
+  if (ng == 1) {
 #pragma unroll
-  for (int rr = 0; rr < NR; ++rr) {  // group partials summed in group order, one right-hand side at a time
-    if (grp < ng && row < nrow) part[grp * Rw + row] = acc[rr];
-    csync();
-    o[rr] = 0.0;
-    if (tid < nrow)
-      for (int q = 0; q < ng; ++q) o[rr] += part[q * Rw + tid];
-    csync();
+    for (int rr = 0; rr < NR; ++rr) o[rr] = 0.0 + acc[rr];  // the grouped form's sum with one group
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {  // group partials summed in group order, one right-hand side at a time
+      if (grp < ng && row < nrow) part[grp * Rw + row] = acc[rr];
+      csync();
+      o[rr] = 0.0;
+      if (tid < nrow)
+        for (int q = 0; q < ng; ++q) o[rr] += part[q * Rw + tid];
+      csync();
+    }
   }
   if (g.mcb > 1) {
     double* tp = p.vbuf + d.tpo + (int64_t)g.rb * g.mcb * kFwdRows;
@@ -464,31 +592,23 @@ __device__ void fwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
 }
 
 // Backward of one item: columns [j0, j1) of a front, x_j = sum_{i >= j}
-// G[i, j] w[i] with w = [y; -x_rest]; warp w owns columns j0 + w + 8k, its
-// lanes stride over the rows of every chunk (register accumulators, fixed
-// order), one warp sum per column at the end.
-__device__ void bwd_item(const SweepDev& p, ItemRec& R, const double* ring, const int* segoff, SlotRec* sr,
-                         int& chunk_seq, double* X, const double* __restrict__ ysave, double* w,
-                         unsigned long long& t_dep) {
+// G[i, j] w[i] with w = [y; -x_rest] (prepared); warp w owns columns
+// j0 + w + 8k, its lanes stride over the rows of every chunk (register
+// accumulators, fixed order), one warp sum per column at the end.
+__device__ void bwd_item(const SweepDev& p, const ItemRec& R, const double* ring, const int* segoff, SlotRec* sr,
+                         int& chunk_seq, double* X, const double* w) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const FrontDesc d = R.d;
   const int64_t fs = (int64_t)R.item.z * p.nsn + R.item.y;
-  const int r = d.r, c = d.c;
   const int32_t* cs = p.cslot + d.vo;
   const ItemGeom g = item_geom(p, d, R.item.x, R.item.w, false);
-  for (int q = g.jlo + tid; q < r; q += kThreadsSweep) {  // static: y at the columns, the update rows' slots
-    const int sl = cs[q];                                   // (kept in w's own entry until the wait is over)
-    w[q] = q < c ? ysave[sl] : __longlong_as_double((long long)sl);
-  }
-  if (d.pfs >= 0) cta_wait(p.done_b + d.pfs, d.pnb);
-  csync();  // every consumer has its copy of the record: the producer may take the next ticket
-  if (tid == 0) {
-    if (p.trace) t_dep = gtimer();
-    mbar_arrive(&R.empty);
-  }
-  for (int q = max(c, g.jlo) + tid; q < r; q += kThreadsSweep) w[q] = -__ldcg(X + (int)__double_as_longlong(w[q]));
-  csync();
   constexpr int kPer = kMaxBwdCols / kWarps;
+  int slj[kPer];  // the columns' slots (static)
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int j = g.jlo + wid + kWarps * k;
+    slj[k] = (lane == 0 && j < g.jhi) ? cs[j] : 0;
+  }
   double acc[kPer];
 #pragma unroll
   for (int k = 0; k < kPer; ++k) acc[k] = 0.0;
@@ -496,7 +616,7 @@ __device__ void bwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
     const int slot = chunk_seq % kSlots;
     const Chunk ch = chunk_of(g, q, false);
     mbar_wait(&sr[slot].full, (chunk_seq / kSlots) & 1);
-    const double* S = ring + slot * kSlot;
+    const double* S = ring + slot * p.slot;
     const int* so = segoff + slot * kMaxSegs;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
@@ -511,20 +631,21 @@ __device__ void bwd_item(const SweepDev& p, ItemRec& R, const double* ring, cons
   for (int k = 0; k < kPer; ++k) {
     const int j = g.jlo + wid + kWarps * k;
     const double sum = warp_sum(acc[k]);
-    if (lane == 0 && j < g.jhi) X[cs[j]] = sum;
+    if (lane == 0 && j < g.jhi) X[slj[k]] = sum;
   }
   cta_signal(p.done_b + fs);
 }
 
-// Warp-specialised persistent CTA: kWarps consumer warps and one producer
-// warp. The producer takes tickets in order and streams every item's panel
-// through a kSlots-deep ring of shared-memory chunks (bulk copies, mbarrier
-// transaction counts), running ahead across item boundaries while the
-// consumers wait on dependencies and compute. A CTA holds at most kItems
-// tickets and its consumers run them in ticket order, so the smallest
-// unfinished ticket is always some CTA's current item, whose dependencies
-// (smaller tickets) are done, and whose chunks come first in its ring: no
-// deadlock.
+// Warp-specialised persistent CTA: kWarps consumer warps, one producer warp
+// and one preparation warp. The producer takes tickets in order and streams
+// every item's panel through a kSlots-deep ring of shared-memory chunks
+// (bulk copies, mbarrier transaction counts); the preparation warp waits for
+// the item's dependencies and assembles its front vector; both run one item
+// ahead of the consumers, which only wait for a prepared item, multiply from
+// shared memory and publish the result. A CTA holds at most kItems tickets
+// and runs them in ticket order, so the smallest unfinished ticket is always
+// some CTA's current item, whose dependencies (smaller tickets) are done,
+// and whose chunks come first in its ring: no deadlock.
 template <bool kFwd, int NR = 1>
 __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __restrict__ items, int n_items,
                                            int32_t* ticket, const double* __restrict__ panel, const double* X,
@@ -532,14 +653,15 @@ __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __rest
                                            RhsStride rs = RhsStride{0, 0, 0}) {
   extern __shared__ __align__(128) double shm[];
   double* ring = shm;
-  double* vec = shm + kSlots * kSlot;
-  double* part = vec + p.vec;
+  double* vecs = shm + kSlots * p.slot;
+  double* part = vecs + (size_t)kItems * p.vec;
   int* segoff = reinterpret_cast<int*>(part + kThreadsSweep);  // kSlots x kMaxSegs
   __shared__ ItemRec rec[kItems];
   __shared__ SlotRec sr[kSlots];
   if (threadIdx.x == 0) {
     for (int k = 0; k < kItems; ++k) {
       mbar_init(&rec[k].info, 1);
+      mbar_init(&rec[k].ready, 32);
       mbar_init(&rec[k].empty, 1);
     }
     for (int k = 0; k < kSlots; ++k) {
@@ -549,6 +671,10 @@ __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __rest
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (threadIdx.x >= kThreadsSweep + 32) {
+    preparer<kFwd, NR>(p, rec, vecs, X, ysave_in, upd, Xw, rs);
+    return;
+  }
   if (threadIdx.x >= kThreadsSweep) {
     producer(p, items, n_items, ticket, panel, rec, sr, ring, segoff, kFwd);
     return;
@@ -556,27 +682,28 @@ __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __rest
   int chunk_seq = 0;
   for (int k = 0;; ++k) {
     ItemRec& R = rec[k % kItems];
-    mbar_wait(&R.info, (k / kItems) & 1);
+    const double* V = vecs + (size_t)(k % kItems) * p.vec;
+    mbar_wait(&R.ready, (k / kItems) & 1);
     if (R.item.x < 0) break;
-    const int tk = R.tk;
-    const unsigned long long t_grab = R.t_grab;
-    unsigned long long t_dep = 0;
     if (kFwd)
-      fwd_item<NR>(p, R, ring, segoff, sr, chunk_seq, X, ysave, upd, vec, part, t_dep, rs);
+      fwd_item<NR>(p, R, ring, segoff, sr, chunk_seq, ysave, upd, V, part, rs);
     else
-      bwd_item(p, R, ring, segoff, sr, chunk_seq, Xw, ysave_in, vec, t_dep);
-    csync();  // vec / part are free (the item record was released after the dependency wait)
-    if (threadIdx.x == 0 && p.trace) {  // per ticket: {grab, dependencies met, done, SM}
-      unsigned long long* tr = p.trace + 4ll * tk;
-      tr[0] = t_grab;
-      tr[1] = t_dep;
-      tr[2] = gtimer();
-      tr[3] = smid();
+      bwd_item(p, R, ring, segoff, sr, chunk_seq, Xw, V);
+    csync();  // every consumer is done with the record and the vector
+    if (threadIdx.x == 0) {
+      if (p.trace) {  // per ticket: {grab, dependencies met, done, SM}
+        unsigned long long* tr = p.trace + 4ll * R.tk;
+        tr[0] = R.t_grab;
+        tr[1] = R.t_dep;
+        tr[2] = gtimer();
+        tr[3] = smid();
+      }
+      mbar_arrive(&R.empty);
     }
   }
 }
 
-__global__ void __launch_bounds__(kThreadsSweep + 32, kMinBlocks) k_sweep_fwd(SweepDev p, const int4* __restrict__ items, int n_items,
+__global__ void __launch_bounds__(kBlockSweep, kMinBlocks) k_sweep_fwd(SweepDev p, const int4* __restrict__ items, int n_items,
                                                              const double* __restrict__ panel,
                                                              const double* __restrict__ X, double* __restrict__ ysave,
                                                              double* upd, const int* __restrict__ skip) {
@@ -588,14 +715,14 @@ __global__ void __launch_bounds__(kThreadsSweep + 32, kMinBlocks) k_sweep_fwd(Sw
 // setup: H = L^{-1} C^T), same items and schedule as k_sweep_fwd.
 constexpr int kMultiRhs = 8;
 static_assert(kMultiRhs * kSmallRows <= 4096, "multi-RHS front vector");
-__global__ void __launch_bounds__(kThreadsSweep + 32, 1) k_sweep_fwd_multi(SweepDev p, const int4* __restrict__ items, int n_items,
+__global__ void __launch_bounds__(kBlockSweep, 1) k_sweep_fwd_multi(SweepDev p, const int4* __restrict__ items, int n_items,
                                                              const double* __restrict__ panel,
                                                              const double* __restrict__ X, double* __restrict__ ysave,
                                                              double* upd, RhsStride rs) {
   sweep_loop<true, kMultiRhs>(p, items, n_items, p.ticket, panel, X, nullptr, nullptr, ysave, upd, rs);
 }
 
-__global__ void __launch_bounds__(kThreadsSweep + 32, kMinBlocks) k_sweep_bwd(SweepDev p, const int4* __restrict__ items, int n_items,
+__global__ void __launch_bounds__(kBlockSweep, kMinBlocks) k_sweep_bwd(SweepDev p, const int4* __restrict__ items, int n_items,
                                                              const double* __restrict__ panel, double* X,
                                                              const double* __restrict__ ysave,
                                                              const int* __restrict__ skip, int ticket_slot) {
@@ -650,6 +777,8 @@ SweepDev sweep_dev(const FactorSet& f, int nsd, int nsn, unsigned long long* tra
                   f.fwd_cols,
                   f.bwd_cols,
                   f.sweep_vec,
+                  f.sweep_slot,
+                  f.sweep_bwd_rows,
                   f.l2_policy_f,
                   trace};
 }
@@ -686,7 +815,7 @@ int sweep_grid(const void* fn, size_t shm) {
   auto it = memo.find(key);
   if (it != memo.end()) return it->second;
   int per_sm = 0, sms = 0;
-  CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsSweep + 32, shm));
+  CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlockSweep, shm));
   CB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int g = std::max(1, per_sm) * sms;
   memo[key] = g;
@@ -736,6 +865,14 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   // shared front vector of this factorisation's sweeps: its largest front
   // (backward) or one column range (forward), 64-double granules
   f.sweep_vec = (std::max({tp.max_rows, f.fwd_cols, kSmallRows}) + 63) & ~63;
+  f.sweep_slot = h->nsd >= 256 ? kSlotWide : kSlotFew;
+  f.sweep_bwd_rows = h->nsd >= 256 ? kBwdRowsWide : kBwdRowsFew;
+#if defined(CUTBDDC_SWEEP_SLOT_DOUBLES) && defined(CUTBDDC_SWEEP_BWD_ROWS)
+  f.sweep_slot = CUTBDDC_SWEEP_SLOT_DOUBLES;
+  f.sweep_bwd_rows = CUTBDDC_SWEEP_BWD_ROWS;
+#endif
+  if (kMaxBwdCols * (f.sweep_bwd_rows + 2) > f.sweep_slot || 16 * (kFwdRows + 2) > f.sweep_slot)
+    throw Failure(CUTBDDC_INTERNAL, "sweep: chunk sizes exceed the ring slot");
   const int fc = f.fwd_cols, bc = f.bwd_cols;
   // S item: a front whose whole forward is one item (one row block, at most
   // small_work panel entries); larger fronts: row blocks x column ranges
@@ -989,9 +1126,9 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
   FactorSet& fm = const_cast<FactorSet&>(f);
   if (tp) fm.trace.alloc((size_t)4 * std::max(f.n_items_f, f.n_items_b) + 4);
   const SweepDev p = sweep_dev(f, nsd, nsn, tp ? fm.trace.p : nullptr);
-  const size_t shm = sweep_shm_bytes(f.sweep_vec);
+  const size_t shm = sweep_shm_bytes(f.sweep_slot, f.sweep_vec);
   device_memo(kMemoSweepAttr, [&] {
-    const int mx = (int)sweep_shm_bytes(kMultiRhs * std::max(kVecMax / kMultiRhs, kSmallRows));
+    const int mx = (int)sweep_shm_bytes(std::max(kSlotWide, kSlotFew), kMultiRhs * std::max(kVecMax / kMultiRhs, kSmallRows));
     CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CB_CUDA(cudaFuncSetAttribute(k_sweep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -1004,7 +1141,7 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
     ProfScope ps(h->prof, s, tag + " fwd");
     if (f.n_items_f > 0) {
       const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd, shm));
-      k_sweep_fwd<<<g, kThreadsSweep + 32, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, skip);
+      k_sweep_fwd<<<g, kBlockSweep, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, skip);
       CB_LAUNCH();
     }
     if (tp) dump_trace(std::string(tp) + "_" + tag + "_fwd.bin", f, true, s);
@@ -1018,7 +1155,7 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
   pb.l2_policy = f.l2_policy_b;
   if (b1 > b0) {
     const int g = std::min(b1 - b0, sweep_grid((const void*)k_sweep_bwd, shm));
-    k_sweep_bwd<<<g, kThreadsSweep + 32, shm, s>>>(pb, f.items_b.p + b0, b1 - b0, f.panel.p, X, ysave, skip, slot);
+    k_sweep_bwd<<<g, kBlockSweep, shm, s>>>(pb, f.items_b.p + b0, b1 - b0, f.panel.p, X, ysave, skip, slot);
     CB_LAUNCH();
   }
   if (tp && phase == kSweepBwd) dump_trace(std::string(tp) + "_" + tag + "_bwd.bin", f, false, s);
@@ -1036,13 +1173,13 @@ void sweep_forward_multi(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, c
   SweepDev p = sweep_dev(f, nsd, nsn, nullptr);
   p.vbuf = vbuf8;
   p.vec = (std::max(f.sweep_vec, kMultiRhs * std::max(f.fwd_cols, kSmallRows)) + 63) & ~63;
-  const size_t shm = sweep_shm_bytes(p.vec);
+  const size_t shm = sweep_shm_bytes(p.slot, p.vec);
   sweep_phase(h, ts, f, nullptr, nullptr, nullptr, nullptr, kSweepAttrOnly);
   CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
   if (f.n_items_f == 0) return;
   const RhsStride rs{(int64_t)nsd * h->slots, f.upd_total, (int64_t)f.vbuf.n};
   const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd_multi, shm));
-  k_sweep_fwd_multi<<<g, kThreadsSweep + 32, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, rs);
+  k_sweep_fwd_multi<<<g, kBlockSweep, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, rs);
   CB_LAUNCH();
 }
 
