@@ -67,8 +67,8 @@ constexpr int kWarps = kThreadsSweep / 32;
 // factorisation (SweepDev::slot, ::bwd_rows): many subdomains -> 4 CTAs per
 // SM with 20 KB slots, few -> 3 CTAs with 28 KB slots (fewer, longer chunks
 // per item). The macros override both.
-constexpr int kSlotWide = 2560, kBwdRowsWide = 78;      // nsd >= 256 (tuned on cfg5)
-constexpr int kSlotFew = 3584, kBwdRowsFew = 110;       // fewer subdomains (tuned on cfg4)
+constexpr int kSlotWide = 2176, kBwdRowsWide = 66;      // floor for nsd >= 256 (cfg5 runs 2752 / 84)
+constexpr int kSlotFew = 2176, kBwdRowsFew = 66;        // floor for fewer subdomains (cfg4 runs 3968 / 122)
 constexpr int kMaxSegs = 32;                        // column segments per chunk
 constexpr int kVecMax = 2048;                       // front vector (shared): at most this many rows per front
 #ifndef CUTBDDC_SWEEP_ITEMS_IN_FLIGHT
@@ -865,13 +865,26 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   // shared front vector of this factorisation's sweeps: its largest front
   // (backward) or one column range (forward), 64-double granules
   f.sweep_vec = (std::max({tp.max_rows, f.fwd_cols, kSmallRows}) + 63) & ~63;
-  f.sweep_slot = h->nsd >= 256 ? kSlotWide : kSlotFew;
-  f.sweep_bwd_rows = h->nsd >= 256 ? kBwdRowsWide : kBwdRowsFew;
+  // ring slots: the largest that still lets 4 (many subdomains) or 3 (few)
+  // CTAs share an SM's 228 KB (1 KB reserved and ~0.5 KB static per CTA)
+  {
+    const int ctas = h->nsd >= 256 ? 4 : 3;
+    const long long per_cta = 228 * 1024 / ctas - 1024 - 512;
+    const long long rest = (long long)sweep_shm_bytes(0, f.sweep_vec);
+    long long slot = (per_cta - rest) / (8 * kSlots) / 32 * 32;
+    slot = std::max<long long>(h->nsd >= 256 ? kSlotWide : kSlotFew, std::min<long long>(slot, 4096));
+    f.sweep_slot = (int)slot;
+    f.sweep_bwd_rows = ((int)slot / kMaxBwdCols - 2) & ~1;  // even: a staged column takes rows + 2 doubles
+  }
 #if defined(CUTBDDC_SWEEP_SLOT_DOUBLES) && defined(CUTBDDC_SWEEP_BWD_ROWS)
   f.sweep_slot = CUTBDDC_SWEEP_SLOT_DOUBLES;
   f.sweep_bwd_rows = CUTBDDC_SWEEP_BWD_ROWS;
 #endif
-  if (kMaxBwdCols * (f.sweep_bwd_rows + 2) > f.sweep_slot || 16 * (kFwdRows + 2) > f.sweep_slot)
+  if (const char* e = std::getenv("CUTBDDC_SWEEP_RING")) std::sscanf(e, "%d,%d", &f.sweep_slot, &f.sweep_bwd_rows);  // A/B hook
+  if (std::getenv("CUTBDDC_SWEEP_STATS"))
+    std::fprintf(stderr, "[sweep stats] nsd %d max_rows %d vec %d slot %d bwd_rows %d shm %zu\n", h->nsd, tp.max_rows,
+                 f.sweep_vec, f.sweep_slot, f.sweep_bwd_rows, sweep_shm_bytes(f.sweep_slot, f.sweep_vec));
+  if (kMaxBwdCols * seg_stride(f.sweep_bwd_rows) > f.sweep_slot || 16 * seg_stride(kFwdRows) > f.sweep_slot)
     throw Failure(CUTBDDC_INTERNAL, "sweep: chunk sizes exceed the ring slot");
   const int fc = f.fwd_cols, bc = f.bwd_cols;
   // S item: a front whose whole forward is one item (one row block, at most
@@ -1128,7 +1141,7 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
   const SweepDev p = sweep_dev(f, nsd, nsn, tp ? fm.trace.p : nullptr);
   const size_t shm = sweep_shm_bytes(f.sweep_slot, f.sweep_vec);
   device_memo(kMemoSweepAttr, [&] {
-    const int mx = (int)sweep_shm_bytes(std::max(kSlotWide, kSlotFew), kMultiRhs * std::max(kVecMax / kMultiRhs, kSmallRows));
+    const int mx = 200 * 1024;  // any ring / vector size in use
     CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CB_CUDA(cudaFuncSetAttribute(k_sweep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
