@@ -319,6 +319,9 @@ def main():
         lp = None
     mesh, block_ids, objs = pb.mesh, pb.block_ids, pb.objects
     n_dof = mesh.n_dof
+    # the caller's BackgroundMesh arrays are page-locked once (cutbddc_host_pin):
+    # the e2e uploads below are asynchronous DMA from pinned host memory
+    pinned = [cb.pin(a) for a in (mesh.phi, mesh.cls, mesh.dof_of_node)]
 
     def assemble(s, mesh_view=None):  # the global partition; a distributed handle takes its own subdomains
         return s.assemble(cfg.block, block_ids, mesh=mesh_view)
@@ -403,6 +406,8 @@ def main():
             roof["traffic"] = json.load(open(tj))["traffic_bytes_per_apply"]
             roof["traffic_source"] = f"profiles/{tname} (ncu --set full, dram read+write)"
             break
+    for a in pinned:
+        cb.unpin(a)
     solver.close()
 
     cfg5 = None

@@ -182,6 +182,14 @@ cutbddc_status cutbddc_gpu_dense_cholesky(cutbddc_gpu* h, int n, const double* a
  * [16]=subdomains of this rank on K = A + rho C^T C while the others use K_c
  * (a mixed K: K_c singular there, e.g. a floating fragment); counted in [11]/[12]. */
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* stats);
+/* Page-lock a caller-owned host buffer (cudaHostRegister) so the uploads of
+ * the mesh view in cutbddc_gpu_assemble and the download of the solution in
+ * cutbddc_gpu_pcg run as asynchronous DMA instead of staged pageable copies.
+ * Optional: the reference's BackgroundMesh arrays (mesh.hpp:77-80) live for
+ * many solves, so the caller pins them once. unpin before freeing. */
+cutbddc_status cutbddc_host_pin(void* ptr, size_t bytes);
+cutbddc_status cutbddc_host_unpin(void* ptr);
+
 /* Measurement hook: average device time of the triangular-solve sweeps of
  * one BDDC apply (interior, Neumann, interior) over `reps` repetitions, and
  * their algorithmic bytes (panel lower parts + front vectors). */

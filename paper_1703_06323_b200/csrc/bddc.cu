@@ -762,6 +762,29 @@ __global__ void __launch_bounds__(256) k_coarse_out(int nc, const int64_t* __res
   X[cslot[rinfo[4 * sd + 2] + j]] += v;
 }
 
+// Slot of every constraint-row entry in its subdomain's (B+1)^3 lattice:
+// entry e is dof[e] seen from local subdomain blk[e]. bad: 1 + the first
+// subdomain found with an object dof outside its block.
+__global__ void k_row_slots(int64_t ne, int n, int B, int nb, int b1, const int32_t* __restrict__ dof,
+                            const int32_t* __restrict__ blk, const int64_t* __restrict__ block_ids,
+                            const int64_t* __restrict__ node_of_dof, int32_t* __restrict__ c_slot,
+                            int* __restrict__ bad) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const int sd = blk[e];
+  const int64_t bid = block_ids[sd];
+  const int bi = (int)(bid / nb / nb), bj = (int)((bid / nb) % nb), bk = (int)(bid % nb);
+  const int64_t v = node_of_dof[dof[e]];
+  const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
+  const int lx = i - bi * B, ly = j - bj * B, lz = k - bk * B;
+  if (lx < 0 || ly < 0 || lz < 0 || lx > B || ly > B || lz > B) {
+    atomicCAS(bad, 0, 1 + sd);
+    c_slot[e] = 0;
+    return;
+  }
+  c_slot[e] = (lx * b1 + ly) * b1 + lz;
+}
+
 __global__ void k_row_sd(int nsd, const int64_t* __restrict__ m_off, int32_t* __restrict__ row_sd) {
   const int sd = blockIdx.x;
   for (int64_t r = m_off[sd] + threadIdx.x; r < m_off[sd + 1]; r += blockDim.x) row_sd[r] = sd;
@@ -945,7 +968,6 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   ProfScope ps_host(h->prof, s, "setup 0 host rows+uploads+weights");
   const int nc = cv ? cv->n_objects : 0;
   const int nsd_g = h->nsd_g, world = h->dist_world, rank = h->dist_rank;
-  std::vector<int64_t> node_of_dof = h->node_of_dof.to_host(s);
   ps_host.next("setup 0a host rows");
   std::vector<std::vector<int>> obj_of_gsd((size_t)nsd_g);  // object ids per global sd (ascending)
   for (int o = 0; o < nc; ++o)
@@ -989,15 +1011,16 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
       cg[(size_t)o].push_back(p);  // ascending global sd
     }
   }
+  // constraint rows: per (subdomain, object) the object's dofs; their slots in
+  // the subdomain's lattice are computed on the device (k_row_slots) from
+  // node_of_dof, so the host never needs the mesh maps
   std::vector<int64_t> m_off((size_t)nsd + 1, 0), c_ptr{0};
-  std::vector<int32_t> c_slot, coarse_id;
+  std::vector<int32_t> c_dof, c_blk, coarse_id;
   std::vector<double> c_val;
   std::vector<uint8_t> corner;
   const int n = h->n, B = h->block, nb = h->nb;
   for (int sd = 0; sd < nsd; ++sd) {
     const int g = h->global_of_local[(size_t)sd];
-    const int64_t bid = h->h_block_ids[(size_t)sd];
-    const int bi = (int)(bid / nb / nb), bj = (int)((bid / nb) % nb), bk = (int)(bid % nb);
     for (int o : obj_of_gsd[(size_t)g]) {
       coarse_id.push_back(o);
       corner.push_back(cv->kinds[o] == CUTBDDC_CORNER);
@@ -1006,15 +1029,11 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
       for (int64_t p = cv->dof_ptr[o]; p < cv->dof_ptr[o + 1]; ++p) {
         const int32_t d = cv->dofs[p];
         if (d < 0 || d >= h->n_dof) throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: dof out of range");
-        const int64_t v = node_of_dof[(size_t)d];
-        const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
-        const int lx = i - bi * B, ly = j - bj * B, lz = k - bk * B;
-        if (lx < 0 || ly < 0 || lz < 0 || lx > B || ly > B || lz > B)
-          throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: object dof not in neighbour subdomain " + std::to_string(g));
-        c_slot.push_back((lx * b1 + ly) * b1 + lz);
+        c_dof.push_back(d);
+        c_blk.push_back(sd);
         c_val.push_back(coef);
       }
-      c_ptr.push_back((int64_t)c_slot.size());
+      c_ptr.push_back((int64_t)c_dof.size());
     }
     m_off[(size_t)sd + 1] = (int64_t)coarse_id.size();
   }
@@ -1034,12 +1053,27 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     for (int64_t r : cg[(size_t)o]) cg_idx.push_back(r);
     cg_ptr.push_back((int64_t)cg_idx.size());
   }
-  if (c_slot.empty()) c_slot.push_back(0), c_val.push_back(0.0);
+  const int64_t n_centries = (int64_t)c_dof.size();
+  if (c_dof.empty()) c_dof.push_back(0), c_blk.push_back(0), c_val.push_back(0.0);
   if (coarse_id.empty()) coarse_id.push_back(0), corner.push_back(0);
   if (cg_idx.empty()) cg_idx.push_back(0);
   h->m_off.upload(m_off, s);
   h->c_ptr.upload(c_ptr, s);
-  h->c_slot.upload(c_slot, s);
+  {
+    DevBuf<int32_t>& d_dof = h->ws_cdof;
+    DevBuf<int32_t>& d_blk = h->ws_cblk;
+    d_dof.upload(c_dof, s);
+    d_blk.upload(c_blk, s);
+    h->c_slot.alloc(c_dof.size());
+    DevBuf<int>& flags = h->ws_flag;  // [0] weights, [1] constraint rows: read together after the weights
+    flags.alloc(2);
+    flags.zero(s);
+    if (n_centries > 0) {
+      k_row_slots<<<grid_for(n_centries, 256), 256, 0, s>>>(n_centries, n, B, nb, b1, d_dof.p, d_blk.p, h->block_ids.p,
+                                                            h->node_of_dof.p, h->c_slot.p, flags.p + 1);
+      CB_LAUNCH();
+    }
+  }
   h->c_val.upload(c_val, s);
   h->coarse_id.upload(coarse_id, s);
   h->cg_ptr.upload(cg_ptr, s);
@@ -1054,9 +1088,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   CB_LAUNCH();
   ps_host.next("setup 0b weights");
   // ---- weights, rho
-  DevBuf<int>& bad = h->ws_flag;
-  bad.alloc(1);
-  bad.zero(s);
+  DevBuf<int>& bad = h->ws_flag;  // zeroed with the constraint rows above
   h->w.alloc((size_t)ns);
   h->dtot.alloc((size_t)std::max<int64_t>(1, h->n_loc));
   h->sv2.alloc((size_t)ns);
@@ -1124,10 +1156,14 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     h->diag_add.zero(s);
     k_diag_add<<<nsd, 128, 0, s>>>(nsd, T, h->m_off.p, h->c_ptr.p, h->c_slot.p, d_corner, h->rho.p, h->diag_add.p);
     CB_LAUNCH();
-    int hbad = 0;
-    CB_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
+    int hbad[2] = {0, 0};
+    CB_CUDA(cudaMemcpyAsync(hbad, bad.p, 8, cudaMemcpyDeviceToHost, s));
     CB_CUDA(cudaStreamSynchronize(s));
-    if (hbad) throw Failure(CUTBDDC_DEGENERATE, "weighting: zero total diagonal at an interface dof");
+    if (hbad[1])
+      throw Failure(CUTBDDC_INVALID_ARGUMENT,
+                    "coarse view: object dof not in neighbour subdomain " +
+                        std::to_string(h->global_of_local[(size_t)(hbad[1] - 1)]));
+    if (hbad[0]) throw Failure(CUTBDDC_DEGENERATE, "weighting: zero total diagonal at an interface dof");
     ps_host.next("setup 1 factorisations");
     // ---- factorisations
     if (!h->tI.ready || h->tI.tpl.b1 != b1) upload_template(h, h->tI, false);

@@ -7,6 +7,7 @@
 namespace cutbddc_b200 {
 
 void classify_device(cutbddc_gpu* h, const cutbddc_geometry* g);
+void node_of_dof_device(cutbddc_gpu* h);  // geometry.cu: node_of_dof from an uploaded dof_of_node
 void assemble_device(cutbddc_gpu* h, const cutbddc_partition_view* part);
 cutbddc_objects* classify_objects_device(cutbddc_gpu* h, int objects, int variant);
 void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weighting);

@@ -123,7 +123,7 @@ void host_to_local(cutbddc_gpu* h, const double* x, DevBuf<double>& loc) {
 }
 // owned entries into the caller's n_dof buffer (others untouched)
 void local_to_host(cutbddc_gpu* h, const double* loc, double* x) {
-  DevBuf<double> g;
+  DevBuf<double>& g = h->ws_global;  // held by the handle: no cudaMalloc / cudaFree per call
   if (h->n_own == h->n_dof) {
     g.alloc((size_t)h->n_dof);
   } else {
@@ -281,13 +281,7 @@ cutbddc_status cutbddc_gpu_assemble(cutbddc_gpu* h, const cutbddc_mesh_view* mes
       h->phi.upload(mesh->phi, (size_t)h->n_nodes, h->stream);
       h->cls.upload(mesh->cls, (size_t)h->n_cells, h->stream);
       h->dof_of_node.upload(mesh->dof_of_node, (size_t)h->n_nodes, h->stream);
-      std::vector<int64_t> nod((size_t)h->n_dof);
-      for (int64_t v = 0; v < h->n_nodes; ++v)
-        if (mesh->dof_of_node[v] >= 0) {
-          if (mesh->dof_of_node[v] >= h->n_dof) throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: dof id out of range");
-          nod[(size_t)mesh->dof_of_node[v]] = v;
-        }
-      h->node_of_dof.upload(nod, h->stream);
+      node_of_dof_device(h);  // inverse map on the device (checks the dof ids)
       h->mesh_ready = true;
     }
     if (!h->mesh_ready) throw Failure(CUTBDDC_INVALID_ARGUMENT, "assemble: no mesh (classify first or pass a view)");
@@ -584,6 +578,20 @@ cutbddc_status cutbddc_gpu_time_factor(cutbddc_gpu* h, double* seconds, double* 
 
 cutbddc_status cutbddc_fp64_peak(int device, double* dmma_tflops, double* dfma_tflops) {
   return guard([&] { fp64_peaks(device, dmma_tflops, dfma_tflops); });
+}
+
+cutbddc_status cutbddc_host_pin(void* ptr, size_t bytes) {
+  return guard([&] {
+    if (!ptr || bytes == 0) throw Failure(CUTBDDC_INVALID_ARGUMENT, "host_pin: empty buffer");
+    CB_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+  });
+}
+
+cutbddc_status cutbddc_host_unpin(void* ptr) {
+  return guard([&] {
+    if (!ptr) throw Failure(CUTBDDC_INVALID_ARGUMENT, "host_unpin: null buffer");
+    CB_CUDA(cudaHostUnregister(ptr));
+  });
 }
 
 cutbddc_status cutbddc_gpu_stats(cutbddc_gpu* h, int64_t* st) {

@@ -73,7 +73,36 @@ __global__ void k_number(int64_t nn, const int32_t* __restrict__ flag, int32_t* 
   }
 }
 
+// node_of_dof from an uploaded dof_of_node map (the caller's BackgroundMesh
+// view); bad[0] is set when a dof id is out of range.
+__global__ void k_node_of_dof(int64_t nn, int64_t n_dof, const int32_t* __restrict__ dof,
+                              int64_t* __restrict__ node_of_dof, int* __restrict__ bad) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = dof[v];
+    if (d < 0) continue;
+    if (d >= n_dof)
+      atomicExch(bad, 1);
+    else
+      node_of_dof[d] = v;
+  }
+}
+
 }  // namespace
+
+void node_of_dof_device(cutbddc_gpu* h) {
+  cudaStream_t s = h->stream;
+  DevBuf<int>& bad = h->ws_flag;
+  bad.alloc(1);
+  bad.zero(s);
+  h->node_of_dof.alloc((size_t)std::max<int64_t>(1, h->n_dof));
+  const int grid = (int)std::min<int64_t>((h->n_nodes + 255) / 256, 148 * 8);
+  k_node_of_dof<<<grid, 256, 0, s>>>(h->n_nodes, h->n_dof, h->dof_of_node.p, h->node_of_dof.p, bad.p);
+  CB_LAUNCH();
+  int hb = 0;
+  CB_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CB_CUDA(cudaStreamSynchronize(s));
+  if (hb) throw Failure(CUTBDDC_INVALID_ARGUMENT, "mesh view: dof id out of range");
+}
 
 void classify_device(cutbddc_gpu* h, const cutbddc_geometry* g) {
   if (g->cells[0] != g->cells[1] || g->cells[1] != g->cells[2])

@@ -86,6 +86,7 @@ EXPORTS = [
     "cutbddc_assign_subdomains", "cutbddc_nccl_unique_id", "cutbddc_gpu_set_distribution", "cutbddc_gpu_time_factor",
     "cutbddc_fp64_peak", "cutbddc_build_exchange_plan", "cutbddc_gpu_exchange_plan", "cutbddc_exchange_plan_free",
     "cutbddc_gpu_time_parts", "cutbddc_gpu_set_problem", "cutbddc_gpu_error_norms", "cutbddc_gpu_dense_cholesky",
+    "cutbddc_host_pin", "cutbddc_host_unpin",
 ]
 
 
@@ -252,6 +253,19 @@ def exchange_plan(mesh: Mesh, block: int, block_ids: np.ndarray, rank_of_sd: np.
     out = C.POINTER(_Plan)()
     _check(lib().cutbddc_build_exchange_plan(C.byref(mv), C.byref(pv), _p(ros, C.c_int32), rank, world, C.byref(out)))
     return _take_plan(out)
+
+
+def pin(a: np.ndarray) -> np.ndarray:
+    """Page-lock a host array in place (cutbddc_host_pin): uploads from it and
+    downloads into it become asynchronous DMA. Call unpin before it is freed."""
+    lib().cutbddc_host_pin.argtypes = [C.c_void_p, C.c_size_t]
+    _check(lib().cutbddc_host_pin(C.c_void_p(a.ctypes.data), C.c_size_t(a.nbytes)))
+    return a
+
+
+def unpin(a: np.ndarray) -> None:
+    lib().cutbddc_host_unpin.argtypes = [C.c_void_p]
+    _check(lib().cutbddc_host_unpin(C.c_void_p(a.ctypes.data)))
 
 
 def nccl_unique_id() -> bytes:
