@@ -317,3 +317,35 @@ def test_cut_elements_warp_form_bit_exact(name):
     assert np.array_equal(ke, ke2) and np.array_equal(fe, fe2)
     assert np.array_equal(beta, beta2) and np.array_equal(empty, empty2)
     s.close()
+
+
+def test_mesh_view_upload_pinned_and_checked():
+    """The caller's BackgroundMesh view (host buffers): the same solve from
+    pageable and from page-locked arrays (cutbddc_host_pin), and a dof id out
+    of range is rejected by the device-side inverse map."""
+    import dataclasses
+    cfg = configs.get("cfg1")
+    s = cb.GpuSolver(0)
+    pb = cb.prepare(s, cfg)
+
+    def solve(mesh):
+        s.assemble(cfg.block, pb.block_ids, mesh=mesh)
+        s.setup_bddc(s.classify_objects(cfg.objects, cfg.variant), cfg.weighting)
+        return s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
+
+    x0, rep0 = solve(pb.mesh)
+    arrays = [pb.mesh.phi, pb.mesh.cls, pb.mesh.dof_of_node]
+    for a in arrays:
+        cb.pin(a)
+    try:
+        x1, rep1 = solve(pb.mesh)
+    finally:
+        for a in arrays:
+            cb.unpin(a)
+    assert rep0["iterations"] == rep1["iterations"] and np.array_equal(x0, x1)
+    bad = pb.mesh.dof_of_node.copy()
+    bad[np.flatnonzero(bad >= 0)[0]] = pb.mesh.n_dof
+    with pytest.raises(cb.CutbddcError) as e:
+        s.assemble(cfg.block, pb.block_ids, mesh=dataclasses.replace(pb.mesh, dof_of_node=bad))
+    assert e.value.code == cb.INVALID_ARGUMENT
+    s.close()
