@@ -93,7 +93,10 @@ void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
                  const int* skip);
 enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3, kSweepAttrOnly = 4 };
 // sweep.cu: forward sweep of kSweepMultiRhs right-hand sides at once
-constexpr int kSweepMultiRhs = 8;
+#ifndef CUTBDDC_MULTI_RHS
+#define CUTBDDC_MULTI_RHS 13  // tuned on B200 (cfg4, m_max 37: three passes; 8: 731 us, 13: 554 us, 16: 653 us)
+#endif
+constexpr int kSweepMultiRhs = CUTBDDC_MULTI_RHS;
 void sweep_forward_multi(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, const double* X, double* ysave,
                          double* upd, double* vbuf8);
 void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,

@@ -713,9 +713,12 @@ __global__ void __launch_bounds__(kBlockSweep, kMinBlocks) k_sweep_fwd(SweepDev 
 
 // Forward sweep of kMultiRhs right-hand sides at once (the coarse-basis
 // setup: H = L^{-1} C^T), same items and schedule as k_sweep_fwd.
-constexpr int kMultiRhs = 8;
+constexpr int kMultiRhs = kSweepMultiRhs;
 static_assert(kMultiRhs * kSmallRows <= 4096, "multi-RHS front vector");
-__global__ void __launch_bounds__(kBlockSweep, 1) k_sweep_fwd_multi(SweepDev p, const int4* __restrict__ items, int n_items,
+#ifndef CUTBDDC_MULTI_MIN_BLOCKS
+#define CUTBDDC_MULTI_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kBlockSweep, CUTBDDC_MULTI_MIN_BLOCKS) k_sweep_fwd_multi(SweepDev p, const int4* __restrict__ items, int n_items,
                                                              const double* __restrict__ panel,
                                                              const double* __restrict__ X, double* __restrict__ ysave,
                                                              double* upd, RhsStride rs) {
@@ -1186,6 +1189,9 @@ void sweep_forward_multi(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, c
   SweepDev p = sweep_dev(f, nsd, nsn, nullptr);
   p.vbuf = vbuf8;
   p.vec = (std::max(f.sweep_vec, kMultiRhs * std::max(f.fwd_cols, kSmallRows)) + 63) & ~63;
+#ifdef CUTBDDC_MULTI_SLOT
+  p.slot = CUTBDDC_MULTI_SLOT;  // the ring geometry is per launch
+#endif
   const size_t shm = sweep_shm_bytes(p.slot, p.vec);
   sweep_phase(h, ts, f, nullptr, nullptr, nullptr, nullptr, kSweepAttrOnly);
   CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
