@@ -57,7 +57,10 @@ __device__ __forceinline__ void assemble_block(double* __restrict__ F, int ld, i
                                                const RowInfo* ri, const RowInfo* rj, const ChildBlocks& cb,
                                                const FactorInput& in, int sd) {
   const int h = i1 - i0, n = h * (j1 - j0);
-  constexpr int kB = 4;
+#ifndef CUTBDDC_ASM_BATCH
+#define CUTBDDC_ASM_BATCH 4
+#endif
+  constexpr int kB = CUTBDDC_ASM_BATCH;
   for (int q0 = threadIdx.x; q0 < n; q0 += kB * blockDim.x) {
     double v[kB];
 #pragma unroll

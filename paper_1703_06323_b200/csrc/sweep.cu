@@ -59,7 +59,10 @@ constexpr int kFwdRows = CUTBDDC_SWEEP_FWD_ROWS;    // forward items of larger f
 // ... cut into column ranges of SweepDev::fwd_cols columns; backward items:
 // column blocks of SweepDev::bwd_cols (<= kMaxBwdCols) columns, all rows
 // below. Both are chosen per factorisation by the plan (choose_item_sizes).
-constexpr int kMaxBwdCols = 32;
+#ifndef CUTBDDC_SWEEP_MAX_BWD_COLS
+#define CUTBDDC_SWEEP_MAX_BWD_COLS 32
+#endif
+constexpr int kMaxBwdCols = CUTBDDC_SWEEP_MAX_BWD_COLS;
 constexpr int kSlots = CUTBDDC_SWEEP_SLOTS;         // staging ring depth (chunks in flight per CTA)
 constexpr int kMinBlocks = CUTBDDC_SWEEP_MIN_BLOCKS;
 constexpr int kWarps = kThreadsSweep / 32;
@@ -69,7 +72,8 @@ constexpr int kWarps = kThreadsSweep / 32;
 // per item). The macros override both.
 constexpr int kSlotWide = 2176, kBwdRowsWide = 66;      // floor for nsd >= 256 (cfg5 runs 2752 / 84)
 constexpr int kSlotFew = 2176, kBwdRowsFew = 66;        // floor for fewer subdomains (cfg4 runs 3968 / 122)
-constexpr int kMaxSegs = 32;                        // column segments per chunk
+constexpr int kMaxSegs = kMaxBwdCols;               // column segments per chunk (a multiple of 32)
+static_assert(kMaxSegs % 32 == 0, "segments per chunk");
 constexpr int kVecMax = 2048;                       // front vector (shared): at most this many rows per front
 #ifndef CUTBDDC_SWEEP_ITEMS_IN_FLIGHT
 #define CUTBDDC_SWEEP_ITEMS_IN_FLIGHT 2
@@ -83,8 +87,7 @@ inline size_t sweep_shm_bytes(int slot, int vec) {
 }
 static_assert(kThreadsSweep % kFwdRows == 0 && kFwdRows % 32 == 0, "forward row blocks");
 static_assert(kMaxBwdCols <= kMaxSegs && kMaxBwdCols % kWarps == 0, "backward column blocks");
-static_assert(kMaxBwdCols * (kBwdRowsWide + 2) <= kSlotWide && 16 * (kFwdRows + 2) <= kSlotWide, "chunk sizes");
-static_assert(kMaxBwdCols * (kBwdRowsFew + 2) <= kSlotFew && 16 * (kFwdRows + 2) <= kSlotFew, "chunk sizes");
+static_assert(16 * (kFwdRows + 2) <= kSlotWide && 16 * (kFwdRows + 2) <= kSlotFew, "chunk sizes");
 enum { kItemS = 0, kItemC = 2 };
 
 // column stride (doubles, even: every staged column starts 16-byte aligned)
@@ -267,29 +270,39 @@ __device__ __forceinline__ void produce_chunk(const FrontDesc& d, const Chunk& c
                                               double* buf, int* segoff, SlotRec& sr, int l2_kind, uint64_t pol) {
   const int lane = threadIdx.x & 31;
   const int stride = seg_stride(ch.hi - ch.lo);
-  const int jj = lane;
-  const int j = ch.ja + jj;
-  int64_t a = 0, n = 0;
-  if (j < ch.jb) {
-    const int first = max(j, ch.lo);
-    if (first < ch.hi) {
-      const int64_t e = d.po + (int64_t)j * d.r + first;
-      a = e & ~1ll;
-      n = ((e + (ch.hi - first) + 1) & ~1ll) - a;
-      segoff[jj] = jj * stride + (int)(e - a) - first;
+  int64_t a[kMaxSegs / 32], n[kMaxSegs / 32];
+  uint32_t mine = 0;
+#pragma unroll
+  for (int u = 0; u < kMaxSegs / 32; ++u) {
+    const int jj = lane + 32 * u;
+    const int j = ch.ja + jj;
+    a[u] = n[u] = 0;
+    if (j < ch.jb) {
+      const int first = max(j, ch.lo);
+      if (first < ch.hi) {
+        const int64_t e = d.po + (int64_t)j * d.r + first;
+        a[u] = e & ~1ll;
+        n[u] = ((e + (ch.hi - first) + 1) & ~1ll) - a[u];
+        segoff[jj] = jj * stride + (int)(e - a[u]) - first;
+      }
     }
+    mine += (uint32_t)(8 * n[u]);
   }
-  const uint32_t bytes = __reduce_add_sync(0xffffffffu, (uint32_t)(8 * n));
+  const uint32_t bytes = __reduce_add_sync(0xffffffffu, mine);
   if (lane == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&sr.full, bytes);
   }
   __syncwarp();
-  if (n > 0) {
-    if (l2_kind)
-      bulk_g2s_hint(buf + jj * stride, panel + a, (uint32_t)(8 * n), &sr.full, pol);
-    else
-      bulk_g2s(buf + jj * stride, panel + a, (uint32_t)(8 * n), &sr.full);
+#pragma unroll
+  for (int u = 0; u < kMaxSegs / 32; ++u) {
+    const int jj = lane + 32 * u;
+    if (n[u] > 0) {
+      if (l2_kind)
+        bulk_g2s_hint(buf + jj * stride, panel + a[u], (uint32_t)(8 * n[u]), &sr.full, pol);
+      else
+        bulk_g2s(buf + jj * stride, panel + a[u], (uint32_t)(8 * n[u]), &sr.full);
+    }
   }
 }
 
@@ -877,7 +890,8 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
     long long slot = (per_cta - rest) / (8 * kSlots) / 32 * 32;
     slot = std::max<long long>(h->nsd >= 256 ? kSlotWide : kSlotFew, std::min<long long>(slot, 4096));
     f.sweep_slot = (int)slot;
-    f.sweep_bwd_rows = ((int)slot / kMaxBwdCols - 2) & ~1;  // even: a staged column takes rows + 2 doubles
+    // backward chunks fill the slot: bwd_cols columns x as many rows as fit (even: a staged column takes rows + 2 doubles)
+    f.sweep_bwd_rows = std::min(1024, ((int)slot / f.bwd_cols - 2) & ~1);
   }
 #if defined(CUTBDDC_SWEEP_SLOT_DOUBLES) && defined(CUTBDDC_SWEEP_BWD_ROWS)
   f.sweep_slot = CUTBDDC_SWEEP_SLOT_DOUBLES;
@@ -887,7 +901,7 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
   if (std::getenv("CUTBDDC_SWEEP_STATS"))
     std::fprintf(stderr, "[sweep stats] nsd %d max_rows %d vec %d slot %d bwd_rows %d shm %zu\n", h->nsd, tp.max_rows,
                  f.sweep_vec, f.sweep_slot, f.sweep_bwd_rows, sweep_shm_bytes(f.sweep_slot, f.sweep_vec));
-  if (kMaxBwdCols * seg_stride(f.sweep_bwd_rows) > f.sweep_slot || 16 * seg_stride(kFwdRows) > f.sweep_slot)
+  if (f.bwd_cols * seg_stride(f.sweep_bwd_rows) > f.sweep_slot || 16 * seg_stride(kFwdRows) > f.sweep_slot)
     throw Failure(CUTBDDC_INTERNAL, "sweep: chunk sizes exceed the ring slot");
   const int fc = f.fwd_cols, bc = f.bwd_cols;
   // S item: a front whose whole forward is one item (one row block, at most
