@@ -233,6 +233,11 @@ __device__ __forceinline__ ItemGeom item_geom(const SweepDev& p, const FrontDesc
       g.jhi = min(min(c, g.i1), g.jlo + kFwdCols);
     }
     g.cw = max(1, min(kMaxSegs, p.slot / seg_stride(g.i1 - g.i0)));
+    // chunks start at multiples of fwd_item's thread-group count ng (a power
+    // of two): the sums do not depend on the ring's slot size
+    const int nr = g.i1 - g.i0;
+    const int ng = nr <= kThreadsSweep / 8 ? 8 : nr <= kThreadsSweep / 4 ? 4 : nr <= kThreadsSweep / 2 ? 2 : 1;
+    if (g.cw >= ng) g.cw &= ~(ng - 1);
     g.nchunk = g.jhi > g.jlo ? (g.jhi - g.jlo + g.cw - 1) / g.cw : 0;
   } else {
     g.jlo = chunk * kBwdCols;
@@ -544,6 +549,8 @@ __device__ void fwd_item(const SweepDev& p, const ItemRec& R, const double* ring
     const double* S = ring + slot * p.slot;
     const int* so = segoff + slot * kMaxSegs;
     if (grp < ng && row < nrow) {
+      // chunk widths are multiples of ng (item_geom): column j of the item
+      // belongs to thread group (j - jlo) % ng whatever the ring's slot size
       const int jend = min(ch.jb, i + 1);
       for (int j = ch.ja + grp; j < jend; j += ng) {
         const double gij = S[so[j - ch.ja] + i];
@@ -634,8 +641,10 @@ __device__ void bwd_item(const SweepDev& p, const ItemRec& R, const double* ring
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const int j = g.jlo + wid + kWarps * k;
-      if (j < g.jhi)
-        for (int i = max(j, ch.lo) + lane; i < ch.hi; i += 32) acc[k] += S[so[j - g.jlo] + i] * w[i];
+      if (j < g.jhi) {  // row i of column j belongs to lane (i - j) % 32, whatever the chunking
+        const int lo = max(j, ch.lo);
+        for (int i = lo + ((lane - (lo - j)) & 31); i < ch.hi; i += 32) acc[k] += S[so[j - g.jlo] + i] * w[i];
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sr[slot].empty);

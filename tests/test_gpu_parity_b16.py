@@ -196,3 +196,31 @@ def test_device_task_list_equals_host(monkeypatch):
         s.close()
         for k in env:
             monkeypatch.delenv(k)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_sweeps_independent_of_ring_configuration(name):
+    """The solve sweeps' sums do not depend on the shared-memory ring's slot
+    size or chunk height (chosen per factorisation from the subdomain count,
+    so ranks of one job may differ): bit-identical solves under four ring
+    configurations."""
+    cfg = configs.get(name)
+    outs = []
+    for ring in (None, "2176,66", "3072,94", "4352,134"):
+        if ring is None:
+            os.environ.pop("CUTBDDC_SWEEP_RING", None)
+        else:
+            os.environ["CUTBDDC_SWEEP_RING"] = ring
+        try:
+            s = cb.GpuSolver(0)
+            pb = cb.prepare(s, cfg)
+            s.setup_bddc(pb.objects, cfg.weighting)
+            x, rep = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
+            outs.append((x, rep["iterations"], np.asarray(rep["residuals"])))
+            s.close()
+        finally:
+            os.environ.pop("CUTBDDC_SWEEP_RING", None)
+    for x, it, res in outs[1:]:
+        assert it == outs[0][1]
+        assert np.array_equal(res, outs[0][2])
+        assert np.array_equal(x, outs[0][0])
