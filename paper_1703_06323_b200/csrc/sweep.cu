@@ -514,7 +514,7 @@ __device__ void preparer(const SweepDev& p, ItemRec* rec, double* vecs, const do
 // parent's update v_rest - o (update rows); several: partial sums to vbuf,
 // the last range of a row block to arrive sums them in range order.
 // v (the assembled right-hand side at the item's columns) comes prepared.
-template <int NR>
+template <int NR, bool kAcc4>
 __device__ void fwd_item(const SweepDev& p, const ItemRec& R, const double* ring, const int* segoff, SlotRec* sr,
                          int& chunk_seq, double* ysave, double* upd, const double* v, double* part, RhsStride rs) {
   const int tid = threadIdx.x;
@@ -540,6 +540,7 @@ __device__ void fwd_item(const SweepDev& p, const ItemRec& R, const double* ring
   const int Rw = (nrow + 31) & ~31, ng = kThreadsSweep / Rw;  // Rw <= kThreadsSweep rows per group, ng groups
   const int row = tid % Rw, grp = tid / Rw, i = g.i0 + row;
   double acc[NR];
+  double a4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
   for (int q = 0; q < g.nchunk; ++q, ++chunk_seq) {
@@ -552,15 +553,36 @@ __device__ void fwd_item(const SweepDev& p, const ItemRec& R, const double* ring
       // chunk widths are multiples of ng (item_geom): column j of the item
       // belongs to thread group (j - jlo) % ng whatever the ring's slot size
       const int jend = min(ch.jb, i + 1);
-      for (int j = ch.ja + grp; j < jend; j += ng) {
-        const double gij = S[so[j - ch.ja] + i];
+      int j = ch.ja + grp;
+      if (NR == 1 && kAcc4) {
+        // four accumulators by (j - jlo) / ng % 4 break the dependent FMA
+        // chain (64 columns per thread of a 128 x 128 tile)
+        auto term = [&](int jj) { return S[so[jj - ch.ja] + i] * v[jj - g.jlo]; };
+        int ph = ((ch.ja - g.jlo) / ng) & 3;
+        if (ph == 1 && j < jend) a4[1] += term(j), j += ng, ph = 2;
+        if (ph == 2 && j < jend) a4[2] += term(j), j += ng, ph = 3;
+        if (ph == 3 && j < jend) a4[3] += term(j), j += ng;
+        for (; j + 3 * ng < jend; j += 4 * ng) {
+          a4[0] += term(j);
+          a4[1] += term(j + ng);
+          a4[2] += term(j + 2 * ng);
+          a4[3] += term(j + 3 * ng);
+        }
+        if (j < jend) a4[0] += term(j), j += ng;
+        if (j < jend) a4[1] += term(j), j += ng;
+        if (j < jend) a4[2] += term(j), j += ng;
+      } else {
+        for (; j < jend; j += ng) {
+          const double gij = S[so[j - ch.ja] + i];
 #pragma unroll
-        for (int rr = 0; rr < NR; ++rr) acc[rr] += gij * v[(j - g.jlo) * NR + rr];
+          for (int rr = 0; rr < NR; ++rr) acc[rr] += gij * v[(j - g.jlo) * NR + rr];
+        }
       }
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&sr[slot].empty);
   }
+  if (NR == 1 && kAcc4) acc[0] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   double o[NR];
   if (ng == 1) {
 #pragma unroll
@@ -668,7 +690,7 @@ __device__ void bwd_item(const SweepDev& p, const ItemRec& R, const double* ring
 // and runs them in ticket order, so the smallest unfinished ticket is always
 // some CTA's current item, whose dependencies (smaller tickets) are done,
 // and whose chunks come first in its ring: no deadlock.
-template <bool kFwd, int NR = 1>
+template <bool kFwd, int NR = 1, bool kAcc4 = false>
 __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __restrict__ items, int n_items,
                                            int32_t* ticket, const double* __restrict__ panel, const double* X,
                                            double* Xw, const double* ysave_in, double* ysave, double* upd,
@@ -708,7 +730,7 @@ __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __rest
     mbar_wait(&R.ready, (k / kItems) & 1);
     if (R.item.x < 0) break;
     if (kFwd)
-      fwd_item<NR>(p, R, ring, segoff, sr, chunk_seq, ysave, upd, V, part, rs);
+      fwd_item<NR, kAcc4>(p, R, ring, segoff, sr, chunk_seq, ysave, upd, V, part, rs);
     else
       bwd_item(p, R, ring, segoff, sr, chunk_seq, Xw, V);
     csync();  // every consumer is done with the record and the vector
@@ -725,12 +747,27 @@ __device__ __forceinline__ void sweep_loop(const SweepDev& p, const int4* __rest
   }
 }
 
+#ifndef CUTBDDC_SWEEP_ACC4
+#define CUTBDDC_SWEEP_ACC4 0  // A/B on B200: four accumulators lose (cfg4 0.291 -> 0.301 ms, cfg5 6.49 -> 6.77 ms per apply)
+#endif
+constexpr bool kFwdAcc4 = CUTBDDC_SWEEP_ACC4 != 0;  // the same arithmetic in both builds (ranks may run either)
+// Two builds of each sweep kernel: kMinBlocks CTAs per SM (48 registers, the
+// many-subdomain ring) and kMinBlocks - 1 (68 registers, the few-subdomain
+// ring, whose larger slots leave room for three CTAs anyway).
 __global__ void __launch_bounds__(kBlockSweep, kMinBlocks) k_sweep_fwd(SweepDev p, const int4* __restrict__ items, int n_items,
                                                              const double* __restrict__ panel,
                                                              const double* __restrict__ X, double* __restrict__ ysave,
                                                              double* upd, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  sweep_loop<true>(p, items, n_items, p.ticket, panel, X, nullptr, nullptr, ysave, upd);
+  sweep_loop<true, 1, kFwdAcc4>(p, items, n_items, p.ticket, panel, X, nullptr, nullptr, ysave, upd);
+}
+__global__ void __launch_bounds__(kBlockSweep, kMinBlocks - 1) k_sweep_fwd_few(SweepDev p, const int4* __restrict__ items,
+                                                                 int n_items, const double* __restrict__ panel,
+                                                                 const double* __restrict__ X,
+                                                                 double* __restrict__ ysave, double* upd,
+                                                                 const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  sweep_loop<true, 1, kFwdAcc4>(p, items, n_items, p.ticket, panel, X, nullptr, nullptr, ysave, upd);
 }
 
 // Forward sweep of kMultiRhs right-hand sides at once (the coarse-basis
@@ -751,6 +788,13 @@ __global__ void __launch_bounds__(kBlockSweep, kMinBlocks) k_sweep_bwd(SweepDev 
                                                              const double* __restrict__ panel, double* X,
                                                              const double* __restrict__ ysave,
                                                              const int* __restrict__ skip, int ticket_slot) {
+  if (skip && *skip) return;
+  sweep_loop<false>(p, items, n_items, p.ticket + ticket_slot, panel, nullptr, X, ysave, nullptr, nullptr);
+}
+__global__ void __launch_bounds__(kBlockSweep, kMinBlocks - 1) k_sweep_bwd_few(SweepDev p, const int4* __restrict__ items,
+                                                                 int n_items, const double* __restrict__ panel,
+                                                                 double* X, const double* __restrict__ ysave,
+                                                                 const int* __restrict__ skip, int ticket_slot) {
   if (skip && *skip) return;
   sweep_loop<false>(p, items, n_items, p.ticket + ticket_slot, panel, nullptr, X, ysave, nullptr, nullptr);
 }
@@ -1170,17 +1214,22 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
     const int mx = 200 * 1024;  // any ring / vector size in use
     CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CB_CUDA(cudaFuncSetAttribute(k_sweep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd_few, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CB_CUDA(cudaFuncSetAttribute(k_sweep_bwd_few, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CB_CUDA(cudaFuncSetAttribute(k_sweep_fwd_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     return 1ll;
   });
   if (phase == kSweepAttrOnly) return;
+  // the 68-register build when the ring leaves room for at most kMinBlocks - 1 CTAs per SM anyway
+  const bool few = (228 * 1024) / (shm + 1536) < (size_t)kMinBlocks;
   const std::string tag = std::string("sweep") + (&f == &h->fI ? "I" : "K");
   if (phase == kSweepFwd) {
     CB_CUDA(cudaMemsetAsync(f.counters.p, 0, sizeof(int32_t) * f.counters.n, s));
     ProfScope ps(h->prof, s, tag + " fwd");
     if (f.n_items_f > 0) {
-      const int g = std::min(f.n_items_f, sweep_grid((const void*)k_sweep_fwd, shm));
-      k_sweep_fwd<<<g, kBlockSweep, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, skip);
+      auto kern = few ? k_sweep_fwd_few : k_sweep_fwd;
+      const int g = std::min(f.n_items_f, sweep_grid((const void*)kern, shm));
+      kern<<<g, kBlockSweep, shm, s>>>(p, f.items_f.p, f.n_items_f, f.panel.p, X, ysave, upd, skip);
       CB_LAUNCH();
     }
     if (tp) dump_trace(std::string(tp) + "_" + tag + "_fwd.bin", f, true, s);
@@ -1193,8 +1242,9 @@ void sweep_phase(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X
   SweepDev pb = p;
   pb.l2_policy = f.l2_policy_b;
   if (b1 > b0) {
-    const int g = std::min(b1 - b0, sweep_grid((const void*)k_sweep_bwd, shm));
-    k_sweep_bwd<<<g, kBlockSweep, shm, s>>>(pb, f.items_b.p + b0, b1 - b0, f.panel.p, X, ysave, skip, slot);
+    auto kern = few ? k_sweep_bwd_few : k_sweep_bwd;
+    const int g = std::min(b1 - b0, sweep_grid((const void*)kern, shm));
+    kern<<<g, kBlockSweep, shm, s>>>(pb, f.items_b.p + b0, b1 - b0, f.panel.p, X, ysave, skip, slot);
     CB_LAUNCH();
   }
   if (tp && phase == kSweepBwd) dump_trace(std::string(tp) + "_" + tag + "_bwd.bin", f, false, s);
