@@ -500,28 +500,54 @@ struct LoadArgs {
   double ox, oy, oz, h;
 };
 
-__global__ void __launch_bounds__(32 * kAccCells) k_cut_acc(int64_t ncut, const double* __restrict__ q8all,
+// Per-warp staging of one batch of kBatch quadrature points: the Q1 factors
+// of every (point, node) pair are evaluated once by the warp and shared by
+// the accumulators (they were rebuilt per accumulator before: ~3x the FP64
+// instructions). Node stride 5 doubles: the eight nodes fall in distinct
+// shared-memory banks.
+constexpr int kBatch = 8;
+struct BatchSmem {
+  double gv[kBatch][8][5];  // volume points: grad (3), val; surface points: n.grad, val
+  double px[kBatch];        // weight of the point
+  double pf[kBatch];        // manufactured problem: f (volume) or g (surface) at the point
+  unsigned char vmap[6 * kVolPts], smap[6 * kSurfPts];  // flat point order -> (tet, point)
+};
+
+#ifndef CB_ACC_MINB
+#define CB_ACC_MINB 6
+#endif
+__global__ void __launch_bounds__(32 * kAccCells, CB_ACC_MINB) k_cut_acc(int64_t ncut, const double* __restrict__ q8all,
                                                              double* __restrict__ accs, int* __restrict__ nvs,
                                                              LoadArgs la) {
   __shared__ PointSmem smem[kAccCells];
+  __shared__ BatchSmem bsm[kAccCells];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * kAccCells + wid;
   if (e >= ncut) return;
   PointSmem& S = smem[wid];
+  BatchSmem& Bt = bsm[wid];
+  int mynv = 0, myns = 0;
   if (lane < 6) {
     PtList L{S.vp[lane], S.sp[lane], 0, 0};
     double q[8];
     for (int i = 0; i < 8; ++i) q[i] = q8all[e * 8 + i];
     tet_points(lane, q, L);
-    S.nv[lane] = L.nv;
-    S.ns[lane] = L.ns;
+    S.nv[lane] = mynv = L.nv;
+    S.ns[lane] = myns = L.ns;
+  }
+  // flat point order (tet, then point): offsets by a warp prefix sum
+  int voff = mynv, soff = myns;
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, voff, d), b2 = __shfl_up_sync(0xffffffffu, soff, d);
+    if (lane >= d) voff += a, soff += b2;
+  }
+  const int nvol = __shfl_sync(0xffffffffu, voff, 5), nsurf = __shfl_sync(0xffffffffu, soff, 5);
+  if (lane < 6) {
+    for (int k = 0; k < mynv; ++k) Bt.vmap[voff - mynv + k] = (unsigned char)(lane * kVolPts + k);
+    for (int k = 0; k < myns; ++k) Bt.smap[soff - myns + k] = (unsigned char)(lane * kSurfPts + k);
   }
   __syncwarp();
-  int nvol = 0, nsurf = 0;
-  for (int t = 0; t < 6; ++t) {
-    nvol += S.nv[t];
-    nsurf += S.ns[t];
-  }
   if (lane == 0) {
     nvs[2 * e] = nvol;
     nvs[2 * e + 1] = nsurf;
@@ -535,68 +561,128 @@ __global__ void __launch_bounds__(32 * kAccCells) k_cut_acc(int64_t ncut, const 
     cy = (double)((cell / n) % n);
     cx = (double)(cell / n / n);
   }
-  for (int it = lane; it < (mms ? kAcc : kAccBase); it += 32) {
-    int kind, i, j;
-    double acc = 0.0;
-    if (it >= kAccBase) {  // G1 / G2 of the Nitsche load
-      const int a = (it - kAccBase) & 7;
-      const bool g2 = it >= kAccBase + 8;
-      for (int t = 0; t < 6; ++t)
-        for (int pnt = 0; pnt < S.ns[t]; ++pnt) {
-          const double* P = S.sp[t][pnt];
-          const double w = P[3];
-          double ga[3], va;
-          q1_gv(P, a, ga, &va);
-          const double gx = mms_u(la.ox + (cx + P[0]) * la.h, la.oy + (cy + P[1]) * la.h, la.oz + (cz + P[2]) * la.h);
-          if (g2) {
-            const double na = P[4] * ga[0] + P[5] * ga[1] + P[6] * ga[2];
-            acc += w * (gx * na);
-          } else {
-            acc += w * (gx * va);
-          }
-        }
-      accs[e * kAcc + it] = acc;
-      continue;
+  const int spt = lane >> 2, sn0 = (lane & 3) * 2;  // staging: this lane's point of the batch and its two nodes
+
+  // ---- volume accumulators: 0-35 D (i <= j), 36-43 F
+  {
+    int kind[2], ai[2], aj[2];
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int it = lane + 32 * k;
+      kind[k] = -1;
+      ai[k] = aj[k] = 0;
+      if (it < 44) acc_index(it, kind[k], ai[k], aj[k]);
     }
-    acc_index(it, kind, i, j);
-    if (kind <= 1) {
-      for (int t = 0; t < 6; ++t)
-        for (int pnt = 0; pnt < S.nv[t]; ++pnt) {
-          const double* P = S.vp[t][pnt];
-          const double w = P[3];
-          double gi[3], gj[3], vi;
-          q1_gv(P, i, gi, &vi);
-          if (kind == 1) {
+    const double* vp = &S.vp[0][0][0];
+    for (int p0 = 0; p0 < nvol; p0 += kBatch) {
+      const int cnt = min(kBatch, nvol - p0);
+      if (spt < cnt) {
+        const double* P = vp + 4 * Bt.vmap[p0 + spt];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          double g[3], val;
+          q1_gv(P, sn0 + q, g, &val);
+          Bt.gv[spt][sn0 + q][0] = g[0];
+          Bt.gv[spt][sn0 + q][1] = g[1];
+          Bt.gv[spt][sn0 + q][2] = g[2];
+          Bt.gv[spt][sn0 + q][3] = val;
+        }
+        if (sn0 == 0) {
+          Bt.px[spt] = P[3];
+          if (mms) Bt.pf[spt] = mms_f(la.ox + (cx + P[0]) * la.h, la.oy + (cy + P[1]) * la.h, la.oz + (cz + P[2]) * la.h);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (kind[k] == 0) {
+          for (int pp = 0; pp < cnt; ++pp) {
+            const double* gi = Bt.gv[pp][ai[k]];
+            const double* gj = Bt.gv[pp][aj[k]];
+            acc[k] += Bt.px[pp] * (gi[0] * gj[0] + gi[1] * gj[1] + gi[2] * gj[2]);
+          }
+        } else if (kind[k] == 1) {
+          for (int pp = 0; pp < cnt; ++pp) {
+            const double vi = Bt.gv[pp][ai[k]][3];
             if (mms)
-              acc += w * (mms_f(la.ox + (cx + P[0]) * la.h, la.oy + (cy + P[1]) * la.h, la.oz + (cz + P[2]) * la.h) * vi);
+              acc[k] += Bt.px[pp] * (Bt.pf[pp] * vi);
             else
-              acc += w * vi;
-          } else {
-            q1_gv(P, j, gj, nullptr);
-            acc += w * (gi[0] * gj[0] + gi[1] * gj[1] + gi[2] * gj[2]);
+              acc[k] += Bt.px[pp] * vi;
           }
         }
-    } else {
-      for (int t = 0; t < 6; ++t)
-        for (int pnt = 0; pnt < S.ns[t]; ++pnt) {
-          const double* P = S.sp[t][pnt];
-          const double w = P[3], nx = P[4], ny = P[5], nz = P[6];
-          double gi[3], gj[3], vi, vj;
-          q1_gv(P, i, gi, &vi);
-          q1_gv(P, j, gj, &vj);
-          if (kind == 2) {
-            const double ni = nx * gi[0] + ny * gi[1] + nz * gi[2];
-            const double nj = nx * gj[0] + ny * gj[1] + nz * gj[2];
-            acc += w * (ni * nj);
-          } else if (kind == 3) {
-            acc += w * (vi * vj);
-          } else {
-            const double ni = nx * gi[0] + ny * gi[1] + nz * gi[2];
-            acc += w * (vj * ni);
-          }
-        }
+      }
+      __syncwarp();
     }
-    accs[e * kAcc + it] = acc;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (kind[k] >= 0) accs[e * kAcc + lane + 32 * k] = acc[k];
+  }
+
+  // ---- surface accumulators: 44-79 B (i <= j), 80-115 M (i <= j), 116-179 N; manufactured: 180-187 G1, 188-195 G2
+  {
+    constexpr int kS = 5;  // (196 - 44) / 32 rounded up
+    const int nacc = (mms ? kAcc : kAccBase) - 44;
+    int kind[kS], ai[kS], aj[kS];
+    double acc[kS];
+#pragma unroll
+    for (int k = 0; k < kS; ++k) {
+      const int it = 44 + lane + 32 * k;
+      kind[k] = -1;
+      ai[k] = aj[k] = 0;
+      acc[k] = 0.0;
+      if (lane + 32 * k < nacc) {
+        if (it >= kAccBase) {
+          kind[k] = it >= kAccBase + 8 ? 6 : 5;  // G2 / G1
+          ai[k] = (it - kAccBase) & 7;
+        } else {
+          acc_index(it, kind[k], ai[k], aj[k]);
+        }
+      }
+    }
+    const double* sp = &S.sp[0][0][0];
+    for (int p0 = 0; p0 < nsurf; p0 += kBatch) {
+      const int cnt = min(kBatch, nsurf - p0);
+      if (spt < cnt) {
+        const double* P = sp + 7 * Bt.smap[p0 + spt];
+        const double nx = P[4], ny = P[5], nz = P[6];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          double g[3], val;
+          q1_gv(P, sn0 + q, g, &val);
+          Bt.gv[spt][sn0 + q][0] = nx * g[0] + ny * g[1] + nz * g[2];
+          Bt.gv[spt][sn0 + q][1] = val;
+        }
+        if (sn0 == 0) {
+          Bt.px[spt] = P[3];
+          if (mms) Bt.pf[spt] = mms_u(la.ox + (cx + P[0]) * la.h, la.oy + (cy + P[1]) * la.h, la.oz + (cz + P[2]) * la.h);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < kS; ++k) {
+        if (kind[k] < 0) continue;
+        for (int pp = 0; pp < cnt; ++pp) {
+          const double w = Bt.px[pp];
+          const double ni = Bt.gv[pp][ai[k]][0], vi = Bt.gv[pp][ai[k]][1];
+          const double nj = Bt.gv[pp][aj[k]][0], vj = Bt.gv[pp][aj[k]][1];
+          if (kind[k] == 2)
+            acc[k] += w * (ni * nj);
+          else if (kind[k] == 3)
+            acc[k] += w * (vi * vj);
+          else if (kind[k] == 4)
+            acc[k] += w * (vj * ni);
+          else if (kind[k] == 5)
+            acc[k] += w * (Bt.pf[pp] * vi);
+          else
+            acc[k] += w * (Bt.pf[pp] * ni);
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int k = 0; k < kS; ++k)
+      if (kind[k] >= 0) accs[e * kAcc + 44 + lane + 32 * k] = acc[k];
   }
 }
 
