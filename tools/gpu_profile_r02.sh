@@ -9,7 +9,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cfg5 --no-batch > gpurun_out/ncu_bench.log 2>&1; echo "ncu1 rc=$?"
 python tools/launch_summary.py gpurun_out/launches_bench.csv > gpurun_out/launches_bench_summary.txt
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base function \
-  -k 'regex:^k_sweep_(fwd|bwd)$' --launch-skip 6 -c 6 \
+  -k 'regex:^k_sweep_(fwd|bwd)(_few)?$' --launch-skip 6 -c 6 \
   -o gpurun_out/sweeps_full -f python tools/apply_profile.py cfg4 > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"
 python tools/ncu_traffic.py gpurun_out/sweeps_full.ncu-rep gpurun_out/sweep_traffic_cfg4.json cfg4-64 6
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dense_dag -c 1 \
