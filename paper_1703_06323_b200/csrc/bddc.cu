@@ -1201,7 +1201,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
       for (int sd = 0; sd < nsd; ++sd) corner_sd[(size_t)sd] = !bad_sd[(size_t)sd];
       h->kform_shell.upload(bad_sd, s);
       h->kform_corner.upload(corner_sd, s);
-      build_sweep_items(h, h->tI, h->fK, &bad_sd);  // K_c sweeps skip the shell subdomains, fKs's the others
+      exclude_sweep_items(h, h->fK, bad_sd);  // K_c sweeps skip the shell subdomains, fKs's the others
       if (!h->tK.ready || h->tK.tpl.b1 != b1) upload_template(h, h->tK, true);
       set_split_flags(h->tK, nsd);
       DevBuf<uint8_t>& mask_s = h->mask_shell;

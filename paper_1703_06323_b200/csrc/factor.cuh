@@ -89,6 +89,7 @@ void build_sweep_plan(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std:
 // the sweeps' item lists (host; run while the GPU factorises: factor_numeric's overlap hook)
 // exclude (optional, per subdomain): subdomains whose fronts get no items
 void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std::vector<uint8_t>* exclude = nullptr);
+void exclude_sweep_items(cutbddc_gpu* h, FactorSet& f, const std::vector<uint8_t>& exclude);  // filter the built lists
 void sweep_solve(cutbddc_gpu* h, const TplSet& ts, const FactorSet& f, double* X, double* ysave, double* upd,
                  const int* skip);
 enum { kSweepFwd = 0, kSweepBwd = 1, kSweepBwdRoot = 2, kSweepBwdRest = 3, kSweepAttrOnly = 4 };

@@ -100,6 +100,7 @@ struct FactorSet {
   int n_items_f = 0, n_items_b = 0;
   int n_items_b_root = 0;                      // leading backward items of the root level
   bool items_ready = false;                    // item lists built (build_sweep_items)
+  std::vector<int4> h_items_f, h_items_b;      // host copies of the full lists (exclude_sweep_items)
   int fwd_cols = 256, bwd_cols = 32;           // sweep item sizes (sweep.cu choose_item_sizes)
   int small_work = 8192;                       // panel entries of the largest one-item forward front
   int sweep_vec = 2048;                        // doubles of the sweeps' shared front vector (largest front, sweep.cu)

@@ -1188,11 +1188,46 @@ void build_sweep_items(cutbddc_gpu* h, const TplSet& ts, FactorSet& f, const std
   }
   f.n_items_f = (int)fw.size();
   f.n_items_b = (int)bw.size();
+  if (!exclude) {  // kept for exclude_sweep_items (a mixed K drops a few subdomains later)
+    f.h_items_f = fw;
+    f.h_items_b = bw;
+  }
   if (fw.empty()) fw.push_back(make_int4(0, 0, 0, 0));
   if (bw.empty()) bw.push_back(make_int4(0, 0, 0, 0));
   f.items_f.upload(fw, s);
   f.items_b.upload(bw, s);
   f.items_ready = true;
+}
+
+// Drop the items of the excluded subdomains from the lists build_sweep_items
+// made for all of them (same order: subdomains are independent, so the rest
+// is still in dependency order). The same lists as a rebuild with `exclude`
+// up to the order of equal-cost items, at a fraction of the host time (cfg5:
+// 260 k items, ~40 ms of sorting saved per setup).
+void exclude_sweep_items(cutbddc_gpu* h, FactorSet& f, const std::vector<uint8_t>& exclude) {
+  cudaStream_t s = h->stream;
+  if (!f.items_ready || (f.h_items_f.empty() && f.h_items_b.empty()))
+    throw Failure(CUTBDDC_INTERNAL, "sweep: no item lists to filter");
+  std::vector<int4> fw, bw;
+  fw.reserve(f.h_items_f.size());
+  bw.reserve(f.h_items_b.size());
+  for (const int4& it : f.h_items_f)
+    if (!exclude[(size_t)it.z]) fw.push_back(it);
+  int nroot = 0;
+  for (size_t q = 0; q < f.h_items_b.size(); ++q) {
+    const int4& it = f.h_items_b[q];
+    if (exclude[(size_t)it.z]) continue;
+    if ((int)q < f.n_items_b_root) ++nroot;
+    bw.push_back(it);
+  }
+  f.n_items_f = (int)fw.size();
+  f.n_items_b = (int)bw.size();
+  f.n_items_b_root = nroot;
+  if (fw.empty()) fw.push_back(make_int4(0, 0, 0, 0));
+  if (bw.empty()) bw.push_back(make_int4(0, 0, 0, 0));
+  f.items_f.upload(fw, s);
+  f.items_b.upload(bw, s);
+  CB_CUDA(cudaStreamSynchronize(s));  // fw / bw leave scope
 }
 
 
