@@ -118,6 +118,10 @@ def test_pcg_parity(name, kw):
     assert np.abs(ro - rg).max() <= 1e-8 * ro[0]
     assert np.linalg.norm(x_o - x_g) <= 1e-8 * np.linalg.norm(x_o)
     assert rep_g["lmin"] >= 1 - 1e-6
+    # condition_estimate: the Lanczos tridiagonal's extreme
+    # eigenvalues against the oracle's (same alphas / betas to ~1e-8)
+    for key in ("lmin", "lmax", "cond"):
+        assert abs(rep_g[key] - rep_o[key]) <= 1e-6 * abs(rep_o[key]), (key, rep_g[key], rep_o[key])
     s.close()
 
 
