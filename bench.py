@@ -87,9 +87,10 @@ class ClockSampler:
         h = pynvml.nvmlDeviceGetHandleByIndex(idx)
         bits = [(n, getattr(pynvml, a)) for n, a in self.REASONS]
 
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)  # constant: asked once
+
         def sample():
             sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             ev = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
             return float(sm), float(mx), {n for n, b in bits if ev & b}
         return sample
@@ -107,7 +108,7 @@ class ClockSampler:
 
     def start(self):
         try:
-            sample, period = self._nvml_sampler(), 0.02
+            sample, period = self._nvml_sampler(), getattr(self, "period", 0.02)
         except Exception:
             sample, period = self._smi_sampler(), 0.2
 
@@ -444,6 +445,7 @@ def main():
             "n_dof": n_dof, "iterations": r0["iterations"], "cond_estimate": r0["cond"],
             "phases_ms": _phases(reps),
             "step_ms": [round(1e3 * (r["t_assembly"] + r["t_setup"] + r["t_pcg"]), 3) for r in reps],
+            "median_step_ms": float(np.median([r["t_assembly"] + r["t_setup"] + r["t_pcg"] for r in reps]) * 1e3),
             "extra_warmup_steps": extra_warm,
             "pcg_dofs_per_s": n_dof / np.mean([r["t_pcg"] for r in reps]),
             "timing": "every step rebuilds the factorisation task list (CUTBDDC_NO_PLAN_CACHE=1)",

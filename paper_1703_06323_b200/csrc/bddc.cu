@@ -764,27 +764,45 @@ __global__ void __launch_bounds__(256) k_coarse_out(int nc, const int64_t* __res
   X[cslot[rinfo[4 * sd + 2] + j]] += v;
 }
 
-// Slot of every constraint-row entry in its subdomain's (B+1)^3 lattice:
-// entry e is dof[e] seen from local subdomain blk[e]. bad: 1 + the first
-// subdomain found with an object dof outside its block.
-__global__ void k_row_slots(int64_t ne, int n, int B, int nb, int b1, const int32_t* __restrict__ dof,
-                            const int32_t* __restrict__ blk, const int64_t* __restrict__ block_ids,
-                            const int64_t* __restrict__ node_of_dof, int32_t* __restrict__ c_slot,
-                            int* __restrict__ bad) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= ne) return;
-  const int sd = blk[e];
+// Constraint rows expanded on the device, a warp per local row (subdomain sd,
+// object o): entry e of the row is the object's e-th dof with coefficient 1
+// (corner) or 1 / |object| (edge / face average), stored as
+// its slot in the subdomain's (B+1)^3 lattice. The host passes only the row
+// pointers and the coarse view's CSR arrays (no per-entry host loop, no
+// per-entry upload). bad[1]: 1 + the first subdomain found with an object dof
+// outside its block; bad[2]: a dof id outside [0, n_dof).
+__global__ void __launch_bounds__(256) k_rows_expand(int64_t mtot, int n, int B, int nb, int b1, int64_t n_dof,
+                                                     const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ row_sd,
+                                                     const int32_t* __restrict__ coarse_id,
+                                                     const uint8_t* __restrict__ corner, const int64_t* __restrict__ dof_ptr,
+                                                     const int32_t* __restrict__ dofs, const int64_t* __restrict__ block_ids,
+                                                     const int64_t* __restrict__ node_of_dof, int32_t* __restrict__ c_slot,
+                                                     double* __restrict__ c_val, int* __restrict__ bad) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (row >= mtot) return;
+  const int lane = threadIdx.x & 31;
+  const int sd = row_sd[row], o = coarse_id[row];
+  const int64_t e0 = c_ptr[row], cnt = c_ptr[row + 1] - e0, d0 = dof_ptr[o];
+  const double coef = corner[row] ? 1.0 : 1.0 / (double)cnt;
   const int64_t bid = block_ids[sd];
   const int bi = (int)(bid / nb / nb), bj = (int)((bid / nb) % nb), bk = (int)(bid % nb);
-  const int64_t v = node_of_dof[dof[e]];
-  const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
-  const int lx = i - bi * B, ly = j - bj * B, lz = k - bk * B;
-  if (lx < 0 || ly < 0 || lz < 0 || lx > B || ly > B || lz > B) {
-    atomicCAS(bad, 0, 1 + sd);
-    c_slot[e] = 0;
-    return;
+  for (int64_t q = lane; q < cnt; q += 32) {
+    const int32_t d = dofs[d0 + q];
+    int slot = 0;
+    if (d < 0 || d >= n_dof) {
+      atomicCAS(bad + 2, 0, 1);
+    } else {
+      const int64_t v = node_of_dof[d];
+      const int k = (int)(v % (n + 1)), j = (int)((v / (n + 1)) % (n + 1)), i = (int)(v / (n + 1) / (n + 1));
+      const int lx = i - bi * B, ly = j - bj * B, lz = k - bk * B;
+      if (lx < 0 || ly < 0 || lz < 0 || lx > B || ly > B || lz > B)
+        atomicCAS(bad + 1, 0, 1 + sd);
+      else
+        slot = (lx * b1 + ly) * b1 + lz;
+    }
+    c_slot[e0 + q] = slot;
+    c_val[e0 + q] = coef;
   }
-  c_slot[e] = (lx * b1 + ly) * b1 + lz;
 }
 
 __global__ void k_row_sd(int nsd, const int64_t* __restrict__ m_off, int32_t* __restrict__ row_sd) {
@@ -998,7 +1016,10 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   const int64_t nstage = (int64_t)world * h->maxrows;
   std::vector<int64_t> srow((size_t)3 * nstage, 0);
   std::vector<int32_t> scoarse((size_t)nstage, 0);
-  std::vector<std::vector<int64_t>> cg((size_t)nc);
+  // cg: per coarse object the staged rows of its copies, ascending global sd (CSR)
+  std::vector<int64_t> cg_ptr((size_t)nc + 1, 0);
+  for (int o = 0; o < nc; ++o) cg_ptr[(size_t)o + 1] = cg_ptr[(size_t)o] + (cv->neigh_ptr[o + 1] - cv->neigh_ptr[o]);
+  std::vector<int64_t> cg_idx((size_t)cg_ptr[(size_t)nc]), cg_cur(cg_ptr.begin(), cg_ptr.end() - 1);
   for (int g = 0; g < nsd_g; ++g) {
     const int q = h->rank_of_gsd[(size_t)g];
     const int64_t first = (int64_t)q * h->maxrows + roff_g[(size_t)g];
@@ -1010,32 +1031,29 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
       srow[(size_t)(3 * p + 2)] = (int64_t)q * h->maxac + aoff_g[(size_t)g];
       const int o = obj_of_gsd[(size_t)g][(size_t)a2];
       scoarse[(size_t)p] = o;
-      cg[(size_t)o].push_back(p);  // ascending global sd
+      cg_idx[(size_t)cg_cur[(size_t)o]++] = p;  // ascending global sd
     }
   }
   // constraint rows: per (subdomain, object) the object's dofs; their slots in
-  // the subdomain's lattice are computed on the device (k_row_slots) from
+  // the subdomain's lattice are computed on the device (k_rows_expand) from
   // node_of_dof, so the host never needs the mesh maps
   std::vector<int64_t> m_off((size_t)nsd + 1, 0), c_ptr{0};
-  std::vector<int32_t> c_dof, c_blk, coarse_id;
-  std::vector<double> c_val;
+  std::vector<int32_t> coarse_id;
   std::vector<uint8_t> corner;
   const int n = h->n, B = h->block, nb = h->nb;
+  {
+    size_t rows = 0;
+    for (int sd = 0; sd < nsd; ++sd) rows += obj_of_gsd[(size_t)h->global_of_local[(size_t)sd]].size();
+    coarse_id.reserve(rows + 1);
+    corner.reserve(rows + 1);
+    c_ptr.reserve(rows + 1);
+  }
   for (int sd = 0; sd < nsd; ++sd) {
     const int g = h->global_of_local[(size_t)sd];
     for (int o : obj_of_gsd[(size_t)g]) {
       coarse_id.push_back(o);
       corner.push_back(cv->kinds[o] == CUTBDDC_CORNER);
-      const int64_t cnt = cv->dof_ptr[o + 1] - cv->dof_ptr[o];
-      const double coef = cv->kinds[o] == CUTBDDC_CORNER ? 1.0 : 1.0 / (double)cnt;
-      for (int64_t p = cv->dof_ptr[o]; p < cv->dof_ptr[o + 1]; ++p) {
-        const int32_t d = cv->dofs[p];
-        if (d < 0 || d >= h->n_dof) throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: dof out of range");
-        c_dof.push_back(d);
-        c_blk.push_back(sd);
-        c_val.push_back(coef);
-      }
-      c_ptr.push_back((int64_t)c_dof.size());
+      c_ptr.push_back(c_ptr.back() + (cv->dof_ptr[o + 1] - cv->dof_ptr[o]));  // entries expanded by k_rows_expand
     }
     m_off[(size_t)sd + 1] = (int64_t)coarse_id.size();
   }
@@ -1050,44 +1068,40 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
   }
   for (int g = 0; g < nsd_g; ++g) m_max = std::max(m_max, (int)obj_of_gsd[(size_t)g].size());  // uniform over ranks
   h->m_max = m_max;
-  std::vector<int64_t> cg_ptr{0}, cg_idx;
-  for (int o = 0; o < nc; ++o) {
-    for (int64_t r : cg[(size_t)o]) cg_idx.push_back(r);
-    cg_ptr.push_back((int64_t)cg_idx.size());
-  }
-  const int64_t n_centries = (int64_t)c_dof.size();
-  if (c_dof.empty()) c_dof.push_back(0), c_blk.push_back(0), c_val.push_back(0.0);
+  const int64_t n_centries = c_ptr.back();
+  const int64_t n_rows = (int64_t)coarse_id.size();
   if (coarse_id.empty()) coarse_id.push_back(0), corner.push_back(0);
   if (cg_idx.empty()) cg_idx.push_back(0);
   h->m_off.upload(m_off, s);
   h->c_ptr.upload(c_ptr, s);
+  h->coarse_id.upload(coarse_id, s);
+  h->corner_row.upload(corner, s);
+  const uint8_t* d_corner = h->corner_row.p;
+  h->row_sd.alloc((size_t)std::max<int64_t>(1, h->m_total));
+  k_row_sd<<<nsd, 128, 0, s>>>(nsd, h->m_off.p, h->row_sd.p);
+  CB_LAUNCH();
   {
-    DevBuf<int32_t>& d_dof = h->ws_cdof;
-    DevBuf<int32_t>& d_blk = h->ws_cblk;
-    d_dof.upload(c_dof, s);
-    d_blk.upload(c_blk, s);
-    h->c_slot.alloc(c_dof.size());
-    DevBuf<int>& flags = h->ws_flag;  // [0] weights, [1] constraint rows: read together after the weights
-    flags.alloc(2);
+    DevBuf<int>& flags = h->ws_flag;  // [0] weights, [1] [2] constraint rows: read together after the weights
+    flags.alloc(3);
     flags.zero(s);
+    h->c_slot.alloc((size_t)std::max<int64_t>(1, n_centries));
+    h->c_val.alloc((size_t)std::max<int64_t>(1, n_centries));
     if (n_centries > 0) {
-      k_row_slots<<<grid_for(n_centries, 256), 256, 0, s>>>(n_centries, n, B, nb, b1, d_dof.p, d_blk.p, h->block_ids.p,
-                                                            h->node_of_dof.p, h->c_slot.p, flags.p + 1);
+      // the coarse view's object dofs (CSR), expanded per (subdomain, object) row on the device
+      h->ws_cdof.upload(cv->dofs, (size_t)cv->dof_ptr[nc], s);
+      h->ws_odofptr.upload(cv->dof_ptr, (size_t)nc + 1, s);
+      k_rows_expand<<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, n, B, nb, b1, h->n_dof, h->c_ptr.p, h->row_sd.p,
+                                                               h->coarse_id.p, d_corner, h->ws_odofptr.p, h->ws_cdof.p,
+                                                               h->block_ids.p, h->node_of_dof.p, h->c_slot.p, h->c_val.p,
+                                                               flags.p);
       CB_LAUNCH();
     }
   }
-  h->c_val.upload(c_val, s);
-  h->coarse_id.upload(coarse_id, s);
   h->cg_ptr.upload(cg_ptr, s);
   h->cg_idx.upload(cg_idx, s);
   h->srow.upload(srow, s);
   h->scoarse.upload(scoarse, s);
-  h->corner_row.upload(corner, s);
-  const uint8_t* d_corner = h->corner_row.p;
   h->ac_off.upload(s_off, s);
-  h->row_sd.alloc((size_t)std::max<int64_t>(1, h->m_total));
-  k_row_sd<<<nsd, 128, 0, s>>>(nsd, h->m_off.p, h->row_sd.p);
-  CB_LAUNCH();
   ps_host.next("setup 0b weights");
   // ---- weights, rho
   DevBuf<int>& bad = h->ws_flag;  // zeroed with the constraint rows above
@@ -1158,9 +1172,10 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
     h->diag_add.zero(s);
     k_diag_add<<<nsd, 128, 0, s>>>(nsd, T, h->m_off.p, h->c_ptr.p, h->c_slot.p, d_corner, h->rho.p, h->diag_add.p);
     CB_LAUNCH();
-    int hbad[2] = {0, 0};
-    CB_CUDA(cudaMemcpyAsync(hbad, bad.p, 8, cudaMemcpyDeviceToHost, s));
+    int hbad[3] = {0, 0, 0};
+    CB_CUDA(cudaMemcpyAsync(hbad, bad.p, 12, cudaMemcpyDeviceToHost, s));
     CB_CUDA(cudaStreamSynchronize(s));
+    if (hbad[2]) throw Failure(CUTBDDC_INVALID_ARGUMENT, "coarse view: dof out of range");
     if (hbad[1])
       throw Failure(CUTBDDC_INVALID_ARGUMENT,
                     "coarse view: object dof not in neighbour subdomain " +

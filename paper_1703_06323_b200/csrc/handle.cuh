@@ -295,7 +295,8 @@ struct cutbddc_gpu {
   cutbddc_b200::DevBuf<int64_t> ws_cells;
   cutbddc_b200::DevBuf<int> ws_flag;
   cutbddc_b200::DevBuf<double> ws_global;             // global-numbered staging vector of the host downloads
-  cutbddc_b200::DevBuf<int32_t> ws_cdof, ws_cblk;   // setup: constraint-row dofs and their local subdomains
+  cutbddc_b200::DevBuf<int32_t> ws_cdof;            // setup: the coarse view's object dofs (CSR values)
+  cutbddc_b200::DevBuf<int64_t> ws_odofptr;         // setup: the coarse view's dof_ptr
   cutbddc_b200::DevBuf<int32_t> ws_coff;                       // corner coarse basis: front column offsets
   cutbddc_b200::DevBuf<double> ws_x8, ws_y8, ws_u8, ws_v8;      // multi-RHS forward sweep vectors
   DagPlan dag_factor;                              // dense_dag.cu: the subdomain factorisations (one launch)

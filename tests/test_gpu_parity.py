@@ -353,3 +353,34 @@ def test_mesh_view_upload_pinned_and_checked():
         s.assemble(cfg.block, pb.block_ids, mesh=dataclasses.replace(pb.mesh, dof_of_node=bad))
     assert e.value.code == cb.INVALID_ARGUMENT
     s.close()
+
+
+def test_coarse_view_checked_on_device():
+    """Constraint rows are expanded on the device (k_rows_expand) from the
+    coarse view's CSR arrays: a dof id outside [0, n_dof) and an object dof
+    that does not lie in a neighbour subdomain's block are both rejected with
+    INVALID_ARGUMENT, and the handle still sets up from the good view."""
+    import dataclasses
+    cfg = configs.get("cfg2")
+    s = cb.GpuSolver(0)
+    pb = cb.prepare(s, cfg)
+    objs = pb.objects
+    faces = np.flatnonzero(np.diff(objs.dof_ptr) > 1)
+    assert len(faces)
+    p = int(objs.dof_ptr[faces[0]])
+    for bad_dof in (s.n_dof, -1):
+        d = objs.dofs.copy()
+        d[p] = bad_dof
+        with pytest.raises(cb.CutbddcError) as e:
+            s.setup_bddc(dataclasses.replace(objs, dofs=d), cfg.weighting)
+        assert e.value.code == cb.INVALID_ARGUMENT and "out of range" in str(e.value)
+    # a dof of the far corner of the mesh is in no block touching the first face object
+    d = objs.dofs.copy()
+    d[p] = s.n_dof - 1 if objs.dofs[p] < s.n_dof // 2 else 0
+    with pytest.raises(cb.CutbddcError) as e:
+        s.setup_bddc(dataclasses.replace(objs, dofs=d), cfg.weighting)
+    assert e.value.code == cb.INVALID_ARGUMENT and "neighbour subdomain" in str(e.value)
+    s.setup_bddc(objs, cfg.weighting)
+    x, rep = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
+    assert rep["converged"]
+    s.close()
