@@ -424,6 +424,54 @@ __global__ void __launch_bounds__(256) k_sub_cells1(SubArgs a, const int32_t* __
   Y[g] = a.odiag ? v + a.odiag[g] * X[g] : v;
 }
 
+// Regular and irregular rows in one launch (the two row classes write disjoint
+// entries of Y): blocks [0, nblk_reg) are k_sub_regular's, the rest
+// k_sub_cells8's (kEight) or k_sub_cells1's, statement for statement, so the
+// bits are those of the separate launches.
+template <bool kEight>
+__global__ void __launch_bounds__(256) k_sub_fused(SubArgs a, const int32_t* __restrict__ rows, int64_t nreg, int nblk_reg,
+                                                   int P, int b1, const double* __restrict__ s27, int64_t lo, int64_t hi,
+                                                   const double* __restrict__ X, double* __restrict__ Y,
+                                                   const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double ks[64];
+  if ((int)blockIdx.x < nblk_reg) {
+    if (threadIdx.x < 27) ks[threadIdx.x] = s27[threadIdx.x];
+    __syncthreads();
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= nreg) return;
+    const int64_t g = rows[j];
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 27; ++q) acc += ks[q] * X[g + (q / 9 - 1) * P + ((q / 3) % 3 - 1) * b1 + (q % 3 - 1)];
+    Y[g] = acc;
+    return;
+  }
+  if (threadIdx.x < 64) ks[threadIdx.x] = a.kint[threadIdx.x];
+  __syncthreads();
+  const int64_t t = ((int64_t)blockIdx.x - nblk_reg) * blockDim.x + threadIdx.x;
+  if (kEight) {
+    const int64_t j = lo + t / 8;
+    const int c = threadIdx.x & 7;
+    const bool live = j < hi;  // whole 8-lane groups are live or not: the shuffles stay convergent
+    const int64_t g = live ? rows[j] : 0;
+    double v = live ? cell_part(a, ks, g, c, X) : 0.0;
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    if (live && c == 0) Y[g] = a.odiag ? v + a.odiag[g] * X[g] : v;
+  } else {
+    const int64_t j = lo + t;
+    if (j >= hi) return;
+    const int64_t g = rows[j];
+    double p[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) p[c] = cell_part(a, ks, g, c, X);
+    const double v = ((p[0] + p[4]) + (p[2] + p[6])) + ((p[1] + p[5]) + (p[3] + p[7]));
+    Y[g] = a.odiag ? v + a.odiag[g] * X[g] : v;
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- distribution
@@ -721,6 +769,19 @@ void sub_apply(cutbddc_gpu* h, int mode, const double* xloc, const double* Xslot
   const int64_t lo = mode == kSubInterface ? h->rows_nint : 0;
   const int64_t hi = mode == kSubInterior ? h->rows_nint : h->rows_n;
   const int64_t lo2 = std::max(lo, h->rows_nreg);  // irregular rows from here
+  const char* env_unfused = std::getenv("CUTBDDC_SUB_UNFUSED");  // A/B and test hook: the separate launches
+  const bool unfused = env_unfused && env_unfused[0] == '1';
+  if (!unfused && lo < h->rows_nreg && hi > lo2) {
+    const int nblk_reg = grid_for(h->rows_nreg, 256);
+    if (hi - lo2 < kCells8Rows)
+      k_sub_fused<true><<<nblk_reg + grid_for((hi - lo2) * 8, 256), 256, 0, st>>>(
+          a, h->op_rows.p, h->rows_nreg, nblk_reg, h->b1 * h->b1, h->b1, h->s27.p, lo2, hi, Xslot, Y, skip);
+    else
+      k_sub_fused<false><<<nblk_reg + grid_for(hi - lo2, 256), 256, 0, st>>>(
+          a, h->op_rows.p, h->rows_nreg, nblk_reg, h->b1 * h->b1, h->b1, h->s27.p, lo2, hi, Xslot, Y, skip);
+    CB_LAUNCH();
+    return;
+  }
   if (lo < h->rows_nreg) {
     k_sub_regular<<<grid_for(h->rows_nreg, 256), 256, 0, st>>>(h->op_rows.p, h->rows_nreg, h->b1 * h->b1, h->b1,
                                                                h->s27.p, Xslot, Y, skip);

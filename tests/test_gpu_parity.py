@@ -384,3 +384,16 @@ def test_coarse_view_checked_on_device():
     x, rep = s.pcg(rtol=cfg.rtol, max_iter=cfg.max_iter)
     assert rep["converged"]
     s.close()
+
+
+def test_operator_rows_one_launch_same_bits(cfg2s, monkeypatch):
+    """The matrix-free operator's regular and cut-cell rows in one launch
+    (k_sub_fused) give the bits of the two separate launches
+    (CUTBDDC_SUB_UNFUSED=1), for Abar x and for one BDDC apply (whose
+    harmonic correction uses the interior rows)."""
+    cfg, o, s, pb = cfg2s
+    x = np.random.default_rng(11).uniform(-1, 1, o.n_dof)
+    y1, z1 = s.spmv(x), s.apply(x)
+    monkeypatch.setenv("CUTBDDC_SUB_UNFUSED", "1")
+    y2, z2 = s.spmv(x), s.apply(x)
+    assert np.array_equal(y1, y2) and np.array_equal(z1, z2)
