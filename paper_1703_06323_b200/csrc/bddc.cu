@@ -561,6 +561,33 @@ __global__ void k_h_cy_sum(int64_t mtot, int nch, int mmax, const int32_t* __res
   cy[row] = v;
 }
 
+// k_h_cy_sum and k_sinv_apply (gl = S^{-1} cy) in one launch, a block per
+// subdomain: the same sums in the same order (chunk partials in chunk order,
+// then the row of S^{-1} left to right), so the bits are those of the two.
+__global__ void __launch_bounds__(128) k_h_cy_sum_sinv(int nch, int mmax, const int64_t* __restrict__ m_off,
+                                                       const int64_t* __restrict__ rinfo, const double* __restrict__ hp,
+                                                       const int64_t* __restrict__ s_off, const double* __restrict__ sinv,
+                                                       double* __restrict__ cy, double* __restrict__ gl,
+                                                       const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double scy[kHcyMaxM];
+  const int sd = blockIdx.x;
+  const int64_t b0 = m_off[sd];
+  const int m = (int)(m_off[sd + 1] - b0), used = (int)((rinfo[4 * sd] + 255) / 256);
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < used; ++c) v += hp[((int64_t)sd * nch + c) * mmax + a];
+    scy[a] = cy[b0 + a] = v;
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    const double* si = sinv + s_off[sd] + (int64_t)a * m;
+    double v = 0.0;
+    for (int b = 0; b < m; ++b) v += si[b] * scy[b];
+    gl[b0 + a] = v;
+  }
+}
+
 // y'[slot_k] += (H u)[k]: blocks (subdomain, 256 compact positions)
 __global__ void k_h_correct(const int64_t* __restrict__ m_off, const int64_t* __restrict__ rinfo,
                             const double* __restrict__ H, const int32_t* __restrict__ hslot,
@@ -1343,7 +1370,7 @@ void setup_bddc_device(cutbddc_gpu* h, const cutbddc_coarse_view* cv, int weight
 }
 
 // cy = H^T y' of every local constraint row (corner formulation)
-void h_cy(cutbddc_gpu* h, const double* Yc, const int* skip) {
+void h_cy(cutbddc_gpu* h, const double* Yc, const int* skip, double* gl_fused = nullptr) {
   if (h->m_total == 0) return;
   if (h->m_max > kHcyMaxM) throw Failure(CUTBDDC_CONFIG, "coarse basis: more than 128 constraint rows in a subdomain");
   const int nch = std::max(1, (h->np_max + 255) / 256);
@@ -1351,6 +1378,12 @@ void h_cy(cutbddc_gpu* h, const double* Yc, const int* skip) {
   k_h_cy<<<dim3(h->nsd, nch), 256, 0, h->stream>>>(h->m_off.p, h->root_info.p, h->hroot.p, h->hslot.p, Yc,
                                                      h->hcy_part.p, h->m_max, skip);
   CB_LAUNCH();
+  if (gl_fused) {  // also gl = S^{-1} cy (not the mixed K: no per-subdomain skip)
+    k_h_cy_sum_sinv<<<h->nsd, 128, 0, h->stream>>>(nch, h->m_max, h->m_off.p, h->root_info.p, h->hcy_part.p, h->ac_off.p,
+                                                   h->sinv.p, h->cy.p, gl_fused, skip);
+    CB_LAUNCH();
+    return;
+  }
   k_h_cy_sum<<<grid_for(h->m_total, 128), 128, 0, h->stream>>>(h->m_total, nch, h->m_max, h->row_sd.p, h->m_off.p,
                                                               h->root_info.p, h->hcy_part.p, h->cy.p, skip,
                                                               h->k_mixed ? h->kform_shell.p : nullptr);
@@ -1400,11 +1433,15 @@ void apply_bddc_device(cutbddc_gpu* h, const double* r, double* z, const int* sk
       double* Yc = corner ? h->ysave.p : h->sv1.p;  // where cy is read and the correction lands
       const int64_t* rinfo = corner ? h->root_info.p : h->root_info_s.p;
       if (corner) {  // cy = H^T y' (a warp per constraint row), gl = S^{-1} cy
-        h_cy(h, Yc, skip);
-        CB_LAUNCH();
-        k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p,
-                                                               h->sinv.p, h->coarse_id.p, h->zc.p, h->cy.p, gl_loc, 0,
-                                                               skip);
+        const char* env_unfused = std::getenv("CUTBDDC_HCY_UNFUSED");  // A/B and test hook: the separate launches
+        if (env_unfused && env_unfused[0] == '1') {
+          h_cy(h, Yc, skip);
+          k_sinv_apply<<<grid_for(std::max<int64_t>(1, h->m_total), 128), 128, 0, s>>>(
+              h->m_total, h->row_sd.p, h->m_off.p, h->ac_off.p, h->sinv.p, h->coarse_id.p, h->zc.p, h->cy.p, gl_loc, 0, skip);
+        } else {
+          h_cy(h, Yc, skip, gl_loc);
+          g_kernel_launches.fetch_sub(1);  // the CB_LAUNCH below counts a launch h_cy has already counted
+        }
       } else {
         k_coarse_in<<<h->nsd, 256, 0, s>>>(T, h->m_off.p, h->c_ptr.p, h->c_slot.p, h->c_val.p, Yc, h->ac_off.p,
                                            h->sinv.p, h->cy.p, gl_loc, skip, rinfo, nullptr, nullptr);

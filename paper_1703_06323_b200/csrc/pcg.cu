@@ -245,8 +245,14 @@ __global__ void k_copy(int64_t n, const double* __restrict__ a, double* __restri
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
-// Loop condition of the whole-solve graph: another iteration unless done.
-__global__ void k_loop_cond(cudaGraphConditionalHandle hc, const int* __restrict__ is) {
+// Last node of the whole-solve graph's WHILE body: k_next, then the loop
+// condition (another iteration unless done).
+__global__ void k_next_cond(cudaGraphConditionalHandle hc, int* __restrict__ is) {
+  if (!is[I_DONE]) {
+    const int k = is[I_ITER] + 1;
+    is[I_ITER] = k;
+    is[I_NOREF] = k % 50 != 0;
+  }
   cudaGraphSetConditional(hc, is[I_DONE] ? 0u : 1u);
 }
 
@@ -259,7 +265,7 @@ double* part1(cutbddc_gpu* h) { return h->partials.p + (int64_t)h->dist_world * 
 // One iteration; refresh: include the k % 50 replacement of r (its kernels
 // check the device flag; with several ranks it is its own graph, so its
 // exchange runs only where it is needed)
-void enqueue_iteration(cutbddc_gpu* h, bool refresh) {
+void enqueue_iteration(cutbddc_gpu* h, bool refresh, const cudaGraphConditionalHandle* hc = nullptr) {
   cudaStream_t s = h->stream;
   int* is = h->iscal.p;
   double* sc = h->scal.p;
@@ -289,12 +295,15 @@ void enqueue_iteration(cutbddc_gpu* h, bool refresh) {
   k_update_p<<<kFlatBlocks, kSegThreads, 0, s>>>(h->n_loc, fin(h), part0(h), sc, h->pz.p, h->pp.p, h->lbe.p,
                                                  h->lcopy_ptr.p, h->lcopy_src.p, h->psl.p, is);
   CB_LAUNCH();
-  k_next<<<1, 1, 0, s>>>(is);
+  if (hc)  // body of the WHILE node: advance and set the loop condition together
+    k_next_cond<<<1, 1, 0, s>>>(*hc, is);
+  else
+    k_next<<<1, 1, 0, s>>>(is);
   CB_LAUNCH();
 }
 
 // One graph for the whole PCG loop on one GPU: a conditional WHILE node whose
-// body is the captured iteration plus k_loop_cond. No host polling and no
+// body is the captured iteration ending in k_next_cond. No host polling and no
 // no-op iterations after convergence. false (and nothing kept) if the driver
 // refuses any step; the caller then uses per-iteration graph launches.
 bool build_while_graph(cutbddc_gpu* h) {
@@ -319,8 +328,7 @@ bool build_while_graph(cutbddc_gpu* h) {
   const long long c0 = g_kernel_launches.load();
   if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
     return fail();
-  enqueue_iteration(h, true);
-  k_loop_cond<<<1, 1, 0, s>>>(hc, h->iscal.p);
+  enqueue_iteration(h, true, &hc);
   const cudaError_t launch_err = cudaGetLastError();
   const cudaError_t cap_err = cudaStreamEndCapture(s, &body);
   g_kernel_launches.store(c0);  // captured, not executed

@@ -397,3 +397,15 @@ def test_operator_rows_one_launch_same_bits(cfg2s, monkeypatch):
     monkeypatch.setenv("CUTBDDC_SUB_UNFUSED", "1")
     y2, z2 = s.spmv(x), s.apply(x)
     assert np.array_equal(y1, y2) and np.array_equal(z1, z2)
+
+
+def test_coarse_rhs_one_launch_same_bits(cfg2s, monkeypatch):
+    """cy = H^T y' chunk sums and gl = S^{-1} cy in one launch
+    (k_h_cy_sum_sinv) against the two separate launches
+    (CUTBDDC_HCY_UNFUSED=1): the apply's bits do not change."""
+    cfg, o, s, pb = cfg2s
+    x = np.random.default_rng(12).uniform(-1, 1, o.n_dof)
+    z1 = s.apply(x)
+    monkeypatch.setenv("CUTBDDC_HCY_UNFUSED", "1")
+    z2 = s.apply(x)
+    assert np.array_equal(z1, z2)
