@@ -747,25 +747,59 @@ __global__ void __launch_bounds__(256) k_coarse_out(int nc, const int64_t* __res
   double* zl = gc + nc;
   double* u = zl + kFusedCoarseM;
   const int sd = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t b0 = m_off[sd];
+  const int m = (int)(m_off[sd + 1] - b0);
+#ifndef CUTBDDC_COARSE_OUT_PLAIN
+  {  // this block's H (or W_r) columns on their way to L2 while gc, zc and u are formed
+    const int cr0 = (int)rinfo[4 * sd], j0 = blockIdx.y * blockDim.x + tid;
+    if (j0 < cr0 && (tid & 15) == 0) {  // one request per 128 bytes
+      const double* base = (Hc ? Hc : W) + rinfo[4 * sd + 3] + j0;
+      for (int a = 0; a < m; ++a) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)a * cr0));
+    }
+  }
+#endif
   for (int lam = tid; lam < nc; lam += blockDim.x) {
     double v = 0.0;
     for (int64_t p = cg_ptr[lam]; p < cg_ptr[lam + 1]; ++p) v += gl[cg_idx[p]];
     gc[lam] = v;
   }
   __syncthreads();
-  const int64_t b0 = m_off[sd];
-  const int m = (int)(m_off[sd + 1] - b0);
-  for (int a = wid; a < m; a += blockDim.x >> 5) {
-    const double* ar = Ainv + (int64_t)coarse_id[b0 + a] * nc;
-    double s0 = 0.0, s1 = 0.0;
+  // zc rows, a warp per row; four rows of a warp in flight at once (each row's
+  // sum keeps its order: s0 over c = lane, lane + 64, ..; s1 over lane + 32, ..)
+#ifdef CUTBDDC_COARSE_OUT_PLAIN
+  constexpr int kRows = 1;
+#else
+  constexpr int kRows = 4;
+#endif
+  const int nw = blockDim.x >> 5;
+  for (int a0 = wid; a0 < m; a0 += nw * kRows) {
+    const double* ar[kRows];
+    double s0[kRows], s1[kRows];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const int a = a0 + r * nw;
+      ar[r] = Ainv + (int64_t)coarse_id[b0 + (a < m ? a : a0)] * nc;
+      s0[r] = s1[r] = 0.0;
+    }
     int c = lane;
     for (; c + 32 < nc; c += 64) {
-      s0 += ar[c] * gc[c];
-      s1 += ar[c + 32] * gc[c + 32];
+      const double g0 = gc[c], g1 = gc[c + 32];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        s0[r] += ar[r][c] * g0;
+        s1[r] += ar[r][c + 32] * g1;
+      }
     }
-    for (; c < nc; c += 32) s0 += ar[c] * gc[c];
-    const double v = warp_sum(s0 + s1);
-    if (lane == 0) zl[a] = v;
+    for (; c < nc; c += 32) {
+      const double g0 = gc[c];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) s0[r] += ar[r][c] * g0;
+    }
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const double v = warp_sum(s0[r] + s1[r]);
+      if (lane == 0 && a0 + r * nw < m) zl[a0 + r * nw] = v;
+    }
   }
   __syncthreads();
   for (int a = tid; a < m; a += blockDim.x) {
