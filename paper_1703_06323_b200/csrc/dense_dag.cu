@@ -940,7 +940,8 @@ void upload_plan(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, cons
 void upload_plan_fronts(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& fr, int64_t n_tasks) {
   cudaStream_t s = h->stream;
   if (fr.size() >= (1u << 24)) throw Failure(CUTBDDC_CONFIG, "dense dag: too many fronts");
-  std::vector<DagFront> dv(fr.size());
+  thread_local std::vector<DagFront> dv;  // storage kept across calls (every entry rewritten)
+  dv.resize(fr.size());
   int64_t cnt = 0;
   for (size_t q = 0; q < fr.size(); ++q) {
     DagFront& d = fr[q].d;
@@ -1008,7 +1009,8 @@ void build_tasks_device(cutbddc_gpu* h, DagPlan& plan, std::vector<HostFront>& f
   std::vector<int4> tpl;
   std::vector<int> tpl_bl;
   std::vector<int2> rng;
-  std::vector<DevFrontPlan> dfp(fp.size());
+  thread_local std::vector<DevFrontPlan> dfp;  // storage kept across calls (every entry rewritten)
+  dfp.resize(fp.size());
   for (size_t x = 0; x < fp.size(); ++x) {
     const FrontPlan& f = fp[x];
     int id = -1;
@@ -1067,6 +1069,11 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
   // (PEN tasks store absolute row indices, so new coarse objects on the same
   // geometry must rebuild the list).
   std::vector<int2> key;
+  {
+    size_t nkey = 0;
+    for (const FactorSpan& sp : spans) nkey += 3 + sp.ts->is_split.size() / 2 + 1 + sp.f->h_rc.size() + (size_t)(sp.sd1 - sp.sd0) + 1;
+    key.reserve(nkey);
+  }
   for (const FactorSpan& sp : spans) {
     key.push_back(make_int2(sp.sd0, sp.sd1));
     key.push_back(make_int2((int)(sp.front_off >> 31), (int)(sp.front_off & 0x7fffffff)));
@@ -1086,13 +1093,23 @@ void dense_dag_factor(cutbddc_gpu* h, const std::vector<FactorSpan>& spans, doub
   const std::vector<int4>* tasks = nullptr;
   if (!hit) {
     ProfScope ps(h->prof, s, "dense dag host+upload");
-    std::vector<HostFront> fr;
+    // the front list and its index scratch keep their storage across calls (per
+    // host thread: batched handles run on several): at cfg5 the list is
+    // ~120k records, and growing a fresh vector was most of this scope's time
+    thread_local std::vector<HostFront> fr;
+    thread_local std::vector<int> idx;
+    fr.clear();
+    {
+      size_t nfr = 0;
+      for (const FactorSpan& sp : spans) nfr += (size_t)(sp.sd1 - sp.sd0) * sp.ts->tpl.sn.size();
+      fr.reserve(nfr);
+    }
     for (size_t g = 0; g < spans.size(); ++g) {
       const FactorSpan& sp = spans[g];
       const TplSet& ts = *sp.ts;
       const FactorSet& f = *sp.f;
       const int nsn = (int)ts.tpl.sn.size();
-      std::vector<int> idx((size_t)(sp.sd1 - sp.sd0) * nsn, -1);
+      idx.assign((size_t)(sp.sd1 - sp.sd0) * nsn, -1);
       for (int sd = sp.sd0; sd < sp.sd1; ++sd)
         for (int sid = 0; sid < nsn; ++sid) {  // postorder: children first
           const size_t fs = (size_t)sd * nsn + sid;
